@@ -1,0 +1,281 @@
+/*
+ * stripefrac_oracle.c — CPU restatement of the reference's Striped UniFrac
+ * hot path, TEST INFRASTRUCTURE ONLY.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load this (as the checker / the CPU baseline). The product path never
+ * links, loads or calls it.
+ *
+ * Pinned: tests/test_oracle.py checks it bit-for-bit against the golden
+ * vectors in tests/golden/ produced by the reference itself (oracle/_ref,
+ * built from /root/reference/proj/src by oracle/Makefile).
+ *
+ * It consumes the same flattened problem as the C ABI (sf_problem layout:
+ * postorder rows, parent rows, lengths, leaf features, CSR table) and follows:
+ *   - leaf rows: relative_abundance / presence      table.cpp:208-222
+ *   - internal rows: pending fold in postorder       embed.cpp:42-82
+ *     (sum for weighted, max/OR for unweighted, starting from 0)
+ *   - fp32: rows and lengths computed in fp64, rounded once  embed.hpp:71-84
+ *   - update_entry, no FMA (compiled -ffp-contract=off)      kernels.hpp:55-66
+ *   - per-slot sequential sum over rows in postorder         kernels.hpp:97-119
+ *   - finalize: t == 0 ? 0 : d / t                            kernels.hpp:251-259
+ *   - stripe pair (k, (k+s+1) mod n)                         stripes.cpp:23-28
+ * Stripe ranges are split over threads with the reference's worker formula
+ * (kernels.hpp:302-303).
+ */
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct orc_problem {
+  int32_t n_rows;
+  const int32_t* parent_row;
+  const double* lengths;
+  const int32_t* leaf_feature;
+  int32_t n_samples;
+  int32_t n_features;
+  const int64_t* feat_ptr;
+  const int32_t* sample_idx;
+  const double* counts;
+  const double* sample_totals;
+} orc_problem;
+
+enum { ORC_UW = 1, ORC_WU = 2, ORC_WN = 3 };
+
+/* ---------------------------------------------------------------- rows */
+/* Embedding rows [0, E) are produced one at a time in postorder; each row is
+ * folded into its parent's pending buffer (embed.cpp:71-79). emit() writes
+ * the row into `row` (n doubles). */
+typedef struct embedder {
+  const orc_problem* p;
+  int weighted;
+  double** pending; /* [E] pending sums per internal row, NULL until a child lands */
+  int32_t cursor;
+} embedder;
+
+static int emb_init(embedder* em, const orc_problem* p, int weighted) {
+  em->p = p;
+  em->weighted = weighted;
+  em->cursor = 0;
+  em->pending = (double**)calloc((size_t)p->n_rows, sizeof(double*));
+  return em->pending ? 0 : -1;
+}
+
+static void emb_free(embedder* em) {
+  if (!em->pending) return;
+  for (int32_t r = 0; r < em->p->n_rows; ++r) free(em->pending[r]);
+  free(em->pending);
+  em->pending = NULL;
+}
+
+static int emb_next(embedder* em, double* row) {
+  const orc_problem* p = em->p;
+  const int n = p->n_samples;
+  const int32_t r = em->cursor++;
+  const int32_t f = p->leaf_feature[r];
+  if (f >= 0) {
+    memset(row, 0, sizeof(double) * (size_t)n);
+    for (int64_t e = p->feat_ptr[f]; e < p->feat_ptr[f + 1]; ++e) {
+      const int s = p->sample_idx[e];
+      const double c = p->counts[e];
+      row[s] = em->weighted ? c / p->sample_totals[s] : (c > 0.0 ? 1.0 : 0.0);
+    }
+  } else {
+    if (!em->pending[r]) return -1; /* internal node emitted before its children */
+    memcpy(row, em->pending[r], sizeof(double) * (size_t)n);
+    free(em->pending[r]);
+    em->pending[r] = NULL;
+  }
+  const int32_t par = p->parent_row[r];
+  if (par >= 0) {
+    if (!em->pending[par]) {
+      em->pending[par] = (double*)calloc((size_t)n, sizeof(double));
+      if (!em->pending[par]) return -1;
+    }
+    double* acc = em->pending[par];
+    if (em->weighted) {
+      for (int i = 0; i < n; ++i) acc[i] += row[i];
+    } else {
+      for (int i = 0; i < n; ++i) acc[i] = acc[i] < row[i] ? row[i] : acc[i]; /* cwiseMax */
+    }
+  }
+  return 0;
+}
+
+int orc_embed_rows(const orc_problem* p, int weighted, double* out) {
+  embedder em;
+  if (emb_init(&em, p, weighted)) return -1;
+  for (int32_t r = 0; r < p->n_rows; ++r)
+    if (emb_next(&em, out + (int64_t)r * p->n_samples)) {
+      emb_free(&em);
+      return -1;
+    }
+  emb_free(&em);
+  return 0;
+}
+
+/* -------------------------------------------------------------- stripes */
+#define DEFINE_ACCUM(NAME, REAL)                                                     \
+  static void NAME(int metric, REAL* dist, REAL* tot, const REAL* emb,               \
+                   const REAL* lens, int filled, int n, int s0, int s1, int start) { \
+    for (int s = s0; s < s1; ++s) {                                                  \
+      REAL* dm = dist + (int64_t)(s - start) * n;                                    \
+      REAL* tt = tot ? tot + (int64_t)(s - start) * n : NULL;                        \
+      for (int k = 0; k < n; ++k) {                                                  \
+        int l = k + s + 1;                                                           \
+        if (l >= n) l -= n;                                                          \
+        REAL d = dm[k];                                                              \
+        REAL t = tt ? tt[k] : (REAL)0;                                               \
+        for (int e = 0; e < filled; ++e) {                                           \
+          const REAL u = emb[(int64_t)e * n + k], v = emb[(int64_t)e * n + l];       \
+          const REAL L = lens[e];                                                    \
+          REAL diff = u - v;                                                         \
+          if (diff < (REAL)0) diff = -diff;                                          \
+          d += diff * L;                                                             \
+          if (metric == ORC_UW)                                                      \
+            t += (u > v ? u : v) * L;                                                \
+          else if (metric == ORC_WN)                                                 \
+            t += (u + v) * L;                                                        \
+        }                                                                            \
+        dm[k] = d;                                                                   \
+        if (tt) tt[k] = t;                                                           \
+      }                                                                              \
+    }                                                                                \
+  }
+DEFINE_ACCUM(accum_f64, double)
+DEFINE_ACCUM(accum_f32, float)
+
+typedef struct job {
+  int metric, prec, filled, n, s0, s1, start;
+  void *dist, *tot;
+  const void *emb, *lens;
+} job;
+
+static void* run_job(void* arg) {
+  const job* j = (const job*)arg;
+  if (j->prec == 8)
+    accum_f64(j->metric, (double*)j->dist, (double*)j->tot, (const double*)j->emb,
+              (const double*)j->lens, j->filled, j->n, j->s0, j->s1, j->start);
+  else
+    accum_f32(j->metric, (float*)j->dist, (float*)j->tot, (const float*)j->emb,
+              (const float*)j->lens, j->filled, j->n, j->s0, j->s1, j->start);
+  return NULL;
+}
+
+/* Full stripe computation: rows streamed in batches of `batch`, stripes
+ * [start, stop) split over `threads` workers per batch. Returns 0 on
+ * success. dist/tot: (stop-start) x n of double (prec 8) or float (prec 4);
+ * tot may be NULL for WU. */
+int orc_compute_stripes(const orc_problem* p, int metric, int prec, int start, int stop,
+                        void* dist, void* tot, int finalize, int threads, int batch) {
+  const int n = p->n_samples;
+  const int E = p->n_rows;
+  const size_t w = prec == 8 ? 8 : 4;
+  const int64_t slots = (int64_t)(stop - start) * n;
+  if (batch < 1) batch = 64;
+  if (threads < 1) threads = 1;
+  if (threads > stop - start) threads = stop - start;
+  memset(dist, 0, (size_t)slots * w);
+  if (tot) memset(tot, 0, (size_t)slots * w);
+  const int has_t = metric != ORC_WU;
+  void* t_use = has_t ? tot : NULL;
+
+  embedder em;
+  if (emb_init(&em, p, metric != ORC_UW)) return -1;
+  double* rows64 = (double*)malloc(sizeof(double) * (size_t)batch * (size_t)n);
+  float* rows32 = prec == 4 ? (float*)malloc(sizeof(float) * (size_t)batch * (size_t)n) : NULL;
+  double* lens64 = (double*)malloc(sizeof(double) * (size_t)batch);
+  float* lens32 = (float*)malloc(sizeof(float) * (size_t)batch);
+  pthread_t* tids = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  job* jobs = (job*)malloc(sizeof(job) * (size_t)threads);
+  int rc = 0;
+  if (!rows64 || (prec == 4 && !rows32) || !lens64 || !lens32 || !tids || !jobs) rc = -1;
+  for (int r0 = 0; rc == 0 && r0 < E; r0 += batch) {
+    const int filled = E - r0 < batch ? E - r0 : batch;
+    for (int i = 0; i < filled; ++i) {
+      if (emb_next(&em, rows64 + (int64_t)i * n)) {
+        rc = -1;
+        break;
+      }
+      lens64[i] = p->lengths[r0 + i];
+    }
+    if (rc) break;
+    const void* emb = rows64;
+    const void* lens = lens64;
+    if (prec == 4) { /* cast_batch: round once */
+      for (int64_t i = 0; i < (int64_t)filled * n; ++i) rows32[i] = (float)rows64[i];
+      for (int i = 0; i < filled; ++i) lens32[i] = (float)lens64[i];
+      emb = rows32;
+      lens = lens32;
+    }
+    const int span = stop - start;
+    for (int wk = 0; wk < threads; ++wk) {
+      job* j = &jobs[wk];
+      j->metric = metric;
+      j->prec = prec;
+      j->filled = filled;
+      j->n = n;
+      j->s0 = start + (int)((int64_t)span * wk / threads);
+      j->s1 = start + (int)((int64_t)span * (wk + 1) / threads);
+      j->start = start;
+      j->dist = dist;
+      j->tot = t_use;
+      j->emb = emb;
+      j->lens = lens;
+      if (threads == 1)
+        run_job(j);
+      else
+        pthread_create(&tids[wk], NULL, run_job, j);
+    }
+    if (threads > 1)
+      for (int wk = 0; wk < threads; ++wk) pthread_join(tids[wk], NULL);
+  }
+  if (rc == 0 && finalize && has_t) {
+    for (int64_t i = 0; i < slots; ++i) {
+      if (prec == 8) {
+        const double t = ((double*)tot)[i];
+        ((double*)dist)[i] = t == 0.0 ? 0.0 : ((double*)dist)[i] / t;
+      } else {
+        const float t = ((float*)tot)[i];
+        ((float*)dist)[i] = t == 0.0f ? 0.0f : ((float*)dist)[i] / t;
+      }
+    }
+  }
+  free(rows64);
+  free(rows32);
+  free(lens64);
+  free(lens32);
+  free(tids);
+  free(jobs);
+  emb_free(&em);
+  return rc;
+}
+
+/* condense (stripes.cpp:68-129) of one finalized full-range stripe set into
+ * an n x n double matrix; returns -1 if an even-n duplicate slot disagrees. */
+int orc_condense(int prec, int n, const void* dist, double* out) {
+  const int S = n / 2;
+  memset(out, 0, sizeof(double) * (size_t)n * (size_t)n);
+  for (int s = 0; s < S; ++s)
+    for (int k = 0; k < n; ++k) {
+      const double v = prec == 8 ? ((const double*)dist)[(int64_t)s * n + k]
+                                 : (double)((const float*)dist)[(int64_t)s * n + k];
+      int l = k + s + 1;
+      if (l >= n) l -= n;
+      if (n % 2 == 0 && s == S - 1 && k >= n / 2) {
+        if (prec == 8) {
+          if (out[(int64_t)k * n + l] != v) return -1;
+        } else { /* duplicate_slots_agree, fp32 (stripes.cpp:51-58) */
+          const float a = (float)out[(int64_t)k * n + l], b = (float)v;
+          const float da = a < b ? b - a : a - b;
+          const float fa = a < 0 ? -a : a, fb = b < 0 ? -b : b;
+          if (!(da <= 1e-6f * (fa > fb ? fa : fb))) return -1;
+        }
+        continue;
+      }
+      out[(int64_t)k * n + l] = v;
+      out[(int64_t)l * n + k] = v;
+    }
+  return 0;
+}

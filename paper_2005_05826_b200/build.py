@@ -1,0 +1,78 @@
+"""Build recipes: the sm_100a CUDA library (product) and the oracle (tests).
+
+The product library ``libstripefrac_cuda.so`` is built in-tree with nvcc for
+``sm_100a`` only. The oracle pieces (``oracle/liboracle_port.so``, the C
+restatement, and ``oracle/_ref/`` built from the reference sources when
+``/root/reference`` is present) are test infrastructure.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+LIB = PKG / "libstripefrac_cuda.so"
+ORACLE = ROOT / "oracle"
+ORACLE_LIB = ORACLE / "liboracle_port.so"
+REFERENCE = Path("/root/reference/proj")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-lineinfo", "-O3", "-std=c++17",
+    "-Xcompiler", "-fPIC,-O3", "-shared",
+    "-Xptxas", "-warn-spills",
+]
+SOURCES = ["sf_api.cu", "host_prep.cpp"]
+HEADERS = ["sf_common.hpp", "embed_kernels.cuh", "stripe_kernels.cuh", "sparse_kernels.cuh"]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and Path(cand).exists():
+            return cand
+    raise RuntimeError("nvcc not found; the CUDA toolkit is required to build stripefrac-b200")
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).exists() and Path(d).stat().st_mtime > t for d in deps)
+
+
+def build_native(force: bool = False, verbose: bool = False) -> Path:
+    deps = [CSRC / s for s in SOURCES + HEADERS] + list((ROOT / "include").glob("*.h"))
+    if force or _stale(LIB, deps):
+        cmd = [_nvcc(), *NVCC_FLAGS, f"-I{ROOT / 'include'}", f"-I{CSRC}",
+               *[str(CSRC / s) for s in SOURCES], "-o", str(LIB)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    return LIB
+
+
+def build_oracle(force: bool = False, verbose: bool = False) -> None:
+    """Test infrastructure: C restatement + (when present) the reference build."""
+    src = ORACLE / "stripefrac_oracle.c"
+    if force or _stale(ORACLE_LIB, [src]):
+        cmd = ["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
+               str(src), "-o", str(ORACLE_LIB)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+    if REFERENCE.exists():
+        subprocess.run(["make", "-s", "-C", str(ORACLE), "-j8"], check=True,
+                       stdout=None if verbose else subprocess.DEVNULL)
+
+
+def build_all(force: bool = False, verbose: bool = False) -> None:
+    build_native(force=force, verbose=verbose)
+    build_oracle(force=force, verbose=verbose)
+
+
+if __name__ == "__main__":
+    build_all(force=True, verbose=True)

@@ -1,0 +1,917 @@
+// C ABI of the B200 Striped-UniFrac hot path (include/stripefrac_cuda.h).
+//
+// Host side of compute_unifrac (kernels.hpp:268-316): validate, schedule the
+// postorder embedding in row chunks, shard stripes over devices, launch
+// K1 (embed) -> K2 (stripe update) per chunk, K3 (finalize), copy back.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "embed_kernels.cuh"
+#include "sf_common.hpp"
+#include "stripe_kernels.cuh"
+#include "stripefrac_cuda.h"
+
+namespace sf {
+
+namespace {
+thread_local std::string g_error;
+}
+void set_error(const std::string& msg) { g_error = msg; }
+const char* last_error() { return g_error.c_str(); }
+
+namespace {
+
+#define SF_CUDA(expr)                                                                   \
+  do {                                                                                  \
+    const cudaError_t e_ = (expr);                                                      \
+    if (e_ != cudaSuccess) {                                                            \
+      set_error(std::string(#expr) + " failed: " + cudaGetErrorString(e_));             \
+      return SF_ECUDA;                                                                  \
+    }                                                                                   \
+  } while (0)
+
+#define SF_TRY(expr)                   \
+  do {                                 \
+    const sf_status st_ = (expr);      \
+    if (st_ != SF_OK) return st_;      \
+  } while (0)
+
+sf_status fail(sf_status st, const std::string& msg) {
+  set_error(msg);
+  return st;
+}
+
+// Device allocation owned by one device.
+struct DevBuf {
+  int dev = -1;
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { reset(); }
+  void reset() {
+    if (p) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      cudaSetDevice(dev);
+      cudaFree(p);
+      if (cur >= 0) cudaSetDevice(cur);
+    }
+    p = nullptr;
+    bytes = 0;
+  }
+  sf_status alloc(int device, size_t nbytes, const char* what) {
+    reset();
+    dev = device;
+    if (nbytes == 0) nbytes = 16;
+    const cudaError_t e = cudaMalloc(&p, nbytes);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return fail(SF_ENOMEM, std::string("cudaMalloc of ") + std::to_string(nbytes) +
+                                 " bytes for " + what + " failed: " + cudaGetErrorString(e));
+    }
+    bytes = nbytes;
+    return SF_OK;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+template <class T>
+sf_status upload(DevBuf& b, int dev, const T* host, size_t count, cudaStream_t st,
+                 const char* what) {
+  SF_TRY(b.alloc(dev, count * sizeof(T), what));
+  if (count) SF_CUDA(cudaMemcpyAsync(b.p, host, count * sizeof(T), cudaMemcpyHostToDevice, st));
+  return SF_OK;
+}
+
+int total_stripes(int n) { return n / 2; }
+
+// ------------------------------------------------------------ devices
+sf_status usable_devices(const sf_exec* ex, std::vector<int>& out) {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(SF_ECUDA, "no CUDA device is available (this library has no CPU fallback)");
+  }
+  std::vector<int> want;
+  if (ex && ex->devices && ex->n_devices > 0) {
+    want.assign(ex->devices, ex->devices + ex->n_devices);
+  } else {
+    const int k = (ex && ex->n_devices > 0) ? std::min(ex->n_devices, count) : count;
+    for (int i = 0; i < k; ++i) want.push_back(i);
+  }
+  for (int d : want) {
+    if (d < 0 || d >= count) return fail(SF_EINVAL, "device ordinal " + std::to_string(d) + " out of range");
+    cudaDeviceProp prop;
+    SF_CUDA(cudaGetDeviceProperties(&prop, d));
+    if (prop.major != 10)
+      return fail(SF_ECUDA, std::string("device ") + std::to_string(d) + " (" + prop.name +
+                                ") is not sm_100; this library is built for sm_100a only");
+  }
+  out = want;
+  return SF_OK;
+}
+
+// ------------------------------------------------------------ validation
+sf_status validate_problem(const sf_problem* p) {
+  if (!p) return fail(SF_EINVAL, "problem is null");
+  if (p->n_samples < 2)
+    return fail(SF_EINVAL, "need at least 2 samples, got " + std::to_string(p->n_samples));
+  if (p->n_rows < 1) return fail(SF_EINVAL, "embedding batch is empty");
+  if (p->n_features < 1) return fail(SF_EINVAL, "table has no features");
+  if (!p->parent_row || !p->lengths || !p->leaf_feature || !p->feat_ptr || !p->sample_idx ||
+      !p->counts || !p->sample_totals)
+    return fail(SF_EINVAL, "problem has a null array");
+  const int E = p->n_rows;
+  for (int r = 0; r < E; ++r) {
+    const int par = p->parent_row[r];
+    if (par != -1 && (par <= r || par >= E))
+      return fail(SF_EINVAL, "row " + std::to_string(r) + " has an invalid parent row (rows must be in postorder)");
+    const double L = p->lengths[r];
+    if (!(L >= 0.0) || L > 1.7976931348623157e308)
+      return fail(SF_EINVAL, "branch length must be finite and non-negative");
+    const int f = p->leaf_feature[r];
+    if (f < -1 || f >= p->n_features) return fail(SF_EINVAL, "leaf feature out of range");
+  }
+  std::vector<char> has_child(static_cast<size_t>(E), 0);
+  for (int r = 0; r < E; ++r)
+    if (p->parent_row[r] >= 0) has_child[static_cast<size_t>(p->parent_row[r])] = 1;
+  for (int r = 0; r < E; ++r) {
+    const bool leaf = p->leaf_feature[r] >= 0;
+    if (leaf == static_cast<bool>(has_child[static_cast<size_t>(r)]))
+      return fail(SF_EINVAL, "row " + std::to_string(r) +
+                                 (leaf ? " is a leaf with children" : " is an internal row without children"));
+  }
+  if (p->feat_ptr[0] != 0) return fail(SF_EINVAL, "feat_ptr[0] must be 0");
+  for (int f = 0; f < p->n_features; ++f) {
+    if (p->feat_ptr[f + 1] < p->feat_ptr[f]) return fail(SF_EINVAL, "feat_ptr is not monotone");
+    int prev = -1;
+    for (int64_t e = p->feat_ptr[f]; e < p->feat_ptr[f + 1]; ++e) {
+      const int s = p->sample_idx[e];
+      if (s <= prev || s >= p->n_samples)
+        return fail(SF_EINVAL, "sample indices of a feature must be ascending and in range");
+      prev = s;
+      const double c = p->counts[e];
+      if (!(c >= 0.0) || c > 1.7976931348623157e308)
+        return fail(SF_EINVAL, "count must be finite and non-negative");
+    }
+  }
+  for (int s = 0; s < p->n_samples; ++s)
+    if (!(p->sample_totals[s] > 0.0))
+      return fail(SF_EINVAL, "sample " + std::to_string(s) + " has no counts");
+  return SF_OK;
+}
+
+sf_status validate_range(int n, int32_t start, int32_t& stop) {
+  const int S = total_stripes(n);
+  if (stop < 0) stop = S;
+  if (start < 0 || stop > S || start >= stop)
+    return fail(SF_EINVAL, "stripe range " + std::to_string(start) + ":" + std::to_string(stop) +
+                               " does not fit in [0," + std::to_string(S) + ")");
+  return SF_OK;
+}
+
+// ------------------------------------------------------------ schedule
+struct Chunk {
+  int32_t r0 = 0, r1 = 0;
+  std::vector<int32_t> leaf_rows, leaf_feat;  // chunk-relative rows
+  std::vector<int32_t> lvl_ptr;               // levels -> [int_rows)
+  std::vector<int32_t> int_rows;              // chunk-relative internal rows
+  std::vector<int32_t> cptr, codes;           // children location codes per int row
+  std::vector<int32_t> carry_src, carry_dst;  // chunk rows -> pending slots
+};
+
+struct Schedule {
+  std::vector<Chunk> chunks;
+  int32_t n_pending = 0;
+  int32_t cmax = 0;
+};
+
+// Postorder rows in chunks of <= cmax rows. Internal rows are grouped by
+// height (children strictly lower), rows whose parent is in a later chunk
+// are carried to pending slots, slots are recycled once consumed.
+Schedule build_schedule(const sf_problem* p, int32_t cmax) {
+  const int E = p->n_rows;
+  std::vector<int32_t> height(static_cast<size_t>(E), 0);
+  std::vector<int32_t> kptr(static_cast<size_t>(E) + 1, 0), kids;
+  for (int r = 0; r < E; ++r) {
+    const int par = p->parent_row[r];
+    if (par >= 0) {
+      height[static_cast<size_t>(par)] = std::max(height[static_cast<size_t>(par)], height[static_cast<size_t>(r)] + 1);
+      ++kptr[static_cast<size_t>(par) + 1];
+    }
+  }
+  for (int r = 0; r < E; ++r) kptr[static_cast<size_t>(r) + 1] += kptr[static_cast<size_t>(r)];
+  kids.assign(static_cast<size_t>(kptr[static_cast<size_t>(E)]), 0);
+  {
+    std::vector<int32_t> at(kptr.begin(), kptr.end() - 1);
+    for (int r = 0; r < E; ++r)  // ascending r: children in postorder = fold order
+      if (p->parent_row[r] >= 0) kids[static_cast<size_t>(at[static_cast<size_t>(p->parent_row[r])]++)] = r;
+  }
+
+  Schedule sch;
+  sch.cmax = cmax;
+  std::vector<int32_t> slot_of(static_cast<size_t>(E), -1);
+  std::vector<int32_t> free_slots;
+  for (int r0 = 0; r0 < E; r0 += cmax) {
+    Chunk c;
+    c.r0 = r0;
+    c.r1 = std::min(E, r0 + cmax);
+    int32_t hmax = 0;
+    for (int r = c.r0; r < c.r1; ++r) {
+      if (p->leaf_feature[r] >= 0) {
+        c.leaf_rows.push_back(r - c.r0);
+        c.leaf_feat.push_back(p->leaf_feature[r]);
+      } else {
+        hmax = std::max(hmax, height[static_cast<size_t>(r)]);
+      }
+    }
+    // bucket internal rows by height
+    std::vector<int32_t> cnt(static_cast<size_t>(hmax) + 2, 0);
+    for (int r = c.r0; r < c.r1; ++r)
+      if (p->leaf_feature[r] < 0) ++cnt[static_cast<size_t>(height[static_cast<size_t>(r)]) + 1];
+    c.lvl_ptr.push_back(0);
+    for (int h = 1; h <= hmax; ++h) {
+      cnt[static_cast<size_t>(h) + 1] += cnt[static_cast<size_t>(h)];
+      c.lvl_ptr.push_back(cnt[static_cast<size_t>(h) + 1]);
+    }
+    c.int_rows.assign(static_cast<size_t>(c.lvl_ptr.back()), 0);
+    std::vector<int32_t> at(cnt.begin() + 1, cnt.end());
+    for (int r = c.r0; r < c.r1; ++r)
+      if (p->leaf_feature[r] < 0) c.int_rows[static_cast<size_t>(at[static_cast<size_t>(height[static_cast<size_t>(r)]) - 1]++)] = r - c.r0;
+    std::vector<int32_t> consumed;
+    c.cptr.push_back(0);
+    for (int32_t rel : c.int_rows) {
+      const int r = c.r0 + rel;
+      for (int32_t e = kptr[static_cast<size_t>(r)]; e < kptr[static_cast<size_t>(r) + 1]; ++e) {
+        const int ch = kids[static_cast<size_t>(e)];
+        if (ch >= c.r0) {
+          c.codes.push_back(ch - c.r0);
+        } else {
+          c.codes.push_back(-1 - slot_of[static_cast<size_t>(ch)]);
+          consumed.push_back(slot_of[static_cast<size_t>(ch)]);
+        }
+      }
+      c.cptr.push_back(static_cast<int32_t>(c.codes.size()));
+    }
+    for (int32_t s : consumed) free_slots.push_back(s);
+    for (int r = c.r0; r < c.r1; ++r) {
+      const int par = p->parent_row[r];
+      if (par >= c.r1) {
+        int32_t slot;
+        if (!free_slots.empty()) {
+          slot = free_slots.back();
+          free_slots.pop_back();
+        } else {
+          slot = sch.n_pending++;
+        }
+        slot_of[static_cast<size_t>(r)] = slot;
+        c.carry_src.push_back(r - c.r0);
+        c.carry_dst.push_back(slot);
+      }
+    }
+    sch.chunks.push_back(std::move(c));
+  }
+  return sch;
+}
+
+// ------------------------------------------------------------ kernel table
+using StripeFn = void (*)(const StripeArgs);
+
+template <int M, class Real, int SRC, bool EXACT>
+struct DenseCfg;
+// fp64: 8 warps along samples (RK=8 each), 1 along stripes (RS=4) -> 64 x 128
+template <int M, int SRC, bool EXACT>
+struct DenseCfg<M, double, SRC, EXACT> {
+  static constexpr int RK = 8, RS = 4, NWK = 8, NWS = 1, RB = 16;
+};
+template <int M, int SRC, bool EXACT>
+struct DenseCfg<M, float, SRC, EXACT> {
+  static constexpr int RK = 8, RS = 4, NWK = 8, NWS = 1, RB = 16;
+};
+
+template <int M, class Real, int SRC, bool EXACT>
+void launch_dense(const StripeArgs& a, cudaStream_t st) {
+  using C = DenseCfg<M, Real, SRC, EXACT>;
+  constexpr int TK = C::NWK * C::RK;
+  constexpr int TS = C::NWS * 32 * C::RS;
+  const dim3 grid((a.n + TK - 1) / TK, (a.s_end - a.s_begin + TS - 1) / TS);
+  stripe_dense_kernel<M, Real, SRC, EXACT, C::RK, C::RS, C::NWK, C::NWS, C::RB>
+      <<<grid, 32 * C::NWK * C::NWS, 0, st>>>(a);
+}
+
+template <class Real, int SRC>
+sf_status dispatch_dense(int metric, bool exact, const StripeArgs& a, cudaStream_t st) {
+  switch (metric) {
+    case SF_UNWEIGHTED:
+      launch_dense<kUW, Real, SRC, false>(a, st);
+      break;
+    case SF_WEIGHTED_UNNORMALIZED:
+      if (exact)
+        launch_dense<kWU, Real, SRC, true>(a, st);
+      else
+        launch_dense<kWU, Real, SRC, false>(a, st);
+      break;
+    case SF_WEIGHTED_NORMALIZED:
+      if (exact)
+        launch_dense<kWN, Real, SRC, true>(a, st);
+      else
+        launch_dense<kWN, Real, SRC, false>(a, st);
+      break;
+    default:
+      return fail(SF_EINVAL, "unknown metric");
+  }
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+sf_status launch_stripes(int metric, int prec, int src, bool exact, const StripeArgs& a,
+                         cudaStream_t st) {
+  if (prec == SF_FP64) {
+    if (src == kSrcBits) return dispatch_dense<double, kSrcBits>(metric, exact, a, st);
+    if (src == kSrcF64) return dispatch_dense<double, kSrcF64>(metric, exact, a, st);
+  } else {
+    if (src == kSrcBits) return dispatch_dense<float, kSrcBits>(metric, exact, a, st);
+    if (src == kSrcF64) return dispatch_dense<float, kSrcF64>(metric, exact, a, st);
+    if (src == kSrcF32) return dispatch_dense<float, kSrcF32>(metric, exact, a, st);
+  }
+  return fail(SF_EINVAL, "unsupported precision/source combination");
+}
+
+int grid_for(int64_t count, int block) {
+  int64_t g = (count + block - 1) / block;
+  return static_cast<int>(std::min<int64_t>(std::max<int64_t>(g, 1), 148 * 32));
+}
+
+}  // namespace
+}  // namespace sf
+
+using namespace sf;
+
+// ------------------------------------------------------------ plan
+struct DeviceState {
+  int dev = -1;
+  int32_t a = 0, b = 0;  // absolute stripe range on this device
+  cudaStream_t stream = nullptr;
+  DevBuf lens, feat_ptr, sidx, counts, totals;
+  DevBuf dist, tot, emb, pend, exec_ctr;
+  DevBuf sched;  // all schedule arrays, packed
+  std::vector<int64_t> sched_off;  // per chunk: offsets of its arrays in `sched`
+  // sparse-bit (unweighted) path
+  DevBuf nodebits, lens_pad;
+  std::vector<cudaEvent_t> events;
+  ~DeviceState() {
+    if (dev >= 0) {
+      cudaSetDevice(dev);
+      for (auto e : events) cudaEventDestroy(e);
+      if (stream) cudaStreamDestroy(stream);
+    }
+  }
+};
+
+struct sf_plan {
+  int metric = 0, prec = 0;
+  int32_t n = 0, E = 0, start = 0, stop = 0;
+  bool bits = false, exact = false;
+  int kernel = 1;  // 1 dense, 2 sparse-bit
+  int64_t row_words = 0;  // per embedding row: words (bits) or doubles (values)
+  Schedule sched;
+  std::vector<std::unique_ptr<DeviceState>> devs;
+  sf_stats stats{};
+  bool ran = false;
+  bool finalized = false;
+};
+
+namespace {
+
+// Sparse node-packed bit kernel for the unweighted metric (kernel 2).
+sf_status sparse_prepare(sf_plan*, DeviceState&, const sf_problem*) {
+  return fail(SF_EINVAL, "the sparse bit kernel is not available in this build");
+}
+sf_status sparse_run(sf_plan*, DeviceState&) {
+  return fail(SF_EINVAL, "the sparse bit kernel is not available in this build");
+}
+
+// Layout of one chunk's schedule arrays inside the packed device buffer.
+enum { kLeafRows, kLeafFeat, kIntRows, kCptr, kCodes, kCarrySrc, kCarryDst, kNumArr };
+
+sf_status upload_schedule(DeviceState& d, const Schedule& s) {
+  std::vector<int32_t> packed;
+  d.sched_off.clear();
+  for (const Chunk& c : s.chunks) {
+    const std::vector<int32_t>* arrs[kNumArr] = {&c.leaf_rows, &c.leaf_feat, &c.int_rows, &c.cptr,
+                                                 &c.codes, &c.carry_src, &c.carry_dst};
+    for (auto* v : arrs) {
+      d.sched_off.push_back(static_cast<int64_t>(packed.size()));
+      packed.insert(packed.end(), v->begin(), v->end());
+      while (packed.size() % 4) packed.push_back(0);  // 16-byte alignment
+    }
+  }
+  return upload(d.sched, d.dev, packed.data(), packed.size(), d.stream, "schedule");
+}
+
+sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
+  SF_CUDA(cudaSetDevice(d.dev));
+  const cudaStream_t st = d.stream;
+  const int n = plan->n;
+  const int64_t rows_here = d.b - d.a;
+  const size_t w = plan->prec == SF_FP64 ? 8 : 4;
+  const int64_t slots = rows_here * n;
+  // events: [0]=start, per chunk (embed start, stripe start, stripe end), fin start, fin end
+  const size_t need_ev = 3 + 3 * plan->sched.chunks.size();
+  while (d.events.size() < need_ev) {
+    cudaEvent_t e;
+    SF_CUDA(cudaEventCreate(&e));
+    d.events.push_back(e);
+  }
+  SF_CUDA(cudaEventRecord(d.events[0], st));
+  SF_CUDA(cudaMemsetAsync(d.dist.p, 0, static_cast<size_t>(slots) * w, st));
+  if (d.tot.p && plan->metric != SF_WEIGHTED_UNNORMALIZED)
+    SF_CUDA(cudaMemsetAsync(d.tot.p, 0, static_cast<size_t>(slots) * w, st));
+  SF_CUDA(cudaMemsetAsync(d.exec_ctr.p, 0, sizeof(unsigned long long), st));
+
+  if (plan->kernel == 2) {
+    SF_TRY(sparse_run(plan, d));
+  } else {
+    const int64_t stride = plan->row_words;
+    for (size_t ci = 0; ci < plan->sched.chunks.size(); ++ci) {
+      const Chunk& c = plan->sched.chunks[ci];
+      const int32_t* base = d.sched.as<int32_t>();
+      auto arr = [&](int k) { return base + d.sched_off[ci * kNumArr + static_cast<size_t>(k)]; };
+      const int C = c.r1 - c.r0;
+      SF_CUDA(cudaEventRecord(d.events[1 + 3 * ci], st));
+      const size_t row_bytes = static_cast<size_t>(stride) * (plan->bits ? 4 : 8);
+      SF_CUDA(cudaMemsetAsync(d.emb.p, 0, row_bytes * static_cast<size_t>(C), st));
+      const int nl = static_cast<int>(c.leaf_rows.size());
+      if (nl > 0) {
+        const int blocks = grid_for(static_cast<int64_t>(nl) * 32, 256);
+        if (plan->bits)
+          embed_leaf_bits<<<blocks, 256, 0, st>>>(d.emb.as<uint32_t>(), stride, arr(kLeafRows),
+                                                  arr(kLeafFeat), nl, d.feat_ptr.as<int64_t>(),
+                                                  d.sidx.as<int32_t>(), d.counts.as<double>());
+        else
+          embed_leaf_values<<<blocks, 256, 0, st>>>(d.emb.as<double>(), stride, arr(kLeafRows),
+                                                    arr(kLeafFeat), nl, d.feat_ptr.as<int64_t>(),
+                                                    d.sidx.as<int32_t>(), d.counts.as<double>(),
+                                                    d.totals.as<double>());
+        SF_CUDA(cudaGetLastError());
+        plan->stats.launches++;
+      }
+      const int ncols = static_cast<int>(plan->bits ? (n + 31) / 32 : n);
+      for (size_t h = 0; h + 1 < c.lvl_ptr.size(); ++h) {
+        const int lo = c.lvl_ptr[h], hi = c.lvl_ptr[h + 1];
+        if (hi <= lo) continue;
+        const dim3 grid((ncols + 127) / 128, std::min(hi - lo, 65535));
+        if (plan->bits)
+          embed_level_bits<<<grid, 128, 0, st>>>(d.emb.as<uint32_t>(), stride, d.pend.as<uint32_t>(),
+                                                 arr(kIntRows) + lo, arr(kCptr) + lo, arr(kCodes),
+                                                 hi - lo, ncols);
+        else
+          embed_level_values<<<grid, 128, 0, st>>>(d.emb.as<double>(), stride, d.pend.as<double>(),
+                                                   arr(kIntRows) + lo, arr(kCptr) + lo, arr(kCodes),
+                                                   hi - lo, ncols);
+        SF_CUDA(cudaGetLastError());
+        plan->stats.launches++;
+      }
+      SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
+      StripeArgs a;
+      a.emb = d.emb.p;
+      a.row_stride = stride;
+      a.lens = d.lens.as<double>() + c.r0;
+      a.C = C;
+      a.n = n;
+      a.s_begin = d.a;
+      a.s_end = d.b;
+      a.dist = d.dist.p;
+      a.tot = plan->metric == SF_WEIGHTED_UNNORMALIZED ? nullptr : d.tot.p;
+      a.exec_updates = d.exec_ctr.as<unsigned long long>();
+      SF_TRY(launch_stripes(plan->metric, plan->prec, plan->bits ? kSrcBits : kSrcF64,
+                            plan->exact, a, st));
+      plan->stats.launches++;
+      SF_CUDA(cudaEventRecord(d.events[3 + 3 * ci], st));
+      const int ncarry = static_cast<int>(c.carry_src.size());
+      if (ncarry > 0) {
+        const dim3 grid((ncols + 127) / 128, std::min(ncarry, 65535));
+        if (plan->bits)
+          embed_carry<uint32_t><<<grid, 128, 0, st>>>(d.emb.as<uint32_t>(), d.pend.as<uint32_t>(),
+                                                      stride, arr(kCarrySrc), arr(kCarryDst),
+                                                      ncarry, ncols);
+        else
+          embed_carry<double><<<grid, 128, 0, st>>>(d.emb.as<double>(), d.pend.as<double>(), stride,
+                                                    arr(kCarrySrc), arr(kCarryDst), ncarry, ncols);
+        SF_CUDA(cudaGetLastError());
+        plan->stats.launches++;
+      }
+    }
+  }
+  const size_t ne = d.events.size();
+  SF_CUDA(cudaEventRecord(d.events[ne - 2], st));
+  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED) {
+    const int blocks = grid_for(slots, 256);
+    if (plan->prec == SF_FP64)
+      finalize_kernel<double><<<blocks, 256, 0, st>>>(d.dist.as<double>(), d.tot.as<double>(), slots);
+    else
+      finalize_kernel<float><<<blocks, 256, 0, st>>>(d.dist.as<float>(), d.tot.as<float>(), slots);
+    SF_CUDA(cudaGetLastError());
+    plan->stats.launches++;
+  }
+  SF_CUDA(cudaEventRecord(d.events[ne - 1], st));
+  return SF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sf_last_error(void) { return sf::last_error(); }
+const char* sf_version(void) { return "stripefrac-b200 0.1.0 (sm_100a)"; }
+
+int32_t sf_device_count(void) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int i = 0; i < count; ++i) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, i) == cudaSuccess && prop.major == 10) ++ok;
+  }
+  return ok;
+}
+
+sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision prec, int32_t start,
+                         int32_t stop, const sf_exec* ex, sf_plan** out) {
+  if (!out) return fail(SF_EINVAL, "out is null");
+  *out = nullptr;
+  if (metric != SF_UNWEIGHTED && metric != SF_WEIGHTED_UNNORMALIZED && metric != SF_WEIGHTED_NORMALIZED)
+    return fail(SF_EINVAL, "unknown metric code " + std::to_string(static_cast<int>(metric)));
+  if (prec != SF_FP32 && prec != SF_FP64)
+    return fail(SF_EINVAL, "unknown precision code " + std::to_string(static_cast<int>(prec)));
+  SF_TRY(validate_problem(p));
+  SF_TRY(validate_range(p->n_samples, start, stop));
+  std::vector<int> devices;
+  SF_TRY(usable_devices(ex, devices));
+
+  auto plan = std::make_unique<sf_plan>();
+  plan->metric = metric;
+  plan->prec = prec;
+  plan->n = p->n_samples;
+  plan->E = p->n_rows;
+  plan->start = start;
+  plan->stop = stop;
+  plan->bits = metric == SF_UNWEIGHTED;
+  plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
+  plan->kernel = (ex && ex->kernel == 2) ? 2 : 1;
+  if (plan->kernel == 2 && metric != SF_UNWEIGHTED)
+    return fail(SF_EINVAL, "the sparse bit kernel implements the unweighted metric only");
+  const int n = p->n_samples;
+  plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;
+  const size_t w = prec == SF_FP64 ? 8 : 4;
+  const bool has_t = metric != SF_WEIGHTED_UNNORMALIZED;
+
+  // stripe split: the reference's worker split formula (kernels.hpp:302-303)
+  const int G = static_cast<int>(devices.size());
+  const int span = stop - start;
+  if (G > span) devices.resize(static_cast<size_t>(span));
+  const int Gu = static_cast<int>(devices.size());
+  for (int g = 0; g < Gu; ++g) {
+    auto d = std::make_unique<DeviceState>();
+    d->dev = devices[static_cast<size_t>(g)];
+    d->a = start + static_cast<int>(static_cast<int64_t>(span) * g / Gu);
+    d->b = start + static_cast<int>(static_cast<int64_t>(span) * (g + 1) / Gu);
+    plan->devs.push_back(std::move(d));
+  }
+
+  // chunk capacity from the smallest device budget
+  const size_t row_bytes = static_cast<size_t>(plan->row_words) * (plan->bits ? 4 : 8);
+  size_t budget = SIZE_MAX;
+  for (auto& d : plan->devs) {
+    SF_CUDA(cudaSetDevice(d->dev));
+    size_t freeb = 0, totalb = 0;
+    SF_CUDA(cudaMemGetInfo(&freeb, &totalb));
+    const size_t stripes_b = static_cast<size_t>(d->b - d->a) * n * w * (has_t ? 2 : 1);
+    const size_t csr_b = static_cast<size_t>(p->feat_ptr[p->n_features]) * 12 + static_cast<size_t>(plan->E) * 64;
+    const size_t avail = freeb > stripes_b + csr_b + (512ull << 20) ? freeb - stripes_b - csr_b - (512ull << 20) : 0;
+    budget = std::min(budget, avail * 3 / 4);
+  }
+  if (ex && ex->mem_budget_bytes > 0) budget = std::min(budget, static_cast<size_t>(ex->mem_budget_bytes));
+  int64_t cmax = static_cast<int64_t>(budget / std::max<size_t>(row_bytes, 1));
+  if (plan->kernel == 2) cmax = plan->E;  // the sparse path keeps all rows
+  cmax = std::min<int64_t>(cmax, plan->E);
+  if (cmax < 1) return fail(SF_ENOMEM, "not enough device memory for one embedding row");
+  for (;;) {
+    plan->sched = build_schedule(p, static_cast<int32_t>(cmax));
+    const size_t need = (static_cast<size_t>(cmax) + static_cast<size_t>(plan->sched.n_pending)) * row_bytes;
+    if (need <= budget || cmax == 1 || plan->kernel == 2) break;
+    cmax = std::max<int64_t>(1, cmax * 3 / 4);
+  }
+  plan->stats.n_chunks = plan->sched.chunks.size();
+
+  for (auto& dp : plan->devs) {
+    DeviceState& d = *dp;
+    SF_CUDA(cudaSetDevice(d.dev));
+    SF_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    const int64_t F = p->n_features;
+    const int64_t nnz = p->feat_ptr[F];
+    SF_TRY(upload(d.lens, d.dev, p->lengths, static_cast<size_t>(plan->E), d.stream, "lengths"));
+    SF_TRY(upload(d.feat_ptr, d.dev, p->feat_ptr, static_cast<size_t>(F + 1), d.stream, "feat_ptr"));
+    SF_TRY(upload(d.sidx, d.dev, p->sample_idx, static_cast<size_t>(nnz), d.stream, "sample_idx"));
+    SF_TRY(upload(d.counts, d.dev, p->counts, static_cast<size_t>(nnz), d.stream, "counts"));
+    SF_TRY(upload(d.totals, d.dev, p->sample_totals, static_cast<size_t>(n), d.stream, "totals"));
+    const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
+    SF_TRY(d.dist.alloc(d.dev, slots * w, "distances"));
+    if (has_t) SF_TRY(d.tot.alloc(d.dev, slots * w, "totals"));
+    SF_TRY(d.exec_ctr.alloc(d.dev, sizeof(unsigned long long), "counter"));
+    if (plan->kernel == 2) {
+      SF_TRY(upload_schedule(d, plan->sched));
+      SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(plan->E) * row_bytes, "embedding rows"));
+      SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));
+      SF_TRY(sparse_prepare(plan.get(), d, p));
+    } else {
+      SF_TRY(upload_schedule(d, plan->sched));
+      SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(cmax) * row_bytes, "embedding chunk"));
+      SF_TRY(d.pend.alloc(d.dev, static_cast<size_t>(std::max(plan->sched.n_pending, 1)) * row_bytes,
+                          "pending rows"));
+    }
+  }
+  *out = plan.release();
+  return SF_OK;
+}
+
+sf_status sf_plan_run(sf_plan* plan, int32_t finalize) {
+  if (!plan) return fail(SF_EINVAL, "plan is null");
+  plan->stats.launches = 0;
+  for (auto& d : plan->devs) SF_TRY(run_device(plan, *d, finalize));
+  plan->ran = true;
+  plan->finalized = finalize != 0;
+  return SF_OK;
+}
+
+sf_status sf_plan_sync(sf_plan* plan) {
+  if (!plan) return fail(SF_EINVAL, "plan is null");
+  double emb = 0, str = 0, fin = 0, tot = 0;
+  uint64_t exec = 0;
+  for (auto& dp : plan->devs) {
+    DeviceState& d = *dp;
+    SF_CUDA(cudaSetDevice(d.dev));
+    SF_CUDA(cudaStreamSynchronize(d.stream));
+    if (!plan->ran) continue;
+    double e_ms = 0, s_ms = 0, f_ms = 0, t_ms = 0;
+    const size_t ne = d.events.size();
+    if (plan->kernel != 2) {
+      for (size_t ci = 0; ci < plan->sched.chunks.size(); ++ci) {
+        float a = 0, b = 0;
+        SF_CUDA(cudaEventElapsedTime(&a, d.events[1 + 3 * ci], d.events[2 + 3 * ci]));
+        SF_CUDA(cudaEventElapsedTime(&b, d.events[2 + 3 * ci], d.events[3 + 3 * ci]));
+        e_ms += a;
+        s_ms += b;
+      }
+    } else {
+      float a = 0, b = 0;
+      SF_CUDA(cudaEventElapsedTime(&a, d.events[1], d.events[2]));
+      SF_CUDA(cudaEventElapsedTime(&b, d.events[2], d.events[3]));
+      e_ms = a;
+      s_ms = b;
+    }
+    float f = 0, t = 0;
+    SF_CUDA(cudaEventElapsedTime(&f, d.events[ne - 2], d.events[ne - 1]));
+    SF_CUDA(cudaEventElapsedTime(&t, d.events[0], d.events[ne - 1]));
+    f_ms = f;
+    t_ms = t;
+    emb = std::max(emb, e_ms);
+    str = std::max(str, s_ms);
+    fin = std::max(fin, f_ms);
+    tot = std::max(tot, t_ms);
+    unsigned long long c = 0;
+    SF_CUDA(cudaMemcpy(&c, d.exec_ctr.p, sizeof(c), cudaMemcpyDeviceToHost));
+    exec += c;
+  }
+  plan->stats.embed_ms = emb;
+  plan->stats.stripe_ms = str;
+  plan->stats.finalize_ms = fin;
+  plan->stats.total_ms = tot;
+  plan->stats.updates_exec = exec;
+  plan->stats.updates_alg = static_cast<uint64_t>(plan->E) * static_cast<uint64_t>(plan->stop - plan->start) *
+                            static_cast<uint64_t>(plan->n);
+  return SF_OK;
+}
+
+sf_status sf_plan_download(sf_plan* plan, void* dist_out, void* tot_out) {
+  if (!plan) return fail(SF_EINVAL, "plan is null");
+  if (!plan->ran) return fail(SF_ESTATE, "plan has not run");
+  if (!dist_out) return fail(SF_EINVAL, "dist_out is null");
+  const bool has_t = plan->metric != SF_WEIGHTED_UNNORMALIZED;
+  const size_t w = plan->prec == SF_FP64 ? 8 : 4;
+  for (auto& dp : plan->devs) {
+    DeviceState& d = *dp;
+    SF_CUDA(cudaSetDevice(d.dev));
+    const size_t off = static_cast<size_t>(d.a - plan->start) * plan->n * w;
+    const size_t bytes = static_cast<size_t>(d.b - d.a) * plan->n * w;
+    SF_CUDA(cudaMemcpyAsync(static_cast<char*>(dist_out) + off, d.dist.p, bytes, cudaMemcpyDeviceToHost, d.stream));
+    if (has_t && tot_out)
+      SF_CUDA(cudaMemcpyAsync(static_cast<char*>(tot_out) + off, d.tot.p, bytes, cudaMemcpyDeviceToHost, d.stream));
+  }
+  for (auto& dp : plan->devs) {
+    SF_CUDA(cudaSetDevice(dp->dev));
+    SF_CUDA(cudaStreamSynchronize(dp->stream));
+  }
+  return SF_OK;
+}
+
+sf_status sf_plan_stats(const sf_plan* plan, sf_stats* out) {
+  if (!plan || !out) return fail(SF_EINVAL, "null argument");
+  *out = plan->stats;
+  return SF_OK;
+}
+
+void sf_plan_destroy(sf_plan* plan) { delete plan; }
+
+sf_status sf_compute_stripes(const sf_problem* p, sf_metric metric, sf_precision prec,
+                             int32_t start, int32_t stop, void* dist_out, void* tot_out,
+                             int32_t finalize, const sf_exec* ex, sf_stats* stats_out) {
+  if (!dist_out) return fail(SF_EINVAL, "dist_out is null");
+  if (metric != SF_WEIGHTED_UNNORMALIZED && !tot_out)
+    return fail(SF_EINVAL, "tot_out is required for ratio metrics");
+  sf_plan* plan = nullptr;
+  SF_TRY(sf_plan_create(p, metric, prec, start, stop, ex, &plan));
+  std::unique_ptr<sf_plan> guard(plan);
+  SF_TRY(sf_plan_run(plan, finalize));
+  SF_TRY(sf_plan_sync(plan));
+  SF_TRY(sf_plan_download(plan, dist_out, tot_out));
+  if (stats_out) *stats_out = plan->stats;
+  return SF_OK;
+}
+
+sf_status sf_accumulate_batch(const void* emb, const void* lengths, int32_t filled,
+                              int32_t n_samples, int32_t padded, sf_metric metric,
+                              sf_precision prec, int32_t start, int32_t stop, void* dist_inout,
+                              void* tot_inout, int32_t device) {
+  if (filled < 1) return fail(SF_EINVAL, "embedding batch is empty");
+  if (n_samples < 2) return fail(SF_EINVAL, "need at least 2 samples");
+  if (padded < n_samples) return fail(SF_EINVAL, "embedding batch shape is inconsistent");
+  if (!emb || !lengths || !dist_inout) return fail(SF_EINVAL, "null argument");
+  const bool has_t = metric != SF_WEIGHTED_UNNORMALIZED;
+  if (has_t && !tot_inout) return fail(SF_EINVAL, "tot_inout is required for ratio metrics");
+  if (prec != SF_FP32 && prec != SF_FP64) return fail(SF_EINVAL, "unknown precision");
+  SF_TRY(validate_range(n_samples, start, stop));
+  sf_exec ex{};
+  ex.n_devices = 1;
+  ex.devices = &device;
+  std::vector<int> devs;
+  SF_TRY(usable_devices(&ex, devs));
+  SF_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  SF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } sg{st};
+  const size_t w = prec == SF_FP64 ? 8 : 4;
+  DevBuf demb, dlen, ddist, dtot;
+  std::vector<double> lens(static_cast<size_t>(filled));
+  for (int i = 0; i < filled; ++i)
+    lens[static_cast<size_t>(i)] = prec == SF_FP64 ? static_cast<const double*>(lengths)[i]
+                                                   : static_cast<double>(static_cast<const float*>(lengths)[i]);
+  SF_TRY(demb.alloc(device, static_cast<size_t>(filled) * padded * w, "batch"));
+  SF_CUDA(cudaMemcpyAsync(demb.p, emb, static_cast<size_t>(filled) * padded * w, cudaMemcpyHostToDevice, st));
+  SF_TRY(upload(dlen, device, lens.data(), lens.size(), st, "lengths"));
+  const size_t slots = static_cast<size_t>(stop - start) * n_samples;
+  SF_TRY(ddist.alloc(device, slots * w, "distances"));
+  SF_CUDA(cudaMemcpyAsync(ddist.p, dist_inout, slots * w, cudaMemcpyHostToDevice, st));
+  if (has_t) {
+    SF_TRY(dtot.alloc(device, slots * w, "totals"));
+    SF_CUDA(cudaMemcpyAsync(dtot.p, tot_inout, slots * w, cudaMemcpyHostToDevice, st));
+  }
+  StripeArgs a;
+  a.emb = demb.p;
+  a.row_stride = padded;
+  a.lens = dlen.as<double>();
+  a.C = filled;
+  a.n = n_samples;
+  a.s_begin = start;
+  a.s_end = stop;
+  a.dist = ddist.p;
+  a.tot = has_t ? dtot.p : nullptr;
+  a.exec_updates = nullptr;
+  SF_TRY(launch_stripes(metric, prec, prec == SF_FP64 ? kSrcF64 : kSrcF32, false, a, st));
+  SF_CUDA(cudaMemcpyAsync(dist_inout, ddist.p, slots * w, cudaMemcpyDeviceToHost, st));
+  if (has_t) SF_CUDA(cudaMemcpyAsync(tot_inout, dtot.p, slots * w, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  return SF_OK;
+}
+
+sf_status sf_embed_rows(const sf_problem* p, int32_t weighted, int32_t r0, int32_t r1,
+                        double* out, int32_t padded, int32_t device) {
+  SF_TRY(validate_problem(p));
+  if (r0 < 0 || r1 > p->n_rows || r0 > r1) return fail(SF_EINVAL, "row range out of bounds");
+  if (padded < p->n_samples) return fail(SF_EINVAL, "padded width is smaller than the sample count");
+  if (!out && r1 > r0) return fail(SF_EINVAL, "out is null");
+  if (r1 == r0) return SF_OK;
+  sf_exec ex{};
+  ex.n_devices = 1;
+  ex.devices = &device;
+  // an embed-only plan: one stripe, one chunk holding every row
+  sf_plan* raw = nullptr;
+  const sf_metric m = weighted ? SF_WEIGHTED_UNNORMALIZED : SF_UNWEIGHTED;
+  ex.mem_budget_bytes = 0;
+  SF_TRY(sf_plan_create(p, m, SF_FP64, 0, 1, &ex, &raw));
+  std::unique_ptr<sf_plan> plan(raw);
+  if (plan->sched.chunks.size() != 1)
+    return fail(SF_ENOMEM, "sf_embed_rows needs the whole embedding to fit on the device");
+  DeviceState& d = *plan->devs[0];
+  SF_TRY(run_device(plan.get(), d, 0));
+  SF_CUDA(cudaStreamSynchronize(d.stream));
+  const int n = p->n_samples;
+  const int64_t rw = plan->row_words;
+  const int64_t rows = r1 - r0;
+  if (plan->bits) {
+    std::vector<uint32_t> h(static_cast<size_t>(rows * rw));
+    SF_CUDA(cudaMemcpy(h.data(), d.emb.as<uint32_t>() + r0 * rw, h.size() * 4, cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < rows; ++r)
+      for (int c = 0; c < padded; ++c)
+        out[r * padded + c] = c < n ? static_cast<double>((h[static_cast<size_t>(r * rw + (c >> 5))] >> (c & 31)) & 1u) : 0.0;
+  } else {
+    std::vector<double> h(static_cast<size_t>(rows * rw));
+    SF_CUDA(cudaMemcpy(h.data(), d.emb.as<double>() + r0 * rw, h.size() * 8, cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < rows; ++r)
+      for (int c = 0; c < padded; ++c) out[r * padded + c] = c < n ? h[static_cast<size_t>(r * rw + c)] : 0.0;
+  }
+  return SF_OK;
+}
+
+sf_status sf_finalize(sf_precision prec, int64_t count, void* dist_inout, const void* tot,
+                      int32_t device) {
+  if (count < 0 || (count > 0 && (!dist_inout || !tot))) return fail(SF_EINVAL, "bad arguments");
+  if (prec != SF_FP32 && prec != SF_FP64) return fail(SF_EINVAL, "unknown precision");
+  if (count == 0) return SF_OK;
+  sf_exec ex{};
+  ex.n_devices = 1;
+  ex.devices = &device;
+  std::vector<int> devs;
+  SF_TRY(usable_devices(&ex, devs));
+  SF_CUDA(cudaSetDevice(device));
+  const size_t w = prec == SF_FP64 ? 8 : 4;
+  DevBuf dd, dt;
+  SF_TRY(dd.alloc(device, static_cast<size_t>(count) * w, "distances"));
+  SF_TRY(dt.alloc(device, static_cast<size_t>(count) * w, "totals"));
+  SF_CUDA(cudaMemcpy(dd.p, dist_inout, static_cast<size_t>(count) * w, cudaMemcpyHostToDevice));
+  SF_CUDA(cudaMemcpy(dt.p, tot, static_cast<size_t>(count) * w, cudaMemcpyHostToDevice));
+  const int blocks = grid_for(count, 256);
+  if (prec == SF_FP64)
+    finalize_kernel<double><<<blocks, 256>>>(dd.as<double>(), dt.as<double>(), count);
+  else
+    finalize_kernel<float><<<blocks, 256>>>(dd.as<float>(), dt.as<float>(), count);
+  SF_CUDA(cudaGetLastError());
+  SF_CUDA(cudaMemcpy(dist_inout, dd.p, static_cast<size_t>(count) * w, cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
+sf_status sf_condense(sf_precision prec, int32_t n, int32_t start, int32_t stop, const void* dist,
+                      double* out, int32_t device) {
+  if (!dist || !out) return fail(SF_EINVAL, "null argument");
+  if (prec != SF_FP32 && prec != SF_FP64) return fail(SF_EINVAL, "unknown precision");
+  if (n < 2) return fail(SF_EINVAL, "need at least 2 samples");
+  SF_TRY(validate_range(n, start, stop));
+  sf_exec ex{};
+  ex.n_devices = 1;
+  ex.devices = &device;
+  std::vector<int> devs;
+  SF_TRY(usable_devices(&ex, devs));
+  SF_CUDA(cudaSetDevice(device));
+  const size_t w = prec == SF_FP64 ? 8 : 4;
+  const size_t slots = static_cast<size_t>(stop - start) * n;
+  const size_t nn = static_cast<size_t>(n) * n;
+  DevBuf dd, dout, dbad;
+  SF_TRY(dd.alloc(device, slots * w, "stripes"));
+  SF_TRY(dout.alloc(device, nn * 8, "matrix"));
+  SF_TRY(dbad.alloc(device, sizeof(int), "flag"));
+  SF_CUDA(cudaMemcpy(dd.p, dist, slots * w, cudaMemcpyHostToDevice));
+  SF_CUDA(cudaMemcpy(dout.p, out, nn * 8, cudaMemcpyHostToDevice));
+  SF_CUDA(cudaMemset(dbad.p, 0, sizeof(int)));
+  const int blocks = grid_for(static_cast<int64_t>(slots), 256);
+  if (prec == SF_FP64)
+    condense_kernel<double><<<blocks, 256>>>(dd.as<double>(), n, start, stop, dout.as<double>(), dbad.as<int>());
+  else
+    condense_kernel<float><<<blocks, 256>>>(dd.as<float>(), n, start, stop, dout.as<double>(), dbad.as<int>());
+  SF_CUDA(cudaGetLastError());
+  int bad = 0;
+  SF_CUDA(cudaMemcpy(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (bad) return fail(SF_EINVAL, "condense: duplicated slot disagrees");
+  SF_CUDA(cudaMemcpy(out, dout.p, nn * 8, cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+"""ctypes binding of oracle/liboracle_port.so — the CPU restatement.
+TEST INFRASTRUCTURE ONLY (tests/, smoke(), bench.py cpu_baseline)."""
+import ctypes as C
+from pathlib import Path
+
+import numpy as np
+
+LIB = Path(__file__).resolve().parent.parent / "oracle" / "liboracle_port.so"
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = C.CDLL(str(LIB))
+        _lib.orc_compute_stripes.restype = C.c_int
+        _lib.orc_compute_stripes.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int]
+        _lib.orc_embed_rows.restype = C.c_int
+        _lib.orc_embed_rows.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        _lib.orc_condense.restype = C.c_int
+        _lib.orc_condense.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    return _lib
+
+
+def compute_stripes(problem, metric: int, prec: int, start: int = 0, stop: int = -1,
+                    finalize: bool = True, threads: int = 1, batch: int = 64):
+    """problem: paper_2005_05826_b200._native.Problem (same struct layout)."""
+    n = problem.n_samples
+    if stop < 0:
+        stop = n // 2
+    dt = np.float64 if prec == 8 else np.float32
+    d = np.zeros((stop - start, n), dt)
+    t = np.zeros((stop - start, n), dt)
+    rc = lib().orc_compute_stripes(C.cast(C.pointer(problem.struct), C.c_void_p), metric, prec,
+                                   start, stop, d.ctypes.data, t.ctypes.data if metric != 2 else None,
+                                   int(finalize), threads, batch)
+    assert rc == 0
+    return d, (t if metric != 2 else None)
+
+
+def embed_rows(problem, weighted: bool):
+    out = np.zeros((problem.n_rows, problem.n_samples), np.float64)
+    rc = lib().orc_embed_rows(C.cast(C.pointer(problem.struct), C.c_void_p), int(weighted),
+                              out.ctypes.data)
+    assert rc == 0
+    return out
+
+
+def condense(prec: int, n: int, dist):
+    out = np.zeros((n, n), np.float64)
+    rc = lib().orc_condense(prec, n, np.ascontiguousarray(dist).ctypes.data, out.ctypes.data)
+    return out if rc == 0 else None
