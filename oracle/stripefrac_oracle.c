@@ -167,10 +167,23 @@ static void* run_job(void* arg) {
  * [start, stop) split over `threads` workers per batch. Returns 0 on
  * success. dist/tot: (stop-start) x n of double (prec 8) or float (prec 4);
  * tot may be NULL for WU. */
+int orc_compute_stripes_rows(const orc_problem* p, int metric, int prec, int start, int stop,
+                             void* dist, void* tot, int finalize, int threads, int batch,
+                             int row_limit);
+
 int orc_compute_stripes(const orc_problem* p, int metric, int prec, int start, int stop,
                         void* dist, void* tot, int finalize, int threads, int batch) {
+  return orc_compute_stripes_rows(p, metric, prec, start, stop, dist, tot, finalize, threads,
+                                  batch, 0);
+}
+
+/* As orc_compute_stripes, but only the first row_limit postorder rows (0 =
+ * all): a bounded sample of the same workload for the CPU baseline. */
+int orc_compute_stripes_rows(const orc_problem* p, int metric, int prec, int start, int stop,
+                             void* dist, void* tot, int finalize, int threads, int batch,
+                             int row_limit) {
   const int n = p->n_samples;
-  const int E = p->n_rows;
+  const int E = row_limit > 0 && row_limit < p->n_rows ? row_limit : p->n_rows;
   const size_t w = prec == 8 ? 8 : 4;
   const int64_t slots = (int64_t)(stop - start) * n;
   if (batch < 1) batch = 64;

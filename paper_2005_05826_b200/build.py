@@ -55,6 +55,20 @@ def build_native(force: bool = False, verbose: bool = False) -> Path:
     return LIB
 
 
+PEAKS_SRC = ROOT / "tools" / "fp_peaks.cu"
+PEAKS_LIB = ROOT / "tools" / "libsf_peaks.so"
+
+
+def build_tools(force: bool = False, verbose: bool = False) -> None:
+    """Measurement tooling: FP64/FP32 FMA peak microbenchmark (roofline denominators)."""
+    if force or _stale(PEAKS_LIB, [PEAKS_SRC]):
+        cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-Xcompiler",
+               "-fPIC", "-shared", str(PEAKS_SRC), "-o", str(PEAKS_LIB)]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True)
+
+
 def build_oracle(force: bool = False, verbose: bool = False) -> None:
     """Test infrastructure: C restatement + (when present) the reference build."""
     src = ORACLE / "stripefrac_oracle.c"
@@ -71,6 +85,7 @@ def build_oracle(force: bool = False, verbose: bool = False) -> None:
 
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_native(force=force, verbose=verbose)
+    build_tools(force=force, verbose=verbose)
     build_oracle(force=force, verbose=verbose)
 
 

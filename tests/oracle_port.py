@@ -51,3 +51,23 @@ def condense(prec: int, n: int, dist):
     out = np.zeros((n, n), np.float64)
     rc = lib().orc_condense(prec, n, np.ascontiguousarray(dist).ctypes.data, out.ctypes.data)
     return out if rc == 0 else None
+
+
+def time_sample(problem, metric: int, prec: int, rows: int, start: int, stop: int, threads: int):
+    """Bounded CPU sample (first `rows` postorder rows x stripes [start, stop)):
+    returns (seconds, updates). Used by bench.py's cpu_baseline leg only."""
+    import time
+    n = problem.n_samples
+    dt = np.float64 if prec == 8 else np.float32
+    d = np.zeros((stop - start, n), dt)
+    t = np.zeros((stop - start, n), dt)
+    f = lib().orc_compute_stripes_rows
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                  C.c_int, C.c_int, C.c_int, C.c_int]
+    t0 = time.perf_counter()
+    rc = f(C.cast(C.pointer(problem.struct), C.c_void_p), metric, prec, start, stop, d.ctypes.data,
+           t.ctypes.data if metric != 2 else None, 0, threads, 64, rows)
+    secs = time.perf_counter() - t0
+    assert rc == 0
+    return secs, rows * (stop - start) * n

@@ -1,0 +1,263 @@
+"""GPU parity: the sm_100a path through the C ABI vs the reference's golden
+vectors (tests/golden, produced by the reference itself) and vs the CPU
+oracle restatement (tests/oracle_port.py) on larger seeded instances.
+
+Tolerances (BASELINE.json north_star, test_kernels.cpp:187-202):
+  * unweighted, any precision: bit-exact (0/1 products are exact, so FMA and
+    mul+add round identically and the per-slot postorder sum is the same);
+  * weighted fp64 with FMA: |got - want| <= 1e-12 * max(1, |want|);
+  * weighted fp32 with FMA: <= max(1e-5 |want|, 1e-6);
+  * weighted, exact (no-FMA) mode: bit-exact in both precisions.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import golden_util as gu
+import oracle_port as op
+from paper_2005_05826_b200 import _native as N
+from paper_2005_05826_b200 import stripefrac as sf
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = [N.KERNEL_DENSE]
+
+
+def _gpu_stripes(problem, metric, prec, start, stop, kernel=N.KERNEL_DENSE, exact=False,
+                 finalize=True, mem_budget=0):
+    n = problem.n_samples
+    dt = np.float64 if prec == 8 else np.float32
+    d = np.full((stop - start, n), np.nan, dt)
+    t = np.full((stop - start, n), np.nan, dt)
+    ex, _keep = N.make_exec([0], kernel, exact, mem_budget)
+    st = N.sf_stats()
+    N.check(N.lib().sf_compute_stripes(problem.ref, metric, prec, start, stop, N.ptr(d),
+                                       N.ptr(t) if metric != 2 else None, int(finalize),
+                                       C.byref(ex), C.byref(st)))
+    return d, (t if metric != 2 else None), st
+
+
+def _assert_close(metric, prec, exact, got, want):
+    if metric == 1 or exact:
+        assert np.array_equal(got, want), f"max |diff| {np.nanmax(np.abs(got - want))}"
+    elif prec == 8:
+        tol = 1e-12 * np.maximum(1.0, np.abs(want))
+        assert np.all(np.abs(got - want) <= tol), f"max |diff| {np.abs(got - want).max()}"
+    else:
+        w = want.astype(np.float64)
+        tol = np.maximum(1e-5 * np.abs(w), 1e-6)
+        assert np.all(np.abs(got.astype(np.float64) - w) <= tol)
+
+
+CASES = gu.all_cases()
+
+
+@pytest.fixture(scope="module")
+def device_ok():
+    assert N.lib().sf_device_count() >= 1, "no sm_100 device visible (GPU tests need a B200)"
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_golden_stripes(device_ok, case, kernel):
+    tree, table = gu.case_inputs(case)
+    problem = sf.flatten(tree, table)
+    n = table.n_samples()
+    for r in case["results"]:
+        metric = int(sf.metric_from_name(r["metric"]))
+        if kernel == N.KERNEL_SPARSE and metric != 1:
+            continue
+        prec = 8 if r["precision"] == "fp64" else 4
+        gd, gt = gu.stripes(r, n)
+        for exact in ((False, True) if metric != 1 else (False,)):
+            d, t, _ = _gpu_stripes(problem, metric, prec, r["start"], r["stop"], kernel, exact)
+            _assert_close(metric, prec, exact, d, gd)
+            if gt is not None:
+                _assert_close(metric, prec, exact, t, gt)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "embedding_weighted" in c],
+                         ids=lambda c: c["name"])
+def test_golden_embedding_rows(device_ok, case):
+    """K1 rows are bit-identical to Embedder::next_batch (embed.cpp:42-82)."""
+    tree, table = gu.case_inputs(case)
+    problem = sf.flatten(tree, table)
+    n = table.n_samples()
+    for weighted, key in ((1, "embedding_weighted"), (0, "embedding_unweighted")):
+        want = np.array(case[key], dtype=np.float64)
+        pad = n + 3
+        out = np.full((problem.n_rows, pad), np.nan)
+        N.check(N.lib().sf_embed_rows(problem.ref, weighted, 0, problem.n_rows, N.ptr(out), pad, 0))
+        assert np.array_equal(out[:, :n], want)
+        assert np.all(out[:, n:] == 0.0)
+
+
+def test_demo_condense_and_tsv_bytes(device_ok):
+    """C1: full DM through condense on device, TSV bytes identical (test_cli.cpp:108-139)."""
+    case = gu.load("demo.json")
+    tree, table = gu.case_inputs(case)
+    for entry in case["dm"]:
+        m = sf.metric_from_name(entry["metric"])
+        p = sf.precision_from_name(entry["precision"])
+        cfg = sf.KernelConfig(metric=m, precision=p)
+        for exact in (False, True):
+            dm = sf.compute_distance_matrix(tree, table, cfg,
+                                            exec_options=sf.ExecOptions(exact=exact))
+            want = np.array(entry["values"]).reshape(dm.n(), dm.n())
+            if m == sf.Metric.Unweighted or exact:
+                assert np.array_equal(dm.values, want)
+                assert sf.to_tsv(dm) == entry["tsv"]
+            else:
+                assert np.allclose(dm.values, want, rtol=1e-12 if p == sf.Precision.Fp64 else 1e-5,
+                                   atol=0 if p == sf.Precision.Fp64 else 1e-6)
+
+
+def test_hand_worked_values(device_ok):
+    """test_kernels.cpp:49-78: two disjoint leaves give 2.0 / 1.0 / 1.0 exactly."""
+    t = sf.parse_newick("(A:1,B:1);")
+    table = sf.make_table(["s1", "s2"], ["A", "B"], [[4, 0], [0, 4]])
+    for v in sf.Variant:
+        wu = sf.compute_distance_matrix(t, table, sf.KernelConfig(sf.Metric.WeightedUnnormalized, v))
+        assert wu.values[0, 1] == 2.0
+        wn = sf.compute_distance_matrix(t, table, sf.KernelConfig(sf.Metric.WeightedNormalized, v))
+        assert wn.values[0, 1] == 1.0
+        uw = sf.compute_distance_matrix(t, table, sf.KernelConfig(sf.Metric.Unweighted, v))
+        assert uw.values[0, 1] == 1.0
+        assert wu.values[0, 0] == 0.0 and wu.values[1, 0] == wu.values[0, 1]
+    t3 = sf.parse_newick("((A:1,B:1):1,C:1);")
+    tb3 = sf.make_table(["s1", "s2"], ["A", "B", "C"], [[1, 0], [0, 1], [0, 0]])
+    uw = sf.compute_distance_matrix(t3, tb3, sf.KernelConfig(sf.Metric.Unweighted))
+    assert abs(uw.values[0, 1] - 2.0 / 3.0) <= 1e-12
+
+
+@pytest.mark.parametrize("metric", [1, 2, 3])
+@pytest.mark.parametrize("prec", [8, 4])
+def test_oracle_random_instances(device_ok, metric, prec):
+    """Seeded instances beyond the fixtures (several CTA tiles, wrap, tails),
+    checked against the pinned CPU restatement."""
+    for seed, n, leaves, dens, subset in [(11, 67, 150, 0.05, 0), (12, 130, 400, 0.02, 300),
+                                          (13, 257, 600, 0.01, 0), (14, 2, 5, 0.5, 0),
+                                          (15, 3, 2, 0.9, 0), (16, 300, 90, 0.2, 0)]:
+        inst = sf.random_instance(seed, n, leaves, dens, subset)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 3, S)]:
+            if start >= stop:
+                continue
+            wd, wt = op.compute_stripes(problem, metric, prec, start, stop)
+            for exact in ((False, True) if metric != 1 else (False,)):
+                d, t, st = _gpu_stripes(problem, metric, prec, start, stop, exact=exact)
+                _assert_close(metric, prec, exact, d, wd)
+                if wt is not None:
+                    _assert_close(metric, prec, exact, t, wt)
+                assert st.updates_alg == problem.n_rows * (stop - start) * n
+
+
+def test_chunked_embedding_with_pending_rows(device_ok):
+    """A tiny device budget forces many postorder chunks and pending slots;
+    results must stay bitwise identical (batch boundaries never change bits)."""
+    inst = sf.random_instance(21, 96, 500, 0.05)
+    problem = sf.flatten(inst.tree, inst.table)
+    for metric in (1, 3):
+        full, fullt, st1 = _gpu_stripes(problem, metric, 8, 0, 48, exact=True)
+        row_bytes = 4 * 3 if metric == 1 else 8 * 96
+        small, smallt, st2 = _gpu_stripes(problem, metric, 8, 0, 48, exact=True,
+                                          mem_budget=row_bytes * 37)
+        assert st2.n_chunks > 5
+        assert np.array_equal(full, small)
+        assert np.array_equal(fullt, smallt)
+
+
+def test_partition_independence_bitwise(device_ok):
+    """test_kernels.cpp:154-170 / acceptance.cpp:237-280: any tiling of [0,S)
+    condenses to the full-range result bit for bit."""
+    inst = sf.random_instance(1234, 17, 40, 0.4)
+    cfg = sf.KernelConfig(sf.Metric.WeightedNormalized, sf.Variant.Tiled)
+    full = sf.compute_distance_matrix(inst.tree, inst.table, cfg)
+    for ranges in ([(0, 8)], [(0, 4), (4, 8)], [(0, 1), (1, 2), (2, 5), (5, 8)]):
+        parts = [sf.compute_unifrac(inst.tree, inst.table, cfg, a, b) for a, b in ranges]
+        merged = sf.condense(parts, inst.table.sample_ids)
+        assert np.array_equal(merged.values, full.values)
+
+
+def test_batch_api_matches_full_run(device_ok):
+    """Embedder + accumulate + finalize (kernels.hpp:232-259) == compute_unifrac."""
+    inst = sf.random_instance(777, 23, 48, 0.4)
+    for m in sf.Metric:
+        cfg = sf.KernelConfig(m, sf.Variant.Tiled)
+        want = sf.compute_unifrac(inst.tree, inst.table, cfg)
+        sh = sf.sheared_to_table(inst.tree, inst.table)
+        em = sf.Embedder(sh, inst.table, sf.embed_mode(m), cfg.resolved_step_size())
+        sset = sf.allocate_stripes(23, 0, 11, m)
+        c = sf.KernelCounters()
+        while (b := em.next_batch(5)) is not None:
+            sf.accumulate(sset, b, cfg, c)
+        sf.finalize(sset)
+        if m == sf.Metric.Unweighted:
+            assert np.array_equal(sset.distances, want.distances)
+        else:
+            assert np.allclose(sset.distances, want.distances, rtol=1e-12, atol=0)
+        E = em.total_rows()
+        assert c.kernel_passes == -(-E // 5)
+        assert c.embedding_reads == 2 * E * 11 * 23
+
+
+def test_counter_law(device_ok):
+    """test_kernels.cpp:123-152: writes = E (naive) or ceil(E/B) per entry."""
+    inst = sf.random_instance(31337, 20, 32, 0.4)
+    E = 2 * 32 - 2
+    c = sf.KernelCounters()
+    sf.compute_unifrac(inst.tree, inst.table,
+                       sf.KernelConfig(sf.Metric.WeightedUnnormalized, sf.Variant.Batched,
+                                       sf.Precision.Fp64, 16), 3, 7, 1, c)
+    entries = 4 * 20
+    passes = (E + 15) // 16
+    assert c.accumulator_writes == passes * entries
+    assert c.embedding_reads == 2 * E * entries
+    assert c.kernel_passes == passes
+
+
+def test_misuse_is_rejected(device_ok):
+    """test_kernels.cpp:219-264."""
+    t = sf.parse_newick("(A:1,B:1);")
+    table = sf.make_table(["s1", "s2"], ["A", "B"], [[4, 1], [1, 4]])
+    with pytest.raises(sf.Error):
+        sf.compute_unifrac(t, table, sf.KernelConfig(sf.Metric.Unweighted), real=np.float32)
+    with pytest.raises(sf.Error):
+        sf.compute_unifrac(t, table, sf.KernelConfig(sf.Metric.Unweighted, batch_capacity=0))
+    with pytest.raises(sf.Error, match="does not fit"):
+        sf.compute_unifrac(t, table, sf.KernelConfig(sf.Metric.Unweighted), 0, 2)
+    em = sf.Embedder(t, table, sf.EmbedMode.Weighted, 16)
+    batch = em.next_batch(64)
+    sset = sf.allocate_stripes(2, 0, 1, sf.Metric.WeightedUnnormalized)
+    cfg = sf.KernelConfig(sf.Metric.WeightedUnnormalized)
+    c = sf.KernelCounters()
+    sf.accumulate(sset, batch, cfg, c)
+    sf.finalize(sset)
+    with pytest.raises(sf.Error):
+        sf.accumulate(sset, batch, cfg, c)
+    with pytest.raises(sf.Error):
+        sf.finalize(sset)
+    s2 = sf.allocate_stripes(2, 0, 1, sf.Metric.WeightedUnnormalized)
+    with pytest.raises(sf.Error):
+        sf.accumulate(s2, sf.EmbeddingBatch(np.zeros((0, 16)), np.zeros(0), 0, 2, 16), cfg, c)
+    with pytest.raises(sf.Error):
+        sf.accumulate(s2, batch, sf.KernelConfig(sf.Metric.Unweighted), c)
+    em2 = sf.Embedder(t, table, sf.EmbedMode.Weighted, 1)
+    with pytest.raises(sf.Error):
+        sf.accumulate(s2, em2.next_batch(64), cfg, c)
+
+
+def test_fp32_mantel_against_fp64(device_ok):
+    """acceptance.cpp:282-309: fp32 vs fp64, r^2 >= 0.9999, p <= 0.001, drift <= 1e-5."""
+    inst = sf.random_instance(60464, 64, 512, 0.3)
+    for m in sf.Metric:
+        d64 = sf.compute_distance_matrix(inst.tree, inst.table, sf.KernelConfig(m))
+        d32 = sf.compute_distance_matrix(inst.tree, inst.table,
+                                         sf.KernelConfig(m, precision=sf.Precision.Fp32, step_size=32))
+        res = sf.mantel(d64, d32, 999, 4)
+        assert res["r_squared"] >= 0.9999 and res["p_value"] <= 0.001
+        iu = np.triu_indices(64, 1)
+        drift = np.abs(d32.values[iu] - d64.values[iu]) / np.maximum(np.abs(d64.values[iu]), 0.1)
+        assert drift.max() <= 1e-5

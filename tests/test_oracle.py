@@ -1,0 +1,95 @@
+"""CPU: pin the oracle and the host-side prerequisites to the reference.
+
+The golden vectors were produced by the reference implementation itself
+(oracle/_ref, built from /root/reference/proj/src). These tests check, bit
+for bit:
+  * the C restatement (oracle/stripefrac_oracle.c) — stripes and embeddings;
+  * shear + postorder flattening (sfh_flatten) — rows, lengths, leaf map;
+  * the synthetic generator (sfh_random_instance) — tables and trees.
+"""
+import numpy as np
+import pytest
+
+import golden_util as gu
+import oracle_port as op
+from paper_2005_05826_b200 import stripefrac as sf
+
+CASES = gu.all_cases()
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_flatten_matches_reference_rows(case):
+    tree, table = gu.case_inputs(case)
+    prob = sf.flatten(tree, table)
+    rows = case["rows"]
+    assert prob.parent_row.tolist() == rows["parent"]
+    assert prob.lengths.tolist() == rows["length"]
+    names = [table.feature_ids[f] if f >= 0 else "" for f in prob.leaf_feature.tolist()]
+    assert names == rows["leaf_name"]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_oracle_stripes_bitwise(case):
+    tree, table = gu.case_inputs(case)
+    prob = sf.flatten(tree, table)
+    n = table.n_samples()
+    for r in case["results"]:
+        m = int(sf.metric_from_name(r["metric"]))
+        p = 8 if r["precision"] == "fp64" else 4
+        gd, gt = gu.stripes(r, n)
+        for threads, batch in ((1, 64), (3, 7)):
+            d, t = op.compute_stripes(prob, m, p, r["start"], r["stop"], threads=threads, batch=batch)
+            assert np.array_equal(d, gd)
+            if gt is not None:
+                assert np.array_equal(t, gt)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if "embedding_weighted" in c],
+                         ids=lambda c: c["name"])
+def test_oracle_embedding_bitwise(case):
+    tree, table = gu.case_inputs(case)
+    prob = sf.flatten(tree, table)
+    for w, key in ((1, "embedding_weighted"), (0, "embedding_unweighted")):
+        assert np.array_equal(op.embed_rows(prob, w), np.array(case[key]))
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c["params"].get("kind") == "instance"],
+                         ids=lambda c: c["name"])
+def test_generator_matches_reference_instance(case):
+    pr = case["params"]
+    inst = sf.random_instance(pr["seed"], pr["n"], pr["leaves"], pr["density"], pr["subset"])
+    tree, table = gu.case_inputs(case)
+    assert inst.table.feature_ids == table.feature_ids
+    assert np.array_equal(inst.table.feat_ptr, table.feat_ptr)
+    assert np.array_equal(inst.table.sample_idx, table.sample_idx)
+    assert np.array_equal(inst.table.counts, table.counts)
+    assert np.array_equal(inst.table.sample_totals, table.sample_totals)
+    a, b = sf.flatten(inst.tree, inst.table), sf.flatten(tree, table)
+    assert np.array_equal(a.parent_row, b.parent_row)
+    assert np.array_equal(a.lengths, b.lengths)
+    assert np.array_equal(a.leaf_feature, b.leaf_feature)
+
+
+def test_oracle_condense_matches_reference_dm():
+    case = gu.load("demo.json")
+    tree, table = gu.case_inputs(case)
+    prob = sf.flatten(tree, table)
+    for entry in case["dm"]:
+        m = int(sf.metric_from_name(entry["metric"]))
+        p = 8 if entry["precision"] == "fp64" else 4
+        d, _ = op.compute_stripes(prob, m, p)
+        got = op.condense(p, table.n_samples(), d)
+        assert np.array_equal(got, np.array(entry["values"]).reshape(got.shape))
+
+
+def test_brute_force_agrees_with_oracle():
+    """The reference's brute-force oracle (validate.cpp:12-81) vs the stripes,
+    1e-12 absolute as in test_kernels.cpp:80-99."""
+    for case in gu.load("instances_small.json"):
+        tree, table = gu.case_inputs(case)
+        prob = sf.flatten(tree, table)
+        n = table.n_samples()
+        for mi, bf in enumerate(case["brute_force"]):
+            d, _ = op.compute_stripes(prob, mi + 1, 8)
+            got = op.condense(8, n, d)
+            assert np.abs(got - np.array(bf).reshape(n, n)).max() <= 1e-12
