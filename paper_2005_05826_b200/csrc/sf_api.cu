@@ -14,6 +14,7 @@
 
 #include "embed_kernels.cuh"
 #include "sf_common.hpp"
+#include "sparse_kernels.cuh"
 #include "stripe_kernels.cuh"
 #include "stripefrac_cuda.h"
 
@@ -397,11 +398,33 @@ struct sf_plan {
 namespace {
 
 // Sparse node-packed bit kernel for the unweighted metric (kernel 2).
-sf_status sparse_prepare(sf_plan*, DeviceState&, const sf_problem*) {
-  return fail(SF_EINVAL, "the sparse bit kernel is not available in this build");
+struct SparseCfg {
+  static constexpr int RK = 4, RS = 2, NWK = 8, NWS = 2;
+  static constexpr int TK = NWK * RK, TS = NWS * 32 * RS;
+};
+
+int64_t sparse_n_ext(int n) {
+  const int64_t need = static_cast<int64_t>(n) + n / 2 + SparseCfg::TK + SparseCfg::TS + 64;
+  return (need + 3) / 4 * 4;
 }
-sf_status sparse_run(sf_plan*, DeviceState&) {
-  return fail(SF_EINVAL, "the sparse bit kernel is not available in this build");
+
+sf_status sparse_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
+  const int64_t W = (plan->E + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(plan->n);
+  SF_TRY(d.nodebits.alloc(d.dev, static_cast<size_t>(W * n_ext) * 4, "node-packed presence bits"));
+  std::vector<double> lens(static_cast<size_t>(W * 32), 0.0);
+  std::copy(p->lengths, p->lengths + plan->E, lens.begin());
+  SF_TRY(upload(d.lens_pad, d.dev, lens.data(), lens.size(), d.stream, "padded lengths"));
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_sparse(const SparseArgs& a, cudaStream_t st) {
+  using C = SparseCfg;
+  const dim3 grid((a.n + C::TK - 1) / C::TK, (a.s_end - a.s_begin + C::TS - 1) / C::TS);
+  stripe_sparse_kernel<Real, C::RK, C::RS, C::NWK, C::NWS><<<grid, 32 * C::NWK * C::NWS, 0, st>>>(a);
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
 }
 
 // Layout of one chunk's schedule arrays inside the packed device buffer.
@@ -442,50 +465,75 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
     SF_CUDA(cudaMemsetAsync(d.tot.p, 0, static_cast<size_t>(slots) * w, st));
   SF_CUDA(cudaMemsetAsync(d.exec_ctr.p, 0, sizeof(unsigned long long), st));
 
-  if (plan->kernel == 2) {
-    SF_TRY(sparse_run(plan, d));
-  } else {
-    const int64_t stride = plan->row_words;
-    for (size_t ci = 0; ci < plan->sched.chunks.size(); ++ci) {
-      const Chunk& c = plan->sched.chunks[ci];
-      const int32_t* base = d.sched.as<int32_t>();
-      auto arr = [&](int k) { return base + d.sched_off[ci * kNumArr + static_cast<size_t>(k)]; };
-      const int C = c.r1 - c.r0;
-      SF_CUDA(cudaEventRecord(d.events[1 + 3 * ci], st));
-      const size_t row_bytes = static_cast<size_t>(stride) * (plan->bits ? 4 : 8);
-      SF_CUDA(cudaMemsetAsync(d.emb.p, 0, row_bytes * static_cast<size_t>(C), st));
-      const int nl = static_cast<int>(c.leaf_rows.size());
-      if (nl > 0) {
-        const int blocks = grid_for(static_cast<int64_t>(nl) * 32, 256);
-        if (plan->bits)
-          embed_leaf_bits<<<blocks, 256, 0, st>>>(d.emb.as<uint32_t>(), stride, arr(kLeafRows),
+  const int64_t stride = plan->row_words;
+  const int ncols = static_cast<int>(plan->bits ? (n + 31) / 32 : n);
+  const int32_t* base = d.sched.as<int32_t>();
+  for (size_t ci = 0; ci < plan->sched.chunks.size(); ++ci) {
+    const Chunk& c = plan->sched.chunks[ci];
+    auto arr = [&](int k) { return base + d.sched_off[ci * kNumArr + static_cast<size_t>(k)]; };
+    const int C = c.r1 - c.r0;
+    SF_CUDA(cudaEventRecord(d.events[1 + 3 * ci], st));
+    // ---- K1: embedding rows of this chunk
+    const size_t row_bytes = static_cast<size_t>(stride) * (plan->bits ? 4 : 8);
+    SF_CUDA(cudaMemsetAsync(d.emb.p, 0, row_bytes * static_cast<size_t>(C), st));
+    const int nl = static_cast<int>(c.leaf_rows.size());
+    if (nl > 0) {
+      const int blocks = grid_for(static_cast<int64_t>(nl) * 32, 256);
+      if (plan->bits)
+        embed_leaf_bits<<<blocks, 256, 0, st>>>(d.emb.as<uint32_t>(), stride, arr(kLeafRows),
+                                                arr(kLeafFeat), nl, d.feat_ptr.as<int64_t>(),
+                                                d.sidx.as<int32_t>(), d.counts.as<double>());
+      else
+        embed_leaf_values<<<blocks, 256, 0, st>>>(d.emb.as<double>(), stride, arr(kLeafRows),
                                                   arr(kLeafFeat), nl, d.feat_ptr.as<int64_t>(),
-                                                  d.sidx.as<int32_t>(), d.counts.as<double>());
-        else
-          embed_leaf_values<<<blocks, 256, 0, st>>>(d.emb.as<double>(), stride, arr(kLeafRows),
-                                                    arr(kLeafFeat), nl, d.feat_ptr.as<int64_t>(),
-                                                    d.sidx.as<int32_t>(), d.counts.as<double>(),
-                                                    d.totals.as<double>());
-        SF_CUDA(cudaGetLastError());
-        plan->stats.launches++;
-      }
-      const int ncols = static_cast<int>(plan->bits ? (n + 31) / 32 : n);
-      for (size_t h = 0; h + 1 < c.lvl_ptr.size(); ++h) {
-        const int lo = c.lvl_ptr[h], hi = c.lvl_ptr[h + 1];
-        if (hi <= lo) continue;
-        const dim3 grid((ncols + 127) / 128, std::min(hi - lo, 65535));
-        if (plan->bits)
-          embed_level_bits<<<grid, 128, 0, st>>>(d.emb.as<uint32_t>(), stride, d.pend.as<uint32_t>(),
+                                                  d.sidx.as<int32_t>(), d.counts.as<double>(),
+                                                  d.totals.as<double>());
+      SF_CUDA(cudaGetLastError());
+      plan->stats.launches++;
+    }
+    for (size_t h = 0; h + 1 < c.lvl_ptr.size(); ++h) {
+      const int lo = c.lvl_ptr[h], hi = c.lvl_ptr[h + 1];
+      if (hi <= lo) continue;
+      const dim3 grid((ncols + 127) / 128, std::min(hi - lo, 65535));
+      if (plan->bits)
+        embed_level_bits<<<grid, 128, 0, st>>>(d.emb.as<uint32_t>(), stride, d.pend.as<uint32_t>(),
+                                               arr(kIntRows) + lo, arr(kCptr) + lo, arr(kCodes),
+                                               hi - lo, ncols);
+      else
+        embed_level_values<<<grid, 128, 0, st>>>(d.emb.as<double>(), stride, d.pend.as<double>(),
                                                  arr(kIntRows) + lo, arr(kCptr) + lo, arr(kCodes),
                                                  hi - lo, ncols);
-        else
-          embed_level_values<<<grid, 128, 0, st>>>(d.emb.as<double>(), stride, d.pend.as<double>(),
-                                                   arr(kIntRows) + lo, arr(kCptr) + lo, arr(kCodes),
-                                                   hi - lo, ncols);
-        SF_CUDA(cudaGetLastError());
-        plan->stats.launches++;
-      }
-      SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
+      SF_CUDA(cudaGetLastError());
+      plan->stats.launches++;
+    }
+    if (plan->kernel == 2) {
+      // node-packed presence bits for the sparse walk
+      const int64_t W = (plan->E + 31) / 32;
+      const int64_t n_ext = sparse_n_ext(n);
+      transpose_bits_kernel<<<grid_for(W * stride * 32, 256), 256, 0, st>>>(
+          d.emb.as<uint32_t>(), stride, plan->E, n, d.nodebits.as<uint32_t>(), n_ext,
+          static_cast<int32_t>(W));
+      extend_columns_kernel<<<grid_for(W * (n_ext - n), 256), 256, 0, st>>>(
+          d.nodebits.as<uint32_t>(), n_ext, n, static_cast<int32_t>(W));
+      SF_CUDA(cudaGetLastError());
+      plan->stats.launches += 2;
+    }
+    SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
+    // ---- K2: stripe update over the chunk's rows
+    if (plan->kernel == 2) {
+      SparseArgs a;
+      a.nb = d.nodebits.as<uint32_t>();
+      a.n_ext = sparse_n_ext(n);
+      a.lens = d.lens_pad.as<double>();
+      a.W = static_cast<int32_t>((plan->E + 31) / 32);
+      a.n = n;
+      a.s_begin = d.a;
+      a.s_end = d.b;
+      a.dist = d.dist.p;
+      a.tot = d.tot.p;
+      a.exec_updates = d.exec_ctr.as<unsigned long long>();
+      SF_TRY(plan->prec == SF_FP64 ? launch_sparse<double>(a, st) : launch_sparse<float>(a, st));
+    } else {
       StripeArgs a;
       a.emb = d.emb.p;
       a.row_stride = stride;
@@ -499,21 +547,21 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
       a.exec_updates = d.exec_ctr.as<unsigned long long>();
       SF_TRY(launch_stripes(plan->metric, plan->prec, plan->bits ? kSrcBits : kSrcF64,
                             plan->exact, a, st));
+    }
+    plan->stats.launches++;
+    SF_CUDA(cudaEventRecord(d.events[3 + 3 * ci], st));
+    const int ncarry = static_cast<int>(c.carry_src.size());
+    if (ncarry > 0) {
+      const dim3 grid((ncols + 127) / 128, std::min(ncarry, 65535));
+      if (plan->bits)
+        embed_carry<uint32_t><<<grid, 128, 0, st>>>(d.emb.as<uint32_t>(), d.pend.as<uint32_t>(),
+                                                    stride, arr(kCarrySrc), arr(kCarryDst),
+                                                    ncarry, ncols);
+      else
+        embed_carry<double><<<grid, 128, 0, st>>>(d.emb.as<double>(), d.pend.as<double>(), stride,
+                                                  arr(kCarrySrc), arr(kCarryDst), ncarry, ncols);
+      SF_CUDA(cudaGetLastError());
       plan->stats.launches++;
-      SF_CUDA(cudaEventRecord(d.events[3 + 3 * ci], st));
-      const int ncarry = static_cast<int>(c.carry_src.size());
-      if (ncarry > 0) {
-        const dim3 grid((ncols + 127) / 128, std::min(ncarry, 65535));
-        if (plan->bits)
-          embed_carry<uint32_t><<<grid, 128, 0, st>>>(d.emb.as<uint32_t>(), d.pend.as<uint32_t>(),
-                                                      stride, arr(kCarrySrc), arr(kCarryDst),
-                                                      ncarry, ncols);
-        else
-          embed_carry<double><<<grid, 128, 0, st>>>(d.emb.as<double>(), d.pend.as<double>(), stride,
-                                                    arr(kCarrySrc), arr(kCarryDst), ncarry, ncols);
-        SF_CUDA(cudaGetLastError());
-        plan->stats.launches++;
-      }
     }
   }
   const size_t ne = d.events.size();
@@ -575,6 +623,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
   plan->kernel = (ex && ex->kernel == 2) ? 2 : 1;
+  // auto: the sparse walk for the unweighted metric (exact, same bits)
+  if ((!ex || ex->kernel == 0) && metric == SF_UNWEIGHTED) plan->kernel = 2;
   if (plan->kernel == 2 && metric != SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the sparse bit kernel implements the unweighted metric only");
   const int n = p->n_samples;
@@ -671,20 +721,12 @@ sf_status sf_plan_sync(sf_plan* plan) {
     if (!plan->ran) continue;
     double e_ms = 0, s_ms = 0, f_ms = 0, t_ms = 0;
     const size_t ne = d.events.size();
-    if (plan->kernel != 2) {
-      for (size_t ci = 0; ci < plan->sched.chunks.size(); ++ci) {
-        float a = 0, b = 0;
-        SF_CUDA(cudaEventElapsedTime(&a, d.events[1 + 3 * ci], d.events[2 + 3 * ci]));
-        SF_CUDA(cudaEventElapsedTime(&b, d.events[2 + 3 * ci], d.events[3 + 3 * ci]));
-        e_ms += a;
-        s_ms += b;
-      }
-    } else {
+    for (size_t ci = 0; ci < plan->sched.chunks.size(); ++ci) {
       float a = 0, b = 0;
-      SF_CUDA(cudaEventElapsedTime(&a, d.events[1], d.events[2]));
-      SF_CUDA(cudaEventElapsedTime(&b, d.events[2], d.events[3]));
-      e_ms = a;
-      s_ms = b;
+      SF_CUDA(cudaEventElapsedTime(&a, d.events[1 + 3 * ci], d.events[2 + 3 * ci]));
+      SF_CUDA(cudaEventElapsedTime(&b, d.events[2 + 3 * ci], d.events[3 + 3 * ci]));
+      e_ms += a;
+      s_ms += b;
     }
     float f = 0, t = 0;
     SF_CUDA(cudaEventElapsedTime(&f, d.events[ne - 2], d.events[ne - 1]));

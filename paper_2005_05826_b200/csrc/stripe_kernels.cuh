@@ -50,16 +50,27 @@ __device__ __forceinline__ float mul_add_rn<float>(float a, float b, float c) {
 // max(u,v) are 0 or 1, so the product is exact and fma == mul+add bitwise.
 // Weighted metrics use one fma per accumulator unless EXACT (two roundings,
 // bit-identical to the reference's no-FMA x86-64 build).
+//
+// The reference writes |u-v| as `diff < 0 ? -diff : diff` and max as
+// `u > v ? u : v`; they differ from fabs/fmax only for NaN and signed zeros.
+// Embedding values here are finite and >= +0 (validated counts, positive
+// totals), and a -0 term cannot change an accumulator that starts at +0 and
+// only grows, so fabs/fmax give identical sums — and map to the |x| operand
+// modifier and DMNMX instead of DSETP+FSEL pairs (4 FP-pipe ops per update).
+__device__ __forceinline__ double abs_r(double x) { return fabs(x); }
+__device__ __forceinline__ float abs_r(float x) { return fabsf(x); }
+__device__ __forceinline__ double max_r(double a, double b) { return fmax(a, b); }
+__device__ __forceinline__ float max_r(float a, float b) { return fmaxf(a, b); }
+
 template <int M, bool EXACT, class Real>
 __device__ __forceinline__ void update_entry(Real u, Real v, Real len, Real& d, Real& t) {
-  Real diff = u - v;
-  diff = diff < Real(0) ? -diff : diff;
+  const Real diff = abs_r(u - v);
   if (EXACT && M != kUW)
     d = mul_add_rn(diff, len, d);
   else
     d = fma_r(diff, len, d);
   if constexpr (M == kUW) {
-    t = fma_r(u > v ? u : v, len, t);
+    t = fma_r(max_r(u, v), len, t);
   } else if constexpr (M == kWN) {
     if (EXACT)
       t = mul_add_rn(u + v, len, t);
@@ -85,7 +96,7 @@ template <int SRC, class Real>
 __device__ __forceinline__ Real load_emb(const void* emb, int64_t row_off, int smp) {
   if constexpr (SRC == kSrcBits) {
     const uint32_t w = static_cast<const uint32_t*>(emb)[row_off + (smp >> 5)];
-    return static_cast<Real>((w >> (smp & 31)) & 1u);
+    return ((w >> (smp & 31)) & 1u) ? Real(1) : Real(0);
   } else if constexpr (SRC == kSrcF64) {
     return static_cast<Real>(static_cast<const double*>(emb)[row_off + smp]);
   } else {
@@ -154,7 +165,7 @@ __global__ void __launch_bounds__(32 * NWK * NWS)
           Real val = Real(0);
           if (e < VW) {
             int pos = P0 + e;
-            if (pos >= n) pos %= n;  // stripe_pair wrap (stripes.cpp:23-28)
+            while (pos >= n) pos -= n;  // stripe_pair wrap (stripes.cpp:23-28)
             val = load_emb<SRC, Real>(a.emb, roff, pos);
           }
           sv[rr][e % RS][e / RS] = val;

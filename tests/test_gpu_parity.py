@@ -21,7 +21,7 @@ from paper_2005_05826_b200 import stripefrac as sf
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [N.KERNEL_DENSE]
+KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE]
 
 
 def _gpu_stripes(problem, metric, prec, start, stop, kernel=N.KERNEL_DENSE, exact=False,
@@ -261,3 +261,28 @@ def test_fp32_mantel_against_fp64(device_ok):
         iu = np.triu_indices(64, 1)
         drift = np.abs(d32.values[iu] - d64.values[iu]) / np.maximum(np.abs(d64.values[iu]), 0.1)
         assert drift.max() <= 1e-5
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_sparse_kernel_matches_dense_bitwise(device_ok, prec):
+    """Both unweighted kernels apply the same adds in the same order."""
+    for seed, n, leaves, dens, subset in [(41, 200, 800, 0.01, 0), (42, 333, 1500, 0.004, 1000),
+                                          (43, 64, 3000, 0.02, 0), (44, 9, 70, 0.3, 0)]:
+        inst = sf.random_instance(seed, n, leaves, dens, subset)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 2, S)]:
+            d1, t1, _ = _gpu_stripes(problem, 1, prec, start, stop, kernel=N.KERNEL_DENSE)
+            d2, t2, st = _gpu_stripes(problem, 1, prec, start, stop, kernel=N.KERNEL_SPARSE)
+            assert np.array_equal(d1, d2) and np.array_equal(t1, t2)
+            wd, wt = op.compute_stripes(problem, 1, prec, start, stop)
+            assert np.array_equal(d2, wd) and np.array_equal(t2, wt)
+            assert st.updates_exec < st.updates_alg
+
+
+def test_sparse_is_the_default_for_unweighted(device_ok):
+    inst = sf.random_instance(45, 50, 100, 0.1)
+    problem = sf.flatten(inst.tree, inst.table)
+    _, _, st = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_AUTO)
+    # the sparse walk only touches rows present in a slot's samples
+    assert st.updates_exec < st.updates_alg
