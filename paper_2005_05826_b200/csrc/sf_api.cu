@@ -421,8 +421,11 @@ sf_status sparse_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
 template <class Real>
 sf_status launch_sparse(const SparseArgs& a, cudaStream_t st) {
   using C = SparseCfg;
+  using T = SparseTile<C::RK, C::RS, C::NWK, C::NWS>;
+  auto* kern = stripe_sparse_kernel<Real, C::RK, C::RS, C::NWK, C::NWS>;
+  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES));
   const dim3 grid((a.n + C::TK - 1) / C::TK, (a.s_end - a.s_begin + C::TS - 1) / C::TS);
-  stripe_sparse_kernel<Real, C::RK, C::RS, C::NWK, C::NWS><<<grid, 32 * C::NWK * C::NWS, 0, st>>>(a);
+  kern<<<grid, T::NT, T::BYTES, st>>>(a);
   SF_CUDA(cudaGetLastError());
   return SF_OK;
 }

@@ -9,19 +9,21 @@
 // (row, slot) although ~98% of them are 0/0 at the EMP shape;
 // here each slot walks only the rows present in either of its samples:
 //
-//   NB[w][c]  = 32 presence bits of rows 32w..32w+31 for sample column c
-//               (word-major, sample columns extended past n so the shifted
-//               operand k+s+1 never wraps inside a tile);
-//   per CTA   = TK samples x TS stripes; rows are streamed in chunks of 32
-//               words (1024 rows): u words [k0, k0+TK), v words
-//               [k0+s0+1, k0+s0+TK+TS), per-column occupancy masks of the
-//               chunk's nonzero words, and the rows' lengths;
-//   per slot  = for each nonzero word of (u | v) (occupancy mask), for each
-//               set bit of o = u | v in ascending order: t += L, and
-//               d += L when the bit is set in x = u ^ v.
-// Lanes run along stripes (same k, consecutive l), so the u side is shared by
-// the warp and shared-memory accesses stay conflict-free although lanes walk
-// different words.
+//   NB[w][c]  = 32 presence bits of rows 32w..32w+31 for sample column c,
+//               row 32w+r at bit (31-r) so FLO yields rows in ascending
+//               order; word-major, sample columns extended past n so the
+//               shifted operand k+s+1 never wraps inside a tile;
+//   per CTA   = TK samples x TS stripes; rows stream in chunks of 32 words
+//               (1024 rows): u words [k0, k0+TK), v words [k0+s0+1, ...),
+//               per-column occupancy masks of the chunk's nonzero words, and
+//               the rows' lengths (bit-reversed per word), staged in smem;
+//   per warp  = its RK x 32*RS slots form a queue; a lane takes the next slot
+//               (ballot + popc), walks the slot's nonzero words and their
+//               set bits in one flattened loop (t += L; d += L if the bit is
+//               also in u ^ v), then takes another slot. Accumulators live in
+//               shared memory, so any lane can continue any slot, and lanes
+//               never wait at word boundaries: the sparse walk stays SIMT-
+//               efficient although per-slot work is very uneven.
 #pragma once
 
 #include <cstdint>
@@ -29,8 +31,8 @@
 namespace sf {
 
 // Sample-packed rows (row r: word c holds samples 32c..32c+31) -> node-packed
-// columns NB[w][col] for col < n (rows >= E are zero). One warp per 32x32
-// bit block, transposed with ballots.
+// bit-reversed columns NB[w][col] for col < n (rows >= E are zero). One warp
+// per 32x32 bit block, transposed with ballots.
 __global__ void transpose_bits_kernel(const uint32_t* __restrict__ rows, int64_t row_words,
                                       int32_t E, int32_t n, uint32_t* __restrict__ nb,
                                       int64_t n_ext, int32_t W) {
@@ -48,7 +50,7 @@ __global__ void transpose_bits_kernel(const uint32_t* __restrict__ rows, int64_t
 #pragma unroll
     for (int b = 0; b < 32; ++b) {
       const uint32_t col = __ballot_sync(0xffffffffu, (mine >> b) & 1u);
-      if (b == lane) out = col;
+      if (b == lane) out = __brev(col);  // row 32w+i -> bit 31-i
     }
     const int64_t smp = c * 32 + lane;
     if (smp < n) nb[w * n_ext + smp] = out;
@@ -80,23 +82,39 @@ struct SparseArgs {
   unsigned long long* exec_updates;
 };
 
-template <class Real, int RK, int RS, int NWK, int NWS>
-__global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const SparseArgs a) {
-  constexpr int NT = 32 * NWK * NWS;
-  constexpr int TK = NWK * RK;          // samples per CTA
-  constexpr int TS = NWS * 32 * RS;     // stripes per CTA
-  constexpr int VW = TK + TS;           // v columns staged (one spare)
-  constexpr int WC = 32;                // words per chunk (1024 rows)
-  constexpr int USTR = TK + 1;          // padded: lanes on different words hit different banks
-  constexpr int LSTR = 33;
+template <int RK, int RS, int NWK, int NWS>
+struct SparseTile {
+  static constexpr int NW = NWK * NWS;
+  static constexpr int NT = 32 * NW;
+  static constexpr int TK = NWK * RK;       // samples per CTA
+  static constexpr int TS = NWS * 32 * RS;  // stripes per CTA
+  static constexpr int VW = TK + TS;        // v columns staged (one spare)
+  static constexpr int WC = 32;             // words per chunk (1024 rows)
+  static constexpr int USTR = TK + 1;       // padded: different words -> different banks
+  static constexpr int LSTR = 33;
+  static constexpr int NSLOT = RK * RS * 32;  // slots per warp
+  // dynamic shared memory layout (bytes)
+  static constexpr int OFF_L = 0;
+  static constexpr int OFF_ACC = OFF_L + WC * LSTR * 8;
+  static constexpr int OFF_U = OFF_ACC + NW * NSLOT * 16;
+  static constexpr int OFF_V = OFF_U + WC * USTR * 4;
+  static constexpr int OFF_OU = OFF_V + WC * VW * 4;
+  static constexpr int OFF_OV = OFF_OU + TK * 4;
+  static constexpr int BYTES = OFF_OV + VW * 4;
   static_assert(VW % 32 == 0, "v window must be a multiple of 32 columns (bank mapping)");
   static_assert(TK + VW <= NT, "one staging thread per column");
+};
 
-  __shared__ uint32_t sU[WC * USTR];
-  __shared__ uint32_t sV[WC * VW];
-  __shared__ uint32_t occU[TK];
-  __shared__ uint32_t occV[VW];
-  __shared__ double sL[WC * LSTR];
+template <class Real, int RK, int RS, int NWK, int NWS>
+__global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const SparseArgs a) {
+  using T = SparseTile<RK, RS, NWK, NWS>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  double* sL = reinterpret_cast<double*>(smem + T::OFF_L);
+  Real* sAcc = reinterpret_cast<Real*>(smem + T::OFF_ACC);  // [NW][NSLOT][2]
+  uint32_t* sU = reinterpret_cast<uint32_t*>(smem + T::OFF_U);
+  uint32_t* sV = reinterpret_cast<uint32_t*>(smem + T::OFF_V);
+  uint32_t* occU = reinterpret_cast<uint32_t*>(smem + T::OFF_OU);
+  uint32_t* occV = reinterpret_cast<uint32_t*>(smem + T::OFF_OV);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -104,105 +122,122 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
   const int wk = warp % NWK;
   const int ws = warp / NWK;
   const int n = a.n;
-  const int k0 = blockIdx.x * TK;
-  const int s0 = a.s_begin + blockIdx.y * TS;
+  const int k0 = blockIdx.x * T::TK;
+  const int s0 = a.s_begin + blockIdx.y * T::TS;
   const int64_t P0 = static_cast<int64_t>(k0) + s0 + 1;
-
+  const unsigned lt_mask = (1u << lane) - 1u;
+  Real* acc = sAcc + warp * T::NSLOT * 2;
   Real* dist = static_cast<Real*>(a.dist);
   Real* tot = static_cast<Real*>(a.tot);
 
-  Real D[RK][RS], T[RK][RS];
-#pragma unroll
-  for (int j = 0; j < RK; ++j)
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const int k = k0 + wk * RK + j;
-      const int s = s0 + ws * 32 * RS + lane + 32 * i;
-      const bool ok = k < n && s < a.s_end;
-      const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
-      D[j][i] = ok ? dist[off] : Real(0);
-      T[j][i] = ok ? tot[off] : Real(0);
-    }
+  // slot q of this warp: j = q / (32*RS) (sample), i = (q / 32) % RS, l = q % 32
+  auto slot_k = [&](int q) { return k0 + wk * RK + q / (32 * RS); };
+  auto slot_s = [&](int q) { return s0 + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS); };
+  // initial accumulators (RMW semantics: the stripes may hold earlier rows)
+  for (int q = lane; q < T::NSLOT; q += 32) {
+    const int k = slot_k(q), s = slot_s(q);
+    const bool ok = k < n && s < a.s_end;
+    const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
+    acc[2 * q] = ok ? dist[off] : Real(0);
+    acc[2 * q + 1] = ok ? tot[off] : Real(0);
+  }
   unsigned long long executed = 0;
 
-  for (int w0 = 0; w0 < a.W; w0 += WC) {
-    const int wc = min(WC, a.W - w0);
+  for (int w0 = 0; w0 < a.W; w0 += T::WC) {
+    const int wc = min(T::WC, a.W - w0);
     __syncthreads();
-    // ---- stage: one thread per column for the words + occupancy mask,
-    //      the rest load lengths
-    if (tid < TK + VW) {
-      const bool is_u = tid < TK;
-      const int col = is_u ? tid : tid - TK;
+    // ---- stage: one thread per column for its words + occupancy mask;
+    //      the remaining threads stage the lengths, bit-reversed per word
+    if (tid < T::TK + T::VW) {
+      const bool is_u = tid < T::TK;
+      const int col = is_u ? tid : tid - T::TK;
       const int64_t gcol = is_u ? static_cast<int64_t>(k0) + col : P0 + col;
       const uint32_t* src = a.nb + static_cast<int64_t>(w0) * a.n_ext + gcol;
       uint32_t occ = 0u;
-      for (int w = 0; w < WC; ++w) {
+#pragma unroll 8
+      for (int w = 0; w < T::WC; ++w) {
         const uint32_t v = w < wc ? __ldg(src + static_cast<int64_t>(w) * a.n_ext) : 0u;
         occ |= (v != 0u ? 1u : 0u) << w;
         if (is_u)
-          sU[w * USTR + col] = v;
+          sU[w * T::USTR + col] = v;
         else
-          sV[w * VW + col] = v;
+          sV[w * T::VW + col] = v;
       }
       if (is_u)
         occU[col] = occ;
       else
         occV[col] = occ;
     } else {
-      for (int e = tid - (TK + VW); e < WC * 32; e += NT - (TK + VW)) {
-        const int w = e >> 5, j = e & 31;
-        sL[w * LSTR + j] = w < wc ? a.lens[static_cast<int64_t>(w0 + w) * 32 + j] : 0.0;
+      for (int e = tid - (T::TK + T::VW); e < T::WC * 32; e += T::NT - (T::TK + T::VW)) {
+        const int w = e >> 5, r = e & 31;
+        sL[w * T::LSTR + (31 - r)] = w < wc ? a.lens[static_cast<int64_t>(w0 + w) * 32 + r] : 0.0;
       }
     }
     __syncthreads();
-    // ---- walk the present rows of every slot, in postorder
-#pragma unroll
-    for (int j = 0; j < RK; ++j) {
-      const int cu = wk * RK + j;
-      const uint32_t ou = occU[cu];
-#pragma unroll
-      for (int i = 0; i < RS; ++i) {
-        const int cv = cu + ws * 32 * RS + lane + 32 * i;
-        uint32_t occ = ou | occV[cv];
-        Real d = D[j][i], t = T[j][i];
-        while (occ) {
-          const int w = __ffs(occ) - 1;
-          occ &= occ - 1u;
-          const uint32_t u = sU[w * USTR + cu];
-          const uint32_t v = sV[w * VW + cv];
-          uint32_t o = u | v;
-          const uint32_t x = u ^ v;
-          const double* Lw = sL + w * LSTR;
-          executed += __popc(o);
-          do {
-            const uint32_t b = o & (0u - o);
-            o ^= b;
-            const Real L = static_cast<Real>(Lw[31 - __clz(b)]);
-            t += L;
-            if (x & b) d += L;
-          } while (o);
+
+    // ---- warp work queue over the warp's slots
+    int next = 0;  // warp-uniform
+    int q = -1;
+    bool loaded = false;
+    uint32_t occ = 0u, o = 0u, x = 0u;
+    int cu = 0, cv = 0;
+    const double* Lw = sL;
+    Real d = Real(0), t = Real(0);
+    for (;;) {
+      const bool idle = (o == 0u) && (occ == 0u);
+      if (idle && loaded) {
+        acc[2 * q] = d;
+        acc[2 * q + 1] = t;
+        loaded = false;
+      }
+      const unsigned req = __ballot_sync(0xffffffffu, idle);
+      if (idle) {
+        q = next + __popc(req & lt_mask);
+        if (q < T::NSLOT) {
+          const int j = q / (32 * RS);
+          cu = wk * RK + j;
+          cv = cu + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS);
+          const bool ok = slot_k(q) < n && slot_s(q) < a.s_end;
+          occ = ok ? (occU[cu] | occV[cv]) : 0u;
+          if (occ) {
+            d = acc[2 * q];
+            t = acc[2 * q + 1];
+            loaded = true;
+          }
         }
-        D[j][i] = d;
-        T[j][i] = t;
+      }
+      next += __popc(req);
+      if (!__any_sync(0xffffffffu, o != 0u || occ != 0u) && next >= T::NSLOT) break;
+      if (o == 0u && occ != 0u) {  // next nonzero word of this slot
+        const int w = __ffs(occ) - 1;
+        occ &= occ - 1u;
+        const uint32_t u = sU[w * T::USTR + cu];
+        const uint32_t v = sV[w * T::VW + cv];
+        o = u | v;
+        x = u ^ v;
+        Lw = sL + w * T::LSTR;
+        executed += __popc(o);
+      }
+      if (o != 0u) {  // lowest present row of the word (bit 31 - r)
+        const int c = 31 - __clz(o);
+        const uint32_t m = 1u << c;
+        o ^= m;
+        const Real L = static_cast<Real>(Lw[c]);
+        t += L;
+        if (x & m) d += L;
       }
     }
   }
-
-#pragma unroll
-  for (int j = 0; j < RK; ++j)
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const int k = k0 + wk * RK + j;
-      const int s = s0 + ws * 32 * RS + lane + 32 * i;
-      if (k < n && s < a.s_end) {
-        const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
-        dist[off] = D[j][i];
-        tot[off] = T[j][i];
-      }
+  __syncwarp();
+  for (int q = lane; q < T::NSLOT; q += 32) {
+    const int k = slot_k(q), s = slot_s(q);
+    if (k < n && s < a.s_end) {
+      const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
+      dist[off] = acc[2 * q];
+      tot[off] = acc[2 * q + 1];
     }
+  }
   if (a.exec_updates) {
-    // count only valid slots' work would need per-slot masks; tails are
-    // small, so the CTA's executed (row, slot) visits are reported as is
     for (int off = 16; off > 0; off >>= 1) executed += __shfl_down_sync(0xffffffffu, executed, off);
     if (lane == 0) atomicAdd(a.exec_updates, executed);
   }
