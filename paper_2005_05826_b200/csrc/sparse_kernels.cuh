@@ -17,13 +17,15 @@
 //               (1024 rows): u words [k0, k0+TK), v words [k0+s0+1, ...),
 //               per-column occupancy masks of the chunk's nonzero words, and
 //               the rows' lengths (bit-reversed per word), staged in smem;
-//   per warp  = its RK x 32*RS slots form a queue; a lane takes the next slot
-//               (ballot + popc), walks the slot's nonzero words and their
-//               set bits in one flattened loop (t += L; d += L if the bit is
-//               also in u ^ v), then takes another slot. Accumulators live in
-//               shared memory, so any lane can continue any slot, and lanes
-//               never wait at word boundaries: the sparse walk stays SIMT-
-//               efficient although per-slot work is very uneven.
+//   per warp  = its RK x 32*RS slots form a queue; a lane walks its slot's
+//               nonzero words (occupancy mask) and their set bits in one
+//               flattened loop, one present row per trip (t += L; d += L if
+//               the bit is also in u ^ v), and when the slot is exhausted it
+//               claims the next one from a shared-memory counter (atomicAdd,
+//               no warp-wide vote). Accumulators live in shared memory, so
+//               any lane can continue any slot and lanes never wait at word
+//               or slot boundaries: the walk stays SIMT-efficient although
+//               per-slot work is very uneven.
 #pragma once
 
 #include <cstdint>
@@ -100,7 +102,8 @@ struct SparseTile {
   static constexpr int OFF_V = OFF_U + WC * USTR * 4;
   static constexpr int OFF_OU = OFF_V + WC * VW * 4;
   static constexpr int OFF_OV = OFF_OU + TK * 4;
-  static constexpr int BYTES = OFF_OV + VW * 4;
+  static constexpr int OFF_CTR = OFF_OV + VW * 4;
+  static constexpr int BYTES = OFF_CTR + NW * 4;
   static_assert(VW % 32 == 0, "v window must be a multiple of 32 columns (bank mapping)");
   static_assert(TK + VW <= NT, "one staging thread per column");
 };
@@ -115,6 +118,7 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
   uint32_t* sV = reinterpret_cast<uint32_t*>(smem + T::OFF_V);
   uint32_t* occU = reinterpret_cast<uint32_t*>(smem + T::OFF_OU);
   uint32_t* occV = reinterpret_cast<uint32_t*>(smem + T::OFF_OV);
+  int* sCtr = reinterpret_cast<int*>(smem + T::OFF_CTR);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -125,7 +129,6 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
   const int k0 = blockIdx.x * T::TK;
   const int s0 = a.s_begin + blockIdx.y * T::TS;
   const int64_t P0 = static_cast<int64_t>(k0) + s0 + 1;
-  const unsigned lt_mask = (1u << lane) - 1u;
   Real* acc = sAcc + warp * T::NSLOT * 2;
   Real* dist = static_cast<Real*>(a.dist);
   Real* tot = static_cast<Real*>(a.tot);
@@ -175,40 +178,48 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
     }
     __syncthreads();
 
-    // ---- warp work queue over the warp's slots
-    int next = 0;  // warp-uniform
-    int q = -1;
+    // ---- per-warp work queue over the warp's slots: lane l starts with slot
+    //      l, then pulls the next unclaimed slot from a shared counter each
+    //      time its slot has no rows left in this chunk; one present row per
+    //      loop trip, no warp-wide votes
+    if (lane == 0) sCtr[warp] = 32;
+    __syncwarp();
+    int q = lane;
     bool loaded = false;
     uint32_t occ = 0u, o = 0u, x = 0u;
     int cu = 0, cv = 0;
     const double* Lw = sL;
     Real d = Real(0), t = Real(0);
-    for (;;) {
-      const bool idle = (o == 0u) && (occ == 0u);
-      if (idle && loaded) {
-        acc[2 * q] = d;
-        acc[2 * q + 1] = t;
-        loaded = false;
+    {
+      cu = wk * RK + q / (32 * RS);
+      cv = cu + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS);
+      occ = (slot_k(q) < n && slot_s(q) < a.s_end) ? (occU[cu] | occV[cv]) : 0u;
+      if (occ) {
+        d = acc[2 * q];
+        t = acc[2 * q + 1];
+        loaded = true;
       }
-      const unsigned req = __ballot_sync(0xffffffffu, idle);
-      if (idle) {
-        q = next + __popc(req & lt_mask);
-        if (q < T::NSLOT) {
-          const int j = q / (32 * RS);
-          cu = wk * RK + j;
+    }
+    for (;;) {
+      if (o == 0u) {
+        while (occ == 0u) {  // slot exhausted for this chunk: take another
+          if (loaded) {
+            acc[2 * q] = d;
+            acc[2 * q + 1] = t;
+            loaded = false;
+          }
+          q = atomicAdd(&sCtr[warp], 1);
+          if (q >= T::NSLOT) goto chunk_done;
+          cu = wk * RK + q / (32 * RS);
           cv = cu + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS);
-          const bool ok = slot_k(q) < n && slot_s(q) < a.s_end;
-          occ = ok ? (occU[cu] | occV[cv]) : 0u;
+          occ = (slot_k(q) < n && slot_s(q) < a.s_end) ? (occU[cu] | occV[cv]) : 0u;
           if (occ) {
             d = acc[2 * q];
             t = acc[2 * q + 1];
             loaded = true;
           }
         }
-      }
-      next += __popc(req);
-      if (!__any_sync(0xffffffffu, o != 0u || occ != 0u) && next >= T::NSLOT) break;
-      if (o == 0u && occ != 0u) {  // next nonzero word of this slot
+        // next nonzero word of this slot
         const int w = __ffs(occ) - 1;
         occ &= occ - 1u;
         const uint32_t u = sU[w * T::USTR + cu];
@@ -218,15 +229,15 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
         Lw = sL + w * T::LSTR;
         executed += __popc(o);
       }
-      if (o != 0u) {  // lowest present row of the word (bit 31 - r)
-        const int c = 31 - __clz(o);
-        const uint32_t m = 1u << c;
-        o ^= m;
-        const Real L = static_cast<Real>(Lw[c]);
-        t += L;
-        if (x & m) d += L;
-      }
+      // lowest present row of the word (row 32w+r sits at bit 31-r)
+      const int c = 31 - __clz(o);
+      const uint32_t m = 1u << c;
+      o ^= m;
+      const Real L = static_cast<Real>(Lw[c]);
+      t += L;
+      if (x & m) d += L;
     }
+  chunk_done:;
   }
   __syncwarp();
   for (int q = lane; q < T::NSLOT; q += 32) {
