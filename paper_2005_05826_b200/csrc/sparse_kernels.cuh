@@ -200,44 +200,50 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
         loaded = true;
       }
     }
-    for (;;) {
+    bool more = true;
+    while (more) {
       if (o == 0u) {
-        while (occ == 0u) {  // slot exhausted for this chunk: take another
+        while (occ == 0u && q < T::NSLOT) {  // slot exhausted for this chunk: take another
           if (loaded) {
             acc[2 * q] = d;
             acc[2 * q + 1] = t;
             loaded = false;
           }
           q = atomicAdd(&sCtr[warp], 1);
-          if (q >= T::NSLOT) goto chunk_done;
-          cu = wk * RK + q / (32 * RS);
-          cv = cu + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS);
-          occ = (slot_k(q) < n && slot_s(q) < a.s_end) ? (occU[cu] | occV[cv]) : 0u;
-          if (occ) {
-            d = acc[2 * q];
-            t = acc[2 * q + 1];
-            loaded = true;
+          if (q < T::NSLOT) {
+            cu = wk * RK + q / (32 * RS);
+            cv = cu + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS);
+            occ = (slot_k(q) < n && slot_s(q) < a.s_end) ? (occU[cu] | occV[cv]) : 0u;
+            if (occ) {
+              d = acc[2 * q];
+              t = acc[2 * q + 1];
+              loaded = true;
+            }
           }
         }
-        // next nonzero word of this slot
-        const int w = __ffs(occ) - 1;
-        occ &= occ - 1u;
-        const uint32_t u = sU[w * T::USTR + cu];
-        const uint32_t v = sV[w * T::VW + cv];
-        o = u | v;
-        x = u ^ v;
-        Lw = sL + w * T::LSTR;
-        executed += __popc(o);
+        if (occ != 0u) {  // next nonzero word of this slot
+          const int w = __ffs(occ) - 1;
+          occ &= occ - 1u;
+          const uint32_t u = sU[w * T::USTR + cu];
+          const uint32_t v = sV[w * T::VW + cv];
+          o = u | v;
+          x = u ^ v;
+          Lw = sL + w * T::LSTR;
+          executed += __popc(o);
+        } else {
+          more = false;  // queue drained
+        }
       }
-      // lowest present row of the word (row 32w+r sits at bit 31-r)
-      const int c = 31 - __clz(o);
-      const uint32_t m = 1u << c;
-      o ^= m;
-      const Real L = static_cast<Real>(Lw[c]);
-      t += L;
-      if (x & m) d += L;
+      if (o != 0u) {
+        // lowest present row of the word (row 32w+r sits at bit 31-r)
+        const int c = 31 - __clz(o);
+        const uint32_t m = 1u << c;
+        o ^= m;
+        const Real L = static_cast<Real>(Lw[c]);
+        t += L;
+        if (x & m) d += L;
+      }
     }
-  chunk_done:;
   }
   __syncwarp();
   for (int q = lane; q < T::NSLOT; q += 32) {
