@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
 #pragma unroll 8
       for (int w = 0; w < T::WC; ++w) {
         const uint32_t v = w < wc ? __ldg(src + static_cast<int64_t>(w) * a.n_ext) : 0u;
-        occ |= (v != 0u ? 1u : 0u) << w;
+        occ |= (v != 0u ? 0x80000000u : 0u) >> w;  // word w at bit 31-w
         if (is_u)
           sU[w * T::USTR + col] = v;
         else
@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
     } else {
       for (int e = tid - (T::TK + T::VW); e < T::WC * 32; e += T::NT - (T::TK + T::VW)) {
         const int w = e >> 5, r = e & 31;
-        sL[w * T::LSTR + (31 - r)] = w < wc ? a.lens[static_cast<int64_t>(w0 + w) * 32 + r] : 0.0;
+        sL[w * T::LSTR + r] = w < wc ? a.lens[static_cast<int64_t>(w0 + w) * 32 + r] : 0.0;
       }
     }
     __syncthreads();
@@ -203,13 +203,20 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
     bool more = true;
     while (more) {
       if (o == 0u) {
-        while (occ == 0u && q < T::NSLOT) {  // slot exhausted for this chunk: take another
+        if (occ == 0u) {
+          // slot exhausted for this chunk: store it, claim the next slot
+          // (one shared atomic per group of claiming lanes)
           if (loaded) {
             acc[2 * q] = d;
             acc[2 * q + 1] = t;
             loaded = false;
           }
-          q = atomicAdd(&sCtr[warp], 1);
+          const unsigned grp = __activemask();
+          const int leader = __ffs(grp) - 1;
+          int base = 0;
+          if (lane == leader) base = atomicAdd(&sCtr[warp], __popc(grp));
+          base = __shfl_sync(grp, base, leader);
+          q = base + __popc(grp & ((1u << lane) - 1u));
           if (q < T::NSLOT) {
             cu = wk * RK + q / (32 * RS);
             cv = cu + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS);
@@ -219,27 +226,27 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
               t = acc[2 * q + 1];
               loaded = true;
             }
+          } else {
+            more = false;  // queue drained
           }
         }
-        if (occ != 0u) {  // next nonzero word of this slot
-          const int w = __ffs(occ) - 1;
-          occ &= occ - 1u;
+        if (occ != 0u) {  // next nonzero word of this slot (word w at bit 31-w)
+          const int w = __clz(occ);
+          occ ^= 0x80000000u >> w;
           const uint32_t u = sU[w * T::USTR + cu];
           const uint32_t v = sV[w * T::VW + cv];
           o = u | v;
           x = u ^ v;
           Lw = sL + w * T::LSTR;
           executed += __popc(o);
-        } else {
-          more = false;  // queue drained
         }
       }
       if (o != 0u) {
-        // lowest present row of the word (row 32w+r sits at bit 31-r)
-        const int c = 31 - __clz(o);
-        const uint32_t m = 1u << c;
+        // lowest present row of the word: row 32w+r sits at bit 31-r
+        const int r = __clz(o);
+        const uint32_t m = 0x80000000u >> r;
         o ^= m;
-        const Real L = static_cast<Real>(Lw[c]);
+        const Real L = static_cast<Real>(Lw[r]);
         t += L;
         if (x & m) d += L;
       }
