@@ -16,16 +16,15 @@
 //   per CTA   = TK samples x TS stripes; rows stream in chunks of 32 words
 //               (1024 rows): u words [k0, k0+TK), v words [k0+s0+1, ...),
 //               per-column occupancy masks of the chunk's nonzero words, and
-//               the rows' lengths (bit-reversed per word), staged in smem;
-//   per warp  = its RK x 32*RS slots form a queue; a lane walks its slot's
-//               nonzero words (occupancy mask) and their set bits in one
-//               flattened loop, one present row per trip (t += L; d += L if
-//               the bit is also in u ^ v), and when the slot is exhausted it
-//               claims the next one from a shared-memory counter (atomicAdd,
-//               no warp-wide vote). Accumulators live in shared memory, so
-//               any lane can continue any slot and lanes never wait at word
-//               or slot boundaries: the walk stays SIMT-efficient although
-//               per-slot work is very uneven.
+//               the rows' lengths, staged in shared memory;
+//   per lane  = RK x RS slots (lanes run along stripes, so the u side is
+//               shared by the warp), accumulators in registers; for each slot
+//               the lane walks the nonzero words of u|v (occupancy mask) and
+//               their set bits in ascending row order: t += L for every bit of
+//               u|v, d += L when the bit is also in u^v.
+// (A per-warp work queue with shared-memory accumulators was tried to even
+//  out the very uneven per-slot work; its divergent claim path cost more than
+//  the divergence it removed — see profiles/.)
 #pragma once
 
 #include <cstdint>
@@ -94,16 +93,13 @@ struct SparseTile {
   static constexpr int WC = 32;             // words per chunk (1024 rows)
   static constexpr int USTR = TK + 1;       // padded: different words -> different banks
   static constexpr int LSTR = 33;
-  static constexpr int NSLOT = RK * RS * 32;  // slots per warp
   // dynamic shared memory layout (bytes)
   static constexpr int OFF_L = 0;
-  static constexpr int OFF_ACC = OFF_L + WC * LSTR * 8;
-  static constexpr int OFF_U = OFF_ACC + NW * NSLOT * 16;
+  static constexpr int OFF_U = OFF_L + WC * LSTR * 8;
   static constexpr int OFF_V = OFF_U + WC * USTR * 4;
   static constexpr int OFF_OU = OFF_V + WC * VW * 4;
   static constexpr int OFF_OV = OFF_OU + TK * 4;
-  static constexpr int OFF_CTR = OFF_OV + VW * 4;
-  static constexpr int BYTES = OFF_CTR + NW * 4;
+  static constexpr int BYTES = OFF_OV + VW * 4;
   static_assert(VW % 32 == 0, "v window must be a multiple of 32 columns (bank mapping)");
   static_assert(TK + VW <= NT, "one staging thread per column");
 };
@@ -112,13 +108,11 @@ template <class Real, int RK, int RS, int NWK, int NWS>
 __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const SparseArgs a) {
   using T = SparseTile<RK, RS, NWK, NWS>;
   extern __shared__ __align__(16) unsigned char smem[];
-  double* sL = reinterpret_cast<double*>(smem + T::OFF_L);
-  Real* sAcc = reinterpret_cast<Real*>(smem + T::OFF_ACC);  // [NW][NSLOT][2]
+  const double* sL = reinterpret_cast<const double*>(smem + T::OFF_L);
   uint32_t* sU = reinterpret_cast<uint32_t*>(smem + T::OFF_U);
   uint32_t* sV = reinterpret_cast<uint32_t*>(smem + T::OFF_V);
   uint32_t* occU = reinterpret_cast<uint32_t*>(smem + T::OFF_OU);
   uint32_t* occV = reinterpret_cast<uint32_t*>(smem + T::OFF_OV);
-  int* sCtr = reinterpret_cast<int*>(smem + T::OFF_CTR);
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -129,28 +123,31 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
   const int k0 = blockIdx.x * T::TK;
   const int s0 = a.s_begin + blockIdx.y * T::TS;
   const int64_t P0 = static_cast<int64_t>(k0) + s0 + 1;
-  Real* acc = sAcc + warp * T::NSLOT * 2;
   Real* dist = static_cast<Real*>(a.dist);
   Real* tot = static_cast<Real*>(a.tot);
 
-  // slot q of this warp: j = q / (32*RS) (sample), i = (q / 32) % RS, l = q % 32
-  auto slot_k = [&](int q) { return k0 + wk * RK + q / (32 * RS); };
-  auto slot_s = [&](int q) { return s0 + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS); };
-  // initial accumulators (RMW semantics: the stripes may hold earlier rows)
-  for (int q = lane; q < T::NSLOT; q += 32) {
-    const int k = slot_k(q), s = slot_s(q);
-    const bool ok = k < n && s < a.s_end;
-    const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
-    acc[2 * q] = ok ? dist[off] : Real(0);
-    acc[2 * q + 1] = ok ? tot[off] : Real(0);
-  }
+  // slot (j, i): sample k0 + wk*RK + j, stripe s0 + ws*32*RS + lane + 32*i
+  Real D[RK][RS], Tt[RK][RS];
+  uint32_t valid = 0u;
+#pragma unroll
+  for (int j = 0; j < RK; ++j)
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const int k = k0 + wk * RK + j;
+      const int s = s0 + ws * 32 * RS + lane + 32 * i;
+      const bool ok = k < n && s < a.s_end;
+      const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
+      D[j][i] = ok ? dist[off] : Real(0);
+      Tt[j][i] = ok ? tot[off] : Real(0);
+      valid |= (ok ? 1u : 0u) << (j * RS + i);
+    }
   unsigned long long executed = 0;
 
   for (int w0 = 0; w0 < a.W; w0 += T::WC) {
     const int wc = min(T::WC, a.W - w0);
     __syncthreads();
-    // ---- stage: one thread per column for its words + occupancy mask;
-    //      the remaining threads stage the lengths, bit-reversed per word
+    // ---- stage: one thread per column for its words + occupancy mask
+    //      (word w at bit 31-w); the remaining threads stage the lengths
     if (tid < T::TK + T::VW) {
       const bool is_u = tid < T::TK;
       const int col = is_u ? tid : tid - T::TK;
@@ -160,7 +157,7 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
 #pragma unroll 8
       for (int w = 0; w < T::WC; ++w) {
         const uint32_t v = w < wc ? __ldg(src + static_cast<int64_t>(w) * a.n_ext) : 0u;
-        occ |= (v != 0u ? 0x80000000u : 0u) >> w;  // word w at bit 31-w
+        occ |= (v != 0u ? 0x80000000u : 0u) >> w;
         if (is_u)
           sU[w * T::USTR + col] = v;
         else
@@ -171,96 +168,62 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
       else
         occV[col] = occ;
     } else {
+      double* sLw = reinterpret_cast<double*>(smem + T::OFF_L);
       for (int e = tid - (T::TK + T::VW); e < T::WC * 32; e += T::NT - (T::TK + T::VW)) {
         const int w = e >> 5, r = e & 31;
-        sL[w * T::LSTR + r] = w < wc ? a.lens[static_cast<int64_t>(w0 + w) * 32 + r] : 0.0;
+        sLw[w * T::LSTR + r] = w < wc ? a.lens[static_cast<int64_t>(w0 + w) * 32 + r] : 0.0;
       }
     }
     __syncthreads();
 
-    // ---- per-warp work queue over the warp's slots: lane l starts with slot
-    //      l, then pulls the next unclaimed slot from a shared counter each
-    //      time its slot has no rows left in this chunk; one present row per
-    //      loop trip, no warp-wide votes
-    if (lane == 0) sCtr[warp] = 32;
-    __syncwarp();
-    int q = lane;
-    bool loaded = false;
-    uint32_t occ = 0u, o = 0u, x = 0u;
-    int cu = 0, cv = 0;
-    const double* Lw = sL;
-    Real d = Real(0), t = Real(0);
-    {
-      cu = wk * RK + q / (32 * RS);
-      cv = cu + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS);
-      occ = (slot_k(q) < n && slot_s(q) < a.s_end) ? (occU[cu] | occV[cv]) : 0u;
-      if (occ) {
-        d = acc[2 * q];
-        t = acc[2 * q + 1];
-        loaded = true;
-      }
-    }
-    bool more = true;
-    while (more) {
-      if (o == 0u) {
-        if (occ == 0u) {
-          // slot exhausted for this chunk: store it, claim the next slot
-          // (one shared atomic per group of claiming lanes)
-          if (loaded) {
-            acc[2 * q] = d;
-            acc[2 * q + 1] = t;
-            loaded = false;
-          }
-          const unsigned grp = __activemask();
-          const int leader = __ffs(grp) - 1;
-          int base = 0;
-          if (lane == leader) base = atomicAdd(&sCtr[warp], __popc(grp));
-          base = __shfl_sync(grp, base, leader);
-          q = base + __popc(grp & ((1u << lane) - 1u));
-          if (q < T::NSLOT) {
-            cu = wk * RK + q / (32 * RS);
-            cv = cu + ws * 32 * RS + (q & 31) + 32 * ((q >> 5) % RS);
-            occ = (slot_k(q) < n && slot_s(q) < a.s_end) ? (occU[cu] | occV[cv]) : 0u;
-            if (occ) {
-              d = acc[2 * q];
-              t = acc[2 * q + 1];
-              loaded = true;
-            }
-          } else {
-            more = false;  // queue drained
-          }
-        }
-        if (occ != 0u) {  // next nonzero word of this slot (word w at bit 31-w)
-          const int w = __clz(occ);
+    // ---- walk the present rows of every slot, in postorder
+#pragma unroll
+    for (int j = 0; j < RK; ++j) {
+      const int cu = wk * RK + j;
+      const uint32_t ou = occU[cu];
+      const uint32_t* pu = sU + cu;
+#pragma unroll
+      for (int i = 0; i < RS; ++i) {
+        if (!(valid & (1u << (j * RS + i)))) continue;
+        const int cv = cu + ws * 32 * RS + lane + 32 * i;
+        const uint32_t* pv = sV + cv;
+        uint32_t occ = ou | occV[cv];
+        Real d = D[j][i], t = Tt[j][i];
+        while (occ) {
+          const int w = __clz(occ);  // next nonzero word (word w at bit 31-w)
           occ ^= 0x80000000u >> w;
-          const uint32_t u = sU[w * T::USTR + cu];
-          const uint32_t v = sV[w * T::VW + cv];
-          o = u | v;
-          x = u ^ v;
-          Lw = sL + w * T::LSTR;
+          const uint32_t u = pu[w * T::USTR];
+          const uint32_t v = pv[w * T::VW];
+          uint32_t o = u | v;
+          const uint32_t x = u ^ v;
+          const double* Lw = sL + w * T::LSTR;
           executed += __popc(o);
+          do {  // present rows in ascending order: row 32w+r sits at bit 31-r
+            const int r = __clz(o);
+            const uint32_t m = 0x80000000u >> r;
+            o ^= m;
+            const Real L = static_cast<Real>(Lw[r]);
+            t += L;
+            if (x & m) d += L;
+          } while (o);
         }
-      }
-      if (o != 0u) {
-        // lowest present row of the word: row 32w+r sits at bit 31-r
-        const int r = __clz(o);
-        const uint32_t m = 0x80000000u >> r;
-        o ^= m;
-        const Real L = static_cast<Real>(Lw[r]);
-        t += L;
-        if (x & m) d += L;
+        D[j][i] = d;
+        Tt[j][i] = t;
       }
     }
   }
-  __syncwarp();
-  for (int q = lane; q < T::NSLOT; q += 32) {
-    const int k = slot_k(q), s = slot_s(q);
-    if (k < n && s < a.s_end) {
+
+#pragma unroll
+  for (int j = 0; j < RK; ++j)
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      if (!(valid & (1u << (j * RS + i)))) continue;
+      const int k = k0 + wk * RK + j;
+      const int s = s0 + ws * 32 * RS + lane + 32 * i;
       const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
-      dist[off] = acc[2 * q];
-      tot[off] = acc[2 * q + 1];
+      dist[off] = D[j][i];
+      tot[off] = Tt[j][i];
     }
-  }
   if (a.exec_updates) {
     for (int off = 16; off > 0; off >>= 1) executed += __shfl_down_sync(0xffffffffu, executed, off);
     if (lane == 0) atomicAdd(a.exec_updates, executed);
