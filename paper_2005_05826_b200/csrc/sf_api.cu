@@ -418,6 +418,18 @@ sf_status sparse_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
   return SF_OK;
 }
 
+template <class Real, int WCH>
+sf_status launch_sparse_flat(const SparseArgs& a, cudaStream_t st) {
+  using C = SparseCfg;
+  using T = FlatTile<C::RK, C::RS, C::NWK, C::NWS, WCH>;
+  auto* kern = stripe_sparse_flat_kernel<Real, C::RK, C::RS, C::NWK, C::NWS, WCH>;
+  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES));
+  const dim3 grid((a.n + C::TK - 1) / C::TK, (a.s_end - a.s_begin + C::TS - 1) / C::TS);
+  kern<<<grid, T::NT, T::BYTES, st>>>(a);
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
 template <class Real>
 sf_status launch_sparse(const SparseArgs& a, cudaStream_t st) {
   using C = SparseCfg;
@@ -509,7 +521,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
       SF_CUDA(cudaGetLastError());
       plan->stats.launches++;
     }
-    if (plan->kernel == 2) {
+    if (plan->kernel >= 2) {
       // node-packed presence bits for the sparse walk
       const int64_t W = (plan->E + 31) / 32;
       const int64_t n_ext = sparse_n_ext(n);
@@ -523,7 +535,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
     }
     SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
     // ---- K2: stripe update over the chunk's rows
-    if (plan->kernel == 2) {
+    if (plan->kernel >= 2) {
       SparseArgs a;
       a.nb = d.nodebits.as<uint32_t>();
       a.n_ext = sparse_n_ext(n);
@@ -535,7 +547,16 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
       a.dist = d.dist.p;
       a.tot = d.tot.p;
       a.exec_updates = d.exec_ctr.as<unsigned long long>();
-      SF_TRY(plan->prec == SF_FP64 ? launch_sparse<double>(a, st) : launch_sparse<float>(a, st));
+      sf_status kst;
+      if (plan->kernel == 3)
+        kst = plan->prec == SF_FP64 ? launch_sparse_flat<double, 32>(a, st)
+                                    : launch_sparse_flat<float, 32>(a, st);
+      else if (plan->kernel == 4)
+        kst = plan->prec == SF_FP64 ? launch_sparse_flat<double, 64>(a, st)
+                                    : launch_sparse_flat<float, 64>(a, st);
+      else
+        kst = plan->prec == SF_FP64 ? launch_sparse<double>(a, st) : launch_sparse<float>(a, st);
+      SF_TRY(kst);
     } else {
       StripeArgs a;
       a.emb = d.emb.p;
@@ -625,10 +646,10 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stop = stop;
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
-  plan->kernel = (ex && ex->kernel == 2) ? 2 : 1;
+  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 4) ? ex->kernel : 1;
   // auto: the sparse walk for the unweighted metric (exact, same bits)
   if ((!ex || ex->kernel == 0) && metric == SF_UNWEIGHTED) plan->kernel = 2;
-  if (plan->kernel == 2 && metric != SF_UNWEIGHTED)
+  if (plan->kernel >= 2 && metric != SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the sparse bit kernel implements the unweighted metric only");
   const int n = p->n_samples;
   plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;
@@ -662,13 +683,13 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   }
   if (ex && ex->mem_budget_bytes > 0) budget = std::min(budget, static_cast<size_t>(ex->mem_budget_bytes));
   int64_t cmax = static_cast<int64_t>(budget / std::max<size_t>(row_bytes, 1));
-  if (plan->kernel == 2) cmax = plan->E;  // the sparse path keeps all rows
+  if (plan->kernel >= 2) cmax = plan->E;  // the sparse path keeps all rows
   cmax = std::min<int64_t>(cmax, plan->E);
   if (cmax < 1) return fail(SF_ENOMEM, "not enough device memory for one embedding row");
   for (;;) {
     plan->sched = build_schedule(p, static_cast<int32_t>(cmax));
     const size_t need = (static_cast<size_t>(cmax) + static_cast<size_t>(plan->sched.n_pending)) * row_bytes;
-    if (need <= budget || cmax == 1 || plan->kernel == 2) break;
+    if (need <= budget || cmax == 1 || plan->kernel >= 2) break;
     cmax = std::max<int64_t>(1, cmax * 3 / 4);
   }
   plan->stats.n_chunks = plan->sched.chunks.size();
@@ -688,7 +709,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     SF_TRY(d.dist.alloc(d.dev, slots * w, "distances"));
     if (has_t) SF_TRY(d.tot.alloc(d.dev, slots * w, "totals"));
     SF_TRY(d.exec_ctr.alloc(d.dev, sizeof(unsigned long long), "counter"));
-    if (plan->kernel == 2) {
+    if (plan->kernel >= 2) {
       SF_TRY(upload_schedule(d, plan->sched));
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(plan->E) * row_bytes, "embedding rows"));
       SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));

@@ -21,7 +21,7 @@ from paper_2005_05826_b200 import stripefrac as sf
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE]
+KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4]  # 3/4: flattened sparse walk, 32/64-word chunks
 
 
 def _gpu_stripes(problem, metric, prec, start, stop, kernel=N.KERNEL_DENSE, exact=False,
@@ -66,7 +66,7 @@ def test_golden_stripes(device_ok, case, kernel):
     n = table.n_samples()
     for r in case["results"]:
         metric = int(sf.metric_from_name(r["metric"]))
-        if kernel == N.KERNEL_SPARSE and metric != 1:
+        if kernel >= N.KERNEL_SPARSE and metric != 1:
             continue
         prec = 8 if r["precision"] == "fp64" else 4
         gd, gt = gu.stripes(r, n)
@@ -273,11 +273,12 @@ def test_sparse_kernel_matches_dense_bitwise(device_ok, prec):
         S = n // 2
         for start, stop in [(0, S), (S // 2, S)]:
             d1, t1, _ = _gpu_stripes(problem, 1, prec, start, stop, kernel=N.KERNEL_DENSE)
-            d2, t2, st = _gpu_stripes(problem, 1, prec, start, stop, kernel=N.KERNEL_SPARSE)
-            assert np.array_equal(d1, d2) and np.array_equal(t1, t2)
             wd, wt = op.compute_stripes(problem, 1, prec, start, stop)
-            assert np.array_equal(d2, wd) and np.array_equal(t2, wt)
-            assert 0 < st.updates_exec <= st.updates_alg
+            for kern in (N.KERNEL_SPARSE, 3, 4):
+                d2, t2, st = _gpu_stripes(problem, 1, prec, start, stop, kernel=kern)
+                assert np.array_equal(d1, d2) and np.array_equal(t1, t2)
+                assert np.array_equal(d2, wd) and np.array_equal(t2, wt)
+                assert 0 < st.updates_exec <= st.updates_alg
 
 
 def test_sparse_is_the_default_for_unweighted(device_ok):
