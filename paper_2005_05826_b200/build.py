@@ -83,10 +83,19 @@ def build_oracle(force: bool = False, verbose: bool = False) -> None:
                        stdout=None if verbose else subprocess.DEVNULL)
 
 
+def build_dropin(verbose: bool = False) -> None:
+    """Test infrastructure: the reference's own suites linked against the drop-in
+    (tests/dropin/Makefile; needs the reference sources, so build container only)."""
+    if REFERENCE.exists():
+        subprocess.run(["make", "-s", "-C", str(ROOT / "tests" / "dropin"), "-j8"], check=True,
+                       stdout=None if verbose else subprocess.DEVNULL)
+
+
 def build_all(force: bool = False, verbose: bool = False) -> None:
     build_native(force=force, verbose=verbose)
     build_tools(force=force, verbose=verbose)
     build_oracle(force=force, verbose=verbose)
+    build_dropin(verbose=verbose)
 
 
 if __name__ == "__main__":
