@@ -72,8 +72,10 @@ typedef struct sf_exec {
   int32_t n_devices;        /* devices to shard stripes over; 0 = all visible */
   const int32_t* devices;   /* explicit ordinals, or NULL for 0..n_devices-1 */
   int64_t mem_budget_bytes; /* per-device cap for embedding chunks; 0 = auto */
-  int32_t kernel;           /* 0 = auto, 1 = dense tiled, 2 = sparse bit (unweighted only) */
-  int32_t flags;            /* bit 0: SF_EXEC_EXACT_NO_FMA (weighted metrics) */
+  int32_t kernel;           /* 0 = auto, 1 = dense tiled, 2 = sparse bit walk (unweighted only,
+                               bitwise), 5 = intersection (unweighted only, exact fixed-point sums) */
+  int32_t flags;            /* bit 0: SF_EXEC_EXACT_NO_FMA: bitwise-identical results (weighted:
+                               no FMA; unweighted auto: the sparse walk instead of kernel 5) */
 } sf_exec;
 
 #define SF_EXEC_EXACT_NO_FMA 1

@@ -5,7 +5,10 @@
 // K1 (embed) -> K2 (stripe update) per chunk, K3 (finalize), copy back.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_scan.cuh>
+
 #include <algorithm>
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -13,6 +16,7 @@
 #include <vector>
 
 #include "embed_kernels.cuh"
+#include "isect_kernels.cuh"
 #include "sf_common.hpp"
 #include "sparse_kernels.cuh"
 #include "stripe_kernels.cuh"
@@ -372,6 +376,9 @@ struct DeviceState {
   std::vector<int64_t> sched_off;  // per chunk: offsets of its arrays in `sched`
   // sparse-bit (unweighted) path
   DevBuf nodebits, lens_pad;
+  // intersection (unweighted) path
+  DevBuf limbs, dmask, cacc, colsum, occ, base, packed, cubtmp;
+  size_t cub_bytes = 0;
   std::vector<cudaEvent_t> events;
   ~DeviceState() {
     if (dev >= 0) {
@@ -386,7 +393,8 @@ struct sf_plan {
   int metric = 0, prec = 0;
   int32_t n = 0, E = 0, start = 0, stop = 0;
   bool bits = false, exact = false;
-  int kernel = 1;  // 1 dense, 2 sparse-bit
+  int kernel = 1;  // 1 dense, 2 sparse-bit walk (3/4 flattened variants), 5 intersection
+  int32_t scale = 0;  // intersection path: limbs hold round(L * 2^scale)
   int64_t row_words = 0;  // per embedding row: words (bits) or doubles (values)
   Schedule sched;
   std::vector<std::unique_ptr<DeviceState>> devs;
@@ -403,9 +411,113 @@ struct SparseCfg {
   static constexpr int TK = NWK * RK, TS = NWS * 32 * RS;
 };
 
+// Intersection kernel for the unweighted metric (kernel 5).
+struct IsectCfg {
+  static constexpr int RK = 4, RS = 2, NWK = 8, NWS = 2;
+  using T = IsectTile<RK, RS, NWK, NWS>;
+};
+
 int64_t sparse_n_ext(int n) {
-  const int64_t need = static_cast<int64_t>(n) + n / 2 + SparseCfg::TK + SparseCfg::TS + 64;
+  const int64_t tile = std::max(SparseCfg::TK + SparseCfg::TS, IsectCfg::T::VW);
+  const int64_t need = static_cast<int64_t>(n) + n / 2 + tile + 64;
   return (need + 3) / 4 * 4;
+}
+
+// Bytes the node-packed paths keep resident on one device (beyond stripes).
+size_t nodepacked_bytes(int kernel, int32_t E, int n) {
+  const int64_t W = (E + 31) / 32;
+  const int64_t G = (W + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(n);
+  size_t b = static_cast<size_t>(E) * static_cast<size_t>((n + 31) / 32) * 4 +
+             static_cast<size_t>(W * n_ext) * 4 + static_cast<size_t>(W) * 32 * 8;
+  if (kernel == 5)
+    b += static_cast<size_t>(W * n_ext) * 4 + static_cast<size_t>(G * n_ext) * 8 +
+         static_cast<size_t>(G) * 1024 * 8 + static_cast<size_t>(n) * 32;
+  return b;
+}
+
+// Fixed-point scale for the intersection path: round(L * 2^q) < 2^63 for the
+// longest branch, so each length is two 32-bit limbs (hi < 2^31).
+int32_t isect_scale(const double* lengths, int32_t E, bool fp32) {
+  double lmax = 0.0;
+  for (int32_t r = 0; r < E; ++r) {
+    const double L = fp32 ? static_cast<double>(static_cast<float>(lengths[r])) : lengths[r];
+    lmax = std::max(lmax, L);
+  }
+  if (!(lmax > 0.0)) return 0;
+  return 62 - std::ilogb(lmax);
+}
+
+sf_status isect_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
+  const int64_t W = (plan->E + 31) / 32;
+  const int64_t G = (W + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(plan->n);
+  const bool fp32 = plan->prec == SF_FP32;
+  plan->scale = isect_scale(p->lengths, plan->E, fp32);
+  std::vector<uint32_t> limbs(static_cast<size_t>(G) * 1024 * 2, 0u);
+  for (int32_t r = 0; r < plan->E; ++r) {
+    const double L = fp32 ? static_cast<double>(static_cast<float>(p->lengths[r])) : p->lengths[r];
+    const uint64_t v = static_cast<uint64_t>(std::nearbyint(std::ldexp(L, plan->scale)));
+    limbs[2 * static_cast<size_t>(r)] = static_cast<uint32_t>(v >> 32);
+    limbs[2 * static_cast<size_t>(r) + 1] = static_cast<uint32_t>(v & 0xffffffffull);
+  }
+  SF_TRY(upload(d.limbs, d.dev, limbs.data(), limbs.size(), d.stream, "length limbs"));
+  SF_TRY(d.dmask.alloc(d.dev, static_cast<size_t>(W) * 4, "dense-row mask"));
+  SF_TRY(d.cacc.alloc(d.dev, 2 * sizeof(unsigned long long), "dense total"));
+  SF_TRY(d.colsum.alloc(d.dev, static_cast<size_t>(plan->n) * 4 * sizeof(unsigned long long), "column sums"));
+  const size_t cells = static_cast<size_t>(G * n_ext);
+  SF_TRY(d.occ.alloc(d.dev, cells * 4, "occupancy"));
+  SF_TRY(d.base.alloc(d.dev, (cells + 1) * 4, "packed offsets"));
+  SF_TRY(d.packed.alloc(d.dev, static_cast<size_t>(W * n_ext) * 4, "packed words"));
+  if (static_cast<uint64_t>(W * n_ext) >= (1ull << 32))
+    return fail(SF_ENOMEM, "problem too large for 32-bit packed offsets");
+  size_t tmp = 0;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
+                                        static_cast<int64_t>(cells + 1), d.stream));
+  d.cub_bytes = tmp;
+  SF_TRY(d.cubtmp.alloc(d.dev, tmp, "scan scratch"));
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_isect(const IsectArgs& a, cudaStream_t st) {
+  using C = IsectCfg;
+  using T = C::T;
+  auto* kern = stripe_isect_kernel<Real, C::RK, C::RS, C::NWK, C::NWS>;
+  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES));
+  const dim3 grid((a.n + T::TK - 1) / T::TK, (a.s_end - a.s_begin + T::TS - 1) / T::TS);
+  kern<<<grid, T::NT, T::BYTES, st>>>(a);
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+// Intersection-path preparation on device: dense mask, occupancy, packing.
+sf_status isect_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
+  const int n = plan->n;
+  const int64_t W = (plan->E + 31) / 32;
+  const int64_t G = (W + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(n);
+  const int64_t cells = G * n_ext;
+  SF_CUDA(cudaMemsetAsync(d.dmask.p, 0, static_cast<size_t>(W) * 4, st));
+  SF_CUDA(cudaMemsetAsync(d.cacc.p, 0, 2 * sizeof(unsigned long long), st));
+  SF_CUDA(cudaMemsetAsync(d.colsum.p, 0, static_cast<size_t>(n) * 4 * sizeof(unsigned long long), st));
+  SF_CUDA(cudaMemsetAsync(d.base.as<uint32_t>() + cells, 0, 4, st));
+  isect_row_count_kernel<<<grid_for(static_cast<int64_t>(plan->E) * 32, 256), 256, 0, st>>>(
+      d.emb.as<uint32_t>(), plan->row_words, plan->E, n, d.limbs.as<uint2>(), d.dmask.as<uint32_t>(),
+      d.cacc.as<unsigned long long>());
+  isect_occ_kernel<<<grid_for(cells, 256), 256, 0, st>>>(
+      d.nodebits.as<uint32_t>(), n_ext, n, static_cast<int32_t>(W), static_cast<int32_t>(G),
+      d.dmask.as<uint32_t>(), d.limbs.as<uint2>(), d.occ.as<uint32_t>(), d.base.as<uint32_t>(),
+      d.colsum.as<unsigned long long>());
+  size_t tmp = d.cub_bytes;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cubtmp.p, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
+                                        cells + 1, st));
+  isect_pack_kernel<<<grid_for(cells, 256), 256, 0, st>>>(
+      d.nodebits.as<uint32_t>(), n_ext, static_cast<int32_t>(W), static_cast<int32_t>(G),
+      d.dmask.as<uint32_t>(), d.base.as<uint32_t>(), d.packed.as<uint32_t>());
+  SF_CUDA(cudaGetLastError());
+  plan->stats.launches += 4;  // row count, occupancy, pack, + the scan's own kernels (>= 1)
+  return SF_OK;
 }
 
 sf_status sparse_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
@@ -532,10 +644,30 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
           d.nodebits.as<uint32_t>(), n_ext, n, static_cast<int32_t>(W));
       SF_CUDA(cudaGetLastError());
       plan->stats.launches += 2;
+      if (plan->kernel == 5) SF_TRY(isect_build(plan, d, st));
     }
     SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
     // ---- K2: stripe update over the chunk's rows
-    if (plan->kernel >= 2) {
+    if (plan->kernel == 5) {
+      IsectArgs a;
+      a.occ = d.occ.as<uint32_t>();
+      a.base = d.base.as<uint32_t>();
+      a.packed = d.packed.as<uint32_t>();
+      a.limbs = d.limbs.as<uint2>();
+      a.colsum = d.colsum.as<unsigned long long>();
+      a.cacc = d.cacc.as<unsigned long long>();
+      a.n_ext = sparse_n_ext(n);
+      a.G = static_cast<int32_t>(((plan->E + 31) / 32 + 31) / 32);
+      a.n = n;
+      a.s_begin = d.a;
+      a.s_end = d.b;
+      a.scale = plan->scale;
+      a.finalize = finalize ? 1 : 0;
+      a.dist = d.dist.p;
+      a.tot = d.tot.p;
+      a.exec_updates = d.exec_ctr.as<unsigned long long>();
+      SF_TRY(plan->prec == SF_FP64 ? launch_isect<double>(a, st) : launch_isect<float>(a, st));
+    } else if (plan->kernel >= 2) {
       SparseArgs a;
       a.nb = d.nodebits.as<uint32_t>();
       a.n_ext = sparse_n_ext(n);
@@ -590,7 +722,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
   }
   const size_t ne = d.events.size();
   SF_CUDA(cudaEventRecord(d.events[ne - 2], st));
-  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED) {
+  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED && plan->kernel != 5) {
     const int blocks = grid_for(slots, 256);
     if (plan->prec == SF_FP64)
       finalize_kernel<double><<<blocks, 256, 0, st>>>(d.dist.as<double>(), d.tot.as<double>(), slots);
@@ -646,12 +778,20 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stop = stop;
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
-  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 4) ? ex->kernel : 1;
-  // auto: the sparse walk for the unweighted metric (exact, same bits)
-  if ((!ex || ex->kernel == 0) && metric == SF_UNWEIGHTED) plan->kernel = 2;
+  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 5) ? ex->kernel : 1;
+  const int n = p->n_samples;
+  // auto, unweighted: the intersection kernel (exact fixed-point sums), or
+  // with SF_EXEC_EXACT_NO_FMA the sparse walk (the reference's adds in the
+  // reference's order: bitwise identical); both keep every row resident, so
+  // a budget too small for that selects the chunked dense kernel.
+  if ((!ex || ex->kernel == 0) && metric == SF_UNWEIGHTED) {
+    const int k = plan->exact ? 2 : 5;
+    const bool fits = !(ex && ex->mem_budget_bytes > 0) ||
+                      nodepacked_bytes(k, p->n_rows, n) <= static_cast<size_t>(ex->mem_budget_bytes);
+    plan->kernel = fits ? k : 1;
+  }
   if (plan->kernel >= 2 && metric != SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the sparse bit kernel implements the unweighted metric only");
-  const int n = p->n_samples;
   plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;
   const size_t w = prec == SF_FP64 ? 8 : 4;
   const bool has_t = metric != SF_WEIGHTED_UNNORMALIZED;
@@ -714,6 +854,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(plan->E) * row_bytes, "embedding rows"));
       SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));
       SF_TRY(sparse_prepare(plan.get(), d, p));
+      if (plan->kernel == 5) SF_TRY(isect_prepare(plan.get(), d, p));
     } else {
       SF_TRY(upload_schedule(d, plan->sched));
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(cmax) * row_bytes, "embedding chunk"));

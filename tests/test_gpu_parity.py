@@ -3,8 +3,13 @@ vectors (tests/golden, produced by the reference itself) and vs the CPU
 oracle restatement (tests/oracle_port.py) on larger seeded instances.
 
 Tolerances (BASELINE.json north_star, test_kernels.cpp:187-202):
-  * unweighted, any precision: bit-exact (0/1 products are exact, so FMA and
-    mul+add round identically and the per-slot postorder sum is the same);
+  * unweighted, walk kernels (dense, sparse walk 2/3/4, and the default under
+    exact mode): bit-exact (0/1 products are exact, so FMA and mul+add round
+    identically and the per-slot postorder sum is the same);
+  * unweighted, intersection kernel (5, the default): the correctly rounded
+    exact sums; fp64 within 1e-12 relative of the reference's sequential sums
+    (and bitwise equal to the exact rational sums, test_isect_is_exact),
+    fp32 within max(1e-5 |x|, 1e-6);
   * weighted fp64 with FMA: |got - want| <= 1e-12 * max(1, |want|);
   * weighted fp32 with FMA: <= max(1e-5 |want|, 1e-6);
   * weighted, exact (no-FMA) mode: bit-exact in both precisions.
@@ -21,7 +26,8 @@ from paper_2005_05826_b200 import stripefrac as sf
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4]  # 3/4: flattened sparse walk, 32/64-word chunks
+KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4, N.KERNEL_ISECT]  # 3/4: flattened sparse walk
+WALKS = (N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4)
 
 
 def _gpu_stripes(problem, metric, prec, start, stop, kernel=N.KERNEL_DENSE, exact=False,
@@ -38,9 +44,14 @@ def _gpu_stripes(problem, metric, prec, start, stop, kernel=N.KERNEL_DENSE, exac
     return d, (t if metric != 2 else None), st
 
 
-def _assert_close(metric, prec, exact, got, want):
-    if metric == 1 or exact:
+def _assert_close(metric, prec, exact, got, want, kernel=N.KERNEL_DENSE):
+    bitwise = exact or (metric == 1 and kernel in WALKS)
+    if bitwise:
         assert np.array_equal(got, want), f"max |diff| {np.nanmax(np.abs(got - want))}"
+    elif metric == 1 and prec == 8:
+        # exact fixed-point sums vs the reference's sequential sums: relative
+        err = np.abs(got - want)
+        assert np.all(err <= 1e-12 * np.abs(want)), f"max rel {np.max(err / np.maximum(np.abs(want), 1e-300))}"
     elif prec == 8:
         tol = 1e-12 * np.maximum(1.0, np.abs(want))
         assert np.all(np.abs(got - want) <= tol), f"max |diff| {np.abs(got - want).max()}"
@@ -72,9 +83,9 @@ def test_golden_stripes(device_ok, case, kernel):
         gd, gt = gu.stripes(r, n)
         for exact in ((False, True) if metric != 1 else (False,)):
             d, t, _ = _gpu_stripes(problem, metric, prec, r["start"], r["stop"], kernel, exact)
-            _assert_close(metric, prec, exact, d, gd)
+            _assert_close(metric, prec, exact, d, gd, kernel)
             if gt is not None:
-                _assert_close(metric, prec, exact, t, gt)
+                _assert_close(metric, prec, exact, t, gt, kernel)
 
 
 @pytest.mark.parametrize("case", [c for c in CASES if "embedding_weighted" in c],
@@ -105,9 +116,12 @@ def test_demo_condense_and_tsv_bytes(device_ok):
             dm = sf.compute_distance_matrix(tree, table, cfg,
                                             exec_options=sf.ExecOptions(exact=exact))
             want = np.array(entry["values"]).reshape(dm.n(), dm.n())
-            if m == sf.Metric.Unweighted or exact:
+            if exact:
                 assert np.array_equal(dm.values, want)
                 assert sf.to_tsv(dm) == entry["tsv"]
+            elif m == sf.Metric.Unweighted:
+                tol = 1e-12 if p == sf.Precision.Fp64 else 1e-5
+                assert np.allclose(dm.values, want, rtol=tol, atol=0 if p == sf.Precision.Fp64 else 1e-6)
             else:
                 assert np.allclose(dm.values, want, rtol=1e-12 if p == sf.Precision.Fp64 else 1e-5,
                                    atol=0 if p == sf.Precision.Fp64 else 1e-6)
@@ -146,12 +160,15 @@ def test_oracle_random_instances(device_ok, metric, prec):
             if start >= stop:
                 continue
             wd, wt = op.compute_stripes(problem, metric, prec, start, stop)
-            for exact in ((False, True) if metric != 1 else (False,)):
-                d, t, st = _gpu_stripes(problem, metric, prec, start, stop, exact=exact)
-                _assert_close(metric, prec, exact, d, wd)
-                if wt is not None:
-                    _assert_close(metric, prec, exact, t, wt)
-                assert st.updates_alg == problem.n_rows * (stop - start) * n
+            for exact in (False, True):
+                for kernel in (N.KERNEL_DENSE, N.KERNEL_AUTO):
+                    d, t, st = _gpu_stripes(problem, metric, prec, start, stop, kernel, exact)
+                    used = kernel if kernel != N.KERNEL_AUTO or metric != 1 else (
+                        N.KERNEL_SPARSE if exact else N.KERNEL_ISECT)
+                    _assert_close(metric, prec, exact, d, wd, used)
+                    if wt is not None:
+                        _assert_close(metric, prec, exact, t, wt, used)
+                    assert st.updates_alg == problem.n_rows * (stop - start) * n
 
 
 def test_chunked_embedding_with_pending_rows(device_ok):
@@ -194,10 +211,7 @@ def test_batch_api_matches_full_run(device_ok):
         while (b := em.next_batch(5)) is not None:
             sf.accumulate(sset, b, cfg, c)
         sf.finalize(sset)
-        if m == sf.Metric.Unweighted:
-            assert np.array_equal(sset.distances, want.distances)
-        else:
-            assert np.allclose(sset.distances, want.distances, rtol=1e-12, atol=0)
+        assert np.allclose(sset.distances, want.distances, rtol=1e-12, atol=0)
         E = em.total_rows()
         assert c.kernel_passes == -(-E // 5)
         assert c.embedding_reads == 2 * E * 11 * 23
@@ -281,9 +295,83 @@ def test_sparse_kernel_matches_dense_bitwise(device_ok, prec):
                 assert 0 < st.updates_exec <= st.updates_alg
 
 
-def test_sparse_is_the_default_for_unweighted(device_ok):
+def test_isect_is_the_default_for_unweighted(device_ok):
     inst = sf.random_instance(45, 50, 100, 0.1)
     problem = sf.flatten(inst.tree, inst.table)
-    _, _, st = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_AUTO)
-    # the sparse walk only touches rows present in a slot's samples
-    assert st.updates_exec < st.updates_alg
+    d5, t5, st = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_ISECT)
+    d0, t0, st0 = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_AUTO)
+    assert np.array_equal(d5, d0) and np.array_equal(t5, t0)
+    # the intersection walk only touches rows shared by a slot's two samples
+    assert 0 < st0.updates_exec < st0.updates_alg
+    _, _, st2 = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_AUTO, exact=True)
+    assert st2.updates_exec > st0.updates_exec  # exact mode walks the union
+
+
+def _exact_stripes(problem, prec, start, stop):
+    """t and d of every slot as exact rationals (Fraction), rounded once:
+    the value a correctly rounded unweighted kernel must return."""
+    from fractions import Fraction
+    n, E = problem.n_samples, problem.n_rows
+    pres = np.zeros((E, n), bool)
+    fp, si = problem.feat_ptr, problem.sample_idx
+    for r in range(E):
+        f = problem.leaf_feature[r]
+        if f >= 0:
+            pres[r, si[fp[f]:fp[f + 1]]] = True
+    for r in range(E):
+        q = problem.parent_row[r]
+        if q >= 0:
+            pres[q] |= pres[r]
+    L = problem.lengths if prec == 8 else problem.lengths.astype(np.float32).astype(np.float64)
+    Lf = [Fraction(float(x)) for x in L]
+    dt = np.float64 if prec == 8 else np.float32
+    d = np.zeros((stop - start, n), dt)
+    t = np.zeros((stop - start, n), dt)
+    for s in range(start, stop):
+        for k in range(n):
+            l = (k + s + 1) % n
+            u, v = pres[:, k], pres[:, l]
+            tt = sum((Lf[e] for e in np.nonzero(u | v)[0]), Fraction(0))
+            dd = sum((Lf[e] for e in np.nonzero(u ^ v)[0]), Fraction(0))
+            t[s - start, k] = dt(float(tt))
+            d[s - start, k] = dt(float(dd))
+    return d, t
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_isect_is_exact(device_ok, prec):
+    """Kernel 5 returns the correctly rounded exact sums (raw, unfinalized),
+    on instances with sparse and dense (complemented) rows, wrap, odd/even n
+    and partial ranges."""
+    for seed, n, leaves, dens in [(51, 40, 60, 0.05), (52, 33, 50, 0.6), (53, 2, 4, 0.5),
+                                  (54, 3, 7, 0.9), (55, 70, 40, 0.3)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 2, S)]:
+            if start >= stop:
+                continue
+            wd, wt = _exact_stripes(problem, prec, start, stop)
+            d, t, _ = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_ISECT, finalize=False)
+            if prec == 8:
+                assert np.array_equal(d, wd) and np.array_equal(t, wt)
+            else:  # fp32: rounded via fp64 (double rounding can move 1 ulp)
+                assert np.all(np.abs(d.astype(np.float64) - wd) <= np.spacing(np.abs(wd).astype(np.float32)))
+                assert np.all(np.abs(t.astype(np.float64) - wt) <= np.spacing(np.abs(wt).astype(np.float32)))
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_isect_matches_oracle_larger(device_ok, prec):
+    """Kernel 5 vs the CPU restatement of the reference (sequential sums) on
+    instances spanning several CTA tiles and 1024-row groups."""
+    for seed, n, leaves, dens, subset in [(61, 300, 1500, 0.01, 0), (62, 517, 2500, 0.004, 2000),
+                                          (63, 129, 700, 0.2, 0), (64, 1000, 3000, 0.002, 0)]:
+        inst = sf.random_instance(seed, n, leaves, dens, subset)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 3, S - 1)]:
+            wd, wt = op.compute_stripes(problem, 1, prec, start, stop)
+            d, t, st = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_ISECT)
+            _assert_close(1, prec, False, d, wd, N.KERNEL_ISECT)
+            _assert_close(1, prec, False, t, wt, N.KERNEL_ISECT)
+            assert st.updates_alg == problem.n_rows * (stop - start) * n
