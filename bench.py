@@ -167,7 +167,7 @@ def run_ours(args, cfg):
     stop_all = min(S, args.stripes) if args.stripes else S
     a = int(stop_all * rank // world)
     b = int(stop_all * (rank + 1) // world)
-    kernel = {"auto": 0, "dense": 1, "sparse": 2, "flat32": 3, "flat64": 4, "isect": 5}[args.kernel]
+    kernel = {"auto": 0, "dense": 1, "sparse": 2, "flat32": 3, "flat64": 4, "isect": 5, "isect2": 6}[args.kernel]
     ex, _keep = N.make_exec([local], kernel)
     plan = C.c_void_p()
     t0 = time.perf_counter()
@@ -368,7 +368,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--kernel", choices=["auto", "dense", "sparse", "flat32", "flat64", "isect"],
+    ap.add_argument("--kernel", choices=["auto", "dense", "sparse", "flat32", "flat64", "isect", "isect2"],
                     default="auto")
     ap.add_argument("--stripes", type=int, default=0, help="limit to stripes [0, N) (debug)")
     ap.add_argument("--e2e-steps", type=int, default=1)

@@ -27,7 +27,7 @@ NVCC_FLAGS = [
     "-Xptxas", "-warn-spills",
 ]
 SOURCES = ["sf_api.cu", "host_prep.cpp"]
-HEADERS = ["sf_common.hpp", "embed_kernels.cuh", "stripe_kernels.cuh", "sparse_kernels.cuh",
+HEADERS = ["sf_common.hpp", "embed_kernels.cuh", "stripe_kernels.cuh", "sparse_kernels.cuh", "isect2_kernels.cuh",
            "isect_kernels.cuh"]
 
 

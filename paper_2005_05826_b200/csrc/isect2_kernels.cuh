@@ -1,0 +1,309 @@
+// K2-UW, intersection form v2 (kernel 6): the same exact algebra as
+// isect_kernels.cuh (t = p_k + p_l + C - G_kl, d = x_k + x_l - 2 G_kl with
+// X_e = S_e or its complement), with a layout chosen for the walk:
+//
+//  * rows are PERMUTED before packing: because the sums are exact, row order
+//    is free. "Heavy" rows (|X_e| >= heavy_min, i.e. the rows most pairs
+//    share) go first, sorted by |X_e| descending; the rest keep postorder
+//    (subtree locality). At the EMP shape this halves the words a slot has to
+//    visit (577 -> ~240 candidate words) and concentrates ~80% of the shared
+//    rows in the first ~4 groups;
+//  * 64-row words (u64), bit (63-i) = permuted row 64w+i; groups of 32 words
+//    (2048 rows) with a per-column occupancy mask, and a second level: one
+//    bit per group per column (gm), so a slot skips every group in which
+//    either column is empty;
+//  * lengths as two exactly representable doubles (hi, lo limbs of the
+//    fixed-point value), accumulated with DADD: every partial sum stays below
+//    2^53, so the accumulation is exact;
+//  * no shared-memory staging and no CTA barriers: each warp owns one u
+//    column (uniform loads) and 32*RS consecutive v columns (coalesced
+//    loads); all reads go through L1/L2, so warps never wait on each other.
+#pragma once
+
+#include <cstdint>
+
+namespace sf {
+
+// ---- preparation ----------------------------------------------------------
+
+// One warp per row: |S_e|, dense flag, and the sort key that puts heavy rows
+// first by |X_e| descending (stable radix sort keeps postorder among ties and
+// among the light rows, whose key is n + 1).
+__global__ void i2_row_key_kernel(const uint32_t* __restrict__ rows, int64_t stride, int32_t E,
+                                  int32_t n, int32_t heavy_min, uint32_t* __restrict__ keys,
+                                  int32_t* __restrict__ vals, uint8_t* __restrict__ dense) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < E; r += nwarps) {
+    const uint32_t* row = rows + r * stride;
+    int m = 0;
+    for (int64_t i = lane; i < stride; i += 32) m += __popc(__ldg(row + i));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m += __shfl_xor_sync(0xffffffffu, m, off);
+    if (lane == 0) {
+      const bool dn = 2 * m > n;
+      const int x = dn ? n - m : m;
+      keys[r] = x >= heavy_min ? static_cast<uint32_t>(n - x) : static_cast<uint32_t>(n + 1);
+      vals[r] = static_cast<int32_t>(r);
+      dense[r] = dn ? 1 : 0;
+    }
+  }
+}
+
+// Permuted row i <- original row perm[i]: dense mask, length limbs as
+// doubles, and C = sum of the dense rows' fixed-point lengths (limb sums).
+__global__ void i2_perm_kernel(const int32_t* __restrict__ perm, int32_t E, int64_t rows_pad,
+                               const uint8_t* __restrict__ dense,
+                               const unsigned long long* __restrict__ fix, int32_t lo_bits,
+                               unsigned long long* __restrict__ dmask64,
+                               double2* __restrict__ limbs, unsigned long long* __restrict__ cacc) {
+  const unsigned long long lo_mask = (1ull << lo_bits) - 1ull;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows_pad;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    if (i >= E) {
+      limbs[i] = make_double2(0.0, 0.0);
+      continue;
+    }
+    const int r = perm[i];
+    const unsigned long long v = fix[r];
+    const unsigned long long hi = v >> lo_bits, lo = v & lo_mask;
+    limbs[i] = make_double2(static_cast<double>(hi), static_cast<double>(lo));
+    if (dense[r]) {
+      atomicOr(dmask64 + (i >> 6), 0x8000000000000000ull >> (i & 63));
+      atomicAdd(cacc, hi);
+      atomicAdd(cacc + 1, lo);
+    }
+  }
+}
+
+// Sample-packed rows -> node-packed 64-row X-words of the permuted rows.
+// One warp per (64-row word w, 32-sample block cb): 2 x 32 ballots.
+__global__ void i2_transpose_kernel(const uint32_t* __restrict__ rows, int64_t stride,
+                                    const int32_t* __restrict__ perm, int32_t E, int32_t n,
+                                    int32_t W, const unsigned long long* __restrict__ dmask64,
+                                    unsigned long long* __restrict__ nx, int64_t n_ext) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t blocks = static_cast<int64_t>(W) * stride;
+  for (int64_t bidx = warp; bidx < blocks; bidx += nwarps) {
+    const int64_t w = bidx / stride;
+    const int64_t cb = bidx - w * stride;
+    const int64_t r1 = 64 * w + lane, r2 = r1 + 32;
+    const uint32_t a = r1 < E ? __ldg(rows + static_cast<int64_t>(perm[r1]) * stride + cb) : 0u;
+    const uint32_t b = r2 < E ? __ldg(rows + static_cast<int64_t>(perm[r2]) * stride + cb) : 0u;
+    unsigned long long out = 0ull;
+#pragma unroll
+    for (int bit = 0; bit < 32; ++bit) {
+      const uint32_t v1 = __ballot_sync(0xffffffffu, (a >> bit) & 1u);
+      const uint32_t v2 = __ballot_sync(0xffffffffu, (b >> bit) & 1u);
+      if (bit == lane)
+        out = (static_cast<unsigned long long>(__brev(v1)) << 32) | static_cast<unsigned long long>(__brev(v2));
+    }
+    const int64_t s = cb * 32 + lane;
+    if (s < n) nx[w * n_ext + s] = out ^ dmask64[w];
+  }
+}
+
+// Wrap columns: nx[w][c] = nx[w][c mod n] for n <= c < n_ext.
+__global__ void i2_extend_kernel(unsigned long long* __restrict__ nx, int64_t n_ext, int32_t n,
+                                 int32_t W) {
+  const int64_t extra = n_ext - n;
+  const int64_t total = static_cast<int64_t>(W) * extra;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = i / extra;
+    const int64_t col = n + i % extra;
+    nx[w * n_ext + col] = nx[w * n_ext + col % n];
+  }
+}
+
+// One thread per (group, column): occupancy mask, nonzero-word count, the
+// group bit of the column, and for real columns the limb sums x_c / p_c.
+// colsum layout: [4][n] = x_hi, x_lo, p_hi, p_lo; gm layout: [NGW][n_ext].
+__global__ void i2_occ_kernel(const unsigned long long* __restrict__ nx, int64_t n_ext, int32_t n,
+                              int32_t W, int32_t G, const unsigned long long* __restrict__ dmask64,
+                              const double2* __restrict__ limbs, uint32_t* __restrict__ occ,
+                              uint32_t* __restrict__ cnt, uint32_t* __restrict__ gm,
+                              unsigned long long* __restrict__ colsum) {
+  const int64_t total = static_cast<int64_t>(G) * n_ext;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(idx / n_ext);
+    const int64_t c = idx - static_cast<int64_t>(g) * n_ext;
+    uint32_t o = 0u;
+    int count = 0;
+    unsigned long long xh = 0, xl = 0, ph = 0, pl = 0;
+    for (int i = 0; i < 32; ++i) {
+      const int w = 32 * g + i;
+      if (w >= W) break;
+      const unsigned long long x = __ldg(nx + static_cast<int64_t>(w) * n_ext + c);
+      if (x == 0ull) continue;
+      o |= 0x80000000u >> i;
+      ++count;
+      if (c < n) {
+        const unsigned long long dm = __ldg(dmask64 + w);
+        unsigned long long b = x;
+        while (b) {
+          const int p = __clzll(static_cast<long long>(b));
+          const unsigned long long m = 0x8000000000000000ull >> p;
+          b ^= m;
+          const double2 L = __ldg(limbs + 64 * static_cast<int64_t>(w) + p);
+          const unsigned long long h = static_cast<unsigned long long>(L.x);
+          const unsigned long long l = static_cast<unsigned long long>(L.y);
+          xh += h;
+          xl += l;
+          if (!(dm & m)) {
+            ph += h;
+            pl += l;
+          }
+        }
+      }
+    }
+    occ[idx] = o;
+    cnt[idx] = static_cast<uint32_t>(count);
+    if (o) atomicOr(gm + static_cast<int64_t>(g >> 5) * n_ext + c, 0x80000000u >> (g & 31));
+    if (c < n && (xh | xl)) {
+      atomicAdd(colsum + c, xh);
+      atomicAdd(colsum + n + c, xl);
+      if (ph | pl) {
+        atomicAdd(colsum + 2 * static_cast<int64_t>(n) + c, ph);
+        atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, pl);
+      }
+    }
+  }
+}
+
+// One thread per (group, column): the nonzero words, in word order.
+__global__ void i2_pack_kernel(const unsigned long long* __restrict__ nx, int64_t n_ext, int32_t W,
+                               int32_t G, const uint32_t* __restrict__ base,
+                               unsigned long long* __restrict__ packed) {
+  const int64_t total = static_cast<int64_t>(G) * n_ext;
+  for (int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < total;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int g = static_cast<int>(idx / n_ext);
+    const int64_t c = idx - static_cast<int64_t>(g) * n_ext;
+    unsigned long long* out = packed + base[idx];
+    for (int i = 0; i < 32; ++i) {
+      const int w = 32 * g + i;
+      if (w >= W) break;
+      const unsigned long long x = __ldg(nx + static_cast<int64_t>(w) * n_ext + c);
+      if (x) *out++ = x;
+    }
+  }
+}
+
+// ---- the stripe kernel ------------------------------------------------------
+
+struct Isect2Args {
+  const uint32_t* occ;                 // [G][n_ext]
+  const uint32_t* base;                // [G*n_ext + 1], in u64 words
+  const unsigned long long* packed;    // nonzero X-words
+  const double2* limbs;                // [G*2048] (hi, lo) of permuted rows
+  const uint32_t* gm;                  // [NGW][n_ext]
+  const unsigned long long* colsum;    // [4][n]
+  const unsigned long long* cacc;      // [2]
+  int64_t n_ext;
+  int32_t G, NGW;
+  int32_t n;
+  int32_t s_begin, s_end;
+  int32_t lo_bits;   // value = hi * 2^lo_bits + lo
+  int32_t scale;     // value = round(L * 2^scale)
+  int32_t finalize;
+  void* dist;
+  void* tot;
+  unsigned long long* exec_updates;
+};
+
+// Exact value v * 2^-scale (v >= 0, a 128-bit integer), correctly rounded.
+__device__ __forceinline__ double i2_fixed_to_double(__int128 v, int scale) {
+  const unsigned __int128 u = static_cast<unsigned __int128>(v);
+  const unsigned long long hi = static_cast<unsigned long long>(u >> 64);
+  const unsigned long long lo = static_cast<unsigned long long>(u);
+  if (hi == 0ull) return ldexp(__ull2double_rn(lo), -scale);
+  const int sh = 64 - __clzll(static_cast<long long>(hi));
+  unsigned long long top = static_cast<unsigned long long>(u >> sh);
+  const unsigned long long rest = sh == 64 ? lo : (lo & ((1ull << sh) - 1ull));
+  top |= rest != 0ull ? 1ull : 0ull;
+  return ldexp(__ull2double_rn(top), sh - scale);
+}
+
+// Warp w of the CTA owns u column k = blockIdx.x*NW + w and the stripes
+// s0 + lane + 32*i (i < RS), s0 = s_begin + blockIdx.y*32*RS.
+template <class Real, int RS, int NW>
+__global__ void __launch_bounds__(32 * NW) stripe_isect2_kernel(const Isect2Args a) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * NW + (threadIdx.x >> 5);
+  const int n = a.n;
+  if (k >= n) return;
+  const int s0 = a.s_begin + blockIdx.y * 32 * RS;
+  const int64_t n_ext = a.n_ext;
+  unsigned long long executed = 0;
+  Real* dist = static_cast<Real*>(a.dist);
+  Real* tot = static_cast<Real*>(a.tot);
+  const unsigned long long* xs = a.colsum;
+
+#pragma unroll 1
+  for (int i = 0; i < RS; ++i) {
+    const int s = s0 + lane + 32 * i;
+    if (s >= a.s_end) break;
+    const int64_t l = static_cast<int64_t>(k) + s + 1;  // extended column, < n_ext
+    double gh = 0.0, gl = 0.0;
+#pragma unroll 1
+    for (int j = 0; j < a.NGW; ++j) {
+      uint32_t gmask = __ldg(a.gm + j * n_ext + k) & __ldg(a.gm + j * n_ext + l);
+      while (gmask) {
+        const int gi = __clz(gmask);
+        gmask ^= 0x80000000u >> gi;
+        const int g = 32 * j + gi;
+        const int64_t gb = static_cast<int64_t>(g) * n_ext;
+        const uint32_t ou = __ldg(a.occ + gb + k);
+        const uint32_t ov = __ldg(a.occ + gb + l);
+        uint32_t o = ou & ov;
+        if (!o) continue;
+        const unsigned long long* pu = a.packed + __ldg(a.base + gb + k);
+        const unsigned long long* pv = a.packed + __ldg(a.base + gb + l);
+        const double2* Lg = a.limbs + static_cast<int64_t>(g) * 2048;
+        do {
+          const int w = __clz(o);
+          o ^= 0x80000000u >> w;
+          const uint32_t above = ~(0xffffffffu >> w);
+          unsigned long long x = __ldg(pu + __popc(ou & above)) & __ldg(pv + __popc(ov & above));
+          executed += __popcll(x);
+          const double2* Lw = Lg + 64 * w;
+          while (x) {
+            const int p = __clzll(static_cast<long long>(x));
+            x ^= 0x8000000000000000ull >> p;
+            const double2 L = __ldg(Lw + p);
+            gh += L.x;
+            gl += L.y;
+          }
+        } while (o);
+      }
+    }
+    const int lm = l >= n ? static_cast<int>(l - n) : static_cast<int>(l);
+    const long long ch = static_cast<long long>(a.cacc[0]);
+    const long long cl = static_cast<long long>(a.cacc[1]);
+    const long long Gh = static_cast<long long>(gh);
+    const long long Gl = static_cast<long long>(gl);
+    const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm]) + ch - Gh;
+    const long long tl = static_cast<long long>(xs[3 * n + k] + xs[3 * n + lm]) + cl - Gl;
+    const long long dh = static_cast<long long>(xs[k] + xs[lm]) - 2 * Gh;
+    const long long dl = static_cast<long long>(xs[n + k] + xs[n + lm]) - 2 * Gl;
+    const __int128 tv = (static_cast<__int128>(th) << a.lo_bits) + tl;
+    const __int128 dv = (static_cast<__int128>(dh) << a.lo_bits) + dl;
+    const Real t = static_cast<Real>(i2_fixed_to_double(tv, a.scale));
+    Real d = static_cast<Real>(i2_fixed_to_double(dv, a.scale));
+    if (a.finalize) d = t == Real(0) ? Real(0) : d / t;
+    const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
+    dist[off] = d;
+    tot[off] = t;
+  }
+  if (a.exec_updates) {
+    for (int off = 16; off > 0; off >>= 1) executed += __shfl_down_sync(0xffffffffu, executed, off);
+    if (lane == 0) atomicAdd(a.exec_updates, executed);
+  }
+}
+
+}  // namespace sf

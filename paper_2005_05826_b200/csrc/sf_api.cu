@@ -5,6 +5,7 @@
 // K1 (embed) -> K2 (stripe update) per chunk, K3 (finalize), copy back.
 #include <cuda_runtime.h>
 
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -16,6 +17,7 @@
 #include <vector>
 
 #include "embed_kernels.cuh"
+#include "isect2_kernels.cuh"
 #include "isect_kernels.cuh"
 #include "sf_common.hpp"
 #include "sparse_kernels.cuh"
@@ -379,6 +381,9 @@ struct DeviceState {
   // intersection (unweighted) path
   DevBuf limbs, dmask, cacc, colsum, occ, base, packed, cubtmp;
   size_t cub_bytes = 0;
+  // intersection v2 (kernel 6): permuted rows, 64-row words, group masks
+  DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm;
+  size_t sort_bytes = 0;
   std::vector<cudaEvent_t> events;
   ~DeviceState() {
     if (dev >= 0) {
@@ -393,8 +398,9 @@ struct sf_plan {
   int metric = 0, prec = 0;
   int32_t n = 0, E = 0, start = 0, stop = 0;
   bool bits = false, exact = false;
-  int kernel = 1;  // 1 dense, 2 sparse-bit walk (3/4 flattened variants), 5 intersection
-  int32_t scale = 0;  // intersection path: limbs hold round(L * 2^scale)
+  int kernel = 1;  // 1 dense, 2 sparse-bit walk (3/4 flattened variants), 5/6 intersection
+  int32_t scale = 0;    // intersection paths: fixed-point lengths round(L * 2^scale)
+  int32_t lo_bits = 32; // kernel 6: value = hi * 2^lo_bits + lo
   int64_t row_words = 0;  // per embedding row: words (bits) or doubles (values)
   Schedule sched;
   std::vector<std::unique_ptr<DeviceState>> devs;
@@ -417,6 +423,11 @@ struct IsectCfg {
   using T = IsectTile<RK, RS, NWK, NWS>;
 };
 
+// Intersection v2 (kernel 6): warp = one u column x 32*RS stripes.
+struct Isect2Cfg {
+  static constexpr int RS = 2, NW = 8;
+};
+
 int64_t sparse_n_ext(int n) {
   const int64_t tile = std::max(SparseCfg::TK + SparseCfg::TS, IsectCfg::T::VW);
   const int64_t need = static_cast<int64_t>(n) + n / 2 + tile + 64;
@@ -428,12 +439,38 @@ size_t nodepacked_bytes(int kernel, int32_t E, int n) {
   const int64_t W = (E + 31) / 32;
   const int64_t G = (W + 31) / 32;
   const int64_t n_ext = sparse_n_ext(n);
-  size_t b = static_cast<size_t>(E) * static_cast<size_t>((n + 31) / 32) * 4 +
-             static_cast<size_t>(W * n_ext) * 4 + static_cast<size_t>(W) * 32 * 8;
+  const size_t rows = static_cast<size_t>(E) * static_cast<size_t>((n + 31) / 32) * 4;
+  if (kernel == 6) {
+    const int64_t W64 = (E + 63) / 64, G64 = (W64 + 31) / 32;
+    return rows + 2 * static_cast<size_t>(W64 * n_ext) * 8 + static_cast<size_t>(G64 * n_ext) * 12 +
+           static_cast<size_t>(G64) * 2048 * 16 + static_cast<size_t>(E) * 32 + static_cast<size_t>(n) * 32;
+  }
+  size_t b = rows + static_cast<size_t>(W * n_ext) * 4 + static_cast<size_t>(W) * 32 * 8;
   if (kernel == 5)
     b += static_cast<size_t>(W * n_ext) * 4 + static_cast<size_t>(G * n_ext) * 8 +
          static_cast<size_t>(G) * 1024 * 8 + static_cast<size_t>(n) * 32;
   return b;
+}
+
+int ceil_log2(int64_t v) {
+  int b = 0;
+  while ((int64_t{1} << b) < v) ++b;
+  return b;
+}
+
+// Kernel 6 fixed point: value = round(L * 2^scale) = hi * 2^lo_bits + lo, with
+// both limb sums over up to E rows below 2^53 (exact in double).
+void isect2_scale(const double* lengths, int32_t E, bool fp32, int32_t* scale, int32_t* lo_bits) {
+  const int cl = ceil_log2(static_cast<int64_t>(E) + 1);
+  const int lb = std::min(32, 53 - cl);
+  const int vb = std::min(63, lb + (53 - cl));
+  double lmax = 0.0;
+  for (int32_t r = 0; r < E; ++r) {
+    const double L = fp32 ? static_cast<double>(static_cast<float>(lengths[r])) : lengths[r];
+    lmax = std::max(lmax, L);
+  }
+  *lo_bits = lb;
+  *scale = lmax > 0.0 ? vb - 1 - std::ilogb(lmax) : 0;
 }
 
 // Fixed-point scale for the intersection path: round(L * 2^q) < 2^63 for the
@@ -476,6 +513,109 @@ sf_status isect_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
                                         static_cast<int64_t>(cells + 1), d.stream));
   d.cub_bytes = tmp;
   SF_TRY(d.cubtmp.alloc(d.dev, tmp, "scan scratch"));
+  return SF_OK;
+}
+
+sf_status isect2_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
+  const int64_t E = plan->E;
+  const int64_t W = (E + 63) / 64;
+  const int64_t G = (W + 31) / 32;
+  const int64_t NGW = (G + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(plan->n);
+  const bool fp32 = plan->prec == SF_FP32;
+  isect2_scale(p->lengths, plan->E, fp32, &plan->scale, &plan->lo_bits);
+  std::vector<unsigned long long> fix(static_cast<size_t>(E));
+  for (int64_t r = 0; r < E; ++r) {
+    const double L = fp32 ? static_cast<double>(static_cast<float>(p->lengths[r])) : p->lengths[r];
+    fix[static_cast<size_t>(r)] = static_cast<unsigned long long>(std::nearbyint(std::ldexp(L, plan->scale)));
+  }
+  SF_TRY(upload(d.fix, d.dev, fix.data(), fix.size(), d.stream, "fixed-point lengths"));
+  SF_TRY(d.keys.alloc(d.dev, static_cast<size_t>(E) * 4, "row keys"));
+  SF_TRY(d.keys_out.alloc(d.dev, static_cast<size_t>(E) * 4, "sorted keys"));
+  SF_TRY(d.vals.alloc(d.dev, static_cast<size_t>(E) * 4, "row ids"));
+  SF_TRY(d.perm.alloc(d.dev, static_cast<size_t>(E) * 4, "row permutation"));
+  SF_TRY(d.dense.alloc(d.dev, static_cast<size_t>(E), "dense flags"));
+  SF_TRY(d.dmask.alloc(d.dev, static_cast<size_t>(W) * 8, "dense-row mask"));
+  SF_TRY(d.limbs.alloc(d.dev, static_cast<size_t>(G) * 2048 * 16, "length limbs"));
+  SF_TRY(d.cacc.alloc(d.dev, 2 * sizeof(unsigned long long), "dense total"));
+  SF_TRY(d.colsum.alloc(d.dev, static_cast<size_t>(plan->n) * 4 * sizeof(unsigned long long), "column sums"));
+  SF_TRY(d.nodebits.alloc(d.dev, static_cast<size_t>(W * n_ext) * 8, "node-packed X words"));
+  const size_t cells = static_cast<size_t>(G * n_ext);
+  SF_TRY(d.occ.alloc(d.dev, cells * 4, "occupancy"));
+  SF_TRY(d.base.alloc(d.dev, (cells + 1) * 4, "packed offsets"));
+  SF_TRY(d.gm.alloc(d.dev, static_cast<size_t>(NGW * n_ext) * 4, "group masks"));
+  SF_TRY(d.packed.alloc(d.dev, static_cast<size_t>(W * n_ext) * 8, "packed words"));
+  if (static_cast<uint64_t>(W * n_ext) >= (1ull << 32))
+    return fail(SF_ENOMEM, "problem too large for 32-bit packed offsets");
+  size_t tmp = 0;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
+                                        static_cast<int64_t>(cells + 1), d.stream));
+  d.cub_bytes = tmp;
+  SF_TRY(d.cubtmp.alloc(d.dev, tmp, "scan scratch"));
+  size_t stmp = 0;
+  SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
+                                          d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
+                                          0, 32, d.stream));
+  d.sort_bytes = stmp;
+  SF_TRY(d.sorttmp.alloc(d.dev, stmp, "sort scratch"));
+  return SF_OK;
+}
+
+// Kernel 6 preparation on device: |S_e|, permutation, X words, occupancy, packing.
+sf_status isect2_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
+  const int n = plan->n;
+  const int64_t E = plan->E;
+  const int64_t W = (E + 63) / 64;
+  const int64_t G = (W + 31) / 32;
+  const int64_t NGW = (G + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(n);
+  const int64_t cells = G * n_ext;
+  const int64_t stride = plan->row_words;
+  // heavy rows: |X_e| >= 0.14 n (SURVEY-style measurement at the EMP shape:
+  // this threshold minimises candidate words per slot)
+  const int heavy_min = std::max(2, static_cast<int>(0.14 * n));
+  SF_CUDA(cudaMemsetAsync(d.dmask.p, 0, static_cast<size_t>(W) * 8, st));
+  SF_CUDA(cudaMemsetAsync(d.cacc.p, 0, 2 * sizeof(unsigned long long), st));
+  SF_CUDA(cudaMemsetAsync(d.colsum.p, 0, static_cast<size_t>(n) * 4 * sizeof(unsigned long long), st));
+  SF_CUDA(cudaMemsetAsync(d.gm.p, 0, static_cast<size_t>(NGW * n_ext) * 4, st));
+  SF_CUDA(cudaMemsetAsync(d.base.as<uint32_t>() + cells, 0, 4, st));
+  i2_row_key_kernel<<<grid_for(E * 32, 256), 256, 0, st>>>(
+      d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min, d.keys.as<uint32_t>(), d.vals.as<int32_t>(),
+      d.dense.as<uint8_t>());
+  size_t stmp = d.sort_bytes;
+  SF_CUDA(cub::DeviceRadixSort::SortPairs(d.sorttmp.p, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
+                                          d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
+                                          0, 32, st));
+  i2_perm_kernel<<<grid_for(G * 2048, 256), 256, 0, st>>>(
+      d.perm.as<int32_t>(), plan->E, G * 2048, d.dense.as<uint8_t>(), d.fix.as<unsigned long long>(),
+      plan->lo_bits, d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.cacc.as<unsigned long long>());
+  i2_transpose_kernel<<<grid_for(W * stride * 32, 256), 256, 0, st>>>(
+      d.emb.as<uint32_t>(), stride, d.perm.as<int32_t>(), plan->E, n, static_cast<int32_t>(W),
+      d.dmask.as<unsigned long long>(), d.nodebits.as<unsigned long long>(), n_ext);
+  i2_extend_kernel<<<grid_for(W * (n_ext - n), 256), 256, 0, st>>>(
+      d.nodebits.as<unsigned long long>(), n_ext, n, static_cast<int32_t>(W));
+  i2_occ_kernel<<<grid_for(cells, 256), 256, 0, st>>>(
+      d.nodebits.as<unsigned long long>(), n_ext, n, static_cast<int32_t>(W), static_cast<int32_t>(G),
+      d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.occ.as<uint32_t>(), d.base.as<uint32_t>(),
+      d.gm.as<uint32_t>(), d.colsum.as<unsigned long long>());
+  size_t tmp = d.cub_bytes;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cubtmp.p, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
+                                        cells + 1, st));
+  i2_pack_kernel<<<grid_for(cells, 256), 256, 0, st>>>(
+      d.nodebits.as<unsigned long long>(), n_ext, static_cast<int32_t>(W), static_cast<int32_t>(G),
+      d.base.as<uint32_t>(), d.packed.as<unsigned long long>());
+  SF_CUDA(cudaGetLastError());
+  plan->stats.launches += 8;  // key, sort, perm, transpose, extend, occupancy, scan, pack
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_isect2(const Isect2Args& a, cudaStream_t st) {
+  using C = Isect2Cfg;
+  auto* kern = stripe_isect2_kernel<Real, C::RS, C::NW>;
+  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
+  kern<<<grid, 32 * C::NW, 0, st>>>(a);
+  SF_CUDA(cudaGetLastError());
   return SF_OK;
 }
 
@@ -633,7 +773,9 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
       SF_CUDA(cudaGetLastError());
       plan->stats.launches++;
     }
-    if (plan->kernel >= 2) {
+    if (plan->kernel == 6) {
+      SF_TRY(isect2_build(plan, d, st));
+    } else if (plan->kernel >= 2) {
       // node-packed presence bits for the sparse walk
       const int64_t W = (plan->E + 31) / 32;
       const int64_t n_ext = sparse_n_ext(n);
@@ -648,7 +790,30 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
     }
     SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
     // ---- K2: stripe update over the chunk's rows
-    if (plan->kernel == 5) {
+    if (plan->kernel == 6) {
+      Isect2Args a;
+      const int64_t W = (plan->E + 63) / 64;
+      a.G = static_cast<int32_t>((W + 31) / 32);
+      a.NGW = (a.G + 31) / 32;
+      a.occ = d.occ.as<uint32_t>();
+      a.base = d.base.as<uint32_t>();
+      a.packed = d.packed.as<unsigned long long>();
+      a.limbs = d.limbs.as<double2>();
+      a.gm = d.gm.as<uint32_t>();
+      a.colsum = d.colsum.as<unsigned long long>();
+      a.cacc = d.cacc.as<unsigned long long>();
+      a.n_ext = sparse_n_ext(n);
+      a.n = n;
+      a.s_begin = d.a;
+      a.s_end = d.b;
+      a.lo_bits = plan->lo_bits;
+      a.scale = plan->scale;
+      a.finalize = finalize ? 1 : 0;
+      a.dist = d.dist.p;
+      a.tot = d.tot.p;
+      a.exec_updates = d.exec_ctr.as<unsigned long long>();
+      SF_TRY(plan->prec == SF_FP64 ? launch_isect2<double>(a, st) : launch_isect2<float>(a, st));
+    } else if (plan->kernel == 5) {
       IsectArgs a;
       a.occ = d.occ.as<uint32_t>();
       a.base = d.base.as<uint32_t>();
@@ -722,7 +887,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
   }
   const size_t ne = d.events.size();
   SF_CUDA(cudaEventRecord(d.events[ne - 2], st));
-  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED && plan->kernel != 5) {
+  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED && plan->kernel < 5) {
     const int blocks = grid_for(slots, 256);
     if (plan->prec == SF_FP64)
       finalize_kernel<double><<<blocks, 256, 0, st>>>(d.dist.as<double>(), d.tot.as<double>(), slots);
@@ -778,7 +943,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stop = stop;
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
-  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 5) ? ex->kernel : 1;
+  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 6) ? ex->kernel : 1;
   const int n = p->n_samples;
   // auto, unweighted: the intersection kernel (exact fixed-point sums), or
   // with SF_EXEC_EXACT_NO_FMA the sparse walk (the reference's adds in the
@@ -853,8 +1018,12 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       SF_TRY(upload_schedule(d, plan->sched));
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(plan->E) * row_bytes, "embedding rows"));
       SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));
-      SF_TRY(sparse_prepare(plan.get(), d, p));
-      if (plan->kernel == 5) SF_TRY(isect_prepare(plan.get(), d, p));
+      if (plan->kernel == 6) {
+        SF_TRY(isect2_prepare(plan.get(), d, p));
+      } else {
+        SF_TRY(sparse_prepare(plan.get(), d, p));
+        if (plan->kernel == 5) SF_TRY(isect_prepare(plan.get(), d, p));
+      }
     } else {
       SF_TRY(upload_schedule(d, plan->sched));
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(cmax) * row_bytes, "embedding chunk"));

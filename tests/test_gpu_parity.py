@@ -26,7 +26,7 @@ from paper_2005_05826_b200 import stripefrac as sf
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4, N.KERNEL_ISECT]  # 3/4: flattened sparse walk
+KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4, N.KERNEL_ISECT, N.KERNEL_ISECT2]  # 3/4: flattened walk
 WALKS = (N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4)
 
 
@@ -338,8 +338,9 @@ def _exact_stripes(problem, prec, start, stop):
     return d, t
 
 
+@pytest.mark.parametrize("kernel", [N.KERNEL_ISECT, N.KERNEL_ISECT2])
 @pytest.mark.parametrize("prec", [8, 4])
-def test_isect_is_exact(device_ok, prec):
+def test_isect_is_exact(device_ok, prec, kernel):
     """Kernel 5 returns the correctly rounded exact sums (raw, unfinalized),
     on instances with sparse and dense (complemented) rows, wrap, odd/even n
     and partial ranges."""
@@ -352,7 +353,7 @@ def test_isect_is_exact(device_ok, prec):
             if start >= stop:
                 continue
             wd, wt = _exact_stripes(problem, prec, start, stop)
-            d, t, _ = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_ISECT, finalize=False)
+            d, t, _ = _gpu_stripes(problem, 1, prec, start, stop, kernel, finalize=False)
             if prec == 8:
                 assert np.array_equal(d, wd) and np.array_equal(t, wt)
             else:  # fp32: rounded via fp64 (double rounding can move 1 ulp)
@@ -360,8 +361,9 @@ def test_isect_is_exact(device_ok, prec):
                 assert np.all(np.abs(t.astype(np.float64) - wt) <= np.spacing(np.abs(wt).astype(np.float32)))
 
 
+@pytest.mark.parametrize("kernel", [N.KERNEL_ISECT, N.KERNEL_ISECT2])
 @pytest.mark.parametrize("prec", [8, 4])
-def test_isect_matches_oracle_larger(device_ok, prec):
+def test_isect_matches_oracle_larger(device_ok, prec, kernel):
     """Kernel 5 vs the CPU restatement of the reference (sequential sums) on
     instances spanning several CTA tiles and 1024-row groups."""
     for seed, n, leaves, dens, subset in [(61, 300, 1500, 0.01, 0), (62, 517, 2500, 0.004, 2000),
@@ -371,7 +373,7 @@ def test_isect_matches_oracle_larger(device_ok, prec):
         S = n // 2
         for start, stop in [(0, S), (S // 3, S - 1)]:
             wd, wt = op.compute_stripes(problem, 1, prec, start, stop)
-            d, t, st = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_ISECT)
-            _assert_close(1, prec, False, d, wd, N.KERNEL_ISECT)
-            _assert_close(1, prec, False, t, wt, N.KERNEL_ISECT)
+            d, t, st = _gpu_stripes(problem, 1, prec, start, stop, kernel)
+            _assert_close(1, prec, False, d, wd, kernel)
+            _assert_close(1, prec, False, t, wt, kernel)
             assert st.updates_alg == problem.n_rows * (stop - start) * n
