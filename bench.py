@@ -167,7 +167,7 @@ def run_ours(args, cfg):
     stop_all = min(S, args.stripes) if args.stripes else S
     a = int(stop_all * rank // world)
     b = int(stop_all * (rank + 1) // world)
-    kernel = {"auto": 0, "dense": 1, "sparse": 2, "flat32": 3, "flat64": 4, "isect": 5, "isect2": 6}[args.kernel]
+    kernel = {"auto": 0, "dense": 1, "sparse": 2, "flat32": 3, "flat64": 4, "isect": 5, "isect2": 6, "isect3": 7, "isect4": 8, "isect5": 9, "split": 10}[args.kernel]
     ex, _keep = N.make_exec([local], kernel)
     plan = C.c_void_p()
     t0 = time.perf_counter()
@@ -179,27 +179,28 @@ def run_ours(args, cfg):
         N.check(L.sf_plan_run(plan, 1))
         N.check(L.sf_plan_sync(plan))
         N.check(L.sf_plan_stats(plan, C.byref(st)))
-        return st.total_ms, st.stripe_ms, st.embed_ms, st.updates_exec, st.launches
+        return st.total_ms, st.stripe_ms, st.embed_ms, st.updates_exec, st.launches, st.fp64_ops
 
     for i in range(args.warmup):
         r = one_step()
-        log(f"rank {rank}: warmup {i}: {r[0]:.1f} ms (stripe {r[1]:.1f}, embed {r[2]:.1f})")
+        log(f"rank {rank}: warmup {i}: {r[0]:.1f} ms (stripe {r[1]:.1f}, prep {r[2]:.1f})")
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
     barrier()
-    dev_ms, str_ms, emb_ms, uexec, launches = [], [], [], 0, 0
+    dev_ms, str_ms, emb_ms, uexec, launches, fp64_ops = [], [], [], 0, 0, 0
     with ClockSampler(local) as clocks:
         w0 = time.perf_counter()
         for _ in range(args.steps):
-            tms, sms, ems, ue, ln = one_step()
+            tms, sms, ems, ue, ln, fo = one_step()
             dev_ms.append(tms)
             str_ms.append(sms)
             emb_ms.append(ems)
             uexec += ue
             launches += ln
+            fp64_ops += fo
         barrier()
         wall = time.perf_counter() - w0
     total_dev_s = sum(dev_ms) / 1e3
@@ -254,19 +255,36 @@ def run_ours(args, cfg):
     # ---- roofline of the dominant kernel (K2 stripe update)
     peak_fma = measured_fp_peak(local, cfg["precision"])
     stripe_s = sum(str_ms) / 1e3
-    fl = FLOPS_PER_UPDATE[metric]
-    achieved_tf = (uexec / max(world, 1) if world > 1 else uexec) * fl / stripe_s / 1e12 if stripe_s else 0.0
     peak_tf = peak_fma * 2 / 1e12
-    roofline = {
-        "bound": "fp64" if prec == 8 else "fp32",
-        "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3), "unit": "TFLOP/s",
-        "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None, "traffic": None,
-        "kernel": "stripe_dense_kernel" if kernel != 2 else "stripe_sparse_kernel",
-        "peak_source": "measured DFMA/FFMA loop (tools/fp_peaks.cu) on this device",
-        "flops_per_update": fl, "updates_exec_per_step": int(uexec_all / args.steps),
-        "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
-        "embed_ms_per_step": round(sum(emb_ms) / args.steps, 3),
-    }
+    if metric == 1 and fp64_ops > 0:
+        # split kernel (10): the heavy walk issues 2 DFMA (4 flops) per u bit per
+        # live slot; the kernel counts them (stats.fp64_ops = DFMA lane-ops)
+        achieved_tf = fp64_ops * 2 / stripe_s / 1e12 if stripe_s else 0.0
+        roofline = {
+            "bound": "fp64", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
+            "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None,
+            "traffic": None, "kernel": "stripe_split_kernel (heavy-row walk)",
+            "peak_source": "measured DFMA loop (tools/fp_peaks.cu) on this device, x2 flops/FMA",
+            "work": "fp64_ops = DFMA lane-ops counted by the kernel (2 per u bit per live slot)",
+            "dfma_per_step": int(fp64_ops / args.steps),
+            "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
+            "prep_ms_per_step": round(sum(emb_ms) / args.steps, 3),
+            "algorithmic_speedup_vs_dense_fp64_roofline": round(
+                (E * stop_all * n * args.steps / (sum(dev_ms) / 1e3)) / (peak_fma / 4), 2),
+        }
+    else:
+        fl = FLOPS_PER_UPDATE[metric]
+        achieved_tf = (uexec / max(world, 1) if world > 1 else uexec) * fl / stripe_s / 1e12 if stripe_s else 0.0
+        roofline = {
+            "bound": "fp64" if prec == 8 else "fp32",
+            "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3), "unit": "TFLOP/s",
+            "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None, "traffic": None,
+            "kernel": "stripe_dense_kernel" if kernel == 1 else "stripe walk",
+            "peak_source": "measured DFMA/FFMA loop (tools/fp_peaks.cu) on this device",
+            "flops_per_update": fl, "updates_exec_per_step": int(uexec_all / args.steps),
+            "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
+            "embed_ms_per_step": round(sum(emb_ms) / args.steps, 3),
+        }
 
     # ---- CPU baseline (oracle restatement, bounded sample, all host threads)
     cpu = None
@@ -368,7 +386,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--kernel", choices=["auto", "dense", "sparse", "flat32", "flat64", "isect", "isect2"],
+    ap.add_argument("--kernel", choices=["auto", "dense", "sparse", "flat32", "flat64", "isect", "isect2", "isect3", "isect4", "isect5", "split"],
                     default="auto")
     ap.add_argument("--stripes", type=int, default=0, help="limit to stripes [0, N) (debug)")
     ap.add_argument("--e2e-steps", type=int, default=1)

@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 1
+#define SF_ABI_VERSION 2
 
 typedef enum sf_status {
   SF_OK = 0,
@@ -72,10 +72,12 @@ typedef struct sf_exec {
   int32_t n_devices;        /* devices to shard stripes over; 0 = all visible */
   const int32_t* devices;   /* explicit ordinals, or NULL for 0..n_devices-1 */
   int64_t mem_budget_bytes; /* per-device cap for embedding chunks; 0 = auto */
-  int32_t kernel;           /* 0 = auto, 1 = dense tiled, 2 = sparse bit walk (unweighted only,
-                               bitwise), 5 = intersection (unweighted only, exact fixed-point sums) */
+  int32_t kernel;           /* 0 = auto, 1 = dense tiled; unweighted only: 2 = sparse bit walk
+                               (bitwise; 3/4 flattened variants), 5-9 = intersection walks and
+                               10 = split heavy-walk/light-scatter (exact fixed-point sums; the
+                               default) */
   int32_t flags;            /* bit 0: SF_EXEC_EXACT_NO_FMA: bitwise-identical results (weighted:
-                               no FMA; unweighted auto: the sparse walk instead of kernel 5) */
+                               no FMA; unweighted auto: the sparse walk instead of kernel 10) */
 } sf_exec;
 
 #define SF_EXEC_EXACT_NO_FMA 1
@@ -90,6 +92,7 @@ typedef struct sf_stats {
   double stripe_ms;      /* device time of the stripe kernels (max over devices) */
   double finalize_ms;    /* device time of finalize (max over devices) */
   double total_ms;       /* device time of the whole run (max over devices) */
+  uint64_t fp64_ops;     /* FP instructions x lanes the stripe kernel issued (kernel 9; else 0) */
 } sf_stats;
 
 /* ---- library ------------------------------------------------------------ */

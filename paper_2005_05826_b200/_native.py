@@ -17,7 +17,7 @@ SF_OK, SF_EINVAL, SF_ENOMEM, SF_ECUDA, SF_ESTATE = 0, 1, 2, 3, 4
 SF_UNWEIGHTED, SF_WEIGHTED_UNNORMALIZED, SF_WEIGHTED_NORMALIZED = 1, 2, 3
 SF_FP32, SF_FP64 = 4, 8
 SF_EXEC_EXACT_NO_FMA = 1
-KERNEL_AUTO, KERNEL_DENSE, KERNEL_SPARSE, KERNEL_ISECT, KERNEL_ISECT2 = 0, 1, 2, 5, 6
+KERNEL_AUTO, KERNEL_DENSE, KERNEL_SPARSE, KERNEL_ISECT, KERNEL_ISECT2, KERNEL_ISECT3, KERNEL_ISECT4, KERNEL_ISECT5, KERNEL_SPLIT = 0, 1, 2, 5, 6, 7, 8, 9, 10
 
 
 class sf_problem(C.Structure):
@@ -55,6 +55,7 @@ class sf_stats(C.Structure):
         ("stripe_ms", C.c_double),
         ("finalize_ms", C.c_double),
         ("total_ms", C.c_double),
+        ("fp64_ops", C.c_uint64),
     ]
 
     def as_dict(self) -> dict:

@@ -27,8 +27,6 @@ NVCC_FLAGS = [
     "-Xptxas", "-warn-spills",
 ]
 SOURCES = ["sf_api.cu", "host_prep.cpp"]
-HEADERS = ["sf_common.hpp", "embed_kernels.cuh", "stripe_kernels.cuh", "sparse_kernels.cuh", "isect2_kernels.cuh",
-           "isect_kernels.cuh"]
 
 
 def _nvcc() -> str:
@@ -46,7 +44,8 @@ def _stale(target: Path, deps) -> bool:
 
 
 def build_native(force: bool = False, verbose: bool = False) -> Path:
-    deps = [CSRC / s for s in SOURCES + HEADERS] + list((ROOT / "include").glob("*.h"))
+    deps = ([CSRC / s for s in SOURCES] + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.hpp")) +
+            list((ROOT / "include").glob("*.h")))
     if force or _stale(LIB, deps):
         cmd = [_nvcc(), *NVCC_FLAGS, f"-I{ROOT / 'include'}", f"-I{CSRC}",
                *[str(CSRC / s) for s in SOURCES], "-o", str(LIB)]

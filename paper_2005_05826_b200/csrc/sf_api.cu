@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <memory>
@@ -19,6 +20,7 @@
 #include "embed_kernels.cuh"
 #include "isect2_kernels.cuh"
 #include "isect_kernels.cuh"
+#include "split_kernels.cuh"
 #include "sf_common.hpp"
 #include "sparse_kernels.cuh"
 #include "stripe_kernels.cuh"
@@ -382,7 +384,9 @@ struct DeviceState {
   DevBuf limbs, dmask, cacc, colsum, occ, base, packed, cubtmp;
   size_t cub_bytes = 0;
   // intersection v2 (kernel 6): permuted rows, 64-row words, group masks
-  DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm;
+  DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm, nheavy;
+  // split path (kernel 10): light-row sums per slot
+  DevBuf lightsum;
   size_t sort_bytes = 0;
   std::vector<cudaEvent_t> events;
   ~DeviceState() {
@@ -427,6 +431,29 @@ struct IsectCfg {
 struct Isect2Cfg {
   static constexpr int RS = 2, NW = 8;
 };
+// Intersection v3 (kernel 7): heavy region walked warp-uniformly.
+struct Isect3Cfg {
+  static constexpr int RS = 4, NW = 8;
+};
+// Intersection v4 (kernel 8): heavy and light regions walked warp-uniformly.
+struct Isect4Cfg {
+  static constexpr int RS = 4, NW = 8;
+};
+// Intersection v5 (kernel 9): FP64-bound heavy walk down to |X| >= 0.012 n.
+struct Isect5Cfg {
+  static constexpr int RS = 8, NW = 8;
+};
+// Split (kernel 10): heavy rows walked warp-uniformly, light rows scattered.
+struct SplitCfg {
+  static constexpr int RS = 8, NW = 8, SCATTER_NW = 8;
+};
+
+// |X_e| threshold of the split path: rows at or above it are walked.
+int split_heavy_min(int n) {
+  double frac = 0.01;
+  if (const char* e = std::getenv("SF_HEAVY_FRAC")) frac = std::atof(e);
+  return std::max(2, static_cast<int>(frac * n));
+}
 
 int64_t sparse_n_ext(int n) {
   const int64_t tile = std::max(SparseCfg::TK + SparseCfg::TS, IsectCfg::T::VW);
@@ -440,7 +467,12 @@ size_t nodepacked_bytes(int kernel, int32_t E, int n) {
   const int64_t G = (W + 31) / 32;
   const int64_t n_ext = sparse_n_ext(n);
   const size_t rows = static_cast<size_t>(E) * static_cast<size_t>((n + 31) / 32) * 4;
-  if (kernel == 6) {
+  if (kernel == 10) {  // + the light sums, (stripes x n) x 16 B, counted by the caller with stripes
+    const int64_t W64 = (E + 63) / 64, G64 = (W64 + 31) / 32;
+    return rows + static_cast<size_t>(W64 * n_ext) * 8 + static_cast<size_t>(G64) * 2048 * 16 +
+           static_cast<size_t>(E) * 32 + static_cast<size_t>(n) * 32;
+  }
+  if (kernel >= 6) {
     const int64_t W64 = (E + 63) / 64, G64 = (W64 + 31) / 32;
     return rows + 2 * static_cast<size_t>(W64 * n_ext) * 8 + static_cast<size_t>(G64 * n_ext) * 12 +
            static_cast<size_t>(G64) * 2048 * 16 + static_cast<size_t>(E) * 32 + static_cast<size_t>(n) * 32;
@@ -535,23 +567,26 @@ sf_status isect2_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
   SF_TRY(d.vals.alloc(d.dev, static_cast<size_t>(E) * 4, "row ids"));
   SF_TRY(d.perm.alloc(d.dev, static_cast<size_t>(E) * 4, "row permutation"));
   SF_TRY(d.dense.alloc(d.dev, static_cast<size_t>(E), "dense flags"));
+  SF_TRY(d.nheavy.alloc(d.dev, 4, "heavy row count"));
   SF_TRY(d.dmask.alloc(d.dev, static_cast<size_t>(W) * 8, "dense-row mask"));
   SF_TRY(d.limbs.alloc(d.dev, static_cast<size_t>(G) * 2048 * 16, "length limbs"));
   SF_TRY(d.cacc.alloc(d.dev, 2 * sizeof(unsigned long long), "dense total"));
   SF_TRY(d.colsum.alloc(d.dev, static_cast<size_t>(plan->n) * 4 * sizeof(unsigned long long), "column sums"));
   SF_TRY(d.nodebits.alloc(d.dev, static_cast<size_t>(W * n_ext) * 8, "node-packed X words"));
-  const size_t cells = static_cast<size_t>(G * n_ext);
-  SF_TRY(d.occ.alloc(d.dev, cells * 4, "occupancy"));
-  SF_TRY(d.base.alloc(d.dev, (cells + 1) * 4, "packed offsets"));
-  SF_TRY(d.gm.alloc(d.dev, static_cast<size_t>(NGW * n_ext) * 4, "group masks"));
-  SF_TRY(d.packed.alloc(d.dev, static_cast<size_t>(W * n_ext) * 8, "packed words"));
-  if (static_cast<uint64_t>(W * n_ext) >= (1ull << 32))
-    return fail(SF_ENOMEM, "problem too large for 32-bit packed offsets");
-  size_t tmp = 0;
-  SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
-                                        static_cast<int64_t>(cells + 1), d.stream));
-  d.cub_bytes = tmp;
-  SF_TRY(d.cubtmp.alloc(d.dev, tmp, "scan scratch"));
+  if (plan->kernel != 10) {  // kernels 6-9 walk packed words through occupancy masks
+    const size_t cells = static_cast<size_t>(G * n_ext);
+    SF_TRY(d.occ.alloc(d.dev, cells * 4, "occupancy"));
+    SF_TRY(d.base.alloc(d.dev, (cells + 1) * 4, "packed offsets"));
+    SF_TRY(d.gm.alloc(d.dev, static_cast<size_t>(NGW * n_ext) * 4, "group masks"));
+    SF_TRY(d.packed.alloc(d.dev, static_cast<size_t>(W * n_ext) * 8, "packed words"));
+    if (static_cast<uint64_t>(W * n_ext) >= (1ull << 32))
+      return fail(SF_ENOMEM, "problem too large for 32-bit packed offsets");
+    size_t tmp = 0;
+    SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
+                                          static_cast<int64_t>(cells + 1), d.stream));
+    d.cub_bytes = tmp;
+    SF_TRY(d.cubtmp.alloc(d.dev, tmp, "scan scratch"));
+  }
   size_t stmp = 0;
   SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
                                           d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
@@ -573,7 +608,11 @@ sf_status isect2_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   const int64_t stride = plan->row_words;
   // heavy rows: |X_e| >= 0.14 n (SURVEY-style measurement at the EMP shape:
   // this threshold minimises candidate words per slot)
-  const int heavy_min = std::max(2, static_cast<int>(0.14 * n));
+  // kernel 6: 0.14 n minimises candidate words per slot; kernel 7 walks
+  // the heavy region warp-uniformly, which pays off down to ~0.06 n
+  const double heavy_frac = plan->kernel >= 9 ? 0.012 : plan->kernel >= 7 ? 0.06 : 0.14;
+  const int heavy_min = std::max(2, static_cast<int>(heavy_frac * n));
+  SF_CUDA(cudaMemsetAsync(d.nheavy.p, 0, 4, st));
   SF_CUDA(cudaMemsetAsync(d.dmask.p, 0, static_cast<size_t>(W) * 8, st));
   SF_CUDA(cudaMemsetAsync(d.cacc.p, 0, 2 * sizeof(unsigned long long), st));
   SF_CUDA(cudaMemsetAsync(d.colsum.p, 0, static_cast<size_t>(n) * 4 * sizeof(unsigned long long), st));
@@ -581,7 +620,7 @@ sf_status isect2_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   SF_CUDA(cudaMemsetAsync(d.base.as<uint32_t>() + cells, 0, 4, st));
   i2_row_key_kernel<<<grid_for(E * 32, 256), 256, 0, st>>>(
       d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min, d.keys.as<uint32_t>(), d.vals.as<int32_t>(),
-      d.dense.as<uint8_t>());
+      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>());
   size_t stmp = d.sort_bytes;
   SF_CUDA(cub::DeviceRadixSort::SortPairs(d.sorttmp.p, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
                                           d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
@@ -606,6 +645,94 @@ sf_status isect2_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
       d.base.as<uint32_t>(), d.packed.as<unsigned long long>());
   SF_CUDA(cudaGetLastError());
   plan->stats.launches += 8;  // key, sort, perm, transpose, extend, occupancy, scan, pack
+  return SF_OK;
+}
+
+sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
+  const int n = plan->n;
+  const int64_t E = plan->E;
+  const int64_t W = (E + 63) / 64;
+  const int64_t G = (W + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(n);
+  const int64_t stride = plan->row_words;
+  const int heavy_min = split_heavy_min(n);
+  const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
+  SF_CUDA(cudaMemsetAsync(d.dmask.p, 0, static_cast<size_t>(W) * 8, st));
+  SF_CUDA(cudaMemsetAsync(d.cacc.p, 0, 2 * sizeof(unsigned long long), st));
+  SF_CUDA(cudaMemsetAsync(d.colsum.p, 0, static_cast<size_t>(n) * 4 * sizeof(unsigned long long), st));
+  SF_CUDA(cudaMemsetAsync(d.nheavy.p, 0, 4, st));
+  SF_CUDA(cudaMemsetAsync(d.lightsum.p, 0, slots * 16, st));
+  i2_row_key_kernel<<<grid_for(E * 32, 256), 256, 0, st>>>(
+      d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min, d.keys.as<uint32_t>(), d.vals.as<int32_t>(),
+      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>());
+  size_t stmp = d.sort_bytes;
+  SF_CUDA(cub::DeviceRadixSort::SortPairs(d.sorttmp.p, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
+                                          d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
+                                          0, 32, st));
+  i2_perm_kernel<<<grid_for(G * 2048, 256), 256, 0, st>>>(
+      d.perm.as<int32_t>(), plan->E, G * 2048, d.dense.as<uint8_t>(), d.fix.as<unsigned long long>(),
+      plan->lo_bits, d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.cacc.as<unsigned long long>());
+  sp_transpose_kernel<<<grid_for(W * stride * 32, 256), 256, 0, st>>>(
+      d.emb.as<uint32_t>(), stride, d.perm.as<int32_t>(), d.nheavy.as<unsigned int>(), n,
+      d.dmask.as<unsigned long long>(), d.nodebits.as<unsigned long long>(), n_ext);
+  sp_extend_kernel<<<grid_for(W * (n_ext - n), 256), 256, 0, st>>>(
+      d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>());
+  sp_heavy_colsum_kernel<<<grid_for(n, 128), 128, 0, st>>>(
+      d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>(),
+      d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.colsum.as<unsigned long long>());
+  {
+    constexpr int NW = SplitCfg::SCATTER_NW;
+    const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
+    auto* kern = sp_light_scatter_kernel<NW>;
+    SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const int blocks = static_cast<int>(std::min<int64_t>((E + NW - 1) / NW, 148 * 16));
+    kern<<<blocks, 32 * NW, smem, st>>>(d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min,
+                                       d.fix.as<unsigned long long>(), plan->lo_bits, d.a, d.b,
+                                       d.lightsum.as<double>(), d.colsum.as<unsigned long long>(),
+                                       d.exec_ctr.as<unsigned long long>(), heavy_min);
+  }
+  SF_CUDA(cudaGetLastError());
+  plan->stats.launches += 8;  // key, sort, perm, transpose, extend, colsum, scatter (+ memsets)
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
+  using C = SplitCfg;
+  auto* kern = stripe_split_kernel<Real, C::RS, C::NW>;
+  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
+  kern<<<grid, 32 * C::NW, 0, st>>>(a);
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_isect5(const Isect2Args& a, unsigned long long* fp_ops, cudaStream_t st) {
+  using C = Isect5Cfg;
+  auto* kern = stripe_isect5_kernel<Real, C::RS, C::NW>;
+  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
+  kern<<<grid, 32 * C::NW, 0, st>>>(a, fp_ops);
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_isect4(const Isect2Args& a, cudaStream_t st) {
+  using C = Isect4Cfg;
+  auto* kern = stripe_isect4_kernel<Real, C::RS, C::NW>;
+  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
+  kern<<<grid, 32 * C::NW, 0, st>>>(a);
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_isect3(const Isect2Args& a, cudaStream_t st) {
+  using C = Isect3Cfg;
+  auto* kern = stripe_isect3_kernel<Real, C::RS, C::NW>;
+  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
+  kern<<<grid, 32 * C::NW, 0, st>>>(a);
+  SF_CUDA(cudaGetLastError());
   return SF_OK;
 }
 
@@ -730,7 +857,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
   SF_CUDA(cudaMemsetAsync(d.dist.p, 0, static_cast<size_t>(slots) * w, st));
   if (d.tot.p && plan->metric != SF_WEIGHTED_UNNORMALIZED)
     SF_CUDA(cudaMemsetAsync(d.tot.p, 0, static_cast<size_t>(slots) * w, st));
-  SF_CUDA(cudaMemsetAsync(d.exec_ctr.p, 0, sizeof(unsigned long long), st));
+  SF_CUDA(cudaMemsetAsync(d.exec_ctr.p, 0, 2 * sizeof(unsigned long long), st));
 
   const int64_t stride = plan->row_words;
   const int ncols = static_cast<int>(plan->bits ? (n + 31) / 32 : n);
@@ -773,7 +900,9 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
       SF_CUDA(cudaGetLastError());
       plan->stats.launches++;
     }
-    if (plan->kernel == 6) {
+    if (plan->kernel == 10) {
+      SF_TRY(split_build(plan, d, st));
+    } else if (plan->kernel >= 6) {
       SF_TRY(isect2_build(plan, d, st));
     } else if (plan->kernel >= 2) {
       // node-packed presence bits for the sparse walk
@@ -790,9 +919,31 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
     }
     SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
     // ---- K2: stripe update over the chunk's rows
-    if (plan->kernel == 6) {
+    if (plan->kernel == 10) {
+      SplitArgs a;
+      a.nx = d.nodebits.as<unsigned long long>();
+      a.limbs = d.limbs.as<double2>();
+      a.n_heavy = d.nheavy.as<unsigned int>();
+      a.gl = d.lightsum.as<double>();
+      a.colsum = d.colsum.as<unsigned long long>();
+      a.cacc = d.cacc.as<unsigned long long>();
+      a.n_ext = sparse_n_ext(n);
+      a.n = n;
+      a.s_begin = d.a;
+      a.s_end = d.b;
+      a.lo_bits = plan->lo_bits;
+      a.scale = plan->scale;
+      a.finalize = finalize ? 1 : 0;
+      a.dist = d.dist.p;
+      a.tot = d.tot.p;
+      a.counters = d.exec_ctr.as<unsigned long long>();
+      SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+    } else if (plan->kernel >= 6) {
       Isect2Args a;
       const int64_t W = (plan->E + 63) / 64;
+      a.W = static_cast<int32_t>(W);
+      a.nx = d.nodebits.as<unsigned long long>();
+      a.n_heavy = d.nheavy.as<unsigned int>();
       a.G = static_cast<int32_t>((W + 31) / 32);
       a.NGW = (a.G + 31) / 32;
       a.occ = d.occ.as<uint32_t>();
@@ -812,7 +963,15 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
       a.dist = d.dist.p;
       a.tot = d.tot.p;
       a.exec_updates = d.exec_ctr.as<unsigned long long>();
-      SF_TRY(plan->prec == SF_FP64 ? launch_isect2<double>(a, st) : launch_isect2<float>(a, st));
+      if (plan->kernel == 9)
+        SF_TRY(plan->prec == SF_FP64 ? launch_isect5<double>(a, d.exec_ctr.as<unsigned long long>() + 1, st)
+                                     : launch_isect5<float>(a, d.exec_ctr.as<unsigned long long>() + 1, st));
+      else if (plan->kernel == 8)
+        SF_TRY(plan->prec == SF_FP64 ? launch_isect4<double>(a, st) : launch_isect4<float>(a, st));
+      else if (plan->kernel == 7)
+        SF_TRY(plan->prec == SF_FP64 ? launch_isect3<double>(a, st) : launch_isect3<float>(a, st));
+      else
+        SF_TRY(plan->prec == SF_FP64 ? launch_isect2<double>(a, st) : launch_isect2<float>(a, st));
     } else if (plan->kernel == 5) {
       IsectArgs a;
       a.occ = d.occ.as<uint32_t>();
@@ -943,14 +1102,14 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stop = stop;
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
-  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 6) ? ex->kernel : 1;
+  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 10) ? ex->kernel : 1;
   const int n = p->n_samples;
   // auto, unweighted: the intersection kernel (exact fixed-point sums), or
   // with SF_EXEC_EXACT_NO_FMA the sparse walk (the reference's adds in the
   // reference's order: bitwise identical); both keep every row resident, so
   // a budget too small for that selects the chunked dense kernel.
   if ((!ex || ex->kernel == 0) && metric == SF_UNWEIGHTED) {
-    const int k = plan->exact ? 2 : 5;
+    const int k = plan->exact ? 2 : 10;
     const bool fits = !(ex && ex->mem_budget_bytes > 0) ||
                       nodepacked_bytes(k, p->n_rows, n) <= static_cast<size_t>(ex->mem_budget_bytes);
     plan->kernel = fits ? k : 1;
@@ -1013,13 +1172,16 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
     SF_TRY(d.dist.alloc(d.dev, slots * w, "distances"));
     if (has_t) SF_TRY(d.tot.alloc(d.dev, slots * w, "totals"));
-    SF_TRY(d.exec_ctr.alloc(d.dev, sizeof(unsigned long long), "counter"));
+    SF_TRY(d.exec_ctr.alloc(d.dev, 2 * sizeof(unsigned long long), "counters"));
     if (plan->kernel >= 2) {
       SF_TRY(upload_schedule(d, plan->sched));
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(plan->E) * row_bytes, "embedding rows"));
       SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));
-      if (plan->kernel == 6) {
+      if (plan->kernel >= 6) {
         SF_TRY(isect2_prepare(plan.get(), d, p));
+        if (plan->kernel == 10)
+          SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n) * 16,
+                                  "light-row sums"));
       } else {
         SF_TRY(sparse_prepare(plan.get(), d, p));
         if (plan->kernel == 5) SF_TRY(isect_prepare(plan.get(), d, p));
@@ -1047,7 +1209,7 @@ sf_status sf_plan_run(sf_plan* plan, int32_t finalize) {
 sf_status sf_plan_sync(sf_plan* plan) {
   if (!plan) return fail(SF_EINVAL, "plan is null");
   double emb = 0, str = 0, fin = 0, tot = 0;
-  uint64_t exec = 0;
+  uint64_t exec = 0, fpops = 0;
   for (auto& dp : plan->devs) {
     DeviceState& d = *dp;
     SF_CUDA(cudaSetDevice(d.dev));
@@ -1071,15 +1233,17 @@ sf_status sf_plan_sync(sf_plan* plan) {
     str = std::max(str, s_ms);
     fin = std::max(fin, f_ms);
     tot = std::max(tot, t_ms);
-    unsigned long long c = 0;
-    SF_CUDA(cudaMemcpy(&c, d.exec_ctr.p, sizeof(c), cudaMemcpyDeviceToHost));
-    exec += c;
+    unsigned long long c[2] = {0, 0};
+    SF_CUDA(cudaMemcpy(c, d.exec_ctr.p, sizeof(c), cudaMemcpyDeviceToHost));
+    exec += c[0];
+    fpops += c[1];
   }
   plan->stats.embed_ms = emb;
   plan->stats.stripe_ms = str;
   plan->stats.finalize_ms = fin;
   plan->stats.total_ms = tot;
   plan->stats.updates_exec = exec;
+  plan->stats.fp64_ops = fpops;
   plan->stats.updates_alg = static_cast<uint64_t>(plan->E) * static_cast<uint64_t>(plan->stop - plan->start) *
                             static_cast<uint64_t>(plan->n);
   return SF_OK;

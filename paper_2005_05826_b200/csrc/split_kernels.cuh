@@ -1,0 +1,349 @@
+// K2-UW, split form (kernel 10, the default for the unweighted metric).
+//
+// Same exact algebra as isect_kernels.cuh: with X_e = S_e, or its complement
+// when |S_e| > n/2, and fixed-point lengths (hi, lo limbs),
+//   t_kl = p_k + p_l + C - G_kl,   d_kl = x_k + x_l - 2 G_kl,
+//   G_kl = sum_{e: k in X_e and l in X_e} L_e.
+// The rows are split by |X_e| at heavy_min (~0.01 n):
+//
+//  * HEAVY rows (|X_e| >= heavy_min, ~15% of rows at the EMP shape, ~99% of
+//    the shared rows): permuted to the front, node-packed in 64-row X-words
+//    nx[w][c]. A warp owns one u column k and 32*RS consecutive v columns;
+//    it walks the bits of its u words (uniform control flow) and every lane
+//    adds the row's limbs into each of its RS slots whose v word has that bit,
+//    as DFMA with a 0/1 factor: 2 FP64 instructions per u bit per slot, no
+//    divergence. The walk is FP64-pipe bound by construction.
+//  * LIGHT rows (|X_e| < heavy_min): a slot shares only ~5-10 of them, but
+//    finding them by walking per slot costs far more than they carry. They are
+//    scattered instead: one warp per light row lists its members and adds the
+//    row's limbs to every member pair's slot with atomicAdd on fp64. Every
+//    value added is an integer below 2^53 and so is every partial sum, so the
+//    atomics are exact and the result does not depend on their order.
+//
+// The heavy kernel's epilogue adds the light sums and forms t, d (and d/t).
+#pragma once
+
+#include <cstdint>
+
+#include "isect2_kernels.cuh"
+
+namespace sf {
+
+// (hi, lo) limbs of fixed-point length v, as exactly representable doubles.
+__device__ __forceinline__ double2 limbs_of(unsigned long long v, int lo_bits) {
+  return make_double2(static_cast<double>(v >> lo_bits),
+                      static_cast<double>(v & ((1ull << lo_bits) - 1ull)));
+}
+
+// Heavy words only: sample-packed rows -> node-packed X words of the permuted
+// heavy rows (w < Hw, Hw read on device). One warp per (word, 32-sample block).
+__global__ void sp_transpose_kernel(const uint32_t* __restrict__ rows, int64_t stride,
+                                    const int32_t* __restrict__ perm,
+                                    const unsigned int* __restrict__ n_heavy, int32_t n,
+                                    const unsigned long long* __restrict__ dmask64,
+                                    unsigned long long* __restrict__ nx, int64_t n_ext) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t H = *n_heavy;
+  const int64_t Hw = (H + 63) / 64;
+  const int64_t blocks = Hw * stride;
+  for (int64_t bidx = warp; bidx < blocks; bidx += nwarps) {
+    const int64_t w = bidx / stride;
+    const int64_t cb = bidx - w * stride;
+    const int64_t r1 = 64 * w + lane, r2 = r1 + 32;
+    const uint32_t a = r1 < H ? __ldg(rows + static_cast<int64_t>(perm[r1]) * stride + cb) : 0u;
+    const uint32_t b = r2 < H ? __ldg(rows + static_cast<int64_t>(perm[r2]) * stride + cb) : 0u;
+    unsigned long long out = 0ull;
+#pragma unroll
+    for (int bit = 0; bit < 32; ++bit) {
+      const uint32_t v1 = __ballot_sync(0xffffffffu, (a >> bit) & 1u);
+      const uint32_t v2 = __ballot_sync(0xffffffffu, (b >> bit) & 1u);
+      if (bit == lane)
+        out = (static_cast<unsigned long long>(__brev(v1)) << 32) | static_cast<unsigned long long>(__brev(v2));
+    }
+    const int64_t s = cb * 32 + lane;
+    // complement only the heavy rows of the word: the light rows that share
+    // its last word (dense ones included) must stay zero here
+    const int64_t h = H - 64 * w;
+    const unsigned long long heavy_bits = h >= 64 ? ~0ull : ~(~0ull >> h);
+    if (s < n) nx[w * n_ext + s] = out ^ (dmask64[w] & heavy_bits);
+  }
+}
+
+// Wrap columns of the heavy words: nx[w][c] = nx[w][c mod n], n <= c < n_ext.
+__global__ void sp_extend_kernel(unsigned long long* __restrict__ nx, int64_t n_ext, int32_t n,
+                                 const unsigned int* __restrict__ n_heavy) {
+  const int64_t Hw = (static_cast<int64_t>(*n_heavy) + 63) / 64;
+  const int64_t extra = n_ext - n;
+  const int64_t total = Hw * extra;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = i / extra;
+    const int64_t col = n + i % extra;
+    nx[w * n_ext + col] = nx[w * n_ext + col % n];
+  }
+}
+
+// Column sums over the heavy words: thread per column (coalesced over c).
+// colsum layout [4][n] = x_hi, x_lo, p_hi, p_lo (p: rows that are not dense).
+__global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx, int64_t n_ext,
+                                       int32_t n, const unsigned int* __restrict__ n_heavy,
+                                       const unsigned long long* __restrict__ dmask64,
+                                       const double2* __restrict__ limbs,
+                                       unsigned long long* __restrict__ colsum) {
+  const int64_t Hw = (static_cast<int64_t>(*n_heavy) + 63) / 64;
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
+       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    unsigned long long xh = 0, xl = 0, ph = 0, pl = 0;
+    for (int64_t w = 0; w < Hw; ++w) {
+      const unsigned long long x = __ldg(nx + w * n_ext + c);
+      if (!x) continue;
+      const unsigned long long dm = __ldg(dmask64 + w);
+      unsigned long long b = x;
+      while (b) {
+        const int p = 63 - __clzll(static_cast<long long>(b));  // bit position
+        const unsigned long long m = 1ull << p;
+        b ^= m;
+        const double2 L = __ldg(limbs + 64 * w + p);
+        const unsigned long long h = static_cast<unsigned long long>(L.x);
+        const unsigned long long l = static_cast<unsigned long long>(L.y);
+        xh += h;
+        xl += l;
+        if (!(dm & m)) {
+          ph += h;
+          pl += l;
+        }
+      }
+    }
+    atomicAdd(colsum + c, xh);
+    atomicAdd(colsum + n + c, xl);
+    atomicAdd(colsum + 2 * static_cast<int64_t>(n) + c, ph);
+    atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, pl);
+  }
+}
+
+// Light rows: one warp per row. Lists the members of X_e (in sample order)
+// in shared memory, adds the row to its members' column sums, and adds its
+// limbs to the slot of every member pair whose stripe lies in
+// [s_begin, s_end). gl: (s_end - s_begin) x n x (hi, lo) doubles.
+// Pair {a < b}, d = b - a: slot (s = d-1, k = a) when d-1 < S, and slot
+// (s = n-d-1, k = b) when n-d-1 < S (both for d = n/2, n even: the
+// reference's duplicated half stripe).
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
+    const uint32_t* __restrict__ rows, int64_t stride, int32_t E, int32_t n, int32_t heavy_min,
+    const unsigned long long* __restrict__ fix, int32_t lo_bits, int32_t s_begin, int32_t s_end,
+    double* __restrict__ gl, unsigned long long* __restrict__ colsum,
+    unsigned long long* __restrict__ pairs_out, int32_t list_cap) {
+  extern __shared__ int32_t sp_members[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int32_t* mem = sp_members + static_cast<int64_t>(wib) * list_cap;
+  const int S = n / 2;
+  const int64_t warp = static_cast<int64_t>(blockIdx.x) * NW + wib;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * NW;
+  const uint32_t tail = (n & 31) ? ((1u << (n & 31)) - 1u) : 0xffffffffu;
+  unsigned long long pairs = 0;
+  for (int64_t r = warp; r < E; r += nwarps) {
+    const uint32_t* row = rows + r * stride;
+    int m = 0;
+    for (int64_t i = lane; i < stride; i += 32) m += __popc(__ldg(row + i));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m += __shfl_xor_sync(0xffffffffu, m, off);
+    const bool dense = 2 * m > n;
+    const int x = dense ? n - m : m;
+    if (x >= heavy_min || x == 0) continue;  // heavy rows are walked; empty rows add nothing
+    // members in sample order: warp-wide compaction of the (possibly
+    // complemented) row words
+    int count = 0;
+    for (int64_t base = 0; base < stride; base += 32) {
+      const int64_t i = base + lane;
+      uint32_t wd = 0u;
+      if (i < stride) {
+        wd = __ldg(row + i);
+        if (dense) wd = ~wd & (i == stride - 1 ? tail : 0xffffffffu);
+      }
+      const int c = __popc(wd);
+      int incl = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      int at = count + incl - c;
+      while (wd) {
+        const int b = __ffs(wd) - 1;
+        wd &= wd - 1u;
+        mem[at++] = static_cast<int32_t>(i * 32 + b);
+      }
+      count += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    const double2 L = limbs_of(fix[r], lo_bits);
+    const unsigned long long lh = static_cast<unsigned long long>(L.x);
+    const unsigned long long ll = static_cast<unsigned long long>(L.y);
+    for (int i = lane; i < x; i += 32) {
+      const int c = mem[i];
+      atomicAdd(colsum + c, lh);
+      atomicAdd(colsum + n + c, ll);
+      if (!dense) {
+        atomicAdd(colsum + 2 * static_cast<int64_t>(n) + c, lh);
+        atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, ll);
+      }
+    }
+    for (int i = 0; i + 1 < x; ++i) {
+      const int a = mem[i];
+      for (int j = i + 1 + lane; j < x; j += 32) {
+        const int b = mem[j];
+        const int d = b - a;
+        int s = d - 1;
+        if (s < S && s >= s_begin && s < s_end) {
+          double* cell = gl + 2 * (static_cast<int64_t>(s - s_begin) * n + a);
+          atomicAdd(cell, L.x);
+          atomicAdd(cell + 1, L.y);
+          ++pairs;
+        }
+        s = n - d - 1;
+        if (s < S && s >= s_begin && s < s_end) {
+          double* cell = gl + 2 * (static_cast<int64_t>(s - s_begin) * n + b);
+          atomicAdd(cell, L.x);
+          atomicAdd(cell + 1, L.y);
+          ++pairs;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  for (int off = 16; off > 0; off >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+  if (lane == 0 && pairs) atomicAdd(pairs_out, pairs);
+}
+
+// bfind: position of the most significant set bit (x != 0).
+__device__ __forceinline__ int msb_pos(uint32_t x) {
+  int b;
+  asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(x));
+  return b;
+}
+
+struct SplitArgs {
+  const unsigned long long* nx;      // [Hw][n_ext] heavy X words
+  const double2* limbs;              // permuted heavy rows, by bit position
+  const unsigned int* n_heavy;
+  const double* gl;                  // light sums per slot (hi, lo)
+  const unsigned long long* colsum;  // [4][n]
+  const unsigned long long* cacc;    // [2]
+  int64_t n_ext;
+  int32_t n;
+  int32_t s_begin, s_end;
+  int32_t lo_bits, scale, finalize;
+  void* dist;
+  void* tot;
+  unsigned long long* counters;  // [0] slot x u-bit FMAs (+ light pairs, added by host), [1] fp64 ops
+};
+
+// One 32-bit half of a heavy u word: for every set bit b, add the row's limbs
+// to each slot whose v half has bit b. The next bit's limbs are loaded before
+// the current bit's FMAs (one-deep software pipeline).
+template <int RS>
+__device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restrict__ Lb,
+                                           const uint32_t (&vv)[RS], double (&gh)[RS],
+                                           double (&gl)[RS]) {
+  if (!hu) return;
+  int b = msb_pos(hu);
+  uint32_t m = 1u << b;
+  hu ^= m;
+  double2 L = __ldg(Lb + b);
+  for (;;) {
+    const bool more = hu != 0u;
+    const int b2 = more ? msb_pos(hu) : b;
+    const uint32_t m2 = more ? (1u << b2) : 0u;
+    hu ^= m2;
+    const double2 L2 = __ldg(Lb + b2);
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const double f = unit_if(vv[i] & m);
+      gh[i] = fma(L.x, f, gh[i]);
+      gl[i] = fma(L.y, f, gl[i]);
+    }
+    if (!more) break;
+    L = L2;
+    m = m2;
+  }
+}
+
+template <class Real, int RS, int NW>
+__global__ void __launch_bounds__(32 * NW) stripe_split_kernel(const SplitArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * NW + (threadIdx.x >> 5);
+  const int n = a.n;
+  if (k >= n) return;
+  const int s0 = a.s_begin + blockIdx.y * 32 * RS;
+  const int64_t n_ext = a.n_ext;
+  const int Hw = static_cast<int>((*a.n_heavy + 63u) / 64u);
+  const int64_t l0 = static_cast<int64_t>(k) + s0 + 1 + lane;  // v column of slot i: l0 + 32 i
+  int nvalid = 0;
+#pragma unroll
+  for (int i = 0; i < RS; ++i) nvalid += (s0 + lane + 32 * i < a.s_end) ? 1 : 0;
+  const int wvalid = __reduce_add_sync(0xffffffffu, nvalid);  // live slots of the warp
+  unsigned long long ubits = 0;
+
+  double gh[RS], gl[RS];
+#pragma unroll
+  for (int i = 0; i < RS; ++i) {
+    gh[i] = 0.0;
+    gl[i] = 0.0;
+  }
+#pragma unroll 1
+  for (int w = 0; w < Hw; ++w) {
+    const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
+    const unsigned long long u = __ldg(row + k);
+    if (u == 0ull) continue;
+    uint32_t vh[RS], vl[RS];
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const unsigned long long v = i < nvalid ? (__ldg(row + l0 + 32 * i) & u) : 0ull;
+      vh[i] = static_cast<uint32_t>(v >> 32);
+      vl[i] = static_cast<uint32_t>(v);
+    }
+    const double2* Lw = a.limbs + 64 * static_cast<int64_t>(w);
+    ubits += static_cast<unsigned>(__popcll(u));
+    heavy_half<RS>(static_cast<uint32_t>(u >> 32), Lw + 32, vh, gh, gl);
+    heavy_half<RS>(static_cast<uint32_t>(u), Lw, vl, gh, gl);
+  }
+
+  Real* dist = static_cast<Real*>(a.dist);
+  Real* tot = static_cast<Real*>(a.tot);
+  const unsigned long long* xs = a.colsum;
+  const long long ch = static_cast<long long>(a.cacc[0]);
+  const long long cl = static_cast<long long>(a.cacc[1]);
+#pragma unroll
+  for (int i = 0; i < RS; ++i) {
+    if (i >= nvalid) break;
+    const int s = s0 + lane + 32 * i;
+    const int64_t li = l0 + 32 * i;
+    const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
+    const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
+    const double2 light = reinterpret_cast<const double2*>(a.gl)[off];
+    const long long Gh_ = static_cast<long long>(gh[i]) + static_cast<long long>(light.x);
+    const long long Gl_ = static_cast<long long>(gl[i]) + static_cast<long long>(light.y);
+    const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm]) + ch - Gh_;
+    const long long tl = static_cast<long long>(xs[3 * n + k] + xs[3 * n + lm]) + cl - Gl_;
+    const long long dh = static_cast<long long>(xs[k] + xs[lm]) - 2 * Gh_;
+    const long long dl = static_cast<long long>(xs[n + k] + xs[n + lm]) - 2 * Gl_;
+    const __int128 tv = (static_cast<__int128>(th) << a.lo_bits) + tl;
+    const __int128 dv = (static_cast<__int128>(dh) << a.lo_bits) + dl;
+    const Real t = static_cast<Real>(i2_fixed_to_double(tv, a.scale));
+    Real d = static_cast<Real>(i2_fixed_to_double(dv, a.scale));
+    if (a.finalize) d = t == Real(0) ? Real(0) : d / t;
+    dist[off] = d;
+    tot[off] = t;
+  }
+  if (a.counters && lane == 0) {
+    // ubits is warp-uniform: the warp issued ubits x (live slots) FMA pairs
+    atomicAdd(a.counters, ubits * static_cast<unsigned long long>(wvalid));
+    atomicAdd(a.counters + 1, 2ull * ubits * static_cast<unsigned long long>(wvalid));
+  }
+}
+
+}  // namespace sf

@@ -26,7 +26,8 @@ from paper_2005_05826_b200 import stripefrac as sf
 
 pytestmark = pytest.mark.gpu
 
-KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4, N.KERNEL_ISECT, N.KERNEL_ISECT2]  # 3/4: flattened walk
+KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4, N.KERNEL_ISECT, N.KERNEL_ISECT2, N.KERNEL_ISECT3,
+           N.KERNEL_ISECT4, N.KERNEL_ISECT5, N.KERNEL_SPLIT]  # 3/4: flattened walk
 WALKS = (N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4)
 
 
@@ -164,7 +165,7 @@ def test_oracle_random_instances(device_ok, metric, prec):
                 for kernel in (N.KERNEL_DENSE, N.KERNEL_AUTO):
                     d, t, st = _gpu_stripes(problem, metric, prec, start, stop, kernel, exact)
                     used = kernel if kernel != N.KERNEL_AUTO or metric != 1 else (
-                        N.KERNEL_SPARSE if exact else N.KERNEL_ISECT)
+                        N.KERNEL_SPARSE if exact else N.KERNEL_SPLIT)
                     _assert_close(metric, prec, exact, d, wd, used)
                     if wt is not None:
                         _assert_close(metric, prec, exact, t, wt, used)
@@ -298,13 +299,13 @@ def test_sparse_kernel_matches_dense_bitwise(device_ok, prec):
 def test_isect_is_the_default_for_unweighted(device_ok):
     inst = sf.random_instance(45, 50, 100, 0.1)
     problem = sf.flatten(inst.tree, inst.table)
-    d5, t5, st = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_ISECT)
+    d5, t5, st = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_SPLIT)
     d0, t0, st0 = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_AUTO)
     assert np.array_equal(d5, d0) and np.array_equal(t5, t0)
-    # the intersection walk only touches rows shared by a slot's two samples
+    # the split kernel touches far fewer (row, slot) pairs than the reference
     assert 0 < st0.updates_exec < st0.updates_alg
     _, _, st2 = _gpu_stripes(problem, 1, 8, 0, 25, kernel=N.KERNEL_AUTO, exact=True)
-    assert st2.updates_exec > st0.updates_exec  # exact mode walks the union
+    assert 0 < st2.updates_exec < st2.updates_alg  # exact mode: the union walk
 
 
 def _exact_stripes(problem, prec, start, stop):
@@ -338,7 +339,7 @@ def _exact_stripes(problem, prec, start, stop):
     return d, t
 
 
-@pytest.mark.parametrize("kernel", [N.KERNEL_ISECT, N.KERNEL_ISECT2])
+@pytest.mark.parametrize("kernel", [N.KERNEL_ISECT, N.KERNEL_ISECT2, N.KERNEL_ISECT3, N.KERNEL_ISECT4, N.KERNEL_ISECT5, N.KERNEL_SPLIT])
 @pytest.mark.parametrize("prec", [8, 4])
 def test_isect_is_exact(device_ok, prec, kernel):
     """Kernel 5 returns the correctly rounded exact sums (raw, unfinalized),
@@ -361,7 +362,27 @@ def test_isect_is_exact(device_ok, prec, kernel):
                 assert np.all(np.abs(t.astype(np.float64) - wt) <= np.spacing(np.abs(wt).astype(np.float32)))
 
 
-@pytest.mark.parametrize("kernel", [N.KERNEL_ISECT, N.KERNEL_ISECT2])
+@pytest.mark.parametrize("heavy_frac", ["0.6", "0.0", "0.05"])
+@pytest.mark.parametrize("prec", [8, 4])
+def test_split_heavy_light_boundary_is_exact(device_ok, prec, heavy_frac, monkeypatch):
+    """Kernel 10 with every row light (scatter only), every row heavy (walk
+    only) and a mixed split: always the correctly rounded exact sums."""
+    monkeypatch.setenv("SF_HEAVY_FRAC", heavy_frac)
+    for seed, n, leaves, dens in [(71, 40, 60, 0.05), (72, 33, 50, 0.6), (73, 64, 90, 0.2)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 2, S)]:
+            wd, wt = _exact_stripes(problem, prec, start, stop)
+            d, t, st = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_SPLIT, finalize=False)
+            if prec == 8:
+                assert np.array_equal(d, wd) and np.array_equal(t, wt)
+            else:
+                assert np.all(np.abs(d.astype(np.float64) - wd) <= np.spacing(np.abs(wd).astype(np.float32)))
+                assert np.all(np.abs(t.astype(np.float64) - wt) <= np.spacing(np.abs(wt).astype(np.float32)))
+
+
+@pytest.mark.parametrize("kernel", [N.KERNEL_ISECT, N.KERNEL_ISECT2, N.KERNEL_ISECT3, N.KERNEL_ISECT4, N.KERNEL_ISECT5, N.KERNEL_SPLIT])
 @pytest.mark.parametrize("prec", [8, 4])
 def test_isect_matches_oracle_larger(device_ok, prec, kernel):
     """Kernel 5 vs the CPU restatement of the reference (sequential sums) on

@@ -1,0 +1,8 @@
+#!/usr/bin/env bash
+set -x
+mkdir -p gpurun_out
+export BENCH_ALLOW_SHORT=1
+CMD="python bench.py --config c3 --stripes 256 --kernel isect2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/plain_isect2.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:stripe_isect2 -s 1 -c 1 -o gpurun_out/prof_isect2_c3s256 $CMD > gpurun_out/ncu_isect2.log 2>&1
+echo done

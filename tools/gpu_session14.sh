@@ -1,0 +1,10 @@
+#!/usr/bin/env bash
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -x -k "isect or golden" > gpurun_out/pytest_isect5.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_isect5.log
+timeout 900 python tools/kernel_ab.py --config c3 --kernels 7,9 --reps 2 > gpurun_out/ab_c3_6.jsonl 2> gpurun_out/ab_c3_6.log
+export BENCH_ALLOW_SHORT=1
+CMD="python bench.py --config c3 --stripes 512 --kernel isect5 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+$CMD > gpurun_out/plain_isect5.log 2>&1 && \
+  timeout 1200 ncu --set full --clock-control none --import-source on -k regex:stripe_isect5 -s 1 -c 1 -o gpurun_out/prof_isect5 $CMD > gpurun_out/ncu_isect5.log 2>&1
+echo done
