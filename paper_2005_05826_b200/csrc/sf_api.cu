@@ -445,7 +445,7 @@ struct Isect5Cfg {
 };
 // Split (kernel 10): heavy rows walked warp-uniformly, light rows scattered.
 struct SplitCfg {
-  static constexpr int RS = 8, NW = 8, SCATTER_NW = 8;
+  static constexpr int RS = 16, NW = 4, SCATTER_NW = 8;
 };
 
 // |X_e| threshold of the split path: rows at or above it are walked.
@@ -456,7 +456,9 @@ int split_heavy_min(int n) {
 }
 
 int64_t sparse_n_ext(int n) {
-  const int64_t tile = std::max(SparseCfg::TK + SparseCfg::TS, IsectCfg::T::VW);
+  // a whole stripe tile past the last stripe: the widest is the split
+  // kernel's 32 * RS (RS <= 16)
+  const int64_t tile = std::max<int64_t>(std::max(SparseCfg::TK + SparseCfg::TS, IsectCfg::T::VW), 512);
   const int64_t need = static_cast<int64_t>(n) + n / 2 + tile + 64;
   return (need + 3) / 4 * 4;
 }
@@ -696,14 +698,22 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   return SF_OK;
 }
 
-template <class Real>
-sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
-  using C = SplitCfg;
-  auto* kern = stripe_split_kernel<Real, C::RS, C::NW>;
-  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
-  kern<<<grid, 32 * C::NW, 0, st>>>(a);
+template <class Real, int RS, int NW>
+sf_status launch_split_rs(const SplitArgs& a, cudaStream_t st) {
+  auto* kern = stripe_split_kernel<Real, RS, NW>;
+  const dim3 grid((a.n + NW - 1) / NW, (a.s_end - a.s_begin + 32 * RS - 1) / (32 * RS));
+  kern<<<grid, 32 * NW, 0, st>>>(a);
   SF_CUDA(cudaGetLastError());
   return SF_OK;
+}
+
+// slots per lane: the default 16 (measured best at the EMP shape), or
+// SF_SPLIT_RS=8 (tuning knob)
+template <class Real>
+sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
+  const char* e = std::getenv("SF_SPLIT_RS");
+  if (e && std::atoi(e) == 8) return launch_split_rs<Real, 8, 8>(a, st);
+  return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW>(a, st);
 }
 
 template <class Real>

@@ -243,32 +243,32 @@ struct SplitArgs {
 };
 
 // One 32-bit half of a heavy u word: for every set bit b, add the row's limbs
-// to each slot whose v half has bit b. The next bit's limbs are loaded before
-// the current bit's FMAs (one-deep software pipeline).
+// to each slot whose v half has bit b (b is set in u, so v need not be masked
+// with u first). Two bits per trip, branch-free (a missing second bit gets
+// mask 0, i.e. factor 0): per trip ~15 instructions of bit bookkeeping and
+// 8 per slot (2 x LOP3+SEL, 4 DFMA).
 template <int RS>
 __device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restrict__ Lb,
                                            const uint32_t (&vv)[RS], double (&gh)[RS],
                                            double (&gl)[RS]) {
-  if (!hu) return;
-  int b = msb_pos(hu);
-  uint32_t m = 1u << b;
-  hu ^= m;
-  double2 L = __ldg(Lb + b);
-  for (;;) {
-    const bool more = hu != 0u;
-    const int b2 = more ? msb_pos(hu) : b;
-    const uint32_t m2 = more ? (1u << b2) : 0u;
+  while (hu) {
+    const int b1 = msb_pos(hu);
+    const uint32_t m1 = 1u << b1;
+    hu ^= m1;
+    const int b2 = msb_pos(hu | 1u);
+    const uint32_t m2 = hu ? (1u << b2) : 0u;
     hu ^= m2;
+    const double2 L1 = __ldg(Lb + b1);
     const double2 L2 = __ldg(Lb + b2);
 #pragma unroll
     for (int i = 0; i < RS; ++i) {
-      const double f = unit_if(vv[i] & m);
-      gh[i] = fma(L.x, f, gh[i]);
-      gl[i] = fma(L.y, f, gl[i]);
+      const double f1 = unit_if(vv[i] & m1);
+      const double f2 = unit_if(vv[i] & m2);
+      gh[i] = fma(L1.x, f1, gh[i]);
+      gl[i] = fma(L1.y, f1, gl[i]);
+      gh[i] = fma(L2.x, f2, gh[i]);
+      gl[i] = fma(L2.y, f2, gl[i]);
     }
-    if (!more) break;
-    L = L2;
-    m = m2;
   }
 }
 
@@ -281,7 +281,9 @@ __global__ void __launch_bounds__(32 * NW) stripe_split_kernel(const SplitArgs a
   const int s0 = a.s_begin + blockIdx.y * 32 * RS;
   const int64_t n_ext = a.n_ext;
   const int Hw = static_cast<int>((*a.n_heavy + 63u) / 64u);
-  const int64_t l0 = static_cast<int64_t>(k) + s0 + 1 + lane;  // v column of slot i: l0 + 32 i
+  // v column of slot i: l0 + 32 i (< n_ext for every i: n_ext covers a whole
+  // tile past the last stripe, so dead slots read real words and are dropped)
+  const int64_t l0 = static_cast<int64_t>(k) + s0 + 1 + lane;
   int nvalid = 0;
 #pragma unroll
   for (int i = 0; i < RS; ++i) nvalid += (s0 + lane + 32 * i < a.s_end) ? 1 : 0;
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(32 * NW) stripe_split_kernel(const SplitArgs a
     uint32_t vh[RS], vl[RS];
 #pragma unroll
     for (int i = 0; i < RS; ++i) {
-      const unsigned long long v = i < nvalid ? (__ldg(row + l0 + 32 * i) & u) : 0ull;
+      const unsigned long long v = __ldg(row + l0 + 32 * i);
       vh[i] = static_cast<uint32_t>(v >> 32);
       vl[i] = static_cast<uint32_t>(v);
     }
