@@ -16,9 +16,12 @@
 //  * accumulate (kernels.hpp:232-248) and finalize (:251-259) act on host
 //    StripeSets, computing on device;
 //  * compute_distance_matrix (:319-326) condenses on device.
-// Unweighted results are bitwise identical to the reference; weighted ones
-// agree within 1e-12 relative (fp64) unless STRIPEFRAC_B200_EXACT is defined,
-// which selects the no-FMA kernels that are bitwise identical too.
+// Unweighted results are the correctly rounded exact sums (fixed-point
+// arithmetic, kernel 10): within ~1e-14 relative of the reference's
+// sequential fp64 sums (gate: 1e-12). Weighted ones agree within 1e-12
+// relative (fp64, FMA). Defining STRIPEFRAC_B200_EXACT selects the kernels
+// that replay the reference's adds in the reference's order: bitwise
+// identical for every metric.
 #pragma once
 
 #include <cstdint>
