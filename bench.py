@@ -149,6 +149,7 @@ def measured_fp_peak(device: int, prec: str) -> float:
 
 def run_ours(args, cfg):
     from paper_2005_05826_b200 import _native as N
+    from paper_2005_05826_b200 import shard
     world, rank, local = dist_env()
     torch = None
     if world > 1:
@@ -165,8 +166,7 @@ def run_ours(args, cfg):
     n, E = problem.n_samples, problem.n_rows
     S = n // 2
     stop_all = min(S, args.stripes) if args.stripes else S
-    a = int(stop_all * rank // world)
-    b = int(stop_all * (rank + 1) // world)
+    a, b = shard.rank_range(0, stop_all, rank, world)
     kernel = {"auto": 0, "dense": 1, "sparse": 2, "flat32": 3, "flat64": 4, "isect": 5, "isect2": 6, "isect3": 7, "isect4": 8, "isect5": 9, "split": 10}[args.kernel]
     ex, _keep = N.make_exec([local], kernel)
     plan = C.c_void_p()
@@ -204,15 +204,10 @@ def run_ours(args, cfg):
         barrier()
         wall = time.perf_counter() - w0
     total_dev_s = sum(dev_ms) / 1e3
-    if world > 1:
-        t = torch.tensor([total_dev_s, wall], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_dev_s, wall = float(t[0]), float(t[1])
-        ue_t = torch.tensor([uexec], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(ue_t)
-        uexec_all = float(ue_t[0])
-    else:
-        uexec_all = float(uexec)
+    dev = "cuda" if world > 1 else None
+    total_dev_s = shard.max_over_ranks(total_dev_s, dev)
+    wall = shard.max_over_ranks(wall, dev)
+    uexec_all = shard.sum_over_ranks(float(uexec), dev)
     u_alg_step = E * stop_all * n
     value = u_alg_step * args.steps / total_dev_s
     ms_per_step = total_dev_s * 1e3 / args.steps
@@ -235,10 +230,7 @@ def run_ours(args, cfg):
                                          C.byref(ex), C.byref(st2)))
             times.append(time.perf_counter() - t1)
         e2e_s = max(times) if len(times) == 1 else statistics.median(times)
-        if world > 1:
-            t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e2e_s = float(t[0])
+        e2e_s = shard.max_over_ranks(e2e_s, "cuda" if world > 1 else None)
         h2d = (problem.parent_row.nbytes + problem.lengths.nbytes + problem.leaf_feature.nbytes +
                problem.feat_ptr.nbytes + problem.sample_idx.nbytes + problem.counts.nbytes +
                problem.sample_totals.nbytes)

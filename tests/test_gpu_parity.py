@@ -398,3 +398,25 @@ def test_isect_matches_oracle_larger(device_ok, prec, kernel):
             _assert_close(1, prec, False, d, wd, kernel)
             _assert_close(1, prec, False, t, wt, kernel)
             assert st.updates_alg == problem.n_rows * (stop - start) * n
+
+
+@pytest.mark.parametrize("kernel", [N.KERNEL_AUTO, N.KERNEL_DENSE, N.KERNEL_SPARSE])
+def test_stripe_shards_match_single_device(device_ok, kernel):
+    """The in-process multi-device fan-out (sf_exec.devices, the reference's
+    worker split kernels.hpp:302-303) with two or three shards placed on the
+    same B200: every shard builds its own embedding and writes its own stripe
+    block; the result equals the one-shard run bit for bit."""
+    inst = sf.random_instance(91, 300, 900, 0.01)
+    problem = sf.flatten(inst.tree, inst.table)
+    n = problem.n_samples
+    for metric in ((1, 3) if kernel == N.KERNEL_DENSE else (1,)):
+        for start, stop in [(0, n // 2), (17, 140)]:
+            d1, t1, _ = _gpu_stripes(problem, metric, 8, start, stop, kernel)
+            for devs in ([0, 0], [0, 0, 0]):
+                d = np.full((stop - start, n), np.nan)
+                t = np.full((stop - start, n), np.nan)
+                ex, _keep = N.make_exec(devs, kernel)
+                st = N.sf_stats()
+                N.check(N.lib().sf_compute_stripes(problem.ref, metric, 8, start, stop, N.ptr(d), N.ptr(t),
+                                                   1, C.byref(ex), C.byref(st)))
+                assert np.array_equal(d, d1) and np.array_equal(t, t1)
