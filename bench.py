@@ -212,6 +212,9 @@ def run_ours(args, cfg):
     value = u_alg_step * args.steps / total_dev_s
     ms_per_step = total_dev_s * 1e3 / args.steps
 
+    L.sf_plan_destroy(plan)  # free the resident plan before the end-to-end calls
+    plan = None
+
     # ---- e2e through the public C ABI: host problem in, host stripes out
     e2e = None
     if not args.no_e2e:
@@ -222,6 +225,10 @@ def run_ours(args, cfg):
         tot_h = _t.empty(((b - a) * n,), dtype=dt, pin_memory=True).numpy() if metric != 2 else None
         st2 = N.sf_stats()
         times = []
+        # one untimed call first (first-touch of the pinned pages, allocator)
+        N.check(L.sf_compute_stripes(problem.ref, metric, prec, a, b, N.ptr(dist_h),
+                                     N.ptr(tot_h) if tot_h is not None else None, 1,
+                                     C.byref(ex), C.byref(st2)))
         for _ in range(max(1, args.e2e_steps)):
             barrier()
             t1 = time.perf_counter()
@@ -241,7 +248,6 @@ def run_ours(args, cfg):
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
-        L.sf_plan_destroy(plan)
         return None
 
     # ---- roofline of the dominant kernel (K2 stripe update)
@@ -311,7 +317,6 @@ def run_ours(args, cfg):
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
         "gpu_launches": int(launches), "wall_seconds_timed": wall,
     }
-    L.sf_plan_destroy(plan)
     if world > 1:
         torch.distributed.destroy_process_group()
     return line
@@ -381,7 +386,7 @@ def main():
     ap.add_argument("--kernel", choices=["auto", "dense", "sparse", "flat32", "flat64", "isect", "isect2", "isect3", "isect4", "isect5", "split"],
                     default="auto")
     ap.add_argument("--stripes", type=int, default=0, help="limit to stripes [0, N) (debug)")
-    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-stripes", type=int, default=256)

@@ -374,6 +374,8 @@ struct DeviceState {
   int dev = -1;
   int32_t a = 0, b = 0;  // absolute stripe range on this device
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;     // D2H overlapped with the split kernel
+  std::vector<cudaEvent_t> chunk_events;  // stripe chunks done (split kernel)
   DevBuf lens, feat_ptr, sidx, counts, totals;
   DevBuf dist, tot, emb, pend, exec_ctr;
   DevBuf sched;  // all schedule arrays, packed
@@ -393,7 +395,9 @@ struct DeviceState {
     if (dev >= 0) {
       cudaSetDevice(dev);
       for (auto e : events) cudaEventDestroy(e);
+      for (auto e : chunk_events) cudaEventDestroy(e);
       if (stream) cudaStreamDestroy(stream);
+      if (copy_stream) cudaStreamDestroy(copy_stream);
     }
   }
 };
@@ -849,7 +853,11 @@ sf_status upload_schedule(DeviceState& d, const Schedule& s) {
   return upload(d.sched, d.dev, packed.data(), packed.size(), d.stream, "schedule");
 }
 
-sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
+// host_d / host_t (optional): this device's slice of the caller's output.
+// With the split kernel the stripes are then computed in chunks and each
+// chunk's D2H copy runs on a second stream while the next chunk computes.
+sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host_d = nullptr,
+                     void* host_t = nullptr) {
   SF_CUDA(cudaSetDevice(d.dev));
   const cudaStream_t st = d.stream;
   const int n = plan->n;
@@ -864,9 +872,11 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
     d.events.push_back(e);
   }
   SF_CUDA(cudaEventRecord(d.events[0], st));
-  SF_CUDA(cudaMemsetAsync(d.dist.p, 0, static_cast<size_t>(slots) * w, st));
-  if (d.tot.p && plan->metric != SF_WEIGHTED_UNNORMALIZED)
-    SF_CUDA(cudaMemsetAsync(d.tot.p, 0, static_cast<size_t>(slots) * w, st));
+  if (plan->kernel != 10) {  // the split kernel writes every slot
+    SF_CUDA(cudaMemsetAsync(d.dist.p, 0, static_cast<size_t>(slots) * w, st));
+    if (d.tot.p && plan->metric != SF_WEIGHTED_UNNORMALIZED)
+      SF_CUDA(cudaMemsetAsync(d.tot.p, 0, static_cast<size_t>(slots) * w, st));
+  }
   SF_CUDA(cudaMemsetAsync(d.exec_ctr.p, 0, 2 * sizeof(unsigned long long), st));
 
   const int64_t stride = plan->row_words;
@@ -941,13 +951,47 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize) {
       a.n = n;
       a.s_begin = d.a;
       a.s_end = d.b;
+      a.out_begin = d.a;
       a.lo_bits = plan->lo_bits;
       a.scale = plan->scale;
       a.finalize = finalize ? 1 : 0;
       a.dist = d.dist.p;
       a.tot = d.tot.p;
       a.counters = d.exec_ctr.as<unsigned long long>();
-      SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+      if (!host_d) {
+        SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+      } else {
+        // chunks of whole 512-stripe tiles; copy each as soon as it is done
+        const int span = d.b - d.a;
+        const int tile = 32 * SplitCfg::RS;
+        const int nch = std::max(1, std::min(8, span / (4 * tile)));
+        const int per = (span + nch - 1) / nch;
+        const int step = (per + tile - 1) / tile * tile;
+        if (!d.copy_stream) SF_CUDA(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking));
+        while (static_cast<int>(d.chunk_events.size()) < nch) {
+          cudaEvent_t e;
+          SF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          d.chunk_events.push_back(e);
+        }
+        int ci = 0;
+        for (int c0 = d.a; c0 < d.b; c0 += step, ++ci) {
+          const int c1 = std::min(d.b, c0 + step);
+          a.s_begin = c0;
+          a.s_end = c1;
+          SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+          plan->stats.launches++;
+          SF_CUDA(cudaEventRecord(d.chunk_events[static_cast<size_t>(ci)], st));
+          SF_CUDA(cudaStreamWaitEvent(d.copy_stream, d.chunk_events[static_cast<size_t>(ci)], 0));
+          const size_t off = static_cast<size_t>(c0 - d.a) * n * w;
+          const size_t bytes = static_cast<size_t>(c1 - c0) * n * w;
+          SF_CUDA(cudaMemcpyAsync(static_cast<char*>(host_d) + off, d.dist.as<char>() + off, bytes,
+                                  cudaMemcpyDeviceToHost, d.copy_stream));
+          if (host_t)
+            SF_CUDA(cudaMemcpyAsync(static_cast<char*>(host_t) + off, d.tot.as<char>() + off, bytes,
+                                    cudaMemcpyDeviceToHost, d.copy_stream));
+        }
+        plan->stats.launches--;  // counted once more below
+      }
     } else if (plan->kernel >= 6) {
       Isect2Args a;
       const int64_t W = (plan->E + 63) / 64;
@@ -1224,6 +1268,7 @@ sf_status sf_plan_sync(sf_plan* plan) {
     DeviceState& d = *dp;
     SF_CUDA(cudaSetDevice(d.dev));
     SF_CUDA(cudaStreamSynchronize(d.stream));
+    if (d.copy_stream) SF_CUDA(cudaStreamSynchronize(d.copy_stream));
     if (!plan->ran) continue;
     double e_ms = 0, s_ms = 0, f_ms = 0, t_ms = 0;
     const size_t ne = d.events.size();
@@ -1298,9 +1343,33 @@ sf_status sf_compute_stripes(const sf_problem* p, sf_metric metric, sf_precision
   sf_plan* plan = nullptr;
   SF_TRY(sf_plan_create(p, metric, prec, start, stop, ex, &plan));
   std::unique_ptr<sf_plan> guard(plan);
-  SF_TRY(sf_plan_run(plan, finalize));
-  SF_TRY(sf_plan_sync(plan));
-  SF_TRY(sf_plan_download(plan, dist_out, tot_out));
+  auto pinned = [](const void* ptr) {
+    cudaPointerAttributes at{};
+    if (!ptr || cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+  };
+  // pageable destinations make cudaMemcpyAsync block the host, which would
+  // serialise the chunks; those get compute-then-download instead
+  if (plan->kernel == 10 && pinned(dist_out) && (!tot_out || pinned(tot_out))) {
+    // download overlapped with the split kernel, chunk by chunk
+    const size_t w = prec == SF_FP64 ? 8 : 4;
+    plan->stats.launches = 0;
+    for (auto& dp : plan->devs) {
+      const size_t off = static_cast<size_t>(dp->a - plan->start) * plan->n * w;
+      SF_TRY(run_device(plan, *dp, finalize, static_cast<char*>(dist_out) + off,
+                        static_cast<char*>(tot_out) + off));
+    }
+    plan->ran = true;
+    plan->finalized = finalize != 0;
+    SF_TRY(sf_plan_sync(plan));
+  } else {
+    SF_TRY(sf_plan_run(plan, finalize));
+    SF_TRY(sf_plan_sync(plan));
+    SF_TRY(sf_plan_download(plan, dist_out, tot_out));
+  }
   if (stats_out) *stats_out = plan->stats;
   return SF_OK;
 }

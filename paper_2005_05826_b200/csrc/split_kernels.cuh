@@ -235,7 +235,8 @@ struct SplitArgs {
   const unsigned long long* cacc;    // [2]
   int64_t n_ext;
   int32_t n;
-  int32_t s_begin, s_end;
+  int32_t s_begin, s_end;  // stripes computed by this launch
+  int32_t out_begin;       // stripe held by row 0 of dist / tot / gl
   int32_t lo_bits, scale, finalize;
   void* dist;
   void* tot;
@@ -325,7 +326,7 @@ __global__ void __launch_bounds__(32 * NW) stripe_split_kernel(const SplitArgs a
     const int s = s0 + lane + 32 * i;
     const int64_t li = l0 + 32 * i;
     const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
-    const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
+    const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
     const double2 light = reinterpret_cast<const double2*>(a.gl)[off];
     const long long Gh_ = static_cast<long long>(gh[i]) + static_cast<long long>(light.x);
     const long long Gl_ = static_cast<long long>(gl[i]) + static_cast<long long>(light.y);

@@ -1,0 +1,4 @@
+#!/usr/bin/env bash
+mkdir -p gpurun_out
+timeout 900 python tools/e2e_probe.py > gpurun_out/e2e_probe.log 2>&1
+echo done
