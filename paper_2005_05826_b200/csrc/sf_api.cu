@@ -449,7 +449,7 @@ struct Isect5Cfg {
 };
 // Split (kernel 10): heavy rows walked warp-uniformly, light rows scattered.
 struct SplitCfg {
-  static constexpr int RS = 16, NW = 4, SCATTER_NW = 8;
+  static constexpr int RS = 16, NW = 8, SCATTER_NW = 8;
 };
 
 // |X_e| threshold of the split path: rows at or above it are walked.
@@ -702,22 +702,30 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   return SF_OK;
 }
 
-template <class Real, int RS, int NW>
+template <class Real, int RS, int NW, bool BITMAJOR = false, bool UPREF = false, bool HALVES = false,
+          int MINB = 1>
 sf_status launch_split_rs(const SplitArgs& a, cudaStream_t st) {
-  auto* kern = stripe_split_kernel<Real, RS, NW>;
+  auto* kern = stripe_split_kernel<Real, RS, NW, BITMAJOR, UPREF, HALVES, MINB>;
   const dim3 grid((a.n + NW - 1) / NW, (a.s_end - a.s_begin + 32 * RS - 1) / (32 * RS));
   kern<<<grid, 32 * NW, 0, st>>>(a);
   SF_CUDA(cudaGetLastError());
   return SF_OK;
 }
 
-// slots per lane: the default 16 (measured best at the EMP shape), or
-// SF_SPLIT_RS=8 (tuning knob)
+// Default: 16 slots per lane, 8 u columns per CTA, v words loaded one 32-bit
+// half at a time (measured best at the EMP shape: profiles/r01_ab_c3_split_variants*).
+// SF_SPLIT_VARIANT selects the measured alternatives for A/B.
 template <class Real>
 sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
-  const char* e = std::getenv("SF_SPLIT_RS");
-  if (e && std::atoi(e) == 8) return launch_split_rs<Real, 8, 8>(a, st);
-  return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW>(a, st);
+  const char* v = std::getenv("SF_SPLIT_VARIANT");
+  const int var = v ? std::atoi(v) : 0;
+  switch (var) {
+    case 1: return launch_split_rs<Real, 16, 4>(a, st);               // 64-bit v words, 4 warps
+    case 2: return launch_split_rs<Real, 16, 4, false, true>(a, st);  // + u word prefetch
+    case 3: return launch_split_rs<Real, 8, 8>(a, st);                // 8 slots per lane
+    case 4: return launch_split_rs<Real, 16, 4, false, false, true>(a, st);
+    default: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true>(a, st);
+  }
 }
 
 template <class Real>

@@ -243,24 +243,38 @@ struct SplitArgs {
   unsigned long long* counters;  // [0] slot x u-bit FMAs (+ light pairs, added by host), [1] fp64 ops
 };
 
-// One 32-bit half of a heavy u word: for every set bit b, add the row's limbs
-// to each slot whose v half has bit b (b is set in u, so v need not be masked
-// with u first). Two bits per trip, branch-free (a missing second bit gets
-// mask 0, i.e. factor 0): per trip ~15 instructions of bit bookkeeping and
-// 8 per slot (2 x LOP3+SEL, 4 DFMA).
-template <int RS>
-__device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restrict__ Lb,
+// The next (up to) two set bits of hu, highest first: positions b1, b2 and
+// masks m1, m2 (0 when absent; the position then points at a valid entry).
+__device__ __forceinline__ void next_two(uint32_t& hu, int& b1, uint32_t& m1, int& b2, uint32_t& m2) {
+  b1 = msb_pos(hu | 1u);
+  m1 = hu ? (1u << b1) : 0u;
+  hu ^= m1;
+  b2 = msb_pos(hu | 1u);
+  m2 = hu ? (1u << b2) : 0u;
+  hu ^= m2;
+}
+
+// Add the limbs of one pair of u bits to every slot whose v half has the bit
+// (the bit is set in u, so v need not be masked with u first). BITMAJOR: bit
+// 1 for all slots, then bit 2; else slot by slot.
+template <int RS, bool BITMAJOR>
+__device__ __forceinline__ void heavy_fma2(const double2 L1, uint32_t m1, const double2 L2, uint32_t m2,
                                            const uint32_t (&vv)[RS], double (&gh)[RS],
                                            double (&gl)[RS]) {
-  while (hu) {
-    const int b1 = msb_pos(hu);
-    const uint32_t m1 = 1u << b1;
-    hu ^= m1;
-    const int b2 = msb_pos(hu | 1u);
-    const uint32_t m2 = hu ? (1u << b2) : 0u;
-    hu ^= m2;
-    const double2 L1 = __ldg(Lb + b1);
-    const double2 L2 = __ldg(Lb + b2);
+  if (BITMAJOR) {
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const double f1 = unit_if(vv[i] & m1);
+      gh[i] = fma(L1.x, f1, gh[i]);
+      gl[i] = fma(L1.y, f1, gl[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const double f2 = unit_if(vv[i] & m2);
+      gh[i] = fma(L2.x, f2, gh[i]);
+      gl[i] = fma(L2.y, f2, gl[i]);
+    }
+  } else {
 #pragma unroll
     for (int i = 0; i < RS; ++i) {
       const double f1 = unit_if(vv[i] & m1);
@@ -273,8 +287,26 @@ __device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restric
   }
 }
 
-template <class Real, int RS, int NW>
-__global__ void __launch_bounds__(32 * NW) stripe_split_kernel(const SplitArgs a) {
+// One 32-bit half of a heavy u word, two bits per step, branch-free.
+// (A ping-pong prefetch of the next step's limbs measured slower: the extra
+// registers cost more occupancy than the hidden L1 latency was worth.)
+template <int RS, bool BITMAJOR>
+__device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restrict__ Lb,
+                                           const uint32_t (&vv)[RS], double (&gh)[RS],
+                                           double (&gl)[RS]) {
+  while (hu) {
+    int b1, b2;
+    uint32_t m1, m2;
+    next_two(hu, b1, m1, b2, m2);
+    const double2 L1 = __ldg(Lb + b1);
+    const double2 L2 = __ldg(Lb + b2);
+    heavy_fma2<RS, BITMAJOR>(L1, m1, L2, m2, vv, gh, gl);
+  }
+}
+
+template <class Real, int RS, int NW, bool BITMAJOR = false, bool UPREF = false, bool HALVES = false,
+          int MINB = 1>
+__global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const SplitArgs a) {
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * NW + (threadIdx.x >> 5);
   const int n = a.n;
@@ -297,22 +329,44 @@ __global__ void __launch_bounds__(32 * NW) stripe_split_kernel(const SplitArgs a
     gh[i] = 0.0;
     gl[i] = 0.0;
   }
+  unsigned long long u_next = (UPREF && Hw > 0) ? __ldg(a.nx + k) : 0ull;
 #pragma unroll 1
   for (int w = 0; w < Hw; ++w) {
     const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
-    const unsigned long long u = __ldg(row + k);
-    if (u == 0ull) continue;
-    uint32_t vh[RS], vl[RS];
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const unsigned long long v = __ldg(row + l0 + 32 * i);
-      vh[i] = static_cast<uint32_t>(v >> 32);
-      vl[i] = static_cast<uint32_t>(v);
+    unsigned long long u;
+    if (UPREF) {
+      u = u_next;  // loaded one word ahead
+      if (w + 1 < Hw) u_next = __ldg(row + n_ext + k);
+    } else {
+      u = __ldg(row + k);
     }
+    if (u == 0ull) continue;
     const double2* Lw = a.limbs + 64 * static_cast<int64_t>(w);
     ubits += static_cast<unsigned>(__popcll(u));
-    heavy_half<RS>(static_cast<uint32_t>(u >> 32), Lw + 32, vh, gh, gl);
-    heavy_half<RS>(static_cast<uint32_t>(u), Lw, vl, gh, gl);
+    if (HALVES) {  // one 32-bit half of the v words live at a time (fewer registers)
+      const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
+      uint32_t vv[RS];
+      if (static_cast<uint32_t>(u >> 32)) {
+#pragma unroll
+        for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
+        heavy_half<RS, BITMAJOR>(static_cast<uint32_t>(u >> 32), Lw + 32, vv, gh, gl);
+      }
+      if (static_cast<uint32_t>(u)) {
+#pragma unroll
+        for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
+        heavy_half<RS, BITMAJOR>(static_cast<uint32_t>(u), Lw, vv, gh, gl);
+      }
+    } else {
+      uint32_t vh[RS], vl[RS];
+#pragma unroll
+      for (int i = 0; i < RS; ++i) {
+        const unsigned long long v = __ldg(row + l0 + 32 * i);
+        vh[i] = static_cast<uint32_t>(v >> 32);
+        vl[i] = static_cast<uint32_t>(v);
+      }
+      heavy_half<RS, BITMAJOR>(static_cast<uint32_t>(u >> 32), Lw + 32, vh, gh, gl);
+      heavy_half<RS, BITMAJOR>(static_cast<uint32_t>(u), Lw, vl, gh, gl);
+    }
   }
 
   Real* dist = static_cast<Real*>(a.dist);

@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--stripes", type=int, default=0)
     ap.add_argument("--metric", default=None)
     ap.add_argument("--precision", default=None)
+    ap.add_argument("--env", default="", help="NAME=v1,v2,... : rerun each kernel per value")
     args = ap.parse_args()
     cfg = dict(bench.CONFIGS[args.config])
     if args.metric:
@@ -41,7 +42,17 @@ def main():
     S = n // 2
     stop = min(S, args.stripes) if args.stripes else S
     ref = None
+    import os
+    runs = []
     for k in [int(x) for x in args.kernels.split(",")]:
+        if args.env:
+            name, vals = args.env.split("=")
+            runs += [(k, name, v) for v in vals.split(",")]
+        else:
+            runs.append((k, None, None))
+    for k, ename, evalue in runs:
+        if ename:
+            os.environ[ename] = evalue
         ex, _keep = N.make_exec([0], k)
         plan = C.c_void_p()
         N.check(L.sf_plan_create(problem.ref, metric, prec, 0, stop, C.byref(ex), C.byref(plan)))
@@ -68,7 +79,8 @@ def main():
         best = min(times[1:])
         print(json.dumps({"kernel": k, "total_ms": best[0], "stripe_ms": best[1],
                           "updates_alg": st.updates_alg, "updates_exec": st.updates_exec,
-                          "alg_per_s": st.updates_alg / (best[0] / 1e3), "bitwise_same_as_first": same, "max_rel_diff_vs_first": rel}),
+                          "alg_per_s": st.updates_alg / (best[0] / 1e3), "bitwise_same_as_first": same, "max_rel_diff_vs_first": rel,
+                          "env": f"{ename}={evalue}" if ename else None}),
               flush=True)
 
 
