@@ -33,7 +33,8 @@ namespace sf {
 __global__ void i2_row_key_kernel(const uint32_t* __restrict__ rows, int64_t stride, int32_t E,
                                   int32_t n, int32_t heavy_min, uint32_t* __restrict__ keys,
                                   int32_t* __restrict__ vals, uint8_t* __restrict__ dense,
-                                  unsigned int* __restrict__ n_heavy) {
+                                  unsigned int* __restrict__ n_heavy,
+                                  int32_t* __restrict__ mcount = nullptr) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -49,6 +50,7 @@ __global__ void i2_row_key_kernel(const uint32_t* __restrict__ rows, int64_t str
       keys[r] = x >= heavy_min ? static_cast<uint32_t>(n - x) : static_cast<uint32_t>(n + 1);
       vals[r] = static_cast<int32_t>(r);
       dense[r] = dn ? 1 : 0;
+      if (mcount) mcount[r] = m;
       if (x >= heavy_min) atomicAdd(n_heavy, 1u);
     }
   }

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstdint>
 #include <cstring>
@@ -387,8 +388,9 @@ struct DeviceState {
   size_t cub_bytes = 0;
   // intersection v2 (kernel 6): permuted rows, 64-row words, group masks
   DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm, nheavy;
-  // split path (kernel 10): light-row sums per slot
-  DevBuf lightsum;
+  // split path (kernel 10): light-row sums per slot, |S_e| per row
+  DevBuf lightsum, mcount;
+  int32_t light_pass = 0;  // stripes per light-sum pass (memory-bounded)
   size_t sort_bytes = 0;
   std::vector<cudaEvent_t> events;
   ~DeviceState() {
@@ -454,7 +456,7 @@ struct SplitCfg {
 
 // |X_e| threshold of the split path: rows at or above it are walked.
 int split_heavy_min(int n) {
-  double frac = 0.01;
+  double frac = 0.012;
   if (const char* e = std::getenv("SF_HEAVY_FRAC")) frac = std::atof(e);
   return std::max(2, static_cast<int>(frac * n));
 }
@@ -654,6 +656,29 @@ sf_status isect2_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   return SF_OK;
 }
 
+// Light rows -> light sums of stripes [s0, s1) (lightsum row 0 = stripe s0);
+// with_colsum: also add the light rows to the column sums (first pass only).
+sf_status split_scatter(sf_plan* plan, DeviceState& d, cudaStream_t st, int s0, int s1, bool with_colsum) {
+  const int n = plan->n;
+  const int64_t E = plan->E;
+  const int heavy_min = split_heavy_min(n);
+  SF_CUDA(cudaMemsetAsync(d.lightsum.p, 0, static_cast<size_t>(s1 - s0) * static_cast<size_t>(n) * 16, st));
+  constexpr int NW = SplitCfg::SCATTER_NW;
+  const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
+  auto* kern = sp_light_scatter_kernel<NW, 8>;
+  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int blocks = static_cast<int>(std::min<int64_t>((E + NW - 1) / NW, 148 * 16));
+  kern<<<blocks, 32 * NW, smem, st>>>(d.emb.as<uint32_t>(), plan->row_words, plan->E, n, d.perm.as<int32_t>(),
+                                     d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>(),
+                                     d.fix.as<unsigned long long>(), plan->lo_bits, s0, s1,
+                                     d.lightsum.as<double>(),
+                                     with_colsum ? d.colsum.as<unsigned long long>() : nullptr,
+                                     d.exec_ctr.as<unsigned long long>(), heavy_min);
+  SF_CUDA(cudaGetLastError());
+  plan->stats.launches++;
+  return SF_OK;
+}
+
 sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   const int n = plan->n;
   const int64_t E = plan->E;
@@ -662,15 +687,13 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   const int64_t n_ext = sparse_n_ext(n);
   const int64_t stride = plan->row_words;
   const int heavy_min = split_heavy_min(n);
-  const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
   SF_CUDA(cudaMemsetAsync(d.dmask.p, 0, static_cast<size_t>(W) * 8, st));
   SF_CUDA(cudaMemsetAsync(d.cacc.p, 0, 2 * sizeof(unsigned long long), st));
   SF_CUDA(cudaMemsetAsync(d.colsum.p, 0, static_cast<size_t>(n) * 4 * sizeof(unsigned long long), st));
   SF_CUDA(cudaMemsetAsync(d.nheavy.p, 0, 4, st));
-  SF_CUDA(cudaMemsetAsync(d.lightsum.p, 0, slots * 16, st));
   i2_row_key_kernel<<<grid_for(E * 32, 256), 256, 0, st>>>(
       d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min, d.keys.as<uint32_t>(), d.vals.as<int32_t>(),
-      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>());
+      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>());
   size_t stmp = d.sort_bytes;
   SF_CUDA(cub::DeviceRadixSort::SortPairs(d.sorttmp.p, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
                                           d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
@@ -686,19 +709,10 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   sp_heavy_colsum_kernel<<<grid_for(n, 128), 128, 0, st>>>(
       d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>(),
       d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.colsum.as<unsigned long long>());
-  {
-    constexpr int NW = SplitCfg::SCATTER_NW;
-    const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
-    auto* kern = sp_light_scatter_kernel<NW>;
-    SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const int blocks = static_cast<int>(std::min<int64_t>((E + NW - 1) / NW, 148 * 16));
-    kern<<<blocks, 32 * NW, smem, st>>>(d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min,
-                                       d.fix.as<unsigned long long>(), plan->lo_bits, d.a, d.b,
-                                       d.lightsum.as<double>(), d.colsum.as<unsigned long long>(),
-                                       d.exec_ctr.as<unsigned long long>(), heavy_min);
-  }
+  // first light pass (the one that also adds the light rows' column sums)
+  SF_TRY(split_scatter(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), true));
   SF_CUDA(cudaGetLastError());
-  plan->stats.launches += 8;  // key, sort, perm, transpose, extend, colsum, scatter (+ memsets)
+  plan->stats.launches += 7;  // key, sort, perm, transpose, extend, colsum (+ memsets)
   return SF_OK;
 }
 
@@ -713,7 +727,9 @@ sf_status launch_split_rs(const SplitArgs& a, cudaStream_t st) {
 }
 
 // Default: 16 slots per lane, 8 u columns per CTA, v words loaded one 32-bit
-// half at a time (measured best at the EMP shape: profiles/r01_ab_c3_split_variants*).
+// half at a time (measured best at the EMP shape: profiles/r01_ab_c3_split_variants*),
+// and at most 128 registers so two CTAs (16 warps) fit per SM: left alone,
+// ptxas drifts to 152 with small source changes, halving occupancy (+37% time).
 // SF_SPLIT_VARIANT selects the measured alternatives for A/B.
 template <class Real>
 sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
@@ -724,7 +740,7 @@ sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
     case 2: return launch_split_rs<Real, 16, 4, false, true>(a, st);  // + u word prefetch
     case 3: return launch_split_rs<Real, 8, 8>(a, st);                // 8 slots per lane
     case 4: return launch_split_rs<Real, 16, 4, false, false, true>(a, st);
-    default: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true>(a, st);
+    default: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2>(a, st);
   }
 }
 
@@ -957,8 +973,6 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       a.cacc = d.cacc.as<unsigned long long>();
       a.n_ext = sparse_n_ext(n);
       a.n = n;
-      a.s_begin = d.a;
-      a.s_end = d.b;
       a.out_begin = d.a;
       a.lo_bits = plan->lo_bits;
       a.scale = plan->scale;
@@ -966,28 +980,32 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       a.dist = d.dist.p;
       a.tot = d.tot.p;
       a.counters = d.exec_ctr.as<unsigned long long>();
-      if (!host_d) {
-        SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
-      } else {
-        // chunks of whole 512-stripe tiles; copy each as soon as it is done
-        const int span = d.b - d.a;
-        const int tile = 32 * SplitCfg::RS;
-        const int nch = std::max(1, std::min(8, span / (4 * tile)));
+      // light-sum passes (one unless memory is short); within a pass, with a
+      // host destination, chunks of whole 512-stripe tiles whose D2H copy
+      // overlaps the next chunk's compute
+      const int tile = 32 * SplitCfg::RS;
+      int ci = 0;
+      if (host_d && !d.copy_stream) SF_CUDA(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking));
+      for (int p0 = d.a; p0 < d.b; p0 += d.light_pass) {
+        const int p1 = std::min(d.b, p0 + d.light_pass);
+        if (p0 != d.a) SF_TRY(split_scatter(plan, d, st, p0, p1, false));
+        a.gl_begin = p0;
+        const int span = p1 - p0;
+        const int nch = host_d ? std::max(1, std::min(8, span / (4 * tile))) : 1;
         const int per = (span + nch - 1) / nch;
         const int step = (per + tile - 1) / tile * tile;
-        if (!d.copy_stream) SF_CUDA(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking));
-        while (static_cast<int>(d.chunk_events.size()) < nch) {
-          cudaEvent_t e;
-          SF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-          d.chunk_events.push_back(e);
-        }
-        int ci = 0;
-        for (int c0 = d.a; c0 < d.b; c0 += step, ++ci) {
-          const int c1 = std::min(d.b, c0 + step);
+        for (int c0 = p0; c0 < p1; c0 += step, ++ci) {
+          const int c1 = std::min(p1, c0 + step);
           a.s_begin = c0;
           a.s_end = c1;
           SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
           plan->stats.launches++;
+          if (!host_d) continue;
+          while (static_cast<int>(d.chunk_events.size()) <= ci) {
+            cudaEvent_t e;
+            SF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            d.chunk_events.push_back(e);
+          }
           SF_CUDA(cudaEventRecord(d.chunk_events[static_cast<size_t>(ci)], st));
           SF_CUDA(cudaStreamWaitEvent(d.copy_stream, d.chunk_events[static_cast<size_t>(ci)], 0));
           const size_t off = static_cast<size_t>(c0 - d.a) * n * w;
@@ -998,8 +1016,8 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
             SF_CUDA(cudaMemcpyAsync(static_cast<char*>(host_t) + off, d.tot.as<char>() + off, bytes,
                                     cudaMemcpyDeviceToHost, d.copy_stream));
         }
-        plan->stats.launches--;  // counted once more below
       }
+      plan->stats.launches--;  // counted once more below
     } else if (plan->kernel >= 6) {
       Isect2Args a;
       const int64_t W = (plan->E + 63) / 64;
@@ -1241,9 +1259,27 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));
       if (plan->kernel >= 6) {
         SF_TRY(isect2_prepare(plan.get(), d, p));
-        if (plan->kernel == 10)
-          SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n) * 16,
-                                  "light-row sums"));
+        if (plan->kernel == 10) {
+          // light sums for the whole range if they fit next to everything
+          // else, else for passes of whole 512-stripe tiles
+          size_t freeb = 0, totalb = 0;
+          SF_CUDA(cudaMemGetInfo(&freeb, &totalb));
+          const size_t per_stripe = static_cast<size_t>(n) * 16;
+          const size_t reserve = (1ull << 30);
+          size_t fit = freeb > reserve ? (freeb - reserve) / per_stripe : 0;
+          if (ex && ex->mem_budget_bytes > 0)
+            fit = std::min(fit, static_cast<size_t>(ex->mem_budget_bytes) / per_stripe);
+          const int span = d.b - d.a;
+          int pass = static_cast<int>(std::min<size_t>(fit, static_cast<size_t>(span)));
+          if (pass < span) pass = std::max(512, pass / 512 * 512);
+          if (const char* e = std::getenv("SF_LIGHT_PASS")) pass = std::max(1, std::atoi(e));  // tests
+          d.light_pass = std::min(pass, span);
+          if (std::getenv("SF_DEBUG"))
+            std::fprintf(stderr, "stripefrac: device %d stripes [%d,%d): light pass %d stripes (free %zu MB)\n",
+                         d.dev, d.a, d.b, d.light_pass, freeb >> 20);
+          SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * per_stripe, "light-row sums"));
+          SF_TRY(d.mcount.alloc(d.dev, static_cast<size_t>(plan->E) * 4, "row presence counts"));
+        }
       } else {
         SF_TRY(sparse_prepare(plan.get(), d, p));
         if (plan->kernel == 5) SF_TRY(isect_prepare(plan.get(), d, p));

@@ -123,18 +123,42 @@ __global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx
   }
 }
 
-// Light rows: one warp per row. Lists the members of X_e (in sample order)
-// in shared memory, adds the row to its members' column sums, and adds its
-// limbs to the slot of every member pair whose stripe lies in
+// Light rows: one warp per row, over the light tail perm[H..E) of the row
+// permutation (|S_e| from the row-key kernel). Lists the members of X_e (in
+// sample order) in shared memory, adds the row to its members' column sums,
+// and adds its limbs to the slot of every member pair whose stripe lies in
 // [s_begin, s_end). gl: (s_end - s_begin) x n x (hi, lo) doubles.
 // Pair {a < b}, d = b - a: slot (s = d-1, k = a) when d-1 < S, and slot
 // (s = n-d-1, k = b) when n-d-1 < S (both for d = n/2, n even: the
-// reference's duplicated half stripe).
-template <int NW>
+// reference's duplicated half stripe). Rows with up to 32*MAXT members keep
+// them in registers (lane j holds members j, j+32, ...) so the pair loop
+// needs one broadcast shared load per a instead of one per pair.
+__device__ __forceinline__ void sp_add_pair(int a, int b, int n, int S, int s_begin, int s_end,
+                                            double2 L, double* __restrict__ gl,
+                                            unsigned long long& pairs) {
+  const int d = b - a;
+  int s = d - 1;
+  if (s < S && s >= s_begin && s < s_end) {
+    double* cell = gl + 2 * (static_cast<int64_t>(s - s_begin) * n + a);
+    atomicAdd(cell, L.x);
+    atomicAdd(cell + 1, L.y);
+    ++pairs;
+  }
+  s = n - d - 1;
+  if (s < S && s >= s_begin && s < s_end) {
+    double* cell = gl + 2 * (static_cast<int64_t>(s - s_begin) * n + b);
+    atomicAdd(cell, L.x);
+    atomicAdd(cell + 1, L.y);
+    ++pairs;
+  }
+}
+
+template <int NW, int MAXT>
 __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
-    const uint32_t* __restrict__ rows, int64_t stride, int32_t E, int32_t n, int32_t heavy_min,
-    const unsigned long long* __restrict__ fix, int32_t lo_bits, int32_t s_begin, int32_t s_end,
-    double* __restrict__ gl, unsigned long long* __restrict__ colsum,
+    const uint32_t* __restrict__ rows, int64_t stride, int32_t E, int32_t n,
+    const int32_t* __restrict__ perm, const unsigned int* __restrict__ n_heavy,
+    const int32_t* __restrict__ mcount, const unsigned long long* __restrict__ fix, int32_t lo_bits,
+    int32_t s_begin, int32_t s_end, double* __restrict__ gl, unsigned long long* __restrict__ colsum,
     unsigned long long* __restrict__ pairs_out, int32_t list_cap) {
   extern __shared__ int32_t sp_members[];
   const int lane = threadIdx.x & 31;
@@ -144,20 +168,19 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
   const int64_t warp = static_cast<int64_t>(blockIdx.x) * NW + wib;
   const int64_t nwarps = static_cast<int64_t>(gridDim.x) * NW;
   const uint32_t tail = (n & 31) ? ((1u << (n & 31)) - 1u) : 0xffffffffu;
+  const int64_t H = *n_heavy;
   unsigned long long pairs = 0;
-  for (int64_t r = warp; r < E; r += nwarps) {
-    const uint32_t* row = rows + r * stride;
-    int m = 0;
-    for (int64_t i = lane; i < stride; i += 32) m += __popc(__ldg(row + i));
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) m += __shfl_xor_sync(0xffffffffu, m, off);
+  for (int64_t idx = H + warp; idx < E; idx += nwarps) {
+    const int r = perm[idx];
+    const int m = mcount[r];
     const bool dense = 2 * m > n;
     const int x = dense ? n - m : m;
-    if (x >= heavy_min || x == 0) continue;  // heavy rows are walked; empty rows add nothing
+    if (x == 0) continue;  // adds nothing anywhere
+    const uint32_t* row = rows + static_cast<int64_t>(r) * stride;
     // members in sample order: warp-wide compaction of the (possibly
     // complemented) row words
     int count = 0;
-    for (int64_t base = 0; base < stride; base += 32) {
+    for (int64_t base = 0; base < stride && count < x; base += 32) {
       const int64_t i = base + lane;
       uint32_t wd = 0u;
       if (i < stride) {
@@ -183,7 +206,7 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
     const double2 L = limbs_of(fix[r], lo_bits);
     const unsigned long long lh = static_cast<unsigned long long>(L.x);
     const unsigned long long ll = static_cast<unsigned long long>(L.y);
-    for (int i = lane; i < x; i += 32) {
+    for (int i = lane; colsum && i < x; i += 32) {  // colsum null on later passes
       const int c = mem[i];
       atomicAdd(colsum + c, lh);
       atomicAdd(colsum + n + c, ll);
@@ -192,25 +215,22 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
         atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, ll);
       }
     }
-    for (int i = 0; i + 1 < x; ++i) {
-      const int a = mem[i];
-      for (int j = i + 1 + lane; j < x; j += 32) {
-        const int b = mem[j];
-        const int d = b - a;
-        int s = d - 1;
-        if (s < S && s >= s_begin && s < s_end) {
-          double* cell = gl + 2 * (static_cast<int64_t>(s - s_begin) * n + a);
-          atomicAdd(cell, L.x);
-          atomicAdd(cell + 1, L.y);
-          ++pairs;
+    if (x <= 32 * MAXT) {
+      int bv[MAXT];
+#pragma unroll
+      for (int t = 0; t < MAXT; ++t) bv[t] = (lane + 32 * t < x) ? mem[lane + 32 * t] : 0;
+      for (int i = 0; i + 1 < x; ++i) {
+        const int a = mem[i];  // broadcast
+#pragma unroll
+        for (int t = 0; t < MAXT; ++t) {
+          const int j = lane + 32 * t;
+          if (j > i && j < x) sp_add_pair(a, bv[t], n, S, s_begin, s_end, L, gl, pairs);
         }
-        s = n - d - 1;
-        if (s < S && s >= s_begin && s < s_end) {
-          double* cell = gl + 2 * (static_cast<int64_t>(s - s_begin) * n + b);
-          atomicAdd(cell, L.x);
-          atomicAdd(cell + 1, L.y);
-          ++pairs;
-        }
+      }
+    } else {
+      for (int i = 0; i + 1 < x; ++i) {
+        const int a = mem[i];
+        for (int j = i + 1 + lane; j < x; j += 32) sp_add_pair(a, mem[j], n, S, s_begin, s_end, L, gl, pairs);
       }
     }
     __syncwarp();
@@ -236,7 +256,8 @@ struct SplitArgs {
   int64_t n_ext;
   int32_t n;
   int32_t s_begin, s_end;  // stripes computed by this launch
-  int32_t out_begin;       // stripe held by row 0 of dist / tot / gl
+  int32_t out_begin;       // stripe held by row 0 of dist / tot
+  int32_t gl_begin;        // stripe held by row 0 of gl (the light-sum pass)
   int32_t lo_bits, scale, finalize;
   void* dist;
   void* tot;
@@ -381,7 +402,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
     const int64_t li = l0 + 32 * i;
     const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
     const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
-    const double2 light = reinterpret_cast<const double2*>(a.gl)[off];
+    const double2 light =
+        reinterpret_cast<const double2*>(a.gl)[static_cast<int64_t>(s - a.gl_begin) * n + k];
     const long long Gh_ = static_cast<long long>(gh[i]) + static_cast<long long>(light.x);
     const long long Gl_ = static_cast<long long>(gl[i]) + static_cast<long long>(light.y);
     const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm]) + ch - Gh_;

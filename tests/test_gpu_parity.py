@@ -420,3 +420,30 @@ def test_stripe_shards_match_single_device(device_ok, kernel):
                 N.check(N.lib().sf_compute_stripes(problem.ref, metric, 8, start, stop, N.ptr(d), N.ptr(t),
                                                    1, C.byref(ex), C.byref(st)))
                 assert np.array_equal(d, d1) and np.array_equal(t, t1)
+
+
+@pytest.mark.parametrize("light_pass", ["1", "3", "1000"])
+def test_split_light_passes_and_pinned_download(device_ok, light_pass, monkeypatch):
+    """Kernel 10 with the light sums built in several stripe passes (as when
+    memory is short) and with the chunked, overlapped download into pinned
+    host memory: bitwise equal to the single-pass, pageable run."""
+    import torch
+    inst = sf.random_instance(93, 301, 1200, 0.01)
+    problem = sf.flatten(inst.tree, inst.table)
+    n = problem.n_samples
+    start, stop = 3, n // 2
+    want_d, want_t, _ = _gpu_stripes(problem, 1, 8, start, stop, N.KERNEL_SPLIT)
+    monkeypatch.setenv("SF_LIGHT_PASS", light_pass)
+    monkeypatch.setenv("SF_HEAVY_FRAC", "0.05")
+    ref_d, ref_t, _ = _gpu_stripes(problem, 1, 8, start, stop, N.KERNEL_SPLIT)
+    assert np.array_equal(ref_d, want_d) and np.array_equal(ref_t, want_t)
+    for prec, dt in ((8, torch.float64), (4, torch.float32)):
+        d = torch.full(((stop - start) * n,), float("nan"), dtype=dt, pin_memory=True).numpy()
+        t = torch.full(((stop - start) * n,), float("nan"), dtype=dt, pin_memory=True).numpy()
+        ex, _keep = N.make_exec([0], N.KERNEL_SPLIT)
+        st = N.sf_stats()
+        N.check(N.lib().sf_compute_stripes(problem.ref, 1, prec, start, stop, N.ptr(d), N.ptr(t), 1,
+                                           C.byref(ex), C.byref(st)))
+        pd, pt, _ = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_SPLIT)
+        assert np.array_equal(d.reshape(stop - start, n), pd)
+        assert np.array_equal(t.reshape(stop - start, n), pt)
