@@ -693,7 +693,8 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   SF_CUDA(cudaMemsetAsync(d.nheavy.p, 0, 4, st));
   i2_row_key_kernel<<<grid_for(E * 32, 256), 256, 0, st>>>(
       d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min, d.keys.as<uint32_t>(), d.vals.as<int32_t>(),
-      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>());
+      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>(),
+      std::getenv("SF_HEAVY_BY_WEIGHT") == nullptr);
   size_t stmp = d.sort_bytes;
   SF_CUDA(cub::DeviceRadixSort::SortPairs(d.sorttmp.p, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
                                           d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
