@@ -43,16 +43,25 @@ CONFIGS = {
     "c3f32": dict(seed=3, n=25000, leaves=300000, density=0.002, subset=0,
                   metric="unweighted", precision="fp32",
                   workload="C3: EMP-shape synthetic, 25k samples x 300k-tip tree, density 0.002, UW fp32"),
+    "c4": dict(seed=3, n=25000, leaves=300000, density=0.002, subset=0,
+               metric="generalized", alpha=0.5, precision="fp64",
+               workload="C4: generalized UniFrac alpha=0.5 fp64 on the C3 synthetic (25k samples x 300k tips)"),
+    "c4f32": dict(seed=3, n=25000, leaves=300000, density=0.002, subset=0,
+                  metric="generalized", alpha=0.5, precision="fp32",
+                  workload="C4: generalized UniFrac alpha=0.5 fp32 on the C3 synthetic (25k samples x 300k tips)"),
+    "c3wn": dict(seed=3, n=25000, leaves=300000, density=0.002, subset=0,
+                 metric="weighted-normalized", precision="fp64",
+                 workload="C3 shape, weighted normalized fp64 (25k samples x 300k tips)"),
     "c5": dict(seed=5, n=113721, leaves=300000, density=0.002, subset=0,
                metric="unweighted", precision="fp32",
                workload="C5: 113,721-sample synthetic, 300k-tip tree, density 0.002, UW fp32"),
     "small": dict(seed=7, n=4000, leaves=40000, density=0.002, subset=0,
                   metric="unweighted", precision="fp64", workload="small UW fp64 (quick check)"),
 }
-METRIC_CODE = {"unweighted": 1, "weighted-unnormalized": 2, "weighted-normalized": 3}
+METRIC_CODE = {"unweighted": 1, "weighted-unnormalized": 2, "weighted-normalized": 3, "generalized": 4}
 # algorithmic FP64/FP32 flops per update of update_entry (kernels.hpp:55-66),
 # FMA counted as 2: UW = sub, fma, max, fma; WN = sub, fma, add, fma; WU = sub, fma
-FLOPS_PER_UPDATE = {1: 6, 2: 3, 3: 6}
+FLOPS_PER_UPDATE = {1: 6, 2: 3, 3: 6, 4: 7}  # generalized: add, sub, div, mul, fma, add + pow (counted as 1)
 
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                  0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
@@ -167,8 +176,8 @@ def run_ours(args, cfg):
     S = n // 2
     stop_all = min(S, args.stripes) if args.stripes else S
     a, b = shard.rank_range(0, stop_all, rank, world)
-    kernel = {"auto": 0, "dense": 1, "sparse": 2, "flat32": 3, "flat64": 4, "isect": 5, "isect2": 6, "isect3": 7, "isect4": 8, "isect5": 9, "split": 10}[args.kernel]
-    ex, _keep = N.make_exec([local], kernel)
+    kernel = {"auto": 0, "dense": 1, "sparse": 2, "flat32": 3, "flat64": 4, "isect": 5, "isect2": 6, "isect3": 7, "isect4": 8, "isect5": 9, "split": 10, "wsparse": 11}[args.kernel]
+    ex, _keep = N.make_exec([local], kernel, alpha=cfg.get("alpha", 1.0))
     plan = C.c_void_p()
     t0 = time.perf_counter()
     N.check(L.sf_plan_create(problem.ref, metric, prec, a, b, C.byref(ex), C.byref(plan)))
@@ -277,7 +286,8 @@ def run_ours(args, cfg):
             "bound": "fp64" if prec == 8 else "fp32",
             "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3), "unit": "TFLOP/s",
             "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None, "traffic": None,
-            "kernel": "stripe_dense_kernel" if kernel == 1 else "stripe walk",
+            "kernel": ("stripe_dense_kernel" if kernel == 1 else
+                       "stripe_wsparse_kernel (present-row walk)" if metric != 1 else "stripe walk"),
             "peak_source": "measured DFMA/FFMA loop (tools/fp_peaks.cu) on this device",
             "flops_per_update": fl, "updates_exec_per_step": int(uexec_all / args.steps),
             "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
@@ -286,7 +296,7 @@ def run_ours(args, cfg):
 
     # ---- CPU baseline (oracle restatement, bounded sample, all host threads)
     cpu = None
-    if not args.no_cpu_baseline and world == 1:
+    if not args.no_cpu_baseline and world == 1 and metric != 4:
         sys.path.insert(0, str(ROOT / "tests"))
         import oracle_port
         threads = os.cpu_count() or 1
@@ -312,6 +322,7 @@ def run_ours(args, cfg):
         "config": {"workload": cfg["workload"], "seed": cfg["seed"], "n_samples": n,
                    "tree_tips": cfg["leaves"], "rows_E": E, "density": cfg["density"],
                    "metric": cfg["metric"], "stripes": [0, stop_all],
+                   **({"alpha": cfg["alpha"]} if "alpha" in cfg else {}),
                    "parallelism": f"stripe-range x{world}", "kernel": args.kernel,
                    "l2": "inputs larger than L2 (no flush)"},
         "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
@@ -329,6 +340,9 @@ def run_reference(args, cfg):
     if rank != 0:
         return None
     metric = cfg["metric"]
+    if metric == "generalized":
+        return {"impl": "reference", "unavailable": "the reference implements no generalized UniFrac "
+                                                    "(common.hpp:19); C4 is an extension"}
     n = cfg["n"]
     threads = os.cpu_count() or 1
     driver = ROOT / "oracle" / "_ref" / "ref_driver"
@@ -383,7 +397,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--kernel", choices=["auto", "dense", "sparse", "flat32", "flat64", "isect", "isect2", "isect3", "isect4", "isect5", "split"],
+    ap.add_argument("--kernel", choices=["auto", "dense", "sparse", "flat32", "flat64", "isect", "isect2", "isect3", "isect4", "isect5", "split", "wsparse"],
                     default="auto")
     ap.add_argument("--stripes", type=int, default=0, help="limit to stripes [0, N) (debug)")
     ap.add_argument("--e2e-steps", type=int, default=3)

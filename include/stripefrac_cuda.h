@@ -27,7 +27,7 @@
 extern "C" {
 #endif
 
-#define SF_ABI_VERSION 2
+#define SF_ABI_VERSION 3
 
 typedef enum sf_status {
   SF_OK = 0,
@@ -41,7 +41,12 @@ typedef enum sf_status {
 typedef enum sf_metric {
   SF_UNWEIGHTED = 1,
   SF_WEIGHTED_UNNORMALIZED = 2,
-  SF_WEIGHTED_NORMALIZED = 3
+  SF_WEIGHTED_NORMALIZED = 3,
+  /* Extension (not in the reference, parity unpinned): generalized UniFrac
+   * with exponent sf_exec.alpha over the weighted embedding (Chen et al.
+   * 2012, in Striped UniFrac's form); finalize divides d by t like WN. It
+   * has no .strf code in the reference's format. */
+  SF_GENERALIZED = 4
 } sf_metric;
 
 /* Precision codes are the scalar width in bytes (.strf byte 5). */
@@ -75,9 +80,11 @@ typedef struct sf_exec {
   int32_t kernel;           /* 0 = auto, 1 = dense tiled; unweighted only: 2 = sparse bit walk
                                (bitwise; 3/4 flattened variants), 5-9 = intersection walks and
                                10 = split heavy-walk/light-scatter (exact fixed-point sums; the
-                               default) */
+                               default); weighted only: 11 = sparse walk over present rows (the
+                               default; the only kernel for SF_GENERALIZED) */
   int32_t flags;            /* bit 0: SF_EXEC_EXACT_NO_FMA: bitwise-identical results (weighted:
                                no FMA; unweighted auto: the sparse walk instead of kernel 10) */
+  double alpha;             /* SF_GENERALIZED only: the exponent, finite, >= 0 (ABI v3) */
 } sf_exec;
 
 #define SF_EXEC_EXACT_NO_FMA 1
@@ -169,6 +176,22 @@ sf_status sf_finalize(sf_precision prec, int64_t count, void* dist_inout, const 
  */
 sf_status sf_condense(sf_precision prec, int32_t n, int32_t start, int32_t stop,
                       const void* dist, double* out, int32_t device);
+
+/*
+ * Mantel permutation test on device. Replaces mantel (validate.cpp:111-159):
+ * m1, m2 are n x n row-major distance matrices (DistanceMatrix::values);
+ * r is the Pearson correlation of their condensed upper triangles and
+ * p = (1 + #{r_perm >= r}) / (1 + permutations), permutation p relabelling
+ * the samples of m2 with the reference's stream (mt19937_64 + std::shuffle
+ * seeded from splitmix64(seed ^ splitmix64(p + 1))). Errors as the
+ * reference: permutations < 1, n < 2, an asymmetric matrix (> 1e-12), zero
+ * variance. r_squared is r * r. The sample-id check is the caller's.
+ */
+sf_status sf_mantel(int32_t n, const double* m1, const double* m2, int32_t permutations,
+                    uint64_t seed, int32_t device, double* r_out, double* p_value_out);
+
+/* Host-only: permutation p of the reference's Mantel stream (n entries). */
+sf_status sf_mantel_permutation(int32_t n, uint64_t seed, int32_t p, int32_t* perm_out);
 
 #ifdef __cplusplus
 }

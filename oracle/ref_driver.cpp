@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <numeric>
 #include <random>
 #include <sstream>
 #include <string>
@@ -312,6 +313,69 @@ int cmd_golden(const std::string& dir, const std::string& demo_dir) {
   return 0;
 }
 
+// Mantel golden vectors (validate.cpp:111-159): reference DMs of seeded
+// instances, r / r^2 / p for several seeds and permutation counts, and the
+// first permutations of a seed (the stream the GPU path must reproduce).
+std::uint64_t mix64(std::uint64_t x) {  // validate.cpp:101-106 (file-local there)
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+int cmd_mantel_golden(const std::string& dir) {
+  std::string j = "{\"cases\":[";
+  struct C { std::uint64_t seed; int n, leaves; double dens; };
+  const C cases[] = {{71, 40, 120, 0.1}, {72, 97, 300, 0.05}, {73, 160, 500, 0.02}};
+  bool first = true;
+  for (const C& c : cases) {
+    const SynthInstance inst = random_instance(c.seed, c.n, c.leaves, c.dens);
+    const auto uw = compute_distance_matrix<double>(inst.tree, inst.table, cfg_of(Metric::Unweighted, Precision::Fp64));
+    const auto wn = compute_distance_matrix<double>(inst.tree, inst.table, cfg_of(Metric::WeightedNormalized, Precision::Fp64));
+    const auto wn32 = compute_distance_matrix<float>(inst.tree, inst.table, cfg_of(Metric::WeightedNormalized, Precision::Fp32));
+    // an independent instance of the same size: r near 0, p-values in the bulk
+    const SynthInstance other = random_instance(c.seed + 100, c.n, c.leaves, c.dens);
+    auto wn_other = compute_distance_matrix<double>(other.tree, other.table, cfg_of(Metric::WeightedNormalized, Precision::Fp64));
+    wn_other.sample_ids = wn.sample_ids;  // same labels: mantel compares by position
+    char params[160];
+    std::snprintf(params, sizeof(params), "\"seed\":%llu,\"n\":%d,\"leaves\":%d,\"density\":%g",
+                  static_cast<unsigned long long>(c.seed), c.n, c.leaves, c.dens);
+    struct R { const char* a; const char* b; const DistanceMatrix* x; const DistanceMatrix* y; int perms; std::uint64_t ms; };
+    const R runs[] = {{"unweighted-fp64", "weighted-normalized-fp64", &uw, &wn, 199, 3},
+                      {"unweighted-fp64", "weighted-normalized-fp64", &uw, &wn, 999, 17},
+                      {"weighted-normalized-fp64", "weighted-normalized-fp32", &wn, &wn32, 99, 11},
+                      {"unweighted-fp64", "weighted-normalized-fp64-other", &uw, &wn_other, 999, 5},
+                      {"unweighted-fp64", "weighted-normalized-fp64-other", &uw, &wn_other, 499, 6}};
+    for (const R& r : runs) {
+      const auto res = mantel(*r.x, *r.y, r.perms, r.ms);
+      if (!first) j += ",";
+      first = false;
+      j += std::string("{") + params + ",\"x\":" + quote(r.a) + ",\"y\":" + quote(r.b) +
+           ",\"permutations\":" + std::to_string(r.perms) + ",\"mantel_seed\":" + std::to_string(r.ms) +
+           ",\"r\":" + num(res.r) + ",\"r_squared\":" + num(res.r_squared) + ",\"p_value\":" +
+           num(res.p_value) + "}";
+    }
+  }
+  j += "],\"permutations\":[";
+  first = true;
+  for (int n : {2, 7, 50})
+    for (std::uint64_t seed : {0ull, 7ull, 123456789ull})
+      for (int p = 0; p < 3; ++p) {
+        std::vector<int> perm(static_cast<std::size_t>(n));
+        std::mt19937_64 rng(mix64(seed ^ mix64(static_cast<std::uint64_t>(p) + 1)));
+        std::iota(perm.begin(), perm.end(), 0);
+        std::shuffle(perm.begin(), perm.end(), rng);
+        if (!first) j += ",";
+        first = false;
+        j += "{\"n\":" + std::to_string(n) + ",\"seed\":" + std::to_string(seed) + ",\"p\":" +
+             std::to_string(p) + ",\"perm\":[";
+        for (int i = 0; i < n; ++i) j += (i ? "," : "") + std::to_string(perm[static_cast<std::size_t>(i)]);
+        j += "]}";
+      }
+  write_file(dir + "/mantel.json", j + "]}");
+  return 0;
+}
+
 // digest of a random_instance, to pin the port of the generator at scale
 int cmd_instance(std::uint64_t seed, int n, int leaves, double density, int subset) {
   const auto t0 = std::chrono::steady_clock::now();
@@ -418,6 +482,7 @@ int main(int argc, char** argv) {
     if (argc < 2) throw Error("usage: ref_driver golden|instance|bench|dm ...");
     const std::string cmd = argv[1];
     if (cmd == "golden" && argc >= 4) return cmd_golden(argv[2], argv[3]);
+    if (cmd == "mantel_golden" && argc >= 3) return cmd_mantel_golden(argv[2]);
     if (cmd == "instance" && argc >= 7)
       return cmd_instance(std::strtoull(argv[2], nullptr, 10), std::atoi(argv[3]), std::atoi(argv[4]),
                           std::atof(argv[5]), std::atoi(argv[6]));

@@ -22,7 +22,17 @@
  *   - stripe pair (k, (k+s+1) mod n)                         stripes.cpp:23-28
  * Stripe ranges are split over threads with the reference's worker formula
  * (kernels.hpp:302-303).
+ *
+ * Generalized UniFrac (metric 4, orc_compute_stripes_generalized) is NOT in
+ * the reference (common.hpp:19): PARITY UNPINNED. It
+ * restates the published definition (Chen et al. 2012, generalized UniFrac
+ * d^(a) = sum b (pA+pB)^a |pA-pB|/(pA+pB) / sum b (pA+pB)^a) in the striped
+ * form of Striped UniFrac (McDonald et al. 2018, the paper this reference
+ * re-implements): over the weighted (relative-abundance) embedding, per row
+ *     s = u + v; if (s != 0) { w = pow(s, a) * L; d += w * (|u-v| / s); t += w; }
+ * then finalize d / t. a = 1 is weighted normalized UniFrac up to rounding.
  */
+#include <math.h>
 #include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -41,7 +51,7 @@ typedef struct orc_problem {
   const double* sample_totals;
 } orc_problem;
 
-enum { ORC_UW = 1, ORC_WU = 2, ORC_WN = 3 };
+enum { ORC_UW = 1, ORC_WU = 2, ORC_WN = 3, ORC_GEN = 4 };
 
 /* ---------------------------------------------------------------- rows */
 /* Embedding rows [0, E) are produced one at a time in postorder; each row is
@@ -116,9 +126,10 @@ int orc_embed_rows(const orc_problem* p, int weighted, double* out) {
 }
 
 /* -------------------------------------------------------------- stripes */
-#define DEFINE_ACCUM(NAME, REAL)                                                     \
+#define DEFINE_ACCUM(NAME, REAL, POW)                                                \
   static void NAME(int metric, REAL* dist, REAL* tot, const REAL* emb,               \
-                   const REAL* lens, int filled, int n, int s0, int s1, int start) { \
+                   const REAL* lens, int filled, int n, int s0, int s1, int start,   \
+                   REAL alpha) {                                                     \
     for (int s = s0; s < s1; ++s) {                                                  \
       REAL* dm = dist + (int64_t)(s - start) * n;                                    \
       REAL* tt = tot ? tot + (int64_t)(s - start) * n : NULL;                        \
@@ -130,6 +141,17 @@ int orc_embed_rows(const orc_problem* p, int weighted, double* out) {
         for (int e = 0; e < filled; ++e) {                                           \
           const REAL u = emb[(int64_t)e * n + k], v = emb[(int64_t)e * n + l];       \
           const REAL L = lens[e];                                                    \
+          if (metric == ORC_GEN) {                                                   \
+            const REAL sum = u + v;                                                  \
+            if (sum != (REAL)0) {                                                    \
+              REAL sub = u - v;                                                      \
+              if (sub < (REAL)0) sub = -sub;                                         \
+              const REAL w = POW(sum, alpha) * L;                                    \
+              d += w * (sub / sum);                                                  \
+              t += w;                                                                \
+            }                                                                        \
+            continue;                                                                \
+          }                                                                          \
           REAL diff = u - v;                                                         \
           if (diff < (REAL)0) diff = -diff;                                          \
           d += diff * L;                                                             \
@@ -143,11 +165,12 @@ int orc_embed_rows(const orc_problem* p, int weighted, double* out) {
       }                                                                              \
     }                                                                                \
   }
-DEFINE_ACCUM(accum_f64, double)
-DEFINE_ACCUM(accum_f32, float)
+DEFINE_ACCUM(accum_f64, double, pow)
+DEFINE_ACCUM(accum_f32, float, powf)
 
 typedef struct job {
   int metric, prec, filled, n, s0, s1, start;
+  double alpha;
   void *dist, *tot;
   const void *emb, *lens;
 } job;
@@ -156,10 +179,10 @@ static void* run_job(void* arg) {
   const job* j = (const job*)arg;
   if (j->prec == 8)
     accum_f64(j->metric, (double*)j->dist, (double*)j->tot, (const double*)j->emb,
-              (const double*)j->lens, j->filled, j->n, j->s0, j->s1, j->start);
+              (const double*)j->lens, j->filled, j->n, j->s0, j->s1, j->start, j->alpha);
   else
     accum_f32(j->metric, (float*)j->dist, (float*)j->tot, (const float*)j->emb,
-              (const float*)j->lens, j->filled, j->n, j->s0, j->s1, j->start);
+              (const float*)j->lens, j->filled, j->n, j->s0, j->s1, j->start, (float)j->alpha);
   return NULL;
 }
 
@@ -170,6 +193,17 @@ static void* run_job(void* arg) {
 int orc_compute_stripes_rows(const orc_problem* p, int metric, int prec, int start, int stop,
                              void* dist, void* tot, int finalize, int threads, int batch,
                              int row_limit);
+static int compute_rows_alpha(const orc_problem* p, int metric, int prec, int start, int stop,
+                              void* dist, void* tot, int finalize, int threads, int batch,
+                              int row_limit, double alpha);
+
+/* Generalized UniFrac with exponent alpha (metric 4; parity unpinned). */
+int orc_compute_stripes_generalized(const orc_problem* p, double alpha, int prec, int start,
+                                    int stop, void* dist, void* tot, int finalize, int threads,
+                                    int batch) {
+  return compute_rows_alpha(p, ORC_GEN, prec, start, stop, dist, tot, finalize, threads, batch, 0,
+                            alpha);
+}
 
 int orc_compute_stripes(const orc_problem* p, int metric, int prec, int start, int stop,
                         void* dist, void* tot, int finalize, int threads, int batch) {
@@ -182,6 +216,13 @@ int orc_compute_stripes(const orc_problem* p, int metric, int prec, int start, i
 int orc_compute_stripes_rows(const orc_problem* p, int metric, int prec, int start, int stop,
                              void* dist, void* tot, int finalize, int threads, int batch,
                              int row_limit) {
+  return compute_rows_alpha(p, metric, prec, start, stop, dist, tot, finalize, threads, batch,
+                            row_limit, 1.0);
+}
+
+static int compute_rows_alpha(const orc_problem* p, int metric, int prec, int start, int stop,
+                              void* dist, void* tot, int finalize, int threads, int batch,
+                              int row_limit, double alpha) {
   const int n = p->n_samples;
   const int E = row_limit > 0 && row_limit < p->n_rows ? row_limit : p->n_rows;
   const size_t w = prec == 8 ? 8 : 4;
@@ -226,6 +267,7 @@ int orc_compute_stripes_rows(const orc_problem* p, int metric, int prec, int sta
     for (int wk = 0; wk < threads; ++wk) {
       job* j = &jobs[wk];
       j->metric = metric;
+      j->alpha = alpha;
       j->prec = prec;
       j->filled = filled;
       j->n = n;

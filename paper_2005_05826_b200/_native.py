@@ -15,9 +15,11 @@ LIB_PATH = Path(__file__).resolve().parent / "libstripefrac_cuda.so"
 
 SF_OK, SF_EINVAL, SF_ENOMEM, SF_ECUDA, SF_ESTATE = 0, 1, 2, 3, 4
 SF_UNWEIGHTED, SF_WEIGHTED_UNNORMALIZED, SF_WEIGHTED_NORMALIZED = 1, 2, 3
+SF_GENERALIZED = 4  # extension: generalized UniFrac (sf_exec.alpha); not in the reference
 SF_FP32, SF_FP64 = 4, 8
 SF_EXEC_EXACT_NO_FMA = 1
 KERNEL_AUTO, KERNEL_DENSE, KERNEL_SPARSE, KERNEL_ISECT, KERNEL_ISECT2, KERNEL_ISECT3, KERNEL_ISECT4, KERNEL_ISECT5, KERNEL_SPLIT = 0, 1, 2, 5, 6, 7, 8, 9, 10
+KERNEL_WSPARSE = 11  # weighted metrics: sparse walk over present rows (the weighted default)
 
 
 class sf_problem(C.Structure):
@@ -42,6 +44,7 @@ class sf_exec(C.Structure):
         ("mem_budget_bytes", C.c_int64),
         ("kernel", C.c_int32),
         ("flags", C.c_int32),
+        ("alpha", C.c_double),  # SF_GENERALIZED only (ABI v3)
     ]
 
 
@@ -83,6 +86,9 @@ SIGNATURES = {
                                 C.c_int32, C.c_int32]),
     "sf_finalize": (C.c_int, [C.c_int, C.c_int64, _P, _P, C.c_int32]),
     "sf_condense": (C.c_int, [C.c_int, C.c_int32, C.c_int32, C.c_int32, _P, _P, C.c_int32]),
+    "sf_mantel": (C.c_int, [C.c_int32, _P, _P, C.c_int32, C.c_uint64, C.c_int32,
+                            C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+    "sf_mantel_permutation": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, _P]),
     "sfh_flatten": (C.c_int, [C.c_int32, _P, _P, C.c_int32, _P, C.POINTER(C.c_int32), _P, _P, _P]),
     "sfh_fnv1a64": (C.c_uint64, [_P, C.c_uint64, C.c_uint64]),
     "sfh_random_instance": (_P, [C.c_uint64, C.c_int32, C.c_int32, C.c_double, C.c_int32]),
@@ -171,12 +177,13 @@ class Problem:
 
 
 def make_exec(devices=None, kernel: int = KERNEL_AUTO, exact: bool = False,
-              mem_budget_bytes: int = 0):
+              mem_budget_bytes: int = 0, alpha: float = 1.0):
     """Build an sf_exec (returned with its device array to keep it alive)."""
     dev_arr = None
     if devices is not None:
         dev_arr = (C.c_int32 * len(devices))(*devices)
     ex = sf_exec(len(devices) if devices is not None else 0,
                  C.cast(dev_arr, C.POINTER(C.c_int32)) if dev_arr is not None else None,
-                 int(mem_budget_bytes), int(kernel), SF_EXEC_EXACT_NO_FMA if exact else 0)
+                 int(mem_budget_bytes), int(kernel), SF_EXEC_EXACT_NO_FMA if exact else 0,
+                 float(alpha))
     return ex, dev_arr

@@ -74,7 +74,7 @@ def build_oracle(force: bool = False, verbose: bool = False) -> None:
     src = ORACLE / "stripefrac_oracle.c"
     if force or _stale(ORACLE_LIB, [src]):
         cmd = ["gcc", "-O2", "-ffp-contract=off", "-fPIC", "-shared", "-pthread",
-               str(src), "-o", str(ORACLE_LIB)]
+               str(src), "-o", str(ORACLE_LIB), "-lm"]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)

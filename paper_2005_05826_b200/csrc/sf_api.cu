@@ -15,6 +15,9 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <numeric>
+#include <random>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -25,6 +28,8 @@
 #include "sf_common.hpp"
 #include "sparse_kernels.cuh"
 #include "stripe_kernels.cuh"
+#include "wsparse_kernels.cuh"
+#include "mantel_kernels.cuh"
 #include "stripefrac_cuda.h"
 
 namespace sf {
@@ -390,6 +395,11 @@ struct DeviceState {
   DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm, nheavy;
   // split path (kernel 10): light-row sums per slot, |S_e| per row
   DevBuf lightsum, mcount;
+  DevBuf lcnt, lptr, lmem, lscantmp;  // banded light scatter: member CSR of the light rows
+  size_t lscan_bytes = 0;
+  bool banded = false;
+  // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
+  DevBuf wnb, woff, wcnt, wpool;
   int32_t light_pass = 0;  // stripes per light-sum pass (memory-bounded)
   size_t sort_bytes = 0;
   std::vector<cudaEvent_t> events;
@@ -408,6 +418,7 @@ struct sf_plan {
   int metric = 0, prec = 0;
   int32_t n = 0, E = 0, start = 0, stop = 0;
   bool bits = false, exact = false;
+  double alpha = 1.0;  // generalized UniFrac exponent
   int kernel = 1;  // 1 dense, 2 sparse-bit walk (3/4 flattened variants), 5/6 intersection
   int32_t scale = 0;    // intersection paths: fixed-point lengths round(L * 2^scale)
   int32_t lo_bits = 32; // kernel 6: value = hi * 2^lo_bits + lo
@@ -450,6 +461,12 @@ struct Isect5Cfg {
   static constexpr int RS = 8, NW = 8;
 };
 // Split (kernel 10): heavy rows walked warp-uniformly, light rows scattered.
+// Weighted sparse walk (kernel 11).
+struct WSparseCfg {
+  static constexpr int RK = 4, RS = 2, NWK = 8, NWS = 2;
+  static constexpr int TK = NWK * RK, TS = NWS * 32 * RS;
+};
+
 struct SplitCfg {
   static constexpr int RS = 16, NW = 8, SCATTER_NW = 8;
 };
@@ -658,11 +675,65 @@ sf_status isect2_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
 
 // Light rows -> light sums of stripes [s0, s1) (lightsum row 0 = stripe s0);
 // with_colsum: also add the light rows to the column sums (first pass only).
+bool light_banded() {
+  const char* e = std::getenv("SF_LIGHT_SCATTER");
+  return !(e && std::atoi(e) == 0);
+}
+
+// Banded light scatter: member CSR once per run, then one launch per
+// (512-stripe x KB-column) band of the pass, sized to stay in L2.
+sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, int p0, int p1,
+                               bool first) {
+  const int n = plan->n;
+  const int64_t E = plan->E;
+  const int heavy_min = split_heavy_min(n);
+  constexpr int NW = SplitCfg::SCATTER_NW;
+  if (first) {
+    sp_light_count_kernel<<<grid_for(E + 1, 256), 256, 0, st>>>(
+        d.perm.as<int32_t>(), plan->E, n, d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>(),
+        d.lcnt.as<uint32_t>());
+    size_t tmp = d.lscan_bytes;
+    SF_CUDA(cub::DeviceScan::ExclusiveSum(d.lscantmp.p, tmp, d.lcnt.as<uint32_t>(), d.lptr.as<uint32_t>(),
+                                          static_cast<int>(E + 1), st));
+    const int blocks = static_cast<int>(std::min<int64_t>((E + NW - 1) / NW, 148 * 16));
+    sp_light_members_kernel<<<blocks, 32 * NW, 0, st>>>(
+        d.emb.as<uint32_t>(), plan->row_words, plan->E, n, d.perm.as<int32_t>(),
+        d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>(), d.lptr.as<uint32_t>(),
+        d.fix.as<unsigned long long>(), plan->lo_bits, d.lmem.as<int32_t>(),
+        d.colsum.as<unsigned long long>());
+    SF_CUDA(cudaGetLastError());
+    plan->stats.launches += 3;
+  }
+  double band_mb = 64.0;
+  if (const char* e = std::getenv("SF_LIGHT_BAND_MB")) band_mb = std::max(1.0, std::atof(e));
+  const int SB = 32 * SplitCfg::RS;
+  const int64_t kb = static_cast<int64_t>(band_mb * 1048576.0 / (16.0 * SB));
+  const int KB = static_cast<int>(std::max<int64_t>(256, std::min<int64_t>(kb, n)));
+  const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
+  auto* kern = sp_light_band_kernel<NW>;
+  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const int blocks = static_cast<int>(std::min<int64_t>((E + NW - 1) / NW, 148 * 16));
+  for (int s0 = p0; s0 < p1; s0 += SB) {
+    const int s1 = std::min(p1, s0 + SB);
+    for (int k0 = 0; k0 < n; k0 += KB) {
+      kern<<<blocks, 32 * NW, smem, st>>>(d.perm.as<int32_t>(), plan->E, n, d.nheavy.as<unsigned int>(),
+                                          d.lptr.as<uint32_t>(), d.lmem.as<int32_t>(),
+                                          d.fix.as<unsigned long long>(), plan->lo_bits, p0, s0, s1, k0,
+                                          std::min(n, k0 + KB), d.lightsum.as<double>(),
+                                          d.exec_ctr.as<unsigned long long>(), heavy_min);
+      plan->stats.launches++;
+    }
+  }
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
 sf_status split_scatter(sf_plan* plan, DeviceState& d, cudaStream_t st, int s0, int s1, bool with_colsum) {
   const int n = plan->n;
   const int64_t E = plan->E;
   const int heavy_min = split_heavy_min(n);
   SF_CUDA(cudaMemsetAsync(d.lightsum.p, 0, static_cast<size_t>(s1 - s0) * static_cast<size_t>(n) * 16, st));
+  if (d.banded) return split_scatter_banded(plan, d, st, s0, s1, with_colsum);
   constexpr int NW = SplitCfg::SCATTER_NW;
   const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
   auto* kern = sp_light_scatter_kernel<NW, 8>;
@@ -860,6 +931,56 @@ sf_status launch_sparse(const SparseArgs& a, cudaStream_t st) {
   return SF_OK;
 }
 
+template <int M, class Real, bool EXACT>
+sf_status launch_wsparse_t(const WSparseArgs& a, cudaStream_t st) {
+  using C = WSparseCfg;
+  using T = WSparseTile<C::RK, C::RS, C::NWK, C::NWS>;
+  auto* kern = stripe_wsparse_kernel<M, Real, EXACT, C::RK, C::RS, C::NWK, C::NWS>;
+  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES));
+  const dim3 grid((a.n + C::TK - 1) / C::TK, (a.s_end - a.s_begin + C::TS - 1) / C::TS);
+  kern<<<grid, T::NT, T::BYTES, st>>>(a);
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_wsparse(int metric, bool exact, const WSparseArgs& a, cudaStream_t st) {
+  if (metric == SF_WEIGHTED_NORMALIZED)
+    return exact ? launch_wsparse_t<kWN, Real, true>(a, st) : launch_wsparse_t<kWN, Real, false>(a, st);
+  if (metric == SF_WEIGHTED_UNNORMALIZED)
+    return exact ? launch_wsparse_t<kWU, Real, true>(a, st) : launch_wsparse_t<kWU, Real, false>(a, st);
+  if (metric == SF_GENERALIZED)
+    return exact ? launch_wsparse_t<kGen, Real, true>(a, st) : launch_wsparse_t<kGen, Real, false>(a, st);
+  return fail(SF_EINVAL, "the weighted sparse walk implements the weighted metrics only");
+}
+
+// Kernel 11, per chunk: presence words + counts -> pool offsets (scan) ->
+// compacted values -> wrapped columns.
+sf_status wsparse_build(sf_plan* plan, DeviceState& d, int32_t C, cudaStream_t st) {
+  const int n = plan->n;
+  const int64_t n_ext = sparse_n_ext(n);
+  const int32_t Wc = (C + 31) / 32;
+  const int64_t cells = static_cast<int64_t>(Wc) * n_ext;
+  ws_pack_kernel<<<grid_for(cells, 256), 256, 0, st>>>(d.emb.as<double>(), plan->row_words, C, n, Wc,
+                                                        n_ext, d.wnb.as<uint32_t>(), d.wcnt.as<uint32_t>());
+  size_t tmp = d.cub_bytes;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cubtmp.p, tmp, d.wcnt.as<uint32_t>(), d.woff.as<uint32_t>(),
+                                        static_cast<int>(cells), st));
+  if (plan->prec == SF_FP64)
+    ws_fill_kernel<double><<<grid_for(static_cast<int64_t>(Wc) * n, 256), 256, 0, st>>>(
+        d.emb.as<double>(), plan->row_words, n, Wc, n_ext, d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(),
+        d.wpool.as<double>());
+  else
+    ws_fill_kernel<float><<<grid_for(static_cast<int64_t>(Wc) * n, 256), 256, 0, st>>>(
+        d.emb.as<double>(), plan->row_words, n, Wc, n_ext, d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(),
+        d.wpool.as<float>());
+  ws_extend_kernel<<<grid_for(static_cast<int64_t>(Wc) * (n_ext - n), 256), 256, 0, st>>>(
+      d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n, Wc, n_ext);
+  SF_CUDA(cudaGetLastError());
+  plan->stats.launches += 4;
+  return SF_OK;
+}
+
 // Layout of one chunk's schedule arrays inside the packed device buffer.
 enum { kLeafRows, kLeafFeat, kIntRows, kCptr, kCodes, kCarrySrc, kCarryDst, kNumArr };
 
@@ -945,7 +1066,9 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       SF_CUDA(cudaGetLastError());
       plan->stats.launches++;
     }
-    if (plan->kernel == 10) {
+    if (plan->kernel == 11) {
+      SF_TRY(wsparse_build(plan, d, C, st));
+    } else if (plan->kernel == 10) {
       SF_TRY(split_build(plan, d, st));
     } else if (plan->kernel >= 6) {
       SF_TRY(isect2_build(plan, d, st));
@@ -964,7 +1087,25 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
     }
     SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
     // ---- K2: stripe update over the chunk's rows
-    if (plan->kernel == 10) {
+    if (plan->kernel == 11) {
+      WSparseArgs a;
+      a.nb = d.wnb.as<uint32_t>();
+      a.off = d.woff.as<uint32_t>();
+      a.pool = d.wpool.p;
+      a.n_ext = sparse_n_ext(n);
+      a.lens = d.lens.as<double>() + c.r0;
+      a.C = C;
+      a.Wc = (C + 31) / 32;
+      a.n = n;
+      a.s_begin = d.a;
+      a.s_end = d.b;
+      a.dist = d.dist.p;
+      a.tot = plan->metric == SF_WEIGHTED_UNNORMALIZED ? nullptr : d.tot.p;
+      a.exec_updates = d.exec_ctr.as<unsigned long long>();
+      a.alpha = plan->alpha;
+      SF_TRY(plan->prec == SF_FP64 ? launch_wsparse<double>(plan->metric, plan->exact, a, st)
+                                   : launch_wsparse<float>(plan->metric, plan->exact, a, st));
+    } else if (plan->kernel == 10) {
       SplitArgs a;
       a.nx = d.nodebits.as<unsigned long long>();
       a.limbs = d.limbs.as<double2>();
@@ -1127,7 +1268,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
   }
   const size_t ne = d.events.size();
   SF_CUDA(cudaEventRecord(d.events[ne - 2], st));
-  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED && plan->kernel < 5) {
+  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED && (plan->kernel < 5 || plan->kernel == 11)) {
     const int blocks = grid_for(slots, 256);
     if (plan->prec == SF_FP64)
       finalize_kernel<double><<<blocks, 256, 0, st>>>(d.dist.as<double>(), d.tot.as<double>(), slots);
@@ -1165,8 +1306,12 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                          int32_t stop, const sf_exec* ex, sf_plan** out) {
   if (!out) return fail(SF_EINVAL, "out is null");
   *out = nullptr;
-  if (metric != SF_UNWEIGHTED && metric != SF_WEIGHTED_UNNORMALIZED && metric != SF_WEIGHTED_NORMALIZED)
+  if (metric != SF_UNWEIGHTED && metric != SF_WEIGHTED_UNNORMALIZED && metric != SF_WEIGHTED_NORMALIZED &&
+      metric != SF_GENERALIZED)
     return fail(SF_EINVAL, "unknown metric code " + std::to_string(static_cast<int>(metric)));
+  const double alpha = ex ? ex->alpha : 0.0;
+  if (metric == SF_GENERALIZED && !(std::isfinite(alpha) && alpha >= 0.0))
+    return fail(SF_EINVAL, "generalized UniFrac needs a finite alpha >= 0");
   if (prec != SF_FP32 && prec != SF_FP64)
     return fail(SF_EINVAL, "unknown precision code " + std::to_string(static_cast<int>(prec)));
   SF_TRY(validate_problem(p));
@@ -1183,7 +1328,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stop = stop;
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
-  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 10) ? ex->kernel : 1;
+  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 11) ? ex->kernel : 1;
   const int n = p->n_samples;
   // auto, unweighted: the intersection kernel (exact fixed-point sums), or
   // with SF_EXEC_EXACT_NO_FMA the sparse walk (the reference's adds in the
@@ -1195,8 +1340,16 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                       nodepacked_bytes(k, p->n_rows, n) <= static_cast<size_t>(ex->mem_budget_bytes);
     plan->kernel = fits ? k : 1;
   }
-  if (plan->kernel >= 2 && metric != SF_UNWEIGHTED)
+  // auto, weighted: the sparse walk over present rows (kernel 11)
+  if ((!ex || ex->kernel == 0) && metric != SF_UNWEIGHTED) plan->kernel = 11;
+  if (plan->kernel >= 2 && plan->kernel <= 10 && metric != SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the sparse bit kernel implements the unweighted metric only");
+  if (plan->kernel == 11 && metric == SF_UNWEIGHTED)
+    return fail(SF_EINVAL, "the weighted sparse walk implements the weighted metrics only");
+  if (metric == SF_GENERALIZED && plan->kernel != 11)
+    return fail(SF_EINVAL, "generalized UniFrac runs on the weighted sparse walk (kernel 11) only");
+  plan->alpha = alpha;
+  const bool wsp = plan->kernel == 11;
   plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;
   const size_t w = prec == SF_FP64 ? 8 : 4;
   const bool has_t = metric != SF_WEIGHTED_UNNORMALIZED;
@@ -1216,6 +1369,10 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
 
   // chunk capacity from the smallest device budget
   const size_t row_bytes = static_cast<size_t>(plan->row_words) * (plan->bits ? 4 : 8);
+  // kernel 11 holds, per chunk row, the dense row + its share of the value
+  // pool (worst case n values) + presence words / counts / offsets
+  const size_t wsp_row_bytes =
+      wsp ? static_cast<size_t>(n) * w + (static_cast<size_t>(sparse_n_ext(n)) * 12 + 31) / 32 : 0;
   size_t budget = SIZE_MAX;
   for (auto& d : plan->devs) {
     SF_CUDA(cudaSetDevice(d->dev));
@@ -1227,15 +1384,23 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     budget = std::min(budget, avail * 3 / 4);
   }
   if (ex && ex->mem_budget_bytes > 0) budget = std::min(budget, static_cast<size_t>(ex->mem_budget_bytes));
-  int64_t cmax = static_cast<int64_t>(budget / std::max<size_t>(row_bytes, 1));
-  if (plan->kernel >= 2) cmax = plan->E;  // the sparse path keeps all rows
+  int64_t cmax = static_cast<int64_t>(budget / std::max<size_t>(row_bytes + wsp_row_bytes, 1));
+  if (plan->kernel >= 2 && !wsp) cmax = plan->E;  // the sparse bit paths keep all rows
+  if (wsp) {
+    // 32-row words never straddle chunks; uint32 pool offsets
+    cmax = std::min<int64_t>(cmax, static_cast<int64_t>(UINT32_MAX / static_cast<uint64_t>(n)) / 32 * 32);
+    if (cmax < plan->E) cmax = cmax / 32 * 32;
+    if (cmax < 32) cmax = std::min<int64_t>(32, plan->E);
+  }
   cmax = std::min<int64_t>(cmax, plan->E);
   if (cmax < 1) return fail(SF_ENOMEM, "not enough device memory for one embedding row");
   for (;;) {
     plan->sched = build_schedule(p, static_cast<int32_t>(cmax));
-    const size_t need = (static_cast<size_t>(cmax) + static_cast<size_t>(plan->sched.n_pending)) * row_bytes;
-    if (need <= budget || cmax == 1 || plan->kernel >= 2) break;
+    const size_t need = (static_cast<size_t>(cmax) + static_cast<size_t>(plan->sched.n_pending)) * row_bytes +
+                        static_cast<size_t>(cmax) * wsp_row_bytes;
+    if (need <= budget || cmax == 1 || (plan->kernel >= 2 && !wsp) || (wsp && cmax <= 32)) break;
     cmax = std::max<int64_t>(1, cmax * 3 / 4);
+    if (wsp) cmax = std::max<int64_t>(32, cmax / 32 * 32);
   }
   plan->stats.n_chunks = plan->sched.chunks.size();
 
@@ -1254,7 +1419,23 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     SF_TRY(d.dist.alloc(d.dev, slots * w, "distances"));
     if (has_t) SF_TRY(d.tot.alloc(d.dev, slots * w, "totals"));
     SF_TRY(d.exec_ctr.alloc(d.dev, 2 * sizeof(unsigned long long), "counters"));
-    if (plan->kernel >= 2) {
+    if (wsp) {
+      SF_TRY(upload_schedule(d, plan->sched));
+      const int32_t cm = plan->sched.cmax;
+      SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(cm) * row_bytes, "embedding chunk"));
+      SF_TRY(d.pend.alloc(d.dev, static_cast<size_t>(std::max(plan->sched.n_pending, 1)) * row_bytes,
+                          "pending rows"));
+      const int64_t cells = static_cast<int64_t>((cm + 31) / 32) * sparse_n_ext(n);
+      SF_TRY(d.wnb.alloc(d.dev, static_cast<size_t>(cells) * 4, "presence words"));
+      SF_TRY(d.wcnt.alloc(d.dev, static_cast<size_t>(cells) * 4, "presence counts"));
+      SF_TRY(d.woff.alloc(d.dev, static_cast<size_t>(cells) * 4, "pool offsets"));
+      SF_TRY(d.wpool.alloc(d.dev, static_cast<size_t>(cm) * static_cast<size_t>(n) * w, "value pool"));
+      size_t tmp = 0;
+      SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.wcnt.as<uint32_t>(), d.woff.as<uint32_t>(),
+                                            static_cast<int>(cells), d.stream));
+      d.cub_bytes = tmp;
+      SF_TRY(d.cubtmp.alloc(d.dev, tmp, "scan scratch"));
+    } else if (plan->kernel >= 2) {
       SF_TRY(upload_schedule(d, plan->sched));
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(plan->E) * row_bytes, "embedding rows"));
       SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));
@@ -1280,6 +1461,21 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                          d.dev, d.a, d.b, d.light_pass, freeb >> 20);
           SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * per_stripe, "light-row sums"));
           SF_TRY(d.mcount.alloc(d.dev, static_cast<size_t>(plan->E) * 4, "row presence counts"));
+          d.banded = light_banded() &&
+                     static_cast<uint64_t>(plan->E) * static_cast<uint64_t>(split_heavy_min(n)) < (1ull << 32);
+          if (d.banded) {
+            const size_t E1 = static_cast<size_t>(plan->E) + 1;
+            SF_TRY(d.lcnt.alloc(d.dev, E1 * 4, "light member counts"));
+            SF_TRY(d.lptr.alloc(d.dev, E1 * 4, "light member offsets"));
+            // light rows have |X_e| < heavy_min members
+            SF_TRY(d.lmem.alloc(d.dev, static_cast<size_t>(plan->E) * static_cast<size_t>(split_heavy_min(n)) * 4,
+                                "light members"));
+            size_t tmp = 0;
+            SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.lcnt.as<uint32_t>(), d.lptr.as<uint32_t>(),
+                                                  static_cast<int>(E1), d.stream));
+            d.lscan_bytes = tmp;
+            SF_TRY(d.lscantmp.alloc(d.dev, tmp, "light scan scratch"));
+          }
         }
       } else {
         SF_TRY(sparse_prepare(plan.get(), d, p));
@@ -1427,6 +1623,8 @@ sf_status sf_accumulate_batch(const void* emb, const void* lengths, int32_t fill
   if (n_samples < 2) return fail(SF_EINVAL, "need at least 2 samples");
   if (padded < n_samples) return fail(SF_EINVAL, "embedding batch shape is inconsistent");
   if (!emb || !lengths || !dist_inout) return fail(SF_EINVAL, "null argument");
+  if (metric != SF_UNWEIGHTED && metric != SF_WEIGHTED_UNNORMALIZED && metric != SF_WEIGHTED_NORMALIZED)
+    return fail(SF_EINVAL, "unknown metric code " + std::to_string(static_cast<int>(metric)));
   const bool has_t = metric != SF_WEIGHTED_UNNORMALIZED;
   if (has_t && !tot_inout) return fail(SF_EINVAL, "tot_inout is required for ratio metrics");
   if (prec != SF_FP32 && prec != SF_FP64) return fail(SF_EINVAL, "unknown precision");
@@ -1575,6 +1773,147 @@ sf_status sf_condense(sf_precision prec, int32_t n, int32_t start, int32_t stop,
   SF_CUDA(cudaMemcpy(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost));
   if (bad) return fail(SF_EINVAL, "condense: duplicated slot disagrees");
   SF_CUDA(cudaMemcpy(out, dout.p, nn * 8, cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
+// ---------------------------------------------------------------- Mantel
+namespace {
+std::uint64_t mantel_mix64(std::uint64_t x) {  // splitmix64, validate.cpp:101-106
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+// The reference's permutation p (validate.cpp:133-136): same engine, same
+// std::shuffle (this host code is built with the same C++ library).
+void mantel_perm(int32_t n, std::uint64_t seed, int32_t p, int32_t* out) {
+  std::vector<int> perm(static_cast<std::size_t>(n));
+  std::mt19937_64 rng(mantel_mix64(seed ^ mantel_mix64(static_cast<std::uint64_t>(p) + 1)));
+  std::iota(perm.begin(), perm.end(), 0);
+  std::shuffle(perm.begin(), perm.end(), rng);
+  std::copy(perm.begin(), perm.end(), out);
+}
+}  // namespace
+
+sf_status sf_mantel_permutation(int32_t n, uint64_t seed, int32_t p, int32_t* perm_out) {
+  if (n < 1 || p < 0 || !perm_out) return fail(SF_EINVAL, "mantel_permutation: bad argument");
+  mantel_perm(n, seed, p, perm_out);
+  return SF_OK;
+}
+
+sf_status sf_mantel(int32_t n, const double* m1, const double* m2, int32_t permutations, uint64_t seed,
+                    int32_t device, double* r_out, double* p_value_out) {
+  if (permutations < 1) return fail(SF_EINVAL, "mantel: need at least 1 permutation");
+  if (!m1 || !m2 || !r_out || !p_value_out) return fail(SF_EINVAL, "null argument");
+  if (n < 2) return fail(SF_EINVAL, "distance matrix needs at least 2 samples");
+  sf_exec ex{};
+  ex.n_devices = 1;
+  ex.devices = &device;
+  std::vector<int> devs;
+  SF_TRY(usable_devices(&ex, devs));
+  SF_CUDA(cudaSetDevice(device));
+  cudaStream_t st;
+  SF_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } guard{st};
+  const size_t nn = static_cast<size_t>(n) * static_cast<size_t>(n);
+  const int32_t nrp = (n + 1) / 2;  // row pairs {i, n-1-i}
+  DevBuf dx, dy, dpart, dpxy, dasym, ddot, dperm, dpp;
+  SF_TRY(dx.alloc(device, nn * 8, "mantel matrix 1"));
+  SF_TRY(dy.alloc(device, nn * 8, "mantel matrix 2"));
+  SF_TRY(dpart.alloc(device, static_cast<size_t>(nrp) * 16, "mantel partials"));
+  SF_TRY(dpxy.alloc(device, static_cast<size_t>(nrp) * 8, "mantel cross partials"));
+  SF_TRY(dasym.alloc(device, 16, "asymmetry flag"));
+  SF_TRY(ddot.alloc(device, static_cast<size_t>(permutations + 1) * 8, "permutation cross terms"));
+  SF_CUDA(cudaMemcpyAsync(dx.p, m1, nn * 8, cudaMemcpyHostToDevice, st));
+  SF_CUDA(cudaMemcpyAsync(dy.p, m2, nn * 8, cudaMemcpyHostToDevice, st));
+  SF_CUDA(cudaMemsetAsync(dasym.p, 0xff, 16, st));
+  std::vector<double> part(static_cast<size_t>(nrp) * 2);
+  // pass 1: means (+ symmetry, as condensed_upper checks, validate.cpp:87-91)
+  mt_stats_kernel<<<nrp, kMantelThreads, 0, st>>>(dx.as<double>(), dy.as<double>(), n, 0, 0.0, 0.0,
+                                                  dpart.as<double>(), dpxy.as<double>(),
+                                                  dasym.as<unsigned long long>());
+  SF_CUDA(cudaGetLastError());
+  unsigned long long asym[2];
+  SF_CUDA(cudaMemcpyAsync(asym, dasym.p, 16, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaMemcpyAsync(part.data(), dpart.p, part.size() * 8, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  for (int m = 0; m < 2; ++m)
+    if (asym[m] != ~0ull)
+      return fail(SF_EINVAL, "distance matrix is asymmetric at (" + std::to_string(asym[m] / static_cast<unsigned>(n)) +
+                                 "," + std::to_string(asym[m] % static_cast<unsigned>(n)) + ")");
+  const double cnt = static_cast<double>(n) * static_cast<double>(n - 1) / 2.0;
+  double sx = 0.0, sy = 0.0;
+  for (int32_t i = 0; i < nrp; ++i) {
+    sx += part[2 * static_cast<size_t>(i)];
+    sy += part[2 * static_cast<size_t>(i) + 1];
+  }
+  const double mx = sx / cnt, my = sy / cnt;
+  // pass 2: sxx, syy (host-ordered) and the sxy partials (device-reduced like
+  // every permutation's cross term)
+  mt_stats_kernel<<<nrp, kMantelThreads, 0, st>>>(dx.as<double>(), dy.as<double>(), n, 1, mx, my,
+                                                  dpart.as<double>(), dpxy.as<double>(),
+                                                  dasym.as<unsigned long long>());
+  mt_reduce_kernel<<<1, kMantelThreads, 0, st>>>(dpxy.as<double>(), nrp, ddot.as<double>() + permutations);
+  SF_CUDA(cudaGetLastError());
+  SF_CUDA(cudaMemcpyAsync(part.data(), dpart.p, part.size() * 8, cudaMemcpyDeviceToHost, st));
+  double sxy = 0.0;
+  SF_CUDA(cudaMemcpyAsync(&sxy, ddot.as<double>() + permutations, 8, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  double sxx = 0.0, syy = 0.0;
+  for (int32_t i = 0; i < nrp; ++i) {
+    sxx += part[2 * static_cast<size_t>(i)];
+    syy += part[2 * static_cast<size_t>(i) + 1];
+  }
+  if (sxx <= 0.0 || syy <= 0.0)
+    return fail(SF_EINVAL, "mantel: a distance matrix has zero variance, correlation is undefined");
+  const double denom = std::sqrt(sxx * syy);
+  const double r = sxy / denom;
+
+  // permutations in batches; the next batch is generated on host threads
+  // while the device works on the current one
+  const int32_t B = static_cast<int32_t>(std::max<int64_t>(
+      1, std::min<int64_t>({permutations, 65535, (int64_t{256} << 20) / (4 * static_cast<int64_t>(n))})));
+  SF_TRY(dperm.alloc(device, static_cast<size_t>(B) * n * 4, "permutations"));
+  SF_TRY(dpp.alloc(device, static_cast<size_t>(B) * nrp * 8, "permutation partials"));
+  int32_t* hperm = nullptr;
+  SF_CUDA(cudaMallocHost(&hperm, static_cast<size_t>(2) * B * n * 4));
+  struct HostGuard {
+    int32_t* p;
+    ~HostGuard() { cudaFreeHost(p); }
+  } hguard{hperm};
+  const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+  auto generate = [&](int32_t p0, int32_t cnt_p, int32_t* dst) {
+    std::vector<std::thread> pool;
+    const int32_t T = static_cast<int32_t>(std::min<unsigned>(hw, static_cast<unsigned>(cnt_p)));
+    for (int32_t t = 0; t < T; ++t)
+      pool.emplace_back([=] {
+        for (int32_t q = t; q < cnt_p; q += T) mantel_perm(n, seed, p0 + q, dst + static_cast<int64_t>(q) * n);
+      });
+    for (auto& th : pool) th.join();
+  };
+  generate(0, std::min(B, permutations), hperm);
+  for (int32_t p0 = 0, buf = 0; p0 < permutations; p0 += B, buf ^= 1) {
+    const int32_t cnt_p = std::min(B, permutations - p0);
+    int32_t* cur = hperm + static_cast<int64_t>(buf) * B * n;
+    SF_CUDA(cudaMemcpyAsync(dperm.p, cur, static_cast<size_t>(cnt_p) * n * 4, cudaMemcpyHostToDevice, st));
+    mt_perm_kernel<<<dim3(static_cast<unsigned>(cnt_p), static_cast<unsigned>(nrp)), kMantelThreads, 0, st>>>(
+        dx.as<double>(), dy.as<double>(), n, mx, my, dperm.as<int32_t>(), nrp, dpp.as<double>());
+    mt_reduce_kernel<<<cnt_p, kMantelThreads, 0, st>>>(dpp.as<double>(), nrp, ddot.as<double>() + p0);
+    SF_CUDA(cudaGetLastError());
+    if (p0 + B < permutations)  // overlaps the kernels just queued
+      generate(p0 + B, std::min(B, permutations - p0 - B), hperm + static_cast<int64_t>(buf ^ 1) * B * n);
+    SF_CUDA(cudaStreamSynchronize(st));  // the other buffer is reused next
+  }
+  std::vector<double> dot(static_cast<size_t>(permutations));
+  SF_CUDA(cudaMemcpy(dot.data(), ddot.p, dot.size() * 8, cudaMemcpyDeviceToHost));
+  int exceed = 0;
+  for (double v : dot)
+    if (v / denom >= r) ++exceed;
+  *r_out = r;
+  *p_value_out = (1.0 + exceed) / (1.0 + permutations);
   return SF_OK;
 }
 

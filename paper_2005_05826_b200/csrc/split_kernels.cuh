@@ -239,6 +239,164 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
   if (lane == 0 && pairs) atomicAdd(pairs_out, pairs);
 }
 
+// ---- Banded light scatter (default). The one-shot scatter above sends each
+// pair's two fp64 atomics to a random 32-byte sector of the whole (stripes x
+// n) light-sum array (5 GB at C3): every atomic is an HBM read-modify-write
+// (ncu: 2.3 TB/s of DRAM traffic, 5% issue). Here the member lists are
+// compacted once (CSR, ascending samples), and the pairs are emitted band by
+// band — a band is a (stripe range x column range) block of the light-sum
+// array sized to stay resident in L2 — by binary-searching, for each member
+// a, the partners b whose slot falls in the band. Atomics then hit L2, and
+// HBM sees each light-sum line about once.
+
+// Members per permuted position (0 for heavy rows): cnt[idx], idx < E.
+__global__ void sp_light_count_kernel(const int32_t* __restrict__ perm, int32_t E, int32_t n,
+                                      const unsigned int* __restrict__ n_heavy,
+                                      const int32_t* __restrict__ mcount, uint32_t* __restrict__ cnt) {
+  const int64_t H = *n_heavy;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= E;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t x = 0;
+    if (i >= H && i < E) {
+      const int m = mcount[perm[i]];
+      x = static_cast<uint32_t>(2 * m > n ? n - m : m);
+    }
+    cnt[i] = x;
+  }
+}
+
+// Members of every light row, ascending, at lmem[lptr[idx] ...]; the light
+// rows' column sums are added here (once per run).
+__global__ void sp_light_members_kernel(const uint32_t* __restrict__ rows, int64_t stride, int32_t E,
+                                        int32_t n, const int32_t* __restrict__ perm,
+                                        const unsigned int* __restrict__ n_heavy,
+                                        const int32_t* __restrict__ mcount,
+                                        const uint32_t* __restrict__ lptr,
+                                        const unsigned long long* __restrict__ fix, int32_t lo_bits,
+                                        int32_t* __restrict__ lmem, unsigned long long* __restrict__ colsum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t tail = (n & 31) ? ((1u << (n & 31)) - 1u) : 0xffffffffu;
+  const int64_t H = *n_heavy;
+  for (int64_t idx = H + warp; idx < E; idx += nwarps) {
+    const int r = perm[idx];
+    const int m = mcount[r];
+    const bool dense = 2 * m > n;
+    const int x = dense ? n - m : m;
+    if (x == 0) continue;
+    const uint32_t* row = rows + static_cast<int64_t>(r) * stride;
+    int32_t* out = lmem + lptr[idx];
+    const double2 L = limbs_of(fix[r], lo_bits);
+    const unsigned long long lh = static_cast<unsigned long long>(L.x);
+    const unsigned long long ll = static_cast<unsigned long long>(L.y);
+    int count = 0;
+    for (int64_t base = 0; base < stride && count < x; base += 32) {
+      const int64_t i = base + lane;
+      uint32_t wd = 0u;
+      if (i < stride) {
+        wd = __ldg(row + i);
+        if (dense) wd = ~wd & (i == stride - 1 ? tail : 0xffffffffu);
+      }
+      const int c = __popc(wd);
+      int incl = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += y;
+      }
+      int at = count + incl - c;
+      while (wd) {
+        const int b = __ffs(wd) - 1;
+        wd &= wd - 1u;
+        const int smp = static_cast<int>(i * 32 + b);
+        out[at++] = smp;
+        atomicAdd(colsum + smp, lh);
+        atomicAdd(colsum + n + smp, ll);
+        if (!dense) {
+          atomicAdd(colsum + 2 * static_cast<int64_t>(n) + smp, lh);
+          atomicAdd(colsum + 3 * static_cast<int64_t>(n) + smp, ll);
+        }
+      }
+      count += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+}
+
+// First index j in [lo, hi) with mem[j] >= key (mem ascending).
+__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ mem, int lo, int hi, int key) {
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (mem[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// One band: slots with stripe in [s0, s1) and column in [k0, k1). gl rows are
+// relative to the light pass start p0 (layout unchanged: (s - p0) * n + k).
+template <int NW>
+__global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
+    const int32_t* __restrict__ perm, int32_t E, int32_t n, const unsigned int* __restrict__ n_heavy,
+    const uint32_t* __restrict__ lptr, const int32_t* __restrict__ lmem,
+    const unsigned long long* __restrict__ fix, int32_t lo_bits, int32_t p0, int32_t s0, int32_t s1,
+    int32_t k0, int32_t k1, double* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
+    int32_t list_cap) {
+  extern __shared__ int32_t sp_band_members[];
+  const int lane = threadIdx.x & 31;
+  const int wib = threadIdx.x >> 5;
+  int32_t* mem = sp_band_members + static_cast<int64_t>(wib) * list_cap;
+  const int S = n / 2;
+  const int se = min(s1, S);  // stripes past S do not exist
+  const int64_t warp = static_cast<int64_t>(blockIdx.x) * NW + wib;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * NW;
+  const int64_t H = *n_heavy;
+  unsigned long long pairs = 0;
+  for (int64_t idx = H + warp; idx < E; idx += nwarps) {
+    const uint32_t b0 = lptr[idx];
+    const int x = static_cast<int>(lptr[idx + 1] - b0);
+    if (x < 2) continue;
+    for (int i = lane; i < x; i += 32) mem[i] = __ldg(lmem + b0 + i);
+    __syncwarp();
+    const double2 L = limbs_of(fix[perm[idx]], lo_bits);
+    for (int i = lane; i + 1 < x; i += 32) {
+      const int a = mem[i];
+      // slot (s = b - a - 1, k = a): b in [a + s0 + 1, a + se]
+      if (a >= k0 && a < k1) {
+        int j = lower_bound_i32(mem, i + 1, x, a + s0 + 1);
+        const int jend = lower_bound_i32(mem, j, x, a + se + 1);
+        for (; j < jend; ++j) {
+          const int s = mem[j] - a - 1;
+          double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + a);
+          atomicAdd(cell, L.x);
+          atomicAdd(cell + 1, L.y);
+          ++pairs;
+        }
+      }
+      // slot (s = n - d - 1, k = b), d = b - a: b in [a + n - se, a + n - 1 - s0] and [k0, k1)
+      const int blo = max(a + n - se, k0);
+      const int bhi = min(a + n - 1 - s0, k1 - 1);
+      if (blo <= bhi) {
+        int j = lower_bound_i32(mem, i + 1, x, blo);
+        const int jend = lower_bound_i32(mem, j, x, bhi + 1);
+        for (; j < jend; ++j) {
+          const int b = mem[j];
+          const int s = n - (b - a) - 1;
+          double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + b);
+          atomicAdd(cell, L.x);
+          atomicAdd(cell + 1, L.y);
+          ++pairs;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  for (int off = 16; off > 0; off >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+  if (lane == 0 && pairs) atomicAdd(pairs_out, pairs);
+}
+
 // bfind: position of the most significant set bit (x != 0).
 __device__ __forceinline__ int msb_pos(uint32_t x) {
   int b;

@@ -25,7 +25,7 @@
 
 namespace sf {
 
-enum : int { kUW = 1, kWU = 2, kWN = 3 };
+enum : int { kUW = 1, kWU = 2, kWN = 3, kGen = 4 };  // kGen: generalized (not in the reference)
 enum : int { kSrcBits = 0, kSrcF64 = 1, kSrcF32 = 2 };
 
 template <class Real>
@@ -76,6 +76,23 @@ __device__ __forceinline__ void update_entry(Real u, Real v, Real len, Real& d, 
       t = mul_add_rn(u + v, len, t);
     else
       t = fma_r(u + v, len, t);
+  }
+}
+
+// Generalized UniFrac (alpha), per present row — not in the reference
+// (parity unpinned; oracle/stripefrac_oracle.c states the published form):
+//   s = u + v; if (s != 0) { w = s^alpha * L; d += w * (|u-v| / s); t += w; }
+__device__ __forceinline__ double pow_r(double x, double a) { return pow(x, a); }
+__device__ __forceinline__ float pow_r(float x, float a) { return powf(x, a); }
+
+template <bool EXACT, class Real>
+__device__ __forceinline__ void update_generalized(Real u, Real v, Real len, Real alpha, Real& d, Real& t) {
+  const Real s = u + v;
+  if (s != Real(0)) {
+    const Real w = pow_r(s, alpha) * len;
+    const Real q = abs_r(u - v) / s;
+    d = EXACT ? mul_add_rn(w, q, d) : fma_r(w, q, d);
+    t += w;
   }
 }
 

@@ -48,6 +48,9 @@ class Metric(enum.IntEnum):  # common.hpp:19; values are the .strf metric codes
     Unweighted = 1
     WeightedUnnormalized = 2
     WeightedNormalized = 3
+    # extension, not in the reference (parity unpinned): generalized UniFrac
+    # with exponent KernelConfig.alpha (SF_GENERALIZED in the C ABI)
+    Generalized = 4
 
 
 class Variant(enum.IntEnum):  # common.hpp:20
@@ -62,7 +65,7 @@ class Precision(enum.IntEnum):  # common.hpp:21; values are scalar widths
 
 
 _METRIC_NAMES = {Metric.Unweighted: "unweighted", Metric.WeightedUnnormalized: "weighted-unnormalized",
-                 Metric.WeightedNormalized: "weighted-normalized"}
+                 Metric.WeightedNormalized: "weighted-normalized", Metric.Generalized: "generalized"}
 _VARIANT_NAMES = {Variant.Naive: "naive", Variant.Batched: "batched", Variant.Tiled: "tiled"}
 
 
@@ -116,6 +119,7 @@ class KernelConfig:
     precision: Precision = Precision.Fp64
     batch_capacity: int = 64
     step_size: int = 0
+    alpha: float = 1.0  # Metric.Generalized only (extension)
 
     def resolved_step_size(self) -> int:
         if self.step_size > 0:
@@ -777,7 +781,7 @@ def compute_unifrac(tree: PhyloTree, table: SampleTable, cfg: KernelConfig, star
     problem = flatten(tree, table)
     sset = allocate_stripes(table.n_samples(), start, stop, cfg.metric, cfg.precision)
     eo = exec_options or ExecOptions()
-    ex, _keep = N.make_exec(eo.devices, eo.kernel, eo.exact, eo.mem_budget_bytes)
+    ex, _keep = N.make_exec(eo.devices, eo.kernel, eo.exact, eo.mem_budget_bytes, cfg.alpha)
     st = N.sf_stats()
     tot_ptr = N.ptr(sset.totals) if sset.has_totals() else None
     _call(N.lib().sf_compute_stripes(problem.ref, int(cfg.metric), int(cfg.precision), start, stop,
@@ -1167,37 +1171,45 @@ def condensed_upper(dm: DistanceMatrix) -> np.ndarray:
     return v[iu].copy()
 
 
-def mantel(m1: DistanceMatrix, m2: DistanceMatrix, permutations: int = 999, seed: int = 1):
-    """Mantel permutation test (validate.cpp:111-159), vectorised on the host.
+@dataclass
+class MantelResult:
+    """MantelResult (validate.hpp:25-31)."""
 
-    The observed r follows the reference formula; permutations come from
-    numpy's PCG64 stream seeded by `seed` (the reference uses mt19937_64 +
-    splitmix64), so p-values agree in distribution, not draw for draw.
-    """
+    r: float = 0.0
+    r_squared: float = 0.0
+    p_value: float = 1.0
+    permutations: int = 0
+    seed: int = 0
+
+    def __getitem__(self, key):  # dict-style access kept for callers of the old mirror
+        return getattr(self, key)
+
+
+def mantel(m1: DistanceMatrix, m2: DistanceMatrix, permutations: int = 999, seed: int = 1,
+           device: int = 0) -> MantelResult:
+    """mantel (validate.cpp:111-159) on device through sf_mantel: the
+    reference's r and its permutation stream (mt19937_64 + std::shuffle from
+    splitmix64 seeds), so p-values match the reference draw for draw."""
     if permutations < 1:
         raise Error("mantel: need at least 1 permutation")
     if m1.n() != m2.n():
         raise Error("mantel: matrices have different sizes")
     if m1.sample_ids and m2.sample_ids and list(m1.sample_ids) != list(m2.sample_ids):
         raise Error("mantel: matrices have different sample orderings")
-    x = condensed_upper(m1)
-    y = condensed_upper(m2)
-    xc = x - x.mean()
-    yc = y - y.mean()
-    sxx, syy = float(xc @ xc), float(yc @ yc)
-    if sxx <= 0.0 or syy <= 0.0:
-        raise Error("mantel: a distance matrix has zero variance, correlation is undefined")
-    denom = math.sqrt(sxx * syy)
-    r = float(xc @ yc) / denom
     n = m1.n()
-    iu = np.triu_indices(n, 1)
-    rng = np.random.default_rng(seed)
-    my = y.mean()
-    exceed = 0
-    for _ in range(permutations):
-        perm = rng.permutation(n)
-        yp = m2.values[perm[iu[0]], perm[iu[1]]] - my
-        if float(xc @ yp) / denom >= r:
-            exceed += 1
-    return {"r": r, "r_squared": r * r, "p_value": (1.0 + exceed) / (1.0 + permutations),
-            "permutations": permutations, "seed": seed}
+    x = np.ascontiguousarray(m1.values, dtype=np.float64)
+    y = np.ascontiguousarray(m2.values, dtype=np.float64)
+    if x.shape != (n, n) or y.shape != (n, n):
+        raise Error("distance matrix is not square")
+    r = C.c_double()
+    p = C.c_double()
+    _call(N.lib().sf_mantel(n, N.ptr(x), N.ptr(y), int(permutations), int(seed) & (2**64 - 1),
+                            int(device), C.byref(r), C.byref(p)))
+    return MantelResult(r.value, r.value * r.value, p.value, int(permutations), int(seed))
+
+
+def mantel_permutation(n: int, seed: int, p: int) -> np.ndarray:
+    """Permutation p of the reference's Mantel stream (host-only helper)."""
+    out = np.empty(n, np.int32)
+    _call(N.lib().sf_mantel_permutation(int(n), int(seed) & (2**64 - 1), int(p), N.ptr(out)))
+    return out

@@ -8,3 +8,4 @@ here="$(cd "$(dirname "$0")" && pwd)"
 make -s -C "$here/../../oracle" -j8
 "$here/../../oracle/_ref/ref_driver" golden "$here" /root/reference/proj/data
 gzip -f -9 "$here/instances_medium.json"
+"$here/../../oracle/_ref/ref_driver" mantel_golden "$here"

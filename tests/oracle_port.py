@@ -39,6 +39,25 @@ def compute_stripes(problem, metric: int, prec: int, start: int = 0, stop: int =
     return d, (t if metric != 2 else None)
 
 
+def compute_stripes_generalized(problem, alpha: float, prec: int, start: int = 0, stop: int = -1,
+                                finalize: bool = True, threads: int = 1, batch: int = 64):
+    """Generalized UniFrac (extension; parity unpinned: not in the reference)."""
+    n = problem.n_samples
+    if stop < 0:
+        stop = n // 2
+    dt = np.float64 if prec == 8 else np.float32
+    d = np.zeros((stop - start, n), dt)
+    t = np.zeros((stop - start, n), dt)
+    f = lib().orc_compute_stripes_generalized
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_double, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                  C.c_int, C.c_int, C.c_int]
+    rc = f(C.cast(C.pointer(problem.struct), C.c_void_p), float(alpha), prec, start, stop,
+           d.ctypes.data, t.ctypes.data, int(finalize), threads, batch)
+    assert rc == 0
+    return d, t
+
+
 def embed_rows(problem, weighted: bool):
     out = np.zeros((problem.n_rows, problem.n_samples), np.float64)
     rc = lib().orc_embed_rows(C.cast(C.pointer(problem.struct), C.c_void_p), int(weighted),

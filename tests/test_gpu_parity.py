@@ -27,8 +27,15 @@ from paper_2005_05826_b200 import stripefrac as sf
 pytestmark = pytest.mark.gpu
 
 KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4, N.KERNEL_ISECT, N.KERNEL_ISECT2, N.KERNEL_ISECT3,
-           N.KERNEL_ISECT4, N.KERNEL_ISECT5, N.KERNEL_SPLIT]  # 3/4: flattened walk
+           N.KERNEL_ISECT4, N.KERNEL_ISECT5, N.KERNEL_SPLIT, N.KERNEL_WSPARSE]  # 3/4: flattened walk
 WALKS = (N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4)
+
+
+def _kernel_serves(kernel, metric):
+    """Dense serves every metric; 2-10 are unweighted-only, 11 weighted-only."""
+    if kernel == N.KERNEL_DENSE or kernel == N.KERNEL_AUTO:
+        return True
+    return (metric != 1) if kernel == N.KERNEL_WSPARSE else (metric == 1)
 
 
 def _gpu_stripes(problem, metric, prec, start, stop, kernel=N.KERNEL_DENSE, exact=False,
@@ -78,7 +85,7 @@ def test_golden_stripes(device_ok, case, kernel):
     n = table.n_samples()
     for r in case["results"]:
         metric = int(sf.metric_from_name(r["metric"]))
-        if kernel >= N.KERNEL_SPARSE and metric != 1:
+        if not _kernel_serves(kernel, metric):
             continue
         prec = 8 if r["precision"] == "fp64" else 4
         gd, gt = gu.stripes(r, n)
@@ -164,8 +171,8 @@ def test_oracle_random_instances(device_ok, metric, prec):
             for exact in (False, True):
                 for kernel in (N.KERNEL_DENSE, N.KERNEL_AUTO):
                     d, t, st = _gpu_stripes(problem, metric, prec, start, stop, kernel, exact)
-                    used = kernel if kernel != N.KERNEL_AUTO or metric != 1 else (
-                        N.KERNEL_SPARSE if exact else N.KERNEL_SPLIT)
+                    used = kernel if kernel != N.KERNEL_AUTO else (
+                        N.KERNEL_WSPARSE if metric != 1 else N.KERNEL_SPARSE if exact else N.KERNEL_SPLIT)
                     _assert_close(metric, prec, exact, d, wd, used)
                     if wt is not None:
                         _assert_close(metric, prec, exact, t, wt, used)
@@ -447,3 +454,142 @@ def test_split_light_passes_and_pinned_download(device_ok, light_pass, monkeypat
         pd, pt, _ = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_SPLIT)
         assert np.array_equal(d.reshape(stop - start, n), pd)
         assert np.array_equal(t.reshape(stop - start, n), pt)
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("metric", [2, 3])
+def test_weighted_sparse_walk_matches_dense_bitwise(device_ok, metric, prec):
+    """Kernel 11 (the weighted default) skips rows absent from both samples —
+    they add exactly +0.0 — and applies the reference's update to the rest in
+    postorder: bit for bit the dense kernel in exact mode, also across
+    chunked embeddings (pool per chunk), partial and wrapped stripe ranges."""
+    for seed, n, leaves, dens in [(31, 200, 700, 0.01), (32, 97, 300, 0.05), (33, 64, 64, 0.3)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 2, S), (3, 4)]:
+            d1, t1, s1 = _gpu_stripes(problem, metric, prec, start, stop, N.KERNEL_DENSE, exact=True)
+            d2, t2, s2 = _gpu_stripes(problem, metric, prec, start, stop, N.KERNEL_WSPARSE, exact=True)
+            assert np.array_equal(d1, d2)
+            if t1 is not None:
+                assert np.array_equal(t1, t2)
+            assert s2.updates_exec < s2.updates_alg
+        # a budget of ~40 rows: 32-row chunks, pending slots, per-chunk pools
+        d3, t3, s3 = _gpu_stripes(problem, metric, prec, 0, S, N.KERNEL_WSPARSE, exact=True,
+                                  mem_budget=40 * 8 * (n + 1) * 2)
+        d1, t1, _ = _gpu_stripes(problem, metric, prec, 0, S, N.KERNEL_DENSE, exact=True)
+        assert s3.n_chunks > 1
+        assert np.array_equal(d1, d3)
+        if t1 is not None:
+            assert np.array_equal(t1, t3)
+        # FMA form: within the stated tolerance of the oracle
+        wd, wt = op.compute_stripes(problem, metric, prec, 0, S)
+        d4, t4, _ = _gpu_stripes(problem, metric, prec, 0, S, N.KERNEL_WSPARSE)
+        _assert_close(metric, prec, False, d4, wd, N.KERNEL_WSPARSE)
+        if wt is not None:
+            _assert_close(metric, prec, False, t4, wt, N.KERNEL_WSPARSE)
+
+
+def test_weighted_sparse_rejects_unweighted(device_ok):
+    inst = sf.random_instance(3, 10, 12, 0.3)
+    problem = sf.flatten(inst.tree, inst.table)
+    with pytest.raises(N.NativeError, match="weighted metrics only"):
+        _gpu_stripes(problem, 1, 8, 0, 5, N.KERNEL_WSPARSE)
+
+
+def _gpu_generalized(problem, alpha, prec, start, stop, exact=False, mem_budget=0):
+    n = problem.n_samples
+    dt = np.float64 if prec == 8 else np.float32
+    d = np.full((stop - start, n), np.nan, dt)
+    t = np.full((stop - start, n), np.nan, dt)
+    ex, _keep = N.make_exec([0], N.KERNEL_AUTO, exact, mem_budget, alpha)
+    st = N.sf_stats()
+    N.check(N.lib().sf_compute_stripes(problem.ref, N.SF_GENERALIZED, prec, start, stop, N.ptr(d),
+                                       N.ptr(t), 1, C.byref(ex), C.byref(st)))
+    return d, t, st
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("alpha", [0.0, 0.5, 1.0, 1.7])
+def test_generalized_matches_oracle(device_ok, alpha, prec):
+    """Generalized UniFrac (extension; parity unpinned — the reference has no
+    generalized metric): kernel 11 vs the oracle's statement of the published
+    form. CUDA pow differs from glibc's by <= 2 ulp, so fp64 is held to 1e-12
+    relative (not bitwise, even in exact mode); fp32 to max(1e-5|x|, 1e-6)."""
+    for seed, n, leaves, dens in [(51, 150, 500, 0.02), (52, 41, 120, 0.1)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 3, S)]:
+            wd, wt = op.compute_stripes_generalized(problem, alpha, prec, start, stop)
+            for exact in (False, True):
+                d, t, _ = _gpu_generalized(problem, alpha, prec, start, stop, exact)
+                for got, want in ((d, wd), (t, wt)):
+                    if prec == 8:
+                        assert np.all(np.abs(got - want) <= 1e-12 * np.maximum(np.abs(want), 1e-300) + 1e-300)
+                    else:
+                        w = want.astype(np.float64)
+                        assert np.all(np.abs(got.astype(np.float64) - w) <= np.maximum(1e-5 * np.abs(w), 1e-6))
+
+
+def test_generalized_alpha1_matches_weighted_normalized(device_ok):
+    inst = sf.random_instance(53, 120, 400, 0.03)
+    problem = sf.flatten(inst.tree, inst.table)
+    S = 60
+    gd, gt, _ = _gpu_generalized(problem, 1.0, 8, 0, S)
+    wd, wt, _ = _gpu_stripes(problem, 3, 8, 0, S)
+    assert np.allclose(gd, wd, rtol=1e-12, atol=1e-15)
+    assert np.allclose(gt, wt, rtol=1e-12, atol=0)
+
+
+def test_generalized_rejects_bad_alpha_and_dense(device_ok):
+    inst = sf.random_instance(54, 10, 12, 0.3)
+    problem = sf.flatten(inst.tree, inst.table)
+    with pytest.raises(N.NativeError, match="alpha"):
+        _gpu_generalized(problem, -1.0, 8, 0, 5)
+    with pytest.raises(N.NativeError, match="alpha"):
+        _gpu_generalized(problem, float("nan"), 8, 0, 5)
+    ex, _keep = N.make_exec([0], N.KERNEL_DENSE, False, 0, 0.5)
+    d = np.zeros((5, 10))
+    with pytest.raises(N.NativeError, match="kernel 11"):
+        N.check(N.lib().sf_compute_stripes(problem.ref, N.SF_GENERALIZED, 8, 0, 5, N.ptr(d), N.ptr(d),
+                                           1, C.byref(ex), None))
+
+
+def test_generalized_python_mirror(device_ok):
+    inst = sf.random_instance(55, 30, 70, 0.1)
+    cfg = sf.KernelConfig(sf.Metric.Generalized, alpha=0.5)
+    dm = sf.compute_distance_matrix(inst.tree, inst.table, cfg)
+    problem = sf.flatten(inst.tree, inst.table)
+    wd, _ = op.compute_stripes_generalized(problem, 0.5, 8)
+    want = op.condense(8, 30, wd)
+    assert np.allclose(dm.values, want, rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("band_mb,light_pass", [("0.05", "0"), ("0.3", "7"), ("1000", "0")])
+def test_split_banded_light_scatter_is_bitwise_the_one_shot_scatter(device_ok, band_mb, light_pass,
+                                                                    monkeypatch):
+    """The banded light scatter (member CSR + per-band binary-searched
+    partners, atomics into an L2-sized block) adds exactly the same limbs to
+    exactly the same slots as the one-shot scatter: integer-valued fp64
+    atomics are order-free, so the results are bit-identical — for tiny bands
+    (many stripe x column blocks), multi-pass light sums, even n (duplicated
+    half stripe), wrapped and partial ranges."""
+    for seed, n, leaves, dens in [(94, 300, 1100, 0.01), (95, 257, 700, 0.03)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        for start, stop in [(0, n // 2), (5, n // 2 - 3)]:
+            monkeypatch.setenv("SF_HEAVY_FRAC", "0.05")
+            monkeypatch.setenv("SF_LIGHT_SCATTER", "0")
+            want_d, want_t, ws = _gpu_stripes(problem, 1, 8, start, stop, N.KERNEL_SPLIT)
+            monkeypatch.delenv("SF_LIGHT_SCATTER")
+            monkeypatch.setenv("SF_LIGHT_BAND_MB", band_mb)
+            if light_pass != "0":
+                monkeypatch.setenv("SF_LIGHT_PASS", light_pass)
+            d, t, gs = _gpu_stripes(problem, 1, 8, start, stop, N.KERNEL_SPLIT)
+            monkeypatch.delenv("SF_LIGHT_BAND_MB")
+            monkeypatch.delenv("SF_LIGHT_PASS", raising=False)
+            assert np.array_equal(d, want_d) and np.array_equal(t, want_t)
+            assert gs.updates_exec == ws.updates_exec  # same light pairs counted
+            wd, wt = op.compute_stripes(problem, 1, 8, start, stop)
+            _assert_close(1, 8, False, d, wd, N.KERNEL_SPLIT)

@@ -93,3 +93,48 @@ def test_brute_force_agrees_with_oracle():
             d, _ = op.compute_stripes(prob, mi + 1, 8)
             got = op.condense(8, n, d)
             assert np.abs(got - np.array(bf).reshape(n, n)).max() <= 1e-12
+
+
+# ---- generalized UniFrac (extension; PARITY UNPINNED: the reference has no
+# generalized metric, common.hpp:19). The C restatement is checked against an
+# independent numpy statement of the published formula over the oracle's own
+# (reference-pinned) weighted embedding rows, and against weighted normalized
+# UniFrac at alpha = 1.
+def _generalized_numpy(problem, alpha, start, stop):
+    emb = op.embed_rows(problem, True)
+    L = np.asarray(problem.lengths, dtype=np.float64)
+    n = problem.n_samples
+    d = np.zeros((stop - start, n))
+    t = np.zeros((stop - start, n))
+    for s in range(start, stop):
+        k = np.arange(n)
+        l = (k + s + 1) % n
+        u, v = emb[:, k], emb[:, l]
+        tot = u + v
+        with np.errstate(divide="ignore", invalid="ignore"):
+            w = np.where(tot > 0, np.power(tot, alpha), 0.0) * L[:, None]
+            q = np.where(tot > 0, np.abs(u - v) / np.where(tot > 0, tot, 1.0), 0.0)
+        d[s - start] = (w * q).sum(axis=0)
+        t[s - start] = w.sum(axis=0)
+    return np.where(t == 0, 0.0, d / np.where(t == 0, 1.0, t)), t
+
+
+@pytest.mark.parametrize("alpha", [0.0, 0.5, 1.0, 1.7])
+def test_generalized_oracle_matches_numpy_statement(alpha):
+    inst = sf.random_instance(41, 23, 60, 0.2)
+    problem = sf.flatten(inst.tree, inst.table)
+    S = problem.n_samples // 2
+    d, t = op.compute_stripes_generalized(problem, alpha, 8, 0, S)
+    wd, wt = _generalized_numpy(problem, alpha, 0, S)
+    assert np.allclose(t, wt, rtol=1e-13, atol=0)
+    assert np.allclose(d, wd, rtol=1e-12, atol=1e-15)
+
+
+def test_generalized_alpha1_is_weighted_normalized():
+    inst = sf.random_instance(42, 31, 80, 0.1)
+    problem = sf.flatten(inst.tree, inst.table)
+    S = problem.n_samples // 2
+    gd, gt = op.compute_stripes_generalized(problem, 1.0, 8, 0, S)
+    wd, wt = op.compute_stripes(problem, 3, 8, 0, S)
+    assert np.allclose(gt, wt, rtol=1e-13, atol=0)
+    assert np.allclose(gd, wd, rtol=1e-12, atol=1e-15)
