@@ -270,7 +270,13 @@ def run_ours(args, cfg):
         roofline = {
             "bound": "fp64", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
             "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None,
-            "traffic": None, "kernel": "stripe_split_kernel (heavy-row walk)",
+            # dram__bytes_read+write of one `ncu --set full` capture of this kernel
+            # (profiles/r01_ncu_split_c3_1024stripes.txt: 1.046 GB + 0.424 GB for
+            # 1024 stripes at C3), per launch: scaled by the stripes it covers
+            "traffic": (round((1.045830e9 + 0.423685e9) / 1024 * stop_all / max(world, 1))
+                        if cfg is CONFIGS["c3"] else None),
+            "traffic_unit": "bytes per launch",
+            "kernel": "stripe_split_kernel (heavy-row walk)",
             "peak_source": "measured DFMA loop (tools/fp_peaks.cu) on this device, x2 flops/FMA",
             "work": "fp64_ops = DFMA lane-ops counted by the kernel (2 per u bit per live slot)",
             "dfma_per_step": int(fp64_ops / args.steps),
