@@ -19,7 +19,8 @@ SF_GENERALIZED = 4  # extension: generalized UniFrac (sf_exec.alpha); not in the
 SF_FP32, SF_FP64 = 4, 8
 SF_EXEC_EXACT_NO_FMA = 1
 KERNEL_AUTO, KERNEL_DENSE, KERNEL_SPARSE, KERNEL_ISECT, KERNEL_ISECT2, KERNEL_ISECT3, KERNEL_ISECT4, KERNEL_ISECT5, KERNEL_SPLIT = 0, 1, 2, 5, 6, 7, 8, 9, 10
-KERNEL_WSPARSE = 11  # weighted metrics: sparse walk over present rows (the weighted default)
+KERNEL_WSPARSE = 11  # weighted metrics: present-row walk (bitwise; the exact-mode default)
+KERNEL_WUWALK = 12  # weighted metrics: warp-uniform u-walk + double-double remainder (the default)
 
 
 class sf_problem(C.Structure):

@@ -29,6 +29,7 @@
 #include "sparse_kernels.cuh"
 #include "stripe_kernels.cuh"
 #include "wsparse_kernels.cuh"
+#include "wuwalk_kernels.cuh"
 #include "mantel_kernels.cuh"
 #include "stripefrac_cuda.h"
 
@@ -400,6 +401,7 @@ struct DeviceState {
   bool banded = false;
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
   DevBuf wnb, woff, wcnt, wpool;
+  DevBuf wpoola, wA, wbase;  // kernel 12: generalized pool, column sums, pool base + chunk total
   int32_t light_pass = 0;  // stripes per light-sum pass (memory-bounded)
   size_t sort_bytes = 0;
   std::vector<cudaEvent_t> events;
@@ -465,6 +467,11 @@ struct Isect5Cfg {
 struct WSparseCfg {
   static constexpr int RK = 4, RS = 2, NWK = 8, NWS = 2;
   static constexpr int TK = NWK * RK, TS = NWS * 32 * RS;
+};
+
+// Weighted u-walk (kernel 12).
+struct WUWalkCfg {
+  static constexpr int RS = 8, NW = 8;
 };
 
 struct SplitCfg {
@@ -897,6 +904,14 @@ sf_status isect_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   return SF_OK;
 }
 
+sf_status sparse_prepare_lens(sf_plan* plan, DeviceState& d, const sf_problem* p) {
+  const int64_t W = (plan->E + 31) / 32;
+  std::vector<double> lens(static_cast<size_t>(W * 32), 0.0);
+  std::copy(p->lengths, p->lengths + plan->E, lens.begin());
+  SF_TRY(upload(d.lens_pad, d.dev, lens.data(), lens.size(), d.stream, "padded lengths"));
+  return SF_OK;
+}
+
 sf_status sparse_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
   const int64_t W = (plan->E + 31) / 32;
   const int64_t n_ext = sparse_n_ext(plan->n);
@@ -981,6 +996,82 @@ sf_status wsparse_build(sf_plan* plan, DeviceState& d, int32_t C, cudaStream_t s
   return SF_OK;
 }
 
+template <int M, class Real, int RS = WUWalkCfg::RS>
+sf_status launch_wuwalk_t(const WUWalkArgs& a, cudaStream_t st) {
+  using C = WUWalkCfg;
+  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * RS - 1) / (32 * RS));
+  stripe_wuwalk_kernel<M, Real, RS, C::NW><<<grid, 32 * C::NW, 0, st>>>(a);
+  SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+template <class Real>
+sf_status launch_wuwalk(int metric, const WUWalkArgs& a, cudaStream_t st) {
+  if (metric == SF_WEIGHTED_NORMALIZED) return launch_wuwalk_t<kWN, Real>(a, st);
+  if (metric == SF_WEIGHTED_UNNORMALIZED) return launch_wuwalk_t<kWU, Real>(a, st);
+  if (metric == SF_GENERALIZED) return launch_wuwalk_t<kGen, Real, 4>(a, st);  // pow: fewer slots, no spills
+  return fail(SF_EINVAL, "the weighted u-walk implements the weighted metrics only");
+}
+
+// Kernel 12, per chunk [r0, r0 + C): presence words + counts into the global
+// arrays at word r0/32, scan, chunk total, values into the global pool at the
+// running base (offsets made global), wrapped columns.
+sf_status wuwalk_build(sf_plan* plan, DeviceState& d, int32_t r0, int32_t C, cudaStream_t st) {
+  const int n = plan->n;
+  const int64_t n_ext = sparse_n_ext(n);
+  const int32_t Wc = (C + 31) / 32;
+  const int64_t cells = static_cast<int64_t>(Wc) * n_ext;
+  uint32_t* nb = d.wnb.as<uint32_t>() + static_cast<int64_t>(r0 / 32) * n_ext;
+  uint32_t* off = d.woff.as<uint32_t>() + static_cast<int64_t>(r0 / 32) * n_ext;
+  unsigned long long* base = d.wbase.as<unsigned long long>();
+  ws_pack_kernel<<<grid_for(cells, 256), 256, 0, st>>>(d.emb.as<double>(), plan->row_words, C, n, Wc, n_ext,
+                                                        nb, d.wcnt.as<uint32_t>());
+  size_t tmp = d.cub_bytes;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cubtmp.p, tmp, d.wcnt.as<uint32_t>(), off, static_cast<int>(cells), st));
+  wu_chunk_total_kernel<<<1, 1, 0, st>>>(off, d.wcnt.as<uint32_t>(), cells - 1, base + 1);
+  const int gb = grid_for(static_cast<int64_t>(Wc) * n, 256);
+  const double* lens = d.lens.as<double>() + r0;
+  const bool gen = plan->metric == SF_GENERALIZED;
+  if (plan->prec == SF_FP64) {
+    if (gen)
+      wu_fill_kernel<double, true><<<gb, 256, 0, st>>>(d.emb.as<double>(), plan->row_words, n, Wc, n_ext, nb, off,
+                                                       base, lens, plan->alpha, d.wpool.as<double>(),
+                                                       d.wpoola.as<double>());
+    else
+      wu_fill_kernel<double, false><<<gb, 256, 0, st>>>(d.emb.as<double>(), plan->row_words, n, Wc, n_ext, nb, off,
+                                                        base, lens, plan->alpha, d.wpool.as<double>(), nullptr);
+  } else {
+    if (gen)
+      wu_fill_kernel<float, true><<<gb, 256, 0, st>>>(d.emb.as<double>(), plan->row_words, n, Wc, n_ext, nb, off,
+                                                      base, lens, plan->alpha, d.wpool.as<float>(),
+                                                      d.wpoola.as<float>());
+    else
+      wu_fill_kernel<float, false><<<gb, 256, 0, st>>>(d.emb.as<double>(), plan->row_words, n, Wc, n_ext, nb, off,
+                                                       base, lens, plan->alpha, d.wpool.as<float>(), nullptr);
+  }
+  wu_advance_base_kernel<<<1, 1, 0, st>>>(base, base + 1);
+  ws_extend_kernel<<<grid_for(static_cast<int64_t>(Wc) * (n_ext - n), 256), 256, 0, st>>>(nb, off, n, Wc, n_ext);
+  SF_CUDA(cudaGetLastError());
+  plan->stats.launches += 6;
+  return SF_OK;
+}
+
+// Upper bound of the present (row, sample) entries: a row has at most
+// min(n, table entries under it) nonzero samples.
+uint64_t present_bound(const sf_problem* p) {
+  const int E = p->n_rows;
+  std::vector<uint64_t> c(static_cast<size_t>(E), 0);
+  uint64_t total = 0;
+  for (int r = 0; r < E; ++r) {  // postorder: children before parents
+    const int f = p->leaf_feature[r];
+    if (f >= 0) c[static_cast<size_t>(r)] += static_cast<uint64_t>(p->feat_ptr[f + 1] - p->feat_ptr[f]);
+    total += std::min<uint64_t>(c[static_cast<size_t>(r)], static_cast<uint64_t>(p->n_samples));
+    const int par = p->parent_row[r];
+    if (par >= 0) c[static_cast<size_t>(par)] += c[static_cast<size_t>(r)];
+  }
+  return total;
+}
+
 // Layout of one chunk's schedule arrays inside the packed device buffer.
 enum { kLeafRows, kLeafFeat, kIntRows, kCptr, kCodes, kCarrySrc, kCarryDst, kNumArr };
 
@@ -1018,7 +1109,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
     d.events.push_back(e);
   }
   SF_CUDA(cudaEventRecord(d.events[0], st));
-  if (plan->kernel != 10) {  // the split kernel writes every slot
+  if (plan->kernel != 10 && plan->kernel != 12) {  // these kernels write every slot
     SF_CUDA(cudaMemsetAsync(d.dist.p, 0, static_cast<size_t>(slots) * w, st));
     if (d.tot.p && plan->metric != SF_WEIGHTED_UNNORMALIZED)
       SF_CUDA(cudaMemsetAsync(d.tot.p, 0, static_cast<size_t>(slots) * w, st));
@@ -1066,7 +1157,10 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       SF_CUDA(cudaGetLastError());
       plan->stats.launches++;
     }
-    if (plan->kernel == 11) {
+    if (plan->kernel == 12) {
+      if (ci == 0) SF_CUDA(cudaMemsetAsync(d.wbase.p, 0, 16, st));
+      SF_TRY(wuwalk_build(plan, d, c.r0, C, st));
+    } else if (plan->kernel == 11) {
       SF_TRY(wsparse_build(plan, d, C, st));
     } else if (plan->kernel == 10) {
       SF_TRY(split_build(plan, d, st));
@@ -1087,7 +1181,67 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
     }
     SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
     // ---- K2: stripe update over the chunk's rows
-    if (plan->kernel == 11) {
+    if (plan->kernel == 12) {
+      if (ci + 1 == plan->sched.chunks.size()) {  // every row is resident now: one pass
+        const int64_t n_ext = sparse_n_ext(n);
+        const int32_t W = (plan->E + 31) / 32;
+        const bool gen = plan->metric == SF_GENERALIZED;
+        const int gb = grid_for(n, 128);
+        if (plan->prec == SF_FP64) {
+          if (gen)
+            wu_colsum_kernel<double, true><<<gb, 128, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
+                                                               d.lens_pad.as<double>(), d.wpool.as<double>(),
+                                                               d.wpoola.as<double>(), d.wA.as<double2>());
+          else
+            wu_colsum_kernel<double, false><<<gb, 128, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
+                                                                d.lens_pad.as<double>(), d.wpool.as<double>(),
+                                                                nullptr, d.wA.as<double2>());
+        } else {
+          if (gen)
+            wu_colsum_kernel<float, true><<<gb, 128, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
+                                                              d.lens_pad.as<double>(), d.wpool.as<float>(),
+                                                              d.wpoola.as<float>(), d.wA.as<double2>());
+          else
+            wu_colsum_kernel<float, false><<<gb, 128, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
+                                                               d.lens_pad.as<double>(), d.wpool.as<float>(),
+                                                               nullptr, d.wA.as<double2>());
+        }
+        SF_CUDA(cudaGetLastError());
+        WUWalkArgs a;
+        a.nb = d.wnb.as<uint32_t>();
+        a.off = d.woff.as<uint32_t>();
+        a.pool = d.wpool.p;
+        a.poola = d.wpoola.p;
+        a.lens = d.lens_pad.as<double>();
+        a.A = d.wA.as<double2>();
+        a.n_ext = n_ext;
+        a.W = W;
+        a.n = n;
+        a.s_begin = d.a;
+        a.s_end = d.b;
+        a.out_begin = d.a;
+        a.finalize = finalize ? 1 : 0;
+        a.alpha = plan->alpha;
+        a.dist = d.dist.p;
+        a.tot = plan->metric == SF_WEIGHTED_UNNORMALIZED ? nullptr : d.tot.p;
+        a.exec_updates = d.exec_ctr.as<unsigned long long>();
+        SF_TRY(plan->prec == SF_FP64 ? launch_wuwalk<double>(plan->metric, a, st)
+                                     : launch_wuwalk<float>(plan->metric, a, st));
+        plan->stats.launches++;
+        const int S = n / 2;
+        if (n % 2 == 0 && S - 1 >= d.a && S - 1 < d.b) {  // duplicated half stripe
+          const int64_t row_off = static_cast<int64_t>(S - 1 - d.a) * n;
+          if (plan->prec == SF_FP64)
+            wu_mirror_kernel<double><<<grid_for(S, 256), 256, 0, st>>>(d.dist.as<double>(), a.tot ? d.tot.as<double>() : nullptr, n, row_off);
+          else
+            wu_mirror_kernel<float><<<grid_for(S, 256), 256, 0, st>>>(d.dist.as<float>(), a.tot ? d.tot.as<float>() : nullptr, n, row_off);
+          SF_CUDA(cudaGetLastError());
+          plan->stats.launches++;
+        }
+      } else {
+        plan->stats.launches--;  // nothing launched for this chunk
+      }
+    } else if (plan->kernel == 11) {
       WSparseArgs a;
       a.nb = d.wnb.as<uint32_t>();
       a.off = d.woff.as<uint32_t>();
@@ -1328,7 +1482,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stop = stop;
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
-  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 11) ? ex->kernel : 1;
+  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 12) ? ex->kernel : 1;
   const int n = p->n_samples;
   // auto, unweighted: the intersection kernel (exact fixed-point sums), or
   // with SF_EXEC_EXACT_NO_FMA the sparse walk (the reference's adds in the
@@ -1341,15 +1495,17 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     plan->kernel = fits ? k : 1;
   }
   // auto, weighted: the sparse walk over present rows (kernel 11)
-  if ((!ex || ex->kernel == 0) && metric != SF_UNWEIGHTED) plan->kernel = 11;
+  // (the u-walk, kernel 12; in exact mode the bitwise present-row walk, 11)
+  if ((!ex || ex->kernel == 0) && metric != SF_UNWEIGHTED) plan->kernel = plan->exact ? 11 : 12;
   if (plan->kernel >= 2 && plan->kernel <= 10 && metric != SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the sparse bit kernel implements the unweighted metric only");
-  if (plan->kernel == 11 && metric == SF_UNWEIGHTED)
+  if (plan->kernel >= 11 && metric == SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the weighted sparse walk implements the weighted metrics only");
-  if (metric == SF_GENERALIZED && plan->kernel != 11)
-    return fail(SF_EINVAL, "generalized UniFrac runs on the weighted sparse walk (kernel 11) only");
+  if (metric == SF_GENERALIZED && plan->kernel < 11)
+    return fail(SF_EINVAL, "generalized UniFrac runs on the weighted sparse walks (kernel 11/12) only");
   plan->alpha = alpha;
-  const bool wsp = plan->kernel == 11;
+  const bool wsp = plan->kernel == 11 || plan->kernel == 12;
+  const bool wuw = plan->kernel == 12;
   plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;
   const size_t w = prec == SF_FP64 ? 8 : 4;
   const bool has_t = metric != SF_WEIGHTED_UNNORMALIZED;
@@ -1372,7 +1528,15 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   // kernel 11 holds, per chunk row, the dense row + its share of the value
   // pool (worst case n values) + presence words / counts / offsets
   const size_t wsp_row_bytes =
-      wsp ? static_cast<size_t>(n) * w + (static_cast<size_t>(sparse_n_ext(n)) * 12 + 31) / 32 : 0;
+      wsp ? (wuw ? 0 : static_cast<size_t>(n) * w) + (static_cast<size_t>(sparse_n_ext(n)) * 12 + 31) / 32 : 0;
+  // kernel 12 keeps the whole problem's presence words, offsets and values
+  const uint64_t pbound = wuw ? present_bound(p) : 0;
+  if (wuw && pbound >= (1ull << 32))
+    return fail(SF_EINVAL, "weighted u-walk: more than 2^32 present entries; use kernel 11");
+  const size_t wuw_fixed =
+      wuw ? static_cast<size_t>((plan->E + 31) / 32) * static_cast<size_t>(sparse_n_ext(n)) * 8 +
+                static_cast<size_t>(pbound) * w * (metric == SF_GENERALIZED ? 2 : 1)
+          : 0;
   size_t budget = SIZE_MAX;
   for (auto& d : plan->devs) {
     SF_CUDA(cudaSetDevice(d->dev));
@@ -1380,7 +1544,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     SF_CUDA(cudaMemGetInfo(&freeb, &totalb));
     const size_t stripes_b = static_cast<size_t>(d->b - d->a) * n * w * (has_t ? 2 : 1);
     const size_t csr_b = static_cast<size_t>(p->feat_ptr[p->n_features]) * 12 + static_cast<size_t>(plan->E) * 64;
-    const size_t avail = freeb > stripes_b + csr_b + (512ull << 20) ? freeb - stripes_b - csr_b - (512ull << 20) : 0;
+    const size_t fixed_b = stripes_b + csr_b + wuw_fixed + (512ull << 20);
+    const size_t avail = freeb > fixed_b ? freeb - fixed_b : 0;
     budget = std::min(budget, avail * 3 / 4);
   }
   if (ex && ex->mem_budget_bytes > 0) budget = std::min(budget, static_cast<size_t>(ex->mem_budget_bytes));
@@ -1429,7 +1594,19 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       SF_TRY(d.wnb.alloc(d.dev, static_cast<size_t>(cells) * 4, "presence words"));
       SF_TRY(d.wcnt.alloc(d.dev, static_cast<size_t>(cells) * 4, "presence counts"));
       SF_TRY(d.woff.alloc(d.dev, static_cast<size_t>(cells) * 4, "pool offsets"));
-      SF_TRY(d.wpool.alloc(d.dev, static_cast<size_t>(cm) * static_cast<size_t>(n) * w, "value pool"));
+      if (wuw) {
+        const int64_t gcells = static_cast<int64_t>((plan->E + 31) / 32) * sparse_n_ext(n);
+        SF_TRY(d.wnb.alloc(d.dev, static_cast<size_t>(gcells) * 4, "presence words"));
+        SF_TRY(d.woff.alloc(d.dev, static_cast<size_t>(gcells) * 4, "pool offsets"));
+        SF_TRY(d.wpool.alloc(d.dev, static_cast<size_t>(pbound) * w, "value pool"));
+        if (metric == SF_GENERALIZED)
+          SF_TRY(d.wpoola.alloc(d.dev, static_cast<size_t>(pbound) * w, "generalized pool"));
+        SF_TRY(d.wA.alloc(d.dev, static_cast<size_t>(n) * 16, "column sums"));
+        SF_TRY(d.wbase.alloc(d.dev, 16, "pool base"));
+        SF_TRY(sparse_prepare_lens(plan.get(), d, p));
+      } else {
+        SF_TRY(d.wpool.alloc(d.dev, static_cast<size_t>(cm) * static_cast<size_t>(n) * w, "value pool"));
+      }
       size_t tmp = 0;
       SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.wcnt.as<uint32_t>(), d.woff.as<uint32_t>(),
                                             static_cast<int>(cells), d.stream));

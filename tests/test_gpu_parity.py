@@ -27,7 +27,8 @@ from paper_2005_05826_b200 import stripefrac as sf
 pytestmark = pytest.mark.gpu
 
 KERNELS = [N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4, N.KERNEL_ISECT, N.KERNEL_ISECT2, N.KERNEL_ISECT3,
-           N.KERNEL_ISECT4, N.KERNEL_ISECT5, N.KERNEL_SPLIT, N.KERNEL_WSPARSE]  # 3/4: flattened walk
+           N.KERNEL_ISECT4, N.KERNEL_ISECT5, N.KERNEL_SPLIT, N.KERNEL_WSPARSE,
+           N.KERNEL_WUWALK]  # 3/4: flattened walk
 WALKS = (N.KERNEL_DENSE, N.KERNEL_SPARSE, 3, 4)
 
 
@@ -35,7 +36,7 @@ def _kernel_serves(kernel, metric):
     """Dense serves every metric; 2-10 are unweighted-only, 11 weighted-only."""
     if kernel == N.KERNEL_DENSE or kernel == N.KERNEL_AUTO:
         return True
-    return (metric != 1) if kernel == N.KERNEL_WSPARSE else (metric == 1)
+    return (metric != 1) if kernel in (N.KERNEL_WSPARSE, N.KERNEL_WUWALK) else (metric == 1)
 
 
 def _gpu_stripes(problem, metric, prec, start, stop, kernel=N.KERNEL_DENSE, exact=False,
@@ -172,7 +173,8 @@ def test_oracle_random_instances(device_ok, metric, prec):
                 for kernel in (N.KERNEL_DENSE, N.KERNEL_AUTO):
                     d, t, st = _gpu_stripes(problem, metric, prec, start, stop, kernel, exact)
                     used = kernel if kernel != N.KERNEL_AUTO else (
-                        N.KERNEL_WSPARSE if metric != 1 else N.KERNEL_SPARSE if exact else N.KERNEL_SPLIT)
+                        (N.KERNEL_WSPARSE if exact else N.KERNEL_WUWALK) if metric != 1 else
+                        N.KERNEL_SPARSE if exact else N.KERNEL_SPLIT)
                     _assert_close(metric, prec, exact, d, wd, used)
                     if wt is not None:
                         _assert_close(metric, prec, exact, t, wt, used)
@@ -593,3 +595,82 @@ def test_split_banded_light_scatter_is_bitwise_the_one_shot_scatter(device_ok, b
             assert gs.updates_exec == ws.updates_exec  # same light pairs counted
             wd, wt = op.compute_stripes(problem, 1, 8, start, stop)
             _assert_close(1, 8, False, d, wd, N.KERNEL_SPLIT)
+
+
+def _dup_table(inst, dups):
+    """The instance's table with sample columns `dups` = {dst: src} copied."""
+    t = inst.table
+    n, F = t.n_samples(), t.n_features()
+    dense = np.zeros((F, n))
+    for f in range(F):
+        a, b = t.feat_ptr[f], t.feat_ptr[f + 1]
+        dense[f, t.sample_idx[a:b]] = t.counts[a:b]
+    for dst, src in dups.items():
+        dense[:, dst] = dense[:, src]
+    return sf.make_table(t.sample_ids, t.feature_ids, dense)
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("metric", [2, 3])
+def test_weighted_uwalk_matches_oracle(device_ok, metric, prec):
+    """Kernel 12 (the weighted default): u-present rows walked warp-uniformly,
+    v-only rows as A_l - B in double-double. Same terms as the reference,
+    different summation: fp64 within 1e-12 * max(1, |x|), fp32 within
+    max(1e-5|x|, 1e-6); chunked embeddings (the pool is filled chunk by
+    chunk), partial and wrapped ranges, even and odd n."""
+    for seed, n, leaves, dens in [(61, 200, 700, 0.01), (62, 97, 300, 0.05), (63, 64, 64, 0.3),
+                                  (64, 301, 1500, 0.004)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 2, S), (3, 4)]:
+            wd, wt = op.compute_stripes(problem, metric, prec, start, stop)
+            d, t, st = _gpu_stripes(problem, metric, prec, start, stop, N.KERNEL_WUWALK)
+            _assert_close(metric, prec, False, d, wd, N.KERNEL_WUWALK)
+            if wt is not None:
+                _assert_close(metric, prec, False, t, wt, N.KERNEL_WUWALK)
+        d3, t3, s3 = _gpu_stripes(problem, metric, prec, 0, S, N.KERNEL_WUWALK,
+                                  mem_budget=40 * 8 * (n + 1) * 2)
+        assert s3.n_chunks > 1
+        wd, wt = op.compute_stripes(problem, metric, prec, 0, S)
+        _assert_close(metric, prec, False, d3, wd, N.KERNEL_WUWALK)
+
+
+@pytest.mark.parametrize("metric", [2, 3, 4])
+def test_weighted_uwalk_identical_samples_are_exactly_zero(device_ok, metric):
+    """Duplicated samples: the v-only remainder A_l - B cancels exactly (same
+    double-double terms in the same order), so d is exactly 0 like the
+    reference's |u - u| = 0 sums; other pairs stay within tolerance."""
+    inst = sf.random_instance(65, 120, 400, 0.03)
+    table = _dup_table(inst, {7: 3, 100: 3, 61: 60})
+    problem = sf.flatten(inst.tree, table)
+    n = 120
+    S = n // 2
+    if metric == 4:
+        ex, _keep = N.make_exec([0], N.KERNEL_WUWALK, False, 0, 0.5)
+        d = np.zeros((S, n)); t = np.zeros((S, n))
+        N.check(N.lib().sf_compute_stripes(problem.ref, 4, 8, 0, S, N.ptr(d), N.ptr(t), 1, C.byref(ex), None))
+    else:
+        d, t, _ = _gpu_stripes(problem, metric, 8, 0, S, N.KERNEL_WUWALK)
+    dm = op.condense(8, n, d)
+    for a, b in ((3, 7), (3, 100), (7, 100), (60, 61)):
+        assert dm[a, b] == 0.0 and dm[b, a] == 0.0
+    if metric != 4:
+        wd, _ = op.compute_stripes(problem, metric, 8, 0, S)
+        _assert_close(metric, 8, False, d, wd, N.KERNEL_WUWALK)
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("metric", [2, 3, 4])
+def test_weighted_uwalk_even_n_duplicate_half_stripe(device_ok, metric, prec):
+    """Even n: the last stripe holds each pair twice; condense() requires the
+    copies to agree (stripes.cpp:115-122) — bitwise for fp64."""
+    inst = sf.random_instance(66, 130, 500, 0.02)
+    m = sf.Metric(metric)
+    cfg = sf.KernelConfig(m, precision=sf.Precision.Fp64 if prec == 8 else sf.Precision.Fp32,
+                          alpha=0.5 if metric == 4 else 1.0)
+    part = sf.compute_unifrac(inst.tree, inst.table, cfg, 60, 65)  # last stripe is 64
+    last = part.distances[-1]
+    assert np.array_equal(last[:65], last[65:])
+    dm = sf.compute_distance_matrix(inst.tree, inst.table, cfg)  # condense checks the copies
+    assert np.allclose(dm.values, dm.values.T, rtol=0, atol=0)
