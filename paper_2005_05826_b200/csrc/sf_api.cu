@@ -395,7 +395,7 @@ struct DeviceState {
   // intersection v2 (kernel 6): permuted rows, 64-row words, group masks
   DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm, nheavy;
   // split path (kernel 10): light-row sums per slot, |S_e| per row
-  DevBuf lightsum, mcount;
+  DevBuf lightsum, mcount, nzmask;
   DevBuf lcnt, lptr, lmem, lscantmp;  // banded light scatter: member CSR of the light rows
   size_t lscan_bytes = 0;
   bool banded = false;
@@ -605,6 +605,9 @@ sf_status isect2_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
   SF_TRY(d.cacc.alloc(d.dev, 2 * sizeof(unsigned long long), "dense total"));
   SF_TRY(d.colsum.alloc(d.dev, static_cast<size_t>(plan->n) * 4 * sizeof(unsigned long long), "column sums"));
   SF_TRY(d.nodebits.alloc(d.dev, static_cast<size_t>(W * n_ext) * 8, "node-packed X words"));
+  if (plan->kernel == 10)
+    SF_TRY(d.nzmask.alloc(d.dev, static_cast<size_t>((W + 31) / 32) * static_cast<size_t>(plan->n) * 4,
+                          "nonzero-word masks"));
   if (plan->kernel != 10) {  // kernels 6-9 walk packed words through occupancy masks
     const size_t cells = static_cast<size_t>(G * n_ext);
     SF_TRY(d.occ.alloc(d.dev, cells * 4, "occupancy"));
@@ -788,6 +791,8 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   sp_heavy_colsum_kernel<<<grid_for(n, 128), 128, 0, st>>>(
       d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>(),
       d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.colsum.as<unsigned long long>());
+  sp_nzmask_kernel<<<grid_for(((W + 31) / 32) * n, 256), 256, 0, st>>>(
+      d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>(), d.nzmask.as<uint32_t>());
   // first light pass (the one that also adds the light rows' column sums)
   SF_TRY(split_scatter(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), true));
   SF_CUDA(cudaGetLastError());
@@ -796,9 +801,9 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
 }
 
 template <class Real, int RS, int NW, bool BITMAJOR = false, bool UPREF = false, bool HALVES = false,
-          int MINB = 1>
+          int MINB = 1, bool LIST = false, bool PREF = false>
 sf_status launch_split_rs(const SplitArgs& a, cudaStream_t st) {
-  auto* kern = stripe_split_kernel<Real, RS, NW, BITMAJOR, UPREF, HALVES, MINB>;
+  auto* kern = stripe_split_kernel<Real, RS, NW, BITMAJOR, UPREF, HALVES, MINB, LIST, PREF>;
   const dim3 grid((a.n + NW - 1) / NW, (a.s_end - a.s_begin + 32 * RS - 1) / (32 * RS));
   kern<<<grid, 32 * NW, 0, st>>>(a);
   SF_CUDA(cudaGetLastError());
@@ -819,6 +824,8 @@ sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
     case 2: return launch_split_rs<Real, 16, 4, false, true>(a, st);  // + u word prefetch
     case 3: return launch_split_rs<Real, 8, 8>(a, st);                // 8 slots per lane
     case 4: return launch_split_rs<Real, 16, 4, false, false, true>(a, st);
+    case 6: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2, true, true>(a, st);
+    case 7: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2, true, false>(a, st);
     default: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2>(a, st);
   }
 }
@@ -1276,6 +1283,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       a.dist = d.dist.p;
       a.tot = d.tot.p;
       a.counters = d.exec_ctr.as<unsigned long long>();
+      a.nz = d.nzmask.as<uint32_t>();
       // light-sum passes (one unless memory is short); within a pass, with a
       // host destination, chunks of whole 512-stripe tiles whose D2H copy
       // overlaps the next chunk's compute

@@ -404,6 +404,30 @@ __device__ __forceinline__ int msb_pos(uint32_t x) {
   return b;
 }
 
+// Nonzero heavy words per column: bit j of nz[g][c] = (nx[32g + j][c] != 0).
+// Thread per (group, column), coalesced over columns.
+__global__ void sp_nzmask_kernel(const unsigned long long* __restrict__ nx, int64_t n_ext, int32_t n,
+                                 const unsigned int* __restrict__ n_heavy, uint32_t* __restrict__ nz) {
+  const int64_t Hw = (static_cast<int64_t>(*n_heavy) + 63) / 64;
+  const int64_t G = (Hw + 31) / 32;
+  const int64_t total = G * n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = i / n;
+    const int64_t c = i - g * n;
+    uint32_t m = 0u;
+    const int64_t left = Hw - 32 * g;
+    const int jmax = left < 32 ? static_cast<int>(left) : 32;
+    for (int j = 0; j < jmax; ++j)
+      if (__ldg(nx + (32 * g + j) * n_ext + c)) m |= 1u << j;
+    nz[g * n + c] = m;
+  }
+}
+
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 struct SplitArgs {
   const unsigned long long* nx;      // [Hw][n_ext] heavy X words
   const double2* limbs;              // permuted heavy rows, by bit position
@@ -420,6 +444,7 @@ struct SplitArgs {
   void* dist;
   void* tot;
   unsigned long long* counters;  // [0] slot x u-bit FMAs (+ light pairs, added by host), [1] fp64 ops
+  const uint32_t* nz;            // [ceil(Hw/32)][n] nonzero-word masks (LIST variants)
 };
 
 // The next (up to) two set bits of hu, highest first: positions b1, b2 and
@@ -483,8 +508,26 @@ __device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restric
   }
 }
 
+// One nonzero heavy word (u != 0) of the warp's column, HALVES layout.
+template <int RS>
+__device__ __forceinline__ void heavy_word(unsigned long long u, const unsigned long long* row,
+                                           const double2* Lw, int64_t l0, double (&gh)[RS], double (&gl)[RS]) {
+  const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
+  uint32_t vv[RS];
+  if (static_cast<uint32_t>(u >> 32)) {
+#pragma unroll
+    for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
+    heavy_half<RS, false>(static_cast<uint32_t>(u >> 32), Lw + 32, vv, gh, gl);
+  }
+  if (static_cast<uint32_t>(u)) {
+#pragma unroll
+    for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
+    heavy_half<RS, false>(static_cast<uint32_t>(u), Lw, vv, gh, gl);
+  }
+}
+
 template <class Real, int RS, int NW, bool BITMAJOR = false, bool UPREF = false, bool HALVES = false,
-          int MINB = 1>
+          int MINB = 1, bool LIST = false, bool PREF = false>
 __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const SplitArgs a) {
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * NW + (threadIdx.x >> 5);
@@ -508,9 +551,32 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
     gh[i] = 0.0;
     gl[i] = 0.0;
   }
+  if (LIST) {
+    // walk only the nonzero words of column k (per-column masks), and pull
+    // the next word's u and v lines into L1 while this word is walked
+    const int G = (Hw + 31) / 32;
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      uint32_t m = __ldg(a.nz + static_cast<int64_t>(g) * n + k);
+      while (m) {
+        const int w = 32 * g + (__ffs(m) - 1);
+        m &= m - 1u;
+        const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
+        if (PREF && m) {
+          const unsigned long long* nrow = a.nx + static_cast<int64_t>(32 * g + (__ffs(m) - 1)) * n_ext;
+          if (lane == 0) prefetch_l1(nrow + k);
+#pragma unroll
+          for (int i = 0; i < RS; ++i) prefetch_l1(nrow + l0 + 32 * i);
+        }
+        const unsigned long long u = __ldg(row + k);
+        ubits += static_cast<unsigned>(__popcll(u));
+        heavy_word<RS>(u, row, a.limbs + 64 * static_cast<int64_t>(w), l0, gh, gl);
+      }
+    }
+  }
   unsigned long long u_next = (UPREF && Hw > 0) ? __ldg(a.nx + k) : 0ull;
 #pragma unroll 1
-  for (int w = 0; w < Hw; ++w) {
+  for (int w = 0; LIST ? false : w < Hw; ++w) {
     const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
     unsigned long long u;
     if (UPREF) {
