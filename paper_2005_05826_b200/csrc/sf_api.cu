@@ -1213,8 +1213,12 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
                                                                d.lens_pad.as<double>(), d.wpool.as<float>(),
                                                                nullptr, d.wA.as<double2>());
         }
+        wu_nzmask_kernel<<<grid_for(static_cast<int64_t>((W + 31) / 32) * n, 256), 256, 0, st>>>(
+            d.wnb.as<uint32_t>(), n_ext, n, W, d.nzmask.as<uint32_t>());
         SF_CUDA(cudaGetLastError());
         WUWalkArgs a;
+        const char* lst = std::getenv("SF_UWALK_LIST");
+        a.nz = (lst && std::atoi(lst) == 0) ? nullptr : d.nzmask.as<uint32_t>();
         a.nb = d.wnb.as<uint32_t>();
         a.off = d.woff.as<uint32_t>();
         a.pool = d.wpool.p;
@@ -1610,6 +1614,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
         if (metric == SF_GENERALIZED)
           SF_TRY(d.wpoola.alloc(d.dev, static_cast<size_t>(pbound) * w, "generalized pool"));
         SF_TRY(d.wA.alloc(d.dev, static_cast<size_t>(n) * 16, "column sums"));
+        SF_TRY(d.nzmask.alloc(d.dev, static_cast<size_t>(((plan->E + 31) / 32 + 31) / 32) * static_cast<size_t>(n) * 4,
+                              "nonzero-word masks"));
         SF_TRY(d.wbase.alloc(d.dev, 16, "pool base"));
         SF_TRY(sparse_prepare_lens(plan.get(), d, p));
       } else {

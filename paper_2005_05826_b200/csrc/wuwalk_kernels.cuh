@@ -122,6 +122,28 @@ __global__ void wu_colsum_kernel(const uint32_t* __restrict__ nb, const uint32_t
   }
 }
 
+// Nonzero presence words per column: bit j of nz[g][c] = (nb[32g + j][c] != 0).
+__global__ void wu_nzmask_kernel(const uint32_t* __restrict__ nb, int64_t n_ext, int32_t n, int32_t W,
+                                 uint32_t* __restrict__ nz) {
+  const int64_t G = (static_cast<int64_t>(W) + 31) / 32;
+  const int64_t total = G * n;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t g = i / n;
+    const int64_t c = i - g * n;
+    const int64_t left = W - 32 * g;
+    const int jmax = left < 32 ? static_cast<int>(left) : 32;
+    uint32_t m = 0u;
+    for (int j = 0; j < jmax; ++j)
+      if (__ldg(nb + (32 * g + j) * n_ext + c)) m |= 1u << j;
+    nz[g * n + c] = m;
+  }
+}
+
+__device__ __forceinline__ void wu_prefetch_l1(const void* p) {
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
+
 struct WUWalkArgs {
   const uint32_t* nb;   // W x n_ext presence words (global)
   const uint32_t* off;  // W x n_ext global pool offsets
@@ -139,6 +161,7 @@ struct WUWalkArgs {
   void* dist;
   void* tot;  // null for WU
   unsigned long long* exec_updates;
+  const uint32_t* nz;  // [ceil(W/32)][n] nonzero-word masks (null: scan every word)
 };
 
 template <int M, class Real, int RS, int NW>
@@ -168,53 +191,83 @@ __global__ void __launch_bounds__(32 * NW, 2) stripe_wuwalk_kernel(const WUWalkA
     if (GEN) t[i] = 0.0;
   }
   unsigned long long ubits = 0;
-#pragma unroll 1
-  for (int w = 0; w < a.W; ++w) {
-    const uint32_t u = __ldg(a.nb + static_cast<int64_t>(w) * n_ext + k);
-    if (!u) continue;
-    const uint32_t ou = __ldg(a.off + static_cast<int64_t>(w) * n_ext + k);
-    const uint32_t* vrow = a.nb + static_cast<int64_t>(w) * n_ext + l0;
-    const uint32_t* orow = a.off + static_cast<int64_t>(w) * n_ext + l0;
-    uint32_t vv[RS], vo[RS];
+  // one nonzero presence word w of column k (u != 0)
+  auto word = [&](int w, uint32_t u) {
+      const uint32_t ou = __ldg(a.off + static_cast<int64_t>(w) * n_ext + k);
+      const uint32_t* vrow = a.nb + static_cast<int64_t>(w) * n_ext + l0;
+      const uint32_t* orow = a.off + static_cast<int64_t>(w) * n_ext + l0;
+      uint32_t vv[RS], vo[RS];
 #pragma unroll
-    for (int i = 0; i < RS; ++i) vv[i] = __ldg(vrow + 32 * i);
+      for (int i = 0; i < RS; ++i) vv[i] = __ldg(vrow + 32 * i);
 #pragma unroll
-    for (int i = 0; i < RS; ++i) vo[i] = (vv[i] & u) ? __ldg(orow + 32 * i) : 0u;
-    ubits += static_cast<unsigned>(__popc(u));
-    const double* Lw = a.lens + 32 * static_cast<int64_t>(w);
-    uint32_t hu = u;
-    uint32_t q = ou;
-    while (hu) {
-      const int r = __clz(hu);
-      const uint32_t m = 0x80000000u >> r;
-      hu ^= m;
-      const double L = static_cast<double>(static_cast<Real>(__ldg(Lw + r)));
-      const double uval = static_cast<double>(pool[q]);
-      // the v-absent term: fl(L*u) in the working precision (reference: |u-0|*L)
-      const double Lu = GEN ? static_cast<double>(poola[q]) : static_cast<double>(static_cast<Real>(L) * pool[q]);
-      ++q;
-      const uint32_t below = ~(0xffffffffu >> r);  // rows 32w..32w+r-1 (r = 0: none)
+      for (int i = 0; i < RS; ++i) vo[i] = (vv[i] & u) ? __ldg(orow + 32 * i) : 0u;
+      ubits += static_cast<unsigned>(__popc(u));
+      const double* Lw = a.lens + 32 * static_cast<int64_t>(w);
+      uint32_t hu = u;
+      uint32_t q = ou;
+      while (hu) {
+        const int r = __clz(hu);
+        const uint32_t m = 0x80000000u >> r;
+        hu ^= m;
+        const double L = static_cast<double>(static_cast<Real>(__ldg(Lw + r)));
+        const double uval = static_cast<double>(pool[q]);
+        // the v-absent term: fl(L*u) in the working precision (reference: |u-0|*L)
+        const double Lu = GEN ? static_cast<double>(poola[q]) : static_cast<double>(static_cast<Real>(L) * pool[q]);
+        ++q;
+        const uint32_t below = ~(0xffffffffu >> r);  // rows 32w..32w+r-1 (r = 0: none)
 #pragma unroll
-      for (int i = 0; i < RS; ++i) {
-        const uint32_t hit = vv[i] & m;
-        const double f = unit_if(!hit);
-        d[i] = fma(Lu, f, d[i]);
-        if (GEN) t[i] = fma(Lu, f, t[i]);
-        if (hit) {
-          const uint32_t qv = vo[i] + static_cast<uint32_t>(__popc(vv[i] & below));
-          const double v = static_cast<double>(pool[qv]);
-          if (GEN) {
-            const double s = uval + v;
-            const double wgt = pow(s, alpha) * L;
-            d[i] = fma(wgt, fabs(uval - v) / s, d[i]);
-            t[i] += wgt;
-            dd_add(bh[i], bl[i], static_cast<double>(poola[qv]));
-          } else {
-            d[i] = fma(fabs(uval - v), L, d[i]);
-            dd_add(bh[i], bl[i], static_cast<double>(static_cast<Real>(L) * pool[qv]));
+        for (int i = 0; i < RS; ++i) {
+          const uint32_t hit = vv[i] & m;
+          const double f = unit_if(!hit);
+          d[i] = fma(Lu, f, d[i]);
+          if (GEN) t[i] = fma(Lu, f, t[i]);
+          if (hit) {
+            const uint32_t qv = vo[i] + static_cast<uint32_t>(__popc(vv[i] & below));
+            const double v = static_cast<double>(pool[qv]);
+            if (GEN) {
+              const double s = uval + v;
+              const double wgt = pow(s, alpha) * L;
+              d[i] = fma(wgt, fabs(uval - v) / s, d[i]);
+              t[i] += wgt;
+              dd_add(bh[i], bl[i], static_cast<double>(poola[qv]));
+            } else {
+              d[i] = fma(fabs(uval - v), L, d[i]);
+              dd_add(bh[i], bl[i], static_cast<double>(static_cast<Real>(L) * pool[qv]));
+            }
           }
         }
       }
+  };
+  if (a.nz) {
+    // nonzero words only (per-column masks); the next word's u/v words and
+    // offsets are pulled into L1 while this one is walked
+    const int G = (a.W + 31) / 32;
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      uint32_t m = __ldg(a.nz + static_cast<int64_t>(g) * n + k);
+      while (m) {
+        const int w = 32 * g + (__ffs(m) - 1);
+        m &= m - 1u;
+        if (m) {
+          const int64_t nrow = static_cast<int64_t>(32 * g + (__ffs(m) - 1)) * n_ext;
+          if (lane == 0) {
+            wu_prefetch_l1(a.nb + nrow + k);
+            wu_prefetch_l1(a.off + nrow + k);
+          }
+#pragma unroll
+          for (int i = 0; i < RS; ++i) {
+            wu_prefetch_l1(a.nb + nrow + l0 + 32 * i);
+            wu_prefetch_l1(a.off + nrow + l0 + 32 * i);
+          }
+        }
+        word(w, __ldg(a.nb + static_cast<int64_t>(w) * n_ext + k));
+      }
+    }
+  } else {
+#pragma unroll 1
+    for (int w = 0; w < a.W; ++w) {
+      const uint32_t u = __ldg(a.nb + static_cast<int64_t>(w) * n_ext + k);
+      if (u) word(w, u);
     }
   }
 

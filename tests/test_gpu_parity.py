@@ -689,3 +689,21 @@ def test_split_variants_are_bitwise_equal(device_ok, variant, monkeypatch):
     monkeypatch.setenv("SF_SPLIT_VARIANT", variant)
     d, t, _ = _gpu_stripes(problem, 1, 8, 2, n // 2, N.KERNEL_SPLIT)
     assert np.array_equal(d, want_d) and np.array_equal(t, want_t)
+
+
+@pytest.mark.parametrize("metric", [3, 4])
+def test_weighted_uwalk_word_list_is_bitwise_the_full_scan(device_ok, metric, monkeypatch):
+    """Walking only the nonzero words (per-column masks + L1 prefetch) visits
+    the same words in the same order as scanning every word: bit-identical."""
+    inst = sf.random_instance(67, 210, 900, 0.01)
+    problem = sf.flatten(inst.tree, inst.table)
+    S = 105
+    out = []
+    for lst in ("1", "0"):
+        monkeypatch.setenv("SF_UWALK_LIST", lst)
+        ex, _keep = N.make_exec([0], N.KERNEL_WUWALK, False, 0, 0.5)
+        d = np.zeros((S, 210)); t = np.zeros((S, 210))
+        N.check(N.lib().sf_compute_stripes(problem.ref, metric, 8, 0, S, N.ptr(d), N.ptr(t), 1,
+                                           C.byref(ex), None))
+        out.append((d, t))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
