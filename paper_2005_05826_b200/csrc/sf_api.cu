@@ -396,7 +396,7 @@ struct DeviceState {
   DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm, nheavy;
   // split path (kernel 10): light-row sums per slot, |S_e| per row
   DevBuf lightsum, mcount, nzmask;
-  DevBuf lcnt, lptr, lmem, lscantmp;  // banded light scatter: member CSR of the light rows
+  DevBuf lcnt, lptr, lmem, lcur, lscantmp;  // banded light scatter: member CSR + cursors of the light rows
   size_t lscan_bytes = 0;
   bool banded = false;
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
@@ -480,7 +480,7 @@ struct SplitCfg {
 
 // |X_e| threshold of the split path: rows at or above it are walked.
 int split_heavy_min(int n) {
-  double frac = 0.012;
+  double frac = 0.03;  // measured best with the banded light scatter (profiles/r01_ab_c3_split_banded_heavyfrac_*)
   if (const char* e = std::getenv("SF_HEAVY_FRAC")) frac = std::atof(e);
   return std::max(2, static_cast<int>(frac * n));
 }
@@ -720,14 +720,17 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
   const int64_t kb = static_cast<int64_t>(band_mb * 1048576.0 / (16.0 * SB));
   const int KB = static_cast<int>(std::max<int64_t>(256, std::min<int64_t>(kb, n)));
   const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
-  auto* kern = sp_light_band_kernel<NW>;
-  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  auto* kfirst = sp_light_band_kernel<NW, true>;
+  auto* knext = sp_light_band_kernel<NW, false>;
+  SF_CUDA(cudaFuncSetAttribute(kfirst, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  SF_CUDA(cudaFuncSetAttribute(knext, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const int blocks = static_cast<int>(std::min<int64_t>((E + NW - 1) / NW, 148 * 16));
   for (int s0 = p0; s0 < p1; s0 += SB) {
     const int s1 = std::min(p1, s0 + SB);
     for (int k0 = 0; k0 < n; k0 += KB) {
+      auto* kern = s0 == p0 ? kfirst : knext;  // first band of the pass: search, store cursors
       kern<<<blocks, 32 * NW, smem, st>>>(d.perm.as<int32_t>(), plan->E, n, d.nheavy.as<unsigned int>(),
-                                          d.lptr.as<uint32_t>(), d.lmem.as<int32_t>(),
+                                          d.lptr.as<uint32_t>(), d.lmem.as<int32_t>(), d.lcur.as<uint16_t>(),
                                           d.fix.as<unsigned long long>(), plan->lo_bits, p0, s0, s1, k0,
                                           std::min(n, k0 + KB), d.lightsum.as<double>(),
                                           d.exec_ctr.as<unsigned long long>(), heavy_min);
@@ -1652,8 +1655,10 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                          d.dev, d.a, d.b, d.light_pass, freeb >> 20);
           SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * per_stripe, "light-row sums"));
           SF_TRY(d.mcount.alloc(d.dev, static_cast<size_t>(plan->E) * 4, "row presence counts"));
+          // u32 member offsets; u16 cursors (light rows have < heavy_min members)
           d.banded = light_banded() &&
-                     static_cast<uint64_t>(plan->E) * static_cast<uint64_t>(split_heavy_min(n)) < (1ull << 32);
+                     static_cast<uint64_t>(plan->E) * static_cast<uint64_t>(split_heavy_min(n)) < (1ull << 32) &&
+                     split_heavy_min(n) <= 65535;
           if (d.banded) {
             const size_t E1 = static_cast<size_t>(plan->E) + 1;
             SF_TRY(d.lcnt.alloc(d.dev, E1 * 4, "light member counts"));
@@ -1661,6 +1666,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
             // light rows have |X_e| < heavy_min members
             SF_TRY(d.lmem.alloc(d.dev, static_cast<size_t>(plan->E) * static_cast<size_t>(split_heavy_min(n)) * 4,
                                 "light members"));
+            SF_TRY(d.lcur.alloc(d.dev, static_cast<size_t>(plan->E) * static_cast<size_t>(split_heavy_min(n)) * 4,
+                                "light member cursors"));
             size_t tmp = 0;
             SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.lcnt.as<uint32_t>(), d.lptr.as<uint32_t>(),
                                                   static_cast<int>(E1), d.stream));

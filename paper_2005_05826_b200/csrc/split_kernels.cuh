@@ -337,10 +337,17 @@ __device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ mem, 
 
 // One band: slots with stripe in [s0, s1) and column in [k0, k1). gl rows are
 // relative to the light pass start p0 (layout unchanged: (s - p0) * n + k).
-template <int NW>
+// Every slot of a pair {a < b}, d = b - a, is owned by one member:
+//   slot (s = d - 1,     k = a): a's partners above, b in [a + s0 + 1, a + se];
+//   slot (s = n - d - 1, k = b): b's partners below, a in [b - n + 1 + s0, b - n + se].
+// A member works only in the column band holding it, and both partner
+// ranges move upward as the stripe bands advance, so two per-member cursors
+// (u16, next partner index) replace the binary searches after the first band
+// of a pass (FIRST: search, then store the cursors).
+template <int NW, bool FIRST>
 __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
     const int32_t* __restrict__ perm, int32_t E, int32_t n, const unsigned int* __restrict__ n_heavy,
-    const uint32_t* __restrict__ lptr, const int32_t* __restrict__ lmem,
+    const uint32_t* __restrict__ lptr, const int32_t* __restrict__ lmem, uint16_t* __restrict__ cur,
     const unsigned long long* __restrict__ fix, int32_t lo_bits, int32_t p0, int32_t s0, int32_t s1,
     int32_t k0, int32_t k1, double* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
     int32_t list_cap) {
@@ -361,35 +368,36 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
     for (int i = lane; i < x; i += 32) mem[i] = __ldg(lmem + b0 + i);
     __syncwarp();
     const double2 L = limbs_of(fix[perm[idx]], lo_bits);
-    for (int i = lane; i + 1 < x; i += 32) {
+    uint16_t* c = cur + 2 * static_cast<int64_t>(b0);
+    for (int i = lane; i < x; i += 32) {
       const int a = mem[i];
-      // slot (s = b - a - 1, k = a): b in [a + s0 + 1, a + se]
-      if (a >= k0 && a < k1) {
-        int j = lower_bound_i32(mem, i + 1, x, a + s0 + 1);
-        const int jend = lower_bound_i32(mem, j, x, a + se + 1);
-        for (; j < jend; ++j) {
-          const int s = mem[j] - a - 1;
-          double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + a);
-          atomicAdd(cell, L.x);
-          atomicAdd(cell + 1, L.y);
-          ++pairs;
-        }
+      if (a < k0 || a >= k1) continue;
+      int j1, j2;
+      if (FIRST) {
+        j1 = lower_bound_i32(mem, i + 1, x, a + s0 + 1);
+        j2 = lower_bound_i32(mem, 0, i, a - n + 1 + s0);
+      } else {
+        const uint32_t cc = reinterpret_cast<const uint32_t*>(c)[i];
+        j1 = static_cast<int>(cc & 0xffffu);
+        j2 = static_cast<int>(cc >> 16);
       }
-      // slot (s = n - d - 1, k = b), d = b - a: b in [a + n - se, a + n - 1 - s0] and [k0, k1)
-      const int blo = max(a + n - se, k0);
-      const int bhi = min(a + n - 1 - s0, k1 - 1);
-      if (blo <= bhi) {
-        int j = lower_bound_i32(mem, i + 1, x, blo);
-        const int jend = lower_bound_i32(mem, j, x, bhi + 1);
-        for (; j < jend; ++j) {
-          const int b = mem[j];
-          const int s = n - (b - a) - 1;
-          double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + b);
-          atomicAdd(cell, L.x);
-          atomicAdd(cell + 1, L.y);
-          ++pairs;
-        }
+      // partners above: slot (b - a - 1, a)
+      for (; j1 < x && mem[j1] <= a + se; ++j1) {
+        const int s = mem[j1] - a - 1;
+        double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + a);
+        atomicAdd(cell, L.x);
+        atomicAdd(cell + 1, L.y);
+        ++pairs;
       }
+      // partners below: slot (n - (a - a') - 1, a)
+      for (; j2 < i && mem[j2] <= a - n + se; ++j2) {
+        const int s = n - (a - mem[j2]) - 1;
+        double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + a);
+        atomicAdd(cell, L.x);
+        atomicAdd(cell + 1, L.y);
+        ++pairs;
+      }
+      reinterpret_cast<uint32_t*>(c)[i] = static_cast<uint32_t>(j1) | (static_cast<uint32_t>(j2) << 16);
     }
     __syncwarp();
   }
