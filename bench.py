@@ -260,7 +260,9 @@ def run_ours(args, cfg):
         return None
 
     # ---- roofline of the dominant kernel (K2 stripe update)
-    peak_fma = measured_fp_peak(local, cfg["precision"])
+    # the split kernel (unweighted) accumulates exact limbs with DFMA in every
+    # output precision: its pipe is FP64 for the fp32 lines too
+    peak_fma = measured_fp_peak(local, "fp64" if (metric == 1 and fp64_ops > 0) else cfg["precision"])
     stripe_s = sum(str_ms) / 1e3
     peak_tf = peak_fma * 2 / 1e12
     if metric == 1 and fp64_ops > 0:
