@@ -9,6 +9,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -829,6 +830,9 @@ sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
     case 4: return launch_split_rs<Real, 16, 4, false, false, true>(a, st);
     case 6: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2, true, true>(a, st);
     case 7: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2, true, false>(a, st);
+    case 8: return launch_split_rs<Real, 8, 8, false, false, true, 3>(a, st);    // 24 warps/SM
+    case 9: return launch_split_rs<Real, 12, 4, false, false, true, 5>(a, st);   // 20 warps/SM
+    case 10: return launch_split_rs<Real, 16, 4, false, false, true, 4>(a, st);  // 16 warps, 4-warp CTAs
     default: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2>(a, st);
   }
 }
@@ -1780,8 +1784,13 @@ sf_status sf_compute_stripes(const sf_problem* p, sf_metric metric, sf_precision
   if (metric != SF_WEIGHTED_UNNORMALIZED && !tot_out)
     return fail(SF_EINVAL, "tot_out is required for ratio metrics");
   sf_plan* plan = nullptr;
+  const bool dbg = std::getenv("SF_DEBUG") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   SF_TRY(sf_plan_create(p, metric, prec, start, stop, ex, &plan));
   std::unique_ptr<sf_plan> guard(plan);
+  if (dbg)
+    std::fprintf(stderr, "stripefrac: plan_create %.1f ms\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   auto pinned = [](const void* ptr) {
     cudaPointerAttributes at{};
     if (!ptr || cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
@@ -1809,6 +1818,10 @@ sf_status sf_compute_stripes(const sf_problem* p, sf_metric metric, sf_precision
     SF_TRY(sf_plan_sync(plan));
     SF_TRY(sf_plan_download(plan, dist_out, tot_out));
   }
+  if (dbg)
+    std::fprintf(stderr, "stripefrac: compute_stripes %.1f ms (device %.1f ms)\n",
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(),
+                 plan->stats.total_ms);
   if (stats_out) *stats_out = plan->stats;
   return SF_OK;
 }
