@@ -273,9 +273,10 @@ def run_ours(args, cfg):
             "bound": "fp64", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
             "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None,
             # dram__bytes_read+write of one `ncu --set full` capture of this kernel
-            # (profiles/r01_ncu_split_c3_1024stripes.txt: 1.046 GB + 0.424 GB for
-            # 1024 stripes at C3), per launch: scaled by the stripes it covers
-            "traffic": (round((1.045830e9 + 0.423685e9) / 1024 * stop_all / max(world, 1))
+            # (profiles/r01_ncu_split_c3_1024stripes.txt: 0.685 GB + 0.406 GB for
+            # 1024 stripes at C3, heavy threshold 0.03), per launch: scaled by
+            # the stripes it covers
+            "traffic": (round((0.685215e9 + 0.406339e9) / 1024 * stop_all / max(world, 1))
                         if cfg is CONFIGS["c3"] else None),
             "traffic_unit": "bytes per launch",
             "kernel": "stripe_split_kernel (heavy-row walk)",
