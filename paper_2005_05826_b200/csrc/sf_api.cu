@@ -715,7 +715,7 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
     SF_CUDA(cudaGetLastError());
     plan->stats.launches += 3;
   }
-  double band_mb = 64.0;
+  double band_mb = 32.0;  // measured: 32 MB <= 64 MB < 96 MB (profiles/r01_ab_c3_split_band*)
   if (const char* e = std::getenv("SF_LIGHT_BAND_MB")) band_mb = std::max(1.0, std::atof(e));
   const int SB = 32 * SplitCfg::RS;
   const int64_t kb = static_cast<int64_t>(band_mb * 1048576.0 / (16.0 * SB));

@@ -85,11 +85,23 @@ __device__ __forceinline__ void update_entry(Real u, Real v, Real len, Real& d, 
 __device__ __forceinline__ double pow_r(double x, double a) { return pow(x, a); }
 __device__ __forceinline__ float pow_r(float x, float a) { return powf(x, a); }
 
+// x^alpha for x > 0 with the common exponents on their exact / correctly
+// rounded forms (sqrt is correctly rounded, CUDA pow is within 2 ulp): the
+// branch is warp-uniform (alpha is a launch argument).
+template <class Real>
+__device__ __forceinline__ Real pow_alpha(Real x, Real alpha) {
+  if (alpha == Real(1)) return x;
+  if (alpha == Real(0.5)) return sqrt(x);
+  if (alpha == Real(0)) return Real(1);
+  if (alpha == Real(2)) return x * x;
+  return pow_r(x, alpha);
+}
+
 template <bool EXACT, class Real>
 __device__ __forceinline__ void update_generalized(Real u, Real v, Real len, Real alpha, Real& d, Real& t) {
   const Real s = u + v;
   if (s != Real(0)) {
-    const Real w = pow_r(s, alpha) * len;
+    const Real w = pow_alpha(s, alpha) * len;
     const Real q = abs_r(u - v) / s;
     d = EXACT ? mul_add_rn(w, q, d) : fma_r(w, q, d);
     t += w;

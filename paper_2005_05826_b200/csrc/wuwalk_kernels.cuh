@@ -85,7 +85,7 @@ __global__ void wu_fill_kernel(const double* __restrict__ emb, int64_t stride, i
       pool[q] = v;
       if (GEN) {
         const Real L = static_cast<Real>(lens[32 * w + r]);
-        poola[q] = pow_r(v, static_cast<Real>(alpha)) * L;
+        poola[q] = pow_alpha(v, static_cast<Real>(alpha)) * L;
       }
       ++q;
     }
@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(32 * NW, 2) stripe_wuwalk_kernel(const WUWalkA
             const double v = static_cast<double>(pool[qv]);
             if (GEN) {
               const double s = uval + v;
-              const double wgt = pow(s, alpha) * L;
+              const double wgt = pow_alpha(s, alpha) * L;
               d[i] = fma(wgt, fabs(uval - v) / s, d[i]);
               t[i] += wgt;
               dd_add(bh[i], bl[i], static_cast<double>(poola[qv]));
