@@ -1,10 +1,9 @@
 #!/usr/bin/env bash
-# GPU round-trip: generalized + banded parity, C3/C2/C4 bench lines.
+# GPU round-trip: end-to-end phase breakdown (C3 fp64/fp32, C2).
 mkdir -p gpurun_out
-export BENCH_ALLOW_SHORT=1
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -m gpu -k "generalized or banded or uwalk" > gpurun_out/pytest_gen.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gen.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.log
-timeout 600 python bench.py --config c2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.log
-timeout 900 python bench.py --config c4 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/bench_c4.json 2> gpurun_out/bench_c4.log
-timeout 900 python bench.py --config c3wn --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/bench_c3wn.json 2> gpurun_out/bench_c3wn.log
+export SF_DEBUG=1
+timeout 900 python tools/e2e_probe.py --config c3 --reps 4 > gpurun_out/e2e_c3.log 2>&1
+timeout 900 python tools/e2e_probe.py --config c3f32 --reps 3 > gpurun_out/e2e_c3f32.log 2>&1
+timeout 600 python tools/e2e_probe.py --config c2 --reps 4 > gpurun_out/e2e_c2.log 2>&1
+nproc > gpurun_out/nproc.txt; free -g >> gpurun_out/nproc.txt
 echo done
