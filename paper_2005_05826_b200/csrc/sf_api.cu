@@ -64,6 +64,38 @@ sf_status fail(sf_status st, const std::string& msg) {
   return st;
 }
 
+// Device memory comes from each device's default stream-ordered pool with an
+// unbounded release threshold: a plan's buffers (tens of GB at C3) go back
+// to the pool when it is destroyed and the next plan takes them without new
+// cudaMalloc/page-table work (plan creation was 70-300 ms of an end-to-end
+// call; see tools/e2e_probe.py).
+void keep_pool(int device) {
+  static bool done[64] = {};
+  if (device < 0 || device >= 64 || done[device]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  cudaGetLastError();
+  done[device] = true;
+}
+
+// Free device memory including what the pool holds but no buffer uses.
+sf_status device_free_bytes(int device, size_t* out) {
+  size_t freeb = 0, totalb = 0;
+  SF_CUDA(cudaMemGetInfo(&freeb, &totalb));
+  cudaMemPool_t pool;
+  uint64_t reserved = 0, used = 0;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess &&
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
+    freeb += static_cast<size_t>(reserved - used);
+  cudaGetLastError();
+  *out = freeb;
+  return SF_OK;
+}
+
 // Device allocation owned by one device.
 struct DevBuf {
   int dev = -1;
@@ -78,7 +110,9 @@ struct DevBuf {
       int cur = -1;
       cudaGetDevice(&cur);
       cudaSetDevice(dev);
-      cudaFree(p);
+      cudaDeviceSynchronize();  // no kernel may still use it (the pool reuses it at once)
+      cudaFreeAsync(p, 0);
+      cudaStreamSynchronize(0);
       if (cur >= 0) cudaSetDevice(cur);
     }
     p = nullptr;
@@ -88,7 +122,9 @@ struct DevBuf {
     reset();
     dev = device;
     if (nbytes == 0) nbytes = 16;
-    const cudaError_t e = cudaMalloc(&p, nbytes);
+    keep_pool(device);
+    cudaError_t e = cudaMallocAsync(&p, nbytes, 0);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(0);  // usable from any stream
     if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();
@@ -409,6 +445,8 @@ struct DeviceState {
   ~DeviceState() {
     if (dev >= 0) {
       cudaSetDevice(dev);
+      if (stream) cudaStreamSynchronize(stream);
+      if (copy_stream) cudaStreamSynchronize(copy_stream);
       for (auto e : events) cudaEventDestroy(e);
       for (auto e : chunk_events) cudaEventDestroy(e);
       if (stream) cudaStreamDestroy(stream);
@@ -1559,8 +1597,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   size_t budget = SIZE_MAX;
   for (auto& d : plan->devs) {
     SF_CUDA(cudaSetDevice(d->dev));
-    size_t freeb = 0, totalb = 0;
-    SF_CUDA(cudaMemGetInfo(&freeb, &totalb));
+    size_t freeb = 0;
+    SF_TRY(device_free_bytes(d->dev, &freeb));
     const size_t stripes_b = static_cast<size_t>(d->b - d->a) * n * w * (has_t ? 2 : 1);
     const size_t csr_b = static_cast<size_t>(p->feat_ptr[p->n_features]) * 12 + static_cast<size_t>(plan->E) * 64;
     const size_t fixed_b = stripes_b + csr_b + wuw_fixed + (512ull << 20);
@@ -1642,8 +1680,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
         if (plan->kernel == 10) {
           // light sums for the whole range if they fit next to everything
           // else, else for passes of whole 512-stripe tiles
-          size_t freeb = 0, totalb = 0;
-          SF_CUDA(cudaMemGetInfo(&freeb, &totalb));
+          size_t freeb = 0;
+          SF_TRY(device_free_bytes(d.dev, &freeb));
           const size_t per_stripe = static_cast<size_t>(n) * 16;
           const size_t reserve = (1ull << 30);
           size_t fit = freeb > reserve ? (freeb - reserve) / per_stripe : 0;
