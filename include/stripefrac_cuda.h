@@ -133,6 +133,15 @@ sf_status sf_plan_run(sf_plan* plan, int32_t finalize);
 sf_status sf_plan_sync(sf_plan* plan);
 /* Copy stripes [start, stop) to host buffers (row-major, see above). */
 sf_status sf_plan_download(sf_plan* plan, void* dist_out, void* tot_out);
+/*
+ * Write the plan's finalized stripes as a .strf file. Replaces
+ * write_stripe_file (stripes.cpp:179-201): same 32-byte header, payload
+ * (finalized distances, then raw totals for UW/WN) and FNV-1a checksum, so
+ * read_stripe_file / merge of the reference read it. The stripes stream
+ * from device memory through pinned staging (no full host copy). Refuses an
+ * unfinalized plan like the reference; SF_GENERALIZED has no format code.
+ */
+sf_status sf_plan_write_strf(sf_plan* plan, const char* path);
 sf_status sf_plan_stats(const sf_plan* plan, sf_stats* out);
 void sf_plan_destroy(sf_plan* plan);
 

@@ -376,6 +376,20 @@ int cmd_mantel_golden(const std::string& dir) {
   return 0;
 }
 
+// .strf files written by the reference itself (stripes.cpp:179-201) for the
+// demo data: byte-level fixtures for the device-streamed writer.
+int cmd_strf_golden(const std::string& dir, const std::string& demo_dir) {
+  const PhyloTree tree = parse_newick_file(demo_dir + "/demo_tree.nwk");
+  const SampleTable table = load_table_file(demo_dir + "/demo_table.tsv", TableFormat::TsvDense);
+  write_stripe_file(dir + "/demo_wn_fp64_0_4.strf",
+                    compute_unifrac<double>(tree, table, cfg_of(Metric::WeightedNormalized, Precision::Fp64), 0, 4));
+  write_stripe_file(dir + "/demo_uw_fp32_1_3.strf",
+                    compute_unifrac<float>(tree, table, cfg_of(Metric::Unweighted, Precision::Fp32), 1, 3));
+  write_stripe_file(dir + "/demo_wu_fp64_0_4.strf",
+                    compute_unifrac<double>(tree, table, cfg_of(Metric::WeightedUnnormalized, Precision::Fp64), 0, 4));
+  return 0;
+}
+
 // digest of a random_instance, to pin the port of the generator at scale
 int cmd_instance(std::uint64_t seed, int n, int leaves, double density, int subset) {
   const auto t0 = std::chrono::steady_clock::now();
@@ -483,6 +497,7 @@ int main(int argc, char** argv) {
     const std::string cmd = argv[1];
     if (cmd == "golden" && argc >= 4) return cmd_golden(argv[2], argv[3]);
     if (cmd == "mantel_golden" && argc >= 3) return cmd_mantel_golden(argv[2]);
+    if (cmd == "strf_golden" && argc >= 4) return cmd_strf_golden(argv[2], argv[3]);
     if (cmd == "instance" && argc >= 7)
       return cmd_instance(std::strtoull(argv[2], nullptr, 10), std::atoi(argv[3]), std::atoi(argv[4]),
                           std::atof(argv[5]), std::atoi(argv[6]));

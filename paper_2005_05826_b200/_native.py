@@ -81,6 +81,7 @@ SIGNATURES = {
     "sf_plan_download": (C.c_int, [_P, _P, _P]),
     "sf_plan_stats": (C.c_int, [_P, C.POINTER(sf_stats)]),
     "sf_plan_destroy": (None, [_P]),
+    "sf_plan_write_strf": (C.c_int, [_P, C.c_char_p]),
     "sf_accumulate_batch": (C.c_int, [_P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int, C.c_int,
                                       C.c_int32, C.c_int32, _P, _P, C.c_int32]),
     "sf_embed_rows": (C.c_int, [C.POINTER(sf_problem), C.c_int32, C.c_int32, C.c_int32, _P,

@@ -2166,4 +2166,100 @@ sf_status sf_mantel(int32_t n, const double* m1, const double* m2, int32_t permu
   return SF_OK;
 }
 
+// ---------------------------------------------------------------- .strf
+// write_stripe_file (stripes.cpp:179-201) straight from the plan's device
+// stripes: 32-byte header, finalized distances then raw totals (UW, WN),
+// FNV-1a 64 (common.cpp:51-58) over the payload. Blocks stream through two
+// pinned staging buffers: the next block's D2H copy overlaps hashing and
+// writing the current one.
+sf_status sf_plan_write_strf(sf_plan* plan, const char* path) {
+  if (!plan || !path) return fail(SF_EINVAL, "null argument");
+  if (!plan->ran) return fail(SF_ESTATE, "plan has not run");
+  if (!plan->finalized) return fail(SF_EINVAL, "refusing to write an unfinalized stripe set");
+  if (plan->metric == SF_GENERALIZED)
+    return fail(SF_EINVAL, "generalized stripes have no .strf metric code");
+  SF_TRY(sf_plan_sync(plan));
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return fail(SF_EINVAL, std::string("cannot open '") + path + "' for writing");
+  struct FileGuard {
+    FILE* f;
+    ~FileGuard() {
+      if (f) std::fclose(f);
+    }
+  } fguard{f};
+  const size_t w = plan->prec == SF_FP64 ? 8 : 4;
+  unsigned char hdr[32] = {'S', 'T', 'R', 'F', 1, static_cast<unsigned char>(w),
+                           static_cast<unsigned char>(plan->metric), 0};
+  const uint64_t dims[3] = {static_cast<uint64_t>(plan->n), static_cast<uint64_t>(plan->start),
+                            static_cast<uint64_t>(plan->stop)};
+  for (int i = 0; i < 3; ++i)
+    for (int b = 0; b < 8; ++b) hdr[8 + 8 * i + b] = static_cast<unsigned char>(dims[i] >> (8 * b));
+  bool ok = std::fwrite(hdr, 1, 32, f) == 32;
+  // blocks: every device's distances, then (ratio metrics) every device's totals
+  struct Block {
+    DeviceState* d;
+    const char* src;
+    size_t bytes;
+  };
+  std::vector<Block> blocks;
+  const bool has_t = plan->metric != SF_WEIGHTED_UNNORMALIZED;
+  for (int arr = 0; arr < (has_t ? 2 : 1); ++arr)
+    for (auto& dp : plan->devs) {
+      const size_t bytes = static_cast<size_t>(dp->b - dp->a) * plan->n * w;
+      blocks.push_back({dp.get(), arr == 0 ? dp->dist.as<char>() : dp->tot.as<char>(), bytes});
+    }
+  constexpr size_t CH = size_t{64} << 20;
+  char* stage = nullptr;
+  SF_CUDA(cudaMallocHost(&stage, 2 * CH));
+  struct HostGuard {
+    char* p;
+    ~HostGuard() { cudaFreeHost(p); }
+  } hguard{stage};
+  cudaEvent_t ev[2];
+  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  SF_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  struct EventGuard {
+    cudaEvent_t* e;
+    ~EventGuard() {
+      cudaEventDestroy(e[0]);
+      cudaEventDestroy(e[1]);
+    }
+  } eguard{ev};
+  // flatten into chunks, issue chunk i+1 before consuming chunk i
+  struct Chunk {
+    DeviceState* d;
+    const char* src;
+    size_t len;
+  };
+  std::vector<Chunk> chunks;
+  for (const Block& b : blocks)
+    for (size_t off = 0; off < b.bytes; off += CH) chunks.push_back({b.d, b.src + off, std::min(CH, b.bytes - off)});
+  auto issue = [&](size_t i) -> sf_status {
+    const Chunk& c = chunks[i];
+    SF_CUDA(cudaSetDevice(c.d->dev));
+    SF_CUDA(cudaMemcpyAsync(stage + (i & 1) * CH, c.src, c.len, cudaMemcpyDeviceToHost, c.d->stream));
+    SF_CUDA(cudaEventRecord(ev[i & 1], c.d->stream));
+    return SF_OK;
+  };
+  uint64_t h = 0xcbf29ce484222325ull;
+  if (!chunks.empty()) SF_TRY(issue(0));
+  for (size_t i = 0; i < chunks.size(); ++i) {
+    SF_CUDA(cudaEventSynchronize(ev[i & 1]));
+    if (i + 1 < chunks.size()) SF_TRY(issue(i + 1));  // other buffer: free since chunk i-1 was consumed
+    const unsigned char* p = reinterpret_cast<const unsigned char*>(stage + (i & 1) * CH);
+    for (size_t k = 0; k < chunks[i].len; ++k) {
+      h ^= p[k];
+      h *= 0x100000001b3ull;
+    }
+    ok = ok && std::fwrite(p, 1, chunks[i].len, f) == chunks[i].len;
+  }
+  unsigned char tail[8];
+  for (int b = 0; b < 8; ++b) tail[b] = static_cast<unsigned char>(h >> (8 * b));
+  ok = ok && std::fwrite(tail, 1, 8, f) == 8;
+  ok = (std::fclose(f) == 0) && ok;
+  fguard.f = nullptr;
+  if (!ok) return fail(SF_EINVAL, std::string("failed writing '") + path + "'");
+  return SF_OK;
+}
+
 }  // extern "C"

@@ -796,6 +796,27 @@ def compute_unifrac(tree: PhyloTree, table: SampleTable, cfg: KernelConfig, star
     return sset
 
 
+def compute_unifrac_to_strf(tree: PhyloTree, table: SampleTable, cfg: KernelConfig, path: str,
+                            start: int = 0, stop: int = -1,
+                            exec_options: Optional[ExecOptions] = None) -> None:
+    """compute_unifrac + write_stripe_file (stripes.cpp:179-201) without a
+    host copy of the stripes: sf_plan_write_strf streams them from device."""
+    _check_cfg(cfg)
+    if stop < 0:
+        stop = total_stripes(table.n_samples())
+    problem = flatten(tree, table)
+    eo = exec_options or ExecOptions()
+    ex, _keep = N.make_exec(eo.devices, eo.kernel, eo.exact, eo.mem_budget_bytes, cfg.alpha)
+    plan = C.c_void_p()
+    _call(N.lib().sf_plan_create(problem.ref, int(cfg.metric), int(cfg.precision), start, stop,
+                                 C.byref(ex), C.byref(plan)))
+    try:
+        _call(N.lib().sf_plan_run(plan, 1))
+        _call(N.lib().sf_plan_write_strf(plan, str(path).encode()))
+    finally:
+        N.lib().sf_plan_destroy(plan)
+
+
 def compute_distance_matrix(tree: PhyloTree, table: SampleTable, cfg: KernelConfig,
                             threads: int = 1, counters: Optional[KernelCounters] = None,
                             real=None, exec_options: Optional[ExecOptions] = None) -> DistanceMatrix:

@@ -707,3 +707,45 @@ def test_weighted_uwalk_word_list_is_bitwise_the_full_scan(device_ok, metric, mo
                                            C.byref(ex), None))
         out.append((d, t))
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+def test_plan_write_strf_matches_reference_files(device_ok, tmp_path):
+    """sf_plan_write_strf streams the stripes from device into the .strf
+    format byte for byte as the reference's write_stripe_file
+    (tests/golden/*.strf written by oracle/_ref; exact mode: the stripes
+    themselves are bitwise the reference's)."""
+    case = gu.load("demo.json")
+    tree, table = gu.case_inputs(case)
+    for name, m, p, a, b in (("demo_wn_fp64_0_4", sf.Metric.WeightedNormalized, sf.Precision.Fp64, 0, 4),
+                             ("demo_uw_fp32_1_3", sf.Metric.Unweighted, sf.Precision.Fp32, 1, 3),
+                             ("demo_wu_fp64_0_4", sf.Metric.WeightedUnnormalized, sf.Precision.Fp64, 0, 4)):
+        out = tmp_path / f"{name}.strf"
+        sf.compute_unifrac_to_strf(tree, table, sf.KernelConfig(m, precision=p), str(out), a, b,
+                                   exec_options=sf.ExecOptions(exact=True))
+        want = (gu.GOLDEN / f"{name}.strf").read_bytes()
+        assert out.read_bytes() == want
+
+
+def test_plan_write_strf_equals_host_writer(device_ok, tmp_path):
+    """Larger instance, several 64 MB-free chunks aside: same bytes as the host
+    writer on the downloaded stripes; refuses unfinalized and generalized."""
+    inst = sf.random_instance(71, 700, 2000, 0.01)
+    for m in (sf.Metric.Unweighted, sf.Metric.WeightedNormalized):
+        cfg = sf.KernelConfig(m)
+        p1 = tmp_path / "dev.strf"
+        sf.compute_unifrac_to_strf(inst.tree, inst.table, cfg, str(p1), 10, 300)
+        part = sf.compute_unifrac(inst.tree, inst.table, cfg, 10, 300)
+        p2 = tmp_path / "host.strf"
+        sf.write_stripe_file(str(p2), part)
+        assert p1.read_bytes() == p2.read_bytes()
+    problem = sf.flatten(inst.tree, inst.table)
+    ex, _keep = N.make_exec([0])
+    plan = C.c_void_p()
+    N.check(N.lib().sf_plan_create(problem.ref, 1, 8, 0, 5, C.byref(ex), C.byref(plan)))
+    N.check(N.lib().sf_plan_run(plan, 0))
+    assert N.lib().sf_plan_write_strf(plan, str(tmp_path / "x.strf").encode()) == N.SF_EINVAL
+    assert "unfinalized" in N.lib().sf_last_error().decode()
+    N.lib().sf_plan_destroy(plan)
+    with pytest.raises(sf.Error, match="no .strf metric code"):
+        sf.compute_unifrac_to_strf(inst.tree, inst.table, sf.KernelConfig(sf.Metric.Generalized, alpha=0.5),
+                                   str(tmp_path / "g.strf"), 0, 5)
