@@ -1,8 +1,8 @@
 #!/usr/bin/env bash
-# GPU round-trip: full parity suite with pooled device memory, e2e phases, C3 bench.
+# GPU round-trip: .strf writer parity, Mantel at C3 scale, C4 fp32 line.
 mkdir -p gpurun_out
-timeout 2000 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-SF_DEBUG=1 timeout 900 python tools/e2e_probe.py --config c3 --reps 4 > gpurun_out/e2e_c3.log 2>&1
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.log
-timeout 600 python bench.py --config c2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.log
+export BENCH_ALLOW_SHORT=1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_mantel.py -q -m gpu -k "strf or mantel" > gpurun_out/pytest_strf.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strf.log
+timeout 1200 python tools/mantel_bench.py --config c3 --perms 999 > gpurun_out/mantel_c3.json 2> gpurun_out/mantel_c3.log
+timeout 900 python bench.py --config c4f32 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/bench_c4f32.json 2> gpurun_out/bench_c4f32.log
 echo done
