@@ -208,18 +208,49 @@ sf_status validate_problem(const sf_problem* p) {
                                  (leaf ? " is a leaf with children" : " is an internal row without children"));
   }
   if (p->feat_ptr[0] != 0) return fail(SF_EINVAL, "feat_ptr[0] must be 0");
-  for (int f = 0; f < p->n_features; ++f) {
+  for (int f = 0; f < p->n_features; ++f)
     if (p->feat_ptr[f + 1] < p->feat_ptr[f]) return fail(SF_EINVAL, "feat_ptr is not monotone");
-    int prev = -1;
-    for (int64_t e = p->feat_ptr[f]; e < p->feat_ptr[f + 1]; ++e) {
-      const int s = p->sample_idx[e];
-      if (s <= prev || s >= p->n_samples)
-        return fail(SF_EINVAL, "sample indices of a feature must be ascending and in range");
-      prev = s;
-      const double c = p->counts[e];
-      if (!(c >= 0.0) || c > 1.7976931348623157e308)
-        return fail(SF_EINVAL, "count must be finite and non-negative");
+  // the table entries (15M at C3) are checked by feature ranges on host
+  // threads; the error reported is the first in feature order, as a
+  // sequential scan would report it
+  const int F = p->n_features;
+  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  std::vector<int> bad_f(static_cast<size_t>(T), F);
+  std::vector<int> bad_kind(static_cast<size_t>(T), 0);
+  auto scan = [&](int t) {
+    const int f0 = static_cast<int>(static_cast<int64_t>(F) * t / T);
+    const int f1 = static_cast<int>(static_cast<int64_t>(F) * (t + 1) / T);
+    for (int f = f0; f < f1; ++f) {
+      int prev = -1;
+      for (int64_t e = p->feat_ptr[f]; e < p->feat_ptr[f + 1]; ++e) {
+        const int smp = p->sample_idx[e];
+        if (smp <= prev || smp >= p->n_samples) {
+          bad_f[static_cast<size_t>(t)] = f;
+          bad_kind[static_cast<size_t>(t)] = 1;
+          return;
+        }
+        prev = smp;
+        const double c = p->counts[e];
+        if (!(c >= 0.0) || c > 1.7976931348623157e308) {
+          bad_f[static_cast<size_t>(t)] = f;
+          bad_kind[static_cast<size_t>(t)] = 2;
+          return;
+        }
+      }
     }
+  };
+  if (p->feat_ptr[F] > (int64_t{1} << 20) && T > 1) {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t) pool.emplace_back(scan, t);
+    for (auto& th : pool) th.join();
+  } else {
+    for (int t = 0; t < T; ++t) scan(t);
+  }
+  for (int t = 0; t < T; ++t) {  // lowest feature range first
+    if (bad_kind[static_cast<size_t>(t)] == 1)
+      return fail(SF_EINVAL, "sample indices of a feature must be ascending and in range");
+    if (bad_kind[static_cast<size_t>(t)] == 2)
+      return fail(SF_EINVAL, "count must be finite and non-negative");
   }
   for (int s = 0; s < p->n_samples; ++s)
     if (!(p->sample_totals[s] > 0.0))
