@@ -550,7 +550,11 @@ struct SplitCfg {
 
 // |X_e| threshold of the split path: rows at or above it are walked.
 int split_heavy_min(int n) {
-  double frac = 0.03;  // measured best with the banded light scatter (profiles/r01_ab_c3_split_banded_heavyfrac_*)
+  // measured best with the banded light scatter: 0.03 at n = 25,000 (C3,
+  // profiles/r01_ab_c3_split_*heavyfrac*), 0.02 at n = 113,721 (C5 shard,
+  // profiles/r01_ab_c5_shard_heavyfrac.jsonl): light pairs grow as x^2 and
+  // their atomics spread over more bands as n grows
+  double frac = n > 25000 ? 0.03 * std::pow(25000.0 / n, 0.25) : 0.03;
   if (const char* e = std::getenv("SF_HEAVY_FRAC")) frac = std::atof(e);
   return std::max(2, static_cast<int>(frac * n));
 }
