@@ -794,6 +794,10 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
   const int64_t kb = static_cast<int64_t>(band_mb * 1048576.0 / (16.0 * SB));
   const int KB = static_cast<int>(std::max<int64_t>(256, std::min<int64_t>(kb, n)));
   const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
+  // SF_LIGHT_DRYRUN=1: everything but the atomics (cost split for A/B only;
+  // the results are then wrong)
+  const char* dr = std::getenv("SF_LIGHT_DRYRUN");
+  const int dry = dr && std::atoi(dr) != 0 ? 1 : 0;
   auto* kfirst = sp_light_band_kernel<NW, true>;
   auto* knext = sp_light_band_kernel<NW, false>;
   SF_CUDA(cudaFuncSetAttribute(kfirst, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -807,7 +811,7 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
                                           d.lptr.as<uint32_t>(), d.lmem.as<int32_t>(), d.lcur.as<uint16_t>(),
                                           d.fix.as<unsigned long long>(), plan->lo_bits, p0, s0, s1, k0,
                                           std::min(n, k0 + KB), d.lightsum.as<double>(),
-                                          d.exec_ctr.as<unsigned long long>(), heavy_min);
+                                          d.exec_ctr.as<unsigned long long>(), heavy_min, dry);
       plan->stats.launches++;
     }
   }
@@ -1094,6 +1098,10 @@ sf_status launch_wuwalk_t(const WUWalkArgs& a, cudaStream_t st) {
 
 template <class Real>
 sf_status launch_wuwalk(int metric, const WUWalkArgs& a, cudaStream_t st) {
+  const char* v = std::getenv("SF_UWALK_VARIANT");  // A/B: 1 = 4 slots per lane, 2 = 12
+  const int var = v ? std::atoi(v) : 0;
+  if (metric == SF_WEIGHTED_NORMALIZED && var == 1) return launch_wuwalk_t<kWN, Real, 4>(a, st);
+  if (metric == SF_WEIGHTED_NORMALIZED && var == 2) return launch_wuwalk_t<kWN, Real, 12>(a, st);
   if (metric == SF_WEIGHTED_NORMALIZED) return launch_wuwalk_t<kWN, Real>(a, st);
   if (metric == SF_WEIGHTED_UNNORMALIZED) return launch_wuwalk_t<kWU, Real>(a, st);
   if (metric == SF_GENERALIZED) return launch_wuwalk_t<kGen, Real, 4>(a, st);  // pow: fewer slots, no spills

@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
     const uint32_t* __restrict__ lptr, const int32_t* __restrict__ lmem, uint16_t* __restrict__ cur,
     const unsigned long long* __restrict__ fix, int32_t lo_bits, int32_t p0, int32_t s0, int32_t s1,
     int32_t k0, int32_t k1, double* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
-    int32_t list_cap) {
+    int32_t list_cap, int32_t dry) {
   extern __shared__ int32_t sp_band_members[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -385,16 +385,20 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
       for (; j1 < x && mem[j1] <= a + se; ++j1) {
         const int s = mem[j1] - a - 1;
         double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + a);
-        atomicAdd(cell, L.x);
-        atomicAdd(cell + 1, L.y);
+        if (!dry) {
+          atomicAdd(cell, L.x);
+          atomicAdd(cell + 1, L.y);
+        }
         ++pairs;
       }
       // partners below: slot (n - (a - a') - 1, a)
       for (; j2 < i && mem[j2] <= a - n + se; ++j2) {
         const int s = n - (a - mem[j2]) - 1;
         double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + a);
-        atomicAdd(cell, L.x);
-        atomicAdd(cell + 1, L.y);
+        if (!dry) {
+          atomicAdd(cell, L.x);
+          atomicAdd(cell + 1, L.y);
+        }
         ++pairs;
       }
       reinterpret_cast<uint32_t*>(c)[i] = static_cast<uint32_t>(j1) | (static_cast<uint32_t>(j2) << 16);

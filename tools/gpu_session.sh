@@ -1,8 +1,8 @@
 #!/usr/bin/env bash
-# GPU round-trip: .strf writer parity, Mantel at C3 scale, C4 fp32 line.
+# GPU round-trip: light-scatter cost split (dry run), u-walk slot variants.
 mkdir -p gpurun_out
 export BENCH_ALLOW_SHORT=1
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_mantel.py -q -m gpu -k "strf or mantel" > gpurun_out/pytest_strf.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_strf.log
-timeout 1200 python tools/mantel_bench.py --config c3 --perms 999 > gpurun_out/mantel_c3.json 2> gpurun_out/mantel_c3.log
-timeout 900 python bench.py --config c4f32 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/bench_c4f32.json 2> gpurun_out/bench_c4f32.log
+timeout 900 python tools/kernel_ab.py --config c3 --kernels 10 --reps 1 --env SF_LIGHT_DRYRUN=0,1 > gpurun_out/ab_dry.jsonl 2> gpurun_out/ab_dry.log
+timeout 900 env SF_LIGHT_BAND_MB=128 python tools/kernel_ab.py --config c3 --kernels 10 --reps 1 --env SF_LIGHT_DRYRUN=0,1 > gpurun_out/ab_dry128.jsonl 2> gpurun_out/ab_dry128.log
+timeout 600 python tools/kernel_ab.py --config c2 --kernels 12 --reps 2 --env SF_UWALK_VARIANT=0,1,2 > gpurun_out/ab_uwvar.jsonl 2> gpurun_out/ab_uwvar.log
 echo done
