@@ -810,7 +810,7 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
       kern<<<blocks, 32 * NW, smem, st>>>(d.perm.as<int32_t>(), plan->E, n, d.nheavy.as<unsigned int>(),
                                           d.lptr.as<uint32_t>(), d.lmem.as<int32_t>(), d.lcur.as<uint16_t>(),
                                           d.fix.as<unsigned long long>(), plan->lo_bits, p0, s0, s1, k0,
-                                          std::min(n, k0 + KB), d.lightsum.as<double>(),
+                                          std::min(n, k0 + KB), d.lightsum.as<unsigned long long>(),
                                           d.exec_ctr.as<unsigned long long>(), heavy_min, dry);
       plan->stats.launches++;
     }
@@ -833,7 +833,7 @@ sf_status split_scatter(sf_plan* plan, DeviceState& d, cudaStream_t st, int s0, 
   kern<<<blocks, 32 * NW, smem, st>>>(d.emb.as<uint32_t>(), plan->row_words, plan->E, n, d.perm.as<int32_t>(),
                                      d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>(),
                                      d.fix.as<unsigned long long>(), plan->lo_bits, s0, s1,
-                                     d.lightsum.as<double>(),
+                                     d.lightsum.as<unsigned long long>(),
                                      with_colsum ? d.colsum.as<unsigned long long>() : nullptr,
                                      d.exec_ctr.as<unsigned long long>(), heavy_min);
   SF_CUDA(cudaGetLastError());
@@ -1363,7 +1363,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       a.nx = d.nodebits.as<unsigned long long>();
       a.limbs = d.limbs.as<double2>();
       a.n_heavy = d.nheavy.as<unsigned int>();
-      a.gl = d.lightsum.as<double>();
+      a.gl = d.lightsum.as<unsigned long long>();
       a.colsum = d.colsum.as<unsigned long long>();
       a.cacc = d.cacc.as<unsigned long long>();
       a.n_ext = sparse_n_ext(n);

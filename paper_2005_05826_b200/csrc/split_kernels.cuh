@@ -133,22 +133,30 @@ __global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx
 // reference's duplicated half stripe). Rows with up to 32*MAXT members keep
 // them in registers (lane j holds members j, j+32, ...) so the pair loop
 // needs one broadcast shared load per a instead of one per pair.
+// Light sums are u64 limb pairs (hi, lo): every limb and partial sum is an
+// integer below 2^53, so integer atomics are exact and order-free (they
+// measured faster in L2 than fp64 atomic adds).
+__device__ __forceinline__ void light_add(unsigned long long* cell, ulonglong2 L) {
+  atomicAdd(cell, L.x);
+  atomicAdd(cell + 1, L.y);
+}
+
+__device__ __forceinline__ ulonglong2 ilimbs_of(unsigned long long v, int lo_bits) {
+  return make_ulonglong2(v >> lo_bits, v & ((1ull << lo_bits) - 1ull));
+}
+
 __device__ __forceinline__ void sp_add_pair(int a, int b, int n, int S, int s_begin, int s_end,
-                                            double2 L, double* __restrict__ gl,
+                                            ulonglong2 L, unsigned long long* __restrict__ gl,
                                             unsigned long long& pairs) {
   const int d = b - a;
   int s = d - 1;
   if (s < S && s >= s_begin && s < s_end) {
-    double* cell = gl + 2 * (static_cast<int64_t>(s - s_begin) * n + a);
-    atomicAdd(cell, L.x);
-    atomicAdd(cell + 1, L.y);
+    light_add(gl + 2 * (static_cast<int64_t>(s - s_begin) * n + a), L);
     ++pairs;
   }
   s = n - d - 1;
   if (s < S && s >= s_begin && s < s_end) {
-    double* cell = gl + 2 * (static_cast<int64_t>(s - s_begin) * n + b);
-    atomicAdd(cell, L.x);
-    atomicAdd(cell + 1, L.y);
+    light_add(gl + 2 * (static_cast<int64_t>(s - s_begin) * n + b), L);
     ++pairs;
   }
 }
@@ -158,7 +166,7 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
     const uint32_t* __restrict__ rows, int64_t stride, int32_t E, int32_t n,
     const int32_t* __restrict__ perm, const unsigned int* __restrict__ n_heavy,
     const int32_t* __restrict__ mcount, const unsigned long long* __restrict__ fix, int32_t lo_bits,
-    int32_t s_begin, int32_t s_end, double* __restrict__ gl, unsigned long long* __restrict__ colsum,
+    int32_t s_begin, int32_t s_end, unsigned long long* __restrict__ gl, unsigned long long* __restrict__ colsum,
     unsigned long long* __restrict__ pairs_out, int32_t list_cap) {
   extern __shared__ int32_t sp_members[];
   const int lane = threadIdx.x & 31;
@@ -203,9 +211,9 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
       count += __shfl_sync(0xffffffffu, incl, 31);
     }
     __syncwarp();
-    const double2 L = limbs_of(fix[r], lo_bits);
-    const unsigned long long lh = static_cast<unsigned long long>(L.x);
-    const unsigned long long ll = static_cast<unsigned long long>(L.y);
+    const ulonglong2 L = ilimbs_of(fix[r], lo_bits);
+    const unsigned long long lh = L.x;
+    const unsigned long long ll = L.y;
     for (int i = lane; colsum && i < x; i += 32) {  // colsum null on later passes
       const int c = mem[i];
       atomicAdd(colsum + c, lh);
@@ -349,7 +357,7 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
     const int32_t* __restrict__ perm, int32_t E, int32_t n, const unsigned int* __restrict__ n_heavy,
     const uint32_t* __restrict__ lptr, const int32_t* __restrict__ lmem, uint16_t* __restrict__ cur,
     const unsigned long long* __restrict__ fix, int32_t lo_bits, int32_t p0, int32_t s0, int32_t s1,
-    int32_t k0, int32_t k1, double* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
+    int32_t k0, int32_t k1, unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
     int32_t list_cap, int32_t dry) {
   extern __shared__ int32_t sp_band_members[];
   const int lane = threadIdx.x & 31;
@@ -367,7 +375,7 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
     if (x < 2) continue;
     for (int i = lane; i < x; i += 32) mem[i] = __ldg(lmem + b0 + i);
     __syncwarp();
-    const double2 L = limbs_of(fix[perm[idx]], lo_bits);
+    const ulonglong2 L = ilimbs_of(fix[perm[idx]], lo_bits);
     uint16_t* c = cur + 2 * static_cast<int64_t>(b0);
     for (int i = lane; i < x; i += 32) {
       const int a = mem[i];
@@ -384,21 +392,13 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
       // partners above: slot (b - a - 1, a)
       for (; j1 < x && mem[j1] <= a + se; ++j1) {
         const int s = mem[j1] - a - 1;
-        double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + a);
-        if (!dry) {
-          atomicAdd(cell, L.x);
-          atomicAdd(cell + 1, L.y);
-        }
+        if (!dry) light_add(gl + 2 * (static_cast<int64_t>(s - p0) * n + a), L);
         ++pairs;
       }
       // partners below: slot (n - (a - a') - 1, a)
       for (; j2 < i && mem[j2] <= a - n + se; ++j2) {
         const int s = n - (a - mem[j2]) - 1;
-        double* cell = gl + 2 * (static_cast<int64_t>(s - p0) * n + a);
-        if (!dry) {
-          atomicAdd(cell, L.x);
-          atomicAdd(cell + 1, L.y);
-        }
+        if (!dry) light_add(gl + 2 * (static_cast<int64_t>(s - p0) * n + a), L);
         ++pairs;
       }
       reinterpret_cast<uint32_t*>(c)[i] = static_cast<uint32_t>(j1) | (static_cast<uint32_t>(j2) << 16);
@@ -444,7 +444,7 @@ struct SplitArgs {
   const unsigned long long* nx;      // [Hw][n_ext] heavy X words
   const double2* limbs;              // permuted heavy rows, by bit position
   const unsigned int* n_heavy;
-  const double* gl;                  // light sums per slot (hi, lo)
+  const unsigned long long* gl;      // light sums per slot (hi, lo limbs, u64)
   const unsigned long long* colsum;  // [4][n]
   const unsigned long long* cacc;    // [2]
   int64_t n_ext;
@@ -638,8 +638,8 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
     const int64_t li = l0 + 32 * i;
     const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
     const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
-    const double2 light =
-        reinterpret_cast<const double2*>(a.gl)[static_cast<int64_t>(s - a.gl_begin) * n + k];
+    const ulonglong2 light =
+        reinterpret_cast<const ulonglong2*>(a.gl)[static_cast<int64_t>(s - a.gl_begin) * n + k];
     const long long Gh_ = static_cast<long long>(gh[i]) + static_cast<long long>(light.x);
     const long long Gl_ = static_cast<long long>(gl[i]) + static_cast<long long>(light.y);
     const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm]) + ch - Gh_;
