@@ -15,10 +15,11 @@
 //    divergence. The walk is FP64-pipe bound by construction.
 //  * LIGHT rows (|X_e| < heavy_min): a slot shares only ~5-10 of them, but
 //    finding them by walking per slot costs far more than they carry. They are
-//    scattered instead: one warp per light row lists its members and adds the
-//    row's limbs to every member pair's slot with atomicAdd on fp64. Every
-//    value added is an integer below 2^53 and so is every partial sum, so the
-//    atomics are exact and the result does not depend on their order.
+//    scattered instead: the light rows' member lists are compacted once and
+//    each member pair's slot gets the row's limbs with u64 atomics, band by
+//    band (L2-resident blocks). Every value added is an integer below 2^53
+//    and so is every partial sum, so the atomics are exact and the result
+//    does not depend on their order.
 //
 // The heavy kernel's epilogue adds the light sums and forms t, d (and d/t).
 #pragma once
@@ -134,8 +135,8 @@ __global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx
 // them in registers (lane j holds members j, j+32, ...) so the pair loop
 // needs one broadcast shared load per a instead of one per pair.
 // Light sums are u64 limb pairs (hi, lo): every limb and partial sum is an
-// integer below 2^53, so integer atomics are exact and order-free (they
-// measured faster in L2 than fp64 atomic adds).
+// integer below 2^53, so integer atomics are exact and order-free (measured
+// as fast as fp64 atomic adds in L2: profiles/r01_ab_c3_light_u64_atomics.jsonl).
 __device__ __forceinline__ void light_add(unsigned long long* cell, ulonglong2 L) {
   atomicAdd(cell, L.x);
   atomicAdd(cell + 1, L.y);
