@@ -1568,8 +1568,18 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     return fail(SF_EINVAL, "generalized UniFrac needs a finite alpha >= 0");
   if (prec != SF_FP32 && prec != SF_FP64)
     return fail(SF_EINVAL, "unknown precision code " + std::to_string(static_cast<int>(prec)));
+  const bool dbg = std::getenv("SF_DEBUG") != nullptr;
+  auto tick = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (!dbg) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "stripefrac:   plan %s %.1f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - tick).count());
+    tick = now;
+  };
   SF_TRY(validate_problem(p));
   SF_TRY(validate_range(p->n_samples, start, stop));
+  phase("validate");
   std::vector<int> devices;
   SF_TRY(usable_devices(ex, devices));
 
@@ -1669,6 +1679,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   }
   plan->stats.n_chunks = plan->sched.chunks.size();
 
+  phase("schedule");
   for (auto& dp : plan->devs) {
     DeviceState& d = *dp;
     SF_CUDA(cudaSetDevice(d.dev));
@@ -1680,6 +1691,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     SF_TRY(upload(d.sidx, d.dev, p->sample_idx, static_cast<size_t>(nnz), d.stream, "sample_idx"));
     SF_TRY(upload(d.counts, d.dev, p->counts, static_cast<size_t>(nnz), d.stream, "counts"));
     SF_TRY(upload(d.totals, d.dev, p->sample_totals, static_cast<size_t>(n), d.stream, "totals"));
+    phase("upload table");
     const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
     SF_TRY(d.dist.alloc(d.dev, slots * w, "distances"));
     if (has_t) SF_TRY(d.tot.alloc(d.dev, slots * w, "totals"));
@@ -1771,6 +1783,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                           "pending rows"));
     }
   }
+  phase("device setup");
   *out = plan.release();
   return SF_OK;
 }
