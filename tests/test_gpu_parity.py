@@ -749,3 +749,42 @@ def test_plan_write_strf_equals_host_writer(device_ok, tmp_path):
     with pytest.raises(sf.Error, match="no .strf metric code"):
         sf.compute_unifrac_to_strf(inst.tree, inst.table, sf.KernelConfig(sf.Metric.Generalized, alpha=0.5),
                                    str(tmp_path / "g.strf"), 0, 5)
+
+
+def test_medium_scale_against_oracle(device_ok):
+    """A size the oracle finishes in seconds on host threads (n = 1,200,
+    E ~ 12k: ~9e9 reference updates per metric): default kernels vs the
+    pinned C restatement — UW split (1e-12 relative), WN u-walk and
+    generalized (1e-12 absolute on values <= 1)."""
+    import os
+    inst = sf.random_instance(81, 1200, 6000, 0.005)
+    problem = sf.flatten(inst.tree, inst.table)
+    S = 600
+    th = os.cpu_count() or 4
+    for metric in (1, 3):
+        wd, wt = op.compute_stripes(problem, metric, 8, 0, S, threads=th)
+        d, t, _ = _gpu_stripes(problem, metric, 8, 0, S, N.KERNEL_AUTO)
+        used = N.KERNEL_SPLIT if metric == 1 else N.KERNEL_WUWALK
+        _assert_close(metric, 8, False, d, wd, used)
+        _assert_close(metric, 8, False, t, wt, used)
+    gd, gt = op.compute_stripes_generalized(problem, 0.5, 8, 0, S, threads=th)
+    d, t, _ = _gpu_generalized(problem, 0.5, 8, 0, S)
+    assert np.all(np.abs(d - gd) <= 1e-12 * np.maximum(1.0, np.abs(gd)))
+    assert np.all(np.abs(t - gt) <= 1e-12 * np.maximum(1.0, np.abs(gt)))
+
+
+def test_split_vs_reference_order_walk_at_4k_samples(device_ok):
+    """Size-independent check at a realistic shape (4,000 samples, 40k-tip
+    tree, EMP density): the default split kernel (exact fixed-point sums) vs
+    the bitwise walk (the reference's adds in the reference's order) — the
+    same matrix within 1e-12 relative everywhere; d <= t; 0 <= d/t <= 1."""
+    inst = sf.random_instance(7, 4000, 40000, 0.002)
+    problem = sf.flatten(inst.tree, inst.table)
+    S = 2000
+    d0, t0, _ = _gpu_stripes(problem, 1, 8, 0, S, N.KERNEL_SPARSE, finalize=False)
+    d1, t1, _ = _gpu_stripes(problem, 1, 8, 0, S, N.KERNEL_SPLIT, finalize=False)
+    assert np.all(np.abs(d1 - d0) <= 1e-12 * np.abs(d0))
+    assert np.all(np.abs(t1 - t0) <= 1e-12 * np.abs(t0))
+    assert np.all(d1 <= t1)
+    f, _, _ = _gpu_stripes(problem, 1, 8, 0, S, N.KERNEL_SPLIT)
+    assert np.all((f >= 0) & (f <= 1))
