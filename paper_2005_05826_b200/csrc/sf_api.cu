@@ -882,9 +882,9 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
 }
 
 template <class Real, int RS, int NW, bool BITMAJOR = false, bool UPREF = false, bool HALVES = false,
-          int MINB = 1, bool LIST = false, bool PREF = false>
+          int MINB = 1, bool LIST = false, bool PREF = false, bool PIPE = false>
 sf_status launch_split_rs(const SplitArgs& a, cudaStream_t st) {
-  auto* kern = stripe_split_kernel<Real, RS, NW, BITMAJOR, UPREF, HALVES, MINB, LIST, PREF>;
+  auto* kern = stripe_split_kernel<Real, RS, NW, BITMAJOR, UPREF, HALVES, MINB, LIST, PREF, PIPE>;
   const dim3 grid((a.n + NW - 1) / NW, (a.s_end - a.s_begin + 32 * RS - 1) / (32 * RS));
   kern<<<grid, 32 * NW, 0, st>>>(a);
   SF_CUDA(cudaGetLastError());
@@ -910,6 +910,11 @@ sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
     case 8: return launch_split_rs<Real, 8, 8, false, false, true, 3>(a, st);    // 24 warps/SM
     case 9: return launch_split_rs<Real, 12, 4, false, false, true, 5>(a, st);   // 20 warps/SM
     case 10: return launch_split_rs<Real, 16, 4, false, false, true, 4>(a, st);  // 16 warps, 4-warp CTAs
+    case 11: return launch_split_rs<Real, 12, 8, false, false, false, 2>(a, st);  // both v halves at once
+    case 12: return launch_split_rs<Real, 14, 8, false, false, false, 2>(a, st);
+    case 13: return launch_split_rs<Real, 12, 8, false, true, false, 2>(a, st);   // + u prefetch
+    case 14: return launch_split_rs<Real, 8, 8, false, false, false, 2, false, false, true>(a, st);   // pipelined words
+    case 15: return launch_split_rs<Real, 10, 8, false, false, false, 2, false, false, true>(a, st);
     default: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2>(a, st);
   }
 }

@@ -540,7 +540,7 @@ __device__ __forceinline__ void heavy_word(unsigned long long u, const unsigned 
 }
 
 template <class Real, int RS, int NW, bool BITMAJOR = false, bool UPREF = false, bool HALVES = false,
-          int MINB = 1, bool LIST = false, bool PREF = false>
+          int MINB = 1, bool LIST = false, bool PREF = false, bool PIPE = false>
 __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const SplitArgs a) {
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * NW + (threadIdx.x >> 5);
@@ -563,6 +563,57 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
   for (int i = 0; i < RS; ++i) {
     gh[i] = 0.0;
     gl[i] = 0.0;
+  }
+  if (PIPE) {
+    // software-pipelined walk of the nonzero words (per-column masks): the
+    // next word's u and 64-bit v words are loaded into registers while the
+    // current word is walked
+    const int G = (Hw + 31) / 32;
+    int g = 0;
+    uint32_t m = 0u;
+    auto next_w = [&]() -> int {  // next nonzero word index, or -1
+      while (!m) {
+        if (g >= G) return -1;
+        m = __ldg(a.nz + static_cast<int64_t>(g) * n + k);
+        ++g;
+      }
+      const int w = 32 * (g - 1) + (__ffs(m) - 1);
+      m &= m - 1u;
+      return w;
+    };
+    int w = next_w();
+    unsigned long long u = 0ull, v[RS];
+    if (w >= 0) {
+      const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
+      u = __ldg(row + k);
+#pragma unroll
+      for (int i = 0; i < RS; ++i) v[i] = __ldg(row + l0 + 32 * i);
+    }
+#pragma unroll 1
+    while (w >= 0) {
+      const int wn = next_w();
+      unsigned long long un = 0ull, vn[RS];
+      if (wn >= 0) {
+        const unsigned long long* nrow = a.nx + static_cast<int64_t>(wn) * n_ext;
+        un = __ldg(nrow + k);
+#pragma unroll
+        for (int i = 0; i < RS; ++i) vn[i] = __ldg(nrow + l0 + 32 * i);
+      }
+      ubits += static_cast<unsigned>(__popcll(u));
+      const double2* Lw = a.limbs + 64 * static_cast<int64_t>(w);
+      uint32_t vh[RS], vl[RS];
+#pragma unroll
+      for (int i = 0; i < RS; ++i) {
+        vh[i] = static_cast<uint32_t>(v[i] >> 32);
+        vl[i] = static_cast<uint32_t>(v[i]);
+      }
+      heavy_half<RS, false>(static_cast<uint32_t>(u >> 32), Lw + 32, vh, gh, gl);
+      heavy_half<RS, false>(static_cast<uint32_t>(u), Lw, vl, gh, gl);
+      w = wn;
+      u = un;
+#pragma unroll
+      for (int i = 0; i < RS; ++i) v[i] = vn[i];
+    }
   }
   if (LIST) {
     // walk only the nonzero words of column k (per-column masks), and pull
@@ -589,7 +640,7 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
   }
   unsigned long long u_next = (UPREF && Hw > 0) ? __ldg(a.nx + k) : 0ull;
 #pragma unroll 1
-  for (int w = 0; LIST ? false : w < Hw; ++w) {
+  for (int w = 0; (LIST || PIPE) ? false : w < Hw; ++w) {
     const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
     unsigned long long u;
     if (UPREF) {
