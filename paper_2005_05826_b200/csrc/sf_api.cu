@@ -1664,6 +1664,39 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     budget = std::min(budget, avail * 3 / 4);
   }
   if (ex && ex->mem_budget_bytes > 0) budget = std::min(budget, static_cast<size_t>(ex->mem_budget_bytes));
+
+  // the table upload (C3: 192 MB from pageable memory) runs on a host thread
+  // while this one builds the schedule
+  std::vector<sf_status> up_status(plan->devs.size(), SF_OK);
+  std::vector<std::string> up_error(plan->devs.size());
+  std::thread uploader([&] {
+    for (size_t i = 0; i < plan->devs.size(); ++i) {
+      DeviceState& d = *plan->devs[i];
+      auto run = [&]() -> sf_status {
+        SF_CUDA(cudaSetDevice(d.dev));
+        SF_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+        const int64_t F = p->n_features;
+        const int64_t nnz = p->feat_ptr[F];
+        SF_TRY(upload(d.lens, d.dev, p->lengths, static_cast<size_t>(plan->E), d.stream, "lengths"));
+        SF_TRY(upload(d.feat_ptr, d.dev, p->feat_ptr, static_cast<size_t>(F + 1), d.stream, "feat_ptr"));
+        SF_TRY(upload(d.sidx, d.dev, p->sample_idx, static_cast<size_t>(nnz), d.stream, "sample_idx"));
+        SF_TRY(upload(d.counts, d.dev, p->counts, static_cast<size_t>(nnz), d.stream, "counts"));
+        SF_TRY(upload(d.totals, d.dev, p->sample_totals, static_cast<size_t>(n), d.stream, "totals"));
+        return SF_OK;
+      };
+      up_status[i] = run();
+      if (up_status[i] != SF_OK) {
+        up_error[i] = sf::last_error();
+        return;
+      }
+    }
+  });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{uploader};
   int64_t cmax = static_cast<int64_t>(budget / std::max<size_t>(row_bytes + wsp_row_bytes, 1));
   if (plan->kernel >= 2 && !wsp) cmax = plan->E;  // the sparse bit paths keep all rows
   if (wsp) {
@@ -1685,18 +1718,13 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stats.n_chunks = plan->sched.chunks.size();
 
   phase("schedule");
+  uploader.join();
+  for (size_t i = 0; i < up_status.size(); ++i)
+    if (up_status[i] != SF_OK) return fail(up_status[i], up_error[i]);
+  phase("upload table (overlapped)");
   for (auto& dp : plan->devs) {
     DeviceState& d = *dp;
     SF_CUDA(cudaSetDevice(d.dev));
-    SF_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
-    const int64_t F = p->n_features;
-    const int64_t nnz = p->feat_ptr[F];
-    SF_TRY(upload(d.lens, d.dev, p->lengths, static_cast<size_t>(plan->E), d.stream, "lengths"));
-    SF_TRY(upload(d.feat_ptr, d.dev, p->feat_ptr, static_cast<size_t>(F + 1), d.stream, "feat_ptr"));
-    SF_TRY(upload(d.sidx, d.dev, p->sample_idx, static_cast<size_t>(nnz), d.stream, "sample_idx"));
-    SF_TRY(upload(d.counts, d.dev, p->counts, static_cast<size_t>(nnz), d.stream, "counts"));
-    SF_TRY(upload(d.totals, d.dev, p->sample_totals, static_cast<size_t>(n), d.stream, "totals"));
-    phase("upload table");
     const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
     SF_TRY(d.dist.alloc(d.dev, slots * w, "distances"));
     if (has_t) SF_TRY(d.tot.alloc(d.dev, slots * w, "totals"));
