@@ -467,6 +467,11 @@ struct DeviceState {
   DevBuf lcnt, lptr, lmem, lcur, lscantmp;  // banded light scatter: member CSR + cursors of the light rows
   size_t lscan_bytes = 0;
   bool banded = false;
+  // entry lists per column band (sp_light_entry_kernel)
+  DevBuf lent, linfo, kcnt;
+  std::vector<uint32_t> koff;
+  int kb_cols = 0;
+  bool entries = false;
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
   DevBuf wnb, woff, wcnt, wpool;
   DevBuf wpoola, wA, wbase;  // kernel 12: generalized pool, column sums, pool base + chunk total
@@ -793,6 +798,64 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
   const int SB = 32 * SplitCfg::RS;
   const int64_t kb = static_cast<int64_t>(band_mb * 1048576.0 / (16.0 * SB));
   const int KB = static_cast<int>(std::max<int64_t>(256, std::min<int64_t>(kb, n)));
+  if (first) {
+    // entry lists per column band (default; SF_LIGHT_ENTRY=0: warp per row)
+    const char* ee = std::getenv("SF_LIGHT_ENTRY");
+    d.entries = !(ee && std::atoi(ee) == 0);
+    const int nkb = (n + KB - 1) / KB;
+    uint32_t M = 0;
+    if (d.entries) {
+      SF_CUDA(cudaMemcpyAsync(&M, d.lptr.as<uint32_t>() + E, 4, cudaMemcpyDeviceToHost, st));
+      SF_CUDA(cudaStreamSynchronize(st));
+      d.entries = nkb <= 1024 && d.lent.alloc(d.dev, static_cast<size_t>(M) * 8, "light entries") == SF_OK &&
+                  d.linfo.alloc(d.dev, static_cast<size_t>(E) * sizeof(LightRow), "light rows") == SF_OK &&
+                  d.kcnt.alloc(d.dev, static_cast<size_t>(nkb + 1) * 4, "band counts") == SF_OK;
+      cudaGetLastError();
+    }
+    if (d.entries) {
+      d.kb_cols = KB;
+      sp_light_rowinfo_kernel<<<grid_for(E, 256), 256, 0, st>>>(
+          d.perm.as<int32_t>(), plan->E, d.nheavy.as<unsigned int>(), d.lptr.as<uint32_t>(),
+          d.fix.as<unsigned long long>(), plan->lo_bits, d.linfo.as<LightRow>());
+      SF_CUDA(cudaMemsetAsync(d.kcnt.p, 0, static_cast<size_t>(nkb + 1) * 4, st));
+      sp_entry_hist_kernel<<<grid_for(M, 256), 256, static_cast<size_t>(nkb) * 4, st>>>(
+          d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E, KB, nkb, d.kcnt.as<uint32_t>());
+      std::vector<uint32_t> cnt(static_cast<size_t>(nkb));
+      SF_CUDA(cudaMemcpyAsync(cnt.data(), d.kcnt.p, static_cast<size_t>(nkb) * 4, cudaMemcpyDeviceToHost, st));
+      SF_CUDA(cudaStreamSynchronize(st));
+      d.koff.assign(static_cast<size_t>(nkb) + 1, 0u);
+      for (int K = 0; K < nkb; ++K) d.koff[static_cast<size_t>(K) + 1] = d.koff[static_cast<size_t>(K)] + cnt[static_cast<size_t>(K)];
+      SF_CUDA(cudaMemcpyAsync(d.kcnt.p, d.koff.data(), static_cast<size_t>(nkb) * 4, cudaMemcpyHostToDevice, st));
+      sp_entry_fill_kernel<<<static_cast<int>(std::min<int64_t>((E + 7) / 8, 148 * 16)), 256, 0, st>>>(
+          d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E, d.nheavy.as<unsigned int>(), KB,
+          d.kcnt.as<uint32_t>(), d.lent.as<uint2>());
+      SF_CUDA(cudaStreamSynchronize(st));  // koff (host) is read below; kcnt was the fill cursor
+      SF_CUDA(cudaGetLastError());
+      plan->stats.launches += 3;
+    }
+  }
+  if (d.entries && d.kb_cols == KB) {
+    const int nkb = static_cast<int>(d.koff.size()) - 1;
+    for (int s0 = p0; s0 < p1; s0 += SB) {
+      const int s1 = std::min(p1, s0 + SB);
+      for (int K = 0; K < nkb; ++K) {
+        const uint32_t t0 = d.koff[static_cast<size_t>(K)], t1 = d.koff[static_cast<size_t>(K) + 1];
+        if (t1 <= t0) continue;
+        const int blocks = static_cast<int>(std::min<int64_t>((t1 - t0 + 255) / 256, 148 * 8));
+        if (s0 == p0)
+          sp_light_entry_kernel<true><<<blocks, 256, 0, st>>>(
+              d.lent.as<uint2>(), t0, t1, d.linfo.as<LightRow>(), d.lmem.as<int32_t>(), d.lcur.as<uint32_t>(), n,
+              p0, s0, s1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>());
+        else
+          sp_light_entry_kernel<false><<<blocks, 256, 0, st>>>(
+              d.lent.as<uint2>(), t0, t1, d.linfo.as<LightRow>(), d.lmem.as<int32_t>(), d.lcur.as<uint32_t>(), n,
+              p0, s0, s1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>());
+        plan->stats.launches++;
+      }
+    }
+    SF_CUDA(cudaGetLastError());
+    return SF_OK;
+  }
   const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
   // SF_LIGHT_DRYRUN=1: everything but the atomics (cost split for A/B only;
   // the results are then wrong)

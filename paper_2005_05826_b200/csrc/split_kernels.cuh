@@ -410,6 +410,118 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
   if (lane == 0 && pairs) atomicAdd(pairs_out, pairs);
 }
 
+// ---- Entry lists per column band (default band scatter). The warp-per-row
+// band kernel above rereads every light row's member list in every band
+// launch (C3: ~190 launches, C5: ~3,000); here each launch only visits the
+// members whose column lies in its band: one thread per (row, member) entry
+// of the column band's list, row data precomputed.
+struct LightRow {
+  uint32_t b0, x;        // member list offset and length
+  unsigned long long lh, ll;  // fixed-point limbs of the row's length
+};
+
+__global__ void sp_light_rowinfo_kernel(const int32_t* __restrict__ perm, int32_t E,
+                                        const unsigned int* __restrict__ n_heavy,
+                                        const uint32_t* __restrict__ lptr,
+                                        const unsigned long long* __restrict__ fix, int32_t lo_bits,
+                                        LightRow* __restrict__ info) {
+  const int64_t H = *n_heavy;
+  for (int64_t idx = H + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < E;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const ulonglong2 L = ilimbs_of(fix[perm[idx]], lo_bits);
+    info[idx] = LightRow{lptr[idx], lptr[idx + 1] - lptr[idx], L.x, L.y};
+  }
+}
+
+// Entries per column band (block histogram in shared memory, <= 1024 bands).
+__global__ void sp_entry_hist_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ lptr,
+                                     int32_t E, int32_t KB, int32_t nkb, uint32_t* __restrict__ kcnt) {
+  extern __shared__ uint32_t hist[];
+  for (int i = threadIdx.x; i < nkb; i += blockDim.x) hist[i] = 0u;
+  __syncthreads();
+  const int64_t M = lptr[E];
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < M;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&hist[lmem[g] / KB], 1u);
+  __syncthreads();
+  for (int i = threadIdx.x; i < nkb; i += blockDim.x)
+    if (hist[i]) atomicAdd(kcnt + i, hist[i]);
+}
+
+// Entries (member g, row idx) into their band's list; warp per light row,
+// warp-aggregated slot claims (a row's members are ascending, so a warp's
+// lanes mostly share one or two bands).
+__global__ void sp_entry_fill_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ lptr,
+                                     int32_t E, const unsigned int* __restrict__ n_heavy, int32_t KB,
+                                     uint32_t* __restrict__ kfill, uint2* __restrict__ ent) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  const int64_t H = *n_heavy;
+  for (int64_t idx = H + warp; idx < E; idx += nwarps) {
+    const uint32_t b0 = lptr[idx];
+    const int x = static_cast<int>(lptr[idx + 1] - b0);  // every entry listed (the histogram counts all)
+    for (int base = 0; base < x; base += 32) {
+      const int i = base + lane;
+      const bool live = i < x;
+      const int K = live ? lmem[b0 + i] / KB : -1;
+      const uint32_t act = __ballot_sync(0xffffffffu, live);
+      if (!live) continue;
+      const uint32_t same = __match_any_sync(act, K);
+      const int leader = __ffs(same) - 1;
+      uint32_t pos = 0;
+      if (lane == leader) pos = atomicAdd(kfill + K, static_cast<uint32_t>(__popc(same)));
+      pos = __shfl_sync(same, pos, leader) + static_cast<uint32_t>(__popc(same & ((1u << lane) - 1u)));
+      ent[pos] = make_uint2(b0 + static_cast<uint32_t>(i), static_cast<uint32_t>(idx));
+    }
+  }
+}
+
+// One band (stripes [s0, s1), the column band whose entries are ent[t0, t1)):
+// same slot ownership and cursors as sp_light_band_kernel.
+template <bool FIRST>
+__global__ void __launch_bounds__(256) sp_light_entry_kernel(
+    const uint2* __restrict__ ent, uint32_t t0, uint32_t t1, const LightRow* __restrict__ info,
+    const int32_t* __restrict__ lmem, uint32_t* __restrict__ cur, int32_t n, int32_t p0, int32_t s0,
+    int32_t s1, unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out) {
+  const int S = n / 2;
+  const int se = min(s1, S);
+  unsigned long long pairs = 0;
+  for (uint32_t t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += gridDim.x * blockDim.x) {
+    const uint2 e = ent[t];
+    const LightRow r = info[e.y];
+    const int32_t* mem = lmem + r.b0;
+    const int x = static_cast<int>(r.x);
+    const int i = static_cast<int>(e.x - r.b0);
+    const int a = mem[i];
+    const ulonglong2 L = make_ulonglong2(r.lh, r.ll);
+    int j1, j2;
+    if (FIRST) {
+      j1 = lower_bound_i32(mem, i + 1, x, a + s0 + 1);
+      j2 = lower_bound_i32(mem, 0, i, a - n + 1 + s0);
+    } else {
+      const uint32_t cc = cur[e.x];
+      j1 = static_cast<int>(cc & 0xffffu);
+      j2 = static_cast<int>(cc >> 16);
+    }
+    for (; j1 < x; ++j1) {  // partners above: slot (b - a - 1, a)
+      const int b = __ldg(mem + j1);
+      if (b > a + se) break;
+      light_add(gl + 2 * (static_cast<int64_t>(b - a - 1 - p0) * n + a), L);
+      ++pairs;
+    }
+    for (; j2 < i; ++j2) {  // partners below: slot (n - (a - a') - 1, a)
+      const int a2 = __ldg(mem + j2);
+      if (a2 > a - n + se) break;
+      light_add(gl + 2 * (static_cast<int64_t>(n - (a - a2) - 1 - p0) * n + a), L);
+      ++pairs;
+    }
+    cur[e.x] = static_cast<uint32_t>(j1) | (static_cast<uint32_t>(j2) << 16);
+  }
+  for (int off = 16; off > 0; off >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+  if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(pairs_out, pairs);
+}
+
 // bfind: position of the most significant set bit (x != 0).
 __device__ __forceinline__ int msb_pos(uint32_t x) {
   int b;

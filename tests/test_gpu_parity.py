@@ -788,3 +788,23 @@ def test_split_vs_reference_order_walk_at_4k_samples(device_ok):
     assert np.all(d1 <= t1)
     f, _, _ = _gpu_stripes(problem, 1, 8, 0, S, N.KERNEL_SPLIT)
     assert np.all((f >= 0) & (f <= 1))
+
+
+@pytest.mark.parametrize("band_mb,light_pass", [("0.05", "0"), ("0.3", "7"), ("32", "0")])
+def test_split_entry_lists_equal_row_scan(device_ok, band_mb, light_pass, monkeypatch):
+    """Column-band entry lists (one thread per member entry, the default)
+    add the same limbs to the same slots as the warp-per-row band scan:
+    bitwise, over tiny bands, several light passes, odd and even n."""
+    for seed, n, leaves, dens in [(98, 300, 1100, 0.01), (99, 257, 700, 0.03)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        monkeypatch.setenv("SF_HEAVY_FRAC", "0.05")
+        monkeypatch.setenv("SF_LIGHT_BAND_MB", band_mb)
+        if light_pass != "0":
+            monkeypatch.setenv("SF_LIGHT_PASS", light_pass)
+        monkeypatch.setenv("SF_LIGHT_ENTRY", "0")
+        want_d, want_t, ws = _gpu_stripes(problem, 1, 8, 2, n // 2, N.KERNEL_SPLIT)
+        monkeypatch.setenv("SF_LIGHT_ENTRY", "1")
+        d, t, gs = _gpu_stripes(problem, 1, 8, 2, n // 2, N.KERNEL_SPLIT)
+        assert np.array_equal(d, want_d) and np.array_equal(t, want_t)
+        assert gs.updates_exec == ws.updates_exec
