@@ -799,9 +799,10 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
   const int64_t kb = static_cast<int64_t>(band_mb * 1048576.0 / (16.0 * SB));
   const int KB = static_cast<int>(std::max<int64_t>(256, std::min<int64_t>(kb, n)));
   if (first) {
-    // entry lists per column band (default; SF_LIGHT_ENTRY=0: warp per row)
+    // entry lists per column band (SF_LIGHT_ENTRY=1) or warp per row (the
+    // default: measured faster at C3, profiles/r01_ab_c3_light_entry.jsonl)
     const char* ee = std::getenv("SF_LIGHT_ENTRY");
-    d.entries = !(ee && std::atoi(ee) == 0);
+    d.entries = ee && std::atoi(ee) != 0;
     const int nkb = (n + KB - 1) / KB;
     uint32_t M = 0;
     if (d.entries) {

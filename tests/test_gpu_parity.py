@@ -792,7 +792,7 @@ def test_split_vs_reference_order_walk_at_4k_samples(device_ok):
 
 @pytest.mark.parametrize("band_mb,light_pass", [("0.05", "0"), ("0.3", "7"), ("32", "0")])
 def test_split_entry_lists_equal_row_scan(device_ok, band_mb, light_pass, monkeypatch):
-    """Column-band entry lists (one thread per member entry, the default)
+    """Column-band entry lists (one thread per member entry, SF_LIGHT_ENTRY=1)
     add the same limbs to the same slots as the warp-per-row band scan:
     bitwise, over tiny bands, several light passes, odd and even n."""
     for seed, n, leaves, dens in [(98, 300, 1100, 0.01), (99, 257, 700, 0.03)]:
