@@ -1,6 +1,9 @@
 #!/usr/bin/env bash
-# GPU round-trip: entry lists vs row scan at the C5 shard.
+# Round-end style GPU pass: smoke, full parity suite, default bench line, reference arm.
 mkdir -p gpurun_out
-export BENCH_ALLOW_SHORT=1
-timeout 1500 python tools/kernel_ab.py --config c5 --stripes 7108 --kernels 10 --reps 1 --env SF_LIGHT_ENTRY=0,1 > gpurun_out/ab_c5_entry.jsonl 2> gpurun_out/ab_c5_entry.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
+timeout 2000 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.log
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.log
+timeout 600 python bench.py --config c2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.log
 echo done
