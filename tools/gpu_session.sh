@@ -1,9 +1,8 @@
 #!/usr/bin/env bash
-# Round-end style GPU pass: smoke, full parity suite, default bench line, reference arm.
+# GPU round-trip: heavy-row order A/B at threshold 0.03; ncu of the u-walk (word lists) at C2.
 mkdir -p gpurun_out
-timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "rc=$?" >> gpurun_out/smoke.log
-timeout 2000 python -m pytest tests -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.log
-timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.log
-timeout 600 python bench.py --config c2 > gpurun_out/bench_c2.json 2> gpurun_out/bench_c2.log
+export BENCH_ALLOW_SHORT=1
+timeout 900 python tools/kernel_ab.py --config c3 --kernels 10 --reps 1 --env SF_HEAVY_BY_WEIGHT=,1 > gpurun_out/ab_order.jsonl 2> gpurun_out/ab_order.log
+CMD="python bench.py --config c2 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"stripe_wuwalk" -s 1 -c 1 -o gpurun_out/prof_wuwalk_c2 $CMD > gpurun_out/ncu_wuwalk.log 2>&1
 echo done

@@ -52,7 +52,10 @@ def main():
             runs.append((k, None, None))
     for k, ename, evalue in runs:
         if ename:
-            os.environ[ename] = evalue
+            if evalue == "":
+                os.environ.pop(ename, None)  # empty value: variable unset
+            else:
+                os.environ[ename] = evalue
         ex, _keep = N.make_exec([0], k)
         plan = C.c_void_p()
         N.check(L.sf_plan_create(problem.ref, metric, prec, 0, stop, C.byref(ex), C.byref(plan)))
