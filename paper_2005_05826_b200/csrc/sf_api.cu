@@ -475,6 +475,7 @@ struct DeviceState {
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
   DevBuf wnb, woff, wcnt, wpool;
   DevBuf wpoola, wA, wbase;  // kernel 12: generalized pool, column sums, pool base + chunk total
+  DevBuf wnbo;               // kernel 12: combined (offset, presence word) cells
   int32_t light_pass = 0;  // stripes per light-sum pass (memory-bounded)
   size_t sort_bytes = 0;
   std::vector<cudaEvent_t> events;
@@ -1372,8 +1373,19 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         }
         wu_nzmask_kernel<<<grid_for(static_cast<int64_t>((W + 31) / 32) * n, 256), 256, 0, st>>>(
             d.wnb.as<uint32_t>(), n_ext, n, W, d.nzmask.as<uint32_t>());
+        // combined cells (SF_UWALK_NBO=0: separate word / offset arrays)
+        const char* nbo_env = std::getenv("SF_UWALK_NBO");
+        const int64_t cells = static_cast<int64_t>(W) * n_ext;
+        bool use_nbo = !(nbo_env && std::atoi(nbo_env) == 0);
+        if (use_nbo && d.wnbo.bytes < static_cast<size_t>(cells) * 8)
+          use_nbo = d.wnbo.alloc(d.dev, static_cast<size_t>(cells) * 8, "word/offset cells") == SF_OK;
+        cudaGetLastError();
+        if (use_nbo)
+          wu_combine_kernel<<<grid_for(cells, 256), 256, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), cells,
+                                                                   d.wnbo.as<unsigned long long>());
         SF_CUDA(cudaGetLastError());
         WUWalkArgs a;
+        a.nbo = use_nbo ? d.wnbo.as<unsigned long long>() : nullptr;
         const char* lst = std::getenv("SF_UWALK_LIST");
         a.nz = (lst && std::atoi(lst) == 0) ? nullptr : d.nzmask.as<uint32_t>();
         a.nb = d.wnb.as<uint32_t>();

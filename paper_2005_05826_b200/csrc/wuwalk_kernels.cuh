@@ -162,7 +162,17 @@ struct WUWalkArgs {
   void* tot;  // null for WU
   unsigned long long* exec_updates;
   const uint32_t* nz;  // [ceil(W/32)][n] nonzero-word masks (null: scan every word)
+  const unsigned long long* nbo;  // [W][n_ext] (offset << 32) | presence word, or null
 };
+
+// One 8-byte cell per (word, column): the presence word and its pool offset
+// arrive in one load (and one sector) instead of two.
+__global__ void wu_combine_kernel(const uint32_t* __restrict__ nb, const uint32_t* __restrict__ off,
+                                  int64_t cells, unsigned long long* __restrict__ nbo) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cells;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    nbo[i] = (static_cast<unsigned long long>(off[i]) << 32) | nb[i];
+}
 
 template <int M, class Real, int RS, int NW>
 __global__ void __launch_bounds__(32 * NW, 2) stripe_wuwalk_kernel(const WUWalkArgs a) {
@@ -193,14 +203,26 @@ __global__ void __launch_bounds__(32 * NW, 2) stripe_wuwalk_kernel(const WUWalkA
   unsigned long long ubits = 0;
   // one nonzero presence word w of column k (u != 0)
   auto word = [&](int w, uint32_t u) {
-      const uint32_t ou = __ldg(a.off + static_cast<int64_t>(w) * n_ext + k);
-      const uint32_t* vrow = a.nb + static_cast<int64_t>(w) * n_ext + l0;
-      const uint32_t* orow = a.off + static_cast<int64_t>(w) * n_ext + l0;
+      uint32_t ou;
       uint32_t vv[RS], vo[RS];
+      if (a.nbo) {
+        const unsigned long long* crow = a.nbo + static_cast<int64_t>(w) * n_ext;
+        ou = static_cast<uint32_t>(__ldg(crow + k) >> 32);
 #pragma unroll
-      for (int i = 0; i < RS; ++i) vv[i] = __ldg(vrow + 32 * i);
+        for (int i = 0; i < RS; ++i) {
+          const unsigned long long c = __ldg(crow + l0 + 32 * i);
+          vv[i] = static_cast<uint32_t>(c);
+          vo[i] = static_cast<uint32_t>(c >> 32);
+        }
+      } else {
+        ou = __ldg(a.off + static_cast<int64_t>(w) * n_ext + k);
+        const uint32_t* vrow = a.nb + static_cast<int64_t>(w) * n_ext + l0;
+        const uint32_t* orow = a.off + static_cast<int64_t>(w) * n_ext + l0;
 #pragma unroll
-      for (int i = 0; i < RS; ++i) vo[i] = (vv[i] & u) ? __ldg(orow + 32 * i) : 0u;
+        for (int i = 0; i < RS; ++i) vv[i] = __ldg(vrow + 32 * i);
+#pragma unroll
+        for (int i = 0; i < RS; ++i) vo[i] = (vv[i] & u) ? __ldg(orow + 32 * i) : 0u;
+      }
       ubits += static_cast<unsigned>(__popc(u));
       const double* Lw = a.lens + 32 * static_cast<int64_t>(w);
       uint32_t hu = u;
@@ -250,17 +272,24 @@ __global__ void __launch_bounds__(32 * NW, 2) stripe_wuwalk_kernel(const WUWalkA
         m &= m - 1u;
         if (m) {
           const int64_t nrow = static_cast<int64_t>(32 * g + (__ffs(m) - 1)) * n_ext;
-          if (lane == 0) {
-            wu_prefetch_l1(a.nb + nrow + k);
-            wu_prefetch_l1(a.off + nrow + k);
-          }
+          if (a.nbo) {
+            if (lane == 0) wu_prefetch_l1(a.nbo + nrow + k);
 #pragma unroll
-          for (int i = 0; i < RS; ++i) {
-            wu_prefetch_l1(a.nb + nrow + l0 + 32 * i);
-            wu_prefetch_l1(a.off + nrow + l0 + 32 * i);
+            for (int i = 0; i < RS; ++i) wu_prefetch_l1(a.nbo + nrow + l0 + 32 * i);
+          } else {
+            if (lane == 0) {
+              wu_prefetch_l1(a.nb + nrow + k);
+              wu_prefetch_l1(a.off + nrow + k);
+            }
+#pragma unroll
+            for (int i = 0; i < RS; ++i) {
+              wu_prefetch_l1(a.nb + nrow + l0 + 32 * i);
+              wu_prefetch_l1(a.off + nrow + l0 + 32 * i);
+            }
           }
         }
-        word(w, __ldg(a.nb + static_cast<int64_t>(w) * n_ext + k));
+        word(w, a.nbo ? static_cast<uint32_t>(__ldg(a.nbo + static_cast<int64_t>(w) * n_ext + k))
+                      : __ldg(a.nb + static_cast<int64_t>(w) * n_ext + k));
       }
     }
   } else {

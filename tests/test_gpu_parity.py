@@ -808,3 +808,21 @@ def test_split_entry_lists_equal_row_scan(device_ok, band_mb, light_pass, monkey
         d, t, gs = _gpu_stripes(problem, 1, 8, 2, n // 2, N.KERNEL_SPLIT)
         assert np.array_equal(d, want_d) and np.array_equal(t, want_t)
         assert gs.updates_exec == ws.updates_exec
+
+
+@pytest.mark.parametrize("metric", [2, 3, 4])
+def test_weighted_uwalk_combined_cells_bitwise(device_ok, metric, monkeypatch):
+    """Combined (offset, presence word) cells feed the u-walk the same words
+    and offsets as the separate arrays: bit-identical."""
+    inst = sf.random_instance(68, 230, 900, 0.01)
+    problem = sf.flatten(inst.tree, inst.table)
+    S = 115
+    out = []
+    for nbo in ("1", "0"):
+        monkeypatch.setenv("SF_UWALK_NBO", nbo)
+        ex, _keep = N.make_exec([0], N.KERNEL_WUWALK, False, 0, 0.5)
+        d = np.zeros((S, 230)); t = np.zeros((S, 230))
+        N.check(N.lib().sf_compute_stripes(problem.ref, metric, 8, 0, S, N.ptr(d), N.ptr(t) if metric != 2 else None,
+                                           1, C.byref(ex), None))
+        out.append((d, t))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
