@@ -463,7 +463,7 @@ struct DeviceState {
   // intersection v2 (kernel 6): permuted rows, 64-row words, group masks
   DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm, nheavy;
   // split path (kernel 10): light-row sums per slot, |S_e| per row
-  DevBuf lightsum, mcount, nzmask;
+  DevBuf lightsum, mcount, nzmask, ilimbs;
   DevBuf lcnt, lptr, lmem, lcur, lscantmp;  // banded light scatter: member CSR + cursors of the light rows
   size_t lscan_bytes = 0;
   bool banded = false;
@@ -1457,6 +1457,17 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       a.tot = d.tot.p;
       a.counters = d.exec_ctr.as<unsigned long long>();
       a.nz = d.nzmask.as<uint32_t>();
+      // A/B: integer-limb heavy walk (IMAD.WIDE instead of DFMA)
+      const char* sv = std::getenv("SF_SPLIT_VARIANT");
+      const bool int_walk = sv && std::atoi(sv) == 16;
+      if (int_walk) {
+        const int64_t cnt = ((plan->E + 63) / 64 + 31) / 32 * 2048;
+        if (d.ilimbs.bytes < static_cast<size_t>(cnt) * 8)
+          SF_TRY(d.ilimbs.alloc(d.dev, static_cast<size_t>(cnt) * 8, "integer limbs"));
+        sp_ilimbs_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(d.limbs.as<double2>(), cnt, plan->lo_bits,
+                                                              d.ilimbs.as<uint2>());
+        SF_CUDA(cudaGetLastError());
+      }
       // light-sum passes (one unless memory is short); within a pass, with a
       // host destination, chunks of whole 512-stripe tiles whose D2H copy
       // overlaps the next chunk's compute
@@ -1475,7 +1486,19 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
           const int c1 = std::min(p1, c0 + step);
           a.s_begin = c0;
           a.s_end = c1;
-          SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+          if (int_walk) {
+            const dim3 grid((a.n + SplitCfg::NW - 1) / SplitCfg::NW,
+                            (a.s_end - a.s_begin + 32 * SplitCfg::RS - 1) / (32 * SplitCfg::RS));
+            if (plan->prec == SF_FP64)
+              stripe_split_int_kernel<double, SplitCfg::RS, SplitCfg::NW, 2><<<grid, 32 * SplitCfg::NW, 0, st>>>(
+                  a, d.ilimbs.as<uint2>());
+            else
+              stripe_split_int_kernel<float, SplitCfg::RS, SplitCfg::NW, 2><<<grid, 32 * SplitCfg::NW, 0, st>>>(
+                  a, d.ilimbs.as<uint2>());
+            SF_CUDA(cudaGetLastError());
+          } else {
+            SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+          }
           plan->stats.launches++;
           if (!host_d) continue;
           while (static_cast<int>(d.chunk_events.size()) <= ci) {

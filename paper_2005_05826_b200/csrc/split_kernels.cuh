@@ -825,4 +825,118 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
   }
 }
 
+// ---- Integer-accumulator variant (A/B: SF_SPLIT_VARIANT=16). Same walk,
+// but each slot accumulates the row's 63-bit fixed-point length as two
+// 32-bit limbs with IMAD.WIDE.U32 (0/1 bit x limb + u64 accumulator) on the
+// integer/FMA pipes instead of DFMA on the FP64 pipe. Exact: a column has at
+// most ~2^14 heavy bits, so each 64-bit limb sum stays below 2^46.
+__global__ void sp_ilimbs_kernel(const double2* __restrict__ limbs, int64_t count, int32_t lo_bits,
+                                 uint2* __restrict__ il) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const double2 L = limbs[i];
+    const unsigned long long v = (static_cast<unsigned long long>(L.x) << lo_bits) +
+                                 static_cast<unsigned long long>(L.y);
+    il[i] = make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
+  }
+}
+
+template <int RS>
+__device__ __forceinline__ void heavy_half_int(uint32_t hu, const uint2* __restrict__ Lb,
+                                               const uint32_t (&vv)[RS], unsigned long long (&al)[RS],
+                                               unsigned long long (&ah)[RS]) {
+  while (hu) {
+    int b1, b2;
+    uint32_t m1, m2;
+    next_two(hu, b1, m1, b2, m2);
+    const uint2 L1 = __ldg(Lb + b1);
+    const uint2 L2 = __ldg(Lb + b2);
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const uint32_t f1 = (vv[i] & m1) ? 1u : 0u;
+      const uint32_t f2 = (vv[i] & m2) ? 1u : 0u;
+      // acc += f * L as one IMAD.WIDE.U32 each (the compiler would otherwise
+      // select and add in two 32-bit halves)
+      asm("mad.wide.u32 %0, %2, %3, %0;\n\tmad.wide.u32 %1, %2, %4, %1;"
+          : "+l"(al[i]), "+l"(ah[i]) : "r"(f1), "r"(L1.x), "r"(L1.y));
+      asm("mad.wide.u32 %0, %2, %3, %0;\n\tmad.wide.u32 %1, %2, %4, %1;"
+          : "+l"(al[i]), "+l"(ah[i]) : "r"(f2), "r"(L2.x), "r"(L2.y));
+    }
+  }
+}
+
+template <class Real, int RS, int NW, int MINB>
+__global__ void __launch_bounds__(32 * NW, MINB) stripe_split_int_kernel(const SplitArgs a, const uint2* il) {
+  const int lane = threadIdx.x & 31;
+  const int k = blockIdx.x * NW + (threadIdx.x >> 5);
+  const int n = a.n;
+  if (k >= n) return;
+  const int s0 = a.s_begin + blockIdx.y * 32 * RS;
+  const int64_t n_ext = a.n_ext;
+  const int Hw = static_cast<int>((*a.n_heavy + 63u) / 64u);
+  const int64_t l0 = static_cast<int64_t>(k) + s0 + 1 + lane;
+  int nvalid = 0;
+#pragma unroll
+  for (int i = 0; i < RS; ++i) nvalid += (s0 + lane + 32 * i < a.s_end) ? 1 : 0;
+  const int wvalid = __reduce_add_sync(0xffffffffu, nvalid);
+  unsigned long long ubits = 0;
+  unsigned long long al[RS], ah[RS];
+#pragma unroll
+  for (int i = 0; i < RS; ++i) {
+    al[i] = 0ull;
+    ah[i] = 0ull;
+  }
+#pragma unroll 1
+  for (int w = 0; w < Hw; ++w) {
+    const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
+    const unsigned long long u = __ldg(row + k);
+    if (u == 0ull) continue;
+    const uint2* Lw = il + 64 * static_cast<int64_t>(w);
+    ubits += static_cast<unsigned>(__popcll(u));
+    const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
+    uint32_t vv[RS];
+    if (static_cast<uint32_t>(u >> 32)) {
+#pragma unroll
+      for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
+      heavy_half_int<RS>(static_cast<uint32_t>(u >> 32), Lw + 32, vv, al, ah);
+    }
+    if (static_cast<uint32_t>(u)) {
+#pragma unroll
+      for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
+      heavy_half_int<RS>(static_cast<uint32_t>(u), Lw, vv, al, ah);
+    }
+  }
+  Real* dist = static_cast<Real*>(a.dist);
+  Real* tot = static_cast<Real*>(a.tot);
+  const unsigned long long* xs = a.colsum;
+  const int lb = a.lo_bits;
+  const __int128 C = (static_cast<__int128>(a.cacc[0]) << lb) + static_cast<__int128>(a.cacc[1]);
+#pragma unroll
+  for (int i = 0; i < RS; ++i) {
+    if (i >= nvalid) break;
+    const int s = s0 + lane + 32 * i;
+    const int64_t li = l0 + 32 * i;
+    const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
+    const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
+    const ulonglong2 light =
+        reinterpret_cast<const ulonglong2*>(a.gl)[static_cast<int64_t>(s - a.gl_begin) * n + k];
+    const __int128 G = (static_cast<__int128>(ah[i]) << 32) + static_cast<__int128>(al[i]) +
+                       (static_cast<__int128>(light.x) << lb) + static_cast<__int128>(light.y);
+    const __int128 P = (static_cast<__int128>(xs[2 * n + k] + xs[2 * n + lm]) << lb) +
+                       static_cast<__int128>(xs[3 * n + k] + xs[3 * n + lm]);
+    const __int128 X = (static_cast<__int128>(xs[k] + xs[lm]) << lb) + static_cast<__int128>(xs[n + k] + xs[n + lm]);
+    const __int128 tv = P + C - G;
+    const __int128 dv = X - 2 * G;
+    const Real t = static_cast<Real>(i2_fixed_to_double(tv, a.scale));
+    Real d = static_cast<Real>(i2_fixed_to_double(dv, a.scale));
+    if (a.finalize) d = t == Real(0) ? Real(0) : d / t;
+    dist[off] = d;
+    tot[off] = t;
+  }
+  if (a.counters && lane == 0) {
+    atomicAdd(a.counters, ubits * static_cast<unsigned long long>(wvalid));
+    atomicAdd(a.counters + 1, 2ull * ubits * static_cast<unsigned long long>(wvalid));
+  }
+}
+
 }  // namespace sf

@@ -677,7 +677,7 @@ def test_weighted_uwalk_even_n_duplicate_half_stripe(device_ok, metric, prec):
     assert np.allclose(dm.values, dm.values.T, rtol=0, atol=0)
 
 
-@pytest.mark.parametrize("variant", ["1", "4", "6", "7", "8", "9", "10", "11", "12", "13", "14", "15"])
+@pytest.mark.parametrize("variant", ["1", "4", "6", "7", "8", "9", "10", "11", "12", "13", "14", "15", "16"])
 def test_split_variants_are_bitwise_equal(device_ok, variant, monkeypatch):
     """The heavy-walk variants (64-bit v words, 4 warps, nonzero-word lists
     with and without L1 prefetch) add the same exact limbs: bit-identical."""
