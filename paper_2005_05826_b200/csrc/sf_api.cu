@@ -18,6 +18,7 @@
 #include <memory>
 #include <numeric>
 #include <random>
+#include <atomic>
 #include <thread>
 #include <string>
 #include <vector>
@@ -165,8 +166,20 @@ sf_status usable_devices(const sf_exec* ex, std::vector<int>& out) {
     const int k = (ex && ex->n_devices > 0) ? std::min(ex->n_devices, count) : count;
     for (int i = 0; i < k; ++i) want.push_back(i);
   }
+  // the architecture check is cached per ordinal: cudaGetDeviceProperties
+  // measured 96-238 ms on some calls (tools/e2e_probe.py, SF_DEBUG), a
+  // single attribute query is cheap, and the full properties are only
+  // fetched for the error message
+  static std::atomic<bool> checked[64] = {};
   for (int d : want) {
     if (d < 0 || d >= count) return fail(SF_EINVAL, "device ordinal " + std::to_string(d) + " out of range");
+    if (d < 64 && checked[d].load(std::memory_order_relaxed)) continue;
+    int major = 0;
+    SF_CUDA(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d));
+    if (major == 10) {
+      if (d < 64) checked[d].store(true, std::memory_order_relaxed);
+      continue;
+    }
     cudaDeviceProp prop;
     SF_CUDA(cudaGetDeviceProperties(&prop, d));
     if (prop.major != 10)
@@ -1686,6 +1699,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   phase("validate");
   std::vector<int> devices;
   SF_TRY(usable_devices(ex, devices));
+  phase("devices");
 
   auto plan = std::make_unique<sf_plan>();
   plan->metric = metric;
@@ -1763,6 +1777,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     budget = std::min(budget, avail * 3 / 4);
   }
   if (ex && ex->mem_budget_bytes > 0) budget = std::min(budget, static_cast<size_t>(ex->mem_budget_bytes));
+  phase("budget");
 
   // the table upload (C3: 192 MB from pageable memory) runs on a host thread
   // while this one builds the schedule
@@ -1796,6 +1811,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       if (t.joinable()) t.join();
     }
   } joiner{uploader};
+  phase("spawn uploader");
   int64_t cmax = static_cast<int64_t>(budget / std::max<size_t>(row_bytes + wsp_row_bytes, 1));
   if (plan->kernel >= 2 && !wsp) cmax = plan->E;  // the sparse bit paths keep all rows
   if (wsp) {
@@ -1863,7 +1879,9 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(plan->E) * row_bytes, "embedding rows"));
       SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));
       if (plan->kernel >= 6) {
+        phase("device alloc");
         SF_TRY(isect2_prepare(plan.get(), d, p));
+        phase("node-packed prepare");
         if (plan->kernel == 10) {
           // light sums for the whole range if they fit next to everything
           // else, else for passes of whole 512-stripe tiles
