@@ -1766,7 +1766,12 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                 static_cast<size_t>(pbound) * w * (metric == SF_GENERALIZED ? 2 : 1)
           : 0;
   size_t budget = SIZE_MAX;
+  // the resident sparse bit kernels (2-10) take every row in one chunk
+  // whatever the budget, so they skip the free-memory query here (it took
+  // 28-64 ms on some calls); kernel 10 sizes its light pass at device setup
+  const bool budget_free = plan->kernel >= 2 && !wsp;
   for (auto& d : plan->devs) {
+    if (budget_free) break;
     SF_CUDA(cudaSetDevice(d->dev));
     size_t freeb = 0;
     SF_TRY(device_free_bytes(d->dev, &freeb));
