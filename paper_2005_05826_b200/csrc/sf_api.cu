@@ -16,6 +16,7 @@
 #include <cstdint>
 #include <cstring>
 #include <memory>
+#include <mutex>
 #include <numeric>
 #include <random>
 #include <atomic>
@@ -464,6 +465,8 @@ struct DeviceState {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;     // D2H overlapped with the split kernel
   std::vector<cudaEvent_t> chunk_events;  // stripe chunks done (split kernel)
+  std::vector<std::pair<size_t, size_t>> chunk_spans;  // (byte offset, bytes) per chunk event
+  bool defer_copy = false;  // record chunk events only; the caller stages the copies
   DevBuf lens, feat_ptr, sidx, counts, totals;
   DevBuf dist, tot, emb, pend, exec_ctr;
   DevBuf sched;  // all schedule arrays, packed
@@ -1520,9 +1523,13 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
             d.chunk_events.push_back(e);
           }
           SF_CUDA(cudaEventRecord(d.chunk_events[static_cast<size_t>(ci)], st));
-          SF_CUDA(cudaStreamWaitEvent(d.copy_stream, d.chunk_events[static_cast<size_t>(ci)], 0));
           const size_t off = static_cast<size_t>(c0 - d.a) * n * w;
           const size_t bytes = static_cast<size_t>(c1 - c0) * n * w;
+          if (d.defer_copy) {
+            d.chunk_spans.emplace_back(off, bytes);
+            continue;
+          }
+          SF_CUDA(cudaStreamWaitEvent(d.copy_stream, d.chunk_events[static_cast<size_t>(ci)], 0));
           SF_CUDA(cudaMemcpyAsync(static_cast<char*>(host_d) + off, d.dist.as<char>() + off, bytes,
                                   cudaMemcpyDeviceToHost, d.copy_stream));
           if (host_t)
@@ -1996,20 +2003,133 @@ sf_status sf_plan_sync(sf_plan* plan) {
   return SF_OK;
 }
 
+// ------------------------------------------------------------ pageable downloads
+// A D2H cudaMemcpy into pageable memory goes through the driver's small
+// staging buffers on one thread (C3: ~16 GB/s, 0.3 s of a 0.77 s call).
+// Pageable destinations instead get a process-wide pinned double buffer:
+// block b+1 is copied device -> pinned while host threads copy block b
+// pinned -> destination (the reference hands out pageable Eigen buffers).
+namespace {
+bool host_pinned(const void* ptr) {
+  cudaPointerAttributes at{};
+  if (!ptr || cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+struct PinnedStaging {
+  std::mutex mu;
+  char* slot[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+};
+PinnedStaging& staging() {
+  static PinnedStaging s;  // freed at process exit by the driver
+  return s;
+}
+
+void parallel_memcpy(char* dst, const char* src, size_t bytes) {
+  const size_t min_piece = 8ull << 20;
+  unsigned hw = std::thread::hardware_concurrency();
+  size_t T = std::min<size_t>(std::max(1u, std::min(hw, 16u)), std::max<size_t>(1, bytes / min_piece));
+  if (T <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t piece = (bytes + T - 1) / T;
+  std::vector<std::thread> th;
+  for (size_t i = 1; i < T; ++i) {
+    const size_t o = i * piece;
+    if (o >= bytes) break;
+    th.emplace_back([=] { std::memcpy(dst + o, src + o, std::min(piece, bytes - o)); });
+  }
+  std::memcpy(dst, src, std::min(piece, bytes));
+  for (auto& t : th) t.join();
+}
+
+// dsrc (device memory of the current device) -> hdst (pageable host), on cs.
+sf_status staged_d2h(cudaStream_t cs, const char* dsrc, char* hdst, size_t bytes) {
+  if (bytes == 0) return SF_OK;
+  PinnedStaging& S = staging();
+  std::lock_guard<std::mutex> lock(S.mu);
+  constexpr size_t kSlot = 128ull << 20;
+  if (!S.slot[0]) {
+    for (int i = 0; i < 2; ++i) {
+      void* h = nullptr;
+      if (cudaHostAlloc(&h, kSlot, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        if (S.slot[0]) cudaFreeHost(S.slot[0]);
+        S.slot[0] = nullptr;
+        // no pinned memory to spare: the driver's own pageable path
+        SF_CUDA(cudaMemcpyAsync(hdst, dsrc, bytes, cudaMemcpyDeviceToHost, cs));
+        SF_CUDA(cudaStreamSynchronize(cs));
+        return SF_OK;
+      }
+      S.slot[i] = static_cast<char*>(h);
+    }
+    S.bytes = kSlot;
+  }
+  cudaEvent_t ev[2];
+  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  if (cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
+    cudaEventDestroy(ev[0]);
+    return fail(SF_ECUDA, "cudaEventCreate failed");
+  }
+  sf_status rc = SF_OK;
+  const size_t nblk = (bytes + S.bytes - 1) / S.bytes;
+  auto issue = [&](size_t b) -> sf_status {
+    const size_t o = b * S.bytes;
+    SF_CUDA(cudaMemcpyAsync(S.slot[b & 1], dsrc + o, std::min(S.bytes, bytes - o), cudaMemcpyDeviceToHost, cs));
+    SF_CUDA(cudaEventRecord(ev[b & 1], cs));
+    return SF_OK;
+  };
+  rc = issue(0);
+  for (size_t b = 0; rc == SF_OK && b < nblk; ++b) {
+    // slot (b+1)&1 was drained by block b-1's host copy, which has returned
+    if (b + 1 < nblk) rc = issue(b + 1);
+    if (rc != SF_OK) break;
+    if (cudaEventSynchronize(ev[b & 1]) != cudaSuccess) {
+      rc = fail(SF_ECUDA, std::string("staged download: ") + cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    const size_t o = b * S.bytes;
+    parallel_memcpy(hdst + o, S.slot[b & 1], std::min(S.bytes, bytes - o));
+  }
+  cudaStreamSynchronize(cs);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  return rc;
+}
+}  // namespace
+
 sf_status sf_plan_download(sf_plan* plan, void* dist_out, void* tot_out) {
   if (!plan) return fail(SF_EINVAL, "plan is null");
   if (!plan->ran) return fail(SF_ESTATE, "plan has not run");
   if (!dist_out) return fail(SF_EINVAL, "dist_out is null");
   const bool has_t = plan->metric != SF_WEIGHTED_UNNORMALIZED;
   const size_t w = plan->prec == SF_FP64 ? 8 : 4;
+  const bool pageable_d = !host_pinned(dist_out);
+  const bool pageable_t = tot_out && !host_pinned(tot_out);
   for (auto& dp : plan->devs) {
     DeviceState& d = *dp;
     SF_CUDA(cudaSetDevice(d.dev));
     const size_t off = static_cast<size_t>(d.a - plan->start) * plan->n * w;
     const size_t bytes = static_cast<size_t>(d.b - d.a) * plan->n * w;
-    SF_CUDA(cudaMemcpyAsync(static_cast<char*>(dist_out) + off, d.dist.p, bytes, cudaMemcpyDeviceToHost, d.stream));
-    if (has_t && tot_out)
-      SF_CUDA(cudaMemcpyAsync(static_cast<char*>(tot_out) + off, d.tot.p, bytes, cudaMemcpyDeviceToHost, d.stream));
+    if (pageable_d) {
+      SF_CUDA(cudaStreamSynchronize(d.stream));
+      SF_TRY(staged_d2h(d.stream, d.dist.as<char>(), static_cast<char*>(dist_out) + off, bytes));
+    } else {
+      SF_CUDA(cudaMemcpyAsync(static_cast<char*>(dist_out) + off, d.dist.p, bytes, cudaMemcpyDeviceToHost, d.stream));
+    }
+    if (has_t && tot_out) {
+      if (pageable_t) {
+        SF_CUDA(cudaStreamSynchronize(d.stream));
+        SF_TRY(staged_d2h(d.stream, d.tot.as<char>(), static_cast<char*>(tot_out) + off, bytes));
+      } else {
+        SF_CUDA(cudaMemcpyAsync(static_cast<char*>(tot_out) + off, d.tot.p, bytes, cudaMemcpyDeviceToHost, d.stream));
+      }
+    }
   }
   for (auto& dp : plan->devs) {
     SF_CUDA(cudaSetDevice(dp->dev));
@@ -2040,17 +2160,37 @@ sf_status sf_compute_stripes(const sf_problem* p, sf_metric metric, sf_precision
   if (dbg)
     std::fprintf(stderr, "stripefrac: plan_create %.1f ms\n",
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
-  auto pinned = [](const void* ptr) {
-    cudaPointerAttributes at{};
-    if (!ptr || cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
-      cudaGetLastError();
-      return false;
+  const bool all_pinned = host_pinned(dist_out) && (!tot_out || host_pinned(tot_out));
+  if (plan->kernel == 10 && !all_pinned) {
+    // pageable destinations: chunk events only, then each finished chunk is
+    // staged through pinned memory while the later chunks compute
+    const size_t w = prec == SF_FP64 ? 8 : 4;
+    plan->stats.launches = 0;
+    for (auto& dp : plan->devs) {
+      const size_t off = static_cast<size_t>(dp->a - plan->start) * plan->n * w;
+      dp->chunk_spans.clear();
+      dp->defer_copy = true;
+      const sf_status rc = run_device(plan, *dp, finalize, static_cast<char*>(dist_out) + off,
+                                      tot_out ? static_cast<char*>(tot_out) + off : nullptr);
+      dp->defer_copy = false;
+      SF_TRY(rc);
     }
-    return at.type == cudaMemoryTypeHost;
-  };
-  // pageable destinations make cudaMemcpyAsync block the host, which would
-  // serialise the chunks; those get compute-then-download instead
-  if (plan->kernel == 10 && pinned(dist_out) && (!tot_out || pinned(tot_out))) {
+    for (auto& dp : plan->devs) {
+      DeviceState& d = *dp;
+      SF_CUDA(cudaSetDevice(d.dev));
+      const size_t off = static_cast<size_t>(d.a - plan->start) * plan->n * w;
+      for (size_t ci = 0; ci < d.chunk_spans.size(); ++ci) {
+        SF_CUDA(cudaEventSynchronize(d.chunk_events[ci]));
+        const size_t co = d.chunk_spans[ci].first, cb = d.chunk_spans[ci].second;
+        SF_TRY(staged_d2h(d.copy_stream, d.dist.as<char>() + co, static_cast<char*>(dist_out) + off + co, cb));
+        if (tot_out && metric != SF_WEIGHTED_UNNORMALIZED)
+          SF_TRY(staged_d2h(d.copy_stream, d.tot.as<char>() + co, static_cast<char*>(tot_out) + off + co, cb));
+      }
+    }
+    plan->ran = true;
+    plan->finalized = finalize != 0;
+    SF_TRY(sf_plan_sync(plan));
+  } else if (plan->kernel == 10) {
     // download overlapped with the split kernel, chunk by chunk
     const size_t w = prec == SF_FP64 ? 8 : 4;
     plan->stats.launches = 0;

@@ -459,6 +459,31 @@ def test_split_light_passes_and_pinned_download(device_ok, light_pass, monkeypat
         assert np.array_equal(t.reshape(stop - start, n), pt)
 
 
+def test_pageable_download_staged_matches_pinned(device_ok):
+    """Pageable destinations are staged through a pinned double buffer
+    (128 MB blocks, host threads copying out) chunk by chunk while the split
+    kernel computes later chunks: bitwise equal to the pinned, overlapped
+    download. n = 17,000 gives 4 chunks of ~290 MB (3 staging blocks each);
+    the weighted metric takes the download-after-compute path."""
+    import torch
+    inst = sf.random_instance(97, 17000, 300, 0.01)
+    problem = sf.flatten(inst.tree, inst.table)
+    n = problem.n_samples
+    start, stop = 0, n // 2
+    for metric, kernel in ((1, N.KERNEL_SPLIT), (3, 0)):
+        pd = torch.full(((stop - start) * n,), float("nan"), dtype=torch.float64, pin_memory=True).numpy()
+        pt = torch.full(((stop - start) * n,), float("nan"), dtype=torch.float64, pin_memory=True).numpy()
+        ex, _keep = N.make_exec([0], kernel)
+        st = N.sf_stats()
+        N.check(N.lib().sf_compute_stripes(problem.ref, metric, 8, start, stop, N.ptr(pd), N.ptr(pt), 1,
+                                           C.byref(ex), C.byref(st)))
+        d, t, _ = _gpu_stripes(problem, metric, 8, start, stop, kernel)
+        assert not np.isnan(d).any() and not np.isnan(t).any()
+        assert np.array_equal(d, pd.reshape(stop - start, n))
+        assert np.array_equal(t, pt.reshape(stop - start, n))
+        del pd, pt, d, t
+
+
 @pytest.mark.parametrize("prec", [8, 4])
 @pytest.mark.parametrize("metric", [2, 3])
 def test_weighted_sparse_walk_matches_dense_bitwise(device_ok, metric, prec):
