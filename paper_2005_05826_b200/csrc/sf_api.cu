@@ -1898,13 +1898,29 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
           // light sums for the whole range if they fit next to everything
           // else, else for passes of whole 512-stripe tiles
           size_t freeb = 0;
-          SF_TRY(device_free_bytes(d.dev, &freeb));
           const size_t per_stripe = static_cast<size_t>(n) * 16;
           const size_t reserve = (1ull << 30);
-          size_t fit = freeb > reserve ? (freeb - reserve) / per_stripe : 0;
+          const int span = d.b - d.a;
+          // without a budget, a probe allocation of the whole range plus the
+          // light member lists and the reserve answers "does it fit"; it
+          // returns to the pool for the allocations below. cudaMemGetInfo
+          // stalls up to ~100 ms on some calls (p99 63 ms on the box).
+          size_t fit = 0;
+          bool probed = false;
+          if (!(ex && ex->mem_budget_bytes > 0) && !std::getenv("SF_LIGHT_PASS")) {
+            const size_t after = static_cast<size_t>(plan->E) * 4 * (3 + 2 * static_cast<size_t>(split_heavy_min(n)));
+            DevBuf probe;
+            if (probe.alloc(d.dev, static_cast<size_t>(span) * per_stripe + after + reserve, "fit probe") == SF_OK) {
+              fit = static_cast<size_t>(span);
+              probed = true;
+            }
+          }
+          if (!probed) {
+            SF_TRY(device_free_bytes(d.dev, &freeb));
+            fit = freeb > reserve ? (freeb - reserve) / per_stripe : 0;
+          }
           if (ex && ex->mem_budget_bytes > 0)
             fit = std::min(fit, static_cast<size_t>(ex->mem_budget_bytes) / per_stripe);
-          const int span = d.b - d.a;
           int pass = static_cast<int>(std::min<size_t>(fit, static_cast<size_t>(span)));
           if (pass < span) pass = std::max(512, pass / 512 * 512);
           if (const char* e = std::getenv("SF_LIGHT_PASS")) pass = std::max(1, std::atoi(e));  // tests
