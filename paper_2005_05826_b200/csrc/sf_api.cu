@@ -1780,11 +1780,23 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   for (auto& d : plan->devs) {
     if (budget_free) break;
     SF_CUDA(cudaSetDevice(d->dev));
-    size_t freeb = 0;
-    SF_TRY(device_free_bytes(d->dev, &freeb));
     const size_t stripes_b = static_cast<size_t>(d->b - d->a) * n * w * (has_t ? 2 : 1);
     const size_t csr_b = static_cast<size_t>(p->feat_ptr[p->n_features]) * 12 + static_cast<size_t>(plan->E) * 64;
     const size_t fixed_b = stripes_b + csr_b + wuw_fixed + (512ull << 20);
+    if (!(ex && ex->mem_budget_bytes > 0)) {
+      // one chunk of every row (no pending rows) if a probe allocation of
+      // it plus the fixed part (with the 4/3 margin below) succeeds; the
+      // memory returns to the pool. cudaMemGetInfo stalls up to ~100 ms.
+      const size_t whole = static_cast<size_t>(plan->E) * (row_bytes + wsp_row_bytes);
+      DevBuf probe;
+      if (whole / 3 < (SIZE_MAX - fixed_b) / 4 &&
+          probe.alloc(d->dev, fixed_b + whole + whole / 3, "fit probe") == SF_OK) {
+        budget = std::min(budget, whole);
+        continue;
+      }
+    }
+    size_t freeb = 0;
+    SF_TRY(device_free_bytes(d->dev, &freeb));
     const size_t avail = freeb > fixed_b ? freeb - fixed_b : 0;
     budget = std::min(budget, avail * 3 / 4);
   }
