@@ -58,6 +58,7 @@ CONFIGS = {
     "small": dict(seed=7, n=4000, leaves=40000, density=0.002, subset=0,
                   metric="unweighted", precision="fp64", workload="small UW fp64 (quick check)"),
 }
+KERNELS = {"auto": 0, "dense": 1, "sparse": 2, "split": 10, "wsparse": 11, "uwalk": 12}
 METRIC_CODE = {"unweighted": 1, "weighted-unnormalized": 2, "weighted-normalized": 3, "generalized": 4}
 # algorithmic FP64/FP32 flops per update of update_entry (kernels.hpp:55-66),
 # FMA counted as 2: UW = sub, fma, max, fma; WN = sub, fma, add, fma; WU = sub, fma
@@ -176,7 +177,7 @@ def run_ours(args, cfg):
     S = n // 2
     stop_all = min(S, args.stripes) if args.stripes else S
     a, b = shard.rank_range(0, stop_all, rank, world)
-    kernel = {"auto": 0, "dense": 1, "sparse": 2, "flat32": 3, "flat64": 4, "isect": 5, "isect2": 6, "isect3": 7, "isect4": 8, "isect5": 9, "split": 10, "wsparse": 11}[args.kernel]
+    kernel = KERNELS[args.kernel]
     ex, _keep = N.make_exec([local], kernel, alpha=cfg.get("alpha", 1.0))
     plan = C.c_void_p()
     t0 = time.perf_counter()
@@ -406,8 +407,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--kernel", choices=["auto", "dense", "sparse", "flat32", "flat64", "isect", "isect2", "isect3", "isect4", "isect5", "split", "wsparse"],
-                    default="auto")
+    ap.add_argument("--kernel", choices=sorted(KERNELS), default="auto")
     ap.add_argument("--stripes", type=int, default=0, help="limit to stripes [0, N) (debug)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")

@@ -231,24 +231,45 @@ StripeSet<Real> compute_unifrac(const PhyloTree& tree, const SampleTable& table,
   return set;
 }
 
-// Full pipeline to a condensed matrix, condensed on device.
+// Full pipeline to a condensed matrix: the stripes never leave the device;
+// condense runs there and the n x n matrix is copied into dm.values once.
 template <class Real>
 DistanceMatrix compute_distance_matrix(const PhyloTree& tree, const SampleTable& table,
                                        const KernelConfig& cfg, int threads = 1,
                                        KernelCounters* counters_out = nullptr) {
-  const StripeSet<Real> set = compute_unifrac<Real>(tree, table, cfg, 0, -1, threads, counters_out);
-  const int n = set.n_samples;
+  (void)threads;
+  constexpr Precision kPrec =
+      std::is_same_v<Real, float> ? Precision::Fp32 : Precision::Fp64;
+  if (cfg.precision != kPrec)
+    throw Error("config asks for " + std::string(name(cfg.precision)) +
+                " but compute_distance_matrix was instantiated for " + std::string(name(kPrec)));
+  if (cfg.batch_capacity < 1) throw Error("batch capacity must be >= 1");
+  if (cfg.resolved_step_size() < 1) throw Error("step size must be >= 1");
+  const int n = table.n_samples();
+  const int S = total_stripes(n);
+  const PhyloTree sheared = sheared_to_table(tree, table);
+  b200::FlatProblem flat;
+  b200::flatten(sheared, table, flat);
+  if (table.n_features() != sheared.n_leaves())
+    throw Error("tree leaves and table features differ; shear the tree first");
   DistanceMatrix dm;
   dm.sample_ids = table.sample_ids;
-  dm.precision = std::is_same_v<Real, float> ? Precision::Fp32 : Precision::Fp64;
-  dm.values = RowMatrix<double>::Zero(n, n);
-  const sf_status st = sf_condense(b200::precision_code<Real>(), n, set.start, set.stop,
-                                   set.distances.data(), dm.values.data(), 0);
+  dm.precision = kPrec;
+  dm.values.resize(n, n);  // every entry is written on device
+  const sf_exec ex = b200::default_exec();
+  const sf_status st = sf_compute_distance_matrix(&flat.p, b200::metric_code(cfg.metric),
+                                                  b200::precision_code<Real>(), dm.values.data(), &ex, nullptr);
   if (st != SF_OK) {
     const std::string msg = sf_last_error();
     if (msg.find("duplicated") != std::string::npos)
       throw Error("condense: duplicated slot disagrees");
     throw Error(msg);
+  }
+  if (counters_out) {
+    const std::uint64_t E = sheared.postorder.size();
+    const std::uint64_t B = static_cast<std::uint64_t>(cfg.batch_capacity);
+    b200::count(*counters_out, cfg, E, static_cast<std::uint64_t>(S) * static_cast<std::uint64_t>(n),
+                (E + B - 1) / B);
   }
   return dm;
 }

@@ -78,10 +78,10 @@ typedef struct sf_exec {
   const int32_t* devices;   /* explicit ordinals, or NULL for 0..n_devices-1 */
   int64_t mem_budget_bytes; /* per-device cap for embedding chunks; 0 = auto */
   int32_t kernel;           /* 0 = auto, 1 = dense tiled; unweighted only: 2 = sparse bit walk
-                               (bitwise; 3/4 flattened variants), 5-9 = intersection walks and
-                               10 = split heavy-walk/light-scatter (exact fixed-point sums; the
-                               default); weighted only: 11 = sparse walk over present rows (the
-                               default; the only kernel for SF_GENERALIZED) */
+                               (bitwise: the reference's adds in its order), 10 = split heavy
+                               walk + light scatter (exact fixed-point sums, correctly rounded;
+                               the default); weighted only: 11 = present-row walk (bitwise in
+                               exact mode), 12 = u-walk (the default; also SF_GENERALIZED) */
   int32_t flags;            /* bit 0: SF_EXEC_EXACT_NO_FMA: bitwise-identical results (weighted:
                                no FMA; unweighted auto: the sparse walk instead of kernel 10) */
   double alpha;             /* SF_GENERALIZED only: the exponent, finite, >= 0 (ABI v3) */
@@ -99,7 +99,7 @@ typedef struct sf_stats {
   double stripe_ms;      /* device time of the stripe kernels (max over devices) */
   double finalize_ms;    /* device time of finalize (max over devices) */
   double total_ms;       /* device time of the whole run (max over devices) */
-  uint64_t fp64_ops;     /* FP instructions x lanes the stripe kernel issued (kernel 9; else 0) */
+  uint64_t fp64_ops;     /* DFMA lane-ops the split kernel's heavy walk issued (kernel 10; else 0) */
 } sf_stats;
 
 /* ---- library ------------------------------------------------------------ */
@@ -133,6 +133,25 @@ sf_status sf_plan_run(sf_plan* plan, int32_t finalize);
 sf_status sf_plan_sync(sf_plan* plan);
 /* Copy stripes [start, stop) to host buffers (row-major, see above). */
 sf_status sf_plan_download(sf_plan* plan, void* dist_out, void* tot_out);
+/*
+ * condense() (stripes.cpp:68-129) of a finalized full-range plan, on device:
+ * out is the caller's row-major n x n fp64 matrix (zero diagonal, mirrored;
+ * even n: the duplicated half-stripe copies must agree, else SF_EINVAL
+ * "condense: duplicated slot disagrees"). The stripes never leave the GPU;
+ * the matrix is copied to the host once.
+ */
+sf_status sf_plan_condense(sf_plan* plan, double* out);
+/*
+ * compute_distance_matrix<Real> (kernels.hpp:319-326): plan over [0, S),
+ * run with finalize, sf_plan_condense into out (n x n). stats_out may be NULL.
+ */
+sf_status sf_compute_distance_matrix(const sf_problem* p, sf_metric metric, sf_precision prec, double* out,
+                                     const sf_exec* ex, sf_stats* stats_out);
+/*
+ * Return the memory the library's per-device pool keeps for reuse across
+ * plans to the device (the pool keeps freed plan buffers by default).
+ */
+sf_status sf_trim_memory(int32_t device);
 /*
  * Write the plan's finalized stripes as a .strf file. Replaces
  * write_stripe_file (stripes.cpp:179-201): same 32-byte header, payload

@@ -313,6 +313,108 @@ int cmd_golden(const std::string& dir, const std::string& demo_dir) {
   return 0;
 }
 
+// Wide branch-length goldens (tests/golden/instances_wide.json): the
+// reference's results on trees whose lengths span many binades, so the
+// GPU path's exact fixed-point levels are exercised where one 63-bit grid
+// would round short branches. Three families:
+//  * random_instance trees with every length redrawn log-uniformly in
+//    [10^lo, 2] (deterministic mt19937_64 stream per seed);
+//  * "twin" samples: cherries with tiny twigs (1e-12 .. 1e-9) under normal
+//    internal branches; sample pairs pick the same cherries and differ only
+//    in which twig, so their distance is carried by branches <= 1e-9 alone;
+//  * a tree whose lengths need several fixed-point levels (1e-300 .. 1e3).
+std::string fmt_len(double v) { return num(v); }
+
+int cmd_wide_golden(const std::string& dir) {
+  std::string j = "[";
+  bool first_case = true;
+  auto add = [&](const std::string& name, const PhyloTree& tree, const SampleTable& table, const std::string& params,
+                 std::vector<std::pair<int, int>> ranges) {
+    if (!first_case) j += ",";
+    first_case = false;
+    j += case_json(name, tree, table, params, false, true, ranges);
+  };
+  // (1) log-uniform lengths on random_instance trees
+  struct W { std::uint64_t seed; int n, leaves; double dens; double lo; };
+  const W ws[] = {{7001, 40, 120, 0.2, -12.0}, {7002, 33, 200, 0.05, -15.0}, {7003, 64, 300, 0.1, -9.0}};
+  for (const W& w : ws) {
+    SynthInstance inst = random_instance(w.seed, w.n, w.leaves, w.dens);
+    std::mt19937_64 rng(w.seed * 7919);
+    std::uniform_real_distribution<double> u(w.lo, std::log10(2.0));
+    for (auto& nd : inst.tree.nodes) nd.length = std::pow(10.0, u(rng));
+    const PhyloTree tree = parse_newick(to_newick(inst.tree));
+    char params[200];
+    std::snprintf(params, sizeof(params),
+                  "{\"kind\":\"wide\",\"seed\":%llu,\"n\":%d,\"leaves\":%d,\"density\":%g,\"log10_min\":%g}",
+                  static_cast<unsigned long long>(w.seed), w.n, w.leaves, w.dens, w.lo);
+    add("wide" + std::to_string(w.seed), tree, inst.table, params, {{0, 3}, {w.n / 4, w.n / 2}});
+  }
+  // (2) twins: distance carried only by twigs <= 1e-9
+  for (std::uint64_t seed : {7101ull, 7102ull}) {
+    std::mt19937_64 rng(seed);
+    std::uniform_real_distribution<double> tw(-12.0, -9.0), nl(0.01, 2.0), coin(0.0, 1.0);
+    const int m = seed == 7101 ? 24 : 41;  // cherries
+    const int pairs = seed == 7101 ? 10 : 17;
+    std::vector<std::string> sub;
+    for (int i = 0; i < m; ++i) {
+      char buf[160];
+      std::snprintf(buf, sizeof(buf), "(T%da:%s,T%db:%s)c%d:%s", i, fmt_len(std::pow(10.0, tw(rng))).c_str(), i,
+                    fmt_len(std::pow(10.0, tw(rng))).c_str(), i, fmt_len(nl(rng)).c_str());
+      sub.push_back(buf);
+    }
+    int inner = 0;
+    while (sub.size() > 1) {  // random joins
+      std::uniform_int_distribution<std::size_t> pick(0, sub.size() - 1);
+      const std::size_t a = pick(rng);
+      std::string A = sub[a];
+      sub.erase(sub.begin() + static_cast<std::ptrdiff_t>(a));
+      std::uniform_int_distribution<std::size_t> pick2(0, sub.size() - 1);
+      const std::size_t b = pick2(rng);
+      std::string B = sub[b];
+      sub.erase(sub.begin() + static_cast<std::ptrdiff_t>(b));
+      sub.push_back("(" + A + "," + B + ")i" + std::to_string(inner++) + ":" + fmt_len(nl(rng)));
+    }
+    const PhyloTree tree = parse_newick(sub[0] + ";");
+    std::vector<std::string> samples, features;
+    for (int s = 0; s < 2 * pairs; ++s) samples.push_back("s" + std::to_string(s));
+    for (int i = 0; i < m; ++i) {
+      features.push_back("T" + std::to_string(i) + "a");
+      features.push_back("T" + std::to_string(i) + "b");
+    }
+    std::vector<double> counts(static_cast<std::size_t>(2 * m) * static_cast<std::size_t>(2 * pairs), 0.0);
+    auto at = [&](int f, int s) -> double& { return counts[static_cast<std::size_t>(f) * (2 * pairs) + s]; };
+    for (int p = 0; p < pairs; ++p) {
+      int flips = 0;
+      for (int i = 0; i < m; ++i) {
+        if (coin(rng) > 0.4) continue;
+        const int side = coin(rng) < 0.5 ? 0 : 1;
+        const bool flip = flips < 1 + p % 3 && coin(rng) < 0.3;
+        flips += flip ? 1 : 0;
+        at(2 * i + side, 2 * p) = 1.0 + std::floor(coin(rng) * 20.0);
+        at(2 * i + (flip ? 1 - side : side), 2 * p + 1) = 1.0 + std::floor(coin(rng) * 20.0);
+      }
+      at(0, 2 * p) += 1.0;  // every sample nonempty
+      at(0, 2 * p + 1) += 1.0;
+    }
+    char params[120];
+    std::snprintf(params, sizeof(params), "{\"kind\":\"twins\",\"seed\":%llu,\"cherries\":%d,\"pairs\":%d}",
+                  static_cast<unsigned long long>(seed), m, pairs);
+    add("twins" + std::to_string(seed), tree, dense_table(samples, features, counts), params, {{1, pairs}});
+  }
+  // (3) lengths needing several fixed-point levels
+  {
+    SynthInstance inst = random_instance(7201, 21, 60, 0.3);
+    std::mt19937_64 rng(7201);
+    std::uniform_real_distribution<double> u(-300.0, 3.0);
+    for (auto& nd : inst.tree.nodes) nd.length = std::pow(10.0, u(rng));
+    const PhyloTree tree = parse_newick(to_newick(inst.tree));
+    add("levels7201", tree, inst.table, "{\"kind\":\"wide\",\"seed\":7201,\"n\":21,\"leaves\":60,\"density\":0.3,\"log10_min\":-300}",
+        {{2, 7}});
+  }
+  write_file(dir + "/instances_wide.json", j + "]");
+  return 0;
+}
+
 // Mantel golden vectors (validate.cpp:111-159): reference DMs of seeded
 // instances, r / r^2 / p for several seeds and permutation counts, and the
 // first permutations of a seed (the stream the GPU path must reproduce).
@@ -497,6 +599,7 @@ int main(int argc, char** argv) {
     const std::string cmd = argv[1];
     if (cmd == "golden" && argc >= 4) return cmd_golden(argv[2], argv[3]);
     if (cmd == "mantel_golden" && argc >= 3) return cmd_mantel_golden(argv[2]);
+    if (cmd == "wide_golden" && argc >= 3) return cmd_wide_golden(argv[2]);
     if (cmd == "strf_golden" && argc >= 4) return cmd_strf_golden(argv[2], argv[3]);
     if (cmd == "instance" && argc >= 7)
       return cmd_instance(std::strtoull(argv[2], nullptr, 10), std::atoi(argv[3]), std::atoi(argv[4]),

@@ -18,7 +18,8 @@ SF_UNWEIGHTED, SF_WEIGHTED_UNNORMALIZED, SF_WEIGHTED_NORMALIZED = 1, 2, 3
 SF_GENERALIZED = 4  # extension: generalized UniFrac (sf_exec.alpha); not in the reference
 SF_FP32, SF_FP64 = 4, 8
 SF_EXEC_EXACT_NO_FMA = 1
-KERNEL_AUTO, KERNEL_DENSE, KERNEL_SPARSE, KERNEL_ISECT, KERNEL_ISECT2, KERNEL_ISECT3, KERNEL_ISECT4, KERNEL_ISECT5, KERNEL_SPLIT = 0, 1, 2, 5, 6, 7, 8, 9, 10
+KERNEL_AUTO, KERNEL_DENSE, KERNEL_SPARSE = 0, 1, 2  # auto, dense tiled (every metric), bitwise union walk (UW)
+KERNEL_SPLIT = 10  # unweighted: heavy walk + light scatter, exact fixed-point sums (the default)
 KERNEL_WSPARSE = 11  # weighted metrics: present-row walk (bitwise; the exact-mode default)
 KERNEL_WUWALK = 12  # weighted metrics: warp-uniform u-walk + double-double remainder (the default)
 
@@ -76,6 +77,10 @@ SIGNATURES = {
                                      _P, _P, C.c_int32, C.POINTER(sf_exec), C.POINTER(sf_stats)]),
     "sf_plan_create": (C.c_int, [C.POINTER(sf_problem), C.c_int, C.c_int, C.c_int32, C.c_int32,
                                  C.POINTER(sf_exec), C.POINTER(_P)]),
+    "sf_plan_condense": (C.c_int, [_P, _P]),
+    "sf_compute_distance_matrix": (C.c_int, [C.POINTER(sf_problem), C.c_int, C.c_int, _P, C.POINTER(sf_exec),
+                                             C.POINTER(sf_stats)]),
+    "sf_trim_memory": (C.c_int, [C.c_int32]),
     "sf_plan_run": (C.c_int, [_P, C.c_int32]),
     "sf_plan_sync": (C.c_int, [_P]),
     "sf_plan_download": (C.c_int, [_P, _P, _P]),

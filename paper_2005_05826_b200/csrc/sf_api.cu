@@ -25,8 +25,7 @@
 #include <vector>
 
 #include "embed_kernels.cuh"
-#include "isect2_kernels.cuh"
-#include "isect_kernels.cuh"
+#include "bits.cuh"
 #include "split_kernels.cuh"
 #include "sf_common.hpp"
 #include "sparse_kernels.cuh"
@@ -66,36 +65,59 @@ sf_status fail(sf_status st, const std::string& msg) {
   return st;
 }
 
-// Device memory comes from each device's default stream-ordered pool with an
-// unbounded release threshold: a plan's buffers (tens of GB at C3) go back
-// to the pool when it is destroyed and the next plan takes them without new
-// cudaMalloc/page-table work (plan creation was 70-300 ms of an end-to-end
-// call; see tools/e2e_probe.py).
-void keep_pool(int device) {
-  static bool done[64] = {};
-  if (device < 0 || device >= 64 || done[device]) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = UINT64_MAX;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  cudaGetLastError();
-  done[device] = true;
+// Device memory comes from a stream-ordered pool the library owns on each
+// device (not the device's default pool, which torch / NCCL in the same
+// process may use), with an unbounded release threshold: a plan's buffers
+// (tens of GB at C3) go back to the pool when it is destroyed and the next
+// plan takes them without new cudaMalloc/page-table work (plan creation was
+// 70-300 ms of an end-to-end call; see tools/e2e_probe.py). sf_trim_memory()
+// returns the pool's unused memory to the device.
+struct PoolSlot {
+  std::once_flag once;
+  cudaMemPool_t pool = nullptr;
+};
+PoolSlot g_pools[64];
+
+cudaMemPool_t device_pool(int device) {
+  if (device < 0 || device >= 64) return nullptr;
+  PoolSlot& s = g_pools[device];
+  std::call_once(s.once, [&] {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+      s.pool = pool;
+    }
+    cudaGetLastError();
+  });
+  return s.pool;
 }
 
-// Free device memory including what the pool holds but no buffer uses.
+// Free device memory including what the library's pool holds but no buffer
+// uses.
 sf_status device_free_bytes(int device, size_t* out) {
   size_t freeb = 0, totalb = 0;
   SF_CUDA(cudaMemGetInfo(&freeb, &totalb));
-  cudaMemPool_t pool;
   uint64_t reserved = 0, used = 0;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess &&
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
+  cudaMemPool_t pool = device_pool(device);
+  if (pool && cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess &&
       cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess && reserved > used)
     freeb += static_cast<size_t>(reserved - used);
   cudaGetLastError();
   *out = freeb;
   return SF_OK;
+}
+
+// Test hook: SF_FORCE_PROBE_FAIL=1 makes every fit probe fail, so the
+// free-memory fallback sizing runs.
+bool probe_disabled() {
+  const char* e = std::getenv("SF_FORCE_PROBE_FAIL");
+  return e && std::atoi(e) != 0;
 }
 
 // Device allocation owned by one device.
@@ -124,8 +146,8 @@ struct DevBuf {
     reset();
     dev = device;
     if (nbytes == 0) nbytes = 16;
-    keep_pool(device);
-    cudaError_t e = cudaMallocAsync(&p, nbytes, 0);
+    cudaMemPool_t pool = device_pool(device);
+    cudaError_t e = pool ? cudaMallocFromPoolAsync(&p, nbytes, pool, 0) : cudaMallocAsync(&p, nbytes, 0);
     if (e == cudaSuccess) e = cudaStreamSynchronize(0);  // usable from any stream
     if (e != cudaSuccess) {
       p = nullptr;
@@ -141,6 +163,27 @@ struct DevBuf {
     return static_cast<T*>(p);
   }
 };
+
+// "Does `bytes` fit?" answered by a probe allocation from the library's
+// pool (cudaMemGetInfo stalls up to ~100 ms on some calls: p99 63 ms on the
+// box). The pool then keeps only `keep` of the probed bytes reserved (what
+// the caller allocates next); the rest is trimmed back to the device.
+bool probe_fits(int device, size_t bytes, size_t keep) {
+  if (probe_disabled()) return false;
+  bool ok = false;
+  {
+    DevBuf probe;
+    ok = probe.alloc(device, bytes, "fit probe") == SF_OK;
+  }
+  cudaGetLastError();
+  if (cudaMemPool_t pool = device_pool(device)) {
+    uint64_t used = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess)
+      cudaMemPoolTrimTo(pool, static_cast<size_t>(used) + keep);
+    cudaGetLastError();
+  }
+  return ok;
+}
 
 template <class T>
 sf_status upload(DevBuf& b, int dev, const T* host, size_t count, cudaStream_t st,
@@ -473,21 +516,20 @@ struct DeviceState {
   std::vector<int64_t> sched_off;  // per chunk: offsets of its arrays in `sched`
   // sparse-bit (unweighted) path
   DevBuf nodebits, lens_pad;
-  // intersection (unweighted) path
-  DevBuf limbs, dmask, cacc, colsum, occ, base, packed, cubtmp;
+  DevBuf cubtmp;  // scan scratch (weighted walks)
   size_t cub_bytes = 0;
-  // intersection v2 (kernel 6): permuted rows, 64-row words, group masks
-  DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, gm, nheavy;
-  // split path (kernel 10): light-row sums per slot, |S_e| per row
-  DevBuf lightsum, mcount, nzmask, ilimbs;
+  // split path (kernel 10): permuted rows, 64-row heavy words, limbs
+  DevBuf limbs, fixbit, dmask, cacc, colsum;
+  DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, nheavy;
+  // light-row sums per slot, |S_e| per row; u-walk nonzero-word masks
+  DevBuf lightsum, mcount, nzmask;
   DevBuf lcnt, lptr, lmem, lcur, lscantmp;  // banded light scatter: member CSR + cursors of the light rows
   size_t lscan_bytes = 0;
   bool banded = false;
-  // entry lists per column band (sp_light_entry_kernel)
-  DevBuf lent, linfo, kcnt;
-  std::vector<uint32_t> koff;
-  int kb_cols = 0;
-  bool entries = false;
+  // deeper fixed-point levels: deep rows, their levels, member CSR, per-slot sums
+  DevBuf drows, dfix, dcnt, dptr, dmem, dent, dcolsum, dcacc, deepsum, dscantmp;
+  size_t dscan_bytes = 0;
+  int64_t deep_entries = 0;
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
   DevBuf wnb, woff, wcnt, wpool;
   DevBuf wpoola, wA, wbase;  // kernel 12: generalized pool, column sums, pool base + chunk total
@@ -495,6 +537,7 @@ struct DeviceState {
   int32_t light_pass = 0;  // stripes per light-sum pass (memory-bounded)
   size_t sort_bytes = 0;
   std::vector<cudaEvent_t> events;
+  uint64_t launches = 0;  // kernel launches of the last run on this device
   ~DeviceState() {
     if (dev >= 0) {
       cudaSetDevice(dev);
@@ -513,9 +556,11 @@ struct sf_plan {
   int32_t n = 0, E = 0, start = 0, stop = 0;
   bool bits = false, exact = false;
   double alpha = 1.0;  // generalized UniFrac exponent
-  int kernel = 1;  // 1 dense, 2 sparse-bit walk (3/4 flattened variants), 5/6 intersection
-  int32_t scale = 0;    // intersection paths: fixed-point lengths round(L * 2^scale)
-  int32_t lo_bits = 32; // kernel 6: value = hi * 2^lo_bits + lo
+  int kernel = 1;  // 1 dense, 2 sparse-bit walk, 10 split, 11 weighted present-row walk, 12 u-walk
+  // split path: exact fixed-point levels of the lengths (fixed_levels)
+  int32_t scale = 0, lo_bits = 32, vb = 63, levels = 1;
+  std::vector<unsigned long long> fix, dfix;
+  std::vector<int32_t> deep_rows;
   int64_t row_words = 0;  // per embedding row: words (bits) or doubles (values)
   Schedule sched;
   std::vector<std::unique_ptr<DeviceState>> devs;
@@ -532,28 +577,6 @@ struct SparseCfg {
   static constexpr int TK = NWK * RK, TS = NWS * 32 * RS;
 };
 
-// Intersection kernel for the unweighted metric (kernel 5).
-struct IsectCfg {
-  static constexpr int RK = 4, RS = 2, NWK = 8, NWS = 2;
-  using T = IsectTile<RK, RS, NWK, NWS>;
-};
-
-// Intersection v2 (kernel 6): warp = one u column x 32*RS stripes.
-struct Isect2Cfg {
-  static constexpr int RS = 2, NW = 8;
-};
-// Intersection v3 (kernel 7): heavy region walked warp-uniformly.
-struct Isect3Cfg {
-  static constexpr int RS = 4, NW = 8;
-};
-// Intersection v4 (kernel 8): heavy and light regions walked warp-uniformly.
-struct Isect4Cfg {
-  static constexpr int RS = 4, NW = 8;
-};
-// Intersection v5 (kernel 9): FP64-bound heavy walk down to |X| >= 0.012 n.
-struct Isect5Cfg {
-  static constexpr int RS = 8, NW = 8;
-};
 // Split (kernel 10): heavy rows walked warp-uniformly, light rows scattered.
 // Weighted sparse walk (kernel 11).
 struct WSparseCfg {
@@ -584,7 +607,7 @@ int split_heavy_min(int n) {
 int64_t sparse_n_ext(int n) {
   // a whole stripe tile past the last stripe: the widest is the split
   // kernel's 32 * RS (RS <= 16)
-  const int64_t tile = std::max<int64_t>(std::max(SparseCfg::TK + SparseCfg::TS, IsectCfg::T::VW), 512);
+  const int64_t tile = std::max<int64_t>(SparseCfg::TK + SparseCfg::TS, 32 * SplitCfg::RS);
   const int64_t need = static_cast<int64_t>(n) + n / 2 + tile + 64;
   return (need + 3) / 4 * 4;
 }
@@ -592,24 +615,14 @@ int64_t sparse_n_ext(int n) {
 // Bytes the node-packed paths keep resident on one device (beyond stripes).
 size_t nodepacked_bytes(int kernel, int32_t E, int n) {
   const int64_t W = (E + 31) / 32;
-  const int64_t G = (W + 31) / 32;
   const int64_t n_ext = sparse_n_ext(n);
   const size_t rows = static_cast<size_t>(E) * static_cast<size_t>((n + 31) / 32) * 4;
   if (kernel == 10) {  // + the light sums, (stripes x n) x 16 B, counted by the caller with stripes
-    const int64_t W64 = (E + 63) / 64, G64 = (W64 + 31) / 32;
-    return rows + static_cast<size_t>(W64 * n_ext) * 8 + static_cast<size_t>(G64) * 2048 * 16 +
+    const int64_t W64 = (E + 63) / 64;
+    return rows + static_cast<size_t>(W64 * n_ext) * 8 + static_cast<size_t>(W64) * 64 * 24 +
            static_cast<size_t>(E) * 32 + static_cast<size_t>(n) * 32;
   }
-  if (kernel >= 6) {
-    const int64_t W64 = (E + 63) / 64, G64 = (W64 + 31) / 32;
-    return rows + 2 * static_cast<size_t>(W64 * n_ext) * 8 + static_cast<size_t>(G64 * n_ext) * 12 +
-           static_cast<size_t>(G64) * 2048 * 16 + static_cast<size_t>(E) * 32 + static_cast<size_t>(n) * 32;
-  }
-  size_t b = rows + static_cast<size_t>(W * n_ext) * 4 + static_cast<size_t>(W) * 32 * 8;
-  if (kernel == 5)
-    b += static_cast<size_t>(W * n_ext) * 4 + static_cast<size_t>(G * n_ext) * 8 +
-         static_cast<size_t>(G) * 1024 * 8 + static_cast<size_t>(n) * 32;
-  return b;
+  return rows + static_cast<size_t>(W * n_ext) * 4 + static_cast<size_t>(W) * 32 * 8;
 }
 
 int ceil_log2(int64_t v) {
@@ -618,78 +631,70 @@ int ceil_log2(int64_t v) {
   return b;
 }
 
-// Kernel 6 fixed point: value = round(L * 2^scale) = hi * 2^lo_bits + lo, with
-// both limb sums over up to E rows below 2^53 (exact in double).
-void isect2_scale(const double* lengths, int32_t E, bool fp32, int32_t* scale, int32_t* lo_bits) {
+// Exact fixed-point levels of the branch lengths (split_kernels.cuh): every
+// length L = sum_j v_j 2^-(scale + vb j) with integers v_j < 2^vb, by
+// truncation from the top level down until the remainder is zero. Limb
+// sums (hi = v >> lo_bits, lo) over up to E rows stay below 2^53, so they
+// are exact in any order. A length on the main grid (every length within
+// 2^(vb-53) of the longest, or with few significant bits) has one level.
+struct FixedLevels {
+  int32_t scale = 0, lo_bits = 32, vb = 63, levels = 1;
+  std::vector<unsigned long long> fix;   // main level, [E]
+  std::vector<int32_t> deep_rows;        // rows with a nonzero deeper level
+  std::vector<unsigned long long> dfix;  // [deep row][levels - 1]
+};
+
+sf_status fixed_levels(const double* lengths, int32_t E, bool fp32, FixedLevels& out) {
+  constexpr int kMaxLevels = 40;  // matches combine_levels (split_kernels.cuh)
   const int cl = ceil_log2(static_cast<int64_t>(E) + 1);
-  const int lb = std::min(32, 53 - cl);
-  const int vb = std::min(63, lb + (53 - cl));
+  out.lo_bits = std::min(32, 53 - cl);
+  out.vb = std::min(63, out.lo_bits + (53 - cl));
   double lmax = 0.0;
   for (int32_t r = 0; r < E; ++r) {
     const double L = fp32 ? static_cast<double>(static_cast<float>(lengths[r])) : lengths[r];
     lmax = std::max(lmax, L);
   }
-  *lo_bits = lb;
-  *scale = lmax > 0.0 ? vb - 1 - std::ilogb(lmax) : 0;
-}
-
-// Fixed-point scale for the intersection path: round(L * 2^q) < 2^63 for the
-// longest branch, so each length is two 32-bit limbs (hi < 2^31).
-int32_t isect_scale(const double* lengths, int32_t E, bool fp32) {
-  double lmax = 0.0;
+  out.scale = lmax > 0.0 ? out.vb - 1 - std::ilogb(lmax) : 0;
+  out.fix.assign(static_cast<size_t>(E), 0ull);
+  out.deep_rows.clear();
+  out.dfix.clear();
+  std::vector<std::vector<unsigned long long>> deep;  // per deep row, its levels 1..
+  int levels = 1;
   for (int32_t r = 0; r < E; ++r) {
-    const double L = fp32 ? static_cast<double>(static_cast<float>(lengths[r])) : lengths[r];
-    lmax = std::max(lmax, L);
+    double rem = fp32 ? static_cast<double>(static_cast<float>(lengths[r])) : lengths[r];
+    // level j: v = floor(rem * 2^(scale + vb j)); rem -= v * 2^-(scale + vb j).
+    // Both steps are exact: the scaled value and its floor are doubles, the
+    // truncated part has no more significant bits than rem, and rem's low
+    // bits are what the subtraction leaves.
+    const double f0 = std::floor(std::ldexp(rem, out.scale));
+    out.fix[static_cast<size_t>(r)] = static_cast<unsigned long long>(f0);
+    rem -= std::ldexp(f0, -out.scale);
+    if (rem == 0.0) continue;
+    std::vector<unsigned long long> v;
+    for (int j = 1; rem != 0.0; ++j) {
+      if (j >= kMaxLevels) return fail(SF_EINVAL, "branch lengths span too many binades for exact sums");
+      const int sc = out.scale + out.vb * j;
+      const double f = std::floor(std::ldexp(rem, sc));
+      v.push_back(static_cast<unsigned long long>(f));
+      rem -= std::ldexp(f, -sc);
+    }
+    levels = std::max(levels, 1 + static_cast<int>(v.size()));
+    out.deep_rows.push_back(r);
+    deep.push_back(std::move(v));
   }
-  if (!(lmax > 0.0)) return 0;
-  return 62 - std::ilogb(lmax);
-}
-
-sf_status isect_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
-  const int64_t W = (plan->E + 31) / 32;
-  const int64_t G = (W + 31) / 32;
-  const int64_t n_ext = sparse_n_ext(plan->n);
-  const bool fp32 = plan->prec == SF_FP32;
-  plan->scale = isect_scale(p->lengths, plan->E, fp32);
-  std::vector<uint32_t> limbs(static_cast<size_t>(G) * 1024 * 2, 0u);
-  for (int32_t r = 0; r < plan->E; ++r) {
-    const double L = fp32 ? static_cast<double>(static_cast<float>(p->lengths[r])) : p->lengths[r];
-    const uint64_t v = static_cast<uint64_t>(std::nearbyint(std::ldexp(L, plan->scale)));
-    limbs[2 * static_cast<size_t>(r)] = static_cast<uint32_t>(v >> 32);
-    limbs[2 * static_cast<size_t>(r) + 1] = static_cast<uint32_t>(v & 0xffffffffull);
-  }
-  SF_TRY(upload(d.limbs, d.dev, limbs.data(), limbs.size(), d.stream, "length limbs"));
-  SF_TRY(d.dmask.alloc(d.dev, static_cast<size_t>(W) * 4, "dense-row mask"));
-  SF_TRY(d.cacc.alloc(d.dev, 2 * sizeof(unsigned long long), "dense total"));
-  SF_TRY(d.colsum.alloc(d.dev, static_cast<size_t>(plan->n) * 4 * sizeof(unsigned long long), "column sums"));
-  const size_t cells = static_cast<size_t>(G * n_ext);
-  SF_TRY(d.occ.alloc(d.dev, cells * 4, "occupancy"));
-  SF_TRY(d.base.alloc(d.dev, (cells + 1) * 4, "packed offsets"));
-  SF_TRY(d.packed.alloc(d.dev, static_cast<size_t>(W * n_ext) * 4, "packed words"));
-  if (static_cast<uint64_t>(W * n_ext) >= (1ull << 32))
-    return fail(SF_ENOMEM, "problem too large for 32-bit packed offsets");
-  size_t tmp = 0;
-  SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
-                                        static_cast<int64_t>(cells + 1), d.stream));
-  d.cub_bytes = tmp;
-  SF_TRY(d.cubtmp.alloc(d.dev, tmp, "scan scratch"));
+  out.levels = levels;
+  out.dfix.assign(deep.size() * static_cast<size_t>(levels - 1), 0ull);
+  for (size_t i = 0; i < deep.size(); ++i)
+    std::copy(deep[i].begin(), deep[i].end(), out.dfix.begin() + static_cast<int64_t>(i) * (levels - 1));
   return SF_OK;
 }
 
-sf_status isect2_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
+// Split path (kernel 10): fixed-point levels on host, device arrays.
+sf_status split_prepare(sf_plan* plan, DeviceState& d) {
   const int64_t E = plan->E;
   const int64_t W = (E + 63) / 64;
-  const int64_t G = (W + 31) / 32;
-  const int64_t NGW = (G + 31) / 32;
   const int64_t n_ext = sparse_n_ext(plan->n);
-  const bool fp32 = plan->prec == SF_FP32;
-  isect2_scale(p->lengths, plan->E, fp32, &plan->scale, &plan->lo_bits);
-  std::vector<unsigned long long> fix(static_cast<size_t>(E));
-  for (int64_t r = 0; r < E; ++r) {
-    const double L = fp32 ? static_cast<double>(static_cast<float>(p->lengths[r])) : p->lengths[r];
-    fix[static_cast<size_t>(r)] = static_cast<unsigned long long>(std::nearbyint(std::ldexp(L, plan->scale)));
-  }
-  SF_TRY(upload(d.fix, d.dev, fix.data(), fix.size(), d.stream, "fixed-point lengths"));
+  SF_TRY(upload(d.fix, d.dev, plan->fix.data(), plan->fix.size(), d.stream, "fixed-point lengths"));
   SF_TRY(d.keys.alloc(d.dev, static_cast<size_t>(E) * 4, "row keys"));
   SF_TRY(d.keys_out.alloc(d.dev, static_cast<size_t>(E) * 4, "sorted keys"));
   SF_TRY(d.vals.alloc(d.dev, static_cast<size_t>(E) * 4, "row ids"));
@@ -697,85 +702,32 @@ sf_status isect2_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
   SF_TRY(d.dense.alloc(d.dev, static_cast<size_t>(E), "dense flags"));
   SF_TRY(d.nheavy.alloc(d.dev, 4, "heavy row count"));
   SF_TRY(d.dmask.alloc(d.dev, static_cast<size_t>(W) * 8, "dense-row mask"));
-  SF_TRY(d.limbs.alloc(d.dev, static_cast<size_t>(G) * 2048 * 16, "length limbs"));
+  SF_TRY(d.limbs.alloc(d.dev, static_cast<size_t>(W) * 64 * 16, "length limbs"));
+  SF_TRY(d.fixbit.alloc(d.dev, static_cast<size_t>(W) * 64 * 8, "fixed-point lengths by bit"));
   SF_TRY(d.cacc.alloc(d.dev, 2 * sizeof(unsigned long long), "dense total"));
   SF_TRY(d.colsum.alloc(d.dev, static_cast<size_t>(plan->n) * 4 * sizeof(unsigned long long), "column sums"));
   SF_TRY(d.nodebits.alloc(d.dev, static_cast<size_t>(W * n_ext) * 8, "node-packed X words"));
-  if (plan->kernel == 10)
-    SF_TRY(d.nzmask.alloc(d.dev, static_cast<size_t>((W + 31) / 32) * static_cast<size_t>(plan->n) * 4,
-                          "nonzero-word masks"));
-  if (plan->kernel != 10) {  // kernels 6-9 walk packed words through occupancy masks
-    const size_t cells = static_cast<size_t>(G * n_ext);
-    SF_TRY(d.occ.alloc(d.dev, cells * 4, "occupancy"));
-    SF_TRY(d.base.alloc(d.dev, (cells + 1) * 4, "packed offsets"));
-    SF_TRY(d.gm.alloc(d.dev, static_cast<size_t>(NGW * n_ext) * 4, "group masks"));
-    SF_TRY(d.packed.alloc(d.dev, static_cast<size_t>(W * n_ext) * 8, "packed words"));
-    if (static_cast<uint64_t>(W * n_ext) >= (1ull << 32))
-      return fail(SF_ENOMEM, "problem too large for 32-bit packed offsets");
-    size_t tmp = 0;
-    SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
-                                          static_cast<int64_t>(cells + 1), d.stream));
-    d.cub_bytes = tmp;
-    SF_TRY(d.cubtmp.alloc(d.dev, tmp, "scan scratch"));
-  }
   size_t stmp = 0;
   SF_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
                                           d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
-                                          0, 32, d.stream));
+                                          0, 1, d.stream));
   d.sort_bytes = stmp;
   SF_TRY(d.sorttmp.alloc(d.dev, stmp, "sort scratch"));
-  return SF_OK;
-}
-
-// Kernel 6 preparation on device: |S_e|, permutation, X words, occupancy, packing.
-sf_status isect2_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
-  const int n = plan->n;
-  const int64_t E = plan->E;
-  const int64_t W = (E + 63) / 64;
-  const int64_t G = (W + 31) / 32;
-  const int64_t NGW = (G + 31) / 32;
-  const int64_t n_ext = sparse_n_ext(n);
-  const int64_t cells = G * n_ext;
-  const int64_t stride = plan->row_words;
-  // heavy rows: |X_e| >= 0.14 n (SURVEY-style measurement at the EMP shape:
-  // this threshold minimises candidate words per slot)
-  // kernel 6: 0.14 n minimises candidate words per slot; kernel 7 walks
-  // the heavy region warp-uniformly, which pays off down to ~0.06 n
-  const double heavy_frac = plan->kernel >= 9 ? 0.012 : plan->kernel >= 7 ? 0.06 : 0.14;
-  const int heavy_min = std::max(2, static_cast<int>(heavy_frac * n));
-  SF_CUDA(cudaMemsetAsync(d.nheavy.p, 0, 4, st));
-  SF_CUDA(cudaMemsetAsync(d.dmask.p, 0, static_cast<size_t>(W) * 8, st));
-  SF_CUDA(cudaMemsetAsync(d.cacc.p, 0, 2 * sizeof(unsigned long long), st));
-  SF_CUDA(cudaMemsetAsync(d.colsum.p, 0, static_cast<size_t>(n) * 4 * sizeof(unsigned long long), st));
-  SF_CUDA(cudaMemsetAsync(d.gm.p, 0, static_cast<size_t>(NGW * n_ext) * 4, st));
-  SF_CUDA(cudaMemsetAsync(d.base.as<uint32_t>() + cells, 0, 4, st));
-  i2_row_key_kernel<<<grid_for(E * 32, 256), 256, 0, st>>>(
-      d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min, d.keys.as<uint32_t>(), d.vals.as<int32_t>(),
-      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>());
-  size_t stmp = d.sort_bytes;
-  SF_CUDA(cub::DeviceRadixSort::SortPairs(d.sorttmp.p, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
-                                          d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
-                                          0, 32, st));
-  i2_perm_kernel<<<grid_for(G * 2048, 256), 256, 0, st>>>(
-      d.perm.as<int32_t>(), plan->E, G * 2048, d.dense.as<uint8_t>(), d.fix.as<unsigned long long>(),
-      plan->lo_bits, d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.cacc.as<unsigned long long>());
-  i2_transpose_kernel<<<grid_for(W * stride * 32, 256), 256, 0, st>>>(
-      d.emb.as<uint32_t>(), stride, d.perm.as<int32_t>(), plan->E, n, static_cast<int32_t>(W),
-      d.dmask.as<unsigned long long>(), d.nodebits.as<unsigned long long>(), n_ext);
-  i2_extend_kernel<<<grid_for(W * (n_ext - n), 256), 256, 0, st>>>(
-      d.nodebits.as<unsigned long long>(), n_ext, n, static_cast<int32_t>(W));
-  i2_occ_kernel<<<grid_for(cells, 256), 256, 0, st>>>(
-      d.nodebits.as<unsigned long long>(), n_ext, n, static_cast<int32_t>(W), static_cast<int32_t>(G),
-      d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.occ.as<uint32_t>(), d.base.as<uint32_t>(),
-      d.gm.as<uint32_t>(), d.colsum.as<unsigned long long>());
-  size_t tmp = d.cub_bytes;
-  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cubtmp.p, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
-                                        cells + 1, st));
-  i2_pack_kernel<<<grid_for(cells, 256), 256, 0, st>>>(
-      d.nodebits.as<unsigned long long>(), n_ext, static_cast<int32_t>(W), static_cast<int32_t>(G),
-      d.base.as<uint32_t>(), d.packed.as<unsigned long long>());
-  SF_CUDA(cudaGetLastError());
-  plan->stats.launches += 8;  // key, sort, perm, transpose, extend, occupancy, scan, pack
+  const int R = static_cast<int>(plan->deep_rows.size());
+  if (R > 0) {
+    const int Jd = plan->levels - 1;
+    SF_TRY(upload(d.drows, d.dev, plan->deep_rows.data(), plan->deep_rows.size(), d.stream, "deep rows"));
+    SF_TRY(upload(d.dfix, d.dev, plan->dfix.data(), plan->dfix.size(), d.stream, "deep levels"));
+    SF_TRY(d.dptr.alloc(d.dev, static_cast<size_t>(R + 1) * 4, "deep member offsets"));
+    SF_TRY(d.dcnt.alloc(d.dev, static_cast<size_t>(R + 1) * 4, "deep member counts"));
+    SF_TRY(d.dcolsum.alloc(d.dev, static_cast<size_t>(Jd) * plan->n * 4 * 8, "deep column sums"));
+    SF_TRY(d.dcacc.alloc(d.dev, static_cast<size_t>(Jd) * 16, "deep dense totals"));
+    size_t tmp = 0;
+    SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, d.dcnt.as<uint32_t>(), d.dptr.as<uint32_t>(), R + 1,
+                                          d.stream));
+    d.dscan_bytes = tmp;
+    SF_TRY(d.dscantmp.alloc(d.dev, tmp, "deep scan scratch"));
+  }
   return SF_OK;
 }
 
@@ -808,77 +760,14 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
         d.fix.as<unsigned long long>(), plan->lo_bits, d.lmem.as<int32_t>(),
         d.colsum.as<unsigned long long>());
     SF_CUDA(cudaGetLastError());
-    plan->stats.launches += 3;
+    d.launches += 3;
   }
   double band_mb = 32.0;  // measured: 32 MB <= 64 MB < 96 MB (profiles/r01_ab_c3_split_band*)
-  if (const char* e = std::getenv("SF_LIGHT_BAND_MB")) band_mb = std::max(1.0, std::atof(e));
+  if (const char* e = std::getenv("SF_LIGHT_BAND_MB")) band_mb = std::max(1e-3, std::atof(e));
   const int SB = 32 * SplitCfg::RS;
   const int64_t kb = static_cast<int64_t>(band_mb * 1048576.0 / (16.0 * SB));
-  const int KB = static_cast<int>(std::max<int64_t>(256, std::min<int64_t>(kb, n)));
-  if (first) {
-    // entry lists per column band (SF_LIGHT_ENTRY=1) or warp per row (the
-    // default: measured faster at C3, profiles/r01_ab_c3_light_entry.jsonl)
-    const char* ee = std::getenv("SF_LIGHT_ENTRY");
-    d.entries = ee && std::atoi(ee) != 0;
-    const int nkb = (n + KB - 1) / KB;
-    uint32_t M = 0;
-    if (d.entries) {
-      SF_CUDA(cudaMemcpyAsync(&M, d.lptr.as<uint32_t>() + E, 4, cudaMemcpyDeviceToHost, st));
-      SF_CUDA(cudaStreamSynchronize(st));
-      d.entries = nkb <= 1024 && d.lent.alloc(d.dev, static_cast<size_t>(M) * 8, "light entries") == SF_OK &&
-                  d.linfo.alloc(d.dev, static_cast<size_t>(E) * sizeof(LightRow), "light rows") == SF_OK &&
-                  d.kcnt.alloc(d.dev, static_cast<size_t>(nkb + 1) * 4, "band counts") == SF_OK;
-      cudaGetLastError();
-    }
-    if (d.entries) {
-      d.kb_cols = KB;
-      sp_light_rowinfo_kernel<<<grid_for(E, 256), 256, 0, st>>>(
-          d.perm.as<int32_t>(), plan->E, d.nheavy.as<unsigned int>(), d.lptr.as<uint32_t>(),
-          d.fix.as<unsigned long long>(), plan->lo_bits, d.linfo.as<LightRow>());
-      SF_CUDA(cudaMemsetAsync(d.kcnt.p, 0, static_cast<size_t>(nkb + 1) * 4, st));
-      sp_entry_hist_kernel<<<grid_for(M, 256), 256, static_cast<size_t>(nkb) * 4, st>>>(
-          d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E, KB, nkb, d.kcnt.as<uint32_t>());
-      std::vector<uint32_t> cnt(static_cast<size_t>(nkb));
-      SF_CUDA(cudaMemcpyAsync(cnt.data(), d.kcnt.p, static_cast<size_t>(nkb) * 4, cudaMemcpyDeviceToHost, st));
-      SF_CUDA(cudaStreamSynchronize(st));
-      d.koff.assign(static_cast<size_t>(nkb) + 1, 0u);
-      for (int K = 0; K < nkb; ++K) d.koff[static_cast<size_t>(K) + 1] = d.koff[static_cast<size_t>(K)] + cnt[static_cast<size_t>(K)];
-      SF_CUDA(cudaMemcpyAsync(d.kcnt.p, d.koff.data(), static_cast<size_t>(nkb) * 4, cudaMemcpyHostToDevice, st));
-      sp_entry_fill_kernel<<<static_cast<int>(std::min<int64_t>((E + 7) / 8, 148 * 16)), 256, 0, st>>>(
-          d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E, d.nheavy.as<unsigned int>(), KB,
-          d.kcnt.as<uint32_t>(), d.lent.as<uint2>());
-      SF_CUDA(cudaStreamSynchronize(st));  // koff (host) is read below; kcnt was the fill cursor
-      SF_CUDA(cudaGetLastError());
-      plan->stats.launches += 3;
-    }
-  }
-  if (d.entries && d.kb_cols == KB) {
-    const int nkb = static_cast<int>(d.koff.size()) - 1;
-    for (int s0 = p0; s0 < p1; s0 += SB) {
-      const int s1 = std::min(p1, s0 + SB);
-      for (int K = 0; K < nkb; ++K) {
-        const uint32_t t0 = d.koff[static_cast<size_t>(K)], t1 = d.koff[static_cast<size_t>(K) + 1];
-        if (t1 <= t0) continue;
-        const int blocks = static_cast<int>(std::min<int64_t>((t1 - t0 + 255) / 256, 148 * 8));
-        if (s0 == p0)
-          sp_light_entry_kernel<true><<<blocks, 256, 0, st>>>(
-              d.lent.as<uint2>(), t0, t1, d.linfo.as<LightRow>(), d.lmem.as<int32_t>(), d.lcur.as<uint32_t>(), n,
-              p0, s0, s1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>());
-        else
-          sp_light_entry_kernel<false><<<blocks, 256, 0, st>>>(
-              d.lent.as<uint2>(), t0, t1, d.linfo.as<LightRow>(), d.lmem.as<int32_t>(), d.lcur.as<uint32_t>(), n,
-              p0, s0, s1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>());
-        plan->stats.launches++;
-      }
-    }
-    SF_CUDA(cudaGetLastError());
-    return SF_OK;
-  }
+  const int KB = static_cast<int>(std::max<int64_t>(std::min<int64_t>(256, n), std::min<int64_t>(kb, n)));
   const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
-  // SF_LIGHT_DRYRUN=1: everything but the atomics (cost split for A/B only;
-  // the results are then wrong)
-  const char* dr = std::getenv("SF_LIGHT_DRYRUN");
-  const int dry = dr && std::atoi(dr) != 0 ? 1 : 0;
   auto* kfirst = sp_light_band_kernel<NW, true>;
   auto* knext = sp_light_band_kernel<NW, false>;
   SF_CUDA(cudaFuncSetAttribute(kfirst, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -892,11 +781,51 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
                                           d.lptr.as<uint32_t>(), d.lmem.as<int32_t>(), d.lcur.as<uint16_t>(),
                                           d.fix.as<unsigned long long>(), plan->lo_bits, p0, s0, s1, k0,
                                           std::min(n, k0 + KB), d.lightsum.as<unsigned long long>(),
-                                          d.exec_ctr.as<unsigned long long>(), heavy_min, dry);
-      plan->stats.launches++;
+                                          d.exec_ctr.as<unsigned long long>(), heavy_min);
+      d.launches++;
     }
   }
   SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+// Deeper fixed-point levels: member lists of the deep rows (first pass) and
+// their pair sums for stripes [s0, s1) into d.deepsum.
+sf_status split_scatter_deep(sf_plan* plan, DeviceState& d, cudaStream_t st, int s0, int s1, bool first) {
+  const int R = static_cast<int>(plan->deep_rows.size());
+  if (R == 0) return SF_OK;
+  const int n = plan->n;
+  const int J = plan->levels;
+  if (first) {
+    SF_CUDA(cudaMemsetAsync(d.dcolsum.p, 0, d.dcolsum.bytes, st));
+    SF_CUDA(cudaMemsetAsync(d.dcacc.p, 0, d.dcacc.bytes, st));
+    sp_deep_count_kernel<<<grid_for(R + 1, 256), 256, 0, st>>>(d.drows.as<int32_t>(), R, n, d.mcount.as<int32_t>(),
+                                                                 d.dcnt.as<uint32_t>());
+    size_t tmp = d.dscan_bytes;
+    SF_CUDA(cub::DeviceScan::ExclusiveSum(d.dscantmp.p, tmp, d.dcnt.as<uint32_t>(), d.dptr.as<uint32_t>(), R + 1,
+                                          st));
+    uint32_t M = 0;
+    SF_CUDA(cudaMemcpyAsync(&M, d.dptr.as<uint32_t>() + R, 4, cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaStreamSynchronize(st));
+    d.deep_entries = M;
+    if (d.dmem.bytes < static_cast<size_t>(M) * 4 + 4) {
+      SF_TRY(d.dmem.alloc(d.dev, static_cast<size_t>(M) * 4 + 4, "deep members"));
+      SF_TRY(d.dent.alloc(d.dev, static_cast<size_t>(M) * 4 + 4, "deep member rows"));
+    }
+    sp_deep_members_kernel<<<grid_for(static_cast<int64_t>(R) * 32, 256), 256, 0, st>>>(
+        d.emb.as<uint32_t>(), plan->row_words, n, d.drows.as<int32_t>(), R, d.mcount.as<int32_t>(),
+        d.dptr.as<uint32_t>(), d.dfix.as<unsigned long long>(), J, plan->lo_bits, d.dmem.as<int32_t>(),
+        d.dent.as<uint32_t>(), d.dcolsum.as<unsigned long long>(), d.dcacc.as<unsigned long long>());
+    SF_CUDA(cudaGetLastError());
+    d.launches += 3;
+  }
+  if (d.deep_entries > 0) {
+    sp_deep_scatter_kernel<<<grid_for(d.deep_entries, 256), 256, 0, st>>>(
+        d.dptr.as<uint32_t>(), d.dmem.as<int32_t>(), d.dent.as<uint32_t>(), d.deep_entries,
+        d.dfix.as<unsigned long long>(), J, plan->lo_bits, n, s0, s1, d.deepsum.as<unsigned long long>());
+    SF_CUDA(cudaGetLastError());
+    d.launches++;
+  }
   return SF_OK;
 }
 
@@ -904,7 +833,10 @@ sf_status split_scatter(sf_plan* plan, DeviceState& d, cudaStream_t st, int s0, 
   const int n = plan->n;
   const int64_t E = plan->E;
   const int heavy_min = split_heavy_min(n);
-  SF_CUDA(cudaMemsetAsync(d.lightsum.p, 0, static_cast<size_t>(s1 - s0) * static_cast<size_t>(n) * 16, st));
+  const size_t cells = static_cast<size_t>(s1 - s0) * static_cast<size_t>(n);
+  SF_CUDA(cudaMemsetAsync(d.lightsum.p, 0, cells * 16, st));
+  if (plan->levels > 1) SF_CUDA(cudaMemsetAsync(d.deepsum.p, 0, cells * 16 * (plan->levels - 1), st));
+  SF_TRY(split_scatter_deep(plan, d, st, s0, s1, with_colsum));
   if (d.banded) return split_scatter_banded(plan, d, st, s0, s1, with_colsum);
   constexpr int NW = SplitCfg::SCATTER_NW;
   const size_t smem = static_cast<size_t>(NW) * static_cast<size_t>(heavy_min) * 4;
@@ -918,7 +850,7 @@ sf_status split_scatter(sf_plan* plan, DeviceState& d, cudaStream_t st, int s0, 
                                      with_colsum ? d.colsum.as<unsigned long long>() : nullptr,
                                      d.exec_ctr.as<unsigned long long>(), heavy_min);
   SF_CUDA(cudaGetLastError());
-  plan->stats.launches++;
+  d.launches++;
   return SF_OK;
 }
 
@@ -926,7 +858,6 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   const int n = plan->n;
   const int64_t E = plan->E;
   const int64_t W = (E + 63) / 64;
-  const int64_t G = (W + 31) / 32;
   const int64_t n_ext = sparse_n_ext(n);
   const int64_t stride = plan->row_words;
   const int heavy_min = split_heavy_min(n);
@@ -934,17 +865,17 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   SF_CUDA(cudaMemsetAsync(d.cacc.p, 0, 2 * sizeof(unsigned long long), st));
   SF_CUDA(cudaMemsetAsync(d.colsum.p, 0, static_cast<size_t>(n) * 4 * sizeof(unsigned long long), st));
   SF_CUDA(cudaMemsetAsync(d.nheavy.p, 0, 4, st));
-  i2_row_key_kernel<<<grid_for(E * 32, 256), 256, 0, st>>>(
+  sp_row_key_kernel<<<grid_for(E * 32, 256), 256, 0, st>>>(
       d.emb.as<uint32_t>(), stride, plan->E, n, heavy_min, d.keys.as<uint32_t>(), d.vals.as<int32_t>(),
-      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>(),
-      std::getenv("SF_HEAVY_BY_WEIGHT") == nullptr);
+      d.dense.as<uint8_t>(), d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>());
   size_t stmp = d.sort_bytes;
   SF_CUDA(cub::DeviceRadixSort::SortPairs(d.sorttmp.p, stmp, d.keys.as<uint32_t>(), d.keys_out.as<uint32_t>(),
                                           d.vals.as<int32_t>(), d.perm.as<int32_t>(), static_cast<int>(E),
-                                          0, 32, st));
-  i2_perm_kernel<<<grid_for(G * 2048, 256), 256, 0, st>>>(
-      d.perm.as<int32_t>(), plan->E, G * 2048, d.dense.as<uint8_t>(), d.fix.as<unsigned long long>(),
-      plan->lo_bits, d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.cacc.as<unsigned long long>());
+                                          0, 1, st));
+  sp_perm_kernel<<<grid_for(W * 64, 256), 256, 0, st>>>(
+      d.perm.as<int32_t>(), plan->E, W * 64, d.dense.as<uint8_t>(), d.fix.as<unsigned long long>(),
+      plan->lo_bits, d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.fixbit.as<unsigned long long>(),
+      d.cacc.as<unsigned long long>());
   sp_transpose_kernel<<<grid_for(W * stride * 32, 256), 256, 0, st>>>(
       d.emb.as<uint32_t>(), stride, d.perm.as<int32_t>(), d.nheavy.as<unsigned int>(), n,
       d.dmask.as<unsigned long long>(), d.nodebits.as<unsigned long long>(), n_ext);
@@ -952,132 +883,22 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
       d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>());
   sp_heavy_colsum_kernel<<<grid_for(n, 128), 128, 0, st>>>(
       d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>(),
-      d.dmask.as<unsigned long long>(), d.limbs.as<double2>(), d.colsum.as<unsigned long long>());
-  sp_nzmask_kernel<<<grid_for(((W + 31) / 32) * n, 256), 256, 0, st>>>(
-      d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>(), d.nzmask.as<uint32_t>());
+      d.dmask.as<unsigned long long>(), d.fixbit.as<unsigned long long>(), plan->lo_bits,
+      d.colsum.as<unsigned long long>());
+  SF_CUDA(cudaGetLastError());
+  d.launches += 7;  // key, sort, perm, transpose, extend, colsum (+ memsets)
   // first light pass (the one that also adds the light rows' column sums)
-  SF_TRY(split_scatter(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), true));
-  SF_CUDA(cudaGetLastError());
-  plan->stats.launches += 7;  // key, sort, perm, transpose, extend, colsum (+ memsets)
-  return SF_OK;
+  return split_scatter(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), true);
 }
 
-template <class Real, int RS, int NW, bool BITMAJOR = false, bool UPREF = false, bool HALVES = false,
-          int MINB = 1, bool LIST = false, bool PREF = false, bool PIPE = false>
-sf_status launch_split_rs(const SplitArgs& a, cudaStream_t st) {
-  auto* kern = stripe_split_kernel<Real, RS, NW, BITMAJOR, UPREF, HALVES, MINB, LIST, PREF, PIPE>;
-  const dim3 grid((a.n + NW - 1) / NW, (a.s_end - a.s_begin + 32 * RS - 1) / (32 * RS));
-  kern<<<grid, 32 * NW, 0, st>>>(a);
-  SF_CUDA(cudaGetLastError());
-  return SF_OK;
-}
-
-// Default: 16 slots per lane, 8 u columns per CTA, v words loaded one 32-bit
-// half at a time (measured best at the EMP shape: profiles/r01_ab_c3_split_variants*),
-// and at most 128 registers so two CTAs (16 warps) fit per SM: left alone,
-// ptxas drifts to 152 with small source changes, halving occupancy (+37% time).
-// SF_SPLIT_VARIANT selects the measured alternatives for A/B.
+// 16 slots per lane, 8 u columns per CTA, v words loaded one 32-bit half at
+// a time, at most 128 registers so two CTAs (16 warps) fit per SM.
 template <class Real>
 sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
-  const char* v = std::getenv("SF_SPLIT_VARIANT");
-  const int var = v ? std::atoi(v) : 0;
-  switch (var) {
-    case 1: return launch_split_rs<Real, 16, 4>(a, st);               // 64-bit v words, 4 warps
-    case 2: return launch_split_rs<Real, 16, 4, false, true>(a, st);  // + u word prefetch
-    case 3: return launch_split_rs<Real, 8, 8>(a, st);                // 8 slots per lane
-    case 4: return launch_split_rs<Real, 16, 4, false, false, true>(a, st);
-    case 6: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2, true, true>(a, st);
-    case 7: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2, true, false>(a, st);
-    case 8: return launch_split_rs<Real, 8, 8, false, false, true, 3>(a, st);    // 24 warps/SM
-    case 9: return launch_split_rs<Real, 12, 4, false, false, true, 5>(a, st);   // 20 warps/SM
-    case 10: return launch_split_rs<Real, 16, 4, false, false, true, 4>(a, st);  // 16 warps, 4-warp CTAs
-    case 11: return launch_split_rs<Real, 12, 8, false, false, false, 2>(a, st);  // both v halves at once
-    case 12: return launch_split_rs<Real, 14, 8, false, false, false, 2>(a, st);
-    case 13: return launch_split_rs<Real, 12, 8, false, true, false, 2>(a, st);   // + u prefetch
-    case 14: return launch_split_rs<Real, 8, 8, false, false, false, 2, false, false, true>(a, st);   // pipelined words
-    case 15: return launch_split_rs<Real, 10, 8, false, false, false, 2, false, false, true>(a, st);
-    default: return launch_split_rs<Real, SplitCfg::RS, SplitCfg::NW, false, false, true, 2>(a, st);
-  }
-}
-
-template <class Real>
-sf_status launch_isect5(const Isect2Args& a, unsigned long long* fp_ops, cudaStream_t st) {
-  using C = Isect5Cfg;
-  auto* kern = stripe_isect5_kernel<Real, C::RS, C::NW>;
-  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
-  kern<<<grid, 32 * C::NW, 0, st>>>(a, fp_ops);
+  constexpr int RS = SplitCfg::RS, NW = SplitCfg::NW;
+  const dim3 grid((a.n + NW - 1) / NW, (a.s_end - a.s_begin + 32 * RS - 1) / (32 * RS));
+  stripe_split_kernel<Real, RS, NW, 2><<<grid, 32 * NW, 0, st>>>(a);
   SF_CUDA(cudaGetLastError());
-  return SF_OK;
-}
-
-template <class Real>
-sf_status launch_isect4(const Isect2Args& a, cudaStream_t st) {
-  using C = Isect4Cfg;
-  auto* kern = stripe_isect4_kernel<Real, C::RS, C::NW>;
-  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
-  kern<<<grid, 32 * C::NW, 0, st>>>(a);
-  SF_CUDA(cudaGetLastError());
-  return SF_OK;
-}
-
-template <class Real>
-sf_status launch_isect3(const Isect2Args& a, cudaStream_t st) {
-  using C = Isect3Cfg;
-  auto* kern = stripe_isect3_kernel<Real, C::RS, C::NW>;
-  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
-  kern<<<grid, 32 * C::NW, 0, st>>>(a);
-  SF_CUDA(cudaGetLastError());
-  return SF_OK;
-}
-
-template <class Real>
-sf_status launch_isect2(const Isect2Args& a, cudaStream_t st) {
-  using C = Isect2Cfg;
-  auto* kern = stripe_isect2_kernel<Real, C::RS, C::NW>;
-  const dim3 grid((a.n + C::NW - 1) / C::NW, (a.s_end - a.s_begin + 32 * C::RS - 1) / (32 * C::RS));
-  kern<<<grid, 32 * C::NW, 0, st>>>(a);
-  SF_CUDA(cudaGetLastError());
-  return SF_OK;
-}
-
-template <class Real>
-sf_status launch_isect(const IsectArgs& a, cudaStream_t st) {
-  using C = IsectCfg;
-  using T = C::T;
-  auto* kern = stripe_isect_kernel<Real, C::RK, C::RS, C::NWK, C::NWS>;
-  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES));
-  const dim3 grid((a.n + T::TK - 1) / T::TK, (a.s_end - a.s_begin + T::TS - 1) / T::TS);
-  kern<<<grid, T::NT, T::BYTES, st>>>(a);
-  SF_CUDA(cudaGetLastError());
-  return SF_OK;
-}
-
-// Intersection-path preparation on device: dense mask, occupancy, packing.
-sf_status isect_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
-  const int n = plan->n;
-  const int64_t W = (plan->E + 31) / 32;
-  const int64_t G = (W + 31) / 32;
-  const int64_t n_ext = sparse_n_ext(n);
-  const int64_t cells = G * n_ext;
-  SF_CUDA(cudaMemsetAsync(d.dmask.p, 0, static_cast<size_t>(W) * 4, st));
-  SF_CUDA(cudaMemsetAsync(d.cacc.p, 0, 2 * sizeof(unsigned long long), st));
-  SF_CUDA(cudaMemsetAsync(d.colsum.p, 0, static_cast<size_t>(n) * 4 * sizeof(unsigned long long), st));
-  SF_CUDA(cudaMemsetAsync(d.base.as<uint32_t>() + cells, 0, 4, st));
-  isect_row_count_kernel<<<grid_for(static_cast<int64_t>(plan->E) * 32, 256), 256, 0, st>>>(
-      d.emb.as<uint32_t>(), plan->row_words, plan->E, n, d.limbs.as<uint2>(), d.dmask.as<uint32_t>(),
-      d.cacc.as<unsigned long long>());
-  isect_occ_kernel<<<grid_for(cells, 256), 256, 0, st>>>(
-      d.nodebits.as<uint32_t>(), n_ext, n, static_cast<int32_t>(W), static_cast<int32_t>(G),
-      d.dmask.as<uint32_t>(), d.limbs.as<uint2>(), d.occ.as<uint32_t>(), d.base.as<uint32_t>(),
-      d.colsum.as<unsigned long long>());
-  size_t tmp = d.cub_bytes;
-  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cubtmp.p, tmp, d.base.as<uint32_t>(), d.base.as<uint32_t>(),
-                                        cells + 1, st));
-  isect_pack_kernel<<<grid_for(cells, 256), 256, 0, st>>>(
-      d.nodebits.as<uint32_t>(), n_ext, static_cast<int32_t>(W), static_cast<int32_t>(G),
-      d.dmask.as<uint32_t>(), d.base.as<uint32_t>(), d.packed.as<uint32_t>());
-  SF_CUDA(cudaGetLastError());
-  plan->stats.launches += 4;  // row count, occupancy, pack, + the scan's own kernels (>= 1)
   return SF_OK;
 }
 
@@ -1096,18 +917,6 @@ sf_status sparse_prepare(sf_plan* plan, DeviceState& d, const sf_problem* p) {
   std::vector<double> lens(static_cast<size_t>(W * 32), 0.0);
   std::copy(p->lengths, p->lengths + plan->E, lens.begin());
   SF_TRY(upload(d.lens_pad, d.dev, lens.data(), lens.size(), d.stream, "padded lengths"));
-  return SF_OK;
-}
-
-template <class Real, int WCH>
-sf_status launch_sparse_flat(const SparseArgs& a, cudaStream_t st) {
-  using C = SparseCfg;
-  using T = FlatTile<C::RK, C::RS, C::NWK, C::NWS, WCH>;
-  auto* kern = stripe_sparse_flat_kernel<Real, C::RK, C::RS, C::NWK, C::NWS, WCH>;
-  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::BYTES));
-  const dim3 grid((a.n + C::TK - 1) / C::TK, (a.s_end - a.s_begin + C::TS - 1) / C::TS);
-  kern<<<grid, T::NT, T::BYTES, st>>>(a);
-  SF_CUDA(cudaGetLastError());
   return SF_OK;
 }
 
@@ -1169,7 +978,7 @@ sf_status wsparse_build(sf_plan* plan, DeviceState& d, int32_t C, cudaStream_t s
   ws_extend_kernel<<<grid_for(static_cast<int64_t>(Wc) * (n_ext - n), 256), 256, 0, st>>>(
       d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n, Wc, n_ext);
   SF_CUDA(cudaGetLastError());
-  plan->stats.launches += 4;
+  d.launches += 4;
   return SF_OK;
 }
 
@@ -1233,7 +1042,7 @@ sf_status wuwalk_build(sf_plan* plan, DeviceState& d, int32_t r0, int32_t C, cud
   wu_advance_base_kernel<<<1, 1, 0, st>>>(base, base + 1);
   ws_extend_kernel<<<grid_for(static_cast<int64_t>(Wc) * (n_ext - n), 256), 256, 0, st>>>(nb, off, n, Wc, n_ext);
   SF_CUDA(cudaGetLastError());
-  plan->stats.launches += 6;
+  d.launches += 6;
   return SF_OK;
 }
 
@@ -1321,7 +1130,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
                                                   d.sidx.as<int32_t>(), d.counts.as<double>(),
                                                   d.totals.as<double>());
       SF_CUDA(cudaGetLastError());
-      plan->stats.launches++;
+      d.launches++;
     }
     for (size_t h = 0; h + 1 < c.lvl_ptr.size(); ++h) {
       const int lo = c.lvl_ptr[h], hi = c.lvl_ptr[h + 1];
@@ -1336,7 +1145,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
                                                  arr(kIntRows) + lo, arr(kCptr) + lo, arr(kCodes),
                                                  hi - lo, ncols);
       SF_CUDA(cudaGetLastError());
-      plan->stats.launches++;
+      d.launches++;
     }
     if (plan->kernel == 12) {
       if (ci == 0) SF_CUDA(cudaMemsetAsync(d.wbase.p, 0, 16, st));
@@ -1345,9 +1154,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       SF_TRY(wsparse_build(plan, d, C, st));
     } else if (plan->kernel == 10) {
       SF_TRY(split_build(plan, d, st));
-    } else if (plan->kernel >= 6) {
-      SF_TRY(isect2_build(plan, d, st));
-    } else if (plan->kernel >= 2) {
+    } else if (plan->kernel == 2) {
       // node-packed presence bits for the sparse walk
       const int64_t W = (plan->E + 31) / 32;
       const int64_t n_ext = sparse_n_ext(n);
@@ -1357,8 +1164,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       extend_columns_kernel<<<grid_for(W * (n_ext - n), 256), 256, 0, st>>>(
           d.nodebits.as<uint32_t>(), n_ext, n, static_cast<int32_t>(W));
       SF_CUDA(cudaGetLastError());
-      plan->stats.launches += 2;
-      if (plan->kernel == 5) SF_TRY(isect_build(plan, d, st));
+      d.launches += 2;
     }
     SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
     // ---- K2: stripe update over the chunk's rows
@@ -1423,7 +1229,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         a.exec_updates = d.exec_ctr.as<unsigned long long>();
         SF_TRY(plan->prec == SF_FP64 ? launch_wuwalk<double>(plan->metric, a, st)
                                      : launch_wuwalk<float>(plan->metric, a, st));
-        plan->stats.launches++;
+        d.launches++;
         const int S = n / 2;
         if (n % 2 == 0 && S - 1 >= d.a && S - 1 < d.b) {  // duplicated half stripe
           const int64_t row_off = static_cast<int64_t>(S - 1 - d.a) * n;
@@ -1432,10 +1238,10 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
           else
             wu_mirror_kernel<float><<<grid_for(S, 256), 256, 0, st>>>(d.dist.as<float>(), a.tot ? d.tot.as<float>() : nullptr, n, row_off);
           SF_CUDA(cudaGetLastError());
-          plan->stats.launches++;
+          d.launches++;
         }
       } else {
-        plan->stats.launches--;  // nothing launched for this chunk
+        d.launches--;  // nothing launched for this chunk
       }
     } else if (plan->kernel == 11) {
       WSparseArgs a;
@@ -1472,18 +1278,11 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       a.dist = d.dist.p;
       a.tot = d.tot.p;
       a.counters = d.exec_ctr.as<unsigned long long>();
-      a.nz = d.nzmask.as<uint32_t>();
-      // A/B: integer-limb heavy walk (IMAD.WIDE instead of DFMA)
-      const char* sv = std::getenv("SF_SPLIT_VARIANT");
-      const bool int_walk = sv && std::atoi(sv) == 16;
-      if (int_walk) {
-        const int64_t cnt = ((plan->E + 63) / 64 + 31) / 32 * 2048;
-        if (d.ilimbs.bytes < static_cast<size_t>(cnt) * 8)
-          SF_TRY(d.ilimbs.alloc(d.dev, static_cast<size_t>(cnt) * 8, "integer limbs"));
-        sp_ilimbs_kernel<<<grid_for(cnt, 256), 256, 0, st>>>(d.limbs.as<double2>(), cnt, plan->lo_bits,
-                                                              d.ilimbs.as<uint2>());
-        SF_CUDA(cudaGetLastError());
-      }
+      a.levels = plan->levels;
+      a.vb = plan->vb;
+      a.dacc = plan->levels > 1 ? d.deepsum.as<unsigned long long>() : nullptr;
+      a.dcolsum = plan->levels > 1 ? d.dcolsum.as<unsigned long long>() : nullptr;
+      a.dcacc = plan->levels > 1 ? d.dcacc.as<unsigned long long>() : nullptr;
       // light-sum passes (one unless memory is short); within a pass, with a
       // host destination, chunks of whole 512-stripe tiles whose D2H copy
       // overlaps the next chunk's compute
@@ -1502,20 +1301,17 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
           const int c1 = std::min(p1, c0 + step);
           a.s_begin = c0;
           a.s_end = c1;
-          if (int_walk) {
-            const dim3 grid((a.n + SplitCfg::NW - 1) / SplitCfg::NW,
-                            (a.s_end - a.s_begin + 32 * SplitCfg::RS - 1) / (32 * SplitCfg::RS));
+          SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+          if (plan->levels > 1) {  // lengths off the main grid: exact multi-level epilogue
+            const int blocks = grid_for(static_cast<int64_t>(c1 - c0) * n, 256);
             if (plan->prec == SF_FP64)
-              stripe_split_int_kernel<double, SplitCfg::RS, SplitCfg::NW, 2><<<grid, 32 * SplitCfg::NW, 0, st>>>(
-                  a, d.ilimbs.as<uint2>());
+              sp_deep_epilogue_kernel<double><<<blocks, 256, 0, st>>>(a);
             else
-              stripe_split_int_kernel<float, SplitCfg::RS, SplitCfg::NW, 2><<<grid, 32 * SplitCfg::NW, 0, st>>>(
-                  a, d.ilimbs.as<uint2>());
+              sp_deep_epilogue_kernel<float><<<blocks, 256, 0, st>>>(a);
             SF_CUDA(cudaGetLastError());
-          } else {
-            SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+            d.launches++;
           }
-          plan->stats.launches++;
+          d.launches++;
           if (!host_d) continue;
           while (static_cast<int>(d.chunk_events.size()) <= ci) {
             cudaEvent_t e;
@@ -1537,61 +1333,8 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
                                     cudaMemcpyDeviceToHost, d.copy_stream));
         }
       }
-      plan->stats.launches--;  // counted once more below
-    } else if (plan->kernel >= 6) {
-      Isect2Args a;
-      const int64_t W = (plan->E + 63) / 64;
-      a.W = static_cast<int32_t>(W);
-      a.nx = d.nodebits.as<unsigned long long>();
-      a.n_heavy = d.nheavy.as<unsigned int>();
-      a.G = static_cast<int32_t>((W + 31) / 32);
-      a.NGW = (a.G + 31) / 32;
-      a.occ = d.occ.as<uint32_t>();
-      a.base = d.base.as<uint32_t>();
-      a.packed = d.packed.as<unsigned long long>();
-      a.limbs = d.limbs.as<double2>();
-      a.gm = d.gm.as<uint32_t>();
-      a.colsum = d.colsum.as<unsigned long long>();
-      a.cacc = d.cacc.as<unsigned long long>();
-      a.n_ext = sparse_n_ext(n);
-      a.n = n;
-      a.s_begin = d.a;
-      a.s_end = d.b;
-      a.lo_bits = plan->lo_bits;
-      a.scale = plan->scale;
-      a.finalize = finalize ? 1 : 0;
-      a.dist = d.dist.p;
-      a.tot = d.tot.p;
-      a.exec_updates = d.exec_ctr.as<unsigned long long>();
-      if (plan->kernel == 9)
-        SF_TRY(plan->prec == SF_FP64 ? launch_isect5<double>(a, d.exec_ctr.as<unsigned long long>() + 1, st)
-                                     : launch_isect5<float>(a, d.exec_ctr.as<unsigned long long>() + 1, st));
-      else if (plan->kernel == 8)
-        SF_TRY(plan->prec == SF_FP64 ? launch_isect4<double>(a, st) : launch_isect4<float>(a, st));
-      else if (plan->kernel == 7)
-        SF_TRY(plan->prec == SF_FP64 ? launch_isect3<double>(a, st) : launch_isect3<float>(a, st));
-      else
-        SF_TRY(plan->prec == SF_FP64 ? launch_isect2<double>(a, st) : launch_isect2<float>(a, st));
-    } else if (plan->kernel == 5) {
-      IsectArgs a;
-      a.occ = d.occ.as<uint32_t>();
-      a.base = d.base.as<uint32_t>();
-      a.packed = d.packed.as<uint32_t>();
-      a.limbs = d.limbs.as<uint2>();
-      a.colsum = d.colsum.as<unsigned long long>();
-      a.cacc = d.cacc.as<unsigned long long>();
-      a.n_ext = sparse_n_ext(n);
-      a.G = static_cast<int32_t>(((plan->E + 31) / 32 + 31) / 32);
-      a.n = n;
-      a.s_begin = d.a;
-      a.s_end = d.b;
-      a.scale = plan->scale;
-      a.finalize = finalize ? 1 : 0;
-      a.dist = d.dist.p;
-      a.tot = d.tot.p;
-      a.exec_updates = d.exec_ctr.as<unsigned long long>();
-      SF_TRY(plan->prec == SF_FP64 ? launch_isect<double>(a, st) : launch_isect<float>(a, st));
-    } else if (plan->kernel >= 2) {
+      d.launches--;  // counted once more below
+    } else if (plan->kernel == 2) {
       SparseArgs a;
       a.nb = d.nodebits.as<uint32_t>();
       a.n_ext = sparse_n_ext(n);
@@ -1603,16 +1346,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       a.dist = d.dist.p;
       a.tot = d.tot.p;
       a.exec_updates = d.exec_ctr.as<unsigned long long>();
-      sf_status kst;
-      if (plan->kernel == 3)
-        kst = plan->prec == SF_FP64 ? launch_sparse_flat<double, 32>(a, st)
-                                    : launch_sparse_flat<float, 32>(a, st);
-      else if (plan->kernel == 4)
-        kst = plan->prec == SF_FP64 ? launch_sparse_flat<double, 64>(a, st)
-                                    : launch_sparse_flat<float, 64>(a, st);
-      else
-        kst = plan->prec == SF_FP64 ? launch_sparse<double>(a, st) : launch_sparse<float>(a, st);
-      SF_TRY(kst);
+      SF_TRY(plan->prec == SF_FP64 ? launch_sparse<double>(a, st) : launch_sparse<float>(a, st));
     } else {
       StripeArgs a;
       a.emb = d.emb.p;
@@ -1628,7 +1362,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       SF_TRY(launch_stripes(plan->metric, plan->prec, plan->bits ? kSrcBits : kSrcF64,
                             plan->exact, a, st));
     }
-    plan->stats.launches++;
+    d.launches++;
     SF_CUDA(cudaEventRecord(d.events[3 + 3 * ci], st));
     const int ncarry = static_cast<int>(c.carry_src.size());
     if (ncarry > 0) {
@@ -1641,21 +1375,43 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         embed_carry<double><<<grid, 128, 0, st>>>(d.emb.as<double>(), d.pend.as<double>(), stride,
                                                   arr(kCarrySrc), arr(kCarryDst), ncarry, ncols);
       SF_CUDA(cudaGetLastError());
-      plan->stats.launches++;
+      d.launches++;
     }
   }
   const size_t ne = d.events.size();
   SF_CUDA(cudaEventRecord(d.events[ne - 2], st));
-  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED && (plan->kernel < 5 || plan->kernel == 11)) {
+  if (finalize && plan->metric != SF_WEIGHTED_UNNORMALIZED && (plan->kernel <= 2 || plan->kernel == 11)) {
     const int blocks = grid_for(slots, 256);
     if (plan->prec == SF_FP64)
       finalize_kernel<double><<<blocks, 256, 0, st>>>(d.dist.as<double>(), d.tot.as<double>(), slots);
     else
       finalize_kernel<float><<<blocks, 256, 0, st>>>(d.dist.as<float>(), d.tot.as<float>(), slots);
     SF_CUDA(cudaGetLastError());
-    plan->stats.launches++;
+    d.launches++;
   }
   SF_CUDA(cudaEventRecord(d.events[ne - 1], st));
+  return SF_OK;
+}
+
+// fn(DeviceState&) for every device of the plan, one host thread per device
+// when there are several (their enqueues, synchronous steps and host copies
+// then overlap); the first failure's status and message are returned on the
+// calling thread (sf_last_error is thread-local).
+template <class F>
+sf_status for_each_device(sf_plan* plan, F&& fn) {
+  const size_t G = plan->devs.size();
+  if (G == 1) return fn(*plan->devs[0]);
+  std::vector<sf_status> st(G, SF_OK);
+  std::vector<std::string> err(G);
+  std::vector<std::thread> th;
+  for (size_t i = 0; i < G; ++i)
+    th.emplace_back([&, i] {
+      st[i] = fn(*plan->devs[i]);
+      if (st[i] != SF_OK) err[i] = sf::last_error();
+    });
+  for (auto& t : th) t.join();
+  for (size_t i = 0; i < G; ++i)
+    if (st[i] != SF_OK) return fail(st[i], err[i]);
   return SF_OK;
 }
 
@@ -1678,6 +1434,20 @@ int32_t sf_device_count(void) {
     if (cudaGetDeviceProperties(&prop, i) == cudaSuccess && prop.major == 10) ++ok;
   }
   return ok;
+}
+
+sf_status sf_trim_memory(int32_t device) {
+  sf_exec ex{};
+  ex.n_devices = 1;
+  ex.devices = &device;
+  std::vector<int> devs;
+  SF_TRY(usable_devices(&ex, devs));
+  if (cudaMemPool_t pool = device_pool(device)) {
+    SF_CUDA(cudaSetDevice(device));
+    SF_CUDA(cudaDeviceSynchronize());
+    SF_CUDA(cudaMemPoolTrimTo(pool, 0));
+  }
+  return SF_OK;
 }
 
 sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision prec, int32_t start,
@@ -1717,7 +1487,11 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stop = stop;
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
-  plan->kernel = (ex && ex->kernel >= 2 && ex->kernel <= 12) ? ex->kernel : 1;
+  if (ex && ex->kernel != 0 && ex->kernel != 1 && ex->kernel != 2 && ex->kernel != 10 && ex->kernel != 11 &&
+      ex->kernel != 12)
+    return fail(SF_EINVAL, "unknown kernel " + std::to_string(ex->kernel) +
+                               " (1 dense, 2 sparse walk, 10 split, 11 weighted walk, 12 u-walk)");
+  plan->kernel = (ex && ex->kernel >= 2) ? ex->kernel : 1;
   const int n = p->n_samples;
   // auto, unweighted: the intersection kernel (exact fixed-point sums), or
   // with SF_EXEC_EXACT_NO_FMA the sparse walk (the reference's adds in the
@@ -1732,8 +1506,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   // auto, weighted: the sparse walk over present rows (kernel 11)
   // (the u-walk, kernel 12; in exact mode the bitwise present-row walk, 11)
   if ((!ex || ex->kernel == 0) && metric != SF_UNWEIGHTED) plan->kernel = plan->exact ? 11 : 12;
-  if (plan->kernel >= 2 && plan->kernel <= 10 && metric != SF_UNWEIGHTED)
-    return fail(SF_EINVAL, "the sparse bit kernel implements the unweighted metric only");
+  if ((plan->kernel == 2 || plan->kernel == 10) && metric != SF_UNWEIGHTED)
+    return fail(SF_EINVAL, "the sparse bit kernels implement the unweighted metric only");
   if (plan->kernel >= 11 && metric == SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the weighted sparse walk implements the weighted metrics only");
   if (metric == SF_GENERALIZED && plan->kernel < 11)
@@ -1788,9 +1562,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       // it plus the fixed part (with the 4/3 margin below) succeeds; the
       // memory returns to the pool. cudaMemGetInfo stalls up to ~100 ms.
       const size_t whole = static_cast<size_t>(plan->E) * (row_bytes + wsp_row_bytes);
-      DevBuf probe;
       if (whole / 3 < (SIZE_MAX - fixed_b) / 4 &&
-          probe.alloc(d->dev, fixed_b + whole + whole / 3, "fit probe") == SF_OK) {
+          probe_fits(d->dev, fixed_b + whole + whole / 3, fixed_b - (512ull << 20) + whole)) {
         budget = std::min(budget, whole);
         continue;
       }
@@ -1861,6 +1634,18 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   for (size_t i = 0; i < up_status.size(); ++i)
     if (up_status[i] != SF_OK) return fail(up_status[i], up_error[i]);
   phase("upload table (overlapped)");
+  if (plan->kernel == 10) {
+    FixedLevels fl;
+    SF_TRY(fixed_levels(p->lengths, plan->E, prec == SF_FP32, fl));
+    plan->scale = fl.scale;
+    plan->lo_bits = fl.lo_bits;
+    plan->vb = fl.vb;
+    plan->levels = fl.levels;
+    plan->fix = std::move(fl.fix);
+    plan->deep_rows = std::move(fl.deep_rows);
+    plan->dfix = std::move(fl.dfix);
+    phase("fixed-point levels");
+  }
   for (auto& dp : plan->devs) {
     DeviceState& d = *dp;
     SF_CUDA(cudaSetDevice(d.dev));
@@ -1902,15 +1687,16 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       SF_TRY(upload_schedule(d, plan->sched));
       SF_TRY(d.emb.alloc(d.dev, static_cast<size_t>(plan->E) * row_bytes, "embedding rows"));
       SF_TRY(d.pend.alloc(d.dev, 16, "pending rows"));
-      if (plan->kernel >= 6) {
+      if (plan->kernel == 10) {
         phase("device alloc");
-        SF_TRY(isect2_prepare(plan.get(), d, p));
+        SF_TRY(split_prepare(plan.get(), d));
         phase("node-packed prepare");
-        if (plan->kernel == 10) {
+        {
           // light sums for the whole range if they fit next to everything
           // else, else for passes of whole 512-stripe tiles
           size_t freeb = 0;
-          const size_t per_stripe = static_cast<size_t>(n) * 16;
+          // light sums (hi, lo) and the deeper levels' pair sums per slot
+          const size_t per_stripe = static_cast<size_t>(n) * 16 * static_cast<size_t>(plan->levels);
           const size_t reserve = (1ull << 30);
           const int span = d.b - d.a;
           // without a budget, a probe allocation of the whole range plus the
@@ -1919,17 +1705,18 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
           // stalls up to ~100 ms on some calls (p99 63 ms on the box).
           size_t fit = 0;
           bool probed = false;
+          // the light member lists and cursors allocated after the light sums
+          const size_t after = static_cast<size_t>(plan->E) * 4 * (3 + 2 * static_cast<size_t>(split_heavy_min(n)));
           if (!(ex && ex->mem_budget_bytes > 0) && !std::getenv("SF_LIGHT_PASS")) {
-            const size_t after = static_cast<size_t>(plan->E) * 4 * (3 + 2 * static_cast<size_t>(split_heavy_min(n)));
-            DevBuf probe;
-            if (probe.alloc(d.dev, static_cast<size_t>(span) * per_stripe + after + reserve, "fit probe") == SF_OK) {
+            const size_t need = static_cast<size_t>(span) * per_stripe + after;
+            if (probe_fits(d.dev, need + reserve, need)) {
               fit = static_cast<size_t>(span);
               probed = true;
             }
           }
           if (!probed) {
             SF_TRY(device_free_bytes(d.dev, &freeb));
-            fit = freeb > reserve ? (freeb - reserve) / per_stripe : 0;
+            fit = freeb > reserve + after ? (freeb - reserve - after) / per_stripe : 0;
           }
           if (ex && ex->mem_budget_bytes > 0)
             fit = std::min(fit, static_cast<size_t>(ex->mem_budget_bytes) / per_stripe);
@@ -1938,9 +1725,13 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
           if (const char* e = std::getenv("SF_LIGHT_PASS")) pass = std::max(1, std::atoi(e));  // tests
           d.light_pass = std::min(pass, span);
           if (std::getenv("SF_DEBUG"))
-            std::fprintf(stderr, "stripefrac: device %d stripes [%d,%d): light pass %d stripes (free %zu MB)\n",
-                         d.dev, d.a, d.b, d.light_pass, freeb >> 20);
-          SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * per_stripe, "light-row sums"));
+            std::fprintf(stderr, "stripefrac: device %d stripes [%d,%d): light pass %d stripes (%s)\n",
+                         d.dev, d.a, d.b, d.light_pass,
+                         probed ? "probe fit" : ("free " + std::to_string(freeb >> 20) + " MB").c_str());
+          SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * n * 16, "light-row sums"));
+          if (plan->levels > 1)
+            SF_TRY(d.deepsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * n * 16 * (plan->levels - 1),
+                                   "deep-level sums"));
           SF_TRY(d.mcount.alloc(d.dev, static_cast<size_t>(plan->E) * 4, "row presence counts"));
           // u32 member offsets; u16 cursors (light rows have < heavy_min members)
           d.banded = light_banded() &&
@@ -1964,7 +1755,6 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
         }
       } else {
         SF_TRY(sparse_prepare(plan.get(), d, p));
-        if (plan->kernel == 5) SF_TRY(isect_prepare(plan.get(), d, p));
       }
     } else {
       SF_TRY(upload_schedule(d, plan->sched));
@@ -1980,8 +1770,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
 
 sf_status sf_plan_run(sf_plan* plan, int32_t finalize) {
   if (!plan) return fail(SF_EINVAL, "plan is null");
-  plan->stats.launches = 0;
-  for (auto& d : plan->devs) SF_TRY(run_device(plan, *d, finalize));
+  for (auto& d : plan->devs) d->launches = 0;
+  SF_TRY(for_each_device(plan, [&](DeviceState& d) { return run_device(plan, d, finalize); }));
   plan->ran = true;
   plan->finalized = finalize != 0;
   return SF_OK;
@@ -2020,6 +1810,8 @@ sf_status sf_plan_sync(sf_plan* plan) {
     exec += c[0];
     fpops += c[1];
   }
+  plan->stats.launches = 0;
+  for (auto& dp : plan->devs) plan->stats.launches += dp->launches;
   plan->stats.embed_ms = emb;
   plan->stats.stripe_ms = str;
   plan->stats.finalize_ms = fin;
@@ -2052,15 +1844,15 @@ struct PinnedStaging {
   char* slot[2] = {nullptr, nullptr};
   size_t bytes = 0;
 };
-PinnedStaging& staging() {
-  static PinnedStaging s;  // freed at process exit by the driver
-  return s;
+// one double buffer per device, so several devices download in parallel
+PinnedStaging& staging(int device) {
+  static PinnedStaging s[64];  // freed at process exit by the driver
+  return s[device & 63];
 }
 
-void parallel_memcpy(char* dst, const char* src, size_t bytes) {
+void parallel_memcpy(char* dst, const char* src, size_t bytes, unsigned max_threads) {
   const size_t min_piece = 8ull << 20;
-  unsigned hw = std::thread::hardware_concurrency();
-  size_t T = std::min<size_t>(std::max(1u, std::min(hw, 16u)), std::max<size_t>(1, bytes / min_piece));
+  size_t T = std::min<size_t>(std::max(1u, max_threads), std::max<size_t>(1, bytes / min_piece));
   if (T <= 1) {
     std::memcpy(dst, src, bytes);
     return;
@@ -2076,10 +1868,17 @@ void parallel_memcpy(char* dst, const char* src, size_t bytes) {
   for (auto& t : th) t.join();
 }
 
-// dsrc (device memory of the current device) -> hdst (pageable host), on cs.
-sf_status staged_d2h(cudaStream_t cs, const char* dsrc, char* hdst, size_t bytes) {
+// Host threads for the pinned -> pageable copies of one of `ndev` devices
+// downloading at once.
+unsigned copy_threads(size_t ndev) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  return std::max(1u, std::min(16u, hw / static_cast<unsigned>(std::max<size_t>(1, ndev))));
+}
+
+// dsrc (memory of `device`, the current device) -> hdst (pageable host), on cs.
+sf_status staged_d2h(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t bytes, unsigned threads) {
   if (bytes == 0) return SF_OK;
-  PinnedStaging& S = staging();
+  PinnedStaging& S = staging(device);
   std::lock_guard<std::mutex> lock(S.mu);
   constexpr size_t kSlot = 128ull << 20;
   if (!S.slot[0]) {
@@ -2122,7 +1921,7 @@ sf_status staged_d2h(cudaStream_t cs, const char* dsrc, char* hdst, size_t bytes
       break;
     }
     const size_t o = b * S.bytes;
-    parallel_memcpy(hdst + o, S.slot[b & 1], std::min(S.bytes, bytes - o));
+    parallel_memcpy(hdst + o, S.slot[b & 1], std::min(S.bytes, bytes - o), threads);
   }
   cudaStreamSynchronize(cs);
   cudaEventDestroy(ev[0]);
@@ -2139,31 +1938,28 @@ sf_status sf_plan_download(sf_plan* plan, void* dist_out, void* tot_out) {
   const size_t w = plan->prec == SF_FP64 ? 8 : 4;
   const bool pageable_d = !host_pinned(dist_out);
   const bool pageable_t = tot_out && !host_pinned(tot_out);
-  for (auto& dp : plan->devs) {
-    DeviceState& d = *dp;
+  const unsigned threads = copy_threads(plan->devs.size());
+  return for_each_device(plan, [&](DeviceState& d) -> sf_status {
     SF_CUDA(cudaSetDevice(d.dev));
     const size_t off = static_cast<size_t>(d.a - plan->start) * plan->n * w;
     const size_t bytes = static_cast<size_t>(d.b - d.a) * plan->n * w;
     if (pageable_d) {
       SF_CUDA(cudaStreamSynchronize(d.stream));
-      SF_TRY(staged_d2h(d.stream, d.dist.as<char>(), static_cast<char*>(dist_out) + off, bytes));
+      SF_TRY(staged_d2h(d.dev, d.stream, d.dist.as<char>(), static_cast<char*>(dist_out) + off, bytes, threads));
     } else {
       SF_CUDA(cudaMemcpyAsync(static_cast<char*>(dist_out) + off, d.dist.p, bytes, cudaMemcpyDeviceToHost, d.stream));
     }
     if (has_t && tot_out) {
       if (pageable_t) {
         SF_CUDA(cudaStreamSynchronize(d.stream));
-        SF_TRY(staged_d2h(d.stream, d.tot.as<char>(), static_cast<char*>(tot_out) + off, bytes));
+        SF_TRY(staged_d2h(d.dev, d.stream, d.tot.as<char>(), static_cast<char*>(tot_out) + off, bytes, threads));
       } else {
         SF_CUDA(cudaMemcpyAsync(static_cast<char*>(tot_out) + off, d.tot.p, bytes, cudaMemcpyDeviceToHost, d.stream));
       }
     }
-  }
-  for (auto& dp : plan->devs) {
-    SF_CUDA(cudaSetDevice(dp->dev));
-    SF_CUDA(cudaStreamSynchronize(dp->stream));
-  }
-  return SF_OK;
+    SF_CUDA(cudaStreamSynchronize(d.stream));
+    return SF_OK;
+  });
 }
 
 sf_status sf_plan_stats(const sf_plan* plan, sf_stats* out) {
@@ -2189,44 +1985,33 @@ sf_status sf_compute_stripes(const sf_problem* p, sf_metric metric, sf_precision
     std::fprintf(stderr, "stripefrac: plan_create %.1f ms\n",
                  std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
   const bool all_pinned = host_pinned(dist_out) && (!tot_out || host_pinned(tot_out));
-  if (plan->kernel == 10 && !all_pinned) {
-    // pageable destinations: chunk events only, then each finished chunk is
-    // staged through pinned memory while the later chunks compute
+  if (plan->kernel == 10) {
+    // the split kernel computes the stripes in chunks; each finished chunk is
+    // copied while the later chunks compute: pinned destinations straight
+    // from a copy stream, pageable ones staged through the device's pinned
+    // double buffer by host threads. One host thread per device.
     const size_t w = prec == SF_FP64 ? 8 : 4;
-    plan->stats.launches = 0;
-    for (auto& dp : plan->devs) {
-      const size_t off = static_cast<size_t>(dp->a - plan->start) * plan->n * w;
-      dp->chunk_spans.clear();
-      dp->defer_copy = true;
-      const sf_status rc = run_device(plan, *dp, finalize, static_cast<char*>(dist_out) + off,
-                                      tot_out ? static_cast<char*>(tot_out) + off : nullptr);
-      dp->defer_copy = false;
-      SF_TRY(rc);
-    }
-    for (auto& dp : plan->devs) {
-      DeviceState& d = *dp;
+    const unsigned threads = copy_threads(plan->devs.size());
+    for (auto& d : plan->devs) d->launches = 0;
+    SF_TRY(for_each_device(plan, [&](DeviceState& d) -> sf_status {
       SF_CUDA(cudaSetDevice(d.dev));
       const size_t off = static_cast<size_t>(d.a - plan->start) * plan->n * w;
+      char* hd = static_cast<char*>(dist_out) + off;
+      char* ht = tot_out ? static_cast<char*>(tot_out) + off : nullptr;
+      d.chunk_spans.clear();
+      d.defer_copy = !all_pinned;
+      const sf_status rc = run_device(plan, d, finalize, hd, ht);
+      d.defer_copy = false;
+      SF_TRY(rc);
       for (size_t ci = 0; ci < d.chunk_spans.size(); ++ci) {
         SF_CUDA(cudaEventSynchronize(d.chunk_events[ci]));
         const size_t co = d.chunk_spans[ci].first, cb = d.chunk_spans[ci].second;
-        SF_TRY(staged_d2h(d.copy_stream, d.dist.as<char>() + co, static_cast<char*>(dist_out) + off + co, cb));
-        if (tot_out && metric != SF_WEIGHTED_UNNORMALIZED)
-          SF_TRY(staged_d2h(d.copy_stream, d.tot.as<char>() + co, static_cast<char*>(tot_out) + off + co, cb));
+        SF_TRY(staged_d2h(d.dev, d.copy_stream, d.dist.as<char>() + co, hd + co, cb, threads));
+        if (ht && metric != SF_WEIGHTED_UNNORMALIZED)
+          SF_TRY(staged_d2h(d.dev, d.copy_stream, d.tot.as<char>() + co, ht + co, cb, threads));
       }
-    }
-    plan->ran = true;
-    plan->finalized = finalize != 0;
-    SF_TRY(sf_plan_sync(plan));
-  } else if (plan->kernel == 10) {
-    // download overlapped with the split kernel, chunk by chunk
-    const size_t w = prec == SF_FP64 ? 8 : 4;
-    plan->stats.launches = 0;
-    for (auto& dp : plan->devs) {
-      const size_t off = static_cast<size_t>(dp->a - plan->start) * plan->n * w;
-      SF_TRY(run_device(plan, *dp, finalize, static_cast<char*>(dist_out) + off,
-                        static_cast<char*>(tot_out) + off));
-    }
+      return SF_OK;
+    }));
     plan->ran = true;
     plan->finalized = finalize != 0;
     SF_TRY(sf_plan_sync(plan));
@@ -2401,6 +2186,79 @@ sf_status sf_condense(sf_precision prec, int32_t n, int32_t start, int32_t stop,
   SF_CUDA(cudaMemcpy(&bad, dbad.p, sizeof(int), cudaMemcpyDeviceToHost));
   if (bad) return fail(SF_EINVAL, "condense: duplicated slot disagrees");
   SF_CUDA(cudaMemcpy(out, dout.p, nn * 8, cudaMemcpyDeviceToHost));
+  return SF_OK;
+}
+
+// ---------------------------------------------------------------- condense
+// condense (stripes.cpp:68-129) of a finalized full-range plan, on device:
+// every device's stripe block is condensed into one n x n fp64 matrix on the
+// plan's first device (other devices' blocks cross NVLink with a peer copy),
+// the diagonal is zeroed, the even-n duplicate copies are verified, and the
+// matrix is copied once into the caller's row-major n x n buffer (pinned:
+// one async copy; pageable: staged through the device's pinned double buffer).
+sf_status sf_plan_condense(sf_plan* plan, double* out) {
+  if (!plan || !out) return fail(SF_EINVAL, "null argument");
+  if (!plan->ran) return fail(SF_ESTATE, "plan has not run");
+  if (!plan->finalized) return fail(SF_EINVAL, "condense needs finalized stripes");
+  const int n = plan->n;
+  if (plan->start != 0 || plan->stop != n / 2)
+    return fail(SF_EINVAL, "stripe parts do not tile [0, " + std::to_string(n / 2) + ")");
+  SF_TRY(sf_plan_sync(plan));
+  DeviceState& d0 = *plan->devs.front();
+  SF_CUDA(cudaSetDevice(d0.dev));
+  const cudaStream_t st = d0.stream;
+  const size_t w = plan->prec == SF_FP64 ? 8 : 4;
+  const size_t nn = static_cast<size_t>(n) * static_cast<size_t>(n);
+  DevBuf mat, bad, peer;
+  SF_TRY(mat.alloc(d0.dev, nn * 8, "distance matrix"));
+  SF_TRY(bad.alloc(d0.dev, sizeof(int), "condense flag"));
+  SF_CUDA(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
+  for (auto& dp : plan->devs) {
+    const DeviceState& d = *dp;
+    const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
+    const void* src = d.dist.p;
+    if (d.dev != d0.dev) {  // the block crosses to the first device
+      if (peer.bytes < slots * w) SF_TRY(peer.alloc(d0.dev, slots * w, "peer stripes"));
+      SF_CUDA(cudaMemcpyPeerAsync(peer.p, d0.dev, d.dist.p, d.dev, slots * w, st));
+      src = peer.p;
+    }
+    const int blocks = grid_for(static_cast<int64_t>(slots), 256);
+    if (plan->prec == SF_FP64)
+      condense_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double*>(src), n, d.a, d.b,
+                                                      mat.as<double>(), bad.as<int>());
+    else
+      condense_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float*>(src), n, d.a, d.b,
+                                                     mat.as<double>(), bad.as<int>());
+    SF_CUDA(cudaGetLastError());
+    if (d.dev != d0.dev) SF_CUDA(cudaStreamSynchronize(st));  // the peer buffer is reused
+  }
+  diagonal_zero_kernel<<<grid_for(n, 256), 256, 0, st>>>(mat.as<double>(), n);
+  SF_CUDA(cudaGetLastError());
+  int flag = 0;
+  SF_CUDA(cudaMemcpyAsync(&flag, bad.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  if (flag) return fail(SF_EINVAL, "condense: duplicated slot disagrees");
+  if (host_pinned(out)) {
+    SF_CUDA(cudaMemcpyAsync(out, mat.p, nn * 8, cudaMemcpyDeviceToHost, st));
+    SF_CUDA(cudaStreamSynchronize(st));
+  } else {
+    SF_TRY(staged_d2h(d0.dev, st, mat.as<char>(), reinterpret_cast<char*>(out), nn * 8, copy_threads(1)));
+  }
+  return SF_OK;
+}
+
+// compute_distance_matrix (kernels.hpp:319-326): full-range plan, finalize,
+// condense on device, one copy of the n x n matrix to the caller.
+sf_status sf_compute_distance_matrix(const sf_problem* p, sf_metric metric, sf_precision prec, double* out,
+                                     const sf_exec* ex, sf_stats* stats_out) {
+  if (!out) return fail(SF_EINVAL, "out is null");
+  if (!p) return fail(SF_EINVAL, "problem is null");
+  sf_plan* plan = nullptr;
+  SF_TRY(sf_plan_create(p, metric, prec, 0, -1, ex, &plan));
+  std::unique_ptr<sf_plan> guard(plan);
+  SF_TRY(sf_plan_run(plan, 1));
+  SF_TRY(sf_plan_condense(plan, out));
+  if (stats_out) *stats_out = plan->stats;
   return SF_OK;
 }
 
@@ -2594,16 +2452,34 @@ sf_status sf_plan_write_strf(sf_plan* plan, const char* path) {
     char* p;
     ~HostGuard() { cudaFreeHost(p); }
   } hguard{stage};
-  cudaEvent_t ev[2];
-  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-  SF_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  // one event pair per device: an event must be recorded on a stream of the
+  // device it was created on (chunks of several devices alternate buffers)
+  struct DevEvents {
+    int dev = -1;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+  };
+  std::vector<DevEvents> evs(plan->devs.size());
   struct EventGuard {
-    cudaEvent_t* e;
+    std::vector<DevEvents>& e;
     ~EventGuard() {
-      cudaEventDestroy(e[0]);
-      cudaEventDestroy(e[1]);
+      for (auto& x : e)
+        for (auto ev : x.ev)
+          if (ev) {
+            cudaSetDevice(x.dev);
+            cudaEventDestroy(ev);
+          }
     }
-  } eguard{ev};
+  } eguard{evs};
+  for (size_t i = 0; i < plan->devs.size(); ++i) {
+    evs[i].dev = plan->devs[i]->dev;
+    SF_CUDA(cudaSetDevice(evs[i].dev));
+    for (auto& ev : evs[i].ev) SF_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
+  auto dev_index = [&](const DeviceState* d) {
+    for (size_t i = 0; i < plan->devs.size(); ++i)
+      if (plan->devs[i].get() == d) return i;
+    return size_t{0};
+  };
   // flatten into chunks, issue chunk i+1 before consuming chunk i
   struct Chunk {
     DeviceState* d;
@@ -2613,17 +2489,18 @@ sf_status sf_plan_write_strf(sf_plan* plan, const char* path) {
   std::vector<Chunk> chunks;
   for (const Block& b : blocks)
     for (size_t off = 0; off < b.bytes; off += CH) chunks.push_back({b.d, b.src + off, std::min(CH, b.bytes - off)});
+  auto event_of = [&](size_t i) { return evs[dev_index(chunks[i].d)].ev[i & 1]; };
   auto issue = [&](size_t i) -> sf_status {
     const Chunk& c = chunks[i];
     SF_CUDA(cudaSetDevice(c.d->dev));
     SF_CUDA(cudaMemcpyAsync(stage + (i & 1) * CH, c.src, c.len, cudaMemcpyDeviceToHost, c.d->stream));
-    SF_CUDA(cudaEventRecord(ev[i & 1], c.d->stream));
+    SF_CUDA(cudaEventRecord(event_of(i), c.d->stream));
     return SF_OK;
   };
   uint64_t h = 0xcbf29ce484222325ull;
   if (!chunks.empty()) SF_TRY(issue(0));
   for (size_t i = 0; i < chunks.size(); ++i) {
-    SF_CUDA(cudaEventSynchronize(ev[i & 1]));
+    SF_CUDA(cudaEventSynchronize(event_of(i)));
     if (i + 1 < chunks.size()) SF_TRY(issue(i + 1));  // other buffer: free since chunk i-1 was consumed
     const unsigned char* p = reinterpret_cast<const unsigned char*>(stage + (i & 1) * CH);
     for (size_t k = 0; k < chunks[i].len; ++k) {

@@ -230,175 +230,5 @@ __global__ void __launch_bounds__(32 * NWK * NWS, 2) stripe_sparse_kernel(const 
   }
 }
 
-// Flattened variant: one loop trip per present row. A lane walks its RK x RS
-// slots one after the other (accumulators of the inactive slots parked in
-// shared memory, [slot][thread] so the parking is conflict-free); fetching
-// the next word and switching to the next slot are short branches inside the
-// same loop, so lanes at different words / slots still issue the row step
-// together instead of waiting for each other at nested-loop exits.
-template <int RK, int RS, int NWK, int NWS, int WCH>
-struct FlatTile {
-  static constexpr int NW = NWK * NWS;
-  static constexpr int NT = 32 * NW;
-  static constexpr int TK = NWK * RK;
-  static constexpr int TS = NWS * 32 * RS;
-  static constexpr int VW = TK + TS;
-  static constexpr int WC = WCH;            // words per chunk
-  static constexpr int NS = RK * RS;        // slots per thread
-  static constexpr int USTR = TK + 1;
-  static constexpr int LSTR = 33;
-  static constexpr int OFF_L = 0;
-  static constexpr int OFF_ACC = OFF_L + WC * LSTR * 8;
-  static constexpr int OFF_U = OFF_ACC + NS * NT * 16;
-  static constexpr int OFF_V = OFF_U + WC * USTR * 4;
-  static constexpr int OFF_OU = OFF_V + WC * VW * 4;
-  static constexpr int OFF_OV = OFF_OU + TK * 8;
-  static constexpr int BYTES = OFF_OV + VW * 8;
-  static_assert(VW % 32 == 0, "v window must be a multiple of 32 columns (bank mapping)");
-  static_assert(TK + VW <= NT, "one staging thread per column");
-  static_assert(WC == 32 || WC == 64, "occupancy masks are 32 or 64 bits");
-};
-
-template <int WC>
-struct OccT;
-template <>
-struct OccT<32> {
-  using type = uint32_t;
-  static __device__ __forceinline__ int lead(uint32_t x) { return __clz(x); }
-  static __device__ __forceinline__ uint32_t bit(int w) { return 0x80000000u >> w; }
-};
-template <>
-struct OccT<64> {
-  using type = unsigned long long;
-  static __device__ __forceinline__ int lead(unsigned long long x) { return __clzll(x); }
-  static __device__ __forceinline__ unsigned long long bit(int w) { return 0x8000000000000000ull >> w; }
-};
-
-template <class Real, int RK, int RS, int NWK, int NWS, int WCH>
-__global__ void __launch_bounds__(32 * NWK * NWS, 1) stripe_sparse_flat_kernel(const SparseArgs a) {
-  using T = FlatTile<RK, RS, NWK, NWS, WCH>;
-  using O = OccT<WCH>;
-  using occ_t = typename O::type;
-  extern __shared__ __align__(16) unsigned char smem[];
-  const double* sL = reinterpret_cast<const double*>(smem + T::OFF_L);
-  Real* sAcc = reinterpret_cast<Real*>(smem + T::OFF_ACC);  // [2*NS][NT]
-  uint32_t* sU = reinterpret_cast<uint32_t*>(smem + T::OFF_U);
-  uint32_t* sV = reinterpret_cast<uint32_t*>(smem + T::OFF_V);
-  occ_t* occU = reinterpret_cast<occ_t*>(smem + T::OFF_OU);
-  occ_t* occV = reinterpret_cast<occ_t*>(smem + T::OFF_OV);
-
-  const int tid = threadIdx.x;
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
-  const int wk = warp % NWK;
-  const int ws = warp / NWK;
-  const int n = a.n;
-  const int k0 = blockIdx.x * T::TK;
-  const int s0 = a.s_begin + blockIdx.y * T::TS;
-  const int64_t P0 = static_cast<int64_t>(k0) + s0 + 1;
-  Real* dist = static_cast<Real*>(a.dist);
-  Real* tot = static_cast<Real*>(a.tot);
-
-  // slot r = j*RS + i: sample k0 + wk*RK + j, stripe s0 + ws*32*RS + lane + 32*i
-  uint32_t valid = 0u;
-  for (int r = 0; r < T::NS; ++r) {
-    const int j = r / RS, i = r % RS;
-    const int k = k0 + wk * RK + j;
-    const int s = s0 + ws * 32 * RS + lane + 32 * i;
-    const bool ok = k < n && s < a.s_end;
-    const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
-    sAcc[(2 * r) * T::NT + tid] = ok ? dist[off] : Real(0);
-    sAcc[(2 * r + 1) * T::NT + tid] = ok ? tot[off] : Real(0);
-    valid |= (ok ? 1u : 0u) << r;
-  }
-  unsigned long long executed = 0;
-
-  for (int w0 = 0; w0 < a.W; w0 += T::WC) {
-    const int wc = min(T::WC, a.W - w0);
-    __syncthreads();
-    if (tid < T::TK + T::VW) {
-      const bool is_u = tid < T::TK;
-      const int col = is_u ? tid : tid - T::TK;
-      const int64_t gcol = is_u ? static_cast<int64_t>(k0) + col : P0 + col;
-      const uint32_t* src = a.nb + static_cast<int64_t>(w0) * a.n_ext + gcol;
-      occ_t occ = 0;
-#pragma unroll 8
-      for (int w = 0; w < T::WC; ++w) {
-        const uint32_t v = w < wc ? __ldg(src + static_cast<int64_t>(w) * a.n_ext) : 0u;
-        if (v) occ |= O::bit(w);
-        if (is_u)
-          sU[w * T::USTR + col] = v;
-        else
-          sV[w * T::VW + col] = v;
-      }
-      if (is_u)
-        occU[col] = occ;
-      else
-        occV[col] = occ;
-    } else {
-      double* sLw = reinterpret_cast<double*>(smem + T::OFF_L);
-      for (int e = tid - (T::TK + T::VW); e < T::WC * 32; e += T::NT - (T::TK + T::VW)) {
-        const int w = e >> 5, rr = e & 31;
-        sLw[w * T::LSTR + rr] = w < wc ? a.lens[static_cast<int64_t>(w0 + w) * 32 + rr] : 0.0;
-      }
-    }
-    __syncthreads();
-
-    int r = -1;  // current slot
-    occ_t occ = 0;
-    uint32_t o = 0u, x = 0u;
-    const uint32_t* pu = sU;
-    const uint32_t* pv = sV;
-    const double* Lw = sL;
-    Real d = Real(0), t = Real(0);
-    for (;;) {
-      if (o == 0u) {
-        if (occ == 0) {  // slot done for this chunk: park it, take the next
-          if (r >= 0) {
-            sAcc[(2 * r) * T::NT + tid] = d;
-            sAcc[(2 * r + 1) * T::NT + tid] = t;
-          }
-          if (++r >= T::NS) break;
-          const int cu = wk * RK + r / RS;
-          const int cv = cu + ws * 32 * RS + lane + 32 * (r % RS);
-          pu = sU + cu;
-          pv = sV + cv;
-          occ = (valid >> r) & 1u ? (occU[cu] | occV[cv]) : occ_t(0);
-          d = sAcc[(2 * r) * T::NT + tid];
-          t = sAcc[(2 * r + 1) * T::NT + tid];
-          continue;
-        }
-        const int w = O::lead(occ);  // next nonzero word of the slot
-        occ ^= O::bit(w);
-        const uint32_t u = pu[w * T::USTR];
-        const uint32_t v = pv[w * T::VW];
-        o = u | v;
-        x = u ^ v;
-        Lw = sL + w * T::LSTR;
-        executed += __popc(o);
-      }
-      const int rr = __clz(o);  // lowest present row: row 32w+rr at bit 31-rr
-      const uint32_t m = 0x80000000u >> rr;
-      o ^= m;
-      const Real L = static_cast<Real>(Lw[rr]);
-      t += L;
-      if (x & m) d += L;
-    }
-  }
-  __syncthreads();
-  for (int r = 0; r < T::NS; ++r) {
-    if (!((valid >> r) & 1u)) continue;
-    const int j = r / RS, i = r % RS;
-    const int k = k0 + wk * RK + j;
-    const int s = s0 + ws * 32 * RS + lane + 32 * i;
-    const int64_t off = static_cast<int64_t>(s - a.s_begin) * n + k;
-    dist[off] = sAcc[(2 * r) * T::NT + tid];
-    tot[off] = sAcc[(2 * r + 1) * T::NT + tid];
-  }
-  if (a.exec_updates) {
-    for (int off = 16; off > 0; off >>= 1) executed += __shfl_down_sync(0xffffffffu, executed, off);
-    if (lane == 0) atomicAdd(a.exec_updates, executed);
-  }
-}
 
 }  // namespace sf

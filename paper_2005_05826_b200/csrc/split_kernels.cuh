@@ -1,43 +1,133 @@
 // K2-UW, split form (kernel 10, the default for the unweighted metric).
 //
-// Same exact algebra as isect_kernels.cuh: with X_e = S_e, or its complement
-// when |S_e| > n/2, and fixed-point lengths (hi, lo limbs),
+// update_entry<Unweighted> (kernels.hpp:55-66) summed over the rows gives
+// t_kl = sum_{k in S_e or l in S_e} L_e and d_kl = sum_{k in S_e xor l in S_e} L_e.
+// With X_e = S_e, or its complement when |S_e| > n/2 ("dense" rows),
 //   t_kl = p_k + p_l + C - G_kl,   d_kl = x_k + x_l - 2 G_kl,
-//   G_kl = sum_{e: k in X_e and l in X_e} L_e.
-// The rows are split by |X_e| at heavy_min (~0.01 n):
+//   G_kl = sum_{e: k in X_e and l in X_e} L_e,
+// x_k / p_k per-column sums (p: non-dense rows only), C the dense rows' sum.
 //
-//  * HEAVY rows (|X_e| >= heavy_min, ~15% of rows at the EMP shape, ~99% of
-//    the shared rows): permuted to the front, node-packed in 64-row X-words
-//    nx[w][c]. A warp owns one u column k and 32*RS consecutive v columns;
-//    it walks the bits of its u words (uniform control flow) and every lane
-//    adds the row's limbs into each of its RS slots whose v word has that bit,
-//    as DFMA with a 0/1 factor: 2 FP64 instructions per u bit per slot, no
-//    divergence. The walk is FP64-pipe bound by construction.
-//  * LIGHT rows (|X_e| < heavy_min): a slot shares only ~5-10 of them, but
-//    finding them by walking per slot costs far more than they carry. They are
-//    scattered instead: the light rows' member lists are compacted once and
-//    each member pair's slot gets the row's limbs with u64 atomics, band by
-//    band (L2-resident blocks). Every value added is an integer below 2^53
-//    and so is every partial sum, so the atomics are exact and the result
-//    does not depend on their order.
+// EXACT ARITHMETIC. Every length is an exact sum of fixed-point levels,
+// L = sum_j v_j 2^-(scale + vb j), v_j < 2^vb integers (truncation, so every
+// level is non-negative; the host splits each double until the remainder is
+// zero: a length on the main grid has one level, a short branch far below
+// the longest one may need two or more). Each level is an integer problem:
+// its limbs (hi = v >> lo_bits, lo) sum below 2^53 over all rows, so every
+// partial sum is exact in any order, and the epilogue assembles the exact
+// rational value of t and d and rounds it once. The result is the correctly
+// rounded exact sum for ANY double lengths.
 //
-// The heavy kernel's epilogue adds the light sums and forms t, d (and d/t).
+//  * HEAVY rows (|X_e| >= heavy_min, ~15% of the rows and ~99% of the shared
+//    rows at the EMP shape) are permuted to the front and node-packed in
+//    64-row words nx[w][c]. A warp owns one u column k and 32*RS v columns;
+//    it walks the set bits of its u words warp-uniformly and every lane adds
+//    the row's main-level limbs to each of its slots whose v word has the bit.
+//    The 0/1 factor is the AND of the v word and the bit mask itself, read as
+//    the high word of a double (low word 0): 2^b for bit b is a power of two
+//    (subnormal for b < 20), so fma(L * 2^-e_b, f, acc) adds L exactly or
+//    adds +0. Per (u bit, slot): one LOP3 + 2 DFMA (the limbs are stored
+//    pre-scaled by 2^-e_b). Bit 31 (the sign bit) goes through a shifted
+//    factor of 2.0.
+//  * LIGHT rows (|X_e| < heavy_min) share only ~5-10 rows per slot. Their
+//    member lists are compacted once; each member pair's slot gets the row's
+//    limbs with u64 atomics, band by band (L2-resident blocks).
+//  * DEEP levels (lengths that are not on the main grid): their rows' member
+//    lists are compacted and every member pair gets the deeper levels' limbs
+//    with u64 atomics into a per-slot, per-level accumulator (typically no
+//    row at all: synthetic lengths are multiples of 2^-52).
+//
+// The heavy kernel's epilogue adds the light (and deep) sums, forms t, d in
+// exact integers and applies finalize (kernels.hpp:251-259).
 #pragma once
 
 #include <cstdint>
 
-#include "isect2_kernels.cuh"
+#include "bits.cuh"
 
 namespace sf {
 
-// (hi, lo) limbs of fixed-point length v, as exactly representable doubles.
-__device__ __forceinline__ double2 limbs_of(unsigned long long v, int lo_bits) {
-  return make_double2(static_cast<double>(v >> lo_bits),
-                      static_cast<double>(v & ((1ull << lo_bits) - 1ull)));
+// ---- preparation ------------------------------------------------------------
+
+// One warp per row: |S_e|, dense flag, and the sort key that puts the heavy
+// rows first (stable radix sort: postorder kept among the heavy rows — subtree
+// locality, 25% fewer nonzero words per column at the EMP shape — and among
+// the light rows, whose key is 1).
+__global__ void sp_row_key_kernel(const uint32_t* __restrict__ rows, int64_t stride, int32_t E,
+                                  int32_t n, int32_t heavy_min, uint32_t* __restrict__ keys,
+                                  int32_t* __restrict__ vals, uint8_t* __restrict__ dense,
+                                  unsigned int* __restrict__ n_heavy, int32_t* __restrict__ mcount) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < E; r += nwarps) {
+    const uint32_t* row = rows + r * stride;
+    int m = 0;
+    for (int64_t i = lane; i < stride; i += 32) m += __popc(__ldg(row + i));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m += __shfl_xor_sync(0xffffffffu, m, off);
+    if (lane == 0) {
+      const bool dn = 2 * m > n;
+      const int x = dn ? n - m : m;
+      keys[r] = x >= heavy_min ? 0u : 1u;
+      vals[r] = static_cast<int32_t>(r);
+      dense[r] = dn ? 1 : 0;
+      mcount[r] = m;
+      if (x >= heavy_min) atomicAdd(n_heavy, 1u);
+    }
+  }
+}
+
+// Exponent e_b of the factor the heavy walk builds for bit b of a 32-bit v
+// half: the double whose high word is 1 << b (low word 0). b < 20: subnormal
+// 2^(b-1042); 20 <= b <= 30: 2^(2^(b-20) - 1023); b = 31 is the sign bit
+// (-0.0), so that bit uses the factor 2.0 = hi word 0x40000000 instead.
+__host__ __device__ __forceinline__ int factor_exp(int b) {
+  if (b < 20) return b - 1042;
+  if (b < 31) return (1 << (b - 20)) - 1023;
+  return 1;
+}
+
+// Limb value stored for the heavy walk: integer limb c (< 2^32) as c * 2^-52
+// (so every accumulator is an exact multiple of 2^-52 below 2), divided by the
+// bit's factor. c * 2^(-52 - e_b) is at most 2^32 * 2^990 and at least
+// 2^-53 (b = 31), both normal doubles.
+__device__ __forceinline__ double scaled_limb(unsigned long long c, int b) {
+  return ldexp(static_cast<double>(c), -52 - factor_exp(b));
+}
+
+// Permuted row i <- original row perm[i]: dense mask, the pre-scaled limbs
+// by bit position for the heavy walk, the integer limbs by bit position (for
+// the column sums), and C = the dense rows' main-level limb sums.
+__global__ void sp_perm_kernel(const int32_t* __restrict__ perm, int32_t E, int64_t rows_pad,
+                               const uint8_t* __restrict__ dense, const unsigned long long* __restrict__ fix,
+                               int32_t lo_bits, unsigned long long* __restrict__ dmask64,
+                               double2* __restrict__ limbs, unsigned long long* __restrict__ fixbit,
+                               unsigned long long* __restrict__ cacc) {
+  const unsigned long long lo_mask = (1ull << lo_bits) - 1ull;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows_pad;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int p = 63 - static_cast<int>(i & 63);  // bit position in the 64-row word
+    const int64_t slot = (i & ~int64_t{63}) + p;
+    if (i >= E) {
+      limbs[slot] = make_double2(0.0, 0.0);
+      fixbit[slot] = 0ull;
+      continue;
+    }
+    const int r = perm[i];
+    const unsigned long long v = fix[r];
+    const unsigned long long hi = v >> lo_bits, lo = v & lo_mask;
+    limbs[slot] = make_double2(scaled_limb(hi, p & 31), scaled_limb(lo, p & 31));
+    fixbit[slot] = v;
+    if (dense[r]) {
+      atomicOr(dmask64 + (i >> 6), 1ull << p);
+      atomicAdd(cacc, hi);
+      atomicAdd(cacc + 1, lo);
+    }
+  }
 }
 
 // Heavy words only: sample-packed rows -> node-packed X words of the permuted
-// heavy rows (w < Hw, Hw read on device). One warp per (word, 32-sample block).
+// heavy rows (w < Hw). One warp per (word, 32-sample block).
 __global__ void sp_transpose_kernel(const uint32_t* __restrict__ rows, int64_t stride,
                                     const int32_t* __restrict__ perm,
                                     const unsigned int* __restrict__ n_heavy, int32_t n,
@@ -91,9 +181,10 @@ __global__ void sp_extend_kernel(unsigned long long* __restrict__ nx, int64_t n_
 __global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx, int64_t n_ext,
                                        int32_t n, const unsigned int* __restrict__ n_heavy,
                                        const unsigned long long* __restrict__ dmask64,
-                                       const double2* __restrict__ limbs,
+                                       const unsigned long long* __restrict__ fixbit, int32_t lo_bits,
                                        unsigned long long* __restrict__ colsum) {
   const int64_t Hw = (static_cast<int64_t>(*n_heavy) + 63) / 64;
+  const unsigned long long lo_mask = (1ull << lo_bits) - 1ull;
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
        c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     unsigned long long xh = 0, xl = 0, ph = 0, pl = 0;
@@ -106,9 +197,8 @@ __global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx
         const int p = 63 - __clzll(static_cast<long long>(b));  // bit position
         const unsigned long long m = 1ull << p;
         b ^= m;
-        const double2 L = __ldg(limbs + 64 * w + p);
-        const unsigned long long h = static_cast<unsigned long long>(L.x);
-        const unsigned long long l = static_cast<unsigned long long>(L.y);
+        const unsigned long long v = __ldg(fixbit + 64 * w + p);
+        const unsigned long long h = v >> lo_bits, l = v & lo_mask;
         xh += h;
         xl += l;
         if (!(dm & m)) {
@@ -124,16 +214,8 @@ __global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx
   }
 }
 
-// Light rows: one warp per row, over the light tail perm[H..E) of the row
-// permutation (|S_e| from the row-key kernel). Lists the members of X_e (in
-// sample order) in shared memory, adds the row to its members' column sums,
-// and adds its limbs to the slot of every member pair whose stripe lies in
-// [s_begin, s_end). gl: (s_end - s_begin) x n x (hi, lo) doubles.
-// Pair {a < b}, d = b - a: slot (s = d-1, k = a) when d-1 < S, and slot
-// (s = n-d-1, k = b) when n-d-1 < S (both for d = n/2, n even: the
-// reference's duplicated half stripe). Rows with up to 32*MAXT members keep
-// them in registers (lane j holds members j, j+32, ...) so the pair loop
-// needs one broadcast shared load per a instead of one per pair.
+// ---- light rows ---------------------------------------------------------------
+
 // Light sums are u64 limb pairs (hi, lo): every limb and partial sum is an
 // integer below 2^53, so integer atomics are exact and order-free (measured
 // as fast as fp64 atomic adds in L2: profiles/r01_ab_c3_light_u64_atomics.jsonl).
@@ -162,6 +244,12 @@ __device__ __forceinline__ void sp_add_pair(int a, int b, int n, int S, int s_be
   }
 }
 
+// One-shot light scatter (used when the banded form's u32/u16 indexing does
+// not fit): one warp per light row, members listed in shared memory in sample
+// order, every member pair's slot(s) in [s_begin, s_end) gets the limbs.
+// Pair {a < b}, d = b - a: slot (s = d-1, k = a) when d-1 < S, and slot
+// (s = n-d-1, k = b) when n-d-1 < S (both for d = n/2, n even: the
+// reference's duplicated half stripe).
 template <int NW, int MAXT>
 __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
     const uint32_t* __restrict__ rows, int64_t stride, int32_t E, int32_t n,
@@ -186,8 +274,6 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
     const int x = dense ? n - m : m;
     if (x == 0) continue;  // adds nothing anywhere
     const uint32_t* row = rows + static_cast<int64_t>(r) * stride;
-    // members in sample order: warp-wide compaction of the (possibly
-    // complemented) row words
     int count = 0;
     for (int64_t base = 0; base < stride && count < x; base += 32) {
       const int64_t i = base + lane;
@@ -213,15 +299,13 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
     }
     __syncwarp();
     const ulonglong2 L = ilimbs_of(fix[r], lo_bits);
-    const unsigned long long lh = L.x;
-    const unsigned long long ll = L.y;
     for (int i = lane; colsum && i < x; i += 32) {  // colsum null on later passes
       const int c = mem[i];
-      atomicAdd(colsum + c, lh);
-      atomicAdd(colsum + n + c, ll);
+      atomicAdd(colsum + c, L.x);
+      atomicAdd(colsum + n + c, L.y);
       if (!dense) {
-        atomicAdd(colsum + 2 * static_cast<int64_t>(n) + c, lh);
-        atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, ll);
+        atomicAdd(colsum + 2 * static_cast<int64_t>(n) + c, L.x);
+        atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, L.y);
       }
     }
     if (x <= 32 * MAXT) {
@@ -248,15 +332,13 @@ __global__ void __launch_bounds__(32 * NW) sp_light_scatter_kernel(
   if (lane == 0 && pairs) atomicAdd(pairs_out, pairs);
 }
 
-// ---- Banded light scatter (default). The one-shot scatter above sends each
-// pair's two fp64 atomics to a random 32-byte sector of the whole (stripes x
-// n) light-sum array (5 GB at C3): every atomic is an HBM read-modify-write
-// (ncu: 2.3 TB/s of DRAM traffic, 5% issue). Here the member lists are
-// compacted once (CSR, ascending samples), and the pairs are emitted band by
-// band — a band is a (stripe range x column range) block of the light-sum
-// array sized to stay resident in L2 — by binary-searching, for each member
-// a, the partners b whose slot falls in the band. Atomics then hit L2, and
-// HBM sees each light-sum line about once.
+// ---- Banded light scatter (default). The one-shot scatter sends each pair's
+// atomics to a random sector of the whole (stripes x n) light-sum array
+// (5 GB at C3): every atomic is an HBM read-modify-write (ncu: 2.3 TB/s of
+// DRAM traffic, 5% issue). Here the member lists are compacted once (CSR,
+// ascending samples), and the pairs are emitted band by band — a band is a
+// (stripe range x column range) block of the light-sum array sized to stay
+// resident in L2.
 
 // Members per permuted position (0 for heavy rows): cnt[idx], idx < E.
 __global__ void sp_light_count_kernel(const int32_t* __restrict__ perm, int32_t E, int32_t n,
@@ -271,6 +353,39 @@ __global__ void sp_light_count_kernel(const int32_t* __restrict__ perm, int32_t 
       x = static_cast<uint32_t>(2 * m > n ? n - m : m);
     }
     cnt[i] = x;
+  }
+}
+
+// Warp-wide compaction of the members of X_e (row words, complemented when
+// dense) into out[0, x), ascending; calls visit(sample) once per member.
+template <class Visit>
+__device__ __forceinline__ void list_members(const uint32_t* __restrict__ row, int64_t stride, bool dense,
+                                             uint32_t tail, int x, int lane, int32_t* __restrict__ out,
+                                             Visit visit) {
+  int count = 0;
+  for (int64_t base = 0; base < stride && count < x; base += 32) {
+    const int64_t i = base + lane;
+    uint32_t wd = 0u;
+    if (i < stride) {
+      wd = __ldg(row + i);
+      if (dense) wd = ~wd & (i == stride - 1 ? tail : 0xffffffffu);
+    }
+    const int c = __popc(wd);
+    int incl = c;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    int at = count + incl - c;
+    while (wd) {
+      const int b = __ffs(wd) - 1;
+      wd &= wd - 1u;
+      const int smp = static_cast<int>(i * 32 + b);
+      out[at++] = smp;
+      visit(smp);
+    }
+    count += __shfl_sync(0xffffffffu, incl, 31);
   }
 }
 
@@ -294,41 +409,16 @@ __global__ void sp_light_members_kernel(const uint32_t* __restrict__ rows, int64
     const bool dense = 2 * m > n;
     const int x = dense ? n - m : m;
     if (x == 0) continue;
-    const uint32_t* row = rows + static_cast<int64_t>(r) * stride;
-    int32_t* out = lmem + lptr[idx];
-    const double2 L = limbs_of(fix[r], lo_bits);
-    const unsigned long long lh = static_cast<unsigned long long>(L.x);
-    const unsigned long long ll = static_cast<unsigned long long>(L.y);
-    int count = 0;
-    for (int64_t base = 0; base < stride && count < x; base += 32) {
-      const int64_t i = base + lane;
-      uint32_t wd = 0u;
-      if (i < stride) {
-        wd = __ldg(row + i);
-        if (dense) wd = ~wd & (i == stride - 1 ? tail : 0xffffffffu);
-      }
-      const int c = __popc(wd);
-      int incl = c;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += y;
-      }
-      int at = count + incl - c;
-      while (wd) {
-        const int b = __ffs(wd) - 1;
-        wd &= wd - 1u;
-        const int smp = static_cast<int>(i * 32 + b);
-        out[at++] = smp;
-        atomicAdd(colsum + smp, lh);
-        atomicAdd(colsum + n + smp, ll);
-        if (!dense) {
-          atomicAdd(colsum + 2 * static_cast<int64_t>(n) + smp, lh);
-          atomicAdd(colsum + 3 * static_cast<int64_t>(n) + smp, ll);
-        }
-      }
-      count += __shfl_sync(0xffffffffu, incl, 31);
-    }
+    const ulonglong2 L = ilimbs_of(fix[r], lo_bits);
+    list_members(rows + static_cast<int64_t>(r) * stride, stride, dense, tail, x, lane, lmem + lptr[idx],
+                 [&](int smp) {
+                   atomicAdd(colsum + smp, L.x);
+                   atomicAdd(colsum + n + smp, L.y);
+                   if (!dense) {
+                     atomicAdd(colsum + 2 * static_cast<int64_t>(n) + smp, L.x);
+                     atomicAdd(colsum + 3 * static_cast<int64_t>(n) + smp, L.y);
+                   }
+                 });
   }
 }
 
@@ -359,7 +449,7 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
     const uint32_t* __restrict__ lptr, const int32_t* __restrict__ lmem, uint16_t* __restrict__ cur,
     const unsigned long long* __restrict__ fix, int32_t lo_bits, int32_t p0, int32_t s0, int32_t s1,
     int32_t k0, int32_t k1, unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
-    int32_t list_cap, int32_t dry) {
+    int32_t list_cap) {
   extern __shared__ int32_t sp_band_members[];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
@@ -393,13 +483,13 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
       // partners above: slot (b - a - 1, a)
       for (; j1 < x && mem[j1] <= a + se; ++j1) {
         const int s = mem[j1] - a - 1;
-        if (!dry) light_add(gl + 2 * (static_cast<int64_t>(s - p0) * n + a), L);
+        light_add(gl + 2 * (static_cast<int64_t>(s - p0) * n + a), L);
         ++pairs;
       }
       // partners below: slot (n - (a - a') - 1, a)
       for (; j2 < i && mem[j2] <= a - n + se; ++j2) {
         const int s = n - (a - mem[j2]) - 1;
-        if (!dry) light_add(gl + 2 * (static_cast<int64_t>(s - p0) * n + a), L);
+        light_add(gl + 2 * (static_cast<int64_t>(s - p0) * n + a), L);
         ++pairs;
       }
       reinterpret_cast<uint32_t*>(c)[i] = static_cast<uint32_t>(j1) | (static_cast<uint32_t>(j2) << 16);
@@ -410,249 +500,240 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
   if (lane == 0 && pairs) atomicAdd(pairs_out, pairs);
 }
 
-// ---- Entry lists per column band (default band scatter). The warp-per-row
-// band kernel above rereads every light row's member list in every band
-// launch (C3: ~190 launches, C5: ~3,000); here each launch only visits the
-// members whose column lies in its band: one thread per (row, member) entry
-// of the column band's list, row data precomputed.
-struct LightRow {
-  uint32_t b0, x;        // member list offset and length
-  unsigned long long lh, ll;  // fixed-point limbs of the row's length
-};
+// ---- deeper fixed-point levels ---------------------------------------------------
+// drows[i] (original row ids, i < R) are the rows with a nonzero value below
+// the main level; dfix[i * (J-1) + (j-1)] their level-j values (j >= 1).
 
-__global__ void sp_light_rowinfo_kernel(const int32_t* __restrict__ perm, int32_t E,
-                                        const unsigned int* __restrict__ n_heavy,
-                                        const uint32_t* __restrict__ lptr,
-                                        const unsigned long long* __restrict__ fix, int32_t lo_bits,
-                                        LightRow* __restrict__ info) {
-  const int64_t H = *n_heavy;
-  for (int64_t idx = H + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < E;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const ulonglong2 L = ilimbs_of(fix[perm[idx]], lo_bits);
-    info[idx] = LightRow{lptr[idx], lptr[idx + 1] - lptr[idx], L.x, L.y};
+__global__ void sp_deep_count_kernel(const int32_t* __restrict__ drows, int32_t R, int32_t n,
+                                     const int32_t* __restrict__ mcount, uint32_t* __restrict__ cnt) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i <= R;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    uint32_t x = 0;
+    if (i < R) {
+      const int m = mcount[drows[i]];
+      x = static_cast<uint32_t>(2 * m > n ? n - m : m);
+    }
+    cnt[i] = x;
   }
 }
 
-// Entries per column band (block histogram in shared memory, <= 1024 bands).
-__global__ void sp_entry_hist_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ lptr,
-                                     int32_t E, int32_t KB, int32_t nkb, uint32_t* __restrict__ kcnt) {
-  extern __shared__ uint32_t hist[];
-  for (int i = threadIdx.x; i < nkb; i += blockDim.x) hist[i] = 0u;
-  __syncthreads();
-  const int64_t M = lptr[E];
-  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < M;
-       g += static_cast<int64_t>(gridDim.x) * blockDim.x)
-    atomicAdd(&hist[lmem[g] / KB], 1u);
-  __syncthreads();
-  for (int i = threadIdx.x; i < nkb; i += blockDim.x)
-    if (hist[i]) atomicAdd(kcnt + i, hist[i]);
-}
-
-// Entries (member g, row idx) into their band's list; warp per light row,
-// warp-aggregated slot claims (a row's members are ascending, so a warp's
-// lanes mostly share one or two bands).
-__global__ void sp_entry_fill_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ lptr,
-                                     int32_t E, const unsigned int* __restrict__ n_heavy, int32_t KB,
-                                     uint32_t* __restrict__ kfill, uint2* __restrict__ ent) {
+// Members of every deep row at dmem[dptr[i] ...] (ascending), the owning deep
+// row of every entry, and the deeper levels' column sums and dense totals:
+// dcolsum [J-1][4][n] as colsum, dcacc [J-1][2].
+__global__ void sp_deep_members_kernel(const uint32_t* __restrict__ rows, int64_t stride, int32_t n,
+                                       const int32_t* __restrict__ drows, int32_t R,
+                                       const int32_t* __restrict__ mcount, const uint32_t* __restrict__ dptr,
+                                       const unsigned long long* __restrict__ dfix, int32_t J, int32_t lo_bits,
+                                       int32_t* __restrict__ dmem, uint32_t* __restrict__ dent,
+                                       unsigned long long* __restrict__ dcolsum,
+                                       unsigned long long* __restrict__ dcacc) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-  const int64_t H = *n_heavy;
-  for (int64_t idx = H + warp; idx < E; idx += nwarps) {
-    const uint32_t b0 = lptr[idx];
-    const int x = static_cast<int>(lptr[idx + 1] - b0);  // every entry listed (the histogram counts all)
-    for (int base = 0; base < x; base += 32) {
-      const int i = base + lane;
-      const bool live = i < x;
-      const int K = live ? lmem[b0 + i] / KB : -1;
-      const uint32_t act = __ballot_sync(0xffffffffu, live);
-      if (!live) continue;
-      const uint32_t same = __match_any_sync(act, K);
-      const int leader = __ffs(same) - 1;
-      uint32_t pos = 0;
-      if (lane == leader) pos = atomicAdd(kfill + K, static_cast<uint32_t>(__popc(same)));
-      pos = __shfl_sync(same, pos, leader) + static_cast<uint32_t>(__popc(same & ((1u << lane) - 1u)));
-      ent[pos] = make_uint2(b0 + static_cast<uint32_t>(i), static_cast<uint32_t>(idx));
+  const uint32_t tail = (n & 31) ? ((1u << (n & 31)) - 1u) : 0xffffffffu;
+  const int64_t n4 = 4 * static_cast<int64_t>(n);
+  for (int64_t i = warp; i < R; i += nwarps) {
+    const int r = drows[i];
+    const int m = mcount[r];
+    const bool dense = 2 * m > n;
+    const int x = dense ? n - m : m;
+    const unsigned long long* v = dfix + i * (J - 1);
+    if (dense && lane < J - 1) {
+      const ulonglong2 L = ilimbs_of(v[lane], lo_bits);
+      atomicAdd(dcacc + 2 * lane, L.x);
+      atomicAdd(dcacc + 2 * lane + 1, L.y);
     }
+    const uint32_t b0 = dptr[i];
+    for (int q = lane; q < x; q += 32) dent[b0 + q] = static_cast<uint32_t>(i);
+    if (x == 0) continue;
+    list_members(rows + static_cast<int64_t>(r) * stride, stride, dense, tail, x, lane, dmem + b0, [&](int smp) {
+      for (int j = 0; j < J - 1; ++j) {
+        if (!v[j]) continue;
+        const ulonglong2 L = ilimbs_of(v[j], lo_bits);
+        unsigned long long* cs = dcolsum + j * n4;
+        atomicAdd(cs + smp, L.x);
+        atomicAdd(cs + n + smp, L.y);
+        if (!dense) {
+          atomicAdd(cs + 2 * static_cast<int64_t>(n) + smp, L.x);
+          atomicAdd(cs + 3 * static_cast<int64_t>(n) + smp, L.y);
+        }
+      }
+    });
   }
 }
 
-// One band (stripes [s0, s1), the column band whose entries are ent[t0, t1)):
-// same slot ownership and cursors as sp_light_band_kernel.
-template <bool FIRST>
-__global__ void __launch_bounds__(256) sp_light_entry_kernel(
-    const uint2* __restrict__ ent, uint32_t t0, uint32_t t1, const LightRow* __restrict__ info,
-    const int32_t* __restrict__ lmem, uint32_t* __restrict__ cur, int32_t n, int32_t p0, int32_t s0,
-    int32_t s1, unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out) {
+__device__ __forceinline__ void deep_add(unsigned long long* __restrict__ dacc, int64_t cell, int32_t J,
+                                         const unsigned long long* __restrict__ v, int lo_bits) {
+  for (int j = 0; j < J - 1; ++j) {
+    if (!v[j]) continue;
+    light_add(dacc + 2 * (cell * (J - 1) + j), ilimbs_of(v[j], lo_bits));
+  }
+}
+
+// Thread per deep-row member entry: every partner above it, both slots of
+// the pair as in sp_add_pair, the deeper levels' limbs into dacc
+// [(s - s_begin) * n + k][J-1] (hi, lo).
+__global__ void sp_deep_scatter_kernel(const uint32_t* __restrict__ dptr, const int32_t* __restrict__ dmem,
+                                       const uint32_t* __restrict__ dent, int64_t M,
+                                       const unsigned long long* __restrict__ dfix, int32_t J, int32_t lo_bits,
+                                       int32_t n, int32_t s_begin, int32_t s_end,
+                                       unsigned long long* __restrict__ dacc) {
   const int S = n / 2;
-  const int se = min(s1, S);
-  unsigned long long pairs = 0;
-  for (uint32_t t = t0 + blockIdx.x * blockDim.x + threadIdx.x; t < t1; t += gridDim.x * blockDim.x) {
-    const uint2 e = ent[t];
-    const LightRow r = info[e.y];
-    const int32_t* mem = lmem + r.b0;
-    const int x = static_cast<int>(r.x);
-    const int i = static_cast<int>(e.x - r.b0);
-    const int a = mem[i];
-    const ulonglong2 L = make_ulonglong2(r.lh, r.ll);
-    int j1, j2;
-    if (FIRST) {
-      j1 = lower_bound_i32(mem, i + 1, x, a + s0 + 1);
-      j2 = lower_bound_i32(mem, 0, i, a - n + 1 + s0);
-    } else {
-      const uint32_t cc = cur[e.x];
-      j1 = static_cast<int>(cc & 0xffffu);
-      j2 = static_cast<int>(cc >> 16);
+  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < M;
+       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t i = dent[g];
+    const int64_t end = dptr[i + 1];
+    const unsigned long long* v = dfix + static_cast<int64_t>(i) * (J - 1);
+    const int a = dmem[g];
+    for (int64_t q = g + 1; q < end; ++q) {
+      const int b = __ldg(dmem + q);
+      const int d = b - a;
+      int s = d - 1;
+      if (s < S && s >= s_begin && s < s_end) deep_add(dacc, static_cast<int64_t>(s - s_begin) * n + a, J, v, lo_bits);
+      s = n - d - 1;
+      if (s < S && s >= s_begin && s < s_end) deep_add(dacc, static_cast<int64_t>(s - s_begin) * n + b, J, v, lo_bits);
     }
-    for (; j1 < x; ++j1) {  // partners above: slot (b - a - 1, a)
-      const int b = __ldg(mem + j1);
-      if (b > a + se) break;
-      light_add(gl + 2 * (static_cast<int64_t>(b - a - 1 - p0) * n + a), L);
-      ++pairs;
-    }
-    for (; j2 < i; ++j2) {  // partners below: slot (n - (a - a') - 1, a)
-      const int a2 = __ldg(mem + j2);
-      if (a2 > a - n + se) break;
-      light_add(gl + 2 * (static_cast<int64_t>(n - (a - a2) - 1 - p0) * n + a), L);
-      ++pairs;
-    }
-    cur[e.x] = static_cast<uint32_t>(j1) | (static_cast<uint32_t>(j2) << 16);
-  }
-  for (int off = 16; off > 0; off >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, off);
-  if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(pairs_out, pairs);
-}
-
-// bfind: position of the most significant set bit (x != 0).
-__device__ __forceinline__ int msb_pos(uint32_t x) {
-  int b;
-  asm("bfind.u32 %0, %1;" : "=r"(b) : "r"(x));
-  return b;
-}
-
-// Nonzero heavy words per column: bit j of nz[g][c] = (nx[32g + j][c] != 0).
-// Thread per (group, column), coalesced over columns.
-__global__ void sp_nzmask_kernel(const unsigned long long* __restrict__ nx, int64_t n_ext, int32_t n,
-                                 const unsigned int* __restrict__ n_heavy, uint32_t* __restrict__ nz) {
-  const int64_t Hw = (static_cast<int64_t>(*n_heavy) + 63) / 64;
-  const int64_t G = (Hw + 31) / 32;
-  const int64_t total = G * n;
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int64_t g = i / n;
-    const int64_t c = i - g * n;
-    uint32_t m = 0u;
-    const int64_t left = Hw - 32 * g;
-    const int jmax = left < 32 ? static_cast<int>(left) : 32;
-    for (int j = 0; j < jmax; ++j)
-      if (__ldg(nx + (32 * g + j) * n_ext + c)) m |= 1u << j;
-    nz[g * n + c] = m;
   }
 }
 
-__device__ __forceinline__ void prefetch_l1(const void* p) {
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
-}
+// ---- heavy walk + epilogue ----------------------------------------------------------
 
 struct SplitArgs {
   const unsigned long long* nx;      // [Hw][n_ext] heavy X words
-  const double2* limbs;              // permuted heavy rows, by bit position
+  const double2* limbs;              // permuted heavy rows, by bit position, pre-scaled (scaled_limb)
   const unsigned int* n_heavy;
-  const unsigned long long* gl;      // light sums per slot (hi, lo limbs, u64)
+  unsigned long long* gl;            // light sums per slot (hi, lo limbs, u64); deep levels: G out
   const unsigned long long* colsum;  // [4][n]
   const unsigned long long* cacc;    // [2]
+  const unsigned long long* dacc;    // deeper levels: [(s - gl_begin) * n + k][J-1] (hi, lo)
+  const unsigned long long* dcolsum; // [J-1][4][n]
+  const unsigned long long* dcacc;   // [J-1][2]
   int64_t n_ext;
   int32_t n;
   int32_t s_begin, s_end;  // stripes computed by this launch
   int32_t out_begin;       // stripe held by row 0 of dist / tot
-  int32_t gl_begin;        // stripe held by row 0 of gl (the light-sum pass)
+  int32_t gl_begin;        // stripe held by row 0 of gl / dacc (the light-sum pass)
   int32_t lo_bits, scale, finalize;
+  int32_t levels, vb;      // fixed-point levels (1: every length on the main grid), bits per level
   void* dist;
   void* tot;
-  unsigned long long* counters;  // [0] slot x u-bit FMAs (+ light pairs, added by host), [1] fp64 ops
-  const uint32_t* nz;            // [ceil(Hw/32)][n] nonzero-word masks (LIST variants)
+  unsigned long long* counters;  // [0] slot x u-bit FMA pairs (+ light pairs, added by host), [1] fp64 ops
 };
 
-// The next (up to) two set bits of hu, highest first: positions b1, b2 and
-// masks m1, m2 (0 when absent; the position then points at a valid entry).
-__device__ __forceinline__ void next_two(uint32_t& hu, int& b1, uint32_t& m1, int& b2, uint32_t& m2) {
-  b1 = msb_pos(hu | 1u);
-  m1 = hu ? (1u << b1) : 0u;
-  hu ^= m1;
-  b2 = msb_pos(hu | 1u);
-  m2 = hu ? (1u << b2) : 0u;
-  hu ^= m2;
-}
-
-// Add the limbs of one pair of u bits to every slot whose v half has the bit
-// (the bit is set in u, so v need not be masked with u first). BITMAJOR: bit
-// 1 for all slots, then bit 2; else slot by slot.
-template <int RS, bool BITMAJOR>
-__device__ __forceinline__ void heavy_fma2(const double2 L1, uint32_t m1, const double2 L2, uint32_t m2,
-                                           const uint32_t (&vv)[RS], double (&gh)[RS],
-                                           double (&gl)[RS]) {
-  if (BITMAJOR) {
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const double f1 = unit_if(vv[i] & m1);
-      gh[i] = fma(L1.x, f1, gh[i]);
-      gl[i] = fma(L1.y, f1, gl[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const double f2 = unit_if(vv[i] & m2);
-      gh[i] = fma(L2.x, f2, gh[i]);
-      gl[i] = fma(L2.y, f2, gl[i]);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const double f1 = unit_if(vv[i] & m1);
-      const double f2 = unit_if(vv[i] & m2);
-      gh[i] = fma(L1.x, f1, gh[i]);
-      gl[i] = fma(L1.y, f1, gl[i]);
-      gh[i] = fma(L2.x, f2, gh[i]);
-      gl[i] = fma(L2.y, f2, gl[i]);
-    }
-  }
-}
-
-// One 32-bit half of a heavy u word, two bits per step, branch-free.
-// (A ping-pong prefetch of the next step's limbs measured slower: the extra
-// registers cost more occupancy than the hidden L1 latency was worth.)
-template <int RS, bool BITMAJOR>
+// One 32-bit half of a heavy u word, two bits per step, branch-free: per
+// bit and slot one LOP3 (v & m, the factor's high word) and two DFMA.
+template <int RS>
 __device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restrict__ Lb,
-                                           const uint32_t (&vv)[RS], double (&gh)[RS],
-                                           double (&gl)[RS]) {
+                                           const uint32_t (&vv)[RS], double (&gh)[RS], double (&gl)[RS]) {
+  if (hu & 0x80000000u) {  // sign bit: factor 2.0 from the bit shifted to 30
+    const double2 L = __ldg(Lb + 31);
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const double f = __hiloint2double(static_cast<int>((vv[i] >> 1) & 0x40000000u), 0);
+      gh[i] = fma(L.x, f, gh[i]);
+      gl[i] = fma(L.y, f, gl[i]);
+    }
+    hu &= 0x7fffffffu;
+  }
   while (hu) {
-    int b1, b2;
-    uint32_t m1, m2;
-    next_two(hu, b1, m1, b2, m2);
+    const int b1 = msb_pos(hu);
+    const uint32_t m1 = 1u << b1;
+    hu ^= m1;
+    const int b2 = msb_pos(hu | 1u);
+    const uint32_t m2 = hu ? (1u << b2) : 0u;
+    hu ^= m2;
     const double2 L1 = __ldg(Lb + b1);
     const double2 L2 = __ldg(Lb + b2);
-    heavy_fma2<RS, BITMAJOR>(L1, m1, L2, m2, vv, gh, gl);
+#pragma unroll
+    for (int i = 0; i < RS; ++i) {
+      const double f1 = __hiloint2double(static_cast<int>(vv[i] & m1), 0);
+      const double f2 = __hiloint2double(static_cast<int>(vv[i] & m2), 0);
+      gh[i] = fma(L1.x, f1, gh[i]);
+      gl[i] = fma(L1.y, f1, gl[i]);
+      gh[i] = fma(L2.x, f2, gh[i]);
+      gl[i] = fma(L2.y, f2, gl[i]);
+    }
   }
 }
 
-// One nonzero heavy word (u != 0) of the warp's column, HALVES layout.
-template <int RS>
-__device__ __forceinline__ void heavy_word(unsigned long long u, const unsigned long long* row,
-                                           const double2* Lw, int64_t l0, double (&gh)[RS], double (&gl)[RS]) {
-  const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
-  uint32_t vv[RS];
-  if (static_cast<uint32_t>(u >> 32)) {
-#pragma unroll
-    for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
-    heavy_half<RS, false>(static_cast<uint32_t>(u >> 32), Lw + 32, vv, gh, gl);
+// Exact t and d of one slot at fixed-point level j >= 1 (128-bit integers).
+__device__ __forceinline__ void deep_level_td(const SplitArgs& a, int j, int64_t cell, int k, int lm, __int128& tv,
+                                              __int128& dv) {
+  const int n = a.n;
+  const unsigned long long* xs = a.dcolsum + static_cast<int64_t>(j - 1) * 4 * n;
+  const ulonglong2 G = reinterpret_cast<const ulonglong2*>(a.dacc)[cell * (a.levels - 1) + (j - 1)];
+  const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm] + a.dcacc[2 * (j - 1)] - G.x);
+  const long long tl = static_cast<long long>(xs[3 * n + k] + xs[3 * n + lm] + a.dcacc[2 * (j - 1) + 1] - G.y);
+  const long long dh = static_cast<long long>(xs[k] + xs[lm] - 2 * G.x);
+  const long long dl = static_cast<long long>(xs[n + k] + xs[n + lm] - 2 * G.y);
+  tv = (static_cast<__int128>(th) << a.lo_bits) + tl;
+  dv = (static_cast<__int128>(dh) << a.lo_bits) + dl;
+}
+
+// sum_j V_j 2^-(scale + vb j) over the slot's levels, correctly rounded:
+// carries are normalized from the deepest level up (every level's value is
+// non-negative), then the leading 64+ bits are gathered from the first
+// nonzero digit down, with a sticky bit for the rest.
+template <class Real>
+__device__ Real combine_levels(const SplitArgs& a, __int128 V0, bool is_t, int64_t cell, int k, int lm) {
+  constexpr int kMaxLevels = 40;
+  unsigned long long dig[kMaxLevels];
+  const int J = a.levels;
+  const unsigned __int128 mask = (static_cast<unsigned __int128>(1) << a.vb) - 1;
+  unsigned __int128 carry = 0;
+  for (int j = J - 1; j >= 1; --j) {
+    __int128 tv, dv;
+    deep_level_td(a, j, cell, k, lm, tv, dv);
+    const unsigned __int128 x = static_cast<unsigned __int128>(is_t ? tv : dv) + carry;
+    dig[j] = static_cast<unsigned long long>(x & mask);
+    carry = x >> a.vb;
   }
-  if (static_cast<uint32_t>(u)) {
-#pragma unroll
-    for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
-    heavy_half<RS, false>(static_cast<uint32_t>(u), Lw, vv, gh, gl);
+  unsigned __int128 acc = static_cast<unsigned __int128>(V0) + carry;
+  int e = 0;  // acc's unit is 2^-(scale + vb e)
+  bool sticky = false;
+  for (int j = 1; j < J; ++j) {
+    if ((acc >> 64) == 0) {
+      acc = (acc << a.vb) | dig[j];
+      e = j;
+    } else if (dig[j]) {
+      sticky = true;
+    }
+  }
+  return u128_to_real<Real>(acc, sticky, -(a.scale + a.vb * e));
+}
+
+// Epilogue when some length has deeper levels: the heavy kernel left the
+// slot's main-level pair sum G (hi, lo limbs as int64) in its light-sum cell.
+template <class Real>
+__global__ void sp_deep_epilogue_kernel(const SplitArgs a) {
+  const int n = a.n;
+  const int64_t total = static_cast<int64_t>(a.s_end - a.s_begin) * n;
+  const unsigned long long* xs = a.colsum;
+  const long long ch = static_cast<long long>(a.cacc[0]);
+  const long long cl = static_cast<long long>(a.cacc[1]);
+  Real* dist = static_cast<Real*>(a.dist);
+  Real* tot = static_cast<Real*>(a.tot);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int s = a.s_begin + static_cast<int>(i / n);
+    const int k = static_cast<int>(i % n);
+    const int lm = static_cast<int>((static_cast<int64_t>(k) + s + 1) % n);
+    const int64_t cell = static_cast<int64_t>(s - a.gl_begin) * n + k;
+    const longlong2 G = reinterpret_cast<const longlong2*>(a.gl)[cell];
+    const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm]) + ch - G.x;
+    const long long tl = static_cast<long long>(xs[3 * n + k] + xs[3 * n + lm]) + cl - G.y;
+    const long long dh = static_cast<long long>(xs[k] + xs[lm]) - 2 * G.x;
+    const long long dl = static_cast<long long>(xs[n + k] + xs[n + lm]) - 2 * G.y;
+    const Real t = combine_levels<Real>(a, (static_cast<__int128>(th) << a.lo_bits) + tl, true, cell, k, lm);
+    Real d = combine_levels<Real>(a, (static_cast<__int128>(dh) << a.lo_bits) + dl, false, cell, k, lm);
+    if (a.finalize) d = t == Real(0) ? Real(0) : d / t;
+    const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
+    dist[off] = d;
+    tot[off] = t;
   }
 }
 
-template <class Real, int RS, int NW, bool BITMAJOR = false, bool UPREF = false, bool HALVES = false,
-          int MINB = 1, bool LIST = false, bool PREF = false, bool PIPE = false>
+template <class Real, int RS, int NW, int MINB>
 __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const SplitArgs a) {
   const int lane = threadIdx.x & 31;
   const int k = blockIdx.x * NW + (threadIdx.x >> 5);
@@ -676,117 +757,25 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
     gh[i] = 0.0;
     gl[i] = 0.0;
   }
-  if (PIPE) {
-    // software-pipelined walk of the nonzero words (per-column masks): the
-    // next word's u and 64-bit v words are loaded into registers while the
-    // current word is walked
-    const int G = (Hw + 31) / 32;
-    int g = 0;
-    uint32_t m = 0u;
-    auto next_w = [&]() -> int {  // next nonzero word index, or -1
-      while (!m) {
-        if (g >= G) return -1;
-        m = __ldg(a.nz + static_cast<int64_t>(g) * n + k);
-        ++g;
-      }
-      const int w = 32 * (g - 1) + (__ffs(m) - 1);
-      m &= m - 1u;
-      return w;
-    };
-    int w = next_w();
-    unsigned long long u = 0ull, v[RS];
-    if (w >= 0) {
-      const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
-      u = __ldg(row + k);
-#pragma unroll
-      for (int i = 0; i < RS; ++i) v[i] = __ldg(row + l0 + 32 * i);
-    }
 #pragma unroll 1
-    while (w >= 0) {
-      const int wn = next_w();
-      unsigned long long un = 0ull, vn[RS];
-      if (wn >= 0) {
-        const unsigned long long* nrow = a.nx + static_cast<int64_t>(wn) * n_ext;
-        un = __ldg(nrow + k);
-#pragma unroll
-        for (int i = 0; i < RS; ++i) vn[i] = __ldg(nrow + l0 + 32 * i);
-      }
-      ubits += static_cast<unsigned>(__popcll(u));
-      const double2* Lw = a.limbs + 64 * static_cast<int64_t>(w);
-      uint32_t vh[RS], vl[RS];
-#pragma unroll
-      for (int i = 0; i < RS; ++i) {
-        vh[i] = static_cast<uint32_t>(v[i] >> 32);
-        vl[i] = static_cast<uint32_t>(v[i]);
-      }
-      heavy_half<RS, false>(static_cast<uint32_t>(u >> 32), Lw + 32, vh, gh, gl);
-      heavy_half<RS, false>(static_cast<uint32_t>(u), Lw, vl, gh, gl);
-      w = wn;
-      u = un;
-#pragma unroll
-      for (int i = 0; i < RS; ++i) v[i] = vn[i];
-    }
-  }
-  if (LIST) {
-    // walk only the nonzero words of column k (per-column masks), and pull
-    // the next word's u and v lines into L1 while this word is walked
-    const int G = (Hw + 31) / 32;
-#pragma unroll 1
-    for (int g = 0; g < G; ++g) {
-      uint32_t m = __ldg(a.nz + static_cast<int64_t>(g) * n + k);
-      while (m) {
-        const int w = 32 * g + (__ffs(m) - 1);
-        m &= m - 1u;
-        const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
-        if (PREF && m) {
-          const unsigned long long* nrow = a.nx + static_cast<int64_t>(32 * g + (__ffs(m) - 1)) * n_ext;
-          if (lane == 0) prefetch_l1(nrow + k);
-#pragma unroll
-          for (int i = 0; i < RS; ++i) prefetch_l1(nrow + l0 + 32 * i);
-        }
-        const unsigned long long u = __ldg(row + k);
-        ubits += static_cast<unsigned>(__popcll(u));
-        heavy_word<RS>(u, row, a.limbs + 64 * static_cast<int64_t>(w), l0, gh, gl);
-      }
-    }
-  }
-  unsigned long long u_next = (UPREF && Hw > 0) ? __ldg(a.nx + k) : 0ull;
-#pragma unroll 1
-  for (int w = 0; (LIST || PIPE) ? false : w < Hw; ++w) {
+  for (int w = 0; w < Hw; ++w) {
     const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
-    unsigned long long u;
-    if (UPREF) {
-      u = u_next;  // loaded one word ahead
-      if (w + 1 < Hw) u_next = __ldg(row + n_ext + k);
-    } else {
-      u = __ldg(row + k);
-    }
+    const unsigned long long u = __ldg(row + k);
     if (u == 0ull) continue;
     const double2* Lw = a.limbs + 64 * static_cast<int64_t>(w);
     ubits += static_cast<unsigned>(__popcll(u));
-    if (HALVES) {  // one 32-bit half of the v words live at a time (fewer registers)
-      const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
-      uint32_t vv[RS];
-      if (static_cast<uint32_t>(u >> 32)) {
+    // one 32-bit half of the v words live at a time (fewer registers)
+    const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
+    uint32_t vv[RS];
+    if (static_cast<uint32_t>(u >> 32)) {
 #pragma unroll
-        for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
-        heavy_half<RS, BITMAJOR>(static_cast<uint32_t>(u >> 32), Lw + 32, vv, gh, gl);
-      }
-      if (static_cast<uint32_t>(u)) {
+      for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
+      heavy_half<RS>(static_cast<uint32_t>(u >> 32), Lw + 32, vv, gh, gl);
+    }
+    if (static_cast<uint32_t>(u)) {
 #pragma unroll
-        for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
-        heavy_half<RS, BITMAJOR>(static_cast<uint32_t>(u), Lw, vv, gh, gl);
-      }
-    } else {
-      uint32_t vh[RS], vl[RS];
-#pragma unroll
-      for (int i = 0; i < RS; ++i) {
-        const unsigned long long v = __ldg(row + l0 + 32 * i);
-        vh[i] = static_cast<uint32_t>(v >> 32);
-        vl[i] = static_cast<uint32_t>(v);
-      }
-      heavy_half<RS, BITMAJOR>(static_cast<uint32_t>(u >> 32), Lw + 32, vh, gh, gl);
-      heavy_half<RS, BITMAJOR>(static_cast<uint32_t>(u), Lw, vl, gh, gl);
+      for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
+      heavy_half<RS>(static_cast<uint32_t>(u), Lw, vv, gh, gl);
     }
   }
 
@@ -802,138 +791,29 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
     const int64_t li = l0 + 32 * i;
     const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
     const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
-    const ulonglong2 light =
-        reinterpret_cast<const ulonglong2*>(a.gl)[static_cast<int64_t>(s - a.gl_begin) * n + k];
-    const long long Gh_ = static_cast<long long>(gh[i]) + static_cast<long long>(light.x);
-    const long long Gl_ = static_cast<long long>(gl[i]) + static_cast<long long>(light.y);
+    const int64_t cell = static_cast<int64_t>(s - a.gl_begin) * n + k;
+    const ulonglong2 light = reinterpret_cast<const ulonglong2*>(a.gl)[cell];
+    // accumulators hold exact multiples of 2^-52 below 2
+    const long long Gh_ = __double2ll_rn(gh[i] * 0x1p52) + static_cast<long long>(light.x);
+    const long long Gl_ = __double2ll_rn(gl[i] * 0x1p52) + static_cast<long long>(light.y);
     const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm]) + ch - Gh_;
     const long long tl = static_cast<long long>(xs[3 * n + k] + xs[3 * n + lm]) + cl - Gl_;
     const long long dh = static_cast<long long>(xs[k] + xs[lm]) - 2 * Gh_;
     const long long dl = static_cast<long long>(xs[n + k] + xs[n + lm]) - 2 * Gl_;
+    if (a.levels > 1) {  // sp_deep_epilogue_kernel finishes the slot
+      reinterpret_cast<longlong2*>(a.gl)[cell] = make_longlong2(Gh_, Gl_);
+      continue;
+    }
     const __int128 tv = (static_cast<__int128>(th) << a.lo_bits) + tl;
     const __int128 dv = (static_cast<__int128>(dh) << a.lo_bits) + dl;
-    const Real t = static_cast<Real>(i2_fixed_to_double(tv, a.scale));
-    Real d = static_cast<Real>(i2_fixed_to_double(dv, a.scale));
+    const Real t = fixed_to_real<Real>(tv, a.scale);
+    Real d = fixed_to_real<Real>(dv, a.scale);
     if (a.finalize) d = t == Real(0) ? Real(0) : d / t;
     dist[off] = d;
     tot[off] = t;
   }
   if (a.counters && lane == 0) {
     // ubits is warp-uniform: the warp issued ubits x (live slots) FMA pairs
-    atomicAdd(a.counters, ubits * static_cast<unsigned long long>(wvalid));
-    atomicAdd(a.counters + 1, 2ull * ubits * static_cast<unsigned long long>(wvalid));
-  }
-}
-
-// ---- Integer-accumulator variant (A/B: SF_SPLIT_VARIANT=16). Same walk,
-// but each slot accumulates the row's 63-bit fixed-point length as two
-// 32-bit limbs with IMAD.WIDE.U32 (0/1 bit x limb + u64 accumulator) on the
-// integer/FMA pipes instead of DFMA on the FP64 pipe. Exact: a column has at
-// most ~2^14 heavy bits, so each 64-bit limb sum stays below 2^46.
-__global__ void sp_ilimbs_kernel(const double2* __restrict__ limbs, int64_t count, int32_t lo_bits,
-                                 uint2* __restrict__ il) {
-  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
-       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const double2 L = limbs[i];
-    const unsigned long long v = (static_cast<unsigned long long>(L.x) << lo_bits) +
-                                 static_cast<unsigned long long>(L.y);
-    il[i] = make_uint2(static_cast<uint32_t>(v), static_cast<uint32_t>(v >> 32));
-  }
-}
-
-template <int RS>
-__device__ __forceinline__ void heavy_half_int(uint32_t hu, const uint2* __restrict__ Lb,
-                                               const uint32_t (&vv)[RS], unsigned long long (&al)[RS],
-                                               unsigned long long (&ah)[RS]) {
-  while (hu) {
-    int b1, b2;
-    uint32_t m1, m2;
-    next_two(hu, b1, m1, b2, m2);
-    const uint2 L1 = __ldg(Lb + b1);
-    const uint2 L2 = __ldg(Lb + b2);
-#pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const uint32_t f1 = (vv[i] & m1) ? 1u : 0u;
-      const uint32_t f2 = (vv[i] & m2) ? 1u : 0u;
-      // acc += f * L as one IMAD.WIDE.U32 each (the compiler would otherwise
-      // select and add in two 32-bit halves)
-      asm("mad.wide.u32 %0, %2, %3, %0;\n\tmad.wide.u32 %1, %2, %4, %1;"
-          : "+l"(al[i]), "+l"(ah[i]) : "r"(f1), "r"(L1.x), "r"(L1.y));
-      asm("mad.wide.u32 %0, %2, %3, %0;\n\tmad.wide.u32 %1, %2, %4, %1;"
-          : "+l"(al[i]), "+l"(ah[i]) : "r"(f2), "r"(L2.x), "r"(L2.y));
-    }
-  }
-}
-
-template <class Real, int RS, int NW, int MINB>
-__global__ void __launch_bounds__(32 * NW, MINB) stripe_split_int_kernel(const SplitArgs a, const uint2* il) {
-  const int lane = threadIdx.x & 31;
-  const int k = blockIdx.x * NW + (threadIdx.x >> 5);
-  const int n = a.n;
-  if (k >= n) return;
-  const int s0 = a.s_begin + blockIdx.y * 32 * RS;
-  const int64_t n_ext = a.n_ext;
-  const int Hw = static_cast<int>((*a.n_heavy + 63u) / 64u);
-  const int64_t l0 = static_cast<int64_t>(k) + s0 + 1 + lane;
-  int nvalid = 0;
-#pragma unroll
-  for (int i = 0; i < RS; ++i) nvalid += (s0 + lane + 32 * i < a.s_end) ? 1 : 0;
-  const int wvalid = __reduce_add_sync(0xffffffffu, nvalid);
-  unsigned long long ubits = 0;
-  unsigned long long al[RS], ah[RS];
-#pragma unroll
-  for (int i = 0; i < RS; ++i) {
-    al[i] = 0ull;
-    ah[i] = 0ull;
-  }
-#pragma unroll 1
-  for (int w = 0; w < Hw; ++w) {
-    const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
-    const unsigned long long u = __ldg(row + k);
-    if (u == 0ull) continue;
-    const uint2* Lw = il + 64 * static_cast<int64_t>(w);
-    ubits += static_cast<unsigned>(__popcll(u));
-    const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
-    uint32_t vv[RS];
-    if (static_cast<uint32_t>(u >> 32)) {
-#pragma unroll
-      for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
-      heavy_half_int<RS>(static_cast<uint32_t>(u >> 32), Lw + 32, vv, al, ah);
-    }
-    if (static_cast<uint32_t>(u)) {
-#pragma unroll
-      for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
-      heavy_half_int<RS>(static_cast<uint32_t>(u), Lw, vv, al, ah);
-    }
-  }
-  Real* dist = static_cast<Real*>(a.dist);
-  Real* tot = static_cast<Real*>(a.tot);
-  const unsigned long long* xs = a.colsum;
-  const int lb = a.lo_bits;
-  const __int128 C = (static_cast<__int128>(a.cacc[0]) << lb) + static_cast<__int128>(a.cacc[1]);
-#pragma unroll
-  for (int i = 0; i < RS; ++i) {
-    if (i >= nvalid) break;
-    const int s = s0 + lane + 32 * i;
-    const int64_t li = l0 + 32 * i;
-    const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
-    const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
-    const ulonglong2 light =
-        reinterpret_cast<const ulonglong2*>(a.gl)[static_cast<int64_t>(s - a.gl_begin) * n + k];
-    const __int128 G = (static_cast<__int128>(ah[i]) << 32) + static_cast<__int128>(al[i]) +
-                       (static_cast<__int128>(light.x) << lb) + static_cast<__int128>(light.y);
-    const __int128 P = (static_cast<__int128>(xs[2 * n + k] + xs[2 * n + lm]) << lb) +
-                       static_cast<__int128>(xs[3 * n + k] + xs[3 * n + lm]);
-    const __int128 X = (static_cast<__int128>(xs[k] + xs[lm]) << lb) + static_cast<__int128>(xs[n + k] + xs[n + lm]);
-    const __int128 tv = P + C - G;
-    const __int128 dv = X - 2 * G;
-    const Real t = static_cast<Real>(i2_fixed_to_double(tv, a.scale));
-    Real d = static_cast<Real>(i2_fixed_to_double(dv, a.scale));
-    if (a.finalize) d = t == Real(0) ? Real(0) : d / t;
-    dist[off] = d;
-    tot[off] = t;
-  }
-  if (a.counters && lane == 0) {
     atomicAdd(a.counters, ubits * static_cast<unsigned long long>(wvalid));
     atomicAdd(a.counters + 1, 2ull * ubits * static_cast<unsigned long long>(wvalid));
   }

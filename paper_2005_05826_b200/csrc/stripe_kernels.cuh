@@ -304,4 +304,11 @@ __global__ void condense_kernel(const Real* __restrict__ dist, int32_t n, int32_
   }
 }
 
+// Zero diagonal of the n x n matrix (condense writes every off-diagonal entry).
+__global__ void diagonal_zero_kernel(double* __restrict__ out, int32_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i * n + i] = 0.0;
+}
+
 }  // namespace sf

@@ -27,7 +27,7 @@
 
 #include <cstdint>
 
-#include "isect2_kernels.cuh"
+#include "bits.cuh"
 #include "stripe_kernels.cuh"
 #include "wsparse_kernels.cuh"
 

@@ -820,9 +820,28 @@ def compute_unifrac_to_strf(tree: PhyloTree, table: SampleTable, cfg: KernelConf
 def compute_distance_matrix(tree: PhyloTree, table: SampleTable, cfg: KernelConfig,
                             threads: int = 1, counters: Optional[KernelCounters] = None,
                             real=None, exec_options: Optional[ExecOptions] = None) -> DistanceMatrix:
-    """compute_distance_matrix<Real> (kernels.hpp:319-326)."""
-    parts = [compute_unifrac(tree, table, cfg, 0, -1, threads, counters, real, exec_options)]
-    return condense(parts, table.sample_ids)
+    """compute_distance_matrix<Real> (kernels.hpp:319-326): the stripes stay
+    on the device; condense (stripes.cpp:68-129) runs there and the n x n
+    matrix is copied to the host once (sf_compute_distance_matrix)."""
+    _check_cfg(cfg, real)
+    n = table.n_samples()
+    S = total_stripes(n)
+    problem = flatten(tree, table)
+    eo = exec_options or ExecOptions()
+    ex, _keep = N.make_exec(eo.devices, eo.kernel, eo.exact, eo.mem_budget_bytes, cfg.alpha)
+    out = np.empty((n, n), dtype=np.float64)
+    st = N.sf_stats()
+    rc = N.lib().sf_compute_distance_matrix(problem.ref, int(cfg.metric), int(cfg.precision), N.ptr(out),
+                                            C.byref(ex), C.byref(st))
+    if rc != N.SF_OK:
+        msg = N.lib().sf_last_error().decode()
+        if "duplicated" in msg:
+            raise Error("condense: duplicated slot disagrees")
+        raise Error(msg)
+    if counters is not None:
+        E = problem.n_rows
+        counters += _counters_for(cfg, E, S * n, -(-E // cfg.batch_capacity))
+    return DistanceMatrix(list(table.sample_ids), out, cfg.precision)
 
 
 # --------------------------------------------------------------- embedding

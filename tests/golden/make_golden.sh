@@ -9,4 +9,6 @@ make -s -C "$here/../../oracle" -j8
 "$here/../../oracle/_ref/ref_driver" golden "$here" /root/reference/proj/data
 gzip -f -9 "$here/instances_medium.json"
 "$here/../../oracle/_ref/ref_driver" mantel_golden "$here"
+"$here/../../oracle/_ref/ref_driver" wide_golden "$here"
+gzip -f -9 "$here/instances_wide.json"
 "$here/../../oracle/_ref/ref_driver" strf_golden "$here" /root/reference/proj/data

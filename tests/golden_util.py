@@ -25,6 +25,7 @@ def all_cases():
     cases += load("hand.json")
     cases += load("instances_small.json")
     cases += load("instances_medium.json.gz")
+    cases += load("instances_wide.json.gz")
     return cases
 
 
