@@ -77,15 +77,15 @@ def log(*a):
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons during the timed region."""
 
-    def __init__(self, index: int):
-        self.index = index
+    def __init__(self, index):
+        self.index = index if isinstance(index, str) else str(index)
         self.proc = None
         self.lines = []
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index),
+                ["nvidia-smi", "-i", self.index,
                  "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
@@ -135,6 +135,40 @@ def dist_env():
     return world, rank, local
 
 
+def host_description() -> dict:
+    """CPU model, host threads and RAM of the machine the CPU legs ran on."""
+    model, ram = None, None
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemTotal"):
+                ram = round(int(ln.split()[1]) / 1048576, 1)
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "host_threads": os.cpu_count(), "ram_gib": ram}
+
+
+def resolve_devices(gpus: int, world: int, visible: int):
+    """Devices this process drives. Under torchrun each rank drives its
+    LOCAL_RANK device (returns None) and --gpus must equal WORLD_SIZE; a
+    single process with --gpus N > 1 shards the stripes over devices
+    0..N-1 in-process (sf_exec.devices). Asking for more GPUs than are
+    visible fails loudly."""
+    if gpus < 1:
+        raise SystemExit(f"bench: --gpus must be >= 1 (got {gpus})")
+    if world > 1:
+        if gpus != world:
+            raise SystemExit(f"bench: --gpus {gpus} but WORLD_SIZE={world}: launch one rank per GPU")
+        return None
+    if gpus > visible:
+        raise SystemExit(f"bench: --gpus {gpus} requested but only {visible} sm_100 device(s) are visible")
+    return list(range(gpus))
+
+
 def make_problem(cfg):
     from paper_2005_05826_b200 import stripefrac as sf
     t0 = time.perf_counter()
@@ -157,19 +191,37 @@ def measured_fp_peak(device: int, prec: str) -> float:
     return max(fn(device, 4000) for _ in range(3))
 
 
+def ncu_traffic(cfg_name: str, kernel: str):
+    """DRAM bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)
+    of the dominant kernel from the committed `ncu --set full` capture of
+    this config (profiles/ncu_traffic.json, written by tools/ncu_summary.py
+    --traffic), with the stripes it covered; None when there is none."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if not p.exists():
+        return None
+    rec = json.loads(p.read_text()).get(f"{cfg_name}:{kernel}")
+    return rec
+
+
 def run_ours(args, cfg):
     from paper_2005_05826_b200 import _native as N
     from paper_2005_05826_b200 import shard
     world, rank, local = dist_env()
     torch = None
+    t_ctx = time.perf_counter()
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     L = N.lib()
-    if L.sf_device_count() < 1:
+    visible = L.sf_device_count()  # first CUDA call of the process: context creation
+    t_ctx = time.perf_counter() - t_ctx
+    if visible < 1:
         raise SystemExit("bench: no sm_100 device visible")
+    devices = resolve_devices(args.gpus, world, visible)
+    my_devs = devices if devices is not None else [local]
+    n_gpus = world if world > 1 else len(my_devs)
     metric = METRIC_CODE[cfg["metric"]]
     prec = 8 if cfg["precision"] == "fp64" else 4
     problem = make_problem(cfg)
@@ -178,44 +230,53 @@ def run_ours(args, cfg):
     stop_all = min(S, args.stripes) if args.stripes else S
     a, b = shard.rank_range(0, stop_all, rank, world)
     kernel = KERNELS[args.kernel]
-    ex, _keep = N.make_exec([local], kernel, alpha=cfg.get("alpha", 1.0))
+    ex, _keep = N.make_exec(my_devs, kernel, alpha=cfg.get("alpha", 1.0))
     plan = C.c_void_p()
     t0 = time.perf_counter()
     N.check(L.sf_plan_create(problem.ref, metric, prec, a, b, C.byref(ex), C.byref(plan)))
-    log(f"rank {rank}: plan stripes [{a},{b}) created in {time.perf_counter() - t0:.2f}s")
+    cold_plan_s = time.perf_counter() - t0
+    log(f"rank {rank}: plan stripes [{a},{b}) on devices {my_devs} created in {cold_plan_s:.2f}s "
+        f"(context {t_ctx:.2f}s)")
     st = N.sf_stats()
 
     def one_step():
+        w0 = time.perf_counter()
         N.check(L.sf_plan_run(plan, 1))
         N.check(L.sf_plan_sync(plan))
+        wall_ms = (time.perf_counter() - w0) * 1e3
         N.check(L.sf_plan_stats(plan, C.byref(st)))
-        return st.total_ms, st.stripe_ms, st.embed_ms, st.updates_exec, st.launches, st.fp64_ops
+        return st.total_ms, st.stripe_ms, st.embed_ms, st.updates_exec, st.launches, st.fp64_ops, wall_ms
 
     for i in range(args.warmup):
         r = one_step()
-        log(f"rank {rank}: warmup {i}: {r[0]:.1f} ms (stripe {r[1]:.1f}, prep {r[2]:.1f})")
+        log(f"rank {rank}: warmup {i}: {r[0]:.1f} ms (stripe {r[1]:.1f}, prep {r[2]:.1f}, host wall {r[6]:.1f})")
 
     def barrier():
         if world > 1:
             torch.distributed.barrier()
 
     barrier()
-    dev_ms, str_ms, emb_ms, uexec, launches, fp64_ops = [], [], [], 0, 0, 0
-    with ClockSampler(local) as clocks:
+    dev_ms, str_ms, emb_ms, wall_ms, uexec, launches, fp64_ops = [], [], [], [], 0, 0, 0
+    with ClockSampler(",".join(str(d) for d in my_devs)) as clocks:
         w0 = time.perf_counter()
         for _ in range(args.steps):
-            tms, sms, ems, ue, ln, fo = one_step()
+            tms, sms, ems, ue, ln, fo, wms = one_step()
             dev_ms.append(tms)
             str_ms.append(sms)
             emb_ms.append(ems)
+            wall_ms.append(wms)
             uexec += ue
             launches += ln
             fp64_ops += fo
         barrier()
         wall = time.perf_counter() - w0
-    total_dev_s = sum(dev_ms) / 1e3
+    # one device: CUDA events on the plan's stream; several devices in one
+    # process: the host clock around run + sync (it includes the launch
+    # stagger between devices, which per-device events would hide); torchrun:
+    # each rank's device time, max over ranks
+    step_s = (sum(wall_ms) if len(my_devs) > 1 else sum(dev_ms)) / 1e3
     dev = "cuda" if world > 1 else None
-    total_dev_s = shard.max_over_ranks(total_dev_s, dev)
+    total_dev_s = shard.max_over_ranks(step_s, dev)
     wall = shard.max_over_ranks(wall, dev)
     uexec_all = shard.sum_over_ranks(float(uexec), dev)
     u_alg_step = E * stop_all * n
@@ -227,12 +288,11 @@ def run_ours(args, cfg):
 
     # ---- e2e through the public C ABI: host problem in, host stripes out
     e2e = None
+    dm_leg = None
     if not args.no_e2e:
-        import torch as _t
         w = 8 if prec == 8 else 4
-        dt = _t.float64 if prec == 8 else _t.float32
-        dist_h = _t.empty(((b - a) * n,), dtype=dt, pin_memory=True).numpy()
-        tot_h = _t.empty(((b - a) * n,), dtype=dt, pin_memory=True).numpy() if metric != 2 else None
+        dist_h = pinned_empty((b - a) * n, prec)
+        tot_h = pinned_empty((b - a) * n, prec) if metric != 2 else None
         st2 = N.sf_stats()
         times = []
         # one untimed call first (first-touch of the pinned pages, allocator)
@@ -253,60 +313,35 @@ def run_ours(args, cfg):
                problem.sample_totals.nbytes)
         d2h = (b - a) * n * w * (2 if metric != 2 else 1)
         e2e = {"value": u_alg_step / e2e_s, "unit": "updates/s", "seconds_per_dm": e2e_s,
+               "calls": len(times), "host_buffers": "pinned",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        del dist_h, tot_h
+        # compute_distance_matrix (kernels.hpp:319-326) into a pageable n x n
+        # matrix (what the C++/Python API hands out): condense on device
+        if world == 1 and not args.stripes and metric != 4 and not args.no_dm:
+            mat = np.empty((n, n), dtype=np.float64)
+            tms = []
+            for i in range(3):
+                t1 = time.perf_counter()
+                N.check(L.sf_compute_distance_matrix(problem.ref, metric, prec, N.ptr(mat), C.byref(ex),
+                                                     C.byref(st2)))
+                tms.append(time.perf_counter() - t1)
+            dm_leg = {"seconds": statistics.median(tms[1:]), "first_call_seconds": tms[0],
+                      "host_buffer": "pageable n x n fp64", "bytes_d2h": n * n * 8,
+                      "api": "sf_compute_distance_matrix (stripes stay on device; condense on device)"}
+            del mat
 
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
         return None
 
-    # ---- roofline of the dominant kernel (K2 stripe update)
-    # the split kernel (unweighted) accumulates exact limbs with DFMA in every
-    # output precision: its pipe is FP64 for the fp32 lines too
-    peak_fma = measured_fp_peak(local, "fp64" if (metric == 1 and fp64_ops > 0) else cfg["precision"])
-    stripe_s = sum(str_ms) / 1e3
-    peak_tf = peak_fma * 2 / 1e12
-    if metric == 1 and fp64_ops > 0:
-        # split kernel (10): the heavy walk issues 2 DFMA (4 flops) per u bit per
-        # live slot; the kernel counts them (stats.fp64_ops = DFMA lane-ops)
-        achieved_tf = fp64_ops * 2 / stripe_s / 1e12 if stripe_s else 0.0
-        roofline = {
-            "bound": "fp64", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
-            "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None,
-            # dram__bytes_read+write of one `ncu --set full` capture of this kernel
-            # (profiles/r01_ncu_split_c3_1024stripes.txt: 0.685 GB + 0.406 GB for
-            # 1024 stripes at C3, heavy threshold 0.03), per launch: scaled by
-            # the stripes it covers
-            "traffic": (round((0.685215e9 + 0.406339e9) / 1024 * stop_all / max(world, 1))
-                        if cfg is CONFIGS["c3"] else None),
-            "traffic_unit": "bytes per launch",
-            "kernel": "stripe_split_kernel (heavy-row walk)",
-            "peak_source": "measured DFMA loop (tools/fp_peaks.cu) on this device, x2 flops/FMA",
-            "work": "fp64_ops = DFMA lane-ops counted by the kernel (2 per u bit per live slot)",
-            "dfma_per_step": int(fp64_ops / args.steps),
-            "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
-            "prep_ms_per_step": round(sum(emb_ms) / args.steps, 3),
-            "algorithmic_speedup_vs_dense_fp64_roofline": round(
-                (E * stop_all * n * args.steps / (sum(dev_ms) / 1e3)) / (peak_fma / 4), 2),
-        }
-    else:
-        fl = FLOPS_PER_UPDATE[metric]
-        achieved_tf = (uexec / max(world, 1) if world > 1 else uexec) * fl / stripe_s / 1e12 if stripe_s else 0.0
-        roofline = {
-            "bound": "fp64" if prec == 8 else "fp32",
-            "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3), "unit": "TFLOP/s",
-            "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None, "traffic": None,
-            "kernel": ("stripe_dense_kernel" if kernel == 1 else
-                       "stripe_wsparse_kernel (present-row walk)" if metric != 1 else "stripe walk"),
-            "peak_source": "measured DFMA/FFMA loop (tools/fp_peaks.cu) on this device",
-            "flops_per_update": fl, "updates_exec_per_step": int(uexec_all / args.steps),
-            "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
-            "embed_ms_per_step": round(sum(emb_ms) / args.steps, 3),
-        }
+    roofline = roofline_record(args, cfg, metric, prec, my_devs[0], world, stop_all, E, n, str_ms, emb_ms,
+                               dev_ms, fp64_ops, uexec, uexec_all, kernel)
 
     # ---- CPU baseline (oracle restatement, bounded sample, all host threads)
     cpu = None
-    if not args.no_cpu_baseline and world == 1 and metric != 4:
+    if not args.no_cpu_baseline and world == 1 and len(my_devs) == 1 and metric != 4:
         sys.path.insert(0, str(ROOT / "tests"))
         import oracle_port
         threads = os.cpu_count() or 1
@@ -320,27 +355,112 @@ def run_ours(args, cfg):
             secs, upd = oracle_port.time_sample(problem, metric, prec, rows, 0, stripes, threads)
         cpu = {"value": upd / secs, "unit": "updates/s", "cores": threads, "kind": "port",
                "sample": f"first {rows} postorder rows x stripes [0,{stripes}) x {n} samples "
-                         f"({upd:.3g} updates, {secs:.2f}s), oracle/stripefrac_oracle.c, -O2 no FMA"}
+                         f"({upd:.3g} updates, {secs:.2f}s), oracle/stripefrac_oracle.c, -O2 no FMA",
+               "host": host_description()}
 
     clk = clocks.summary()
     line = {
         "metric": "UniFrac node x pair updates/s (full distance matrix)",
-        "value": value, "unit": "updates/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_per_step, "full_dm_seconds": ms_per_step / 1e3,
+        "value": value, "unit": "updates/s", "n_gpus": n_gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step,
+        # host to host, in-memory problem -> finalized stripes in host memory
+        "full_dm_seconds": e2e["seconds_per_dm"] if e2e else None,
+        "device_seconds_per_dm": ms_per_step / 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64" if prec == 8 else "f32", "data": "synthetic (reference random_instance, seeded)",
         "config": {"workload": cfg["workload"], "seed": cfg["seed"], "n_samples": n,
                    "tree_tips": cfg["leaves"], "rows_E": E, "density": cfg["density"],
                    "metric": cfg["metric"], "stripes": [0, stop_all],
                    **({"alpha": cfg["alpha"]} if "alpha" in cfg else {}),
-                   "parallelism": f"stripe-range x{world}", "kernel": args.kernel,
-                   "l2": "inputs larger than L2 (no flush)"},
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clk,
-        "gpu_launches": int(launches), "wall_seconds_timed": wall,
+                   "parallelism": (f"stripe ranges over {world} ranks (torchrun, one GPU each)" if world > 1
+                                   else f"stripe ranges over {len(my_devs)} device(s) in one process"),
+                   "kernel": args.kernel, "l2": "inputs larger than L2 (no flush)",
+                   "step_timer": ("CUDA events (max over ranks)" if len(my_devs) == 1
+                                  else "host clock around run+sync over all devices")},
+        "e2e": e2e, "distance_matrix_e2e": dm_leg, "roofline": roofline, "cpu_baseline": cpu,
+        "clocks": clk, "gpu_launches": int(launches), "wall_seconds_timed": wall,
+        "cold_start": {"context_init_seconds": round(t_ctx, 3), "first_plan_create_seconds": round(cold_plan_s, 3),
+                       "note": "first CUDA call + first plan of the process (pool, module load, first "
+                               "allocations); the e2e calls above are warm"},
     }
     if world > 1:
         torch.distributed.destroy_process_group()
     return line
+
+
+def pinned_empty(count: int, prec: int):
+    import torch as _t
+    dt = _t.float64 if prec == 8 else _t.float32
+    return _t.empty((count,), dtype=dt, pin_memory=True).numpy()
+
+
+def roofline_record(args, cfg, metric, prec, device, world, stop_all, E, n, str_ms, emb_ms, dev_ms, fp64_ops,
+                    uexec, uexec_all, kernel):
+    """The dominant kernel's roofline (rank 0's share of the work)."""
+    stripe_s = sum(str_ms) / 1e3
+    cfg_name = args.config
+    if metric == 1 and fp64_ops > 0:
+        # split kernel (10): the heavy walk issues 2 DFMA (4 flops) per u bit
+        # per live slot, counted by the kernel (stats.fp64_ops = DFMA lane-ops);
+        # it accumulates exact limbs with DFMA in every output precision
+        peak_fma = measured_fp_peak(device, "fp64")
+        peak_tf = peak_fma * 2 / 1e12
+        achieved_tf = fp64_ops * 2 / stripe_s / 1e12 if stripe_s else 0.0
+        tr = ncu_traffic(cfg_name, "stripe_split_kernel")
+        traffic = None
+        if tr:  # per launch of the bench's step: scale the capture's stripes to this launch
+            traffic = round(tr["dram_bytes"] / tr["stripes"] * (stop_all / max(world, 1)))
+        return {
+            "bound": "fp64", "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3),
+            "unit": "TFLOP/s", "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None,
+            "traffic": traffic, "traffic_unit": "DRAM bytes per launch",
+            "traffic_source": (f"{tr['source']} ({tr['stripes']} stripes, scaled per stripe)" if tr else None),
+            "kernel": "stripe_split_kernel (heavy-row walk, kernel 10)",
+            "peak_source": "measured DFMA loop (tools/fp_peaks.cu) on this device, x2 flops/FMA",
+            "work": "fp64_ops = DFMA lane-ops counted by the kernel (2 per u bit per live slot)",
+            "dfma_per_step": int(fp64_ops / args.steps),
+            "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
+            "prep_ms_per_step": round(sum(emb_ms) / args.steps, 3),
+            "algorithmic_speedup_vs_dense_fp64_roofline": round(
+                (E * stop_all * n * args.steps / (sum(dev_ms) / 1e3)) / (peak_fma / 4), 2),
+        }
+    if metric != 1 and fp64_ops > 0:
+        # u-walk (12): the kernel counts the FP64-pipe instructions x live
+        # lanes it issues (its accumulators are fp64 in both precisions)
+        peak_fma = measured_fp_peak(device, "fp64")
+        peak_tf = peak_fma * 2 / 1e12
+        achieved_tf = fp64_ops * 2 / stripe_s / 1e12 if stripe_s else 0.0
+        tr = ncu_traffic(cfg_name, "stripe_wuwalk_kernel")
+        return {
+            "bound": "fp64", "achieved": round(achieved_tf, 3),
+            "peak": round(peak_tf, 3), "unit": "TFLOP/s",
+            "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None,
+            "traffic": round(tr["dram_bytes"] / tr["stripes"] * stop_all) if tr else None,
+            "traffic_unit": "DRAM bytes per launch",
+            "traffic_source": (f"{tr['source']} ({tr['stripes']} stripes, scaled per stripe)" if tr else None),
+            "kernel": "stripe_wuwalk_kernel (u-walk, kernel 12)",
+            "peak_source": "measured DFMA/FFMA loop (tools/fp_peaks.cu) on this device, x2 flops/FMA",
+            "work": ("fp64_ops = FP64-pipe instructions x live lanes counted by the kernel (1 DFMA per u row "
+                     "and slot, 8 per shared row), reported as 2 flops each against the DFMA peak"),
+            "fma_per_step": int(fp64_ops / args.steps),
+            "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
+            "prep_ms_per_step": round(sum(emb_ms) / args.steps, 3),
+        }
+    peak_fma = measured_fp_peak(device, "fp64" if prec == 8 else "fp32")
+    peak_tf = peak_fma * 2 / 1e12
+    fl = FLOPS_PER_UPDATE[metric]
+    achieved_tf = (uexec / max(world, 1) if world > 1 else uexec) * fl / stripe_s / 1e12 if stripe_s else 0.0
+    return {
+        "bound": "fp64" if prec == 8 else "fp32",
+        "achieved": round(achieved_tf, 3), "peak": round(peak_tf, 3), "unit": "TFLOP/s",
+        "frac": round(achieved_tf / peak_tf, 4) if peak_tf else None, "traffic": None,
+        "kernel": {1: "stripe_dense_kernel", 2: "stripe_sparse_kernel", 11: "stripe_wsparse_kernel"}.get(kernel,
+                                                                                                       "auto"),
+        "peak_source": "measured DFMA/FFMA loop (tools/fp_peaks.cu) on this device",
+        "flops_per_update": fl, "updates_exec_per_step": int(uexec_all / args.steps),
+        "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
+        "embed_ms_per_step": round(sum(emb_ms) / args.steps, 3),
+    }
 
 
 def run_reference(args, cfg):
@@ -367,9 +487,9 @@ def run_reference(args, cfg):
         secs = rec["seconds"][args.warmup:] or rec["seconds"]
         upd = rec["updates_per_rep"]
         kind = "reference"
-        sample = (f"reference compute_unifrac hot loop (Embedder::next_batch + accumulate_stripes, "
-                  f"{threads} std::threads): one 64-row batch x stripes [0,{stripes}) x {n} samples "
-                  f"per step; setup (instance + Embedder) {rec['setup_s']:.1f}s untimed")
+        sample = (f"reference compute_unifrac hot loop, timed per step: Embedder::next_batch + cast_batch + "
+                  f"accumulate_stripes over {threads} std::threads, one 64-row batch x stripes [0,{stripes}) x "
+                  f"{n} samples; setup (instance + Embedder ctor) {rec['setup_s']:.1f}s untimed")
     else:
         sys.path.insert(0, str(ROOT / "tests"))
         import oracle_port
@@ -395,7 +515,7 @@ def run_reference(args, cfg):
                    "tree_tips": cfg["leaves"], "density": cfg["density"], "metric": metric,
                    "parallelism": f"{threads} CPU threads"},
         "cpu_baseline": {"value": value, "unit": "updates/s", "cores": threads, "kind": kind,
-                         "sample": sample},
+                         "sample": sample, "host": host_description()},
         "e2e": {"value": value, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -412,6 +532,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dm", action="store_true", help="skip the compute_distance_matrix leg")
     ap.add_argument("--ref-stripes", type=int, default=256)
     args = ap.parse_args()
     if args.warmup < 3 and not os.environ.get("BENCH_ALLOW_SHORT"):

@@ -534,9 +534,11 @@ int cmd_bench(std::uint64_t seed, int n, int leaves, double density, int subset,
     std::vector<double> secs;
     std::uint64_t updates = 0;
     for (int r = 0; r < reps; ++r) {
+      // timed: the reference's per-batch work, Embedder::next_batch +
+      // cast_batch + accumulate_stripes over the worker split
+      const auto t1 = std::chrono::steady_clock::now();
       auto b64 = em.next_batch(cfg.batch_capacity);
       if (!b64) break;
-      const auto t1 = std::chrono::steady_clock::now();
       const EmbeddingBatch<Real> b = cast_batch<Real>(*b64);
       const int workers = std::min(threads, set.n_stripes());
       std::vector<KernelCounters> partial(static_cast<std::size_t>(workers));

@@ -11,7 +11,12 @@ from pathlib import Path
 
 import numpy as np
 
+import os
+
 LIB_PATH = Path(__file__).resolve().parent / "libstripefrac_cuda.so"
+# A/B only: SF_LIB names an alternative build of the same library (tools/build_ab.sh)
+if os.environ.get("SF_LIB"):
+    LIB_PATH = Path(os.environ["SF_LIB"]).resolve()
 
 SF_OK, SF_EINVAL, SF_ENOMEM, SF_ECUDA, SF_ESTATE = 0, 1, 2, 3, 4
 SF_UNWEIGHTED, SF_WEIGHTED_UNNORMALIZED, SF_WEIGHTED_NORMALIZED = 1, 2, 3

@@ -25,6 +25,7 @@ NVCC_FLAGS = [
     "-lineinfo", "-O3", "-std=c++17",
     "-Xcompiler", "-fPIC,-O3", "-shared",
     "-Xptxas", "-warn-spills",
+    "-lcublasLt", "-Xlinker", "-rpath", "-Xlinker", "/usr/local/cuda/lib64",
 ]
 SOURCES = ["sf_api.cu", "host_prep.cpp"]
 
@@ -43,16 +44,18 @@ def _stale(target: Path, deps) -> bool:
     return any(Path(d).exists() and Path(d).stat().st_mtime > t for d in deps)
 
 
-def build_native(force: bool = False, verbose: bool = False) -> Path:
+def build_native(force: bool = False, verbose: bool = False, out: Path = LIB, defines=()) -> Path:
+    """The product library; `defines` (-D...) and `out` build A/B variants
+    of the same sources (tools/build_ab.sh), never the product path."""
     deps = ([CSRC / s for s in SOURCES] + sorted(CSRC.glob("*.cuh")) + sorted(CSRC.glob("*.hpp")) +
             list((ROOT / "include").glob("*.h")))
-    if force or _stale(LIB, deps):
-        cmd = [_nvcc(), *NVCC_FLAGS, f"-I{ROOT / 'include'}", f"-I{CSRC}",
-               *[str(CSRC / s) for s in SOURCES], "-o", str(LIB)]
+    if force or _stale(out, deps):
+        cmd = [_nvcc(), *NVCC_FLAGS, *defines, f"-I{ROOT / 'include'}", f"-I{CSRC}",
+               *[str(CSRC / s) for s in SOURCES], "-o", str(out)]
         if verbose:
             print(" ".join(cmd))
         subprocess.run(cmd, check=True)
-    return LIB
+    return out
 
 
 PEAKS_SRC = ROOT / "tools" / "fp_peaks.cu"

@@ -3,6 +3,7 @@
 // Host side of compute_unifrac (kernels.hpp:268-316): validate, schedule the
 // postorder embedding in row chunks, shard stripes over devices, launch
 // K1 (embed) -> K2 (stripe update) per chunk, K3 (finalize), copy back.
+#include <cublasLt.h>
 #include <cuda_runtime.h>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -25,6 +26,7 @@
 #include <vector>
 
 #include "embed_kernels.cuh"
+#include "gram_kernels.cuh"
 #include "bits.cuh"
 #include "split_kernels.cuh"
 #include "sf_common.hpp"
@@ -530,6 +532,16 @@ struct DeviceState {
   DevBuf drows, dfix, dcnt, dptr, dmem, dent, dcolsum, dcacc, deepsum, dscantmp;
   size_t dscan_bytes = 0;
   int64_t deep_entries = 0;
+  // heavy rows on the tensor cores (gram_kernels.cuh): 0/1 rows B, digit
+  // table, per-block digit planes A', GEMM output C, cuBLASLt state
+  DevBuf gbits, growdig, gmask, gdj, gA, gC, gws;
+  int64_t gram_kp = 0;
+  int32_t gram_nd = 0;
+  cublasLtHandle_t lt = nullptr;
+  cublasLtMatmulDesc_t lt_op = nullptr;
+  cublasLtMatrixLayout_t lt_a = nullptr, lt_b = nullptr, lt_c = nullptr;
+  cublasLtMatmulAlgo_t lt_algo{};
+  int64_t lt_m = 0, lt_n = 0, lt_k = 0;
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
   DevBuf wnb, woff, wcnt, wpool;
   DevBuf wpoola, wA, wbase;  // kernel 12: generalized pool, column sums, pool base + chunk total
@@ -545,6 +557,11 @@ struct DeviceState {
       if (copy_stream) cudaStreamSynchronize(copy_stream);
       for (auto e : events) cudaEventDestroy(e);
       for (auto e : chunk_events) cudaEventDestroy(e);
+      if (lt_a) cublasLtMatrixLayoutDestroy(lt_a);
+      if (lt_b) cublasLtMatrixLayoutDestroy(lt_b);
+      if (lt_c) cublasLtMatrixLayoutDestroy(lt_c);
+      if (lt_op) cublasLtMatmulDescDestroy(lt_op);
+      if (lt) cublasLtDestroy(lt);
       if (stream) cudaStreamDestroy(stream);
       if (copy_stream) cudaStreamDestroy(copy_stream);
     }
@@ -589,8 +606,26 @@ struct WUWalkCfg {
   static constexpr int RS = 8, NW = 8;
 };
 
+#ifndef SF_SPLIT_V
+#define SF_SPLIT_V 16
+#endif
+#ifndef SF_SPLIT_UC
+#define SF_SPLIT_UC 1
+#endif
+#ifndef SF_SPLIT_NW
+#define SF_SPLIT_NW 8
+#endif
+#ifndef SF_SPLIT_MINB
+#define SF_SPLIT_MINB 2
+#endif
+#ifndef SF_SPLIT_FG
+#define SF_SPLIT_FG 1
+#endif
 struct SplitCfg {
-  static constexpr int RS = 16, NW = 8, SCATTER_NW = 8;
+  static constexpr int V = SF_SPLIT_V, UC = SF_SPLIT_UC, NW = SF_SPLIT_NW, MINB = SF_SPLIT_MINB,
+                       FG = SF_SPLIT_FG;
+  static constexpr int RS = 16;  // light-band stripe height / download chunk unit: 512 stripes
+  static constexpr int SCATTER_NW = 8;
 };
 
 // |X_e| threshold of the split path: rows at or above it are walked.
@@ -607,7 +642,10 @@ int split_heavy_min(int n) {
 int64_t sparse_n_ext(int n) {
   // a whole stripe tile past the last stripe: the widest is the split
   // kernel's 32 * RS (RS <= 16)
-  const int64_t tile = std::max<int64_t>(SparseCfg::TK + SparseCfg::TS, 32 * SplitCfg::RS);
+  // a whole tile past the last stripe: the DFMA walk's 32 V + UC columns, the
+  // tensor-core path's GEMM block (<= 1024 u columns)
+  const int64_t tile = std::max<int64_t>(std::max<int64_t>(SparseCfg::TK + SparseCfg::TS, 1024),
+                                         std::max(32 * SplitCfg::RS, 32 * SplitCfg::V + SplitCfg::UC));
   const int64_t need = static_cast<int64_t>(n) + n / 2 + tile + 64;
   return (need + 3) / 4 * 4;
 }
@@ -891,14 +929,175 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   return split_scatter(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), true);
 }
 
-// 16 slots per lane, 8 u columns per CTA, v words loaded one 32-bit half at
-// a time, at most 128 registers so two CTAs (16 warps) fit per SM.
+// Heavy-walk tile (SplitCfg): V v-slots per lane x UC u columns per warp,
+// NW warps per CTA, MINB CTAs per SM (register cap), FG factors formed
+// ahead of their DFMAs. The tile shape is a compile-time choice
+// (-DSF_SPLIT_V=... etc. builds the A/B libraries of tools/build_ab.sh).
 template <class Real>
 sf_status launch_split(const SplitArgs& a, cudaStream_t st) {
-  constexpr int RS = SplitCfg::RS, NW = SplitCfg::NW;
-  const dim3 grid((a.n + NW - 1) / NW, (a.s_end - a.s_begin + 32 * RS - 1) / (32 * RS));
-  stripe_split_kernel<Real, RS, NW, 2><<<grid, 32 * NW, 0, st>>>(a);
+  constexpr int V = SplitCfg::V, UC = SplitCfg::UC, NW = SplitCfg::NW;
+  const int64_t cols = (static_cast<int64_t>(a.n) + UC - 1) / UC;
+  const dim3 grid(static_cast<unsigned>((cols + NW - 1) / NW),
+                  static_cast<unsigned>((a.s_end - a.s_begin + UC - 1 + 32 * V - 1) / (32 * V)));
+  stripe_split_kernel<Real, V, UC, NW, SplitCfg::MINB, SplitCfg::FG><<<grid, 32 * NW, 0, st>>>(a);
   SF_CUDA(cudaGetLastError());
+  return SF_OK;
+}
+
+// ---- heavy rows on the tensor cores (gram_kernels.cuh) ----------------------
+#define SF_LT(expr)                                                                       \
+  do {                                                                                    \
+    const cublasStatus_t s_ = (expr);                                                     \
+    if (s_ != CUBLAS_STATUS_SUCCESS)                                                      \
+      return fail(SF_ECUDA, std::string(#expr) + " failed: cuBLASLt status " + std::to_string(static_cast<int>(s_))); \
+  } while (0)
+
+// The tensor-core heavy path is the default; SF_HEAVY_GEMM=0 selects the
+// DFMA heavy walk (stripe_split_kernel) for A/B and the bitwise cross-check.
+bool heavy_gemm_enabled() {
+  const char* e = std::getenv("SF_HEAVY_GEMM");
+  return !(e && std::atoi(e) == 0);
+}
+
+// u columns per GEMM block: the window of v columns a block reads is
+// (stripes + BK - 1) wide, so smaller blocks waste less on short stripe
+// ranges; 1024 at the full C3 range.
+int gram_block(int span) {
+  if (const char* e = std::getenv("SF_GRAM_BK")) return std::max(16, std::atoi(e) / 16 * 16);
+  int bk = 1024;
+  while (bk > 128 && span < 4 * bk) bk /= 2;
+  return bk;
+}
+
+// Once per run, after split_build: heavy-row count and digit planes to host,
+// the 0/1 rows B (all n_ext columns) and the digit table.
+sf_status gram_prepare(sf_plan* plan, DeviceState& d, cudaStream_t st) {
+  const int64_t n_ext = sparse_n_ext(plan->n);
+  const int64_t W64 = (static_cast<int64_t>(plan->E) + 63) / 64;
+  if (d.gmask.bytes < 8) SF_TRY(d.gmask.alloc(d.dev, 8, "digit plane mask"));
+  SF_CUDA(cudaMemsetAsync(d.gmask.p, 0, 8, st));
+  // digits of every permuted row (a bound on the heavy rows: all rows)
+  const int64_t kp_max = (W64 * 64 + 127) / 128 * 128;
+  if (d.growdig.bytes < static_cast<size_t>(kp_max) * kMaxDigits)
+    SF_TRY(d.growdig.alloc(d.dev, static_cast<size_t>(kp_max) * kMaxDigits, "row digits"));
+  sp_gram_rowdig_kernel<<<grid_for(kp_max, 256), 256, 0, st>>>(d.fixbit.as<unsigned long long>(),
+                                                                 d.nheavy.as<unsigned int>(), kp_max,
+                                                                 d.growdig.as<int8_t>(), d.gmask.as<unsigned int>());
+  SF_CUDA(cudaGetLastError());
+  unsigned int hm[2] = {0u, 0u};
+  SF_CUDA(cudaMemcpyAsync(hm, d.nheavy.p, 4, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaMemcpyAsync(hm + 1, d.gmask.p, 4, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  const int64_t H = hm[0];
+  const int64_t Kp = std::max<int64_t>(128, (H + 127) / 128 * 128);
+  std::vector<int32_t> dj;
+  for (int j = 0; j < kMaxDigits; ++j)
+    if (hm[1] & (1u << j)) dj.push_back(j);
+  if (dj.empty()) dj.push_back(0);  // no heavy length: one (zero) plane keeps the shapes valid
+  d.gram_kp = Kp;
+  d.gram_nd = static_cast<int32_t>(dj.size());
+  if (d.gdj.bytes < dj.size() * 4) SF_TRY(d.gdj.alloc(d.dev, kMaxDigits * 4, "digit planes"));
+  SF_CUDA(cudaMemcpyAsync(d.gdj.p, dj.data(), dj.size() * 4, cudaMemcpyHostToDevice, st));
+  const size_t bbytes = static_cast<size_t>(n_ext) * static_cast<size_t>(Kp);
+  if (d.gbits.bytes < bbytes) SF_TRY(d.gbits.alloc(d.dev, bbytes, "heavy 0/1 rows"));
+  sp_gram_bits_kernel<<<grid_for((Kp / 64) * n_ext, 256), 256, 0, st>>>(
+      d.nodebits.as<unsigned long long>(), n_ext, d.nheavy.as<unsigned int>(), Kp, d.gbits.as<int8_t>());
+  SF_CUDA(cudaGetLastError());
+  d.launches += 2;
+  return SF_OK;
+}
+
+// cuBLASLt int8 GEMM C (M x N, int32, col-major) = A^T B, A stored K x M and
+// B stored K x N (both K-contiguous), shapes cached per device.
+sf_status gram_matmul(DeviceState& d, int64_t M, int64_t N, int64_t K, const int8_t* A, const int8_t* B, int32_t* C,
+                      cudaStream_t st) {
+  if (!d.lt) SF_LT(cublasLtCreate(&d.lt));
+  if (!d.lt_op) {
+    SF_LT(cublasLtMatmulDescCreate(&d.lt_op, CUBLAS_COMPUTE_32I, CUDA_R_32I));
+    const cublasOperation_t ta = CUBLAS_OP_T, tb = CUBLAS_OP_N;
+    SF_LT(cublasLtMatmulDescSetAttribute(d.lt_op, CUBLASLT_MATMUL_DESC_TRANSA, &ta, sizeof(ta)));
+    SF_LT(cublasLtMatmulDescSetAttribute(d.lt_op, CUBLASLT_MATMUL_DESC_TRANSB, &tb, sizeof(tb)));
+  }
+  constexpr size_t kWorkspace = size_t{64} << 20;
+  if (d.gws.bytes < kWorkspace) SF_TRY(d.gws.alloc(d.dev, kWorkspace, "GEMM workspace"));
+  if (M != d.lt_m || N != d.lt_n || K != d.lt_k) {
+    if (d.lt_a) cublasLtMatrixLayoutDestroy(d.lt_a);
+    if (d.lt_b) cublasLtMatrixLayoutDestroy(d.lt_b);
+    if (d.lt_c) cublasLtMatrixLayoutDestroy(d.lt_c);
+    d.lt_a = d.lt_b = d.lt_c = nullptr;
+    d.lt_m = d.lt_n = d.lt_k = 0;
+    SF_LT(cublasLtMatrixLayoutCreate(&d.lt_a, CUDA_R_8I, static_cast<uint64_t>(K), static_cast<uint64_t>(M), K));
+    SF_LT(cublasLtMatrixLayoutCreate(&d.lt_b, CUDA_R_8I, static_cast<uint64_t>(K), static_cast<uint64_t>(N), K));
+    SF_LT(cublasLtMatrixLayoutCreate(&d.lt_c, CUDA_R_32I, static_cast<uint64_t>(M), static_cast<uint64_t>(N), M));
+    cublasLtMatmulPreference_t pref = nullptr;
+    SF_LT(cublasLtMatmulPreferenceCreate(&pref));
+    struct PrefGuard {
+      cublasLtMatmulPreference_t p;
+      ~PrefGuard() { cublasLtMatmulPreferenceDestroy(p); }
+    } pg{pref};
+    const size_t ws = kWorkspace;
+    SF_LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws, sizeof(ws)));
+    cublasLtMatmulHeuristicResult_t res{};
+    int nres = 0;
+    SF_LT(cublasLtMatmulAlgoGetHeuristic(d.lt, d.lt_op, d.lt_a, d.lt_b, d.lt_c, d.lt_c, pref, 1, &res, &nres));
+    if (nres < 1) return fail(SF_ECUDA, "cuBLASLt has no int8 GEMM for this shape");
+    d.lt_algo = res.algo;
+    d.lt_m = M, d.lt_n = N, d.lt_k = K;
+  }
+  const int32_t alpha = 1, beta = 0;
+  SF_LT(cublasLtMatmul(d.lt, d.lt_op, &alpha, A, d.lt_a, B, d.lt_b, &beta, C, d.lt_c, C, d.lt_c, &d.lt_algo,
+                       d.gws.p, kWorkspace, st));
+  return SF_OK;
+}
+
+// Stripes [c0, c1) of the plan's device: per block of BK u columns, its
+// digit planes, one GEMM against the window of v columns, the epilogue.
+sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, int32_t finalize,
+                   cudaStream_t st) {
+  const int n = plan->n;
+  const int span = c1 - c0;
+  const int bk = gram_block(span);
+  const int64_t Kp = d.gram_kp;
+  const int nd = d.gram_nd;
+  const int64_t M = static_cast<int64_t>(bk) * nd;
+  const int64_t W = span + bk - 1;  // window columns
+  if (d.gA.bytes < static_cast<size_t>(M * Kp)) SF_TRY(d.gA.alloc(d.dev, static_cast<size_t>(M * Kp), "digit planes A"));
+  if (d.gC.bytes < static_cast<size_t>(M * W) * 4) SF_TRY(d.gC.alloc(d.dev, static_cast<size_t>(M * W) * 4, "GEMM output"));
+  GramArgs g;
+  g.C = d.gC.as<int32_t>();
+  g.dj = d.gdj.as<int32_t>();
+  g.nd = nd;
+  g.bk = bk;
+  g.c0 = c0;
+  g.c1 = c1;
+  g.M = M;
+  g.n = n;
+  g.out_begin = d.a;
+  g.gl_begin = gl_begin;
+  g.lo_bits = plan->lo_bits;
+  g.scale = plan->scale;
+  g.finalize = finalize ? 1 : 0;
+  g.levels = plan->levels;
+  g.gl = d.lightsum.as<unsigned long long>();
+  g.colsum = d.colsum.as<unsigned long long>();
+  g.cacc = d.cacc.as<unsigned long long>();
+  g.dist = d.dist.p;
+  g.tot = d.tot.p;
+  for (int k0 = 0; k0 < n; k0 += bk) {
+    sp_gram_digits_kernel<<<grid_for(static_cast<int64_t>(bk) * (Kp / 16), 256), 256, 0, st>>>(
+        d.gbits.as<int8_t>(), Kp, k0, bk, n, d.growdig.as<int8_t>(), d.gdj.as<int32_t>(), nd, d.gA.as<int8_t>());
+    SF_CUDA(cudaGetLastError());
+    const int64_t l_start = static_cast<int64_t>(k0) + c0 + 1;  // < n_ext - W (sparse_n_ext)
+    SF_TRY(gram_matmul(d, M, W, Kp, d.gA.as<int8_t>(), d.gbits.as<int8_t>() + l_start * Kp, d.gC.as<int32_t>(), st));
+    g.k0 = k0;
+    const int64_t slots = static_cast<int64_t>(span) * std::min(bk, n - k0);
+    if (plan->prec == SF_FP64)
+      sp_gram_epilogue_kernel<double><<<grid_for(slots, 256), 256, 0, st>>>(g);
+    else
+      sp_gram_epilogue_kernel<float><<<grid_for(slots, 256), 256, 0, st>>>(g);
+    SF_CUDA(cudaGetLastError());
+    d.launches += 3;
+  }
   return SF_OK;
 }
 
@@ -1227,6 +1426,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         a.dist = d.dist.p;
         a.tot = plan->metric == SF_WEIGHTED_UNNORMALIZED ? nullptr : d.tot.p;
         a.exec_updates = d.exec_ctr.as<unsigned long long>();
+        a.fp64_ops = d.exec_ctr.as<unsigned long long>() + 1;
         SF_TRY(plan->prec == SF_FP64 ? launch_wuwalk<double>(plan->metric, a, st)
                                      : launch_wuwalk<float>(plan->metric, a, st));
         d.launches++;
@@ -1287,6 +1487,21 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       // host destination, chunks of whole 512-stripe tiles whose D2H copy
       // overlaps the next chunk's compute
       const int tile = 32 * SplitCfg::RS;
+      bool gram = heavy_gemm_enabled();
+      if (gram) {
+        // the tensor-core operands are sized by the heavy-row count, known
+        // only now; without the memory for them the DFMA heavy walk (the
+        // same exact sums, bit for bit) takes the heavy rows
+        const sf_status gs = gram_prepare(plan, d, st);
+        if (gs == SF_ENOMEM) {
+          gram = false;
+          cudaGetLastError();
+          if (std::getenv("SF_DEBUG"))
+            std::fprintf(stderr, "stripefrac: device %d: %s; heavy rows on the DFMA walk\n", d.dev, sf::last_error());
+        } else {
+          SF_TRY(gs);
+        }
+      }
       int ci = 0;
       if (host_d && !d.copy_stream) SF_CUDA(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking));
       for (int p0 = d.a; p0 < d.b; p0 += d.light_pass) {
@@ -1301,7 +1516,11 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
           const int c1 = std::min(p1, c0 + step);
           a.s_begin = c0;
           a.s_end = c1;
-          SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+          if (gram) {
+            SF_TRY(gram_run(plan, d, c0, c1, p0, finalize, st));
+          } else {
+            SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
+          }
           if (plan->levels > 1) {  // lengths off the main grid: exact multi-level epilogue
             const int blocks = grid_for(static_cast<int64_t>(c1 - c0) * n, 256);
             if (plan->prec == SF_FP64)

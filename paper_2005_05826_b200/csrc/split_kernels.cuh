@@ -621,14 +621,17 @@ struct SplitArgs {
 };
 
 // One 32-bit half of a heavy u word, two bits per step, branch-free: per
-// bit and slot one LOP3 (v & m, the factor's high word) and two DFMA.
-template <int RS>
+// bit and slot one LOP3 (v & m, the factor's high word) and two DFMA. The
+// factors of FG slots are formed before their DFMAs, so a DFMA does not wait
+// on the LOP3 just before it.
+template <int V, int FG>
 __device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restrict__ Lb,
-                                           const uint32_t (&vv)[RS], double (&gh)[RS], double (&gl)[RS]) {
+                                           const uint32_t (&vv)[V], double (&gh)[V], double (&gl)[V]) {
+  static_assert(V % FG == 0, "factor groups must tile the slots");
   if (hu & 0x80000000u) {  // sign bit: factor 2.0 from the bit shifted to 30
     const double2 L = __ldg(Lb + 31);
 #pragma unroll
-    for (int i = 0; i < RS; ++i) {
+    for (int i = 0; i < V; ++i) {
       const double f = __hiloint2double(static_cast<int>((vv[i] >> 1) & 0x40000000u), 0);
       gh[i] = fma(L.x, f, gh[i]);
       gl[i] = fma(L.y, f, gl[i]);
@@ -645,13 +648,23 @@ __device__ __forceinline__ void heavy_half(uint32_t hu, const double2* __restric
     const double2 L1 = __ldg(Lb + b1);
     const double2 L2 = __ldg(Lb + b2);
 #pragma unroll
-    for (int i = 0; i < RS; ++i) {
-      const double f1 = __hiloint2double(static_cast<int>(vv[i] & m1), 0);
-      const double f2 = __hiloint2double(static_cast<int>(vv[i] & m2), 0);
-      gh[i] = fma(L1.x, f1, gh[i]);
-      gl[i] = fma(L1.y, f1, gl[i]);
-      gh[i] = fma(L2.x, f2, gh[i]);
-      gl[i] = fma(L2.y, f2, gl[i]);
+    for (int i0 = 0; i0 < V; i0 += FG) {
+      double f1[FG], f2[FG];
+#pragma unroll
+      for (int j = 0; j < FG; ++j) {
+        f1[j] = __hiloint2double(static_cast<int>(vv[i0 + j] & m1), 0);
+        f2[j] = __hiloint2double(static_cast<int>(vv[i0 + j] & m2), 0);
+      }
+#pragma unroll
+      for (int j = 0; j < FG; ++j) {
+        gh[i0 + j] = fma(L1.x, f1[j], gh[i0 + j]);
+        gl[i0 + j] = fma(L1.y, f1[j], gl[i0 + j]);
+      }
+#pragma unroll
+      for (int j = 0; j < FG; ++j) {
+        gh[i0 + j] = fma(L2.x, f2[j], gh[i0 + j]);
+        gl[i0 + j] = fma(L2.y, f2[j], gl[i0 + j]);
+      }
     }
   }
 }
@@ -733,49 +746,76 @@ __global__ void sp_deep_epilogue_kernel(const SplitArgs a) {
   }
 }
 
-template <class Real, int RS, int NW, int MINB>
+// Warp tile: UC consecutive u columns k0 .. k0+UC-1 x the 32 V v columns
+// l = k0 + s0 + 1 + lane + 32 i (i < V). Slot (k0 + c, l) is stripe
+// s = s0 + lane + 32 i - c, so a tile's stripes shift by one per u column:
+// the grid's y tiles cover [s_begin - UC + 1, s_end) and slots outside
+// [s_begin, s_end) are computed but not written. Every v word a lane loads
+// serves UC u columns.
+template <class Real, int V, int UC, int NW, int MINB, int FG>
 __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const SplitArgs a) {
   const int lane = threadIdx.x & 31;
-  const int k = blockIdx.x * NW + (threadIdx.x >> 5);
+  const int k0 = (blockIdx.x * NW + (threadIdx.x >> 5)) * UC;
   const int n = a.n;
-  if (k >= n) return;
-  const int s0 = a.s_begin + blockIdx.y * 32 * RS;
+  if (k0 >= n) return;
+  const int s0 = a.s_begin + blockIdx.y * 32 * V;
   const int64_t n_ext = a.n_ext;
   const int Hw = static_cast<int>((*a.n_heavy + 63u) / 64u);
   // v column of slot i: l0 + 32 i (< n_ext for every i: n_ext covers a whole
   // tile past the last stripe, so dead slots read real words and are dropped)
-  const int64_t l0 = static_cast<int64_t>(k) + s0 + 1 + lane;
-  int nvalid = 0;
+  const int64_t l0 = static_cast<int64_t>(k0) + s0 + 1 + lane;
+  int nvalid[UC];
+  int wvalid[UC];
 #pragma unroll
-  for (int i = 0; i < RS; ++i) nvalid += (s0 + lane + 32 * i < a.s_end) ? 1 : 0;
-  const int wvalid = __reduce_add_sync(0xffffffffu, nvalid);  // live slots of the warp
-  unsigned long long ubits = 0;
-
-  double gh[RS], gl[RS];
+  for (int c = 0; c < UC; ++c) {
+    nvalid[c] = 0;
 #pragma unroll
-  for (int i = 0; i < RS; ++i) {
-    gh[i] = 0.0;
-    gl[i] = 0.0;
+    for (int i = 0; i < V; ++i) {
+      const int s = s0 + lane + 32 * i - c;
+      nvalid[c] += (k0 + c < n && s >= a.s_begin && s < a.s_end) ? 1 : 0;
+    }
+    wvalid[c] = __reduce_add_sync(0xffffffffu, nvalid[c]);  // live slots of the warp in column c
   }
+  unsigned long long work = 0;  // sum over columns of u bits x live slots
+
+  double gh[UC][V], gl[UC][V];
+#pragma unroll
+  for (int c = 0; c < UC; ++c)
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      gh[c][i] = 0.0;
+      gl[c][i] = 0.0;
+    }
 #pragma unroll 1
   for (int w = 0; w < Hw; ++w) {
     const unsigned long long* row = a.nx + static_cast<int64_t>(w) * n_ext;
-    const unsigned long long u = __ldg(row + k);
-    if (u == 0ull) continue;
+    unsigned long long u[UC];
+    unsigned long long any = 0ull;
+#pragma unroll
+    for (int c = 0; c < UC; ++c) {
+      u[c] = k0 + c < n ? __ldg(row + k0 + c) : 0ull;
+      any |= u[c];
+    }
+    if (any == 0ull) continue;
     const double2* Lw = a.limbs + 64 * static_cast<int64_t>(w);
-    ubits += static_cast<unsigned>(__popcll(u));
+#pragma unroll
+    for (int c = 0; c < UC; ++c) work += static_cast<unsigned long long>(__popcll(u[c])) * wvalid[c];
     // one 32-bit half of the v words live at a time (fewer registers)
     const uint32_t* row32 = reinterpret_cast<const uint32_t*>(row);
-    uint32_t vv[RS];
-    if (static_cast<uint32_t>(u >> 32)) {
+    uint32_t vv[V];
+    if (static_cast<uint32_t>(any >> 32)) {
 #pragma unroll
-      for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
-      heavy_half<RS>(static_cast<uint32_t>(u >> 32), Lw + 32, vv, gh, gl);
+      for (int i = 0; i < V; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i) + 1);
+#pragma unroll
+      for (int c = 0; c < UC; ++c)
+        if (static_cast<uint32_t>(u[c] >> 32)) heavy_half<V, FG>(static_cast<uint32_t>(u[c] >> 32), Lw + 32, vv, gh[c], gl[c]);
     }
-    if (static_cast<uint32_t>(u)) {
+    if (static_cast<uint32_t>(any)) {
 #pragma unroll
-      for (int i = 0; i < RS; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
-      heavy_half<RS>(static_cast<uint32_t>(u), Lw, vv, gh, gl);
+      for (int i = 0; i < V; ++i) vv[i] = __ldg(row32 + 2 * (l0 + 32 * i));
+#pragma unroll
+      for (int c = 0; c < UC; ++c)
+        if (static_cast<uint32_t>(u[c])) heavy_half<V, FG>(static_cast<uint32_t>(u[c]), Lw, vv, gh[c], gl[c]);
     }
   }
 
@@ -785,37 +825,41 @@ __global__ void __launch_bounds__(32 * NW, MINB) stripe_split_kernel(const Split
   const long long ch = static_cast<long long>(a.cacc[0]);
   const long long cl = static_cast<long long>(a.cacc[1]);
 #pragma unroll
-  for (int i = 0; i < RS; ++i) {
-    if (i >= nvalid) break;
-    const int s = s0 + lane + 32 * i;
-    const int64_t li = l0 + 32 * i;
-    const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
-    const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
-    const int64_t cell = static_cast<int64_t>(s - a.gl_begin) * n + k;
-    const ulonglong2 light = reinterpret_cast<const ulonglong2*>(a.gl)[cell];
-    // accumulators hold exact multiples of 2^-52 below 2
-    const long long Gh_ = __double2ll_rn(gh[i] * 0x1p52) + static_cast<long long>(light.x);
-    const long long Gl_ = __double2ll_rn(gl[i] * 0x1p52) + static_cast<long long>(light.y);
-    const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm]) + ch - Gh_;
-    const long long tl = static_cast<long long>(xs[3 * n + k] + xs[3 * n + lm]) + cl - Gl_;
-    const long long dh = static_cast<long long>(xs[k] + xs[lm]) - 2 * Gh_;
-    const long long dl = static_cast<long long>(xs[n + k] + xs[n + lm]) - 2 * Gl_;
-    if (a.levels > 1) {  // sp_deep_epilogue_kernel finishes the slot
-      reinterpret_cast<longlong2*>(a.gl)[cell] = make_longlong2(Gh_, Gl_);
-      continue;
+  for (int c = 0; c < UC; ++c) {
+    const int k = k0 + c;
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const int s = s0 + lane + 32 * i - c;
+      if (k >= n || s < a.s_begin || s >= a.s_end) continue;
+      const int64_t li = l0 + 32 * i;
+      const int lm = li >= n ? static_cast<int>(li - n) : static_cast<int>(li);
+      const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
+      const int64_t cell = static_cast<int64_t>(s - a.gl_begin) * n + k;
+      const ulonglong2 light = reinterpret_cast<const ulonglong2*>(a.gl)[cell];
+      // accumulators hold exact multiples of 2^-52 below 2
+      const long long Gh_ = __double2ll_rn(gh[c][i] * 0x1p52) + static_cast<long long>(light.x);
+      const long long Gl_ = __double2ll_rn(gl[c][i] * 0x1p52) + static_cast<long long>(light.y);
+      if (a.levels > 1) {  // sp_deep_epilogue_kernel finishes the slot
+        reinterpret_cast<longlong2*>(a.gl)[cell] = make_longlong2(Gh_, Gl_);
+        continue;
+      }
+      const long long th = static_cast<long long>(xs[2 * n + k] + xs[2 * n + lm]) + ch - Gh_;
+      const long long tl = static_cast<long long>(xs[3 * n + k] + xs[3 * n + lm]) + cl - Gl_;
+      const long long dh = static_cast<long long>(xs[k] + xs[lm]) - 2 * Gh_;
+      const long long dl = static_cast<long long>(xs[n + k] + xs[n + lm]) - 2 * Gl_;
+      const __int128 tv = (static_cast<__int128>(th) << a.lo_bits) + tl;
+      const __int128 dv = (static_cast<__int128>(dh) << a.lo_bits) + dl;
+      const Real t = fixed_to_real<Real>(tv, a.scale);
+      Real d = fixed_to_real<Real>(dv, a.scale);
+      if (a.finalize) d = t == Real(0) ? Real(0) : d / t;
+      dist[off] = d;
+      tot[off] = t;
     }
-    const __int128 tv = (static_cast<__int128>(th) << a.lo_bits) + tl;
-    const __int128 dv = (static_cast<__int128>(dh) << a.lo_bits) + dl;
-    const Real t = fixed_to_real<Real>(tv, a.scale);
-    Real d = fixed_to_real<Real>(dv, a.scale);
-    if (a.finalize) d = t == Real(0) ? Real(0) : d / t;
-    dist[off] = d;
-    tot[off] = t;
   }
   if (a.counters && lane == 0) {
-    // ubits is warp-uniform: the warp issued ubits x (live slots) FMA pairs
-    atomicAdd(a.counters, ubits * static_cast<unsigned long long>(wvalid));
-    atomicAdd(a.counters + 1, 2ull * ubits * static_cast<unsigned long long>(wvalid));
+    // work is warp-uniform: the warp issued work FMA pairs on live slots
+    atomicAdd(a.counters, work);
+    atomicAdd(a.counters + 1, 2ull * work);
   }
 }
 

@@ -161,6 +161,7 @@ struct WUWalkArgs {
   void* dist;
   void* tot;  // null for WU
   unsigned long long* exec_updates;
+  unsigned long long* fp64_ops;  // FP64-pipe lane-instructions issued (roofline), or null
   const uint32_t* nz;  // [ceil(W/32)][n] nonzero-word masks (null: scan every word)
   const unsigned long long* nbo;  // [W][n_ext] (offset << 32) | presence word, or null
 };
@@ -201,6 +202,7 @@ __global__ void __launch_bounds__(32 * NW, 2) stripe_wuwalk_kernel(const WUWalkA
     if (GEN) t[i] = 0.0;
   }
   unsigned long long ubits = 0;
+  unsigned hits = 0;  // this lane's shared (u and v present) slot-rows
   // one nonzero presence word w of column k (u != 0)
   auto word = [&](int w, uint32_t u) {
       uint32_t ou;
@@ -244,6 +246,7 @@ __global__ void __launch_bounds__(32 * NW, 2) stripe_wuwalk_kernel(const WUWalkA
           d[i] = fma(Lu, f, d[i]);
           if (GEN) t[i] = fma(Lu, f, t[i]);
           if (hit) {
+            ++hits;
             const uint32_t qv = vo[i] + static_cast<uint32_t>(__popc(vv[i] & below));
             const double v = static_cast<double>(pool[qv]);
             if (GEN) {
@@ -333,6 +336,16 @@ __global__ void __launch_bounds__(32 * NW, 2) stripe_wuwalk_kernel(const WUWalkA
   }
   if (a.exec_updates && lane == 0)
     atomicAdd(a.exec_updates, ubits * static_cast<unsigned long long>(wvalid));
+  if (a.fp64_ops) {
+    // per (u row, live slot): the absent-term DFMA (+ t for generalized);
+    // per shared row: WN/WU d DFMA + fl(L*v) DMUL + TwoSum (5 DADD) + lo DADD = 8,
+    // generalized: d DFMA, t DADD, |u-v|, u+v, TwoSum = 9 (pow and the divide
+    // not counted: a lower bound)
+    const unsigned long long per_hit = GEN ? 9ull : 8ull;
+    unsigned long long h = __reduce_add_sync(0xffffffffu, hits);
+    if (lane == 0)
+      atomicAdd(a.fp64_ops, ubits * static_cast<unsigned long long>(wvalid) * (GEN ? 2ull : 1ull) + h * per_hit);
+  }
 }
 
 // Even n: the last stripe (s = n/2 - 1) holds every pair twice, (k, k+n/2)

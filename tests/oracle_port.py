@@ -90,3 +90,22 @@ def time_sample(problem, metric: int, prec: int, rows: int, start: int, stop: in
     secs = time.perf_counter() - t0
     assert rc == 0
     return secs, rows * (stop - start) * n
+
+
+def sparse_stripes(problem, metric: int, prec: int, start: int = 0, stop: int = -1,
+                   finalize: bool = True, threads: int = 1):
+    """orc_sparse_stripes: the reference's arithmetic over each sample's
+    present rows only (no dense embedding): the checker at C3/C5 scale."""
+    n = problem.n_samples
+    if stop < 0:
+        stop = n // 2
+    dt = np.float64 if prec == 8 else np.float32
+    d = np.zeros((stop - start, n), dt)
+    t = np.zeros((stop - start, n), dt)
+    f = lib().orc_sparse_stripes
+    f.restype = C.c_int
+    f.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int]
+    rc = f(C.cast(C.pointer(problem.struct), C.c_void_p), metric, prec, start, stop, d.ctypes.data,
+           t.ctypes.data if metric != 2 else None, int(finalize), threads)
+    assert rc == 0
+    return d, (t if metric != 2 else None)

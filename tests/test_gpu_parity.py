@@ -846,3 +846,33 @@ def test_weighted_uwalk_combined_cells_bitwise(device_ok, metric, monkeypatch):
                                            1, C.byref(ex), None))
         out.append((d, t))
     assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+def test_heavy_gemm_is_bitwise_the_dfma_walk(device_ok, prec, monkeypatch):
+    """Heavy rows on the tensor cores (int8 digit-plane GEMMs, the default)
+    and on the DFMA walk (SF_HEAVY_GEMM=0) compute the same exact integer
+    sums: bit-identical stripes — mixed, all-heavy and all-light splits,
+    several light passes, wide branch lengths (deep levels), odd/even n,
+    wrap and partial ranges, GEMM blocks narrower than the range."""
+    rng = np.random.default_rng(5)
+    for seed, n, leaves, dens, frac, lp, wide, bk in [
+            (111, 300, 1100, 0.01, "0.02", "0", False, "0"), (112, 257, 700, 0.03, "0.0", "7", False, "64"),
+            (113, 130, 500, 0.05, "0.05", "0", True, "0"), (114, 64, 90, 0.3, "0.6", "0", False, "16")]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        if wide:
+            problem.lengths[:] = 10.0 ** rng.uniform(-30, 0.3, problem.n_rows)
+        monkeypatch.setenv("SF_HEAVY_FRAC", frac)
+        if lp != "0":
+            monkeypatch.setenv("SF_LIGHT_PASS", lp)
+        if bk != "0":
+            monkeypatch.setenv("SF_GRAM_BK", bk)
+        for start, stop in [(0, n // 2), (3, n // 2 - 2)]:
+            monkeypatch.setenv("SF_HEAVY_GEMM", "0")
+            wd, wt, _ = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_SPLIT)
+            monkeypatch.delenv("SF_HEAVY_GEMM")
+            d, t, _ = _gpu_stripes(problem, 1, prec, start, stop, N.KERNEL_SPLIT)
+            assert np.array_equal(d, wd) and np.array_equal(t, wt)
+        for var in ("SF_LIGHT_PASS", "SF_GRAM_BK"):
+            monkeypatch.delenv(var, raising=False)

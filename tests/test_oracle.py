@@ -138,3 +138,54 @@ def test_generalized_alpha1_is_weighted_normalized():
     wd, wt = op.compute_stripes(problem, 3, 8, 0, S)
     assert np.allclose(gt, wt, rtol=1e-13, atol=0)
     assert np.allclose(gd, wd, rtol=1e-12, atol=1e-15)
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c["name"] for c in CASES])
+def test_sparse_oracle_bitwise_against_reference(case):
+    """The sparse restatement (present rows only, no dense embedding: the
+    checker at C3/C5 scale) reproduces the reference's stripes bit for bit."""
+    tree, table = gu.case_inputs(case)
+    prob = sf.flatten(tree, table)
+    n = table.n_samples()
+    for r in case["results"]:
+        m = int(sf.metric_from_name(r["metric"]))
+        p = 8 if r["precision"] == "fp64" else 4
+        gd, gt = gu.stripes(r, n)
+        d, t = op.sparse_stripes(prob, m, p, r["start"], r["stop"], threads=3)
+        assert np.array_equal(d, gd)
+        if gt is not None:
+            assert np.array_equal(t, gt)
+
+
+@pytest.mark.parametrize("metric", [1, 2, 3])
+@pytest.mark.parametrize("prec", [8, 4])
+def test_sparse_oracle_equals_dense_oracle(metric, prec):
+    """Sparse vs dense restatement on seeded instances (leaf subsets, odd and
+    even n, partial ranges, one thread and several), raw and finalized."""
+    for seed, n, leaves, dens, subset in [(301, 60, 400, 0.02, 0), (302, 97, 900, 0.005, 700),
+                                          (303, 40, 60, 0.4, 0)]:
+        inst = sf.random_instance(seed, n, leaves, dens, subset)
+        prob = sf.flatten(inst.tree, inst.table)
+        for start, stop, fin in ((0, n // 2, True), (n // 5, n // 2 - 1, False)):
+            wd, wt = op.compute_stripes(prob, metric, prec, start, stop, finalize=fin)
+            for th in (1, 4):
+                d, t = op.sparse_stripes(prob, metric, prec, start, stop, finalize=fin, threads=th)
+                assert np.array_equal(d, wd)
+                if wt is not None:
+                    assert np.array_equal(t, wt)
+
+
+def test_sparse_oracle_is_the_reference_at_c2():
+    """C2 full range (WN fp64, 5k samples x 50k tips, 1.25e12 reference
+    updates): the sparse restatement's stripes are the reference's own, bit
+    for bit (sha256 of ref_driver's output, tests/golden/reference_hashes.json)."""
+    import hashlib
+    import json
+    import os
+    rec = json.loads((gu.GOLDEN / "reference_hashes.json").read_text())["c2_weighted-normalized_fp64_0_2500"]
+    inst = sf.random_instance(2, 5000, 50000, 0.002, 0, finalize_tree=False)
+    prob = sf.flatten(inst.tree, inst.table)
+    d, t = op.sparse_stripes(prob, 3, 8, 0, 2500, threads=os.cpu_count() or 1)
+    h = hashlib.sha256(d.tobytes())
+    h.update(t.tobytes())
+    assert h.hexdigest() == rec["sha256"]

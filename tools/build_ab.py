@@ -1,0 +1,45 @@
+#!/usr/bin/env python
+"""Build A/B variants of the product library (tile shapes of the split
+kernel) into tools/ab/lib_<name>.so; run them with SF_LIB=<path>. The
+product library itself is built with the defaults (build.py)."""
+import sys
+from concurrent.futures import ThreadPoolExecutor
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+from paper_2005_05826_b200 import build  # noqa: E402
+
+VARIANTS = {
+    "v16u1f1": dict(V=16, UC=1, NW=8, MINB=2, FG=1),
+    "v16u1f4": dict(V=16, UC=1, NW=8, MINB=2, FG=4),
+    "v8u2f1": dict(V=8, UC=2, NW=8, MINB=2, FG=1),
+    "v8u2f4": dict(V=8, UC=2, NW=8, MINB=2, FG=4),
+    "v4u4f4": dict(V=4, UC=4, NW=8, MINB=2, FG=4),
+    "v8u1f4m3": dict(V=8, UC=1, NW=8, MINB=3, FG=4),
+    "v6u2f2m3": dict(V=6, UC=2, NW=8, MINB=3, FG=2),
+    "v4u2f4m4": dict(V=4, UC=2, NW=8, MINB=4, FG=4),
+    "v12u1f4": dict(V=12, UC=1, NW=8, MINB=2, FG=4),
+    "v8u2f2": dict(V=8, UC=2, NW=8, MINB=2, FG=2),
+    "v8u1f2m3": dict(V=8, UC=1, NW=8, MINB=3, FG=2),
+    "v4u2f2m3": dict(V=4, UC=2, NW=8, MINB=3, FG=2),
+    "v16u1f16m1": dict(V=16, UC=1, NW=8, MINB=1, FG=16),
+    "v16u1f8m1": dict(V=16, UC=1, NW=8, MINB=1, FG=8),
+    "v24u1f8m1": dict(V=24, UC=1, NW=8, MINB=1, FG=8),
+    "v32u1f8m1": dict(V=32, UC=1, NW=4, MINB=1, FG=8),
+    "v16u1f4n4m4": dict(V=16, UC=1, NW=4, MINB=4, FG=4),
+}
+
+
+def one(name, cfg):
+    defines = [f"-DSF_SPLIT_{k}={v}" for k, v in cfg.items()]
+    out = ROOT / "tools" / "ab" / f"lib_{name}.so"
+    build.build_native(force=True, out=out, defines=defines)
+    return name
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(VARIANTS)
+    with ThreadPoolExecutor(4) as ex:
+        for n in ex.map(lambda n: one(n, VARIANTS[n]), names):
+            print("built", n)
