@@ -238,6 +238,7 @@ def run_ours(args, cfg):
     log(f"rank {rank}: plan stripes [{a},{b}) on devices {my_devs} created in {cold_plan_s:.2f}s "
         f"(context {t_ctx:.2f}s)")
     st = N.sf_stats()
+    tens = []  # (tensor ops, tensor ms) per step
 
     def one_step():
         w0 = time.perf_counter()
@@ -245,6 +246,7 @@ def run_ours(args, cfg):
         N.check(L.sf_plan_sync(plan))
         wall_ms = (time.perf_counter() - w0) * 1e3
         N.check(L.sf_plan_stats(plan, C.byref(st)))
+        tens.append((st.tensor_ops, st.tensor_ms))
         return st.total_ms, st.stripe_ms, st.embed_ms, st.updates_exec, st.launches, st.fp64_ops, wall_ms
 
     for i in range(args.warmup):
@@ -256,6 +258,7 @@ def run_ours(args, cfg):
             torch.distributed.barrier()
 
     barrier()
+    tens.clear()
     dev_ms, str_ms, emb_ms, wall_ms, uexec, launches, fp64_ops = [], [], [], [], 0, 0, 0
     with ClockSampler(",".join(str(d) for d in my_devs)) as clocks:
         w0 = time.perf_counter()
@@ -337,7 +340,7 @@ def run_ours(args, cfg):
         return None
 
     roofline = roofline_record(args, cfg, metric, prec, my_devs[0], world, stop_all, E, n, str_ms, emb_ms,
-                               dev_ms, fp64_ops, uexec, uexec_all, kernel)
+                               dev_ms, fp64_ops, uexec, uexec_all, kernel, tens)
 
     # ---- CPU baseline (oracle restatement, bounded sample, all host threads)
     cpu = None
@@ -394,11 +397,64 @@ def pinned_empty(count: int, prec: int):
     return _t.empty((count,), dtype=dt, pin_memory=True).numpy()
 
 
+def measured_int8_peak() -> dict:
+    """Dense int8 tensor-core peak measured live on this device: cuBLASLt's
+    int8 GEMM (torch._int_mm) at a large square-ish shape, best of 5."""
+    import torch
+    M, K, N = 8192, 65536, 8192
+    a = torch.ones((M, K), dtype=torch.int8, device="cuda")
+    b = torch.ones((K, N), dtype=torch.int8, device="cuda").t().contiguous().t()
+    torch._int_mm(a, b)
+    torch.cuda.synchronize()
+    best = float("inf")
+    for _ in range(5):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        torch._int_mm(a, b)
+        e.record()
+        torch.cuda.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del a, b
+    torch.cuda.empty_cache()
+    return {"tops": 2 * M * K * N / best / 1e9, "shape": f"{M}x{K}x{N}"}
+
+
 def roofline_record(args, cfg, metric, prec, device, world, stop_all, E, n, str_ms, emb_ms, dev_ms, fp64_ops,
-                    uexec, uexec_all, kernel):
+                    uexec, uexec_all, kernel, tens):
     """The dominant kernel's roofline (rank 0's share of the work)."""
     stripe_s = sum(str_ms) / 1e3
     cfg_name = args.config
+    t_ops = sum(o for o, _ in tens)
+    t_ms = sum(m for _, m in tens)
+    if metric == 1 and t_ops > 0 and t_ms > 0:
+        # split kernel (10), heavy rows on the int8 tensor cores: the GEMMs'
+        # ops (2 per MAC over the M x W x K rectangles issued) / their
+        # CUDA-event time, against the dense int8 peak measured live
+        pk = measured_int8_peak()
+        achieved = t_ops / (t_ms / 1e3) / 1e12
+        bf16 = None
+        try:
+            bf16 = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()).get("bf16_tflops")
+        except (OSError, ValueError):
+            pass
+        tr = ncu_traffic(cfg_name, "heavy_gemm")
+        return {
+            "bound": "tensor", "achieved": round(achieved, 1), "peak": round(pk["tops"], 1),
+            "unit": "TFLOP/s", "unit_note": "int8 tensor-core ops (MAC = 2), exact integer accumulation",
+            "frac": round(achieved / pk["tops"], 4),
+            "traffic": (round(tr["dram_bytes"] / tr["stripes"] * (stop_all / max(world, 1))) if tr else None),
+            "traffic_unit": "DRAM bytes per step (all heavy GEMM launches)",
+            "traffic_source": (f"{tr['source']} ({tr['stripes']} stripes, scaled per stripe)" if tr else None),
+            "kernel": "heavy-row int8 digit-plane GEMMs (cuBLASLt IMMA, tcgen05) of the split path",
+            "peak_source": (f"cuBLASLt int8 GEMM {pk['shape']} measured live on this device (best of 5)"
+                            + (f"; MEASURED_PEAKS bf16 {bf16} TF/s x2 = {2 * bf16:.0f} for reference" if bf16 else "")),
+            "tensor_ops_per_step": int(t_ops / args.steps),
+            "gemm_ms_per_step": round(t_ms / args.steps, 3),
+            "heavy_phase_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
+            "prep_light_ms_per_step": round(sum(emb_ms) / args.steps, 3),
+            "algorithmic_speedup_vs_dense_fp64_roofline": round(
+                (E * stop_all * n * args.steps / (sum(dev_ms) / 1e3)) / (measured_fp_peak(device, "fp64") / 4), 2),
+        }
     if metric == 1 and fp64_ops > 0:
         # split kernel (10): the heavy walk issues 2 DFMA (4 flops) per u bit
         # per live slot, counted by the kernel (stats.fp64_ops = DFMA lane-ops);

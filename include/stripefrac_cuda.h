@@ -99,7 +99,10 @@ typedef struct sf_stats {
   double stripe_ms;      /* device time of the stripe kernels (max over devices) */
   double finalize_ms;    /* device time of finalize (max over devices) */
   double total_ms;       /* device time of the whole run (max over devices) */
-  uint64_t fp64_ops;     /* DFMA lane-ops the split kernel's heavy walk issued (kernel 10; else 0) */
+  uint64_t fp64_ops;     /* FP64-pipe lane-ops of the DFMA heavy walk (kernel 10 with SF_HEAVY_GEMM=0)
+                            or the weighted u-walk (kernel 12); else 0 */
+  uint64_t tensor_ops;   /* int8 tensor-core ops (2 per MAC) of the heavy-row GEMMs (kernel 10) */
+  double tensor_ms;      /* device time of those GEMMs (sum of launches, max over devices) */
 } sf_stats;
 
 /* ---- library ------------------------------------------------------------ */

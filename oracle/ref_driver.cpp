@@ -593,6 +593,48 @@ int cmd_dm(std::uint64_t seed, int n, int leaves, double density, int subset, Me
   return 0;
 }
 
+// dm_multi: one reference instance, several (metric, precision, range)
+// computations: compute_unifrac<Real> per spec "metric:precision:start:stop",
+// stripes (finalized distances, raw totals) to <outdir>/<spec>.bin, one JSON
+// line per spec (tools/reference_at_scale.sh).
+int cmd_dm_multi(std::uint64_t seed, int n, int leaves, double density, int subset, int threads,
+                 const std::string& outdir, int nspec, char** specs) {
+  const auto tg = std::chrono::steady_clock::now();
+  const SynthInstance inst = random_instance(seed, n, leaves, density, subset);
+  const double gen_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - tg).count();
+  for (int i = 0; i < nspec; ++i) {
+    std::string spec = specs[i];
+    std::vector<std::string> f;
+    for (std::size_t a = 0, b; a <= spec.size(); a = b + 1) {
+      b = spec.find(':', a);
+      if (b == std::string::npos) b = spec.size();
+      f.push_back(spec.substr(a, b - a));
+    }
+    if (f.size() != 4) throw Error("spec must be metric:precision:start:stop");
+    const Metric m = metric_from_name(f[0]);
+    const Precision p = precision_from_name(f[1]);
+    const int start = std::atoi(f[2].c_str()), stop = std::atoi(f[3].c_str());
+    const auto t0 = std::chrono::steady_clock::now();
+    std::string blob;
+    if (p == Precision::Fp64) {
+      auto set = compute_unifrac<double>(inst.tree, inst.table, cfg_of(m, p), start, stop, threads, nullptr);
+      blob.append(reinterpret_cast<const char*>(set.distances.data()), set.distances.size() * sizeof(double));
+      blob.append(reinterpret_cast<const char*>(set.totals.data()), set.totals.size() * sizeof(double));
+    } else {
+      auto set = compute_unifrac<float>(inst.tree, inst.table, cfg_of(m, p), start, stop, threads, nullptr);
+      blob.append(reinterpret_cast<const char*>(set.distances.data()), set.distances.size() * sizeof(float));
+      blob.append(reinterpret_cast<const char*>(set.totals.data()), set.totals.size() * sizeof(float));
+    }
+    const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    std::string name = f[0] + "_" + f[1] + "_" + f[2] + "_" + f[3];
+    write_file(outdir + "/" + name + ".bin", blob);
+    std::printf("{\"spec\":\"%s\",\"seconds\":%.3f,\"instance_seconds\":%.3f,\"threads\":%d}\n", name.c_str(),
+                secs, gen_s, threads);
+    std::fflush(stdout);
+  }
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -602,6 +644,9 @@ int main(int argc, char** argv) {
     if (cmd == "golden" && argc >= 4) return cmd_golden(argv[2], argv[3]);
     if (cmd == "mantel_golden" && argc >= 3) return cmd_mantel_golden(argv[2]);
     if (cmd == "wide_golden" && argc >= 3) return cmd_wide_golden(argv[2]);
+    if (cmd == "dm_multi" && argc >= 10)
+      return cmd_dm_multi(std::strtoull(argv[2], nullptr, 10), std::atoi(argv[3]), std::atoi(argv[4]),
+                          std::atof(argv[5]), std::atoi(argv[6]), std::atoi(argv[7]), argv[8], argc - 9, argv + 9);
     if (cmd == "strf_golden" && argc >= 4) return cmd_strf_golden(argv[2], argv[3]);
     if (cmd == "instance" && argc >= 7)
       return cmd_instance(std::strtoull(argv[2], nullptr, 10), std::atoi(argv[3]), std::atoi(argv[4]),

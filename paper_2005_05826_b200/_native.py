@@ -66,6 +66,8 @@ class sf_stats(C.Structure):
         ("finalize_ms", C.c_double),
         ("total_ms", C.c_double),
         ("fp64_ops", C.c_uint64),
+        ("tensor_ops", C.c_uint64),
+        ("tensor_ms", C.c_double),
     ]
 
     def as_dict(self) -> dict:

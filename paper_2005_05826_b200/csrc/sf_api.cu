@@ -510,7 +510,12 @@ struct DeviceState {
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;     // D2H overlapped with the split kernel
   std::vector<cudaEvent_t> chunk_events;  // stripe chunks done (split kernel)
-  std::vector<std::pair<size_t, size_t>> chunk_spans;  // (byte offset, bytes) per chunk event
+  // a finished block of the device's stripes: rows [row0, row0 + rows)
+  // (relative to the device's first stripe) x columns [col0, col0 + cols)
+  struct Span {
+    int64_t row0, rows, col0, cols;
+  };
+  std::vector<Span> chunk_spans;  // one per chunk event
   bool defer_copy = false;  // record chunk events only; the caller stages the copies
   DevBuf lens, feat_ptr, sidx, counts, totals;
   DevBuf dist, tot, emb, pend, exec_ctr;
@@ -528,6 +533,10 @@ struct DeviceState {
   DevBuf lcnt, lptr, lmem, lcur, lscantmp;  // banded light scatter: member CSR + cursors of the light rows
   size_t lscan_bytes = 0;
   bool banded = false;
+  // column-owned light scatter: entries (light rows containing each column)
+  DevBuf ccnt, cptr, cent, cscantmp;
+  size_t cscan_bytes = 0;
+  bool light_columns = false;
   // deeper fixed-point levels: deep rows, their levels, member CSR, per-slot sums
   DevBuf drows, dfix, dcnt, dptr, dmem, dent, dcolsum, dcacc, deepsum, dscantmp;
   size_t dscan_bytes = 0;
@@ -542,6 +551,9 @@ struct DeviceState {
   cublasLtMatrixLayout_t lt_a = nullptr, lt_b = nullptr, lt_c = nullptr;
   cublasLtMatmulAlgo_t lt_algo{};
   int64_t lt_m = 0, lt_n = 0, lt_k = 0;
+  std::vector<cudaEvent_t> gemm_ev;  // (start, end) per heavy GEMM of the run
+  size_t gemm_count = 0;
+  uint64_t gemm_ops = 0;
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
   DevBuf wnb, woff, wcnt, wpool;
   DevBuf wpoola, wA, wbase;  // kernel 12: generalized pool, column sums, pool base + chunk total
@@ -557,6 +569,7 @@ struct DeviceState {
       if (copy_stream) cudaStreamSynchronize(copy_stream);
       for (auto e : events) cudaEventDestroy(e);
       for (auto e : chunk_events) cudaEventDestroy(e);
+      for (auto e : gemm_ev) cudaEventDestroy(e);
       if (lt_a) cublasLtMatrixLayoutDestroy(lt_a);
       if (lt_b) cublasLtMatrixLayoutDestroy(lt_b);
       if (lt_c) cublasLtMatrixLayoutDestroy(lt_c);
@@ -800,6 +813,38 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
     SF_CUDA(cudaGetLastError());
     d.launches += 3;
   }
+  if (d.light_columns) {
+    if (first) {  // column-major entry CSR of the light member lists
+      SF_CUDA(cudaMemsetAsync(d.ccnt.p, 0, static_cast<size_t>(n + 1) * 4, st));
+      const int wblocks = static_cast<int>(std::min<int64_t>((E + 7) / 8, 148 * 16));
+      sp_col_count_kernel<<<wblocks, 256, 0, st>>>(d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E,
+                                                   d.nheavy.as<unsigned int>(), d.ccnt.as<uint32_t>());
+      size_t tmp = d.cscan_bytes;
+      SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cscantmp.p, tmp, d.ccnt.as<uint32_t>(), d.cptr.as<uint32_t>(), n + 1,
+                                            st));
+      uint32_t M = 0;
+      SF_CUDA(cudaMemcpyAsync(&M, d.cptr.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, st));
+      SF_CUDA(cudaMemcpyAsync(d.ccnt.p, d.cptr.p, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, st));
+      SF_CUDA(cudaStreamSynchronize(st));
+      if (d.cent.bytes < static_cast<size_t>(M) * 8 + 8) SF_TRY(d.cent.alloc(d.dev, static_cast<size_t>(M) * 8 + 8, "column entries"));
+      sp_col_fill_kernel<<<wblocks, 256, 0, st>>>(d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E,
+                                                  d.nheavy.as<unsigned int>(), d.ccnt.as<uint32_t>(),
+                                                  d.cent.as<uint2>());
+      SF_CUDA(cudaGetLastError());
+      d.launches += 3;
+    }
+    constexpr int NT = 512;
+    auto* kern = sp_light_column_kernel<NT>;
+    const int smem = 2 * kLightWin * 8;
+    SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<std::min(n, 65535), NT, smem, st>>>(d.cptr.as<uint32_t>(), d.cent.as<uint2>(), d.lptr.as<uint32_t>(),
+                                             d.lmem.as<int32_t>(), d.perm.as<int32_t>(), d.fix.as<unsigned long long>(),
+                                             plan->lo_bits, n, p0, p0, p1, d.lightsum.as<unsigned long long>(),
+                                             d.exec_ctr.as<unsigned long long>());
+    SF_CUDA(cudaGetLastError());
+    d.launches++;
+    return SF_OK;
+  }
   double band_mb = 32.0;  // measured: 32 MB <= 64 MB < 96 MB (profiles/r01_ab_c3_split_band*)
   if (const char* e = std::getenv("SF_LIGHT_BAND_MB")) band_mb = std::max(1e-3, std::atof(e));
   const int SB = 32 * SplitCfg::RS;
@@ -872,7 +917,8 @@ sf_status split_scatter(sf_plan* plan, DeviceState& d, cudaStream_t st, int s0, 
   const int64_t E = plan->E;
   const int heavy_min = split_heavy_min(n);
   const size_t cells = static_cast<size_t>(s1 - s0) * static_cast<size_t>(n);
-  SF_CUDA(cudaMemsetAsync(d.lightsum.p, 0, cells * 16, st));
+  // the column-owned scatter writes every light-sum cell of the pass
+  if (!(d.banded && d.light_columns)) SF_CUDA(cudaMemsetAsync(d.lightsum.p, 0, cells * 16, st));
   if (plan->levels > 1) SF_CUDA(cudaMemsetAsync(d.deepsum.p, 0, cells * 16 * (plan->levels - 1), st));
   SF_TRY(split_scatter_deep(plan, d, st, s0, s1, with_colsum));
   if (d.banded) return split_scatter_banded(plan, d, st, s0, s1, with_colsum);
@@ -1053,7 +1099,7 @@ sf_status gram_matmul(DeviceState& d, int64_t M, int64_t N, int64_t K, const int
 // Stripes [c0, c1) of the plan's device: per block of BK u columns, its
 // digit planes, one GEMM against the window of v columns, the epilogue.
 sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, int32_t finalize,
-                   cudaStream_t st) {
+                   cudaStream_t st, int k_begin, int k_end) {
   const int n = plan->n;
   const int span = c1 - c0;
   const int bk = gram_block(span);
@@ -1083,12 +1129,21 @@ sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, 
   g.cacc = d.cacc.as<unsigned long long>();
   g.dist = d.dist.p;
   g.tot = d.tot.p;
-  for (int k0 = 0; k0 < n; k0 += bk) {
+  for (int k0 = k_begin; k0 < k_end; k0 += bk) {
     sp_gram_digits_kernel<<<grid_for(static_cast<int64_t>(bk) * (Kp / 16), 256), 256, 0, st>>>(
         d.gbits.as<int8_t>(), Kp, k0, bk, n, d.growdig.as<int8_t>(), d.gdj.as<int32_t>(), nd, d.gA.as<int8_t>());
     SF_CUDA(cudaGetLastError());
     const int64_t l_start = static_cast<int64_t>(k0) + c0 + 1;  // < n_ext - W (sparse_n_ext)
+    while (d.gemm_ev.size() < 2 * (d.gemm_count + 1)) {
+      cudaEvent_t e;
+      SF_CUDA(cudaEventCreate(&e));
+      d.gemm_ev.push_back(e);
+    }
+    SF_CUDA(cudaEventRecord(d.gemm_ev[2 * d.gemm_count], st));
     SF_TRY(gram_matmul(d, M, W, Kp, d.gA.as<int8_t>(), d.gbits.as<int8_t>() + l_start * Kp, d.gC.as<int32_t>(), st));
+    SF_CUDA(cudaEventRecord(d.gemm_ev[2 * d.gemm_count + 1], st));
+    ++d.gemm_count;
+    d.gemm_ops += 2ull * static_cast<uint64_t>(M) * static_cast<uint64_t>(W) * static_cast<uint64_t>(Kp);
     g.k0 = k0;
     const int64_t slots = static_cast<int64_t>(span) * std::min(bk, n - k0);
     if (plan->prec == SF_FP64)
@@ -1298,6 +1353,8 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
     d.events.push_back(e);
   }
   SF_CUDA(cudaEventRecord(d.events[0], st));
+  d.gemm_count = 0;
+  d.gemm_ops = 0;
   if (plan->kernel != 10 && plan->kernel != 12) {  // these kernels write every slot
     SF_CUDA(cudaMemsetAsync(d.dist.p, 0, static_cast<size_t>(slots) * w, st));
     if (d.tot.p && plan->metric != SF_WEIGHTED_UNNORMALIZED)
@@ -1504,52 +1561,81 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       }
       int ci = 0;
       if (host_d && !d.copy_stream) SF_CUDA(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking));
+      // a finished block: event, then its D2H copy on the copy stream (or,
+      // pageable destinations, recorded for the caller's staged copies)
+      auto finished = [&](int r0, int r1, int k0, int k1) -> sf_status {
+        if (!host_d) return SF_OK;
+        while (static_cast<int>(d.chunk_events.size()) <= ci) {
+          cudaEvent_t e;
+          SF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+          d.chunk_events.push_back(e);
+        }
+        SF_CUDA(cudaEventRecord(d.chunk_events[static_cast<size_t>(ci)], st));
+        const DeviceState::Span sp{r0 - d.a, r1 - r0, k0, k1 - k0};
+        ++ci;
+        if (d.defer_copy) {
+          d.chunk_spans.push_back(sp);
+          return SF_OK;
+        }
+        SF_CUDA(cudaStreamWaitEvent(d.copy_stream, d.chunk_events[static_cast<size_t>(ci - 1)], 0));
+        const size_t pitch = static_cast<size_t>(n) * w;
+        const size_t off = static_cast<size_t>(sp.row0) * pitch + static_cast<size_t>(sp.col0) * w;
+        SF_CUDA(cudaMemcpy2DAsync(static_cast<char*>(host_d) + off, pitch, d.dist.as<char>() + off, pitch,
+                                  static_cast<size_t>(sp.cols) * w, static_cast<size_t>(sp.rows),
+                                  cudaMemcpyDeviceToHost, d.copy_stream));
+        if (host_t)
+          SF_CUDA(cudaMemcpy2DAsync(static_cast<char*>(host_t) + off, pitch, d.tot.as<char>() + off, pitch,
+                                    static_cast<size_t>(sp.cols) * w, static_cast<size_t>(sp.rows),
+                                    cudaMemcpyDeviceToHost, d.copy_stream));
+        return SF_OK;
+      };
+      auto deep_epilogue = [&](int c0, int c1, int k0, int k1) -> sf_status {
+        if (plan->levels <= 1) return SF_OK;  // lengths off the main grid: exact multi-level epilogue
+        a.s_begin = c0;
+        a.s_end = c1;
+        a.k_begin = k0;
+        a.k_end = k1;
+        const int blocks = grid_for(static_cast<int64_t>(c1 - c0) * (k1 - k0), 256);
+        if (plan->prec == SF_FP64)
+          sp_deep_epilogue_kernel<double><<<blocks, 256, 0, st>>>(a);
+        else
+          sp_deep_epilogue_kernel<float><<<blocks, 256, 0, st>>>(a);
+        SF_CUDA(cudaGetLastError());
+        d.launches++;
+        return SF_OK;
+      };
       for (int p0 = d.a; p0 < d.b; p0 += d.light_pass) {
         const int p1 = std::min(d.b, p0 + d.light_pass);
         if (p0 != d.a) SF_TRY(split_scatter(plan, d, st, p0, p1, false));
         a.gl_begin = p0;
         const int span = p1 - p0;
+        if (gram) {
+          // the GEMM blocks run along the u columns over the whole pass; with
+          // a host destination, every group of blocks (a column strip of the
+          // pass's stripes) is copied while the next group computes
+          const int bk = gram_block(span);
+          const int ngrp = host_d ? std::max(1, std::min(8, n / (2 * bk))) : 1;
+          const int gw = ((n + ngrp - 1) / ngrp + bk - 1) / bk * bk;
+          for (int k0 = 0; k0 < n; k0 += gw) {
+            const int k1 = std::min(n, k0 + gw);
+            SF_TRY(gram_run(plan, d, p0, p1, p0, finalize, st, k0, k1));
+            SF_TRY(deep_epilogue(p0, p1, k0, k1));
+            SF_TRY(finished(p0, p1, k0, k1));
+          }
+          continue;
+        }
+        // DFMA heavy walk: chunks of whole 512-stripe tiles
         const int nch = host_d ? std::max(1, std::min(8, span / (4 * tile))) : 1;
         const int per = (span + nch - 1) / nch;
         const int step = (per + tile - 1) / tile * tile;
-        for (int c0 = p0; c0 < p1; c0 += step, ++ci) {
+        for (int c0 = p0; c0 < p1; c0 += step) {
           const int c1 = std::min(p1, c0 + step);
           a.s_begin = c0;
           a.s_end = c1;
-          if (gram) {
-            SF_TRY(gram_run(plan, d, c0, c1, p0, finalize, st));
-          } else {
-            SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
-          }
-          if (plan->levels > 1) {  // lengths off the main grid: exact multi-level epilogue
-            const int blocks = grid_for(static_cast<int64_t>(c1 - c0) * n, 256);
-            if (plan->prec == SF_FP64)
-              sp_deep_epilogue_kernel<double><<<blocks, 256, 0, st>>>(a);
-            else
-              sp_deep_epilogue_kernel<float><<<blocks, 256, 0, st>>>(a);
-            SF_CUDA(cudaGetLastError());
-            d.launches++;
-          }
+          SF_TRY(plan->prec == SF_FP64 ? launch_split<double>(a, st) : launch_split<float>(a, st));
           d.launches++;
-          if (!host_d) continue;
-          while (static_cast<int>(d.chunk_events.size()) <= ci) {
-            cudaEvent_t e;
-            SF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            d.chunk_events.push_back(e);
-          }
-          SF_CUDA(cudaEventRecord(d.chunk_events[static_cast<size_t>(ci)], st));
-          const size_t off = static_cast<size_t>(c0 - d.a) * n * w;
-          const size_t bytes = static_cast<size_t>(c1 - c0) * n * w;
-          if (d.defer_copy) {
-            d.chunk_spans.emplace_back(off, bytes);
-            continue;
-          }
-          SF_CUDA(cudaStreamWaitEvent(d.copy_stream, d.chunk_events[static_cast<size_t>(ci)], 0));
-          SF_CUDA(cudaMemcpyAsync(static_cast<char*>(host_d) + off, d.dist.as<char>() + off, bytes,
-                                  cudaMemcpyDeviceToHost, d.copy_stream));
-          if (host_t)
-            SF_CUDA(cudaMemcpyAsync(static_cast<char*>(host_t) + off, d.tot.as<char>() + off, bytes,
-                                    cudaMemcpyDeviceToHost, d.copy_stream));
+          SF_TRY(deep_epilogue(c0, c1, 0, n));
+          SF_TRY(finished(c0, c1, 0, n));
         }
       }
       d.launches--;  // counted once more below
@@ -1970,6 +2056,18 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                                                   static_cast<int>(E1), d.stream));
             d.lscan_bytes = tmp;
             SF_TRY(d.lscantmp.alloc(d.dev, tmp, "light scan scratch"));
+            // column-owned light scatter (default; SF_LIGHT_MODE=band: the banded kernel)
+            const char* lm = std::getenv("SF_LIGHT_MODE");
+            d.light_columns = !(lm && std::string(lm) == "band");
+            if (d.light_columns) {
+              SF_TRY(d.ccnt.alloc(d.dev, static_cast<size_t>(n + 1) * 4, "column entry counts"));
+              SF_TRY(d.cptr.alloc(d.dev, static_cast<size_t>(n + 1) * 4, "column entry offsets"));
+              size_t ct = 0;
+              SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, ct, d.ccnt.as<uint32_t>(), d.cptr.as<uint32_t>(), n + 1,
+                                                    d.stream));
+              d.cscan_bytes = ct;
+              SF_TRY(d.cscantmp.alloc(d.dev, ct, "column scan scratch"));
+            }
           }
         }
       } else {
@@ -1998,8 +2096,8 @@ sf_status sf_plan_run(sf_plan* plan, int32_t finalize) {
 
 sf_status sf_plan_sync(sf_plan* plan) {
   if (!plan) return fail(SF_EINVAL, "plan is null");
-  double emb = 0, str = 0, fin = 0, tot = 0;
-  uint64_t exec = 0, fpops = 0;
+  double emb = 0, str = 0, fin = 0, tot = 0, tens = 0;
+  uint64_t exec = 0, fpops = 0, tops = 0;
   for (auto& dp : plan->devs) {
     DeviceState& d = *dp;
     SF_CUDA(cudaSetDevice(d.dev));
@@ -2020,6 +2118,14 @@ sf_status sf_plan_sync(sf_plan* plan) {
     SF_CUDA(cudaEventElapsedTime(&t, d.events[0], d.events[ne - 1]));
     f_ms = f;
     t_ms = t;
+    double g_ms = 0;
+    for (size_t i = 0; i < d.gemm_count; ++i) {
+      float g = 0;
+      SF_CUDA(cudaEventElapsedTime(&g, d.gemm_ev[2 * i], d.gemm_ev[2 * i + 1]));
+      g_ms += g;
+    }
+    tens = std::max(tens, g_ms);
+    tops += d.gemm_ops;
     emb = std::max(emb, e_ms);
     str = std::max(str, s_ms);
     fin = std::max(fin, f_ms);
@@ -2037,6 +2143,8 @@ sf_status sf_plan_sync(sf_plan* plan) {
   plan->stats.total_ms = tot;
   plan->stats.updates_exec = exec;
   plan->stats.fp64_ops = fpops;
+  plan->stats.tensor_ops = tops;
+  plan->stats.tensor_ms = tens;
   plan->stats.updates_alg = static_cast<uint64_t>(plan->E) * static_cast<uint64_t>(plan->stop - plan->start) *
                             static_cast<uint64_t>(plan->n);
   return SF_OK;
@@ -2087,6 +2195,12 @@ void parallel_memcpy(char* dst, const char* src, size_t bytes, unsigned max_thre
   for (auto& t : th) t.join();
 }
 
+// A 2D block (rows x width bytes, device pitch = host pitch) of device
+// memory -> pageable host, through the device's pinned double buffer: as
+// many whole rows per staging block as fit, host threads scatter the rows.
+sf_status staged_d2h_2d(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t pitch, size_t width,
+                        size_t rows, unsigned threads);
+
 // Host threads for the pinned -> pageable copies of one of `ndev` devices
 // downloading at once.
 unsigned copy_threads(size_t ndev) {
@@ -2094,27 +2208,34 @@ unsigned copy_threads(size_t ndev) {
   return std::max(1u, std::min(16u, hw / static_cast<unsigned>(std::max<size_t>(1, ndev))));
 }
 
+// The device's two pinned staging slots (allocated on first use; false when
+// no pinned memory is available). Caller holds S.mu.
+bool ensure_staging(PinnedStaging& S) {
+  constexpr size_t kSlot = 128ull << 20;
+  if (S.slot[0]) return true;
+  for (int i = 0; i < 2; ++i) {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, kSlot, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      if (S.slot[0]) cudaFreeHost(S.slot[0]);
+      S.slot[0] = nullptr;
+      return false;
+    }
+    S.slot[i] = static_cast<char*>(h);
+  }
+  S.bytes = kSlot;
+  return true;
+}
+
 // dsrc (memory of `device`, the current device) -> hdst (pageable host), on cs.
 sf_status staged_d2h(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t bytes, unsigned threads) {
   if (bytes == 0) return SF_OK;
   PinnedStaging& S = staging(device);
   std::lock_guard<std::mutex> lock(S.mu);
-  constexpr size_t kSlot = 128ull << 20;
-  if (!S.slot[0]) {
-    for (int i = 0; i < 2; ++i) {
-      void* h = nullptr;
-      if (cudaHostAlloc(&h, kSlot, cudaHostAllocPortable) != cudaSuccess) {
-        cudaGetLastError();
-        if (S.slot[0]) cudaFreeHost(S.slot[0]);
-        S.slot[0] = nullptr;
-        // no pinned memory to spare: the driver's own pageable path
-        SF_CUDA(cudaMemcpyAsync(hdst, dsrc, bytes, cudaMemcpyDeviceToHost, cs));
-        SF_CUDA(cudaStreamSynchronize(cs));
-        return SF_OK;
-      }
-      S.slot[i] = static_cast<char*>(h);
-    }
-    S.bytes = kSlot;
+  if (!ensure_staging(S)) {  // no pinned memory to spare: the driver's own pageable path
+    SF_CUDA(cudaMemcpyAsync(hdst, dsrc, bytes, cudaMemcpyDeviceToHost, cs));
+    SF_CUDA(cudaStreamSynchronize(cs));
+    return SF_OK;
   }
   cudaEvent_t ev[2];
   SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
@@ -2146,6 +2267,56 @@ sf_status staged_d2h(int device, cudaStream_t cs, const char* dsrc, char* hdst, 
   cudaEventDestroy(ev[0]);
   cudaEventDestroy(ev[1]);
   return rc;
+}
+}  // namespace
+
+namespace {
+sf_status staged_d2h_2d(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t pitch, size_t width,
+                        size_t rows, unsigned threads) {
+  if (rows == 0 || width == 0) return SF_OK;
+  if (width == pitch) return staged_d2h(device, cs, dsrc, hdst, width * rows, threads);
+  PinnedStaging& S = staging(device);
+  std::lock_guard<std::mutex> lock(S.mu);
+  if (!ensure_staging(S)) {  // no pinned memory: the driver's own pageable 2D copy
+    SF_CUDA(cudaMemcpy2DAsync(hdst, pitch, dsrc, pitch, width, rows, cudaMemcpyDeviceToHost, cs));
+    SF_CUDA(cudaStreamSynchronize(cs));
+    return SF_OK;
+  }
+  const size_t per = std::max<size_t>(1, S.bytes / width);  // rows per staging block
+  const size_t nblk = (rows + per - 1) / per;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 2; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } eg{ev};
+  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  SF_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  auto issue = [&](size_t b) -> sf_status {
+    const size_t r0 = b * per, nr = std::min(per, rows - r0);
+    SF_CUDA(cudaMemcpy2DAsync(S.slot[b & 1], width, dsrc + r0 * pitch, pitch, width, nr, cudaMemcpyDeviceToHost, cs));
+    SF_CUDA(cudaEventRecord(ev[b & 1], cs));
+    return SF_OK;
+  };
+  SF_TRY(issue(0));
+  for (size_t b = 0; b < nblk; ++b) {
+    if (b + 1 < nblk) SF_TRY(issue(b + 1));
+    SF_CUDA(cudaEventSynchronize(ev[b & 1]));
+    const size_t r0 = b * per, nr = std::min(per, rows - r0);
+    const char* src = S.slot[b & 1];
+    // scatter the rows over host threads
+    const size_t T = std::max<size_t>(1, std::min<size_t>(threads, nr));
+    std::vector<std::thread> th;
+    auto part = [&](size_t t) {
+      for (size_t r = t; r < nr; r += T) std::memcpy(hdst + (r0 + r) * pitch, src + r * width, width);
+    };
+    for (size_t t = 1; t < T; ++t) th.emplace_back(part, t);
+    part(0);
+    for (auto& x : th) x.join();
+  }
+  return SF_OK;
 }
 }  // namespace
 
@@ -2222,12 +2393,15 @@ sf_status sf_compute_stripes(const sf_problem* p, sf_metric metric, sf_precision
       const sf_status rc = run_device(plan, d, finalize, hd, ht);
       d.defer_copy = false;
       SF_TRY(rc);
+      const size_t pitch = static_cast<size_t>(plan->n) * w;
       for (size_t ci = 0; ci < d.chunk_spans.size(); ++ci) {
         SF_CUDA(cudaEventSynchronize(d.chunk_events[ci]));
-        const size_t co = d.chunk_spans[ci].first, cb = d.chunk_spans[ci].second;
-        SF_TRY(staged_d2h(d.dev, d.copy_stream, d.dist.as<char>() + co, hd + co, cb, threads));
+        const DeviceState::Span& sp = d.chunk_spans[ci];
+        const size_t co = static_cast<size_t>(sp.row0) * pitch + static_cast<size_t>(sp.col0) * w;
+        const size_t width = static_cast<size_t>(sp.cols) * w, rows = static_cast<size_t>(sp.rows);
+        SF_TRY(staged_d2h_2d(d.dev, d.copy_stream, d.dist.as<char>() + co, hd + co, pitch, width, rows, threads));
         if (ht && metric != SF_WEIGHTED_UNNORMALIZED)
-          SF_TRY(staged_d2h(d.dev, d.copy_stream, d.tot.as<char>() + co, ht + co, cb, threads));
+          SF_TRY(staged_d2h_2d(d.dev, d.copy_stream, d.tot.as<char>() + co, ht + co, pitch, width, rows, threads));
       }
       return SF_OK;
     }));

@@ -500,6 +500,114 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
   if (lane == 0 && pairs) atomicAdd(pairs_out, pairs);
 }
 
+// ---- Column-owned light scatter (default). Every slot (s, k) of a light
+// pair is owned by one member, the column k (slot (b - a - 1, a) by a for its
+// partners above, slot (n - (a - b) - 1, a) by a for its partners below), so
+// one CTA per column can accumulate all of that column's light sums in
+// shared memory: the light rows containing the column are its entries (a
+// column-major CSR of the light member lists), each entry walks its row's
+// sorted members from its own position — partners above while the stripe is
+// below the window's end, partners below from the start of the list — and
+// the window (up to kLightWin stripes of (hi, lo) limbs) is written to the
+// light-sum array once. No global atomics; the limb sums are exact integers,
+// so the order of the shared-memory atomics does not change the bits.
+constexpr int kLightWin = 12800;  // stripes per shared-memory window (200 KB of limbs)
+
+// Entries per column: one count per light member (rows with >= 2 members).
+__global__ void sp_col_count_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ lptr,
+                                    int32_t E, const unsigned int* __restrict__ n_heavy,
+                                    uint32_t* __restrict__ ccnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t idx = *n_heavy + warp; idx < E; idx += nwarps) {
+    const uint32_t b0 = lptr[idx];
+    const int x = static_cast<int>(lptr[idx + 1] - b0);
+    if (x < 2) continue;
+    for (int i = lane; i < x; i += 32) atomicAdd(ccnt + lmem[b0 + i], 1u);
+  }
+}
+
+// Column entries: (permuted light row idx, position of the column in the
+// row's member list). Warp per light row, one claim per member.
+__global__ void sp_col_fill_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ lptr,
+                                   int32_t E, const unsigned int* __restrict__ n_heavy,
+                                   uint32_t* __restrict__ cfill, uint2* __restrict__ cent) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t idx = *n_heavy + warp; idx < E; idx += nwarps) {
+    const uint32_t b0 = lptr[idx];
+    const int x = static_cast<int>(lptr[idx + 1] - b0);
+    if (x < 2) continue;  // no pair
+    for (int i = lane; i < x; i += 32) {
+      const uint32_t pos = atomicAdd(cfill + lmem[b0 + i], 1u);
+      cent[pos] = make_uint2(static_cast<uint32_t>(idx), static_cast<uint32_t>(i));
+    }
+  }
+}
+
+__device__ __forceinline__ void shared_add_u64(unsigned long long* p, unsigned long long v) {
+  atomicAdd(p, v);  // ATOMS.CAS loop on sm_100a; exact (integer limbs)
+}
+
+// One CTA per column k: stripes [s0, s1) of the light sums (rows relative to
+// the pass start p0), in windows of kLightWin stripes.
+template <int NT>
+__global__ void __launch_bounds__(NT) sp_light_column_kernel(
+    const uint32_t* __restrict__ cptr, const uint2* __restrict__ cent, const uint32_t* __restrict__ lptr,
+    const int32_t* __restrict__ lmem, const int32_t* __restrict__ perm, const unsigned long long* __restrict__ fix,
+    int32_t lo_bits, int32_t n, int32_t p0, int32_t s0, int32_t s1, unsigned long long* __restrict__ gl,
+    unsigned long long* __restrict__ pairs_out) {
+  extern __shared__ unsigned long long lacc[];  // [win][2]
+  const int S = n / 2;
+  const int send = min(s1, S);
+  unsigned long long pairs = 0;
+  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+    const uint32_t e0 = cptr[k], e1 = cptr[k + 1];
+    for (int w0 = s0; w0 < send; w0 += kLightWin) {
+      const int w1 = min(send, w0 + kLightWin);
+      const int ww = w1 - w0;
+      for (int i = threadIdx.x; i < 2 * ww; i += NT) lacc[i] = 0ull;
+      __syncthreads();
+      for (uint32_t e = e0 + threadIdx.x; e < e1; e += NT) {
+        const uint2 en = cent[e];
+        const uint32_t b0 = lptr[en.x];
+        const int x = static_cast<int>(lptr[en.x + 1] - b0);
+        const int i = static_cast<int>(en.y);
+        const int32_t* mem = lmem + b0;
+        const ulonglong2 L = ilimbs_of(__ldg(fix + perm[en.x]), lo_bits);
+        // partners above: slot (b - k - 1, k), b in [k + w0 + 1, k + w1]
+        int j = w0 > 0 ? lower_bound_i32(mem, i + 1, x, k + w0 + 1) : i + 1;
+        for (; j < x; ++j) {
+          const int s = __ldg(mem + j) - k - 1;
+          if (s >= w1) break;
+          unsigned long long* c = lacc + 2 * (s - w0);
+          shared_add_u64(c, L.x);
+          shared_add_u64(c + 1, L.y);
+          ++pairs;
+        }
+        // partners below: slot (n - (k - b) - 1, k), b in [k - n + 1 + w0, k - n + w1]
+        for (j = w0 > 0 ? lower_bound_i32(mem, 0, i, k - n + 1 + w0) : 0; j < i; ++j) {
+          const int s = n - (k - __ldg(mem + j)) - 1;
+          if (s >= w1) break;
+          unsigned long long* c = lacc + 2 * (s - w0);
+          shared_add_u64(c, L.x);
+          shared_add_u64(c + 1, L.y);
+          ++pairs;
+        }
+      }
+      __syncthreads();
+      for (int t = threadIdx.x; t < ww; t += NT)
+        reinterpret_cast<ulonglong2*>(gl)[static_cast<int64_t>(w0 + t - p0) * n + k] =
+            make_ulonglong2(lacc[2 * t], lacc[2 * t + 1]);
+      __syncthreads();
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+  if ((threadIdx.x & 31) == 0 && pairs) atomicAdd(pairs_out, pairs);
+}
+
 // ---- deeper fixed-point levels ---------------------------------------------------
 // drows[i] (original row ids, i < R) are the rows with a nonzero value below
 // the main level; dfix[i * (J-1) + (j-1)] their level-j values (j >= 1).
@@ -615,6 +723,7 @@ struct SplitArgs {
   int32_t gl_begin;        // stripe held by row 0 of gl / dacc (the light-sum pass)
   int32_t lo_bits, scale, finalize;
   int32_t levels, vb;      // fixed-point levels (1: every length on the main grid), bits per level
+  int32_t k_begin = 0, k_end = 0;  // sp_deep_epilogue_kernel: columns of this launch
   void* dist;
   void* tot;
   unsigned long long* counters;  // [0] slot x u-bit FMA pairs (+ light pairs, added by host), [1] fp64 ops
@@ -720,7 +829,8 @@ __device__ Real combine_levels(const SplitArgs& a, __int128 V0, bool is_t, int64
 template <class Real>
 __global__ void sp_deep_epilogue_kernel(const SplitArgs a) {
   const int n = a.n;
-  const int64_t total = static_cast<int64_t>(a.s_end - a.s_begin) * n;
+  const int kw = a.k_end - a.k_begin;
+  const int64_t total = static_cast<int64_t>(a.s_end - a.s_begin) * kw;
   const unsigned long long* xs = a.colsum;
   const long long ch = static_cast<long long>(a.cacc[0]);
   const long long cl = static_cast<long long>(a.cacc[1]);
@@ -728,8 +838,8 @@ __global__ void sp_deep_epilogue_kernel(const SplitArgs a) {
   Real* tot = static_cast<Real*>(a.tot);
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int s = a.s_begin + static_cast<int>(i / n);
-    const int k = static_cast<int>(i % n);
+    const int s = a.s_begin + static_cast<int>(i / kw);
+    const int k = a.k_begin + static_cast<int>(i % kw);
     const int lm = static_cast<int>((static_cast<int64_t>(k) + s + 1) % n);
     const int64_t cell = static_cast<int64_t>(s - a.gl_begin) * n + k;
     const longlong2 G = reinterpret_cast<const longlong2*>(a.gl)[cell];

@@ -626,12 +626,12 @@ def test_generalized_python_mirror(device_ok):
 @pytest.mark.parametrize("band_mb,light_pass", [("0.05", "0"), ("0.3", "7"), ("1000", "0")])
 def test_split_banded_light_scatter_is_bitwise_the_one_shot_scatter(device_ok, band_mb, light_pass,
                                                                     monkeypatch):
-    """The banded light scatter (member CSR + per-band binary-searched
-    partners, atomics into an L2-sized block) adds exactly the same limbs to
-    exactly the same slots as the one-shot scatter: integer-valued fp64
-    atomics are order-free, so the results are bit-identical — for tiny bands
-    (many stripe x column blocks), multi-pass light sums, even n (duplicated
-    half stripe), wrapped and partial ranges."""
+    """The column-owned light scatter (shared-memory windows per column, the
+    default) and the banded one (member CSR + per-band partners, atomics into
+    an L2-sized block) add exactly the same limbs to exactly the same slots
+    as the one-shot scatter: integer atomics are order-free, so the results
+    are bit-identical — for tiny bands, multi-pass light sums, even n
+    (duplicated half stripe), wrapped and partial ranges."""
     for seed, n, leaves, dens in [(94, 300, 1100, 0.01), (95, 257, 700, 0.03)]:
         inst = sf.random_instance(seed, n, leaves, dens)
         problem = sf.flatten(inst.tree, inst.table)
@@ -643,11 +643,14 @@ def test_split_banded_light_scatter_is_bitwise_the_one_shot_scatter(device_ok, b
             monkeypatch.setenv("SF_LIGHT_BAND_MB", band_mb)
             if light_pass != "0":
                 monkeypatch.setenv("SF_LIGHT_PASS", light_pass)
-            d, t, gs = _gpu_stripes(problem, 1, 8, start, stop, N.KERNEL_SPLIT)
+            for mode in ("column", "band"):  # column-owned (default) and banded
+                monkeypatch.setenv("SF_LIGHT_MODE", mode)
+                d, t, gs = _gpu_stripes(problem, 1, 8, start, stop, N.KERNEL_SPLIT)
+                assert np.array_equal(d, want_d) and np.array_equal(t, want_t)
+                assert gs.updates_exec == ws.updates_exec  # same light pairs counted
+            monkeypatch.delenv("SF_LIGHT_MODE")
             monkeypatch.delenv("SF_LIGHT_BAND_MB")
             monkeypatch.delenv("SF_LIGHT_PASS", raising=False)
-            assert np.array_equal(d, want_d) and np.array_equal(t, want_t)
-            assert gs.updates_exec == ws.updates_exec  # same light pairs counted
             wd, wt = op.compute_stripes(problem, 1, 8, start, stop)
             _assert_close(1, 8, False, d, wd, N.KERNEL_SPLIT)
 

@@ -189,3 +189,20 @@ def test_sparse_oracle_is_the_reference_at_c2():
     h = hashlib.sha256(d.tobytes())
     h.update(t.tobytes())
     assert h.hexdigest() == rec["sha256"]
+
+
+def test_sparse_oracle_is_the_reference_at_c3():
+    """C3 (EMP shape, 25k samples x 300k tips), the last 16 stripes (wrap and
+    the even-n duplicate stripe), UW fp64: the sparse restatement's stripes
+    are the reference's own (sha256 of ref_driver's output on the GPU box
+    host, where the reference's 60 GB dense leaf_rows_ fit)."""
+    import hashlib
+    import json
+    import os
+    rec = json.loads((gu.GOLDEN / "reference_hashes.json").read_text())["c3_unweighted_fp64_12484_12500"]
+    inst = sf.random_instance(3, 25000, 300000, 0.002, 0, finalize_tree=False)
+    prob = sf.flatten(inst.tree, inst.table)
+    d, t = op.sparse_stripes(prob, 1, 8, 12484, 12500, threads=os.cpu_count() or 1)
+    h = hashlib.sha256(d.tobytes())
+    h.update(t.tobytes())
+    assert h.hexdigest() == rec["sha256"]

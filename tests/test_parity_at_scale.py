@@ -115,10 +115,12 @@ def test_c2_wn_fp64_full_range_against_the_reference():
 
 
 def _pinned_to_reference(name, d, t):
+    """The restatement's stripes are the reference's own (sha256 of the
+    reference's output on this range, tools/reference_at_scale.sh)."""
     want = _reference_hash(name)
-    if want is not None:  # ranges the reference was run on (tools/reference_at_scale.sh)
-        assert _stripes_sha256(d, t) == want, f"sparse restatement != reference ({name})"
-        _report(f"{name}: sparse restatement == reference", bitwise=True)
+    assert want is not None, f"no reference hash recorded for {name}"
+    assert _stripes_sha256(d, t) == want, f"sparse restatement != reference ({name})"
+    _report(f"{name}: sparse restatement == reference", bitwise=True)
 
 
 @pytest.mark.parametrize("start,stop", C3_RANGES)

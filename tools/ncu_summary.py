@@ -47,5 +47,34 @@ def main(path):
                     print(f"{'raw':40s} {name[:60]:60s} {v[i]:>16s} {units[i]}")
 
 
+def traffic(path, key, regex, stripes):
+    """Sum dram__bytes_read + dram__bytes_write over the captured launches
+    whose kernel name matches `regex` and record it in
+    profiles/ncu_traffic.json under `key` (config:kernel) with the stripes
+    the capture covered (bench.py scales it per stripe)."""
+    import json
+    import re
+    from pathlib import Path
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(raw.splitlines()))
+    h, vals = r[0], r[2:]
+    ik, ir, iw = h.index("Kernel Name"), h.index("dram__bytes_read.sum"), h.index("dram__bytes_write.sum")
+    unit_r, unit_w = r[1][ir], r[1][iw]
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    tot, nk = 0.0, 0
+    for v in vals:
+        if re.search(regex, v[ik]):
+            tot += float(v[ir].replace(",", "")) * scale[unit_r] + float(v[iw].replace(",", "")) * scale[unit_w]
+            nk += 1
+    out = Path(__file__).resolve().parent.parent / "profiles" / "ncu_traffic.json"
+    db = json.loads(out.read_text()) if out.exists() else {}
+    db[key] = {"dram_bytes": tot, "launches": nk, "stripes": int(stripes), "source": Path(path).name}
+    out.write_text(json.dumps(db, indent=1) + "\n")
+    print(key, db[key])
+
+
 if __name__ == "__main__":
-    main(sys.argv[1])
+    if len(sys.argv) > 1 and sys.argv[1] == "--traffic":
+        traffic(sys.argv[2], sys.argv[3], sys.argv[4], sys.argv[5])
+    else:
+        main(sys.argv[1])
