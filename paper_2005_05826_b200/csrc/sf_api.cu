@@ -10,6 +10,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -166,6 +167,18 @@ struct DevBuf {
   }
 };
 
+// Memory the library's pool holds for reuse (reserved, not in use).
+size_t pool_free_bytes(int device) {
+  uint64_t used = 0, reserved = 0;
+  cudaMemPool_t pool = device_pool(device);
+  if (!pool || cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) != cudaSuccess ||
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return reserved > used ? static_cast<size_t>(reserved - used) : 0;
+}
+
 // "Does `bytes` fit?" answered by a probe allocation from the library's
 // pool (cudaMemGetInfo stalls up to ~100 ms on some calls: p99 63 ms on the
 // box). The pool then keeps only `keep` of the probed bytes reserved (what
@@ -179,9 +192,14 @@ bool probe_fits(int device, size_t bytes, size_t keep) {
   }
   cudaGetLastError();
   if (cudaMemPool_t pool = device_pool(device)) {
-    uint64_t used = 0;
+    uint64_t used = 0, reserved = 0;
     if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used) == cudaSuccess)
       cudaMemPoolTrimTo(pool, static_cast<size_t>(used) + keep);
+    if (std::getenv("SF_DEBUG") &&
+        cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved) == cudaSuccess)
+      std::fprintf(stderr, "stripefrac: device %d pool: probe %zu MB %s, used %llu MB, reserved %llu MB\n", device,
+                   bytes >> 20, ok ? "fits" : "fails", static_cast<unsigned long long>(used >> 20),
+                   static_cast<unsigned long long>(reserved >> 20));
     cudaGetLastError();
   }
   return ok;
@@ -534,7 +552,7 @@ struct DeviceState {
   size_t lscan_bytes = 0;
   bool banded = false;
   // column-owned light scatter: entries (light rows containing each column)
-  DevBuf ccnt, cptr, cent, cscantmp;
+  DevBuf ccnt, cptr, cent, cscantmp, linfo;
   size_t cscan_bytes = 0;
   bool light_columns = false;
   // deeper fixed-point levels: deep rows, their levels, member CSR, per-slot sums
@@ -709,30 +727,71 @@ sf_status fixed_levels(const double* lengths, int32_t E, bool fp32, FixedLevels&
   out.fix.assign(static_cast<size_t>(E), 0ull);
   out.deep_rows.clear();
   out.dfix.clear();
+  // main level from the double's bits (L = m 2^(x-1075), m < 2^53): v0 =
+  // floor(m 2^(x-1075+scale)), the row is deep iff bits are shifted out;
+  // rows split over host threads, deep rows (rare) take the exact ldexp
+  // loop below, in row order
+  const int T = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+  std::vector<std::vector<int32_t>> deep_of(static_cast<size_t>(T));
+  auto main_level = [&](int t) {
+    const int32_t r0 = static_cast<int32_t>(static_cast<int64_t>(E) * t / T);
+    const int32_t r1 = static_cast<int32_t>(static_cast<int64_t>(E) * (t + 1) / T);
+    for (int32_t r = r0; r < r1; ++r) {
+      const double L = fp32 ? static_cast<double>(static_cast<float>(lengths[r])) : lengths[r];
+      uint64_t bits;
+      std::memcpy(&bits, &L, 8);
+      const int x = static_cast<int>((bits >> 52) & 0x7ff);
+      uint64_t m = bits & ((uint64_t{1} << 52) - 1);
+      if (x) m |= uint64_t{1} << 52;
+      const int sh = (x ? x - 1075 : -1074) + out.scale;
+      uint64_t v = 0;
+      bool deep = false;
+      if (m == 0) {
+        v = 0;
+      } else if (sh >= 0) {
+        v = m << sh;  // < 2^vb: L <= lmax
+      } else if (sh > -64) {
+        v = m >> -sh;
+        deep = (m & ((uint64_t{1} << -sh) - 1)) != 0;
+      } else {
+        deep = true;
+      }
+      out.fix[static_cast<size_t>(r)] = v;
+      if (deep) deep_of[static_cast<size_t>(t)].push_back(r);
+    }
+  };
+  if (E > (1 << 16) && T > 1) {
+    std::vector<std::thread> pool;
+    for (int t = 0; t < T; ++t) pool.emplace_back(main_level, t);
+    for (auto& th : pool) th.join();
+  } else {
+    for (int t = 0; t < T; ++t) main_level(t);
+  }
   std::vector<std::vector<unsigned long long>> deep;  // per deep row, its levels 1..
   int levels = 1;
-  for (int32_t r = 0; r < E; ++r) {
-    double rem = fp32 ? static_cast<double>(static_cast<float>(lengths[r])) : lengths[r];
-    // level j: v = floor(rem * 2^(scale + vb j)); rem -= v * 2^-(scale + vb j).
-    // Both steps are exact: the scaled value and its floor are doubles, the
-    // truncated part has no more significant bits than rem, and rem's low
-    // bits are what the subtraction leaves.
-    const double f0 = std::floor(std::ldexp(rem, out.scale));
-    out.fix[static_cast<size_t>(r)] = static_cast<unsigned long long>(f0);
-    rem -= std::ldexp(f0, -out.scale);
-    if (rem == 0.0) continue;
-    std::vector<unsigned long long> v;
-    for (int j = 1; rem != 0.0; ++j) {
-      if (j >= kMaxLevels) return fail(SF_EINVAL, "branch lengths span too many binades for exact sums");
-      const int sc = out.scale + out.vb * j;
-      const double f = std::floor(std::ldexp(rem, sc));
-      v.push_back(static_cast<unsigned long long>(f));
-      rem -= std::ldexp(f, -sc);
+  for (const auto& rows : deep_of)
+    for (int32_t r : rows) {
+      double rem = fp32 ? static_cast<double>(static_cast<float>(lengths[r])) : lengths[r];
+      // level j: v = floor(rem * 2^(scale + vb j)); rem -= v * 2^-(scale + vb j).
+      // Both steps are exact: the scaled value and its floor are doubles, the
+      // truncated part has no more significant bits than rem, and rem's low
+      // bits are what the subtraction leaves.
+      const double f0 = std::floor(std::ldexp(rem, out.scale));
+      if (static_cast<unsigned long long>(f0) != out.fix[static_cast<size_t>(r)])
+        return fail(SF_EINVAL, "fixed-point levels: main level mismatch (internal error)");
+      rem -= std::ldexp(f0, -out.scale);
+      std::vector<unsigned long long> v;
+      for (int j = 1; rem != 0.0; ++j) {
+        if (j >= kMaxLevels) return fail(SF_EINVAL, "branch lengths span too many binades for exact sums");
+        const int sc = out.scale + out.vb * j;
+        const double f = std::floor(std::ldexp(rem, sc));
+        v.push_back(static_cast<unsigned long long>(f));
+        rem -= std::ldexp(f, -sc);
+      }
+      levels = std::max(levels, 1 + static_cast<int>(v.size()));
+      out.deep_rows.push_back(r);
+      deep.push_back(std::move(v));
     }
-    levels = std::max(levels, 1 + static_cast<int>(v.size()));
-    out.deep_rows.push_back(r);
-    deep.push_back(std::move(v));
-  }
   out.levels = levels;
   out.dfix.assign(deep.size() * static_cast<size_t>(levels - 1), 0ull);
   for (size_t i = 0; i < deep.size(); ++i)
@@ -830,16 +889,22 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
       sp_col_fill_kernel<<<wblocks, 256, 0, st>>>(d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E,
                                                   d.nheavy.as<unsigned int>(), d.ccnt.as<uint32_t>(),
                                                   d.cent.as<uint2>());
+      if (d.linfo.bytes < static_cast<size_t>(E) * sizeof(LightRowInfo))
+        SF_TRY(d.linfo.alloc(d.dev, static_cast<size_t>(E) * sizeof(LightRowInfo), "light row records"));
+      sp_light_rowinfo_kernel<<<grid_for(E, 256), 256, 0, st>>>(d.perm.as<int32_t>(), plan->E,
+                                                                 d.nheavy.as<unsigned int>(), d.lptr.as<uint32_t>(),
+                                                                 d.fix.as<unsigned long long>(),
+                                                                 d.linfo.as<LightRowInfo>());
       SF_CUDA(cudaGetLastError());
-      d.launches += 3;
+      d.launches += 4;
     }
     constexpr int NT = 512;
     auto* kern = sp_light_column_kernel<NT>;
     const int smem = 2 * kLightWin * 8;
     SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<std::min(n, 65535), NT, smem, st>>>(d.cptr.as<uint32_t>(), d.cent.as<uint2>(), d.lptr.as<uint32_t>(),
-                                             d.lmem.as<int32_t>(), d.perm.as<int32_t>(), d.fix.as<unsigned long long>(),
-                                             plan->lo_bits, n, p0, p0, p1, d.lightsum.as<unsigned long long>(),
+    kern<<<std::min(n, 65535), NT, smem, st>>>(d.cptr.as<uint32_t>(), d.cent.as<uint2>(),
+                                             d.linfo.as<LightRowInfo>(), d.lmem.as<int32_t>(), plan->lo_bits, n,
+                                             p0, p0, p1, d.lightsum.as<unsigned long long>(),
                                              d.exec_ctr.as<unsigned long long>());
     SF_CUDA(cudaGetLastError());
     d.launches++;
@@ -1083,11 +1148,29 @@ sf_status gram_matmul(DeviceState& d, int64_t M, int64_t N, int64_t K, const int
     } pg{pref};
     const size_t ws = kWorkspace;
     SF_LT(cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_MAX_WORKSPACE_BYTES, &ws, sizeof(ws)));
-    cublasLtMatmulHeuristicResult_t res{};
-    int nres = 0;
-    SF_LT(cublasLtMatmulAlgoGetHeuristic(d.lt, d.lt_op, d.lt_a, d.lt_b, d.lt_c, d.lt_c, pref, 1, &res, &nres));
-    if (nres < 1) return fail(SF_ECUDA, "cuBLASLt has no int8 GEMM for this shape");
-    d.lt_algo = res.algo;
+    // the chosen algorithm per (device, shape) is cached process-wide: every
+    // plan of the same problem asks for the same shapes
+    static std::mutex mu;
+    static std::vector<std::pair<std::array<int64_t, 4>, cublasLtMatmulAlgo_t>> cache;
+    const std::array<int64_t, 4> key{d.dev, M, N, K};
+    bool hit = false;
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      for (const auto& c : cache)
+        if (c.first == key) {
+          d.lt_algo = c.second;
+          hit = true;
+        }
+    }
+    if (!hit) {
+      cublasLtMatmulHeuristicResult_t res{};
+      int nres = 0;
+      SF_LT(cublasLtMatmulAlgoGetHeuristic(d.lt, d.lt_op, d.lt_a, d.lt_b, d.lt_c, d.lt_c, pref, 1, &res, &nres));
+      if (nres < 1) return fail(SF_ECUDA, "cuBLASLt has no int8 GEMM for this shape");
+      d.lt_algo = res.algo;
+      std::lock_guard<std::mutex> lk(mu);
+      cache.emplace_back(key, res.algo);
+    }
     d.lt_m = M, d.lt_n = N, d.lt_k = K;
   }
   const int32_t alpha = 1, beta = 0;
@@ -1340,6 +1423,13 @@ sf_status upload_schedule(DeviceState& d, const Schedule& s) {
 sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host_d = nullptr,
                      void* host_t = nullptr) {
   SF_CUDA(cudaSetDevice(d.dev));
+  const bool dbg = std::getenv("SF_DEBUG") != nullptr;
+  const auto t_run = std::chrono::steady_clock::now();
+  auto phase = [&](const char* what) {
+    if (dbg)
+      std::fprintf(stderr, "stripefrac:   run dev %d %s at %.1f ms (host)\n", d.dev, what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_run).count());
+  };
   const cudaStream_t st = d.stream;
   const int n = plan->n;
   const int64_t rows_here = d.b - d.a;
@@ -1409,7 +1499,9 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
     } else if (plan->kernel == 11) {
       SF_TRY(wsparse_build(plan, d, C, st));
     } else if (plan->kernel == 10) {
+      phase("embedding enqueued");
       SF_TRY(split_build(plan, d, st));
+      phase("split prep + first light pass enqueued");
     } else if (plan->kernel == 2) {
       // node-packed presence bits for the sparse walk
       const int64_t W = (plan->E + 31) / 32;
@@ -1550,6 +1642,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         // only now; without the memory for them the DFMA heavy walk (the
         // same exact sums, bit for bit) takes the heavy rows
         const sf_status gs = gram_prepare(plan, d, st);
+        phase("tensor-core operands prepared");
         if (gs == SF_ENOMEM) {
           gram = false;
           cudaGetLastError();
@@ -1639,6 +1732,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         }
       }
       d.launches--;  // counted once more below
+      phase("heavy rows + copies enqueued");
     } else if (plan->kernel == 2) {
       SparseArgs a;
       a.nb = d.nodebits.as<uint32_t>();
@@ -1720,6 +1814,205 @@ sf_status for_each_device(sf_plan* plan, F&& fn) {
   return SF_OK;
 }
 
+// ------------------------------------------------------------ pageable downloads
+// A D2H cudaMemcpy into pageable memory goes through the driver's small
+// staging buffers on one thread (C3: ~16 GB/s, 0.3 s of a 0.77 s call).
+// Pageable destinations instead get a process-wide pinned double buffer:
+// block b+1 is copied device -> pinned while host threads copy block b
+// pinned -> destination (the reference hands out pageable Eigen buffers).
+bool host_pinned(const void* ptr) {
+  cudaPointerAttributes at{};
+  if (!ptr || cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+struct PinnedStaging {
+  std::mutex mu;
+  char* slot[2] = {nullptr, nullptr};
+  size_t bytes = 0;
+};
+// one double buffer per device, so several devices download in parallel
+PinnedStaging& staging(int device) {
+  static PinnedStaging s[64];  // freed at process exit by the driver
+  return s[device & 63];
+}
+
+void parallel_memcpy(char* dst, const char* src, size_t bytes, unsigned max_threads) {
+  const size_t min_piece = 8ull << 20;
+  size_t T = std::min<size_t>(std::max(1u, max_threads), std::max<size_t>(1, bytes / min_piece));
+  if (T <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t piece = (bytes + T - 1) / T;
+  std::vector<std::thread> th;
+  for (size_t i = 1; i < T; ++i) {
+    const size_t o = i * piece;
+    if (o >= bytes) break;
+    th.emplace_back([=] { std::memcpy(dst + o, src + o, std::min(piece, bytes - o)); });
+  }
+  std::memcpy(dst, src, std::min(piece, bytes));
+  for (auto& t : th) t.join();
+}
+
+// A 2D block (rows x width bytes, device pitch = host pitch) of device
+// memory -> pageable host, through the device's pinned double buffer: as
+// many whole rows per staging block as fit, host threads scatter the rows.
+sf_status staged_d2h_2d(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t pitch, size_t width,
+                        size_t rows, unsigned threads);
+
+// Host threads for the pinned -> pageable copies of one of `ndev` devices
+// downloading at once.
+unsigned copy_threads(size_t ndev) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  return std::max(1u, std::min(16u, hw / static_cast<unsigned>(std::max<size_t>(1, ndev))));
+}
+
+// The device's two pinned staging slots (allocated on first use; false when
+// no pinned memory is available). Caller holds S.mu.
+bool ensure_staging(PinnedStaging& S) {
+  constexpr size_t kSlot = 128ull << 20;
+  if (S.slot[0]) return true;
+  for (int i = 0; i < 2; ++i) {
+    void* h = nullptr;
+    if (cudaHostAlloc(&h, kSlot, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      if (S.slot[0]) cudaFreeHost(S.slot[0]);
+      S.slot[0] = nullptr;
+      return false;
+    }
+    S.slot[i] = static_cast<char*>(h);
+  }
+  S.bytes = kSlot;
+  return true;
+}
+
+// dsrc (memory of `device`, the current device) -> hdst (pageable host), on cs.
+sf_status staged_d2h(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t bytes, unsigned threads) {
+  if (bytes == 0) return SF_OK;
+  PinnedStaging& S = staging(device);
+  std::lock_guard<std::mutex> lock(S.mu);
+  if (!ensure_staging(S)) {  // no pinned memory to spare: the driver's own pageable path
+    SF_CUDA(cudaMemcpyAsync(hdst, dsrc, bytes, cudaMemcpyDeviceToHost, cs));
+    SF_CUDA(cudaStreamSynchronize(cs));
+    return SF_OK;
+  }
+  cudaEvent_t ev[2];
+  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  if (cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
+    cudaEventDestroy(ev[0]);
+    return fail(SF_ECUDA, "cudaEventCreate failed");
+  }
+  sf_status rc = SF_OK;
+  const size_t nblk = (bytes + S.bytes - 1) / S.bytes;
+  auto issue = [&](size_t b) -> sf_status {
+    const size_t o = b * S.bytes;
+    SF_CUDA(cudaMemcpyAsync(S.slot[b & 1], dsrc + o, std::min(S.bytes, bytes - o), cudaMemcpyDeviceToHost, cs));
+    SF_CUDA(cudaEventRecord(ev[b & 1], cs));
+    return SF_OK;
+  };
+  rc = issue(0);
+  for (size_t b = 0; rc == SF_OK && b < nblk; ++b) {
+    // slot (b+1)&1 was drained by block b-1's host copy, which has returned
+    if (b + 1 < nblk) rc = issue(b + 1);
+    if (rc != SF_OK) break;
+    if (cudaEventSynchronize(ev[b & 1]) != cudaSuccess) {
+      rc = fail(SF_ECUDA, std::string("staged download: ") + cudaGetErrorString(cudaGetLastError()));
+      break;
+    }
+    const size_t o = b * S.bytes;
+    parallel_memcpy(hdst + o, S.slot[b & 1], std::min(S.bytes, bytes - o), threads);
+  }
+  cudaStreamSynchronize(cs);
+  cudaEventDestroy(ev[0]);
+  cudaEventDestroy(ev[1]);
+  return rc;
+}
+// hsrc (pageable host) -> ddst (memory of `device`, the current device), on
+// cs, through the device's pinned double buffer: host threads fill slot b+1
+// while slot b's copy runs (pageable H2D goes through the driver's small
+// staging buffers on one thread). Returns when the copy is done.
+sf_status staged_h2d(int device, cudaStream_t cs, const char* hsrc, char* ddst, size_t bytes, unsigned threads) {
+  if (bytes == 0) return SF_OK;
+  PinnedStaging& S = staging(device);
+  std::lock_guard<std::mutex> lock(S.mu);
+  if (!ensure_staging(S)) {
+    SF_CUDA(cudaMemcpyAsync(ddst, hsrc, bytes, cudaMemcpyHostToDevice, cs));
+    SF_CUDA(cudaStreamSynchronize(cs));
+    return SF_OK;
+  }
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 2; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } eg{ev};
+  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  SF_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  const size_t nblk = (bytes + S.bytes - 1) / S.bytes;
+  for (size_t b = 0; b < nblk; ++b) {
+    const size_t o = b * S.bytes, len = std::min(S.bytes, bytes - o);
+    if (b >= 2) SF_CUDA(cudaEventSynchronize(ev[b & 1]));  // slot b&1 was sent by block b-2
+    parallel_memcpy(S.slot[b & 1], hsrc + o, len, threads);
+    SF_CUDA(cudaMemcpyAsync(ddst + o, S.slot[b & 1], len, cudaMemcpyHostToDevice, cs));
+    SF_CUDA(cudaEventRecord(ev[b & 1], cs));
+  }
+  SF_CUDA(cudaStreamSynchronize(cs));
+  return SF_OK;
+}
+
+sf_status staged_d2h_2d(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t pitch, size_t width,
+                        size_t rows, unsigned threads) {
+  if (rows == 0 || width == 0) return SF_OK;
+  if (width == pitch) return staged_d2h(device, cs, dsrc, hdst, width * rows, threads);
+  PinnedStaging& S = staging(device);
+  std::lock_guard<std::mutex> lock(S.mu);
+  if (!ensure_staging(S)) {  // no pinned memory: the driver's own pageable 2D copy
+    SF_CUDA(cudaMemcpy2DAsync(hdst, pitch, dsrc, pitch, width, rows, cudaMemcpyDeviceToHost, cs));
+    SF_CUDA(cudaStreamSynchronize(cs));
+    return SF_OK;
+  }
+  const size_t per = std::max<size_t>(1, S.bytes / width);  // rows per staging block
+  const size_t nblk = (rows + per - 1) / per;
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  struct EvGuard {
+    cudaEvent_t* e;
+    ~EvGuard() {
+      for (int i = 0; i < 2; ++i)
+        if (e[i]) cudaEventDestroy(e[i]);
+    }
+  } eg{ev};
+  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+  SF_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
+  auto issue = [&](size_t b) -> sf_status {
+    const size_t r0 = b * per, nr = std::min(per, rows - r0);
+    SF_CUDA(cudaMemcpy2DAsync(S.slot[b & 1], width, dsrc + r0 * pitch, pitch, width, nr, cudaMemcpyDeviceToHost, cs));
+    SF_CUDA(cudaEventRecord(ev[b & 1], cs));
+    return SF_OK;
+  };
+  SF_TRY(issue(0));
+  for (size_t b = 0; b < nblk; ++b) {
+    if (b + 1 < nblk) SF_TRY(issue(b + 1));
+    SF_CUDA(cudaEventSynchronize(ev[b & 1]));
+    const size_t r0 = b * per, nr = std::min(per, rows - r0);
+    const char* src = S.slot[b & 1];
+    // scatter the rows over host threads
+    const size_t T = std::max<size_t>(1, std::min<size_t>(threads, nr));
+    std::vector<std::thread> th;
+    auto part = [&](size_t t) {
+      for (size_t r = t; r < nr; r += T) std::memcpy(hdst + (r0 + r) * pitch, src + r * width, width);
+    };
+    for (size_t t = 1; t < T; ++t) th.emplace_back(part, t);
+    part(0);
+    for (auto& x : th) x.join();
+  }
+  return SF_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -1895,8 +2188,20 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
         const int64_t nnz = p->feat_ptr[F];
         SF_TRY(upload(d.lens, d.dev, p->lengths, static_cast<size_t>(plan->E), d.stream, "lengths"));
         SF_TRY(upload(d.feat_ptr, d.dev, p->feat_ptr, static_cast<size_t>(F + 1), d.stream, "feat_ptr"));
-        SF_TRY(upload(d.sidx, d.dev, p->sample_idx, static_cast<size_t>(nnz), d.stream, "sample_idx"));
-        SF_TRY(upload(d.counts, d.dev, p->counts, static_cast<size_t>(nnz), d.stream, "counts"));
+        // the table's big arrays (C3: 180 MB) through the pinned staging buffers
+        SF_TRY(d.sidx.alloc(d.dev, static_cast<size_t>(nnz) * 4, "sample_idx"));
+        SF_TRY(d.counts.alloc(d.dev, static_cast<size_t>(nnz) * 8, "counts"));
+        const unsigned th = copy_threads(plan->devs.size());
+        if (host_pinned(p->sample_idx))
+          SF_CUDA(cudaMemcpyAsync(d.sidx.p, p->sample_idx, static_cast<size_t>(nnz) * 4, cudaMemcpyHostToDevice, d.stream));
+        else
+          SF_TRY(staged_h2d(d.dev, d.stream, reinterpret_cast<const char*>(p->sample_idx), d.sidx.as<char>(),
+                            static_cast<size_t>(nnz) * 4, th));
+        if (host_pinned(p->counts))
+          SF_CUDA(cudaMemcpyAsync(d.counts.p, p->counts, static_cast<size_t>(nnz) * 8, cudaMemcpyHostToDevice, d.stream));
+        else
+          SF_TRY(staged_h2d(d.dev, d.stream, reinterpret_cast<const char*>(p->counts), d.counts.as<char>(),
+                            static_cast<size_t>(nnz) * 8, th));
         SF_TRY(upload(d.totals, d.dev, p->sample_totals, static_cast<size_t>(n), d.stream, "totals"));
         return SF_OK;
       };
@@ -2014,7 +2319,10 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
           const size_t after = static_cast<size_t>(plan->E) * 4 * (3 + 2 * static_cast<size_t>(split_heavy_min(n)));
           if (!(ex && ex->mem_budget_bytes > 0) && !std::getenv("SF_LIGHT_PASS")) {
             const size_t need = static_cast<size_t>(span) * per_stripe + after;
-            if (probe_fits(d.dev, need + reserve, need)) {
+            // steady state: the pool still holds the previous plan's freed
+            // blocks, so the same allocations are served again without a probe
+            // (a probe's single large block would fragment them)
+            if (pool_free_bytes(d.dev) >= need + reserve || probe_fits(d.dev, need + reserve, need)) {
               fit = static_cast<size_t>(span);
               probed = true;
             }
@@ -2150,175 +2458,7 @@ sf_status sf_plan_sync(sf_plan* plan) {
   return SF_OK;
 }
 
-// ------------------------------------------------------------ pageable downloads
-// A D2H cudaMemcpy into pageable memory goes through the driver's small
-// staging buffers on one thread (C3: ~16 GB/s, 0.3 s of a 0.77 s call).
-// Pageable destinations instead get a process-wide pinned double buffer:
-// block b+1 is copied device -> pinned while host threads copy block b
-// pinned -> destination (the reference hands out pageable Eigen buffers).
-namespace {
-bool host_pinned(const void* ptr) {
-  cudaPointerAttributes at{};
-  if (!ptr || cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
-  return at.type == cudaMemoryTypeHost;
-}
 
-struct PinnedStaging {
-  std::mutex mu;
-  char* slot[2] = {nullptr, nullptr};
-  size_t bytes = 0;
-};
-// one double buffer per device, so several devices download in parallel
-PinnedStaging& staging(int device) {
-  static PinnedStaging s[64];  // freed at process exit by the driver
-  return s[device & 63];
-}
-
-void parallel_memcpy(char* dst, const char* src, size_t bytes, unsigned max_threads) {
-  const size_t min_piece = 8ull << 20;
-  size_t T = std::min<size_t>(std::max(1u, max_threads), std::max<size_t>(1, bytes / min_piece));
-  if (T <= 1) {
-    std::memcpy(dst, src, bytes);
-    return;
-  }
-  const size_t piece = (bytes + T - 1) / T;
-  std::vector<std::thread> th;
-  for (size_t i = 1; i < T; ++i) {
-    const size_t o = i * piece;
-    if (o >= bytes) break;
-    th.emplace_back([=] { std::memcpy(dst + o, src + o, std::min(piece, bytes - o)); });
-  }
-  std::memcpy(dst, src, std::min(piece, bytes));
-  for (auto& t : th) t.join();
-}
-
-// A 2D block (rows x width bytes, device pitch = host pitch) of device
-// memory -> pageable host, through the device's pinned double buffer: as
-// many whole rows per staging block as fit, host threads scatter the rows.
-sf_status staged_d2h_2d(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t pitch, size_t width,
-                        size_t rows, unsigned threads);
-
-// Host threads for the pinned -> pageable copies of one of `ndev` devices
-// downloading at once.
-unsigned copy_threads(size_t ndev) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  return std::max(1u, std::min(16u, hw / static_cast<unsigned>(std::max<size_t>(1, ndev))));
-}
-
-// The device's two pinned staging slots (allocated on first use; false when
-// no pinned memory is available). Caller holds S.mu.
-bool ensure_staging(PinnedStaging& S) {
-  constexpr size_t kSlot = 128ull << 20;
-  if (S.slot[0]) return true;
-  for (int i = 0; i < 2; ++i) {
-    void* h = nullptr;
-    if (cudaHostAlloc(&h, kSlot, cudaHostAllocPortable) != cudaSuccess) {
-      cudaGetLastError();
-      if (S.slot[0]) cudaFreeHost(S.slot[0]);
-      S.slot[0] = nullptr;
-      return false;
-    }
-    S.slot[i] = static_cast<char*>(h);
-  }
-  S.bytes = kSlot;
-  return true;
-}
-
-// dsrc (memory of `device`, the current device) -> hdst (pageable host), on cs.
-sf_status staged_d2h(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t bytes, unsigned threads) {
-  if (bytes == 0) return SF_OK;
-  PinnedStaging& S = staging(device);
-  std::lock_guard<std::mutex> lock(S.mu);
-  if (!ensure_staging(S)) {  // no pinned memory to spare: the driver's own pageable path
-    SF_CUDA(cudaMemcpyAsync(hdst, dsrc, bytes, cudaMemcpyDeviceToHost, cs));
-    SF_CUDA(cudaStreamSynchronize(cs));
-    return SF_OK;
-  }
-  cudaEvent_t ev[2];
-  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-  if (cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming) != cudaSuccess) {
-    cudaEventDestroy(ev[0]);
-    return fail(SF_ECUDA, "cudaEventCreate failed");
-  }
-  sf_status rc = SF_OK;
-  const size_t nblk = (bytes + S.bytes - 1) / S.bytes;
-  auto issue = [&](size_t b) -> sf_status {
-    const size_t o = b * S.bytes;
-    SF_CUDA(cudaMemcpyAsync(S.slot[b & 1], dsrc + o, std::min(S.bytes, bytes - o), cudaMemcpyDeviceToHost, cs));
-    SF_CUDA(cudaEventRecord(ev[b & 1], cs));
-    return SF_OK;
-  };
-  rc = issue(0);
-  for (size_t b = 0; rc == SF_OK && b < nblk; ++b) {
-    // slot (b+1)&1 was drained by block b-1's host copy, which has returned
-    if (b + 1 < nblk) rc = issue(b + 1);
-    if (rc != SF_OK) break;
-    if (cudaEventSynchronize(ev[b & 1]) != cudaSuccess) {
-      rc = fail(SF_ECUDA, std::string("staged download: ") + cudaGetErrorString(cudaGetLastError()));
-      break;
-    }
-    const size_t o = b * S.bytes;
-    parallel_memcpy(hdst + o, S.slot[b & 1], std::min(S.bytes, bytes - o), threads);
-  }
-  cudaStreamSynchronize(cs);
-  cudaEventDestroy(ev[0]);
-  cudaEventDestroy(ev[1]);
-  return rc;
-}
-}  // namespace
-
-namespace {
-sf_status staged_d2h_2d(int device, cudaStream_t cs, const char* dsrc, char* hdst, size_t pitch, size_t width,
-                        size_t rows, unsigned threads) {
-  if (rows == 0 || width == 0) return SF_OK;
-  if (width == pitch) return staged_d2h(device, cs, dsrc, hdst, width * rows, threads);
-  PinnedStaging& S = staging(device);
-  std::lock_guard<std::mutex> lock(S.mu);
-  if (!ensure_staging(S)) {  // no pinned memory: the driver's own pageable 2D copy
-    SF_CUDA(cudaMemcpy2DAsync(hdst, pitch, dsrc, pitch, width, rows, cudaMemcpyDeviceToHost, cs));
-    SF_CUDA(cudaStreamSynchronize(cs));
-    return SF_OK;
-  }
-  const size_t per = std::max<size_t>(1, S.bytes / width);  // rows per staging block
-  const size_t nblk = (rows + per - 1) / per;
-  cudaEvent_t ev[2] = {nullptr, nullptr};
-  struct EvGuard {
-    cudaEvent_t* e;
-    ~EvGuard() {
-      for (int i = 0; i < 2; ++i)
-        if (e[i]) cudaEventDestroy(e[i]);
-    }
-  } eg{ev};
-  SF_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
-  SF_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
-  auto issue = [&](size_t b) -> sf_status {
-    const size_t r0 = b * per, nr = std::min(per, rows - r0);
-    SF_CUDA(cudaMemcpy2DAsync(S.slot[b & 1], width, dsrc + r0 * pitch, pitch, width, nr, cudaMemcpyDeviceToHost, cs));
-    SF_CUDA(cudaEventRecord(ev[b & 1], cs));
-    return SF_OK;
-  };
-  SF_TRY(issue(0));
-  for (size_t b = 0; b < nblk; ++b) {
-    if (b + 1 < nblk) SF_TRY(issue(b + 1));
-    SF_CUDA(cudaEventSynchronize(ev[b & 1]));
-    const size_t r0 = b * per, nr = std::min(per, rows - r0);
-    const char* src = S.slot[b & 1];
-    // scatter the rows over host threads
-    const size_t T = std::max<size_t>(1, std::min<size_t>(threads, nr));
-    std::vector<std::thread> th;
-    auto part = [&](size_t t) {
-      for (size_t r = t; r < nr; r += T) std::memcpy(hdst + (r0 + r) * pitch, src + r * width, width);
-    };
-    for (size_t t = 1; t < T; ++t) th.emplace_back(part, t);
-    part(0);
-    for (auto& x : th) x.join();
-  }
-  return SF_OK;
-}
-}  // namespace
 
 sf_status sf_plan_download(sf_plan* plan, void* dist_out, void* tot_out) {
   if (!plan) return fail(SF_EINVAL, "plan is null");

@@ -547,60 +547,135 @@ __global__ void sp_col_fill_kernel(const int32_t* __restrict__ lmem, const uint3
   }
 }
 
-__device__ __forceinline__ void shared_add_u64(unsigned long long* p, unsigned long long v) {
-  atomicAdd(p, v);  // ATOMS.CAS loop on sm_100a; exact (integer limbs)
+// One light contribution into the shared-memory window: the row's value v
+// (< 2^63) as four 16-bit limbs into four 32-bit accumulators (native
+// shared atomic adds). Exact while a cell takes at most 65537 additions; a
+// cell takes one per light row holding the column, so columns with more
+// entries use 64-bit (hi, lo) compare-and-swap adds instead (WIDE).
+template <bool WIDE>
+__device__ __forceinline__ void window_add(uint32_t* cell, unsigned long long v, ulonglong2 L) {
+  if (WIDE) {
+    unsigned long long* c = reinterpret_cast<unsigned long long*>(cell);
+    atomicAdd(c, L.x);
+    atomicAdd(c + 1, L.y);
+  } else {
+    atomicAdd(cell, static_cast<uint32_t>(v & 0xffffu));
+    atomicAdd(cell + 1, static_cast<uint32_t>((v >> 16) & 0xffffu));
+    atomicAdd(cell + 2, static_cast<uint32_t>((v >> 32) & 0xffffu));
+    atomicAdd(cell + 3, static_cast<uint32_t>(v >> 48));
+  }
+}
+
+// Per light row (by permuted index): member list offset and length, and its
+// main-level value — one 16-byte record, L2-resident (C3: ~8 MB).
+struct LightRowInfo {
+  uint32_t b0, x;
+  unsigned long long v;
+};
+
+__global__ void sp_light_rowinfo_kernel(const int32_t* __restrict__ perm, int32_t E,
+                                        const unsigned int* __restrict__ n_heavy, const uint32_t* __restrict__ lptr,
+                                        const unsigned long long* __restrict__ fix, LightRowInfo* __restrict__ info) {
+  for (int64_t idx = *n_heavy + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; idx < E;
+       idx += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    info[idx] = LightRowInfo{lptr[idx], lptr[idx + 1] - lptr[idx], fix[perm[idx]]};
+}
+
+// One warp per entry (light row holding the column): the lanes walk the
+// row's sorted members 32 at a time from the entry's own position. The next
+// entry's record is loaded while the current one is walked.
+template <bool WIDE>
+__device__ __forceinline__ void light_column_window(const uint32_t e0, const uint32_t e1, const uint2* __restrict__ cent,
+                                                    const LightRowInfo* __restrict__ info,
+                                                    const int32_t* __restrict__ lmem, int32_t lo_bits, int k, int n,
+                                                    int w0, int w1, uint32_t* __restrict__ acc,
+                                                    unsigned long long& pairs) {
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  uint32_t e = e0 + wid;
+  uint2 en = e < e1 ? cent[e] : make_uint2(0u, 0u);
+  LightRowInfo ri{0u, 0u, 0ull};
+  if (e < e1) ri = info[en.x];
+  for (; e < e1; e += nw) {
+    // prefetch the next entry of this warp
+    const uint32_t en_next = e + nw;
+    uint2 nen = make_uint2(0u, 0u);
+    if (en_next < e1) nen = cent[en_next];
+    const int x = static_cast<int>(ri.x);
+    const int i = static_cast<int>(en.y);
+    const int32_t* mem = lmem + ri.b0;
+    const unsigned long long v = ri.v;
+    const ulonglong2 L = ilimbs_of(v, lo_bits);
+    // partners above: slot (b - k - 1, k), b in [k + w0 + 1, k + w1]
+    int j0 = w0 > 0 ? lower_bound_i32(mem, i + 1, x, k + w0 + 1) : i + 1;
+    for (int j = j0 + lane;; j += 32) {
+      int s = w1;
+      if (j < x) s = __ldg(mem + j) - k - 1;
+      const bool live = s < w1;
+      if (live) {
+        window_add<WIDE>(acc + 4 * (s - w0), v, L);
+        ++pairs;
+      }
+      if (!__all_sync(0xffffffffu, live)) break;  // sorted: later members are past the window
+    }
+    // partners below: slot (n - (k - b) - 1, k), b in [k - n + 1 + w0, k - n + w1]
+    j0 = w0 > 0 ? lower_bound_i32(mem, 0, i, k - n + 1 + w0) : 0;
+    for (int j = j0 + lane;; j += 32) {
+      int s = w1;
+      if (j < i) s = n - (k - __ldg(mem + j)) - 1;
+      const bool live = s < w1;
+      if (live) {
+        window_add<WIDE>(acc + 4 * (s - w0), v, L);
+        ++pairs;
+      }
+      if (!__all_sync(0xffffffffu, live)) break;
+    }
+    en = nen;
+    if (en_next < e1) ri = info[en.x];
+  }
 }
 
 // One CTA per column k: stripes [s0, s1) of the light sums (rows relative to
 // the pass start p0), in windows of kLightWin stripes.
 template <int NT>
 __global__ void __launch_bounds__(NT) sp_light_column_kernel(
-    const uint32_t* __restrict__ cptr, const uint2* __restrict__ cent, const uint32_t* __restrict__ lptr,
-    const int32_t* __restrict__ lmem, const int32_t* __restrict__ perm, const unsigned long long* __restrict__ fix,
-    int32_t lo_bits, int32_t n, int32_t p0, int32_t s0, int32_t s1, unsigned long long* __restrict__ gl,
-    unsigned long long* __restrict__ pairs_out) {
-  extern __shared__ unsigned long long lacc[];  // [win][2]
+    const uint32_t* __restrict__ cptr, const uint2* __restrict__ cent, const LightRowInfo* __restrict__ info,
+    const int32_t* __restrict__ lmem, int32_t lo_bits, int32_t n, int32_t p0, int32_t s0, int32_t s1,
+    unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out) {
+  extern __shared__ uint32_t lacc[];  // [win][4]
   const int S = n / 2;
   const int send = min(s1, S);
+  const unsigned long long lo_mask = (1ull << lo_bits) - 1ull;
   unsigned long long pairs = 0;
   for (int k = blockIdx.x; k < n; k += gridDim.x) {
     const uint32_t e0 = cptr[k], e1 = cptr[k + 1];
+    const bool wide = e1 - e0 > 65535u;  // 16-bit limbs could overflow a 32-bit cell
     for (int w0 = s0; w0 < send; w0 += kLightWin) {
       const int w1 = min(send, w0 + kLightWin);
       const int ww = w1 - w0;
-      for (int i = threadIdx.x; i < 2 * ww; i += NT) lacc[i] = 0ull;
+      for (int t = threadIdx.x; t < 4 * ww; t += NT) lacc[t] = 0u;
       __syncthreads();
-      for (uint32_t e = e0 + threadIdx.x; e < e1; e += NT) {
-        const uint2 en = cent[e];
-        const uint32_t b0 = lptr[en.x];
-        const int x = static_cast<int>(lptr[en.x + 1] - b0);
-        const int i = static_cast<int>(en.y);
-        const int32_t* mem = lmem + b0;
-        const ulonglong2 L = ilimbs_of(__ldg(fix + perm[en.x]), lo_bits);
-        // partners above: slot (b - k - 1, k), b in [k + w0 + 1, k + w1]
-        int j = w0 > 0 ? lower_bound_i32(mem, i + 1, x, k + w0 + 1) : i + 1;
-        for (; j < x; ++j) {
-          const int s = __ldg(mem + j) - k - 1;
-          if (s >= w1) break;
-          unsigned long long* c = lacc + 2 * (s - w0);
-          shared_add_u64(c, L.x);
-          shared_add_u64(c + 1, L.y);
-          ++pairs;
+      if (wide)
+        light_column_window<true>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+      else
+        light_column_window<false>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+      __syncthreads();
+      for (int t = threadIdx.x; t < ww; t += NT) {
+        ulonglong2 out;
+        if (wide) {
+          out = reinterpret_cast<const ulonglong2*>(lacc)[t];
+        } else {  // the window's exact sum, re-split into (hi, lo): only hi * 2^lo_bits + lo is used
+          const uint4 c = reinterpret_cast<const uint4*>(lacc)[t];
+          const unsigned __int128 v = static_cast<unsigned __int128>(c.x) +
+                                      (static_cast<unsigned __int128>(c.y) << 16) +
+                                      (static_cast<unsigned __int128>(c.z) << 32) +
+                                      (static_cast<unsigned __int128>(c.w) << 48);
+          out = make_ulonglong2(static_cast<unsigned long long>(v >> lo_bits),
+                                static_cast<unsigned long long>(v) & lo_mask);
         }
-        // partners below: slot (n - (k - b) - 1, k), b in [k - n + 1 + w0, k - n + w1]
-        for (j = w0 > 0 ? lower_bound_i32(mem, 0, i, k - n + 1 + w0) : 0; j < i; ++j) {
-          const int s = n - (k - __ldg(mem + j)) - 1;
-          if (s >= w1) break;
-          unsigned long long* c = lacc + 2 * (s - w0);
-          shared_add_u64(c, L.x);
-          shared_add_u64(c + 1, L.y);
-          ++pairs;
-        }
+        reinterpret_cast<ulonglong2*>(gl)[static_cast<int64_t>(w0 + t - p0) * n + k] = out;
       }
-      __syncthreads();
-      for (int t = threadIdx.x; t < ww; t += NT)
-        reinterpret_cast<ulonglong2*>(gl)[static_cast<int64_t>(w0 + t - p0) * n + k] =
-            make_ulonglong2(lacc[2 * t], lacc[2 * t + 1]);
       __syncthreads();
     }
   }
