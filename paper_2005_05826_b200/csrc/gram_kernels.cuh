@@ -44,8 +44,8 @@ __device__ __forceinline__ void balanced_digits(unsigned long long v, int8_t (&d
   }
 }
 
-// Digits of every permuted heavy row i < Kp (zero past H), by row:
-// rowdig[i * kMaxDigits + j], and the OR of the nonzero planes into *mask.
+// Digits of every permuted heavy row i < Kp (zero past H), plane-major:
+// rowdig[j * Kp + i], and the OR of the nonzero planes into *mask.
 __global__ void sp_gram_rowdig_kernel(const unsigned long long* __restrict__ fixbit,
                                       const unsigned int* __restrict__ n_heavy, int64_t Kp,
                                       int8_t* __restrict__ rowdig, unsigned int* __restrict__ mask) {
@@ -59,7 +59,7 @@ __global__ void sp_gram_rowdig_kernel(const unsigned long long* __restrict__ fix
     balanced_digits(v, d);
 #pragma unroll
     for (int j = 0; j < kMaxDigits; ++j) {
-      rowdig[i * kMaxDigits + j] = d[j];
+      rowdig[j * Kp + i] = d[j];
       if (d[j]) m |= 1u << j;
     }
   }
@@ -100,10 +100,11 @@ __global__ void sp_gram_bits_kernel(const unsigned long long* __restrict__ nx, i
 }
 
 // A'[(k - k0) * nd + jj][i] = B[k][i] ? d_{dj[jj]}(row i) : 0 for the BK u
-// columns of the block: one thread per (column, 16-row chunk).
+// columns of the block: one thread per (column, 16-row chunk); the 0/1
+// bytes become byte masks (x * 0xff, no carries) ANDed with the plane.
 __global__ void sp_gram_digits_kernel(const int8_t* __restrict__ B, int64_t Kp, int32_t k0, int32_t bk,
-                                      int32_t n, const int8_t* __restrict__ rowdig, const int32_t* __restrict__ dj,
-                                      int32_t nd, int8_t* __restrict__ Ap) {
+                                      int32_t n, const int8_t* __restrict__ rowdig, int64_t plane_stride,
+                                      const int32_t* __restrict__ dj, int32_t nd, int8_t* __restrict__ Ap) {
   const int64_t chunks = Kp / 16;
   const int64_t total = static_cast<int64_t>(bk) * chunks;
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
@@ -113,23 +114,11 @@ __global__ void sp_gram_digits_kernel(const int8_t* __restrict__ B, int64_t Kp, 
     const int64_t k = k0 + kk;
     uint4 bits = make_uint4(0u, 0u, 0u, 0u);
     if (k < n) bits = __ldg(reinterpret_cast<const uint4*>(B + k * Kp) + ch);
-    const uint32_t bw[4] = {bits.x, bits.y, bits.z, bits.w};
+    const uint4 m = make_uint4(bits.x * 0xffu, bits.y * 0xffu, bits.z * 0xffu, bits.w * 0xffu);
     for (int jj = 0; jj < nd; ++jj) {
-      const int j = dj[jj];
-      uint32_t ow[4];
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        uint32_t o = 0;
-#pragma unroll
-        for (int t4 = 0; t4 < 4; ++t4) {
-          const int64_t i = 16 * ch + 4 * b + t4;
-          const uint32_t bit = (bw[b] >> (8 * t4)) & 1u;
-          const uint32_t dv = static_cast<uint8_t>(__ldg(rowdig + i * kMaxDigits + j));
-          o |= (bit ? dv : 0u) << (8 * t4);
-        }
-        ow[b] = o;
-      }
-      reinterpret_cast<uint4*>(Ap + (kk * nd + jj) * Kp)[ch] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+      const uint4 dv = __ldg(reinterpret_cast<const uint4*>(rowdig + static_cast<int64_t>(dj[jj]) * plane_stride) + ch);
+      reinterpret_cast<uint4*>(Ap + (kk * nd + jj) * Kp)[ch] =
+          make_uint4(dv.x & m.x, dv.y & m.y, dv.z & m.z, dv.w & m.w);
     }
   }
 }
@@ -142,8 +131,11 @@ struct GramArgs {
   int64_t M;
   int32_t n;
   int32_t out_begin, gl_begin;
-  int32_t lo_bits, scale, finalize, levels;
-  unsigned long long* gl;            // light sums (hi, lo); deep levels: G out
+  int32_t lo_bits, scale, finalize, levels, vb;
+  unsigned long long* gl;            // light sums (hi, lo); more than two levels: G out
+  const unsigned long long* dacc;    // two levels: the second level's pair sums [cell] (hi, lo)
+  const unsigned long long* dcolsum; // [4][n] second level
+  const unsigned long long* dcacc;   // [2] second level
   const unsigned long long* colsum;  // [4][n]
   const unsigned long long* cacc;    // [2]
   void* dist;
@@ -177,7 +169,7 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
     const int64_t cell = static_cast<int64_t>(s - a.gl_begin) * n + k;
     const ulonglong2 light = reinterpret_cast<const ulonglong2*>(a.gl)[cell];
     G += (static_cast<__int128>(light.x) << a.lo_bits) + static_cast<__int128>(light.y);
-    if (a.levels > 1) {  // sp_deep_epilogue_kernel finishes the slot from (hi, lo)
+    if (a.levels > 2) {  // sp_deep_epilogue_kernel finishes the slot from (hi, lo)
       reinterpret_cast<longlong2*>(a.gl)[cell] =
           make_longlong2(static_cast<long long>(G >> a.lo_bits), static_cast<long long>(G & lo_mask));
       continue;
@@ -186,8 +178,24 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
                        static_cast<__int128>(xs[3 * n + k] + xs[3 * n + l]);
     const __int128 X = (static_cast<__int128>(xs[k] + xs[l]) << a.lo_bits) +
                        static_cast<__int128>(xs[n + k] + xs[n + l]);
-    const Real tv = fixed_to_real<Real>(P + Cd - G, a.scale);
-    Real dv = fixed_to_real<Real>(X - 2 * G, a.scale);
+    Real tv, dv;
+    if (a.levels == 2) {  // lengths off the main grid: the second level, exact, fused
+      const unsigned long long* ys = a.dcolsum;
+      const ulonglong2 G1l = reinterpret_cast<const ulonglong2*>(a.dacc)[cell];
+      const __int128 G1 = (static_cast<__int128>(G1l.x) << a.lo_bits) + static_cast<__int128>(G1l.y);
+      const __int128 P1 = (static_cast<__int128>(ys[2 * n + k] + ys[2 * n + l]) << a.lo_bits) +
+                          static_cast<__int128>(ys[3 * n + k] + ys[3 * n + l]);
+      const __int128 X1 = (static_cast<__int128>(ys[k] + ys[l]) << a.lo_bits) +
+                          static_cast<__int128>(ys[n + k] + ys[n + l]);
+      const __int128 C1 = (static_cast<__int128>(a.dcacc[0]) << a.lo_bits) + static_cast<__int128>(a.dcacc[1]);
+      tv = two_levels_to_real<Real>(static_cast<unsigned __int128>(P + Cd - G),
+                                    static_cast<unsigned __int128>(P1 + C1 - G1), a.vb, a.scale);
+      dv = two_levels_to_real<Real>(static_cast<unsigned __int128>(X - 2 * G),
+                                    static_cast<unsigned __int128>(X1 - 2 * G1), a.vb, a.scale);
+    } else {
+      tv = fixed_to_real<Real>(P + Cd - G, a.scale);
+      dv = fixed_to_real<Real>(X - 2 * G, a.scale);
+    }
     if (a.finalize) dv = tv == Real(0) ? Real(0) : dv / tv;
     const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
     dist[off] = dv;

@@ -562,7 +562,7 @@ struct DeviceState {
   // heavy rows on the tensor cores (gram_kernels.cuh): 0/1 rows B, digit
   // table, per-block digit planes A', GEMM output C, cuBLASLt state
   DevBuf gbits, growdig, gmask, gdj, gA, gC, gws;
-  int64_t gram_kp = 0;
+  int64_t gram_kp = 0, gram_kpmax = 0;  // heavy rows (padded), digit-plane stride
   int32_t gram_nd = 0;
   cublasLtHandle_t lt = nullptr;
   cublasLtMatmulDesc_t lt_op = nullptr;
@@ -898,7 +898,10 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
       SF_CUDA(cudaGetLastError());
       d.launches += 4;
     }
-    constexpr int NT = 512;
+#ifndef SF_LIGHT_NT
+#define SF_LIGHT_NT 1024
+#endif
+    constexpr int NT = SF_LIGHT_NT;  // the kernel is bound by member-load latency: many warps
     auto* kern = sp_light_column_kernel<NT>;
     const int smem = 2 * kLightWin * 8;
     SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1089,6 +1092,7 @@ sf_status gram_prepare(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   SF_CUDA(cudaMemsetAsync(d.gmask.p, 0, 8, st));
   // digits of every permuted row (a bound on the heavy rows: all rows)
   const int64_t kp_max = (W64 * 64 + 127) / 128 * 128;
+  d.gram_kpmax = kp_max;
   if (d.growdig.bytes < static_cast<size_t>(kp_max) * kMaxDigits)
     SF_TRY(d.growdig.alloc(d.dev, static_cast<size_t>(kp_max) * kMaxDigits, "row digits"));
   sp_gram_rowdig_kernel<<<grid_for(kp_max, 256), 256, 0, st>>>(d.fixbit.as<unsigned long long>(),
@@ -1207,6 +1211,10 @@ sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, 
   g.scale = plan->scale;
   g.finalize = finalize ? 1 : 0;
   g.levels = plan->levels;
+  g.vb = plan->vb;
+  g.dacc = plan->levels > 1 ? d.deepsum.as<unsigned long long>() : nullptr;
+  g.dcolsum = plan->levels > 1 ? d.dcolsum.as<unsigned long long>() : nullptr;
+  g.dcacc = plan->levels > 1 ? d.dcacc.as<unsigned long long>() : nullptr;
   g.gl = d.lightsum.as<unsigned long long>();
   g.colsum = d.colsum.as<unsigned long long>();
   g.cacc = d.cacc.as<unsigned long long>();
@@ -1214,7 +1222,8 @@ sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, 
   g.tot = d.tot.p;
   for (int k0 = k_begin; k0 < k_end; k0 += bk) {
     sp_gram_digits_kernel<<<grid_for(static_cast<int64_t>(bk) * (Kp / 16), 256), 256, 0, st>>>(
-        d.gbits.as<int8_t>(), Kp, k0, bk, n, d.growdig.as<int8_t>(), d.gdj.as<int32_t>(), nd, d.gA.as<int8_t>());
+        d.gbits.as<int8_t>(), Kp, k0, bk, n, d.growdig.as<int8_t>(), d.gram_kpmax, d.gdj.as<int32_t>(), nd,
+        d.gA.as<int8_t>());
     SF_CUDA(cudaGetLastError());
     const int64_t l_start = static_cast<int64_t>(k0) + c0 + 1;  // < n_ext - W (sparse_n_ext)
     while (d.gemm_ev.size() < 2 * (d.gemm_count + 1)) {
@@ -1712,7 +1721,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
           for (int k0 = 0; k0 < n; k0 += gw) {
             const int k1 = std::min(n, k0 + gw);
             SF_TRY(gram_run(plan, d, p0, p1, p0, finalize, st, k0, k1));
-            SF_TRY(deep_epilogue(p0, p1, k0, k1));
+            if (plan->levels > 2) SF_TRY(deep_epilogue(p0, p1, k0, k1));  // two levels: fused in the epilogue
             SF_TRY(finished(p0, p1, k0, k1));
           }
           continue;

@@ -511,7 +511,14 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
 // the window (up to kLightWin stripes of (hi, lo) limbs) is written to the
 // light-sum array once. No global atomics; the limb sums are exact integers,
 // so the order of the shared-memory atomics does not change the bits.
-constexpr int kLightWin = 12800;  // stripes per shared-memory window (200 KB of limbs)
+#ifndef SF_LIGHT_WIN
+#define SF_LIGHT_WIN 12800
+#endif
+#ifndef SF_LIGHT_UNROLL
+#define SF_LIGHT_UNROLL 4
+#endif
+constexpr int kLightWin = SF_LIGHT_WIN;        // stripes per shared-memory window (16 B each)
+constexpr int kLightUnroll = SF_LIGHT_UNROLL;  // member loads in flight per lane
 
 // Entries per column: one count per light member (rows with >= 2 members).
 __global__ void sp_col_count_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ lptr,
@@ -607,29 +614,49 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
     const int32_t* mem = lmem + ri.b0;
     const unsigned long long v = ri.v;
     const ulonglong2 L = ilimbs_of(v, lo_bits);
-    // partners above: slot (b - k - 1, k), b in [k + w0 + 1, k + w1]
+    // partners above: slot (b - k - 1, k), b in [k + w0 + 1, k + w1]; the
+    // member loads are issued kUnroll x 32 at a time (the kernel is bound by
+    // their latency: each row's list is read once per member column)
     int j0 = w0 > 0 ? lower_bound_i32(mem, i + 1, x, k + w0 + 1) : i + 1;
-    for (int j = j0 + lane;; j += 32) {
-      int s = w1;
-      if (j < x) s = __ldg(mem + j) - k - 1;
-      const bool live = s < w1;
-      if (live) {
-        window_add<WIDE>(acc + 4 * (s - w0), v, L);
-        ++pairs;
+    for (int jb = j0;; jb += 32 * kLightUnroll) {
+      int s[kLightUnroll];
+#pragma unroll
+      for (int u = 0; u < kLightUnroll; ++u) {
+        const int j = jb + lane + 32 * u;
+        s[u] = j < x ? __ldg(mem + j) - k - 1 : w1;
       }
-      if (!__all_sync(0xffffffffu, live)) break;  // sorted: later members are past the window
+      bool all_live = true;
+#pragma unroll
+      for (int u = 0; u < kLightUnroll; ++u) {
+        const bool live = s[u] < w1;
+        all_live = all_live && live;
+        if (live) {
+          window_add<WIDE>(acc + 4 * (s[u] - w0), v, L);
+          ++pairs;
+        }
+      }
+      if (!__all_sync(0xffffffffu, all_live)) break;  // sorted: later members are past the window
     }
     // partners below: slot (n - (k - b) - 1, k), b in [k - n + 1 + w0, k - n + w1]
     j0 = w0 > 0 ? lower_bound_i32(mem, 0, i, k - n + 1 + w0) : 0;
-    for (int j = j0 + lane;; j += 32) {
-      int s = w1;
-      if (j < i) s = n - (k - __ldg(mem + j)) - 1;
-      const bool live = s < w1;
-      if (live) {
-        window_add<WIDE>(acc + 4 * (s - w0), v, L);
-        ++pairs;
+    for (int jb = j0;; jb += 32 * kLightUnroll) {
+      int s[kLightUnroll];
+#pragma unroll
+      for (int u = 0; u < kLightUnroll; ++u) {
+        const int j = jb + lane + 32 * u;
+        s[u] = j < i ? n - (k - __ldg(mem + j)) - 1 : w1;
       }
-      if (!__all_sync(0xffffffffu, live)) break;
+      bool all_live = true;
+#pragma unroll
+      for (int u = 0; u < kLightUnroll; ++u) {
+        const bool live = s[u] < w1;
+        all_live = all_live && live;
+        if (live) {
+          window_add<WIDE>(acc + 4 * (s[u] - w0), v, L);
+          ++pairs;
+        }
+      }
+      if (!__all_sync(0xffffffffu, all_live)) break;
     }
     en = nen;
     if (en_next < e1) ri = info[en.x];

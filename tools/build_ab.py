@@ -11,6 +11,11 @@ sys.path.insert(0, str(ROOT))
 from paper_2005_05826_b200 import build  # noqa: E402
 
 VARIANTS = {
+    # light column kernel: window stripes / member loads in flight / threads
+    "lw12800u8": dict(LIGHT_WIN=12800, LIGHT_UNROLL=8, LIGHT_NT=1024),
+    "lw6400u4": dict(LIGHT_WIN=6400, LIGHT_UNROLL=4, LIGHT_NT=1024),
+    "lw6400u8": dict(LIGHT_WIN=6400, LIGHT_UNROLL=8, LIGHT_NT=1024),
+    "lw4224u4n512": dict(LIGHT_WIN=4224, LIGHT_UNROLL=4, LIGHT_NT=512),
     "v16u1f1": dict(V=16, UC=1, NW=8, MINB=2, FG=1),
     "v16u1f4": dict(V=16, UC=1, NW=8, MINB=2, FG=4),
     "v8u2f1": dict(V=8, UC=2, NW=8, MINB=2, FG=1),
