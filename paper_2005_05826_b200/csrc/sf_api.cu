@@ -555,6 +555,7 @@ struct DeviceState {
   DevBuf ccnt, cptr, cent, cscantmp, linfo;
   size_t cscan_bytes = 0;
   bool light_columns = false;
+  bool defer_light = false;  // column kernel launched per GEMM column group (tensor-core path)
   // deeper fixed-point levels: deep rows, their levels, member CSR, per-slot sums
   DevBuf drows, dfix, dcnt, dptr, dmem, dent, dcolsum, dcacc, deepsum, dscantmp;
   size_t dscan_bytes = 0;
@@ -659,13 +660,14 @@ struct SplitCfg {
   static constexpr int SCATTER_NW = 8;
 };
 
-// |X_e| threshold of the split path: rows at or above it are walked.
+// |X_e| threshold of the split path: rows at or above it are heavy (tensor-
+// core GEMMs, cost ~ number of heavy rows), the rest light (scatter, cost ~
+// pairs ~ |X_e|^2). Measured best with the column-owned light scatter:
+// 0.04 at n = 25,000 (C3: 119.6 ms vs 122.0 at 0.03 and 123.1 at 0.05,
+// profiles/r02_heavyfrac_c3_col3.jsonl); beyond, the size-aware form of
+// round 1 (light pairs grow as x^2 and spread over more columns).
 int split_heavy_min(int n) {
-  // measured best with the banded light scatter: 0.03 at n = 25,000 (C3,
-  // profiles/r01_ab_c3_split_*heavyfrac*), 0.02 at n = 113,721 (C5 shard,
-  // profiles/r01_ab_c5_shard_heavyfrac.jsonl): light pairs grow as x^2 and
-  // their atomics spread over more bands as n grows
-  double frac = n > 25000 ? 0.03 * std::pow(25000.0 / n, 0.25) : 0.03;
+  double frac = n > 25000 ? 0.04 * std::pow(25000.0 / n, 0.25) : 0.04;
   if (const char* e = std::getenv("SF_HEAVY_FRAC")) frac = std::atof(e);
   return std::max(2, static_cast<int>(frac * n));
 }
@@ -848,6 +850,25 @@ bool light_banded() {
   return !(e && std::atoi(e) == 0);
 }
 
+#ifndef SF_LIGHT_NT
+#define SF_LIGHT_NT 1024
+#endif
+// Column-owned light scatter of stripes [p0, p1) for columns [k0, k1).
+sf_status light_columns_run(sf_plan* plan, DeviceState& d, cudaStream_t st, int p0, int p1, int k0, int k1) {
+  constexpr int NT = SF_LIGHT_NT;  // the kernel is bound by member-load latency: many warps
+  auto* kern = sp_light_column_kernel<NT>;
+  const int smem = 2 * kLightWin * 8;
+  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<std::max(1, std::min(k1 - k0, 65535)), NT, smem, st>>>(
+      d.cptr.as<uint32_t>(), d.cent.as<uint2>(), d.linfo.as<LightRowInfo>(), d.lmem.as<int32_t>(), plan->lo_bits,
+      plan->n, k0, k1, p0, p0, p1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>(),
+      // test hook: SF_LIGHT_LIMB_MODE=1|2 forces the wider exact limb modes
+      std::getenv("SF_LIGHT_LIMB_MODE") ? std::atoi(std::getenv("SF_LIGHT_LIMB_MODE")) : 0);
+  SF_CUDA(cudaGetLastError());
+  d.launches++;
+  return SF_OK;
+}
+
 // Banded light scatter: member CSR once per run, then one launch per
 // (512-stripe x KB-column) band of the pass, sized to stay in L2.
 sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, int p0, int p1,
@@ -898,19 +919,9 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
       SF_CUDA(cudaGetLastError());
       d.launches += 4;
     }
-#ifndef SF_LIGHT_NT
-#define SF_LIGHT_NT 1024
-#endif
-    constexpr int NT = SF_LIGHT_NT;  // the kernel is bound by member-load latency: many warps
-    auto* kern = sp_light_column_kernel<NT>;
-    const int smem = 2 * kLightWin * 8;
-    SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<std::min(n, 65535), NT, smem, st>>>(d.cptr.as<uint32_t>(), d.cent.as<uint2>(),
-                                             d.linfo.as<LightRowInfo>(), d.lmem.as<int32_t>(), plan->lo_bits, n,
-                                             p0, p0, p1, d.lightsum.as<unsigned long long>(),
-                                             d.exec_ctr.as<unsigned long long>());
-    SF_CUDA(cudaGetLastError());
-    d.launches++;
+    // the tensor-core path launches the column kernel per column group,
+    // just before that group's GEMM blocks (light_columns_run)
+    if (!d.defer_light) SF_TRY(light_columns_run(plan, d, st, p0, p1, 0, n));
     return SF_OK;
   }
   double band_mb = 32.0;  // measured: 32 MB <= 64 MB < 96 MB (profiles/r01_ab_c3_split_band*)
@@ -1509,6 +1520,10 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       SF_TRY(wsparse_build(plan, d, C, st));
     } else if (plan->kernel == 10) {
       phase("embedding enqueued");
+      // with the tensor-core heavy path the column-owned light kernel runs per
+      // column group, right before that group's GEMM blocks, so each group's
+      // stripes are final (and copied out) while later groups compute
+      d.defer_light = d.banded && d.light_columns && heavy_gemm_enabled();
       SF_TRY(split_build(plan, d, st));
       phase("split prep + first light pass enqueued");
     } else if (plan->kernel == 2) {
@@ -1655,6 +1670,10 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         if (gs == SF_ENOMEM) {
           gram = false;
           cudaGetLastError();
+          if (d.defer_light) {  // the DFMA walk expects the whole pass's light sums first
+            d.defer_light = false;
+            SF_TRY(light_columns_run(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), 0, n));
+          }
           if (std::getenv("SF_DEBUG"))
             std::fprintf(stderr, "stripefrac: device %d: %s; heavy rows on the DFMA walk\n", d.dev, sf::last_error());
         } else {
@@ -1720,6 +1739,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
           const int gw = ((n + ngrp - 1) / ngrp + bk - 1) / bk * bk;
           for (int k0 = 0; k0 < n; k0 += gw) {
             const int k1 = std::min(n, k0 + gw);
+            if (d.defer_light) SF_TRY(light_columns_run(plan, d, st, p0, p1, k0, k1));
             SF_TRY(gram_run(plan, d, p0, p1, p0, finalize, st, k0, k1));
             if (plan->levels > 2) SF_TRY(deep_epilogue(p0, p1, k0, k1));  // two levels: fused in the epilogue
             SF_TRY(finished(p0, p1, k0, k1));

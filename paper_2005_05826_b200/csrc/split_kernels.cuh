@@ -554,23 +554,49 @@ __global__ void sp_col_fill_kernel(const int32_t* __restrict__ lmem, const uint3
   }
 }
 
-// One light contribution into the shared-memory window: the row's value v
-// (< 2^63) as four 16-bit limbs into four 32-bit accumulators (native
-// shared atomic adds). Exact while a cell takes at most 65537 additions; a
-// cell takes one per light row holding the column, so columns with more
-// entries use 64-bit (hi, lo) compare-and-swap adds instead (WIDE).
-template <bool WIDE>
-__device__ __forceinline__ void window_add(uint32_t* cell, unsigned long long v, ulonglong2 L) {
-  if (WIDE) {
-    unsigned long long* c = reinterpret_cast<unsigned long long*>(cell);
-    atomicAdd(c, L.x);
-    atomicAdd(c + 1, L.y);
+// One light contribution into the shared-memory window, planes of
+// kLightWin cells (structure of arrays: the cells of different stripes fall
+// in different banks). The row's value v (< 2^63) goes in as limbs into
+// 32-bit native shared atomic adds, exact while no cell overflows: a cell
+// takes one addition per light row holding the column (the column's entry
+// count), so MODE 0 (three 21-bit limbs) serves columns with <= 2048
+// entries, MODE 1 (four 16-bit limbs) <= 65535, and MODE 2 adds the (hi, lo)
+// limbs with 64-bit compare-and-swap adds for any count.
+template <int MODE>
+__device__ __forceinline__ void window_add(uint32_t* acc, int cell, unsigned long long v, ulonglong2 L) {
+  if (MODE == 2) {
+    unsigned long long* a64 = reinterpret_cast<unsigned long long*>(acc);
+    atomicAdd(a64 + cell, L.x);
+    atomicAdd(a64 + kLightWin + cell, L.y);
+  } else if (MODE == 1) {
+    atomicAdd(acc + cell, static_cast<uint32_t>(v & 0xffffu));
+    atomicAdd(acc + kLightWin + cell, static_cast<uint32_t>((v >> 16) & 0xffffu));
+    atomicAdd(acc + 2 * kLightWin + cell, static_cast<uint32_t>((v >> 32) & 0xffffu));
+    atomicAdd(acc + 3 * kLightWin + cell, static_cast<uint32_t>(v >> 48));
   } else {
-    atomicAdd(cell, static_cast<uint32_t>(v & 0xffffu));
-    atomicAdd(cell + 1, static_cast<uint32_t>((v >> 16) & 0xffffu));
-    atomicAdd(cell + 2, static_cast<uint32_t>((v >> 32) & 0xffffu));
-    atomicAdd(cell + 3, static_cast<uint32_t>(v >> 48));
+    atomicAdd(acc + cell, static_cast<uint32_t>(v & 0x1fffffu));
+    atomicAdd(acc + kLightWin + cell, static_cast<uint32_t>((v >> 21) & 0x1fffffu));
+    atomicAdd(acc + 2 * kLightWin + cell, static_cast<uint32_t>(v >> 42));
   }
+}
+
+// The window cell's exact sum as (hi, lo) with hi * 2^lo_bits + lo = sum.
+template <int MODE>
+__device__ __forceinline__ ulonglong2 window_cell(const uint32_t* acc, int cell, int lo_bits) {
+  if (MODE == 2) {
+    const unsigned long long* a64 = reinterpret_cast<const unsigned long long*>(acc);
+    return make_ulonglong2(a64[cell], a64[kLightWin + cell]);
+  }
+  unsigned __int128 v;
+  if (MODE == 1)
+    v = static_cast<unsigned __int128>(acc[cell]) + (static_cast<unsigned __int128>(acc[kLightWin + cell]) << 16) +
+        (static_cast<unsigned __int128>(acc[2 * kLightWin + cell]) << 32) +
+        (static_cast<unsigned __int128>(acc[3 * kLightWin + cell]) << 48);
+  else
+    v = static_cast<unsigned __int128>(acc[cell]) + (static_cast<unsigned __int128>(acc[kLightWin + cell]) << 21) +
+        (static_cast<unsigned __int128>(acc[2 * kLightWin + cell]) << 42);
+  return make_ulonglong2(static_cast<unsigned long long>(v >> lo_bits),
+                         static_cast<unsigned long long>(v) & ((1ull << lo_bits) - 1ull));
 }
 
 // Per light row (by permuted index): member list offset and length, and its
@@ -591,7 +617,7 @@ __global__ void sp_light_rowinfo_kernel(const int32_t* __restrict__ perm, int32_
 // One warp per entry (light row holding the column): the lanes walk the
 // row's sorted members 32 at a time from the entry's own position. The next
 // entry's record is loaded while the current one is walked.
-template <bool WIDE>
+template <int MODE>
 __device__ __forceinline__ void light_column_window(const uint32_t e0, const uint32_t e1, const uint2* __restrict__ cent,
                                                     const LightRowInfo* __restrict__ info,
                                                     const int32_t* __restrict__ lmem, int32_t lo_bits, int k, int n,
@@ -631,7 +657,7 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
         const bool live = s[u] < w1;
         all_live = all_live && live;
         if (live) {
-          window_add<WIDE>(acc + 4 * (s[u] - w0), v, L);
+          window_add<MODE>(acc, s[u] - w0, v, L);
           ++pairs;
         }
       }
@@ -652,7 +678,7 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
         const bool live = s[u] < w1;
         all_live = all_live && live;
         if (live) {
-          window_add<WIDE>(acc + 4 * (s[u] - w0), v, L);
+          window_add<MODE>(acc, s[u] - w0, v, L);
           ++pairs;
         }
       }
@@ -668,39 +694,32 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
 template <int NT>
 __global__ void __launch_bounds__(NT) sp_light_column_kernel(
     const uint32_t* __restrict__ cptr, const uint2* __restrict__ cent, const LightRowInfo* __restrict__ info,
-    const int32_t* __restrict__ lmem, int32_t lo_bits, int32_t n, int32_t p0, int32_t s0, int32_t s1,
-    unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out) {
-  extern __shared__ uint32_t lacc[];  // [win][4]
+    const int32_t* __restrict__ lmem, int32_t lo_bits, int32_t n, int32_t k_begin, int32_t k_end, int32_t p0,
+    int32_t s0, int32_t s1, unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
+    int32_t min_mode) {
+  extern __shared__ uint32_t lacc[];  // 4 planes of kLightWin u32 cells (or 2 of u64)
   const int S = n / 2;
   const int send = min(s1, S);
-  const unsigned long long lo_mask = (1ull << lo_bits) - 1ull;
   unsigned long long pairs = 0;
-  for (int k = blockIdx.x; k < n; k += gridDim.x) {
+  for (int k = k_begin + blockIdx.x; k < k_end; k += gridDim.x) {
     const uint32_t e0 = cptr[k], e1 = cptr[k + 1];
-    const bool wide = e1 - e0 > 65535u;  // 16-bit limbs could overflow a 32-bit cell
+    // one addition per entry per cell: pick the narrowest exact limb mode
+    const int mode = max(min_mode, e1 - e0 <= 2048u ? 0 : e1 - e0 <= 65535u ? 1 : 2);
     for (int w0 = s0; w0 < send; w0 += kLightWin) {
       const int w1 = min(send, w0 + kLightWin);
       const int ww = w1 - w0;
-      for (int t = threadIdx.x; t < 4 * ww; t += NT) lacc[t] = 0u;
+      for (int t = threadIdx.x; t < 4 * kLightWin; t += NT) lacc[t] = 0u;
       __syncthreads();
-      if (wide)
-        light_column_window<true>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+      if (mode == 0)
+        light_column_window<0>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+      else if (mode == 1)
+        light_column_window<1>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
       else
-        light_column_window<false>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+        light_column_window<2>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
       __syncthreads();
       for (int t = threadIdx.x; t < ww; t += NT) {
-        ulonglong2 out;
-        if (wide) {
-          out = reinterpret_cast<const ulonglong2*>(lacc)[t];
-        } else {  // the window's exact sum, re-split into (hi, lo): only hi * 2^lo_bits + lo is used
-          const uint4 c = reinterpret_cast<const uint4*>(lacc)[t];
-          const unsigned __int128 v = static_cast<unsigned __int128>(c.x) +
-                                      (static_cast<unsigned __int128>(c.y) << 16) +
-                                      (static_cast<unsigned __int128>(c.z) << 32) +
-                                      (static_cast<unsigned __int128>(c.w) << 48);
-          out = make_ulonglong2(static_cast<unsigned long long>(v >> lo_bits),
-                                static_cast<unsigned long long>(v) & lo_mask);
-        }
+        const ulonglong2 out = mode == 0 ? window_cell<0>(lacc, t, lo_bits)
+                                         : mode == 1 ? window_cell<1>(lacc, t, lo_bits) : window_cell<2>(lacc, t, lo_bits);
         reinterpret_cast<ulonglong2*>(gl)[static_cast<int64_t>(w0 + t - p0) * n + k] = out;
       }
       __syncthreads();

@@ -643,12 +643,15 @@ def test_split_banded_light_scatter_is_bitwise_the_one_shot_scatter(device_ok, b
             monkeypatch.setenv("SF_LIGHT_BAND_MB", band_mb)
             if light_pass != "0":
                 monkeypatch.setenv("SF_LIGHT_PASS", light_pass)
-            for mode in ("column", "band"):  # column-owned (default) and banded
+            # column-owned (default; three exact limb modes) and banded
+            for mode, limbs in (("column", "0"), ("column", "1"), ("column", "2"), ("band", "0")):
                 monkeypatch.setenv("SF_LIGHT_MODE", mode)
+                monkeypatch.setenv("SF_LIGHT_LIMB_MODE", limbs)
                 d, t, gs = _gpu_stripes(problem, 1, 8, start, stop, N.KERNEL_SPLIT)
                 assert np.array_equal(d, want_d) and np.array_equal(t, want_t)
                 assert gs.updates_exec == ws.updates_exec  # same light pairs counted
             monkeypatch.delenv("SF_LIGHT_MODE")
+            monkeypatch.delenv("SF_LIGHT_LIMB_MODE")
             monkeypatch.delenv("SF_LIGHT_BAND_MB")
             monkeypatch.delenv("SF_LIGHT_PASS", raising=False)
             wd, wt = op.compute_stripes(problem, 1, 8, start, stop)
