@@ -564,6 +564,7 @@ struct DeviceState {
   // table, per-block digit planes A', GEMM output C, cuBLASLt state
   DevBuf gbits, growdig, gmask, gdj, gA, gC, gws;
   int64_t gram_kp = 0, gram_kpmax = 0;  // heavy rows (padded), digit-plane stride
+  int64_t gram_h = 0;                   // heavy rows
   int32_t gram_nd = 0;
   cublasLtHandle_t lt = nullptr;
   cublasLtMatmulDesc_t lt_op = nullptr;
@@ -573,6 +574,7 @@ struct DeviceState {
   std::vector<cudaEvent_t> gemm_ev;  // (start, end) per heavy GEMM of the run
   size_t gemm_count = 0;
   uint64_t gemm_ops = 0;
+  uint64_t heavy_updates = 0;  // (heavy row, slot) pairs the GEMMs covered (updates_exec)
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
   DevBuf wnb, woff, wcnt, wpool;
   DevBuf wpoola, wA, wbase;  // kernel 12: generalized pool, column sums, pool base + chunk total
@@ -1121,6 +1123,7 @@ sf_status gram_prepare(sf_plan* plan, DeviceState& d, cudaStream_t st) {
     if (hm[1] & (1u << j)) dj.push_back(j);
   if (dj.empty()) dj.push_back(0);  // no heavy length: one (zero) plane keeps the shapes valid
   d.gram_kp = Kp;
+  d.gram_h = H;
   d.gram_nd = static_cast<int32_t>(dj.size());
   if (d.gdj.bytes < dj.size() * 4) SF_TRY(d.gdj.alloc(d.dev, kMaxDigits * 4, "digit planes"));
   SF_CUDA(cudaMemcpyAsync(d.gdj.p, dj.data(), dj.size() * 4, cudaMemcpyHostToDevice, st));
@@ -1247,6 +1250,8 @@ sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, 
     SF_CUDA(cudaEventRecord(d.gemm_ev[2 * d.gemm_count + 1], st));
     ++d.gemm_count;
     d.gemm_ops += 2ull * static_cast<uint64_t>(M) * static_cast<uint64_t>(W) * static_cast<uint64_t>(Kp);
+    d.heavy_updates += static_cast<uint64_t>(d.gram_h) * static_cast<uint64_t>(span) *
+                       static_cast<uint64_t>(std::min(bk, k_end - k0));
     g.k0 = k0;
     const int64_t slots = static_cast<int64_t>(span) * std::min(bk, n - k0);
     if (plan->prec == SF_FP64)
@@ -1465,6 +1470,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
   SF_CUDA(cudaEventRecord(d.events[0], st));
   d.gemm_count = 0;
   d.gemm_ops = 0;
+  d.heavy_updates = 0;
   if (plan->kernel != 10 && plan->kernel != 12) {  // these kernels write every slot
     SF_CUDA(cudaMemsetAsync(d.dist.p, 0, static_cast<size_t>(slots) * w, st));
     if (d.tot.p && plan->metric != SF_WEIGHTED_UNNORMALIZED)
@@ -2463,6 +2469,7 @@ sf_status sf_plan_sync(sf_plan* plan) {
     }
     tens = std::max(tens, g_ms);
     tops += d.gemm_ops;
+    exec += d.heavy_updates;
     emb = std::max(emb, e_ms);
     str = std::max(str, s_ms);
     fin = std::max(fin, f_ms);

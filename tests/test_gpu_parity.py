@@ -882,3 +882,39 @@ def test_heavy_gemm_is_bitwise_the_dfma_walk(device_ok, prec, monkeypatch):
             assert np.array_equal(d, wd) and np.array_equal(t, wt)
         for var in ("SF_LIGHT_PASS", "SF_GRAM_BK"):
             monkeypatch.delenv(var, raising=False)
+
+
+def test_fit_probe_fallback_sizing_matches(device_ok, monkeypatch):
+    """With the pool fit probes disabled (SF_FORCE_PROBE_FAIL=1) the plans
+    size their chunks and light passes from free device memory instead: the
+    results are bit-identical (the fallback was untested)."""
+    inst = sf.random_instance(131, 300, 1200, 0.01)
+    problem = sf.flatten(inst.tree, inst.table)
+    for metric in (1, 3):
+        want = _gpu_stripes(problem, metric, 8, 0, 150, N.KERNEL_AUTO)
+        monkeypatch.setenv("SF_FORCE_PROBE_FAIL", "1")
+        got = _gpu_stripes(problem, metric, 8, 0, 150, N.KERNEL_AUTO)
+        monkeypatch.delenv("SF_FORCE_PROBE_FAIL")
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+def test_plan_write_strf_over_several_devices(device_ok, tmp_path):
+    """A plan sharded over devices writes the same .strf as a one-device
+    plan (each device's chunks are recorded on events of its own device —
+    ADVICE r1). Distinct devices when the box has them, else two shards of
+    device 0."""
+    inst = sf.random_instance(132, 400, 1500, 0.01)
+    problem = sf.flatten(inst.tree, inst.table)
+    ndev = min(2, N.lib().sf_device_count())
+    devs = list(range(ndev)) if ndev >= 2 else [0, 0]
+    paths = []
+    for dl in ([0], devs):
+        ex, _keep = N.make_exec(dl)
+        plan = C.c_void_p()
+        N.check(N.lib().sf_plan_create(problem.ref, 1, 8, 0, 200, C.byref(ex), C.byref(plan)))
+        N.check(N.lib().sf_plan_run(plan, 1))
+        p = tmp_path / f"p{len(dl)}.strf"
+        N.check(N.lib().sf_plan_write_strf(plan, str(p).encode()))
+        N.lib().sf_plan_destroy(plan)
+        paths.append(p.read_bytes())
+    assert paths[0] == paths[1]
