@@ -58,7 +58,7 @@ CONFIGS = {
     "small": dict(seed=7, n=4000, leaves=40000, density=0.002, subset=0,
                   metric="unweighted", precision="fp64", workload="small UW fp64 (quick check)"),
 }
-KERNELS = {"auto": 0, "dense": 1, "sparse": 2, "split": 10, "wsparse": 11, "uwalk": 12}
+KERNELS = {"auto": 0, "dense": 1, "sparse": 2, "split": 10, "wsparse": 11, "uwalk": 12, "wsplit": 13}
 METRIC_CODE = {"unweighted": 1, "weighted-unnormalized": 2, "weighted-normalized": 3, "generalized": 4}
 # algorithmic FP64/FP32 flops per update of update_entry (kernels.hpp:55-66),
 # FMA counted as 2: UW = sub, fma, max, fma; WN = sub, fma, add, fma; WU = sub, fma
@@ -479,6 +479,29 @@ def roofline_record(args, cfg, metric, prec, device, world, stop_all, E, n, str_
             "prep_ms_per_step": round(sum(emb_ms) / args.steps, 3),
             "algorithmic_speedup_vs_dense_fp64_roofline": round(
                 (E * stop_all * n * args.steps / (sum(dev_ms) / 1e3)) / (peak_fma / 4), 2),
+        }
+    if metric != 1 and t_ms > 0 and fp64_ops > 0:
+        # weighted split (13): the dense heavy-row kernel issues one DADD + one
+        # DFMA (fp32: FADD + FFMA) per (heavy row, slot); its CUDA-event time
+        # against the measured FMA-instruction peak of that pipe
+        pipe = "fp64" if prec == 8 else "fp32"
+        peak_fma = measured_fp_peak(device, pipe)
+        rate = fp64_ops / (t_ms / 1e3)
+        tr = ncu_traffic(cfg_name, "wx_dense_kernel")
+        return {
+            "bound": pipe, "achieved": round(rate * 2 / 1e12, 3), "peak": round(peak_fma * 2 / 1e12, 3),
+            "unit": "TFLOP/s", "frac": round(rate / peak_fma, 4) if peak_fma else None,
+            "unit_note": ("FMA-equivalent: pipe instructions x 2 (each (heavy row, slot) is a DADD + a DFMA, "
+                          "|u - v| an operand modifier), so frac = the pipe's issue fraction"),
+            "traffic": round(tr["dram_bytes"] / tr["stripes"] * (stop_all / max(world, 1))) if tr else None,
+            "traffic_unit": "DRAM bytes per launch",
+            "traffic_source": (f"{tr['source']} ({tr['stripes']} stripes, scaled per stripe)" if tr else None),
+            "kernel": "wx_dense_kernel (weighted split, kernel 13: heavy rows dense)",
+            "peak_source": "measured DFMA/FFMA loop (tools/fp_peaks.cu) on this device, x2 flops/FMA",
+            "pipe_ops_per_step": int(fp64_ops / args.steps),
+            "dense_ms_per_step": round(t_ms / args.steps, 3),
+            "stripe_ms_per_step": round(stripe_s * 1e3 / args.steps, 3),
+            "prep_ms_per_step": round(sum(emb_ms) / args.steps, 3),
         }
     if metric != 1 and fp64_ops > 0:
         # u-walk (12): the kernel counts the FP64-pipe instructions x live

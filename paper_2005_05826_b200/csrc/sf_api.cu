@@ -35,6 +35,7 @@
 #include "stripe_kernels.cuh"
 #include "wsparse_kernels.cuh"
 #include "wuwalk_kernels.cuh"
+#include "wsplit_kernels.cuh"
 #include "mantel_kernels.cuh"
 #include "stripefrac_cuda.h"
 
@@ -578,8 +579,16 @@ struct DeviceState {
   // weighted sparse walk (kernel 11): per chunk presence words, pool offsets, values
   DevBuf wnb, woff, wcnt, wpool;
   DevBuf wpoola, wA, wbase;  // kernel 12: generalized pool, column sums, pool base + chunk total
+  // kernel 13: row counts / flags / scans, dense heavy rows, light member and
+  // column lists, light column sums, the light part of every slot
+  DevBuf ws_cnt, ws_hflag, ws_hidx, ws_lcnt, ws_lptr, ws_hmask, ws_lmask, ws_UH, ws_LH, ws_lmid, ws_lval,
+      ws_ccnt, ws_cptr, ws_crow, ws_cval, ws_AL, ws_lightd, ws_tmp, ws_prank, ws_crank;
+  uint64_t host_fp64_ops = 0;  // FP64/FP32-pipe lane-ops counted on the host (kernel 13's dense part)
   DevBuf wnbo;               // kernel 12: combined (offset, presence word) cells
   int32_t light_pass = 0;  // stripes per light-sum pass (memory-bounded)
+  // tensor-core path: the light sums are sized at run time, once the GEMM
+  // operands (sized by the heavy-row count) are allocated
+  bool light_lazy = false, light_sized = false;
   size_t sort_bytes = 0;
   std::vector<cudaEvent_t> events;
   uint64_t launches = 0;  // kernel launches of the last run on this device
@@ -606,8 +615,11 @@ struct sf_plan {
   int metric = 0, prec = 0;
   int32_t n = 0, E = 0, start = 0, stop = 0;
   bool bits = false, exact = false;
+  size_t mem_budget = 0;  // sf_exec.mem_budget_bytes (0: none)
   double alpha = 1.0;  // generalized UniFrac exponent
-  int kernel = 1;  // 1 dense, 2 sparse-bit walk, 10 split, 11 weighted present-row walk, 12 u-walk
+  int kernel = 1;  // 1 dense, 2 sparse-bit walk, 10 split, 11 weighted present-row walk, 12 u-walk,
+                   // 13 weighted split
+  int32_t ws_G = 0, ws_nd = 8;  // kernel 13: fixed-point grid 2^-G of the light part, digit planes
   // split path: exact fixed-point levels of the lengths (fixed_levels)
   int32_t scale = 0, lo_bits = 32, vb = 63, levels = 1;
   std::vector<unsigned long long> fix, dfix;
@@ -993,6 +1005,51 @@ sf_status split_scatter_deep(sf_plan* plan, DeviceState& d, cudaStream_t st, int
   return SF_OK;
 }
 
+// Light-sum passes: the whole stripe range if its light sums (and deeper
+// levels' pair sums) fit next to everything else plus `after` bytes still to
+// be allocated, else passes of whole 512-stripe tiles; allocates them.
+sf_status light_sums_alloc(sf_plan* plan, DeviceState& d, size_t after) {
+  const int n = plan->n;
+  size_t freeb = 0;
+  // light sums (hi, lo) and the deeper levels' pair sums per slot
+  const size_t per_stripe = static_cast<size_t>(n) * 16 * static_cast<size_t>(plan->levels);
+  const size_t reserve = (1ull << 30);
+  const int span = d.b - d.a;
+  // without a budget, a probe allocation of the whole range plus `after` and
+  // the reserve answers "does it fit"; it returns to the pool for the
+  // allocations below. cudaMemGetInfo stalls up to ~100 ms on some calls
+  // (p99 63 ms on the box).
+  size_t fit = 0;
+  bool probed = false;
+  if (plan->mem_budget == 0 && !std::getenv("SF_LIGHT_PASS")) {
+    const size_t need = static_cast<size_t>(span) * per_stripe + after;
+    // steady state: the pool still holds the previous plan's freed blocks,
+    // so the same allocations are served again without a probe (a probe's
+    // single large block would fragment them)
+    if (pool_free_bytes(d.dev) >= need + reserve || probe_fits(d.dev, need + reserve, need)) {
+      fit = static_cast<size_t>(span);
+      probed = true;
+    }
+  }
+  if (!probed) {
+    SF_TRY(device_free_bytes(d.dev, &freeb));
+    fit = freeb > reserve + after ? (freeb - reserve - after) / per_stripe : 0;
+  }
+  if (plan->mem_budget > 0) fit = std::min(fit, plan->mem_budget / per_stripe);
+  int pass = static_cast<int>(std::min<size_t>(fit, static_cast<size_t>(span)));
+  if (pass < span) pass = std::max(512, pass / 512 * 512);
+  if (const char* e = std::getenv("SF_LIGHT_PASS")) pass = std::max(1, std::atoi(e));  // tests
+  d.light_pass = std::min(pass, span);
+  if (std::getenv("SF_DEBUG"))
+    std::fprintf(stderr, "stripefrac: device %d stripes [%d,%d): light pass %d stripes (%s)\n", d.dev, d.a, d.b,
+                 d.light_pass, probed ? "probe fit" : ("free " + std::to_string(freeb >> 20) + " MB").c_str());
+  SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * n * 16, "light-row sums"));
+  if (plan->levels > 1)
+    SF_TRY(d.deepsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * n * 16 * (plan->levels - 1),
+                           "deep-level sums"));
+  return SF_OK;
+}
+
 sf_status split_scatter(sf_plan* plan, DeviceState& d, cudaStream_t st, int s0, int s1, bool with_colsum) {
   const int n = plan->n;
   const int64_t E = plan->E;
@@ -1053,6 +1110,9 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   SF_CUDA(cudaGetLastError());
   d.launches += 7;  // key, sort, perm, transpose, extend, colsum (+ memsets)
   // first light pass (the one that also adds the light rows' column sums)
+  // tensor-core path with run-time light sums: the member lists and the
+  // column CSR now; the first pass's deep scatter once the sums exist
+  if (d.light_lazy) return split_scatter_banded(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), true);
   return split_scatter(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), true);
 }
 
@@ -1408,6 +1468,164 @@ sf_status wuwalk_build(sf_plan* plan, DeviceState& d, int32_t r0, int32_t C, cud
   return SF_OK;
 }
 
+// Heavy threshold of kernel 13 as a fraction of n (SF_WHEAVY_FRAC).
+double ws_heavy_frac() {
+  const char* e = std::getenv("SF_WHEAVY_FRAC");
+  return e ? std::atof(e) : 0.2;
+}
+
+// Kernel 13 (wsplit_kernels.cuh), after kernel 12's build of every chunk and
+// the column sums: row counts -> heavy / light split -> dense heavy rows and
+// light lists -> light scatter (exact) -> dense heavy rows + epilogue.
+template <class Real>
+sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream_t st) {
+  const int n = plan->n;
+  const int32_t E = plan->E;
+  const int32_t W = (E + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(n);
+  const uint32_t* nb = d.wnb.as<uint32_t>();
+  const uint32_t* off = d.woff.as<uint32_t>();
+  const Real* pool = d.wpool.as<Real>();
+  const int64_t Wr = static_cast<int64_t>(W) * 32;
+  // row counts and the split
+  if (d.ws_cnt.bytes < static_cast<size_t>(Wr) * 4) SF_TRY(d.ws_cnt.alloc(d.dev, static_cast<size_t>(Wr) * 4, "row counts"));
+  if (d.ws_hflag.bytes < static_cast<size_t>(E + 1) * 4) SF_TRY(d.ws_hflag.alloc(d.dev, static_cast<size_t>(E + 1) * 4, "heavy flags"));
+  if (d.ws_hidx.bytes < static_cast<size_t>(E + 1) * 4) SF_TRY(d.ws_hidx.alloc(d.dev, static_cast<size_t>(E + 1) * 4, "heavy index"));
+  if (d.ws_lcnt.bytes < static_cast<size_t>(E + 1) * 8) SF_TRY(d.ws_lcnt.alloc(d.dev, static_cast<size_t>(E + 1) * 8, "light counts"));
+  if (d.ws_lptr.bytes < static_cast<size_t>(E + 1) * 8) SF_TRY(d.ws_lptr.alloc(d.dev, static_cast<size_t>(E + 1) * 8, "light rows"));
+  if (d.ws_hmask.bytes < static_cast<size_t>(W) * 4) SF_TRY(d.ws_hmask.alloc(d.dev, static_cast<size_t>(W) * 4, "heavy masks"));
+  if (d.ws_lmask.bytes < static_cast<size_t>(W) * 4) SF_TRY(d.ws_lmask.alloc(d.dev, static_cast<size_t>(W) * 4, "light masks"));
+  if (d.ws_ccnt.bytes < static_cast<size_t>(n + 1) * 8) SF_TRY(d.ws_ccnt.alloc(d.dev, static_cast<size_t>(n + 1) * 8, "column counts"));
+  if (d.ws_cptr.bytes < static_cast<size_t>(n + 1) * 8) SF_TRY(d.ws_cptr.alloc(d.dev, static_cast<size_t>(n + 1) * 8, "column lists"));
+  if (d.ws_AL.bytes < static_cast<size_t>(n) * 16) SF_TRY(d.ws_AL.alloc(d.dev, static_cast<size_t>(n) * 16, "light column sums"));
+  size_t t1 = 0, t2 = 0, t3 = 0;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, d.ws_hflag.as<uint32_t>(), d.ws_hidx.as<uint32_t>(), E + 1, st));
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t2, d.ws_lcnt.as<unsigned long long>(),
+                                        d.ws_lptr.as<unsigned long long>(), E + 1, st));
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, d.ws_ccnt.as<unsigned long long>(),
+                                        d.ws_cptr.as<unsigned long long>(), n + 1, st));
+  const size_t tb = std::max(t1, std::max(t2, t3));
+  if (d.ws_tmp.bytes < tb) SF_TRY(d.ws_tmp.alloc(d.dev, tb, "scan scratch"));
+  wx_rowcount_kernel<<<std::min(W, 148 * 16), 256, 0, st>>>(nb, n_ext, n, W, E, d.ws_cnt.as<uint32_t>());
+  const uint32_t thr = static_cast<uint32_t>(std::max(1.0, std::ceil(ws_heavy_frac() * n)));
+  wx_classify_kernel<<<grid_for(Wr, 256), 256, 0, st>>>(d.ws_cnt.as<uint32_t>(), d.lens_pad.as<double>(), E, W, thr,
+                                                         d.ws_hflag.as<uint32_t>(), d.ws_lcnt.as<unsigned long long>(),
+                                                         d.ws_hmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>());
+  size_t tmp = d.ws_tmp.bytes;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.ws_tmp.p, tmp, d.ws_hflag.as<uint32_t>(), d.ws_hidx.as<uint32_t>(), E + 1, st));
+  tmp = d.ws_tmp.bytes;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.ws_tmp.p, tmp, d.ws_lcnt.as<unsigned long long>(),
+                                        d.ws_lptr.as<unsigned long long>(), E + 1, st));
+  SF_CUDA(cudaGetLastError());
+  uint32_t Hh = 0;
+  unsigned long long LT = 0;
+  SF_CUDA(cudaMemcpyAsync(&Hh, d.ws_hidx.as<uint32_t>() + E, 4, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaMemcpyAsync(&LT, d.ws_lptr.as<unsigned long long>() + E, 8, cudaMemcpyDeviceToHost, st));
+  SF_CUDA(cudaStreamSynchronize(st));
+  const int64_t H = Hh;
+  const int S = n / 2;
+  const int64_t ldh = (static_cast<int64_t>(n) + S + kWSK + kWSS + 64 + 3) / 4 * 4;
+  const size_t w = sizeof(Real);
+  const size_t uh_bytes = static_cast<size_t>(std::max<int64_t>(H, 1)) * static_cast<size_t>(ldh) * w;
+  if (d.ws_UH.bytes < uh_bytes) SF_TRY(d.ws_UH.alloc(d.dev, uh_bytes, "dense heavy rows"));
+  if (d.ws_LH.bytes < static_cast<size_t>(std::max<int64_t>(H, 1)) * w)
+    SF_TRY(d.ws_LH.alloc(d.dev, static_cast<size_t>(std::max<int64_t>(H, 1)) * w, "heavy lengths"));
+  const size_t lt = static_cast<size_t>(std::max<unsigned long long>(LT, 1));
+  if (d.ws_lmid.bytes < lt * 4) SF_TRY(d.ws_lmid.alloc(d.dev, lt * 4, "light members"));
+  if (d.ws_lval.bytes < lt * w) SF_TRY(d.ws_lval.alloc(d.dev, lt * w, "light member values"));
+  if (d.ws_crow.bytes < lt * 4) SF_TRY(d.ws_crow.alloc(d.dev, lt * 4, "column light rows"));
+  if (d.ws_cval.bytes < lt * w) SF_TRY(d.ws_cval.alloc(d.dev, lt * w, "column light values"));
+  if (d.ws_crank.bytes < lt * 4) SF_TRY(d.ws_crank.alloc(d.dev, lt * 4, "column ranks"));
+  const size_t pool_entries = std::max<size_t>(d.wpool.bytes / w, 1);
+  if (d.ws_prank.bytes < pool_entries * 4) SF_TRY(d.ws_prank.alloc(d.dev, pool_entries * 4, "member ranks"));
+  const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
+  if (d.ws_lightd.bytes < slots * 8) SF_TRY(d.ws_lightd.alloc(d.dev, slots * 8, "light part"));
+  // dense heavy rows, light member lists, column lists
+  SF_CUDA(cudaMemsetAsync(d.ws_UH.p, 0, uh_bytes, st));
+  wx_heavylen_kernel<Real><<<grid_for(E, 256), 256, 0, st>>>(d.ws_hflag.as<uint32_t>(), d.ws_hidx.as<uint32_t>(),
+                                                              d.lens_pad.as<double>(), E, d.ws_LH.as<Real>());
+  wx_fill_kernel<Real><<<std::min<int64_t>((W + 7) / 8, 148 * 64), 256, 0, st>>>(
+      nb, off, pool, n_ext, n, W, d.ws_hmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>(), d.ws_hidx.as<uint32_t>(),
+      d.ws_lptr.as<unsigned long long>(), ldh, d.ws_UH.as<Real>(), d.ws_lmid.as<int32_t>(), d.ws_lval.as<Real>(),
+      d.ws_prank.as<uint32_t>());
+  if (H > 0)
+    wx_extend_kernel<Real><<<grid_for(H * (ldh - n), 256), 256, 0, st>>>(d.ws_UH.as<Real>(), H, ldh, n);
+  wx_colcount_kernel<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
+      nb, d.nzmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>(), n_ext, n, W, d.ws_ccnt.as<unsigned long long>());
+  tmp = d.ws_tmp.bytes;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.ws_tmp.p, tmp, d.ws_ccnt.as<unsigned long long>(),
+                                        d.ws_cptr.as<unsigned long long>(), n + 1, st));
+  wx_colfill_kernel<Real><<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
+      nb, off, d.nzmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>(), pool, d.ws_prank.as<uint32_t>(),
+      d.lens_pad.as<double>(), n_ext, n, W, plan->ws_G, d.ws_cptr.as<unsigned long long>(), d.ws_crow.as<int32_t>(),
+      d.ws_cval.as<Real>(), d.ws_crank.as<uint32_t>(), d.ws_AL.as<unsigned long long>());
+  SF_CUDA(cudaGetLastError());
+  // light part of every slot (exact), then the dense heavy rows + epilogue
+  WSLightArgs la;
+  la.cptr = d.ws_cptr.as<unsigned long long>();
+  la.crow = d.ws_crow.as<int32_t>();
+  la.cval = d.ws_cval.p;
+  la.crank = d.ws_crank.as<uint32_t>();
+  la.lptr = d.ws_lptr.as<unsigned long long>();
+  la.lmid = d.ws_lmid.as<int32_t>();
+  la.lval = d.ws_lval.p;
+  la.lens = d.lens_pad.as<double>();
+  la.AL = d.ws_AL.as<unsigned long long>();
+  la.n = n;
+  la.s_begin = d.a;
+  la.s_end = d.b;
+  la.out_begin = d.a;
+  const int span = d.b - d.a;
+  la.G = plan->ws_G;
+  la.nd = plan->ws_nd;
+  const int max_tile = kWSLightSmem / (4 * la.nd);
+  const int ntiles = (span + max_tile - 1) / max_tile;
+  la.tile = (span + ntiles - 1) / ntiles;
+  la.lightd = d.ws_lightd.as<double>();
+  la.pairs = d.exec_ctr.as<unsigned long long>();
+  const size_t lsmem = static_cast<size_t>(la.nd) * static_cast<size_t>(la.tile) * 4;
+  SF_CUDA(cudaFuncSetAttribute(wx_light_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
+  wx_light_kernel<Real><<<dim3(static_cast<unsigned>(n), static_cast<unsigned>(ntiles)), kWSLightThreads, lsmem, st>>>(la);
+  SF_CUDA(cudaGetLastError());
+  WSDenseArgs da;
+  da.UH = d.ws_UH.p;
+  da.LH = d.ws_LH.p;
+  da.H = H;
+  da.ldh = ldh;
+  da.n = n;
+  da.s_begin = d.a;
+  da.s_end = d.b;
+  da.out_begin = d.a;
+  da.finalize = finalize ? 1 : 0;
+  da.lightd = d.ws_lightd.as<double>();
+  da.A = d.wA.as<double2>();
+  da.dist = d.dist.p;
+  da.tot = plan->metric == SF_WEIGHTED_UNNORMALIZED ? nullptr : d.tot.p;
+  const size_t dsmem = (2 * kWSR * (2 * kWSK + kWSS) + 2 * kWSR) * w;
+  const dim3 dgrid(static_cast<unsigned>((n + kWSK - 1) / kWSK), static_cast<unsigned>((span + kWSS - 1) / kWSS));
+  while (d.gemm_ev.size() < 2 * (d.gemm_count + 1)) {
+    cudaEvent_t e;
+    SF_CUDA(cudaEventCreate(&e));
+    d.gemm_ev.push_back(e);
+  }
+  SF_CUDA(cudaEventRecord(d.gemm_ev[2 * d.gemm_count], st));
+  if (plan->metric == SF_WEIGHTED_UNNORMALIZED) {
+    SF_CUDA(cudaFuncSetAttribute(wx_dense_kernel<kWU, Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem)));
+    wx_dense_kernel<kWU, Real><<<dgrid, kWSThreads, dsmem, st>>>(da);
+  } else {
+    SF_CUDA(cudaFuncSetAttribute(wx_dense_kernel<kWN, Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem)));
+    wx_dense_kernel<kWN, Real><<<dgrid, kWSThreads, dsmem, st>>>(da);
+  }
+  SF_CUDA(cudaGetLastError());
+  SF_CUDA(cudaEventRecord(d.gemm_ev[2 * d.gemm_count + 1], st));
+  ++d.gemm_count;
+  const uint64_t live = static_cast<uint64_t>(span) * static_cast<uint64_t>(n);
+  d.host_fp64_ops += 2ull * static_cast<uint64_t>(H) * live;  // DADD + DFMA per (heavy row, slot)
+  d.heavy_updates += static_cast<uint64_t>(H) * live;
+  d.launches += 14;
+  return SF_OK;
+}
+
 // Upper bound of the present (row, sample) entries: a row has at most
 // min(n, table entries under it) nonzero samples.
 uint64_t present_bound(const sf_problem* p) {
@@ -1471,7 +1689,8 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
   d.gemm_count = 0;
   d.gemm_ops = 0;
   d.heavy_updates = 0;
-  if (plan->kernel != 10 && plan->kernel != 12) {  // these kernels write every slot
+  d.host_fp64_ops = 0;
+  if (plan->kernel != 10 && plan->kernel != 12 && plan->kernel != 13) {  // these kernels write every slot
     SF_CUDA(cudaMemsetAsync(d.dist.p, 0, static_cast<size_t>(slots) * w, st));
     if (d.tot.p && plan->metric != SF_WEIGHTED_UNNORMALIZED)
       SF_CUDA(cudaMemsetAsync(d.tot.p, 0, static_cast<size_t>(slots) * w, st));
@@ -1519,7 +1738,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       SF_CUDA(cudaGetLastError());
       d.launches++;
     }
-    if (plan->kernel == 12) {
+    if (plan->kernel == 12 || plan->kernel == 13) {
       if (ci == 0) SF_CUDA(cudaMemsetAsync(d.wbase.p, 0, 16, st));
       SF_TRY(wuwalk_build(plan, d, c.r0, C, st));
     } else if (plan->kernel == 11) {
@@ -1546,33 +1765,37 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
     }
     SF_CUDA(cudaEventRecord(d.events[2 + 3 * ci], st));
     // ---- K2: stripe update over the chunk's rows
-    if (plan->kernel == 12) {
+    if (plan->kernel == 12 || plan->kernel == 13) {
       if (ci + 1 == plan->sched.chunks.size()) {  // every row is resident now: one pass
         const int64_t n_ext = sparse_n_ext(n);
         const int32_t W = (plan->E + 31) / 32;
         const bool gen = plan->metric == SF_GENERALIZED;
-        const int gb = grid_for(n, 128);
+        const int gb = (n + 31) / 32;  // wu_colsum_kernel: 32 columns per block
         if (plan->prec == SF_FP64) {
           if (gen)
-            wu_colsum_kernel<double, true><<<gb, 128, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
+            wu_colsum_kernel<double, true><<<gb, 32 * kColParts, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
                                                                d.lens_pad.as<double>(), d.wpool.as<double>(),
                                                                d.wpoola.as<double>(), d.wA.as<double2>());
           else
-            wu_colsum_kernel<double, false><<<gb, 128, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
+            wu_colsum_kernel<double, false><<<gb, 32 * kColParts, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
                                                                 d.lens_pad.as<double>(), d.wpool.as<double>(),
                                                                 nullptr, d.wA.as<double2>());
         } else {
           if (gen)
-            wu_colsum_kernel<float, true><<<gb, 128, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
+            wu_colsum_kernel<float, true><<<gb, 32 * kColParts, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
                                                               d.lens_pad.as<double>(), d.wpool.as<float>(),
                                                               d.wpoola.as<float>(), d.wA.as<double2>());
           else
-            wu_colsum_kernel<float, false><<<gb, 128, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
+            wu_colsum_kernel<float, false><<<gb, 32 * kColParts, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), n_ext, n, W,
                                                                d.lens_pad.as<double>(), d.wpool.as<float>(),
                                                                nullptr, d.wA.as<double2>());
         }
         wu_nzmask_kernel<<<grid_for(static_cast<int64_t>((W + 31) / 32) * n, 256), 256, 0, st>>>(
             d.wnb.as<uint32_t>(), n_ext, n, W, d.nzmask.as<uint32_t>());
+        if (plan->kernel == 13) {
+          SF_TRY(plan->prec == SF_FP64 ? wsplit_run<double>(plan, d, finalize, st)
+                                       : wsplit_run<float>(plan, d, finalize, st));
+        } else {
         // combined cells (SF_UWALK_NBO=0: separate word / offset arrays)
         const char* nbo_env = std::getenv("SF_UWALK_NBO");
         const int64_t cells = static_cast<int64_t>(W) * n_ext;
@@ -1609,13 +1832,15 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         SF_TRY(plan->prec == SF_FP64 ? launch_wuwalk<double>(plan->metric, a, st)
                                      : launch_wuwalk<float>(plan->metric, a, st));
         d.launches++;
+        }
         const int S = n / 2;
         if (n % 2 == 0 && S - 1 >= d.a && S - 1 < d.b) {  // duplicated half stripe
           const int64_t row_off = static_cast<int64_t>(S - 1 - d.a) * n;
+          const bool has_tot = plan->metric != SF_WEIGHTED_UNNORMALIZED;
           if (plan->prec == SF_FP64)
-            wu_mirror_kernel<double><<<grid_for(S, 256), 256, 0, st>>>(d.dist.as<double>(), a.tot ? d.tot.as<double>() : nullptr, n, row_off);
+            wu_mirror_kernel<double><<<grid_for(S, 256), 256, 0, st>>>(d.dist.as<double>(), has_tot ? d.tot.as<double>() : nullptr, n, row_off);
           else
-            wu_mirror_kernel<float><<<grid_for(S, 256), 256, 0, st>>>(d.dist.as<float>(), a.tot ? d.tot.as<float>() : nullptr, n, row_off);
+            wu_mirror_kernel<float><<<grid_for(S, 256), 256, 0, st>>>(d.dist.as<float>(), has_tot ? d.tot.as<float>() : nullptr, n, row_off);
           SF_CUDA(cudaGetLastError());
           d.launches++;
         }
@@ -1676,15 +1901,38 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         if (gs == SF_ENOMEM) {
           gram = false;
           cudaGetLastError();
-          if (d.defer_light) {  // the DFMA walk expects the whole pass's light sums first
-            d.defer_light = false;
-            SF_TRY(light_columns_run(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), 0, n));
-          }
           if (std::getenv("SF_DEBUG"))
             std::fprintf(stderr, "stripefrac: device %d: %s; heavy rows on the DFMA walk\n", d.dev, sf::last_error());
         } else {
           SF_TRY(gs);
         }
+      }
+      if (d.light_lazy) {
+        if (!d.light_sized) {
+          // the light sums next to the GEMM operands still to come (gram_run)
+          size_t extra = 0;
+          if (gram) {
+            const int span_all = d.b - d.a;
+            const int64_t bk = gram_block(span_all);
+            const int64_t M = bk * d.gram_nd;
+            extra = static_cast<size_t>(M * d.gram_kp) + static_cast<size_t>(M * (span_all + bk - 1)) * 4;
+          }
+          SF_TRY(light_sums_alloc(plan, d, extra));
+          d.light_sized = true;
+        }
+        // the first pass's deeper-level sums (split_build left them for now)
+        const int p1 = std::min(d.b, d.a + d.light_pass);
+        if (plan->levels > 1) {
+          SF_CUDA(cudaMemsetAsync(d.deepsum.p, 0,
+                                  static_cast<size_t>(p1 - d.a) * n * 16 * static_cast<size_t>(plan->levels - 1), st));
+          SF_TRY(split_scatter_deep(plan, d, st, d.a, p1, true));
+        }
+        a.gl = d.lightsum.as<unsigned long long>();
+        a.dacc = plan->levels > 1 ? d.deepsum.as<unsigned long long>() : nullptr;
+      }
+      if (!gram && d.defer_light) {  // the DFMA walk expects the whole pass's light sums first
+        d.defer_light = false;
+        SF_TRY(light_columns_run(plan, d, st, d.a, std::min(d.b, d.a + d.light_pass), 0, n));
       }
       int ci = 0;
       if (host_d && !d.copy_stream) SF_CUDA(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking));
@@ -2120,10 +2368,11 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   plan->stop = stop;
   plan->bits = metric == SF_UNWEIGHTED;
   plan->exact = ex && (ex->flags & SF_EXEC_EXACT_NO_FMA);
+  plan->mem_budget = (ex && ex->mem_budget_bytes > 0) ? static_cast<size_t>(ex->mem_budget_bytes) : 0;
   if (ex && ex->kernel != 0 && ex->kernel != 1 && ex->kernel != 2 && ex->kernel != 10 && ex->kernel != 11 &&
-      ex->kernel != 12)
+      ex->kernel != 12 && ex->kernel != 13)
     return fail(SF_EINVAL, "unknown kernel " + std::to_string(ex->kernel) +
-                               " (1 dense, 2 sparse walk, 10 split, 11 weighted walk, 12 u-walk)");
+                               " (1 dense, 2 sparse walk, 10 split, 11 weighted walk, 12 u-walk, 13 weighted split)");
   plan->kernel = (ex && ex->kernel >= 2) ? ex->kernel : 1;
   const int n = p->n_samples;
   // auto, unweighted: the intersection kernel (exact fixed-point sums), or
@@ -2143,11 +2392,25 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     return fail(SF_EINVAL, "the sparse bit kernels implement the unweighted metric only");
   if (plan->kernel >= 11 && metric == SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the weighted sparse walk implements the weighted metrics only");
-  if (metric == SF_GENERALIZED && plan->kernel < 11)
+  if (metric == SF_GENERALIZED && (plan->kernel < 11 || plan->kernel == 13))
     return fail(SF_EINVAL, "generalized UniFrac runs on the weighted sparse walks (kernel 11/12) only");
   plan->alpha = alpha;
-  const bool wsp = plan->kernel == 11 || plan->kernel == 12;
-  const bool wuw = plan->kernel == 12;
+  const bool wsp = plan->kernel == 11 || plan->kernel == 12 || plan->kernel == 13;
+  const bool wuw = plan->kernel == 12 || plan->kernel == 13;
+  if (plan->kernel == 13) {
+    // light part's fixed-point grid: every sum (<= AL_k + AL_l <= 2 sum L, the
+    // values being relative abundances <= 1) below 2^125, terms (<= 3 Lmax
+    // 2^G in magnitude) in nd balanced 16-bit digits
+    double tl = 0.0, lmax = 0.0;
+    for (int32_t r = 0; r < p->n_rows; ++r) {
+      tl += p->lengths[r];
+      lmax = std::max(lmax, p->lengths[r]);
+    }
+    const double bound = 2.0 * tl + 4.0 * lmax + 1.0;
+    plan->ws_G = 125 - (std::ilogb(bound) + 1);
+    const int term_bits = (lmax > 0 ? std::ilogb(3.0 * lmax) + 2 : 1) + plan->ws_G + 1;
+    plan->ws_nd = std::min(8, std::max(1, (term_bits + 15) / 16));
+  }
   plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;
   const size_t w = prec == SF_FP64 ? 8 : 4;
   const bool has_t = metric != SF_WEIGHTED_UNNORMALIZED;
@@ -2337,49 +2600,17 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
         SF_TRY(split_prepare(plan.get(), d));
         phase("node-packed prepare");
         {
-          // light sums for the whole range if they fit next to everything
-          // else, else for passes of whole 512-stripe tiles
-          size_t freeb = 0;
-          // light sums (hi, lo) and the deeper levels' pair sums per slot
-          const size_t per_stripe = static_cast<size_t>(n) * 16 * static_cast<size_t>(plan->levels);
-          const size_t reserve = (1ull << 30);
           const int span = d.b - d.a;
-          // without a budget, a probe allocation of the whole range plus the
-          // light member lists and the reserve answers "does it fit"; it
-          // returns to the pool for the allocations below. cudaMemGetInfo
-          // stalls up to ~100 ms on some calls (p99 63 ms on the box).
-          size_t fit = 0;
-          bool probed = false;
-          // the light member lists and cursors allocated after the light sums
           const size_t after = static_cast<size_t>(plan->E) * 4 * (3 + 2 * static_cast<size_t>(split_heavy_min(n)));
-          if (!(ex && ex->mem_budget_bytes > 0) && !std::getenv("SF_LIGHT_PASS")) {
-            const size_t need = static_cast<size_t>(span) * per_stripe + after;
-            // steady state: the pool still holds the previous plan's freed
-            // blocks, so the same allocations are served again without a probe
-            // (a probe's single large block would fragment them)
-            if (pool_free_bytes(d.dev) >= need + reserve || probe_fits(d.dev, need + reserve, need)) {
-              fit = static_cast<size_t>(span);
-              probed = true;
-            }
-          }
-          if (!probed) {
-            SF_TRY(device_free_bytes(d.dev, &freeb));
-            fit = freeb > reserve + after ? (freeb - reserve - after) / per_stripe : 0;
-          }
-          if (ex && ex->mem_budget_bytes > 0)
-            fit = std::min(fit, static_cast<size_t>(ex->mem_budget_bytes) / per_stripe);
-          int pass = static_cast<int>(std::min<size_t>(fit, static_cast<size_t>(span)));
-          if (pass < span) pass = std::max(512, pass / 512 * 512);
-          if (const char* e = std::getenv("SF_LIGHT_PASS")) pass = std::max(1, std::atoi(e));  // tests
-          d.light_pass = std::min(pass, span);
-          if (std::getenv("SF_DEBUG"))
-            std::fprintf(stderr, "stripefrac: device %d stripes [%d,%d): light pass %d stripes (%s)\n",
-                         d.dev, d.a, d.b, d.light_pass,
-                         probed ? "probe fit" : ("free " + std::to_string(freeb >> 20) + " MB").c_str());
-          SF_TRY(d.lightsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * n * 16, "light-row sums"));
-          if (plan->levels > 1)
-            SF_TRY(d.deepsum.alloc(d.dev, static_cast<size_t>(d.light_pass) * n * 16 * (plan->levels - 1),
-                                   "deep-level sums"));
+          const char* lm0 = std::getenv("SF_LIGHT_MODE");
+          d.light_lazy = light_banded() && !(lm0 && std::string(lm0) == "band") && heavy_gemm_enabled() &&
+                         static_cast<uint64_t>(plan->E) * static_cast<uint64_t>(split_heavy_min(n)) < (1ull << 32) &&
+                         split_heavy_min(n) <= 65535;
+          d.light_sized = false;
+          if (d.light_lazy)
+            d.light_pass = span;  // placeholder: sized in run_device after the GEMM operands
+          else
+            SF_TRY(light_sums_alloc(plan.get(), d, after));
           SF_TRY(d.mcount.alloc(d.dev, static_cast<size_t>(plan->E) * 4, "row presence counts"));
           // u32 member offsets; u16 cursors (light rows have < heavy_min members)
           d.banded = light_banded() &&
@@ -2477,7 +2708,7 @@ sf_status sf_plan_sync(sf_plan* plan) {
     unsigned long long c[2] = {0, 0};
     SF_CUDA(cudaMemcpy(c, d.exec_ctr.p, sizeof(c), cudaMemcpyDeviceToHost));
     exec += c[0];
-    fpops += c[1];
+    fpops += c[1] + d.host_fp64_ops;
   }
   plan->stats.launches = 0;
   for (auto& dp : plan->devs) plan->stats.launches += dp->launches;

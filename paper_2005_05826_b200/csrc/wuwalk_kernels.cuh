@@ -93,16 +93,26 @@ __global__ void wu_fill_kernel(const double* __restrict__ emb, int64_t stride, i
 }
 
 // Per-column double-double sums A[c] = sum over present rows of fl(L*v)
-// (generalized: of fl(L*v^a), the poola entries). Thread per column.
+// (generalized: of fl(L*v^a), the poola entries). Block = 32 columns x
+// kColParts word ranges (loads coalesced across the columns); the parts'
+// partial sums combine in a fixed order, so the result is deterministic.
+constexpr int kColParts = 8;
+
 template <class Real, bool GEN>
-__global__ void wu_colsum_kernel(const uint32_t* __restrict__ nb, const uint32_t* __restrict__ off,
-                                 int64_t n_ext, int32_t n, int32_t W, const double* __restrict__ lens,
-                                 const Real* __restrict__ pool, const Real* __restrict__ poola,
-                                 double2* __restrict__ A) {
-  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
-       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    double hi = 0.0, lo = 0.0;
-    for (int32_t w = 0; w < W; ++w) {
+__global__ void __launch_bounds__(32 * kColParts) wu_colsum_kernel(const uint32_t* __restrict__ nb,
+                                                                 const uint32_t* __restrict__ off, int64_t n_ext,
+                                                                 int32_t n, int32_t W, const double* __restrict__ lens,
+                                                                 const Real* __restrict__ pool,
+                                                                 const Real* __restrict__ poola,
+                                                                 double2* __restrict__ A) {
+  __shared__ double2 part[kColParts][32];
+  const int cl = threadIdx.x & 31, pi = threadIdx.x >> 5;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + cl;
+  const int32_t per = (W + kColParts - 1) / kColParts;
+  const int32_t w0 = pi * per, w1 = min(W, w0 + per);
+  double hi = 0.0, lo = 0.0;
+  if (c < n) {
+    for (int32_t w = w0; w < w1; ++w) {
       uint32_t bits = __ldg(nb + w * n_ext + c);
       if (!bits) continue;
       uint32_t q = __ldg(off + w * n_ext + c);
@@ -117,6 +127,15 @@ __global__ void wu_colsum_kernel(const uint32_t* __restrict__ nb, const uint32_t
         dd_add(hi, lo, term);
         ++q;
       }
+    }
+  }
+  part[pi][cl] = make_double2(hi, lo);
+  __syncthreads();
+  if (pi == 0 && c < n) {
+    for (int j = 1; j < kColParts; ++j) {
+      const double2 o = part[j][cl];
+      dd_add(hi, lo, o.x);
+      lo += o.y;
     }
     A[c] = make_double2(hi, lo);
   }

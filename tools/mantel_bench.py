@@ -1,10 +1,12 @@
 #!/usr/bin/env python
 """Mantel at scale on device: the fp64-vs-fp32 validation of
-the C3 unweighted matrix (acceptance.cpp:282-309's check, 25k samples), with
-999 permutations of the reference's stream, timed end to end.
+a benchmark configuration's matrix (acceptance.cpp:282-309's check; C3
+unweighted, C4 generalized alpha=0.5), with 999 permutations of the
+reference's stream, timed end to end, plus the fp32-vs-fp64 drift
+statistics of the two matrices.
 
-  python tools/mantel_bench.py [--config c3] [--perms 999]
-Prints one JSON line (r, p, seconds, gathered pairs per second).
+  python tools/mantel_bench.py [--config c3|c4] [--perms 999]
+Prints one JSON line (r, p, drift, seconds, gathered pairs per second).
 """
 import argparse
 import ctypes as C
@@ -21,17 +23,14 @@ import bench  # noqa: E402
 from paper_2005_05826_b200 import _native as N  # noqa: E402
 
 
-def full_matrix(problem, prec):
-    L = N.lib()
+def full_matrix(problem, cfg, prec):
+    """The n x n matrix through sf_compute_distance_matrix (device-resident
+    stripes, device condense)."""
     n = problem.n_samples
-    S = n // 2
-    dt = np.float64 if prec == 8 else np.float32
-    d = np.empty((S, n), dt)
-    t = np.empty((S, n), dt)
-    ex, _keep = N.make_exec([0])
-    N.check(L.sf_compute_stripes(problem.ref, 1, prec, 0, S, N.ptr(d), N.ptr(t), 1, C.byref(ex), None))
-    out = np.zeros((n, n))
-    N.check(L.sf_condense(prec, n, 0, S, N.ptr(d), N.ptr(out), 0))
+    out = np.empty((n, n))
+    ex, _keep = N.make_exec([0], alpha=cfg.get("alpha", 1.0))
+    N.check(N.lib().sf_compute_distance_matrix(problem.ref, bench.METRIC_CODE[cfg["metric"]], prec, N.ptr(out),
+                                               C.byref(ex), None))
     return out
 
 
@@ -45,9 +44,17 @@ def main():
     problem = bench.make_problem(cfg)
     n = problem.n_samples
     t0 = time.perf_counter()
-    m64 = full_matrix(problem, 8)
-    m32 = full_matrix(problem, 4)
+    m64 = full_matrix(problem, cfg, 8)
+    m32 = full_matrix(problem, cfg, 4)
     t1 = time.perf_counter()
+    iu = np.triu_indices(n, 1)
+    a64, a32 = m64[iu], m32[iu]
+    diff = np.abs(a32 - a64)
+    nz = a64 != 0
+    drift = {"max_abs": float(diff.max()), "mean_abs": float(diff.mean()),
+             "max_rel": float(np.max(diff[nz] / a64[nz])) if nz.any() else 0.0,
+             "exact_zeros_fp64": int((~nz).sum()), "zeros_mismatched": int(np.sum(~nz & (a32 != 0)))}
+    del a64, a32, diff, nz
     r = C.c_double()
     p = C.c_double()
     N.check(N.lib().sf_mantel(n, N.ptr(m64), N.ptr(m32), args.perms, args.seed, 0, C.byref(r), C.byref(p)))
@@ -55,7 +62,6 @@ def main():
     pairs = n * (n - 1) // 2
     # host baseline: one permutation's cross term, vectorised numpy gather
     # (the reference's loop is scalar: validate.cpp:131-149)
-    iu = np.triu_indices(n, 1)
     x = m64[iu] - m64[iu].mean()
     perm = np.random.default_rng(0).permutation(n)
     th0 = time.perf_counter()
@@ -63,7 +69,8 @@ def main():
     float(x @ (y - y.mean()))
     host_perm_s = time.perf_counter() - th0
     print(json.dumps({
-        "what": "mantel(UW fp64 DM, UW fp32 DM) on device, reference permutation stream",
+        "what": f"mantel({cfg['metric']} fp64 DM, fp32 DM) on device, reference permutation stream",
+        "config": args.config, "fp32_vs_fp64": drift,
         "workload": cfg["workload"], "n_samples": n, "permutations": args.perms, "seed": args.seed,
         "r": r.value, "r_squared": r.value ** 2, "p_value": p.value,
         "mantel_seconds": t2 - t1, "matrices_seconds": t1 - t0,
