@@ -81,7 +81,9 @@ typedef struct sf_exec {
                                (bitwise: the reference's adds in its order), 10 = split heavy
                                walk + light scatter (exact fixed-point sums, correctly rounded;
                                the default); weighted only: 11 = present-row walk (bitwise in
-                               exact mode), 12 = u-walk (the default; also SF_GENERALIZED) */
+                               exact mode), 12 = u-walk (the SF_GENERALIZED default), 13 = weighted
+                               split: dense heavy rows + exact fixed-point light scatter (the
+                               WN / WU default; falls back to 12 without the memory for it) */
   int32_t flags;            /* bit 0: SF_EXEC_EXACT_NO_FMA: bitwise-identical results (weighted:
                                no FMA; unweighted auto: the sparse walk instead of kernel 10) */
   double alpha;             /* SF_GENERALIZED only: the exponent, finite, >= 0 (ABI v3) */
@@ -99,10 +101,12 @@ typedef struct sf_stats {
   double stripe_ms;      /* device time of the stripe kernels (max over devices) */
   double finalize_ms;    /* device time of finalize (max over devices) */
   double total_ms;       /* device time of the whole run (max over devices) */
-  uint64_t fp64_ops;     /* FP64-pipe lane-ops of the DFMA heavy walk (kernel 10 with SF_HEAVY_GEMM=0)
-                            or the weighted u-walk (kernel 12); else 0 */
+  uint64_t fp64_ops;     /* FP64-pipe lane-ops of the DFMA heavy walk (kernel 10 with SF_HEAVY_GEMM=0),
+                            the weighted u-walk (kernel 12) or the weighted split's dense heavy rows
+                            (kernel 13: DADD + DFMA per heavy row and slot; fp32: the FP32 pipe); else 0 */
   uint64_t tensor_ops;   /* int8 tensor-core ops (2 per MAC) of the heavy-row GEMMs (kernel 10) */
-  double tensor_ms;      /* device time of those GEMMs (sum of launches, max over devices) */
+  double tensor_ms;      /* device time of the heavy-row kernels: kernel 10's GEMMs, kernel 13's
+                            dense kernel (sum of launches, max over devices) */
 } sf_stats;
 
 /* ---- library ------------------------------------------------------------ */

@@ -1584,8 +1584,18 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
   la.lightd = d.ws_lightd.as<double>();
   la.pairs = d.exec_ctr.as<unsigned long long>();
   const size_t lsmem = static_cast<size_t>(la.nd) * static_cast<size_t>(la.tile) * 4;
-  SF_CUDA(cudaFuncSetAttribute(wx_light_kernel<Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
-  wx_light_kernel<Real><<<dim3(static_cast<unsigned>(n), static_cast<unsigned>(ntiles)), kWSLightThreads, lsmem, st>>>(la);
+  auto light = [&](auto* kern) -> sf_status {
+    SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
+    kern<<<dim3(static_cast<unsigned>(n), static_cast<unsigned>(ntiles)), kWSLightThreads, lsmem, st>>>(la);
+    return SF_OK;
+  };
+  switch (la.nd) {  // digit planes: 16 bits each, from the lengths' range (plan time)
+    case 4: SF_TRY(light(wx_light_kernel<Real, 4>)); break;
+    case 5: SF_TRY(light(wx_light_kernel<Real, 5>)); break;
+    case 6: SF_TRY(light(wx_light_kernel<Real, 6>)); break;
+    case 7: SF_TRY(light(wx_light_kernel<Real, 7>)); break;
+    default: SF_TRY(light(wx_light_kernel<Real, 8>)); break;
+  }
   SF_CUDA(cudaGetLastError());
   WSDenseArgs da;
   da.UH = d.ws_UH.p;
@@ -1792,46 +1802,58 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         }
         wu_nzmask_kernel<<<grid_for(static_cast<int64_t>((W + 31) / 32) * n, 256), 256, 0, st>>>(
             d.wnb.as<uint32_t>(), n_ext, n, W, d.nzmask.as<uint32_t>());
+        bool uwalk = plan->kernel == 12;
         if (plan->kernel == 13) {
-          SF_TRY(plan->prec == SF_FP64 ? wsplit_run<double>(plan, d, finalize, st)
-                                       : wsplit_run<float>(plan, d, finalize, st));
-        } else {
-        // combined cells (SF_UWALK_NBO=0: separate word / offset arrays)
-        const char* nbo_env = std::getenv("SF_UWALK_NBO");
-        const int64_t cells = static_cast<int64_t>(W) * n_ext;
-        bool use_nbo = !(nbo_env && std::atoi(nbo_env) == 0);
-        if (use_nbo && d.wnbo.bytes < static_cast<size_t>(cells) * 8)
-          use_nbo = d.wnbo.alloc(d.dev, static_cast<size_t>(cells) * 8, "word/offset cells") == SF_OK;
-        cudaGetLastError();
-        if (use_nbo)
-          wu_combine_kernel<<<grid_for(cells, 256), 256, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), cells,
-                                                                   d.wnbo.as<unsigned long long>());
-        SF_CUDA(cudaGetLastError());
-        WUWalkArgs a;
-        a.nbo = use_nbo ? d.wnbo.as<unsigned long long>() : nullptr;
-        const char* lst = std::getenv("SF_UWALK_LIST");
-        a.nz = (lst && std::atoi(lst) == 0) ? nullptr : d.nzmask.as<uint32_t>();
-        a.nb = d.wnb.as<uint32_t>();
-        a.off = d.woff.as<uint32_t>();
-        a.pool = d.wpool.p;
-        a.poola = d.wpoola.p;
-        a.lens = d.lens_pad.as<double>();
-        a.A = d.wA.as<double2>();
-        a.n_ext = n_ext;
-        a.W = W;
-        a.n = n;
-        a.s_begin = d.a;
-        a.s_end = d.b;
-        a.out_begin = d.a;
-        a.finalize = finalize ? 1 : 0;
-        a.alpha = plan->alpha;
-        a.dist = d.dist.p;
-        a.tot = plan->metric == SF_WEIGHTED_UNNORMALIZED ? nullptr : d.tot.p;
-        a.exec_updates = d.exec_ctr.as<unsigned long long>();
-        a.fp64_ops = d.exec_ctr.as<unsigned long long>() + 1;
-        SF_TRY(plan->prec == SF_FP64 ? launch_wuwalk<double>(plan->metric, a, st)
-                                     : launch_wuwalk<float>(plan->metric, a, st));
-        d.launches++;
+          // without the memory for its dense rows / light lists the weighted
+          // split hands the run to the u-walk (same tolerance, no extra memory)
+          const sf_status ws = plan->prec == SF_FP64 ? wsplit_run<double>(plan, d, finalize, st)
+                                                     : wsplit_run<float>(plan, d, finalize, st);
+          if (ws == SF_ENOMEM) {
+            cudaGetLastError();
+            if (std::getenv("SF_DEBUG"))
+              std::fprintf(stderr, "stripefrac: device %d: %s; weighted rows on the u-walk\n", d.dev, sf::last_error());
+            uwalk = true;
+          } else {
+            SF_TRY(ws);
+          }
+        }
+        if (uwalk) {
+          // combined cells (SF_UWALK_NBO=0: separate word / offset arrays)
+          const char* nbo_env = std::getenv("SF_UWALK_NBO");
+          const int64_t cells = static_cast<int64_t>(W) * n_ext;
+          bool use_nbo = !(nbo_env && std::atoi(nbo_env) == 0);
+          if (use_nbo && d.wnbo.bytes < static_cast<size_t>(cells) * 8)
+            use_nbo = d.wnbo.alloc(d.dev, static_cast<size_t>(cells) * 8, "word/offset cells") == SF_OK;
+          cudaGetLastError();
+          if (use_nbo)
+            wu_combine_kernel<<<grid_for(cells, 256), 256, 0, st>>>(d.wnb.as<uint32_t>(), d.woff.as<uint32_t>(), cells,
+                                                                     d.wnbo.as<unsigned long long>());
+          SF_CUDA(cudaGetLastError());
+          WUWalkArgs a;
+          a.nbo = use_nbo ? d.wnbo.as<unsigned long long>() : nullptr;
+          const char* lst = std::getenv("SF_UWALK_LIST");
+          a.nz = (lst && std::atoi(lst) == 0) ? nullptr : d.nzmask.as<uint32_t>();
+          a.nb = d.wnb.as<uint32_t>();
+          a.off = d.woff.as<uint32_t>();
+          a.pool = d.wpool.p;
+          a.poola = d.wpoola.p;
+          a.lens = d.lens_pad.as<double>();
+          a.A = d.wA.as<double2>();
+          a.n_ext = n_ext;
+          a.W = W;
+          a.n = n;
+          a.s_begin = d.a;
+          a.s_end = d.b;
+          a.out_begin = d.a;
+          a.finalize = finalize ? 1 : 0;
+          a.alpha = plan->alpha;
+          a.dist = d.dist.p;
+          a.tot = plan->metric == SF_WEIGHTED_UNNORMALIZED ? nullptr : d.tot.p;
+          a.exec_updates = d.exec_ctr.as<unsigned long long>();
+          a.fp64_ops = d.exec_ctr.as<unsigned long long>() + 1;
+          SF_TRY(plan->prec == SF_FP64 ? launch_wuwalk<double>(plan->metric, a, st)
+                                       : launch_wuwalk<float>(plan->metric, a, st));
+          d.launches++;
         }
         const int S = n / 2;
         if (n % 2 == 0 && S - 1 >= d.a && S - 1 < d.b) {  // duplicated half stripe
@@ -2385,9 +2407,10 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                       nodepacked_bytes(k, p->n_rows, n) <= static_cast<size_t>(ex->mem_budget_bytes);
     plan->kernel = fits ? k : 1;
   }
-  // auto, weighted: the sparse walk over present rows (kernel 11)
-  // (the u-walk, kernel 12; in exact mode the bitwise present-row walk, 11)
-  if ((!ex || ex->kernel == 0) && metric != SF_UNWEIGHTED) plan->kernel = plan->exact ? 11 : 12;
+  // auto, weighted: WN / WU the weighted split (kernel 13), generalized the
+  // u-walk (12); in exact mode the bitwise present-row walk (11)
+  if ((!ex || ex->kernel == 0) && metric != SF_UNWEIGHTED)
+    plan->kernel = plan->exact ? 11 : metric == SF_GENERALIZED ? 12 : 13;
   if ((plan->kernel == 2 || plan->kernel == 10) && metric != SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the sparse bit kernels implement the unweighted metric only");
   if (plan->kernel >= 11 && metric == SF_UNWEIGHTED)
@@ -2409,7 +2432,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     const double bound = 2.0 * tl + 4.0 * lmax + 1.0;
     plan->ws_G = 125 - (std::ilogb(bound) + 1);
     const int term_bits = (lmax > 0 ? std::ilogb(3.0 * lmax) + 2 : 1) + plan->ws_G + 1;
-    plan->ws_nd = std::min(8, std::max(1, (term_bits + 15) / 16));
+    plan->ws_nd = std::min(8, std::max(4, (term_bits + 15) / 16));
   }
   plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;
   const size_t w = prec == SF_FP64 ? 8 : 4;

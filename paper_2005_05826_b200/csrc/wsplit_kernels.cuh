@@ -47,6 +47,28 @@ __device__ __forceinline__ unsigned __int128 wx_to_fix(double x, int G) {
   return 0;
 }
 
+// 64-bit shifts with PTX semantics: amounts >= 64 give 0.
+__device__ __forceinline__ unsigned long long wx_shl(unsigned long long x, uint32_t s) {
+  unsigned long long r;
+  asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(s));
+  return r;
+}
+__device__ __forceinline__ unsigned long long wx_shr(unsigned long long x, uint32_t s) {
+  unsigned long long r;
+  asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(x), "r"(s));
+  return r;
+}
+
+// The same value as two 64-bit words (lo, hi), branch-free.
+__device__ __forceinline__ void wx_fix2(double x, int G, unsigned long long& lo, unsigned long long& hi) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  const int ex = static_cast<int>(b >> 52);  // x >= 0
+  const unsigned long long m = (b & ((1ull << 52) - 1ull)) | (ex ? (1ull << 52) : 0ull);
+  const int sh = (ex ? ex : 1) - 1075 + G;  // value = m 2^sh on the grid
+  lo = sh >= 0 ? wx_shl(m, static_cast<uint32_t>(sh)) : wx_shr(m, static_cast<uint32_t>(-sh));
+  hi = sh >= 64 ? wx_shl(m, static_cast<uint32_t>(sh - 64)) : wx_shr(m, static_cast<uint32_t>(64 - sh));
+}
+
 // ---- build --------------------------------------------------------------------
 
 // m_r: samples with row r present (presence words nb[w][c], row 32w+i at bit 31-i).
@@ -306,7 +328,10 @@ struct WSLightArgs {
 constexpr int kWSLightThreads = 1024;
 constexpr int kWSLightSmem = 200 * 1024;  // digit planes: nd x tile x 4 bytes
 constexpr int kWSFold = 32768;            // rows between carry normalisations (2^15 x 2^15 adds < 2^31)
-constexpr int kWSUnroll = 4;              // member loads in flight per lane
+#ifndef SF_WS_UNROLL
+#define SF_WS_UNROLL 4
+#endif
+constexpr int kWSUnroll = SF_WS_UNROLL;   // member loads in flight per lane
 
 // first index in [a, b) of the sorted ids with id >= x
 __device__ __forceinline__ unsigned long long wx_lower(const int32_t* __restrict__ ids, unsigned long long a,
@@ -322,11 +347,16 @@ __device__ __forceinline__ unsigned long long wx_lower(const int32_t* __restrict
 }
 
 // Members [p, ...) of one row with ids <= hi, slot = id + sh: the lanes take
-// 32 x kWSUnroll at a time until the sorted ids pass hi.
-template <class Real>
+// 32 x kWSUnroll at a time until the sorted ids pass hi. Per pair the exact
+// X = fix(t1) - fix(e_v) - fix(e_u) goes in as balanced 16-bit digits: with
+// the row constant c = B - fix(e_u), B = sum_j 2^15 2^(16 j) (all 8 fields),
+// the digits of Y = fix(t1) - fix(e_v) + c are d_j + 2^15, so each digit is a
+// fixed 16-bit field of Y (no 128-bit shifts).
+template <class Real, int ND>
 __device__ __forceinline__ void wx_light_walk(const WSLightArgs& a, unsigned long long p, unsigned long long pe,
-                                              int32_t hi, int32_t sh, Real u, Real L, __int128 fu, int32_t* planes,
-                                              int T, int nd, int G, unsigned long long& pairs) {
+                                              int32_t hi, int32_t sh, Real u, Real L, unsigned long long c_lo,
+                                              unsigned long long c_hi, uint32_t planes_s, int T, int G,
+                                              unsigned long long& pairs) {
   const int lane = threadIdx.x & 31;
   const Real* __restrict__ lval = static_cast<const Real*>(a.lval);
   for (unsigned long long pb = p;; pb += 32 * kWSUnroll) {
@@ -346,17 +376,27 @@ __device__ __forceinline__ void wx_light_walk(const WSLightArgs& a, unsigned lon
         continue;
       }
       ++pairs;
-      const int q = id[j] + sh;
+      // shared-window address of the slot in digit plane 0
+      const uint32_t cell = planes_s + 4u * static_cast<uint32_t>(id[j] + sh);
       const Real t1 = (u > v[j] ? u - v[j] : v[j] - u) * L;
       const Real ev = v[j] * L;
-      __int128 x = static_cast<__int128>(wx_to_fix(static_cast<double>(t1), G)) -
-                   static_cast<__int128>(wx_to_fix(static_cast<double>(ev), G)) - fu;
+      unsigned long long tl, th, el, eh;
+      wx_fix2(static_cast<double>(t1), G, tl, th);
+      wx_fix2(static_cast<double>(ev), G, el, eh);
+      // Y = T - E + c (mod 2^128)
+      const unsigned long long s1 = tl + c_lo;
+      unsigned long long yh = th + c_hi + (s1 < tl ? 1ull : 0ull);
+      const unsigned long long yl = s1 - el;
+      yh = yh - eh - (s1 < el ? 1ull : 0ull);
+      const uint32_t w[4] = {static_cast<uint32_t>(yl), static_cast<uint32_t>(yl >> 32), static_cast<uint32_t>(yh),
+                             static_cast<uint32_t>(yh >> 32)};
+      // the ND planes' digits (those above are 0: |X| < 2^(16 ND - 1)); a
+      // zero digit is added too (cheaper than branching around it)
 #pragma unroll
-      for (int d = 0; d < 8; ++d) {
-        if (d >= nd) break;
-        const int32_t dg = static_cast<int16_t>(static_cast<uint16_t>(static_cast<unsigned __int128>(x)));
-        if (dg) atomicAdd(planes + d * T + q, dg);
-        x = (x - dg) >> 16;
+      for (int d = 0; d < ND; ++d) {
+        const int32_t dg = static_cast<int32_t>((w[d >> 1] >> (16 * (d & 1))) & 0xffffu) - 0x8000;
+        asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(cell + 4u * static_cast<uint32_t>(d * T)), "r"(dg)
+                     : "memory");
       }
     }
     if (!__all_sync(0xffffffffu, more)) break;
@@ -368,7 +408,7 @@ __device__ __forceinline__ void wx_light_walk(const WSLightArgs& a, unsigned lon
 // position in the row's list when the window starts right after k), exact
 // digit-plane accumulation; then each slot's exact light sum AL_k + AL_l +
 // sum, rounded once.
-template <class Real>
+template <class Real, int ND>
 __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLightArgs a) {
   extern __shared__ int32_t planes[];  // [nd][tile]
   const int k = blockIdx.x;
@@ -376,11 +416,9 @@ __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLi
   const int s_lo = a.s_begin + static_cast<int>(blockIdx.y) * a.tile;
   const int s_hi = min(a.s_end, s_lo + a.tile);
   const int T = a.tile;
-  const int nd = a.nd;
+  constexpr int nd = ND;
   const int G = a.G;
   const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
-  constexpr int NW = kWSLightThreads / 32;
   const Real* __restrict__ cval = static_cast<const Real*>(a.cval);
   const unsigned long long r0 = a.cptr[k], r1 = a.cptr[k + 1];
   // the window l = k + s + 1, s in [s_lo, s_hi): ids in (k + s_lo, k + s_hi]
@@ -393,25 +431,38 @@ __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLi
   const bool hasB = xb >= n;
   const int32_t shA = -k - 1 - s_lo, shB = n - k - 1 - s_lo;
   for (int i = threadIdx.x; i < nd * T; i += kWSLightThreads) planes[i] = 0;
+  const uint32_t planes_s = static_cast<uint32_t>(__cvta_generic_to_shared(planes));
   __syncthreads();
   unsigned long long pairs = 0;
+  __shared__ unsigned int next_row;  // rows are taken dynamically: lists differ in length
   for (unsigned long long f0 = r0; f0 < r1; f0 += kWSFold) {
     const unsigned long long f1 = min(r1, f0 + kWSFold);
-    for (unsigned long long e = f0 + warp; e < f1; e += NW) {
+    if (threadIdx.x == 0) next_row = 0u;
+    __syncthreads();
+    for (;;) {
+      unsigned int j = 0;
+      if (lane == 0) j = atomicAdd(&next_row, 1u);
+      const unsigned long long e = f0 + __shfl_sync(0xffffffffu, j, 0);
+      if (e >= f1) break;
       const int32_t r = __ldg(a.crow + e);
       const Real u = cval[e];
       const uint32_t rank = __ldg(a.crank + e);
       const Real L = static_cast<Real>(__ldg(a.lens + r));
-      const __int128 fu = static_cast<__int128>(wx_to_fix(static_cast<double>(L * u), G));
+      // c = B - fix(e_u), B = 0x8000 in every 16-bit field
+      unsigned long long fl_, fh_;
+      wx_fix2(static_cast<double>(L * u), G, fl_, fh_);
+      const unsigned long long b_lo = 0x8000800080008000ull, b_hi = 0x8000800080008000ull;
+      const unsigned long long c_lo = b_lo - fl_;
+      const unsigned long long c_hi = b_hi - fh_ - (b_lo < fl_ ? 1ull : 0ull);
       const unsigned long long m0 = __ldg(a.lptr + r), m1 = __ldg(a.lptr + r + 1);
       const unsigned long long me = m0 + rank;  // the column itself
       if (hasA) {
         const unsigned long long pa = s_lo == 0 ? me + 1 : wx_lower(a.lmid, me + 1, m1, static_cast<int32_t>(xa));
-        wx_light_walk<Real>(a, pa, m1, hiA, shA, u, L, fu, planes, T, nd, G, pairs);
+        wx_light_walk<Real, ND>(a, pa, m1, hiA, shA, u, L, c_lo, c_hi, planes_s, T, G, pairs);
       }
       if (hasB) {
         const unsigned long long pb = loB == 0 ? m0 : wx_lower(a.lmid, m0, me, loB);
-        wx_light_walk<Real>(a, pb, me, hiB, shB, u, L, fu, planes, T, nd, G, pairs);
+        wx_light_walk<Real, ND>(a, pb, me, hiB, shB, u, L, c_lo, c_hi, planes_s, T, G, pairs);
       }
     }
     if (f1 < r1) {  // carry-normalise the planes before the next rows
@@ -467,7 +518,10 @@ struct WSDenseArgs {
 };
 
 constexpr int kWSK = 128, kWSS = 128;  // tile: u columns x stripes
-constexpr int kWSR = 8;                // heavy rows per stage
+#ifndef SF_WS_R
+#define SF_WS_R 16
+#endif
+constexpr int kWSR = SF_WS_R;          // heavy rows per cp.async stage
 constexpr int kWSThreads = 256;        // 16 x 16 threads, 8 x 8 slots each (stride 16)
 
 __device__ __forceinline__ void wx_cp8(void* smem, const void* gmem) {

@@ -12,10 +12,14 @@ from paper_2005_05826_b200 import build  # noqa: E402
 
 VARIANTS = {
     # light column kernel: window stripes / member loads in flight / threads
-    "lw12800u8": dict(LIGHT_WIN=12800, LIGHT_UNROLL=8, LIGHT_NT=1024),
-    "lw6400u4": dict(LIGHT_WIN=6400, LIGHT_UNROLL=4, LIGHT_NT=1024),
-    "lw6400u8": dict(LIGHT_WIN=6400, LIGHT_UNROLL=8, LIGHT_NT=1024),
-    "lw4224u4n512": dict(LIGHT_WIN=4224, LIGHT_UNROLL=4, LIGHT_NT=512),
+    "lw12800u8": dict(SF_LIGHT_WIN=12800, SF_LIGHT_UNROLL=8, SF_LIGHT_NT=1024),
+    "lw6400u4": dict(SF_LIGHT_WIN=6400, SF_LIGHT_UNROLL=4, SF_LIGHT_NT=1024),
+    "lw6400u8": dict(SF_LIGHT_WIN=6400, SF_LIGHT_UNROLL=8, SF_LIGHT_NT=1024),
+    "lw4224u4n512": dict(SF_LIGHT_WIN=4224, SF_LIGHT_UNROLL=4, SF_LIGHT_NT=512),
+    # weighted split: dense rows per cp.async stage / light member loads in flight
+    "wsr16": dict(SF_WS_R=16),
+    "wsu2": dict(SF_WS_UNROLL=2),
+    "wsu8": dict(SF_WS_UNROLL=8),
     "v16u1f1": dict(V=16, UC=1, NW=8, MINB=2, FG=1),
     "v16u1f4": dict(V=16, UC=1, NW=8, MINB=2, FG=4),
     "v8u2f1": dict(V=8, UC=2, NW=8, MINB=2, FG=1),
@@ -37,7 +41,7 @@ VARIANTS = {
 
 
 def one(name, cfg):
-    defines = [f"-DSF_SPLIT_{k}={v}" for k, v in cfg.items()]
+    defines = [f"-D{k}={v}" if k.startswith("SF_") else f"-DSF_SPLIT_{k}={v}" for k, v in cfg.items()]
     out = ROOT / "tools" / "ab" / f"lib_{name}.so"
     build.build_native(force=True, out=out, defines=defines)
     return name
