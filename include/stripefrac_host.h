@@ -57,6 +57,40 @@ const double* sfh_instance_sample_totals(const sfh_instance* inst); /* [n] */
 /* FNV-1a 64 over raw bytes, chainable (common.cpp:50-57); the .strf checksum. */
 uint64_t sfh_fnv1a64(const void* data, uint64_t len, uint64_t h);
 
+/*
+ * write_tsv(path, dm) (stripes.cpp:311-340): the n x n row-major matrix as
+ * the reference's TSV — a header of the ids, then per row its id and the
+ * values with "%.<digits>g" (17 for fp64, 9 for fp32), tab-separated —
+ * byte for byte, formatted by `threads` host threads (0 = all) in row blocks
+ * written in order. Replaces the reference's single-threaded snprintf loop
+ * (C3: 6.25e8 values, a 12.5 GB file).
+ */
+sf_status sfh_write_tsv(const char* path, int32_t n, const char* const* ids, const double* values,
+                        int32_t digits, int32_t threads);
+
+/*
+ * load_table_file(path, TableFormat::TsvSparse) (table.cpp:105-168, 176-184):
+ * feature<TAB>sample<TAB>value triplets, an optional leading "#samples"
+ * header pinning the sample order (else first appearance), duplicates of a
+ * (feature, sample) summed in file order, features in byte order, samples
+ * ascending, zero sums dropped, totals summed in feature order — the same
+ * table bit for bit, and the same first error ("<path>: line N: ..."), parsed
+ * by `threads` host threads (0 = all) instead of one std::map insertion per
+ * triplet. The table is an opaque handle read through the accessors below.
+ */
+typedef struct sfh_table sfh_table;
+sf_status sfh_load_table_sparse(const char* path, int32_t threads, sfh_table** out);
+void sfh_table_free(sfh_table* t);
+int32_t sfh_table_n_samples(const sfh_table* t);
+int32_t sfh_table_n_features(const sfh_table* t);
+int64_t sfh_table_nnz(const sfh_table* t);
+const char* sfh_table_sample_id(const sfh_table* t, int32_t i);
+const char* sfh_table_feature_id(const sfh_table* t, int32_t i);
+const int64_t* sfh_table_feat_ptr(const sfh_table* t);
+const int32_t* sfh_table_sample_idx(const sfh_table* t);
+const double* sfh_table_counts(const sfh_table* t);
+const double* sfh_table_sample_totals(const sfh_table* t);
+
 #ifdef __cplusplus
 }
 #endif

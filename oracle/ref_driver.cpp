@@ -635,6 +635,70 @@ int cmd_dm_multi(std::uint64_t seed, int n, int leaves, double density, int subs
   return 0;
 }
 
+// The reference's own load_table_file on a table file, dumped as one JSON
+// object (ids, CSR with %.17g values, totals) or {"error": "..."} — the
+// checker of the native sparse loader (tests/test_abi.py).
+int cmd_table(const std::string& path, const std::string& fmt, bool timing_only) {
+  auto jstr = [](const std::string& x) {
+    std::string o = "\"";
+    for (const unsigned char c : x) {
+      if (c == '"' || c == '\\') {
+        o += '\\';
+        o += static_cast<char>(c);
+      } else if (c < 0x20) {
+        char b[8];
+        std::snprintf(b, sizeof(b), "\\u%04x", c);
+        o += b;
+      } else {
+        o += static_cast<char>(c);
+      }
+    }
+    return o + "\"";
+  };
+  try {
+    const auto t0 = std::chrono::steady_clock::now();
+    const SampleTable t = load_table_file(path, table_format_from_name(fmt));
+    if (timing_only) {
+      std::printf("{\"seconds\":%.3f,\"features\":%zu,\"samples\":%zu}\n",
+                  std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(), t.feature_ids.size(),
+                  t.sample_ids.size());
+      return 0;
+    }
+    std::string o = "{\"samples\":[";
+    for (size_t i = 0; i < t.sample_ids.size(); ++i) o += (i ? "," : "") + jstr(t.sample_ids[i]);
+    o += "],\"features\":[";
+    for (size_t i = 0; i < t.feature_ids.size(); ++i) o += (i ? "," : "") + jstr(t.feature_ids[i]);
+    o += "],\"feat_ptr\":[0";
+    size_t nnz = 0;
+    for (const auto& row : t.entries) o += "," + std::to_string(nnz += row.size());
+    o += "],\"sample_idx\":[";
+    bool first = true;
+    for (const auto& row : t.entries)
+      for (const auto& e : row) {
+        o += (first ? "" : ",") + std::to_string(e.first);
+        first = false;
+      }
+    char b[40];
+    o += "],\"counts\":[";
+    first = true;
+    for (const auto& row : t.entries)
+      for (const auto& e : row) {
+        std::snprintf(b, sizeof(b), "%.17g", e.second);
+        o += (first ? "" : ",") + std::string(b);
+        first = false;
+      }
+    o += "],\"totals\":[";
+    for (size_t i = 0; i < t.sample_totals.size(); ++i) {
+      std::snprintf(b, sizeof(b), "%.17g", t.sample_totals[i]);
+      o += (i ? "," : "") + std::string(b);
+    }
+    std::printf("%s]}\n", o.c_str());
+  } catch (const std::exception& e) {
+    std::printf("{\"error\":%s}\n", jstr(e.what()).c_str());
+  }
+  return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -648,6 +712,7 @@ int main(int argc, char** argv) {
       return cmd_dm_multi(std::strtoull(argv[2], nullptr, 10), std::atoi(argv[3]), std::atoi(argv[4]),
                           std::atof(argv[5]), std::atoi(argv[6]), std::atoi(argv[7]), argv[8], argc - 9, argv + 9);
     if (cmd == "strf_golden" && argc >= 4) return cmd_strf_golden(argv[2], argv[3]);
+    if (cmd == "table" && argc >= 4) return cmd_table(argv[2], argv[3], argc >= 5 && std::string(argv[4]) == "time");
     if (cmd == "instance" && argc >= 7)
       return cmd_instance(std::strtoull(argv[2], nullptr, 10), std::atoi(argv[3]), std::atoi(argv[4]),
                           std::atof(argv[5]), std::atoi(argv[6]));

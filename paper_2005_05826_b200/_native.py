@@ -106,6 +106,18 @@ SIGNATURES = {
     "sf_mantel_permutation": (C.c_int, [C.c_int32, C.c_uint64, C.c_int32, _P]),
     "sfh_flatten": (C.c_int, [C.c_int32, _P, _P, C.c_int32, _P, C.POINTER(C.c_int32), _P, _P, _P]),
     "sfh_fnv1a64": (C.c_uint64, [_P, C.c_uint64, C.c_uint64]),
+    "sfh_write_tsv": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(C.c_char_p), _P, C.c_int32, C.c_int32]),
+    "sfh_load_table_sparse": (C.c_int, [C.c_char_p, C.c_int32, C.POINTER(_P)]),
+    "sfh_table_free": (None, [_P]),
+    "sfh_table_n_samples": (C.c_int32, [_P]),
+    "sfh_table_n_features": (C.c_int32, [_P]),
+    "sfh_table_nnz": (C.c_int64, [_P]),
+    "sfh_table_sample_id": (C.c_char_p, [_P, C.c_int32]),
+    "sfh_table_feature_id": (C.c_char_p, [_P, C.c_int32]),
+    "sfh_table_feat_ptr": (C.POINTER(C.c_int64), [_P]),
+    "sfh_table_sample_idx": (C.POINTER(C.c_int32), [_P]),
+    "sfh_table_counts": (C.POINTER(C.c_double), [_P]),
+    "sfh_table_sample_totals": (C.POINTER(C.c_double), [_P]),
     "sfh_random_instance": (_P, [C.c_uint64, C.c_int32, C.c_int32, C.c_double, C.c_int32]),
     "sfh_instance_free": (None, [_P]),
     "sfh_instance_n_nodes": (C.c_int32, [_P]),

@@ -589,7 +589,32 @@ def load_table(stream, fmt: str = "tsv-dense") -> SampleTable:
     raise Error(f"unknown table format '{fmt}'")
 
 
-def load_table_file(path: str, fmt: str = "tsv-dense") -> SampleTable:
+def _load_sparse_native(path: str, threads: int = 0) -> SampleTable:
+    """load_table_file(path, TsvSparse) through the native parallel loader
+    (sfh_load_table_sparse): the same table bit for bit, the same errors."""
+    L = N.lib()
+    h = C.c_void_p()
+    st = L.sfh_load_table_sparse(str(path).encode(), int(threads), C.byref(h))
+    if st != 0:
+        raise Error(L.sf_last_error().decode("utf-8", "replace"))
+    try:
+        ns, nf, nnz = L.sfh_table_n_samples(h), L.sfh_table_n_features(h), L.sfh_table_nnz(h)
+        samples = [L.sfh_table_sample_id(h, i).decode() for i in range(ns)]
+        feats = [L.sfh_table_feature_id(h, i).decode() for i in range(nf)]
+        ptr = np.ctypeslib.as_array(L.sfh_table_feat_ptr(h), shape=(nf + 1,)).copy()
+        sidx = np.ctypeslib.as_array(L.sfh_table_sample_idx(h), shape=(max(nnz, 1),))[:nnz].copy()
+        cnt = np.ctypeslib.as_array(L.sfh_table_counts(h), shape=(max(nnz, 1),))[:nnz].copy()
+        tot = np.ctypeslib.as_array(L.sfh_table_sample_totals(h), shape=(ns,)).copy()
+    finally:
+        L.sfh_table_free(h)
+    return SampleTable(samples, feats, ptr, sidx, cnt, tot)
+
+
+def load_table_file(path: str, fmt: str = "tsv-dense", threads: int = 0) -> SampleTable:
+    """load_table_file (table.cpp:176-184); 'tsv-sparse' files go through the
+    native parallel loader."""
+    if fmt == "tsv-sparse":
+        return _load_sparse_native(path, threads)
     try:
         with open(path, "r", encoding="utf-8", newline="") as fh:
             text = fh.read()
@@ -1159,12 +1184,17 @@ def to_tsv(dm: DistanceMatrix) -> str:
     return "".join(out)
 
 
-def write_tsv(path: str, dm: DistanceMatrix) -> None:
-    try:
-        with open(path, "w", encoding="utf-8", newline="") as fh:
-            fh.write(to_tsv(dm))
-    except OSError:
-        raise Error(f"cannot open '{path}' for writing") from None
+def write_tsv(path: str, dm: DistanceMatrix, threads: int = 0) -> None:
+    """write_tsv (stripes.cpp:334-340) through the native parallel writer
+    (sfh_write_tsv): the same bytes as to_tsv, formatted by `threads` host
+    threads (0 = all)."""
+    n = dm.n()
+    if len(dm.sample_ids) != n:
+        raise Error(f"distance matrix has {len(dm.sample_ids)} ids for {n} samples")
+    digits = 9 if dm.precision == Precision.Fp32 else 17
+    ids = (C.c_char_p * max(n, 1))(*[s.encode() for s in dm.sample_ids])
+    vals = np.ascontiguousarray(dm.values, dtype=np.float64)
+    _call(N.lib().sfh_write_tsv(str(path).encode(), n, ids, N.ptr(vals), digits, int(threads)))
 
 
 def read_tsv_file(path: str) -> DistanceMatrix:

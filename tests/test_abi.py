@@ -168,3 +168,127 @@ def test_counter_law_is_host_side():
     cfg = sf.KernelConfig(sf.Metric.WeightedNormalized, sf.Variant.Naive, batch_capacity=4)
     c = sf._counters_for(cfg, 10, 50, 3)
     assert (c.accumulator_writes, c.embedding_reads, c.kernel_passes) == (500, 1000, 3)
+
+
+def test_native_tsv_writer_is_the_reference_bytes(tmp_path):
+    """sfh_write_tsv (parallel host writer) writes the reference's own TSV
+    bytes (goldens written by write_tsv, stripes.cpp:311-340) for every demo
+    matrix, with any thread count, and agrees with the Python to_tsv on
+    random and edge values (0, 1, tiny, huge, fp32 digits)."""
+    import sys
+    sys.path.insert(0, str(Path(__file__).resolve().parent))
+    import golden_util as gu
+    case = gu.load("demo.json")
+    tree, table = gu.case_inputs(case)
+    for entry in case["dm"]:
+        n = table.n_samples()
+        dm = sf.DistanceMatrix(list(table.sample_ids), np.array(entry["values"]).reshape(n, n),
+                               sf.precision_from_name(entry["precision"]))
+        for threads in (1, 3, 0):
+            path = tmp_path / f"dm{threads}.tsv"
+            sf.write_tsv(str(path), dm, threads=threads)
+            assert path.read_bytes() == entry["tsv"].encode()
+    rng = np.random.default_rng(3)
+    n = 77
+    vals = rng.random((n, n)) ** 7
+    vals[0, :5] = [0.0, 1.0, 5e-324, 1.7976931348623157e308, 0.1]
+    for prec in (sf.Precision.Fp64, sf.Precision.Fp32):
+        dm = sf.DistanceMatrix([f"s{i}" for i in range(n)], vals, prec)
+        path = tmp_path / "r.tsv"
+        sf.write_tsv(str(path), dm, threads=5)
+        assert path.read_text() == sf.to_tsv(dm)
+    with pytest.raises(sf.Error):
+        sf.write_tsv(str(tmp_path / "no" / "such" / "dir.tsv"), dm)
+
+
+def _sparse_cases():
+    rng = np.random.default_rng(11)
+    cases = {}
+    # random triplets, unordered, duplicates, some zero values, CRLF, blank lines
+    lines = []
+    for _ in range(4000):
+        f = f"feat{rng.integers(0, 300)}"
+        s = f"s{rng.integers(0, 40)}"
+        v = float(rng.choice([0.0, 1.0, 2.5, 1e-3, 7.0, 0.1]))
+        lines.append(f"{f}\t{s}\t{v!r}")
+    for i in range(0, len(lines), 97):
+        lines.insert(i, "")
+    cases["unpinned"] = "\n".join(lines) + "\n"
+    cases["crlf"] = "\r\n".join(lines)
+    cases["pinned"] = "#samples\t" + "\t".join(f"s{i}" for i in range(40)) + "\n" + "\n".join(lines)
+    cases["blank_then_header"] = "\n\n#samples\ts1\ts2\nB\ts2\t1\nA\ts1\t2\nB\ts2\t1\n"
+    cases["unicode_and_bytes"] = "ét\ts1\t1\nZ\ts1\t1\n_a\ts2\t3\n"
+    return cases
+
+
+@pytest.mark.parametrize("name", list(_sparse_cases()))
+def test_native_sparse_loader_matches_the_reference_restatement(tmp_path, name):
+    """sfh_load_table_sparse (parallel native loader) vs the Python statement
+    of load_sparse (table.cpp:105-168): identical ids, CSR and totals, bit for
+    bit, with any thread count."""
+    text = _sparse_cases()[name]
+    path = tmp_path / "t.tsv"
+    path.write_bytes(text.encode())
+    want = sf.load_table(text, "tsv-sparse")
+    for threads in (1, 4, 0):
+        got = sf.load_table_file(str(path), "tsv-sparse", threads=threads)
+        assert got.sample_ids == want.sample_ids and got.feature_ids == want.feature_ids
+        assert np.array_equal(got.feat_ptr, want.feat_ptr)
+        assert np.array_equal(got.sample_idx, want.sample_idx)
+        assert np.array_equal(got.counts, want.counts)
+        assert np.array_equal(got.sample_totals, want.sample_totals)
+
+
+@pytest.mark.parametrize("text,msg", [
+    ("A\ts1\n", "line 1: expected feature<TAB>sample<TAB>value"),
+    ("A\ts1\t1\n\t\ts2\n", "line 2: feature id is empty"),
+    ("A\ts1\t1\nB\ts1\t1\t2\n", "line 2: expected feature<TAB>sample<TAB>value"),
+    ("A\ts1\t1\n\ts1\t1\n", "line 2: feature id is empty"),
+    ("A\ts1\t1\nB\t\t1\n", "line 2: sample id is empty"),
+    ("A\ts1\t1x\n", "line 1: bad count '1x'"),
+    ("A\ts1\tinf\n", "line 1: count must be finite"),
+    ("A\ts1\t-1\n", "line 1: count must be non-negative"),
+    ("#samples\ts1\nA\ts2\t1\n", "line 2: sample 's2' not in the #samples header"),
+    ("#samples\n", "#samples header names no samples"),
+    ("#samples\ts1\ts1\n", "duplicate sample id 's1'"),
+    ("", "sparse table names no samples"),
+    ("#samples\ts1\ts2\nA\ts1\t1\n", "sample 's2' has no counts"),
+    ("A\ts1\t0\n", "sample 's1' has no counts"),
+])
+def test_native_sparse_loader_errors(tmp_path, text, msg):
+    """The reference's first error, prefixed by the path (table.cpp:180-183)."""
+    path = tmp_path / "bad.tsv"
+    path.write_bytes(text.encode())
+    with pytest.raises(sf.Error) as e:
+        sf.load_table_file(str(path), "tsv-sparse")
+    assert str(e.value) == f"{path}: {msg}"
+    with pytest.raises(sf.Error):
+        sf.load_table(text, "tsv-sparse")
+
+
+REF_DRIVER = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "ref_driver"
+
+
+@pytest.mark.skipif(not REF_DRIVER.exists(), reason="reference not built (oracle/_ref)")
+@pytest.mark.parametrize("name", list(_sparse_cases()) + ["err_fields", "err_pinned", "err_nocounts"])
+def test_native_sparse_loader_is_the_reference_loader(tmp_path, name):
+    """Against the reference's own load_table_file (oracle/_ref/ref_driver
+    table, compiled from /root/reference): same ids, CSR, counts and totals
+    (printed %.17g: exact), or the same error message."""
+    import json
+    import subprocess
+    text = {**_sparse_cases(), "err_fields": "A\ts1\t1\nB\ts1\n", "err_pinned": "#samples\ts1\nA\ts9\t1\n",
+            "err_nocounts": "#samples\ts1\ts2\nA\ts1\t1\n"}[name]
+    path = tmp_path / "t.tsv"
+    path.write_bytes(text.encode())
+    ref = json.loads(subprocess.run([str(REF_DRIVER), "table", str(path), "tsv-sparse"], capture_output=True,
+                                    text=True, check=True).stdout)
+    if "error" in ref:
+        with pytest.raises(sf.Error) as e:
+            sf.load_table_file(str(path), "tsv-sparse")
+        assert str(e.value) == ref["error"]
+        return
+    got = sf.load_table_file(str(path), "tsv-sparse", threads=3)
+    assert got.sample_ids == ref["samples"] and got.feature_ids == ref["features"]
+    assert got.feat_ptr.tolist() == ref["feat_ptr"] and got.sample_idx.tolist() == ref["sample_idx"]
+    assert got.counts.tolist() == ref["counts"] and got.sample_totals.tolist() == ref["totals"]
