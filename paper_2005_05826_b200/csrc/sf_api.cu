@@ -391,6 +391,10 @@ Schedule build_schedule(const sf_problem* p, int32_t cmax) {
     Chunk c;
     c.r0 = r0;
     c.r1 = std::min(E, r0 + cmax);
+    c.leaf_rows.reserve(static_cast<size_t>(c.r1 - c.r0));
+    c.leaf_feat.reserve(static_cast<size_t>(c.r1 - c.r0));
+    c.codes.reserve(static_cast<size_t>(c.r1 - c.r0));
+    c.cptr.reserve(static_cast<size_t>(c.r1 - c.r0) / 2 + 2);
     int32_t hmax = 0;
     for (int r = c.r0; r < c.r1; ++r) {
       if (p->leaf_feature[r] >= 0) {
@@ -549,7 +553,7 @@ struct DeviceState {
   DevBuf fix, keys, vals, keys_out, perm, dense, sorttmp, nheavy;
   // light-row sums per slot, |S_e| per row; u-walk nonzero-word masks
   DevBuf lightsum, mcount, nzmask;
-  DevBuf lcnt, lptr, lmem, lcur, lscantmp;  // banded light scatter: member CSR + cursors of the light rows
+  DevBuf lcnt, lptr, lmem, lcur, lscantmp, lmem16;  // banded light scatter: member CSR + cursors of the light rows
   size_t lscan_bytes = 0;
   bool banded = false;
   // column-owned light scatter: entries (light rows containing each column)
@@ -869,15 +873,21 @@ bool light_banded() {
 #endif
 // Column-owned light scatter of stripes [p0, p1) for columns [k0, k1).
 sf_status light_columns_run(sf_plan* plan, DeviceState& d, cudaStream_t st, int p0, int p1, int k0, int k1) {
-  constexpr int NT = SF_LIGHT_NT;  // the kernel is bound by member-load latency: many warps
-  auto* kern = sp_light_column_kernel<NT>;
+  constexpr int NT = SF_LIGHT_NT;  // the kernel is bound by member-list reads: many warps
   const int smem = 2 * kLightWin * 8;
-  SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<std::max(1, std::min(k1 - k0, 65535)), NT, smem, st>>>(
-      d.cptr.as<uint32_t>(), d.cent.as<uint2>(), d.linfo.as<LightRowInfo>(), d.lmem.as<int32_t>(), plan->lo_bits,
-      plan->n, k0, k1, p0, p0, p1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>(),
-      // test hook: SF_LIGHT_LIMB_MODE=1|2 forces the wider exact limb modes
-      std::getenv("SF_LIGHT_LIMB_MODE") ? std::atoi(std::getenv("SF_LIGHT_LIMB_MODE")) : 0);
+  // test hook: SF_LIGHT_LIMB_MODE=1|2 forces the wider exact limb modes
+  const int min_mode = std::getenv("SF_LIGHT_LIMB_MODE") ? std::atoi(std::getenv("SF_LIGHT_LIMB_MODE")) : 0;
+  auto launch = [&](auto* kern, const auto* mem) -> sf_status {
+    SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<std::max(1, std::min(k1 - k0, 65535)), NT, smem, st>>>(
+        d.cptr.as<uint32_t>(), d.cent.as<uint2>(), d.linfo.as<LightRowInfo>(), mem, plan->lo_bits, plan->n, k0, k1,
+        p0, p0, p1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>(), min_mode);
+    return SF_OK;
+  };
+  if (d.lmem16.p)
+    SF_TRY(launch(sp_light_column_kernel<NT, uint16_t>, d.lmem16.as<uint16_t>()));
+  else
+    SF_TRY(launch(sp_light_column_kernel<NT, int32_t>, d.lmem.as<int32_t>()));
   SF_CUDA(cudaGetLastError());
   d.launches++;
   return SF_OK;
@@ -916,11 +926,24 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
       size_t tmp = d.cscan_bytes;
       SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cscantmp.p, tmp, d.ccnt.as<uint32_t>(), d.cptr.as<uint32_t>(), n + 1,
                                             st));
-      uint32_t M = 0;
+      uint32_t M = 0, members = 0;
       SF_CUDA(cudaMemcpyAsync(&M, d.cptr.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, st));
+      SF_CUDA(cudaMemcpyAsync(&members, d.lptr.as<uint32_t>() + E, 4, cudaMemcpyDeviceToHost, st));
       SF_CUDA(cudaMemcpyAsync(d.ccnt.p, d.cptr.p, static_cast<size_t>(n) * 4, cudaMemcpyDeviceToDevice, st));
       SF_CUDA(cudaStreamSynchronize(st));
       if (d.cent.bytes < static_cast<size_t>(M) * 8 + 8) SF_TRY(d.cent.alloc(d.dev, static_cast<size_t>(M) * 8 + 8, "column entries"));
+      // 16-bit member lists for the column kernel (n <= 65536; SF_LIGHT_MEM16=0: 32-bit)
+      const char* m16 = std::getenv("SF_LIGHT_MEM16");
+      if (n <= 65536 && !(m16 && std::atoi(m16) == 0)) {
+        if (d.lmem16.bytes < static_cast<size_t>(members) * 2 + 2)
+          SF_TRY(d.lmem16.alloc(d.dev, static_cast<size_t>(members) * 2 + 2, "16-bit light members"));
+        sp_narrow_members_kernel<<<grid_for(members, 256), 256, 0, st>>>(d.lmem.as<int32_t>(),
+                                                                          d.lptr.as<uint32_t>() + E,
+                                                                          d.lmem16.as<uint16_t>());
+        d.launches++;
+      } else {
+        d.lmem16.reset();
+      }
       sp_col_fill_kernel<<<wblocks, 256, 0, st>>>(d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E,
                                                   d.nheavy.as<unsigned int>(), d.ccnt.as<uint32_t>(),
                                                   d.cent.as<uint2>());

@@ -423,10 +423,11 @@ __global__ void sp_light_members_kernel(const uint32_t* __restrict__ rows, int64
 }
 
 // First index j in [lo, hi) with mem[j] >= key (mem ascending).
-__device__ __forceinline__ int lower_bound_i32(const int32_t* __restrict__ mem, int lo, int hi, int key) {
+template <class M>
+__device__ __forceinline__ int lower_bound_i32(const M* __restrict__ mem, int lo, int hi, int key) {
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (mem[mid] < key)
+    if (static_cast<int>(mem[mid]) < key)
       lo = mid + 1;
     else
       hi = mid;
@@ -519,6 +520,14 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
 #endif
 constexpr int kLightWin = SF_LIGHT_WIN;        // stripes per shared-memory window (16 B each)
 constexpr int kLightUnroll = SF_LIGHT_UNROLL;  // member loads in flight per lane
+
+// 16-bit copy of the light member lists (n <= 65536) for the column kernel.
+__global__ void sp_narrow_members_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ total,
+                                         uint16_t* __restrict__ lmem16) {
+  const uint32_t m = *total;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    lmem16[i] = static_cast<uint16_t>(lmem[i]);
+}
 
 // Entries per column: one count per light member (rows with >= 2 members).
 __global__ void sp_col_count_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ lptr,
@@ -617,10 +626,10 @@ __global__ void sp_light_rowinfo_kernel(const int32_t* __restrict__ perm, int32_
 // One warp per entry (light row holding the column): the lanes walk the
 // row's sorted members 32 at a time from the entry's own position. The next
 // entry's record is loaded while the current one is walked.
-template <int MODE>
+template <int MODE, class M>
 __device__ __forceinline__ void light_column_window(const uint32_t e0, const uint32_t e1, const uint2* __restrict__ cent,
                                                     const LightRowInfo* __restrict__ info,
-                                                    const int32_t* __restrict__ lmem, int32_t lo_bits, int k, int n,
+                                                    const M* __restrict__ lmem, int32_t lo_bits, int k, int n,
                                                     int w0, int w1, uint32_t* __restrict__ acc,
                                                     unsigned long long& pairs) {
   const int lane = threadIdx.x & 31;
@@ -637,7 +646,7 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
     if (en_next < e1) nen = cent[en_next];
     const int x = static_cast<int>(ri.x);
     const int i = static_cast<int>(en.y);
-    const int32_t* mem = lmem + ri.b0;
+    const M* mem = lmem + ri.b0;
     const unsigned long long v = ri.v;
     const ulonglong2 L = ilimbs_of(v, lo_bits);
     // partners above: slot (b - k - 1, k), b in [k + w0 + 1, k + w1]; the
@@ -649,7 +658,7 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
 #pragma unroll
       for (int u = 0; u < kLightUnroll; ++u) {
         const int j = jb + lane + 32 * u;
-        s[u] = j < x ? __ldg(mem + j) - k - 1 : w1;
+        s[u] = j < x ? static_cast<int>(__ldg(mem + j)) - k - 1 : w1;
       }
       bool all_live = true;
 #pragma unroll
@@ -670,7 +679,7 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
 #pragma unroll
       for (int u = 0; u < kLightUnroll; ++u) {
         const int j = jb + lane + 32 * u;
-        s[u] = j < i ? n - (k - __ldg(mem + j)) - 1 : w1;
+        s[u] = j < i ? n - (k - static_cast<int>(__ldg(mem + j))) - 1 : w1;
       }
       bool all_live = true;
 #pragma unroll
@@ -691,10 +700,12 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
 
 // One CTA per column k: stripes [s0, s1) of the light sums (rows relative to
 // the pass start p0), in windows of kLightWin stripes.
-template <int NT>
+// M: the member type, uint16_t when n <= 65536 (half the bytes of the
+// member lists each column re-reads: the kernel is bound by those reads).
+template <int NT, class M>
 __global__ void __launch_bounds__(NT) sp_light_column_kernel(
     const uint32_t* __restrict__ cptr, const uint2* __restrict__ cent, const LightRowInfo* __restrict__ info,
-    const int32_t* __restrict__ lmem, int32_t lo_bits, int32_t n, int32_t k_begin, int32_t k_end, int32_t p0,
+    const M* __restrict__ lmem, int32_t lo_bits, int32_t n, int32_t k_begin, int32_t k_end, int32_t p0,
     int32_t s0, int32_t s1, unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
     int32_t min_mode) {
   extern __shared__ uint32_t lacc[];  // 4 planes of kLightWin u32 cells (or 2 of u64)
@@ -711,11 +722,11 @@ __global__ void __launch_bounds__(NT) sp_light_column_kernel(
       for (int t = threadIdx.x; t < 4 * kLightWin; t += NT) lacc[t] = 0u;
       __syncthreads();
       if (mode == 0)
-        light_column_window<0>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+        light_column_window<0, M>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
       else if (mode == 1)
-        light_column_window<1>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+        light_column_window<1, M>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
       else
-        light_column_window<2>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+        light_column_window<2, M>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
       __syncthreads();
       for (int t = threadIdx.x; t < ww; t += NT) {
         const ulonglong2 out = mode == 0 ? window_cell<0>(lacc, t, lo_bits)

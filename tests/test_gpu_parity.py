@@ -918,3 +918,16 @@ def test_plan_write_strf_over_several_devices(device_ok, tmp_path):
         N.lib().sf_plan_destroy(plan)
         paths.append(p.read_bytes())
     assert paths[0] == paths[1]
+
+
+def test_light_column_16bit_members_are_bitwise_the_32bit(device_ok, monkeypatch):
+    """The column kernel reads 16-bit member lists when n <= 65536: the same
+    exact light sums as the 32-bit lists (SF_LIGHT_MEM16=0), bit for bit."""
+    inst = sf.random_instance(141, 900, 5000, 0.01)
+    problem = sf.flatten(inst.tree, inst.table)
+    for prec in (8, 4):
+        want = _gpu_stripes(problem, 1, prec, 0, 450, N.KERNEL_SPLIT)
+        monkeypatch.setenv("SF_LIGHT_MEM16", "0")
+        got = _gpu_stripes(problem, 1, prec, 0, 450, N.KERNEL_SPLIT)
+        monkeypatch.delenv("SF_LIGHT_MEM16")
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
