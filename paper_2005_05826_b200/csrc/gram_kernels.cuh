@@ -165,7 +165,17 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
     if (l >= n) l -= n;
     const int32_t* cp = a.C + static_cast<int64_t>(kk + ds) * a.M + static_cast<int64_t>(kk) * a.nd;
     __int128 G = 0;
-    for (int jj = 0; jj < a.nd; ++jj) G += static_cast<__int128>(cp[jj]) * (static_cast<__int128>(1) << (8 * a.dj[jj]));
+    if (a.nd == 8 && a.dj[0] == 0 && a.dj[7] == 7) {
+      // planes 0..7: the slot's 32 bytes as two 16-byte loads, combined
+      // Horner-style from the top digit (no per-plane 128-bit shifts)
+      const int4 lo = __ldg(reinterpret_cast<const int4*>(cp));
+      const int4 hi = __ldg(reinterpret_cast<const int4*>(cp) + 1);
+      const int32_t c8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
+#pragma unroll
+      for (int jj = 7; jj >= 0; --jj) G = G * 256 + static_cast<__int128>(c8[jj]);
+    } else {
+      for (int jj = 0; jj < a.nd; ++jj) G += static_cast<__int128>(cp[jj]) * (static_cast<__int128>(1) << (8 * a.dj[jj]));
+    }
     const int64_t cell = static_cast<int64_t>(s - a.gl_begin) * n + k;
     const ulonglong2 light = reinterpret_cast<const ulonglong2*>(a.gl)[cell];
     G += (static_cast<__int128>(light.x) << a.lo_bits) + static_cast<__int128>(light.y);
