@@ -4,6 +4,13 @@
 
 #include <cstdint>
 
+// Streaming (evict-first) loads/stores for the write-once / read-once slot
+// arrays (light sums, final stripes), so they do not evict reused operands
+// from L2. -DSF_LIGHT_STREAM=0 builds the plain-access A/B library.
+#ifndef SF_LIGHT_STREAM
+#define SF_LIGHT_STREAM 1
+#endif
+
 namespace sf {
 
 // bfind: position of the most significant set bit (x != 0).

@@ -177,7 +177,13 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
       for (int jj = 0; jj < a.nd; ++jj) G += static_cast<__int128>(cp[jj]) * (static_cast<__int128>(1) << (8 * a.dj[jj]));
     }
     const int64_t cell = static_cast<int64_t>(s - a.gl_begin) * n + k;
+#if SF_LIGHT_STREAM
+    const longlong2 lraw = __ldcs(reinterpret_cast<const longlong2*>(a.gl) + cell);  // read once
+    const ulonglong2 light = make_ulonglong2(static_cast<unsigned long long>(lraw.x),
+                                             static_cast<unsigned long long>(lraw.y));
+#else
     const ulonglong2 light = reinterpret_cast<const ulonglong2*>(a.gl)[cell];
+#endif
     G += (static_cast<__int128>(light.x) << a.lo_bits) + static_cast<__int128>(light.y);
     if (a.levels > 2) {  // sp_deep_epilogue_kernel finishes the slot from (hi, lo)
       reinterpret_cast<longlong2*>(a.gl)[cell] =
@@ -208,8 +214,13 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
     }
     if (a.finalize) dv = tv == Real(0) ? Real(0) : dv / tv;
     const int64_t off = static_cast<int64_t>(s - a.out_begin) * n + k;
+#if SF_LIGHT_STREAM
+    __stcs(dist + off, dv);  // final stripes: leave L2 to the GEMM operands
+    __stcs(tot + off, tv);
+#else
     dist[off] = dv;
     tot[off] = tv;
+#endif
   }
 }
 

@@ -519,6 +519,14 @@ __global__ void __launch_bounds__(32 * NW) sp_light_band_kernel(
 #define SF_LIGHT_UNROLL 4
 #endif
 constexpr int kLightWin = SF_LIGHT_WIN;        // stripes per shared-memory window (16 B each)
+// a column entry is read once per window: streaming (evict-first) load
+__device__ __forceinline__ uint2 ld_entry(const uint2* p) {
+#if SF_LIGHT_STREAM
+  return __ldcs(p);
+#else
+  return *p;
+#endif
+}
 constexpr int kLightUnroll = SF_LIGHT_UNROLL;  // member loads in flight per lane
 
 // 16-bit copy of the light member lists (n <= 65536) for the column kernel.
@@ -636,14 +644,14 @@ __device__ __forceinline__ void light_column_window(const uint32_t e0, const uin
   const int wid = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
   uint32_t e = e0 + wid;
-  uint2 en = e < e1 ? cent[e] : make_uint2(0u, 0u);
+  uint2 en = e < e1 ? ld_entry(cent + e) : make_uint2(0u, 0u);
   LightRowInfo ri{0u, 0u, 0ull};
   if (e < e1) ri = info[en.x];
   for (; e < e1; e += nw) {
     // prefetch the next entry of this warp
     const uint32_t en_next = e + nw;
     uint2 nen = make_uint2(0u, 0u);
-    if (en_next < e1) nen = cent[en_next];
+    if (en_next < e1) nen = ld_entry(cent + en_next);
     const int x = static_cast<int>(ri.x);
     const int i = static_cast<int>(en.y);
     const M* mem = lmem + ri.b0;
@@ -731,7 +739,15 @@ __global__ void __launch_bounds__(NT) sp_light_column_kernel(
       for (int t = threadIdx.x; t < ww; t += NT) {
         const ulonglong2 out = mode == 0 ? window_cell<0>(lacc, t, lo_bits)
                                          : mode == 1 ? window_cell<1>(lacc, t, lo_bits) : window_cell<2>(lacc, t, lo_bits);
-        reinterpret_cast<ulonglong2*>(gl)[static_cast<int64_t>(w0 + t - p0) * n + k] = out;
+        ulonglong2* cell = reinterpret_cast<ulonglong2*>(gl) + static_cast<int64_t>(w0 + t - p0) * n + k;
+#if SF_LIGHT_STREAM
+        // written once, read once by the epilogue much later: streaming
+        // stores keep the 5 GB of light sums from evicting the member lists
+        __stcs(reinterpret_cast<longlong2*>(cell), make_longlong2(static_cast<long long>(out.x),
+                                                                   static_cast<long long>(out.y)));
+#else
+        *cell = out;
+#endif
       }
       __syncthreads();
     }

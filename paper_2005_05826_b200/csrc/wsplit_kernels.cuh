@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLi
     const unsigned __int128 ALl =
         (static_cast<unsigned __int128>(a.AL[2 * l + 1]) << 64) | static_cast<unsigned __int128>(a.AL[2 * l]);
     const unsigned __int128 tot = ALk + ALl + static_cast<unsigned __int128>(v);  // >= 0: the exact light sum
-    a.lightd[static_cast<int64_t>(s - a.out_begin) * n + k] = u128_to_real<double>(tot, false, -G);
+    __stcs(a.lightd + static_cast<int64_t>(s - a.out_begin) * n + k, u128_to_real<double>(tot, false, -G));
   }
   if (a.pairs) {
     for (int o = 16; o; o >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, o);
@@ -614,9 +614,9 @@ __global__ void __launch_bounds__(kWSThreads, 1) wx_dense_kernel(const WSDenseAr
       const int k = k0 + tk + 16 * i;
       if (k >= n) break;
       const int64_t o = static_cast<int64_t>(s - a.out_begin) * n + k;
-      const double dv = static_cast<double>(acc[i][j]) + a.lightd[o];
+      const double dv = static_cast<double>(acc[i][j]) + __ldcs(a.lightd + o);  // read once
       if (M == kWU) {
-        dist[o] = static_cast<Real>(dv);
+        __stcs(dist + o, static_cast<Real>(dv));
         continue;
       }
       const int64_t li = static_cast<int64_t>(k) + s + 1;
@@ -633,8 +633,8 @@ __global__ void __launch_bounds__(kWSThreads, 1) wx_dense_kernel(const WSDenseAr
       const Real tr = static_cast<Real>(tv);
       Real dr = static_cast<Real>(dv);
       if (a.finalize) dr = tr == Real(0) ? Real(0) : dr / tr;
-      dist[o] = dr;
-      tot[o] = tr;
+      __stcs(dist + o, dr);  // final stripes: keep L2 for the staged heavy rows
+      __stcs(tot + o, tr);
     }
   }
 }
