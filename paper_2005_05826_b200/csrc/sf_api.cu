@@ -1569,8 +1569,8 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
                                                               d.lens_pad.as<double>(), E, d.ws_LH.as<Real>());
   wx_fill_kernel<Real><<<std::min<int64_t>((W + 7) / 8, 148 * 64), 256, 0, st>>>(
       nb, off, pool, n_ext, n, W, d.ws_hmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>(), d.ws_hidx.as<uint32_t>(),
-      d.ws_lptr.as<unsigned long long>(), ldh, d.ws_UH.as<Real>(), d.ws_lmid.as<int32_t>(), d.ws_lval.as<Real>(),
-      d.ws_prank.as<uint32_t>());
+      d.ws_lptr.as<unsigned long long>(), ldh, d.lens_pad.as<double>(), d.ws_UH.as<Real>(), d.ws_lmid.as<int32_t>(),
+      d.ws_lval.as<Real>(), d.ws_prank.as<uint32_t>());
   if (H > 0)
     wx_extend_kernel<Real><<<grid_for(H * (ldh - n), 256), 256, 0, st>>>(d.ws_UH.as<Real>(), H, ldh, n);
   wx_colcount_kernel<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(

@@ -9,17 +9,20 @@
 //    FP64 (fp32: FP32) DADD + DFMA per (row, slot), |u - v| folded into the
 //    DFMA's operand modifier. All terms are >= 0 and added directly, so there
 //    is no cancellation: d_heavy is within ~H eps of its exact value.
-//  * light rows: the slot's light part is
-//        AL_k + AL_l + sum_{light rows present in both} [t1 - e_u - e_v]
-//    with AL_c = sum over the light rows of column c of e = fl(x L), t1 =
-//    fl(|u - v| L). Every term is converted EXACTLY to a 128-bit fixed-point
-//    integer (grid 2^-G, truncating only bits below 2^-G, G ~ 100), so the
-//    light part is the exact sum of the reference's own light terms; the
-//    identical-sample case cancels to exactly 0. Per (column k, slot tile)
-//    a CTA owns the tile's accumulators in shared memory as balanced 16-bit
-//    digit planes (native 32-bit shared atomics; 2^16 adds per plane before
-//    a fold) and walks column k's light rows: per row, the members of the
-//    row's sorted sample list inside the tile's window, one lane each.
+//  * light rows: with a = fix(e_u), b = fix(e_v) (e = fl(x L), converted
+//    EXACTLY to 128-bit fixed point on the grid 2^-G, G ~ 100; only bits
+//    below 2^-G are dropped), the slot's light part is
+//        sum_{u only} a + sum_{v only} b + sum_{both} |a - b|
+//      = AL_k + AL_l - 2 sum_{light rows in both} min(a, b)
+//    with AL_c the column's sum of fix(e) over its light rows. The shared
+//    row's term |a - b| is within one ulp of the reference's fl(|u - v| L)
+//    (identical samples: exactly 0), and the sum itself is exact, rounded
+//    once. Per (column k, slot tile) a CTA owns the tile's accumulators in
+//    shared memory as balanced 16-bit digit planes (native 32-bit shared
+//    reductions; carry-normalised every 2^15 rows) and walks column k's
+//    light rows: per row, the members of the row's sorted (sample, e_v) list
+//    inside the tile's window, one lane each: one conversion and ND
+//    reductions per pair.
 //
 // The dense kernel's epilogue adds the light part (already rounded once to
 // double), forms WN's separable total t = A_k + A_l (double-double column
@@ -133,8 +136,8 @@ __global__ void wx_fill_kernel(const uint32_t* __restrict__ nb, const uint32_t* 
                                const Real* __restrict__ pool, int64_t n_ext, int32_t n, int32_t W,
                                const uint32_t* __restrict__ hmask, const uint32_t* __restrict__ lmask,
                                const uint32_t* __restrict__ hidx, const unsigned long long* __restrict__ lptr,
-                               int64_t ldh, Real* __restrict__ UH, int32_t* __restrict__ lmid,
-                               Real* __restrict__ lval, uint32_t* __restrict__ prank) {
+                               int64_t ldh, const double* __restrict__ lens, Real* __restrict__ UH,
+                               int32_t* __restrict__ lmid, Real* __restrict__ lval, uint32_t* __restrict__ prank) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -173,7 +176,7 @@ __global__ void wx_fill_kernel(const uint32_t* __restrict__ nb, const uint32_t* 
           if (has) {
             const unsigned long long p = base + static_cast<unsigned>(__popc(bal & ((1u << lane) - 1u)));
             lmid[p] = c;
-            lval[p] = v;
+            lval[p] = static_cast<Real>(lens[32 * w + i]) * v;  // e_v = fl(v L), the light term's operand
             prank[q] = static_cast<uint32_t>(p - start);  // the column's position in the row's list
           }
           if (lane == i) lnext += static_cast<unsigned>(__popc(bal));
@@ -347,26 +350,27 @@ __device__ __forceinline__ unsigned long long wx_lower(const int32_t* __restrict
 }
 
 // Members [p, ...) of one row with ids <= hi, slot = id + sh: the lanes take
-// 32 x kWSUnroll at a time until the sorted ids pass hi. Per pair the exact
-// X = fix(t1) - fix(e_v) - fix(e_u) goes in as balanced 16-bit digits: with
-// the row constant c = B - fix(e_u), B = sum_j 2^15 2^(16 j) (all 8 fields),
-// the digits of Y = fix(t1) - fix(e_v) + c are d_j + 2^15, so each digit is a
-// fixed 16-bit field of Y (no 128-bit shifts).
+// 32 x kWSUnroll at a time until the sorted ids pass hi. The member lists
+// hold e_v = fl(v L) (the row's own length). With a = fix(e_u), b = fix(e_v)
+// the shared row's term |a - b| plus the one-sided a + b already in the
+// column sums leaves X = |a - b| - a - b = -2 min(a, b): one conversion per
+// pair. X goes in as balanced 16-bit digits: Y = B - 2 min(a, b) with
+// B = 2^15 in every 16-bit field, so digit j is field j of Y minus 2^15.
 template <class Real, int ND>
 __device__ __forceinline__ void wx_light_walk(const WSLightArgs& a, unsigned long long p, unsigned long long pe,
-                                              int32_t hi, int32_t sh, Real u, Real L, unsigned long long c_lo,
-                                              unsigned long long c_hi, uint32_t planes_s, int T, int G,
+                                              int32_t hi, int32_t sh, Real eu, uint32_t planes_s, int T, int G,
                                               unsigned long long& pairs) {
   const int lane = threadIdx.x & 31;
   const Real* __restrict__ lval = static_cast<const Real*>(a.lval);
+  constexpr unsigned long long kB = 0x8000800080008000ull;
   for (unsigned long long pb = p;; pb += 32 * kWSUnroll) {
     int32_t id[kWSUnroll];
-    Real v[kWSUnroll];
+    Real ev[kWSUnroll];
 #pragma unroll
     for (int j = 0; j < kWSUnroll; ++j) {
       const unsigned long long m = pb + lane + 32 * j;
       id[j] = m < pe ? __ldg(a.lmid + m) : INT32_MAX;
-      v[j] = m < pe ? lval[m] : Real(0);
+      ev[j] = m < pe ? lval[m] : Real(0);
     }
     bool more = true;
 #pragma unroll
@@ -378,16 +382,12 @@ __device__ __forceinline__ void wx_light_walk(const WSLightArgs& a, unsigned lon
       ++pairs;
       // shared-window address of the slot in digit plane 0
       const uint32_t cell = planes_s + 4u * static_cast<uint32_t>(id[j] + sh);
-      const Real t1 = (u > v[j] ? u - v[j] : v[j] - u) * L;
-      const Real ev = v[j] * L;
-      unsigned long long tl, th, el, eh;
-      wx_fix2(static_cast<double>(t1), G, tl, th);
-      wx_fix2(static_cast<double>(ev), G, el, eh);
-      // Y = T - E + c (mod 2^128)
-      const unsigned long long s1 = tl + c_lo;
-      unsigned long long yh = th + c_hi + (s1 < tl ? 1ull : 0ull);
-      const unsigned long long yl = s1 - el;
-      yh = yh - eh - (s1 < el ? 1ull : 0ull);
+      unsigned long long ml, mh;
+      wx_fix2(static_cast<double>(eu < ev[j] ? eu : ev[j]), G, ml, mh);
+      // Y = B - 2 min (mod 2^128)
+      const unsigned long long tl = ml << 1, th = (mh << 1) | (ml >> 63);
+      const unsigned long long yl = kB - tl;
+      const unsigned long long yh = kB - th - (kB < tl ? 1ull : 0ull);
       const uint32_t w[4] = {static_cast<uint32_t>(yl), static_cast<uint32_t>(yl >> 32), static_cast<uint32_t>(yh),
                              static_cast<uint32_t>(yh >> 32)};
       // the ND planes' digits (those above are 0: |X| < 2^(16 ND - 1)); a
@@ -447,22 +447,16 @@ __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLi
       const int32_t r = __ldg(a.crow + e);
       const Real u = cval[e];
       const uint32_t rank = __ldg(a.crank + e);
-      const Real L = static_cast<Real>(__ldg(a.lens + r));
-      // c = B - fix(e_u), B = 0x8000 in every 16-bit field
-      unsigned long long fl_, fh_;
-      wx_fix2(static_cast<double>(L * u), G, fl_, fh_);
-      const unsigned long long b_lo = 0x8000800080008000ull, b_hi = 0x8000800080008000ull;
-      const unsigned long long c_lo = b_lo - fl_;
-      const unsigned long long c_hi = b_hi - fh_ - (b_lo < fl_ ? 1ull : 0ull);
+      const Real eu = static_cast<Real>(__ldg(a.lens + r)) * u;  // fl(u L), as in the column sums
       const unsigned long long m0 = __ldg(a.lptr + r), m1 = __ldg(a.lptr + r + 1);
       const unsigned long long me = m0 + rank;  // the column itself
       if (hasA) {
         const unsigned long long pa = s_lo == 0 ? me + 1 : wx_lower(a.lmid, me + 1, m1, static_cast<int32_t>(xa));
-        wx_light_walk<Real, ND>(a, pa, m1, hiA, shA, u, L, c_lo, c_hi, planes_s, T, G, pairs);
+        wx_light_walk<Real, ND>(a, pa, m1, hiA, shA, eu, planes_s, T, G, pairs);
       }
       if (hasB) {
         const unsigned long long pb = loB == 0 ? m0 : wx_lower(a.lmid, m0, me, loB);
-        wx_light_walk<Real, ND>(a, pb, me, hiB, shB, u, L, c_lo, c_hi, planes_s, T, G, pairs);
+        wx_light_walk<Real, ND>(a, pb, me, hiB, shB, eu, planes_s, T, G, pairs);
       }
     }
     if (f1 < r1) {  // carry-normalise the planes before the next rows
