@@ -1494,7 +1494,7 @@ sf_status wuwalk_build(sf_plan* plan, DeviceState& d, int32_t r0, int32_t C, cud
 // Heavy threshold of kernel 13 as a fraction of n (SF_WHEAVY_FRAC).
 double ws_heavy_frac() {
   const char* e = std::getenv("SF_WHEAVY_FRAC");
-  return e ? std::atof(e) : 0.2;
+  return e ? std::atof(e) : 0.25;
 }
 
 // Kernel 13 (wsplit_kernels.cuh), after kernel 12's build of every chunk and
