@@ -481,9 +481,10 @@ def roofline_record(args, cfg, metric, prec, device, world, stop_all, E, n, str_
                 (E * stop_all * n * args.steps / (sum(dev_ms) / 1e3)) / (peak_fma / 4), 2),
         }
     if metric != 1 and t_ms > 0 and fp64_ops > 0:
-        # weighted split (13): the dense heavy-row kernel issues one DADD + one
-        # DFMA (fp32: FADD + FFMA) per (heavy row, slot); its CUDA-event time
-        # against the measured FMA-instruction peak of that pipe
+        # weighted split (13): the dense heavy-row kernel's FP64-pipe (fp32:
+        # FP32-pipe) instructions, counted per (heavy row, slot) from its SASS
+        # (WN/WU: DADD + DFMA; generalized alpha = 0.5: 14), over its CUDA-event
+        # time, against the measured FMA-instruction peak of that pipe
         pipe = "fp64" if prec == 8 else "fp32"
         peak_fma = measured_fp_peak(device, pipe)
         rate = fp64_ops / (t_ms / 1e3)
@@ -491,8 +492,8 @@ def roofline_record(args, cfg, metric, prec, device, world, stop_all, E, n, str_
         return {
             "bound": pipe, "achieved": round(rate * 2 / 1e12, 3), "peak": round(peak_fma * 2 / 1e12, 3),
             "unit": "TFLOP/s", "frac": round(rate / peak_fma, 4) if peak_fma else None,
-            "unit_note": ("FMA-equivalent: pipe instructions x 2 (each (heavy row, slot) is a DADD + a DFMA, "
-                          "|u - v| an operand modifier), so frac = the pipe's issue fraction"),
+            "unit_note": ("FMA-equivalent: pipe instructions x 2 (WN/WU: each (heavy row, slot) is a DADD + a "
+                          "DFMA, |u - v| an operand modifier), so frac = the pipe's issue fraction"),
             "traffic": round(tr["dram_bytes"] / tr["stripes"] * (stop_all / max(world, 1))) if tr else None,
             "traffic_unit": "DRAM bytes per launch",
             "traffic_source": (f"{tr['source']} ({tr['stripes']} stripes, scaled per stripe)" if tr else None),

@@ -586,7 +586,7 @@ struct DeviceState {
   // kernel 13: row counts / flags / scans, dense heavy rows, light member and
   // column lists, light column sums, the light part of every slot
   DevBuf ws_cnt, ws_hflag, ws_hidx, ws_lcnt, ws_lptr, ws_hmask, ws_lmask, ws_UH, ws_LH, ws_lmid, ws_lval,
-      ws_ccnt, ws_cptr, ws_crow, ws_cval, ws_AL, ws_lightd, ws_tmp, ws_prank, ws_crank;
+      ws_ccnt, ws_cptr, ws_crow, ws_cval, ws_AL, ws_lightd, ws_tmp, ws_prank, ws_crank, ws_lvala, ws_lightt;
   uint64_t host_fp64_ops = 0;  // FP64/FP32-pipe lane-ops counted on the host (kernel 13's dense part)
   DevBuf wnbo;               // kernel 12: combined (offset, presence word) cells
   int32_t light_pass = 0;  // stripes per light-sum pass (memory-bounded)
@@ -1049,7 +1049,9 @@ sf_status light_sums_alloc(sf_plan* plan, DeviceState& d, size_t after) {
     // steady state: the pool still holds the previous plan's freed blocks,
     // so the same allocations are served again without a probe (a probe's
     // single large block would fragment them)
-    if (pool_free_bytes(d.dev) >= need + reserve || probe_fits(d.dev, need + reserve, need)) {
+    // (the reserve is headroom for allocations outside the pool: in the
+    // steady state they exist already, so free pool bytes >= need suffice)
+    if (pool_free_bytes(d.dev) >= need || probe_fits(d.dev, need + reserve, need)) {
       fit = static_cast<size_t>(span);
       probed = true;
     }
@@ -1504,6 +1506,8 @@ template <class Real>
 sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream_t st) {
   const int n = plan->n;
   const int32_t E = plan->E;
+  const bool gen = plan->metric == SF_GENERALIZED;
+  const bool sq = gen && plan->alpha == 0.5;  // alpha = 0.5: one rsqrt per term
   const int32_t W = (E + 31) / 32;
   const int64_t n_ext = sparse_n_ext(n);
   const uint32_t* nb = d.wnb.as<uint32_t>();
@@ -1556,6 +1560,7 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
   const size_t lt = static_cast<size_t>(std::max<unsigned long long>(LT, 1));
   if (d.ws_lmid.bytes < lt * 4) SF_TRY(d.ws_lmid.alloc(d.dev, lt * 4, "light members"));
   if (d.ws_lval.bytes < lt * w) SF_TRY(d.ws_lval.alloc(d.dev, lt * w, "light member values"));
+  if (gen && d.ws_lvala.bytes < lt * w) SF_TRY(d.ws_lvala.alloc(d.dev, lt * w, "light one-sided terms"));
   if (d.ws_crow.bytes < lt * 4) SF_TRY(d.ws_crow.alloc(d.dev, lt * 4, "column light rows"));
   if (d.ws_cval.bytes < lt * w) SF_TRY(d.ws_cval.alloc(d.dev, lt * w, "column light values"));
   if (d.ws_crank.bytes < lt * 4) SF_TRY(d.ws_crank.alloc(d.dev, lt * 4, "column ranks"));
@@ -1563,14 +1568,24 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
   if (d.ws_prank.bytes < pool_entries * 4) SF_TRY(d.ws_prank.alloc(d.dev, pool_entries * 4, "member ranks"));
   const size_t slots = static_cast<size_t>(d.b - d.a) * static_cast<size_t>(n);
   if (d.ws_lightd.bytes < slots * 8) SF_TRY(d.ws_lightd.alloc(d.dev, slots * 8, "light part"));
+  if (gen && d.ws_lightt.bytes < slots * 8) SF_TRY(d.ws_lightt.alloc(d.dev, slots * 8, "light part of the totals"));
   // dense heavy rows, light member lists, column lists
   SF_CUDA(cudaMemsetAsync(d.ws_UH.p, 0, uh_bytes, st));
   wx_heavylen_kernel<Real><<<grid_for(E, 256), 256, 0, st>>>(d.ws_hflag.as<uint32_t>(), d.ws_hidx.as<uint32_t>(),
                                                               d.lens_pad.as<double>(), E, d.ws_LH.as<Real>());
-  wx_fill_kernel<Real><<<std::min<int64_t>((W + 7) / 8, 148 * 64), 256, 0, st>>>(
-      nb, off, pool, n_ext, n, W, d.ws_hmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>(), d.ws_hidx.as<uint32_t>(),
-      d.ws_lptr.as<unsigned long long>(), ldh, d.lens_pad.as<double>(), d.ws_UH.as<Real>(), d.ws_lmid.as<int32_t>(),
-      d.ws_lval.as<Real>(), d.ws_prank.as<uint32_t>());
+  {
+    const int fb = static_cast<int>(std::min<int64_t>((W + 7) / 8, 148 * 64));
+    auto fill = [&](auto* kern) {
+      kern<<<fb, 256, 0, st>>>(nb, off, pool, n_ext, n, W, d.ws_hmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>(),
+                               d.ws_hidx.as<uint32_t>(), d.ws_lptr.as<unsigned long long>(), ldh,
+                               d.lens_pad.as<double>(), plan->alpha, d.ws_UH.as<Real>(), d.ws_lmid.as<int32_t>(),
+                               d.ws_lval.as<Real>(), gen ? d.ws_lvala.as<Real>() : nullptr, d.ws_prank.as<uint32_t>());
+    };
+    if (gen)
+      fill(wx_fill_kernel<Real, true>);
+    else
+      fill(wx_fill_kernel<Real, false>);
+  }
   if (H > 0)
     wx_extend_kernel<Real><<<grid_for(H * (ldh - n), 256), 256, 0, st>>>(d.ws_UH.as<Real>(), H, ldh, n);
   wx_colcount_kernel<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
@@ -1578,10 +1593,18 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
   tmp = d.ws_tmp.bytes;
   SF_CUDA(cub::DeviceScan::ExclusiveSum(d.ws_tmp.p, tmp, d.ws_ccnt.as<unsigned long long>(),
                                         d.ws_cptr.as<unsigned long long>(), n + 1, st));
-  wx_colfill_kernel<Real><<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
-      nb, off, d.nzmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>(), pool, d.ws_prank.as<uint32_t>(),
-      d.lens_pad.as<double>(), n_ext, n, W, plan->ws_G, d.ws_cptr.as<unsigned long long>(), d.ws_crow.as<int32_t>(),
-      d.ws_cval.as<Real>(), d.ws_crank.as<uint32_t>(), d.ws_AL.as<unsigned long long>());
+  {
+    auto colfill = [&](auto* kern) {
+      kern<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
+          nb, off, d.nzmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>(), pool, d.ws_prank.as<uint32_t>(),
+          d.lens_pad.as<double>(), plan->alpha, n_ext, n, W, plan->ws_G, d.ws_cptr.as<unsigned long long>(),
+          d.ws_crow.as<int32_t>(), d.ws_cval.as<Real>(), d.ws_crank.as<uint32_t>(), d.ws_AL.as<unsigned long long>());
+    };
+    if (gen)
+      colfill(wx_colfill_kernel<Real, true>);
+    else
+      colfill(wx_colfill_kernel<Real, false>);
+  }
   SF_CUDA(cudaGetLastError());
   // light part of every slot (exact), then the dense heavy rows + epilogue
   WSLightArgs la;
@@ -1592,6 +1615,9 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
   la.lptr = d.ws_lptr.as<unsigned long long>();
   la.lmid = d.ws_lmid.as<int32_t>();
   la.lval = d.ws_lval.p;
+  la.lvala = gen ? d.ws_lvala.p : nullptr;
+  la.alpha = plan->alpha;
+  la.lightt = gen ? d.ws_lightt.as<double>() : nullptr;
   la.lens = d.lens_pad.as<double>();
   la.AL = d.ws_AL.as<unsigned long long>();
   la.n = n;
@@ -1601,24 +1627,35 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
   const int span = d.b - d.a;
   la.G = plan->ws_G;
   la.nd = plan->ws_nd;
-  const int max_tile = kWSLightSmem / (4 * la.nd);
+  const int max_tile = kWSLightSmem / (4 * la.nd * (gen ? 2 : 1));
   const int ntiles = (span + max_tile - 1) / max_tile;
   la.tile = (span + ntiles - 1) / ntiles;
   la.lightd = d.ws_lightd.as<double>();
   la.pairs = d.exec_ctr.as<unsigned long long>();
-  const size_t lsmem = static_cast<size_t>(la.nd) * static_cast<size_t>(la.tile) * 4;
+  const size_t lsmem = static_cast<size_t>(la.nd) * static_cast<size_t>(la.tile) * 4 * (gen ? 2 : 1);
   auto light = [&](auto* kern) -> sf_status {
     SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
     kern<<<dim3(static_cast<unsigned>(n), static_cast<unsigned>(ntiles)), kWSLightThreads, lsmem, st>>>(la);
     return SF_OK;
   };
-  switch (la.nd) {  // digit planes: 16 bits each, from the lengths' range (plan time)
-    case 4: SF_TRY(light(wx_light_kernel<Real, 4>)); break;
-    case 5: SF_TRY(light(wx_light_kernel<Real, 5>)); break;
-    case 6: SF_TRY(light(wx_light_kernel<Real, 6>)); break;
-    case 7: SF_TRY(light(wx_light_kernel<Real, 7>)); break;
-    default: SF_TRY(light(wx_light_kernel<Real, 8>)); break;
-  }
+  // digit planes: 16 bits each, from the lengths' range (plan time);
+  // -1 weighted, 0 generalized (pow), 1 generalized alpha = 0.5 (rsqrt)
+  auto by_nd = [&](auto genc) -> sf_status {
+    constexpr int GA = decltype(genc)::value;
+    switch (la.nd) {
+      case 4: return light(wx_light_kernel<Real, 4, GA>);
+      case 5: return light(wx_light_kernel<Real, 5, GA>);
+      case 6: return light(wx_light_kernel<Real, 6, GA>);
+      case 7: return light(wx_light_kernel<Real, 7, GA>);
+      default: return light(wx_light_kernel<Real, 8, GA>);
+    }
+  };
+  if (!gen)
+    SF_TRY(by_nd(std::integral_constant<int, -1>{}));
+  else if (sq)
+    SF_TRY(by_nd(std::integral_constant<int, 1>{}));
+  else
+    SF_TRY(by_nd(std::integral_constant<int, 0>{}));
   SF_CUDA(cudaGetLastError());
   WSDenseArgs da;
   da.UH = d.ws_UH.p;
@@ -1631,29 +1668,41 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
   da.out_begin = d.a;
   da.finalize = finalize ? 1 : 0;
   da.lightd = d.ws_lightd.as<double>();
+  da.lightt = gen ? d.ws_lightt.as<double>() : nullptr;
+  da.alpha = plan->alpha;
   da.A = d.wA.as<double2>();
   da.dist = d.dist.p;
   da.tot = plan->metric == SF_WEIGHTED_UNNORMALIZED ? nullptr : d.tot.p;
-  const size_t dsmem = (2 * kWSR * (2 * kWSK + kWSS) + 2 * kWSR) * w;
-  const dim3 dgrid(static_cast<unsigned>((n + kWSK - 1) / kWSK), static_cast<unsigned>((span + kWSS - 1) / kWSS));
   while (d.gemm_ev.size() < 2 * (d.gemm_count + 1)) {
     cudaEvent_t e;
     SF_CUDA(cudaEventCreate(&e));
     d.gemm_ev.push_back(e);
   }
-  SF_CUDA(cudaEventRecord(d.gemm_ev[2 * d.gemm_count], st));
-  if (plan->metric == SF_WEIGHTED_UNNORMALIZED) {
-    SF_CUDA(cudaFuncSetAttribute(wx_dense_kernel<kWU, Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem)));
-    wx_dense_kernel<kWU, Real><<<dgrid, kWSThreads, dsmem, st>>>(da);
-  } else {
-    SF_CUDA(cudaFuncSetAttribute(wx_dense_kernel<kWN, Real>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem)));
-    wx_dense_kernel<kWN, Real><<<dgrid, kWSThreads, dsmem, st>>>(da);
-  }
+  auto dense = [&](auto* kern, int kt) -> sf_status {
+    const size_t dsmem = (2 * kWSR * (2 * static_cast<size_t>(kt) + kWSS) + 2 * kWSR) * w;
+    const dim3 dgrid(static_cast<unsigned>((n + kt - 1) / kt), static_cast<unsigned>((span + kWSS - 1) / kWSS));
+    SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(dsmem)));
+    SF_CUDA(cudaEventRecord(d.gemm_ev[2 * d.gemm_count], st));
+    kern<<<dgrid, kWSThreads, dsmem, st>>>(da);
+    return SF_OK;
+  };
+  if (plan->metric == SF_WEIGHTED_UNNORMALIZED)
+    SF_TRY(dense(wx_dense_kernel<kWU, Real, false>, wx_dense_kt<kWU>()));
+  else if (!gen)
+    SF_TRY(dense(wx_dense_kernel<kWN, Real, false>, wx_dense_kt<kWN>()));
+  else if (sq)
+    SF_TRY(dense(wx_dense_kernel<kGen, Real, true>, wx_dense_kt<kGen>()));
+  else
+    SF_TRY(dense(wx_dense_kernel<kGen, Real, false>, wx_dense_kt<kGen>()));
   SF_CUDA(cudaGetLastError());
   SF_CUDA(cudaEventRecord(d.gemm_ev[2 * d.gemm_count + 1], st));
   ++d.gemm_count;
   const uint64_t live = static_cast<uint64_t>(span) * static_cast<uint64_t>(n);
-  d.host_fp64_ops += 2ull * static_cast<uint64_t>(H) * live;  // DADD + DFMA per (heavy row, slot)
+  // FP64-pipe instructions per (heavy row, slot), from the kernels' SASS:
+  // DADD + DFMA (WN/WU); 14 for generalized alpha = 0.5 (DADD x3, DSETP x2,
+  // DMUL x4, DFMA x5 around one MUFU.RSQ64H); the pow path is not counted
+  const uint64_t per = gen ? (sq ? 14ull : 0ull) : 2ull;
+  d.host_fp64_ops += per * static_cast<uint64_t>(H) * live;
   d.heavy_updates += static_cast<uint64_t>(H) * live;
   d.launches += 14;
   return SF_OK;
@@ -2438,8 +2487,8 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     return fail(SF_EINVAL, "the sparse bit kernels implement the unweighted metric only");
   if (plan->kernel >= 11 && metric == SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the weighted sparse walk implements the weighted metrics only");
-  if (metric == SF_GENERALIZED && (plan->kernel < 11 || plan->kernel == 13))
-    return fail(SF_EINVAL, "generalized UniFrac runs on the weighted sparse walks (kernel 11/12) only");
+  if (metric == SF_GENERALIZED && plan->kernel < 11)
+    return fail(SF_EINVAL, "generalized UniFrac runs on the weighted kernels (11/12/13) only");
   plan->alpha = alpha;
   const bool wsp = plan->kernel == 11 || plan->kernel == 12 || plan->kernel == 13;
   const bool wuw = plan->kernel == 12 || plan->kernel == 13;
@@ -2452,9 +2501,11 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
       tl += p->lengths[r];
       lmax = std::max(lmax, p->lengths[r]);
     }
-    const double bound = 2.0 * tl + 4.0 * lmax + 1.0;
+    // generalized: a shared row's terms reach (u + v)^alpha L <= 2^alpha L
+    const double f = metric == SF_GENERALIZED ? std::max(1.0, std::exp2(alpha)) : 1.0;
+    const double bound = (2.0 * tl + 4.0 * lmax) * f + 1.0;
     plan->ws_G = 125 - (std::ilogb(bound) + 1);
-    const int term_bits = (lmax > 0 ? std::ilogb(3.0 * lmax) + 2 : 1) + plan->ws_G + 1;
+    const int term_bits = (lmax > 0 ? std::ilogb(3.0 * lmax * f) + 2 : 1) + plan->ws_G + 1;
     plan->ws_nd = std::min(8, std::max(4, (term_bits + 15) / 16));
   }
   plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;

@@ -34,6 +34,7 @@
 #include <cstdint>
 
 #include "bits.cuh"
+#include "stripe_kernels.cuh"
 #include "wsparse_kernels.cuh"
 
 namespace sf {
@@ -70,6 +71,26 @@ __device__ __forceinline__ void wx_fix2(double x, int G, unsigned long long& lo,
   const int sh = (ex ? ex : 1) - 1075 + G;  // value = m 2^sh on the grid
   lo = sh >= 0 ? wx_shl(m, static_cast<uint32_t>(sh)) : wx_shr(m, static_cast<uint32_t>(-sh));
   hi = sh >= 64 ? wx_shl(m, static_cast<uint32_t>(sh - 64)) : wx_shr(m, static_cast<uint32_t>(64 - sh));
+}
+
+// Generalized UniFrac (extension) per-row terms, s = u + v > 0:
+// d_s = w |u - v| / s, t_s = w with w = s^alpha L (stripe_kernels.cuh's
+// update_generalized). SQ: alpha = 0.5 through one rsqrt (d_s = L |u-v| /
+// sqrt(s), t_s = L sqrt(s)), within a few ulp of the sqrt + divide form.
+// s = 0 (both absent) gives 0, 0.
+template <class Real, bool SQ>
+__device__ __forceinline__ void wx_gen_terms(Real u, Real v, Real L, Real alpha, Real& ds, Real& ts) {
+  const Real s = u + v;
+  const Real ad = u > v ? u - v : v - u;
+  if (SQ) {
+    const Real r = s > Real(0) ? rsqrt(s) : Real(0);
+    ds = (ad * r) * L;
+    ts = (s * r) * L;
+  } else {
+    const Real w = s > Real(0) ? pow_alpha(s, alpha) * L : Real(0);
+    ds = s > Real(0) ? w * (ad / s) : Real(0);
+    ts = w;
+  }
 }
 
 // ---- build --------------------------------------------------------------------
@@ -131,13 +152,14 @@ __global__ void wx_classify_kernel(const uint32_t* __restrict__ cnt, const doubl
 
 // Warp per presence word: heavy rows' values into the dense matrix UH (zeroed
 // before), light rows' (sample, value) members in sample order at lptr[r].
-template <class Real>
+template <class Real, bool GEN>
 __global__ void wx_fill_kernel(const uint32_t* __restrict__ nb, const uint32_t* __restrict__ off,
                                const Real* __restrict__ pool, int64_t n_ext, int32_t n, int32_t W,
                                const uint32_t* __restrict__ hmask, const uint32_t* __restrict__ lmask,
                                const uint32_t* __restrict__ hidx, const unsigned long long* __restrict__ lptr,
-                               int64_t ldh, const double* __restrict__ lens, Real* __restrict__ UH,
-                               int32_t* __restrict__ lmid, Real* __restrict__ lval, uint32_t* __restrict__ prank) {
+                               int64_t ldh, const double* __restrict__ lens, double alpha, Real* __restrict__ UH,
+                               int32_t* __restrict__ lmid, Real* __restrict__ lval, Real* __restrict__ lvala,
+                               uint32_t* __restrict__ prank) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -176,7 +198,13 @@ __global__ void wx_fill_kernel(const uint32_t* __restrict__ nb, const uint32_t* 
           if (has) {
             const unsigned long long p = base + static_cast<unsigned>(__popc(bal & ((1u << lane) - 1u)));
             lmid[p] = c;
-            lval[p] = static_cast<Real>(lens[32 * w + i]) * v;  // e_v = fl(v L), the light term's operand
+            const Real L = static_cast<Real>(lens[32 * w + i]);
+            if (GEN) {  // v itself and the one-sided term a_v = v^alpha L
+              lval[p] = v;
+              lvala[p] = pow_alpha(v, static_cast<Real>(alpha)) * L;
+            } else {
+              lval[p] = L * v;  // e_v = fl(v L), the light term's operand
+            }
             prank[q] = static_cast<uint32_t>(p - start);  // the column's position in the row's list
           }
           if (lane == i) lnext += static_cast<unsigned>(__popc(bal));
@@ -236,11 +264,12 @@ __global__ void wx_colcount_kernel(const uint32_t* __restrict__ nb, const uint32
 // the row's member list) and AL_k = sum of fix(fl(u L)) over them. Warp per
 // column: lane g takes the 32-word groups g, g + 32, ... in turn, each round
 // placed after the previous round's entries by a warp scan.
-template <class Real>
+template <class Real, bool GEN>
 __global__ void wx_colfill_kernel(const uint32_t* __restrict__ nb, const uint32_t* __restrict__ off,
                                   const uint32_t* __restrict__ nz, const uint32_t* __restrict__ lmask,
                                   const Real* __restrict__ pool, const uint32_t* __restrict__ prank,
-                                  const double* __restrict__ lens, int64_t n_ext, int32_t n, int32_t W, int G,
+                                  const double* __restrict__ lens, double alpha, int64_t n_ext, int32_t n, int32_t W,
+                                  int G,
                                   const unsigned long long* __restrict__ cptr, int32_t* __restrict__ crow,
                                   Real* __restrict__ cval, uint32_t* __restrict__ crank,
                                   unsigned long long* __restrict__ AL) {
@@ -284,7 +313,9 @@ __global__ void wx_colfill_kernel(const uint32_t* __restrict__ nb, const uint32_
           cval[p] = u;
           crank[p] = prank[q];
           ++p;
-          const Real e = static_cast<Real>(lens[r]) * u;
+          // the one-sided term: fl(u L) (weighted), u^alpha L (generalized)
+          const Real e = GEN ? pow_alpha(u, static_cast<Real>(alpha)) * static_cast<Real>(lens[r])
+                             : static_cast<Real>(lens[r]) * u;
           acc += wx_to_fix(static_cast<double>(e), G);
         }
       }
@@ -315,7 +346,9 @@ struct WSLightArgs {
   const uint32_t* crank;           // the column's position in each row's member list
   const unsigned long long* lptr;  // [E + 1] light rows' member lists (sorted samples)
   const int32_t* lmid;
-  const void* lval;                // Real
+  const void* lval;                // Real: e_v = fl(v L) (weighted) or v (generalized)
+  const void* lvala;               // Real: a_v = v^alpha L (generalized), else null
+  double alpha;
   const double* lens;
   const unsigned long long* AL;    // [n] x 2 (lo, hi)
   int32_t n;
@@ -325,6 +358,7 @@ struct WSLightArgs {
   int32_t G;                       // fixed-point grid 2^-G
   int32_t nd;                      // 16-bit digit planes (<= 8)
   double* lightd;                  // [stripes][n] light part, rounded once
+  double* lightt;                  // generalized: the totals' light part, else null
   unsigned long long* pairs;       // light (row, slot) pairs scattered (stats), or null
 };
 
@@ -403,14 +437,76 @@ __device__ __forceinline__ void wx_light_walk(const WSLightArgs& a, unsigned lon
   }
 }
 
+// Generalized (extension): the shared row's d and t terms replace the
+// one-sided a_u + a_v already in the column sums, X = fix(term) - fix(a_v) -
+// fix(a_u) for each, two sets of digit planes (t at plane ND). The row
+// constant c = B - fix(a_u).
+template <class Real, int ND, bool SQ>
+__device__ __forceinline__ void wx_light_walk_gen(const WSLightArgs& a, unsigned long long p, unsigned long long pe,
+                                                  int32_t hi, int32_t sh, Real u, Real L, unsigned long long c_lo,
+                                                  unsigned long long c_hi, uint32_t planes_s, int T, int G,
+                                                  unsigned long long& pairs) {
+  const int lane = threadIdx.x & 31;
+  const Real* __restrict__ lval = static_cast<const Real*>(a.lval);
+  const Real* __restrict__ lvala = static_cast<const Real*>(a.lvala);
+  const Real alpha = static_cast<Real>(a.alpha);
+  for (unsigned long long pb = p;; pb += 32 * kWSUnroll) {
+    int32_t id[kWSUnroll];
+    Real v[kWSUnroll], av[kWSUnroll];
+#pragma unroll
+    for (int j = 0; j < kWSUnroll; ++j) {
+      const unsigned long long m = pb + lane + 32 * j;
+      id[j] = m < pe ? __ldg(a.lmid + m) : INT32_MAX;
+      v[j] = m < pe ? lval[m] : Real(0);
+      av[j] = m < pe ? lvala[m] : Real(0);
+    }
+    bool more = true;
+#pragma unroll
+    for (int j = 0; j < kWSUnroll; ++j) {
+      if (id[j] > hi) {
+        more = false;
+        continue;
+      }
+      ++pairs;
+      const uint32_t cell = planes_s + 4u * static_cast<uint32_t>(id[j] + sh);
+      Real ds, ts;
+      wx_gen_terms<Real, SQ>(u, v[j], L, alpha, ds, ts);
+      unsigned long long el, eh;
+      wx_fix2(static_cast<double>(av[j]), G, el, eh);
+      // c - fix(a_v), then + fix(term) for d and for t
+      const unsigned long long bl = c_lo - el;
+      const unsigned long long bh = c_hi - eh - (c_lo < el ? 1ull : 0ull);
+#pragma unroll
+      for (int which = 0; which < 2; ++which) {
+        unsigned long long tl, th;
+        wx_fix2(static_cast<double>(which ? ts : ds), G, tl, th);
+        const unsigned long long yl = bl + tl;
+        const unsigned long long yh = bh + th + (yl < bl ? 1ull : 0ull);
+        const uint32_t w[4] = {static_cast<uint32_t>(yl), static_cast<uint32_t>(yl >> 32), static_cast<uint32_t>(yh),
+                               static_cast<uint32_t>(yh >> 32)};
+        const uint32_t base = cell + 4u * static_cast<uint32_t>(which * ND * T);
+#pragma unroll
+        for (int d = 0; d < ND; ++d) {
+          const int32_t dg = static_cast<int32_t>((w[d >> 1] >> (16 * (d & 1))) & 0xffffu) - 0x8000;
+          asm volatile("red.shared.add.s32 [%0], %1;" ::"r"(base + 4u * static_cast<uint32_t>(d * T)), "r"(dg)
+                       : "memory");
+        }
+      }
+    }
+    if (!__all_sync(0xffffffffu, more)) break;
+  }
+}
+
 // Per (column k, tile of slots): column k's light rows, warp per row, the
 // members of the row inside the tile's window (from the column's own
 // position in the row's list when the window starts right after k), exact
 // digit-plane accumulation; then each slot's exact light sum AL_k + AL_l +
 // sum, rounded once.
-template <class Real, int ND>
+template <class Real, int ND, int GENA>
 __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLightArgs a) {
-  extern __shared__ int32_t planes[];  // [nd][tile]
+  constexpr bool GEN = GENA >= 0;
+  constexpr int NP = GEN ? 2 : 1;      // plane sets: d (and t)
+  extern __shared__ int32_t planes[];  // [NP][nd][tile]
   const int k = blockIdx.x;
   const int n = a.n;
   const int s_lo = a.s_begin + static_cast<int>(blockIdx.y) * a.tile;
@@ -430,7 +526,7 @@ __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLi
   const int32_t hiB = static_cast<int32_t>(xb - n);
   const bool hasB = xb >= n;
   const int32_t shA = -k - 1 - s_lo, shB = n - k - 1 - s_lo;
-  for (int i = threadIdx.x; i < nd * T; i += kWSLightThreads) planes[i] = 0;
+  for (int i = threadIdx.x; i < NP * nd * T; i += kWSLightThreads) planes[i] = 0;
   const uint32_t planes_s = static_cast<uint32_t>(__cvta_generic_to_shared(planes));
   __syncthreads();
   unsigned long long pairs = 0;
@@ -447,29 +543,38 @@ __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLi
       const int32_t r = __ldg(a.crow + e);
       const Real u = cval[e];
       const uint32_t rank = __ldg(a.crank + e);
-      const Real eu = static_cast<Real>(__ldg(a.lens + r)) * u;  // fl(u L), as in the column sums
+      const Real L = static_cast<Real>(__ldg(a.lens + r));
       const unsigned long long m0 = __ldg(a.lptr + r), m1 = __ldg(a.lptr + r + 1);
       const unsigned long long me = m0 + rank;  // the column itself
-      if (hasA) {
-        const unsigned long long pa = s_lo == 0 ? me + 1 : wx_lower(a.lmid, me + 1, m1, static_cast<int32_t>(xa));
-        wx_light_walk<Real, ND>(a, pa, m1, hiA, shA, eu, planes_s, T, G, pairs);
-      }
-      if (hasB) {
-        const unsigned long long pb = loB == 0 ? m0 : wx_lower(a.lmid, m0, me, loB);
-        wx_light_walk<Real, ND>(a, pb, me, hiB, shB, eu, planes_s, T, G, pairs);
+      const unsigned long long pa =
+          hasA ? (s_lo == 0 ? me + 1 : wx_lower(a.lmid, me + 1, m1, static_cast<int32_t>(xa))) : 0ull;
+      const unsigned long long pb = hasB ? (loB == 0 ? m0 : wx_lower(a.lmid, m0, me, loB)) : 0ull;
+      if constexpr (GEN) {
+        // c = B - fix(a_u), a_u = u^alpha L as in the column sums
+        unsigned long long fl_, fh_;
+        wx_fix2(static_cast<double>(pow_alpha(u, static_cast<Real>(a.alpha)) * L), G, fl_, fh_);
+        const unsigned long long kB = 0x8000800080008000ull;
+        const unsigned long long c_lo = kB - fl_, c_hi = kB - fh_ - (kB < fl_ ? 1ull : 0ull);
+        if (hasA) wx_light_walk_gen<Real, ND, GENA == 1>(a, pa, m1, hiA, shA, u, L, c_lo, c_hi, planes_s, T, G, pairs);
+        if (hasB) wx_light_walk_gen<Real, ND, GENA == 1>(a, pb, me, hiB, shB, u, L, c_lo, c_hi, planes_s, T, G, pairs);
+      } else {
+        const Real eu = L * u;  // fl(u L), as in the column sums
+        if (hasA) wx_light_walk<Real, ND>(a, pa, m1, hiA, shA, eu, planes_s, T, G, pairs);
+        if (hasB) wx_light_walk<Real, ND>(a, pb, me, hiB, shB, eu, planes_s, T, G, pairs);
       }
     }
     if (f1 < r1) {  // carry-normalise the planes before the next rows
       __syncthreads();
-      for (int q = threadIdx.x; q < T; q += kWSLightThreads) {
+      for (int q = threadIdx.x; q < NP * T; q += kWSLightThreads) {
+        int32_t* pl = planes + (q / T) * nd * T + (q % T);
         int32_t carry = 0;
         for (int d = 0; d + 1 < nd; ++d) {
-          const int32_t v = planes[d * T + q] + carry;
+          const int32_t v = pl[d * T] + carry;
           const int32_t lo = static_cast<int16_t>(static_cast<uint16_t>(v));
           carry = (v - lo) >> 16;
-          planes[d * T + q] = lo;
+          pl[d * T] = lo;
         }
-        planes[(nd - 1) * T + q] += carry;
+        pl[(nd - 1) * T] += carry;
       }
       __syncthreads();
     }
@@ -480,14 +585,18 @@ __global__ void __launch_bounds__(kWSLightThreads, 1) wx_light_kernel(const WSLi
   for (int q = threadIdx.x; q < T; q += kWSLightThreads) {
     const int s = s_lo + q;
     if (s >= s_hi) break;
-    __int128 v = 0;
-    for (int d = nd - 1; d >= 0; --d) v = v * 65536 + static_cast<__int128>(planes[d * T + q]);
     const int64_t li = static_cast<int64_t>(k) + s + 1;
     const int l = static_cast<int>(li >= n ? li - n : li);
     const unsigned __int128 ALl =
         (static_cast<unsigned __int128>(a.AL[2 * l + 1]) << 64) | static_cast<unsigned __int128>(a.AL[2 * l]);
-    const unsigned __int128 tot = ALk + ALl + static_cast<unsigned __int128>(v);  // >= 0: the exact light sum
-    __stcs(a.lightd + static_cast<int64_t>(s - a.out_begin) * n + k, u128_to_real<double>(tot, false, -G));
+#pragma unroll
+    for (int set = 0; set < NP; ++set) {
+      __int128 v = 0;
+      for (int d = nd - 1; d >= 0; --d) v = v * 65536 + static_cast<__int128>(planes[(set * nd + d) * T + q]);
+      const unsigned __int128 tot = ALk + ALl + static_cast<unsigned __int128>(v);  // >= 0: the exact light sum
+      __stcs((set ? a.lightt : a.lightd) + static_cast<int64_t>(s - a.out_begin) * n + k,
+             u128_to_real<double>(tot, false, -G));
+    }
   }
   if (a.pairs) {
     for (int o = 16; o; o >>= 1) pairs += __shfl_down_sync(0xffffffffu, pairs, o);
@@ -506,12 +615,19 @@ struct WSDenseArgs {
   int32_t out_begin;
   int32_t finalize;
   const double* lightd;   // [stripes][n]
+  const double* lightt;   // generalized: the totals' light part
   const double2* A;       // [n] WN column sums (double-double), t = A_k + A_l
+  double alpha;           // generalized exponent
   void* dist;
   void* tot;              // null for WU
 };
 
 constexpr int kWSK = 128, kWSS = 128;  // tile: u columns x stripes
+// u columns per CTA tile: generalized keeps d and t accumulators, so half
+template <int M>
+__host__ __device__ constexpr int wx_dense_kt() {
+  return M == kGen ? kWSK / 2 : kWSK;
+}
 #ifndef SF_WS_R
 #define SF_WS_R 16
 #endif
@@ -527,15 +643,18 @@ __device__ __forceinline__ void wx_cp4(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem));
 }
 
-template <int M, class Real>
+template <int M, class Real, bool SQ>
 __global__ void __launch_bounds__(kWSThreads, 1) wx_dense_kernel(const WSDenseArgs a) {
-  constexpr int UW = kWSK, VW = kWSK + kWSS;  // staged values per row (VW - 1 used)
+  constexpr bool GEN = M == kGen;
+  constexpr int KT = wx_dense_kt<M>();  // u columns of the tile
+  constexpr int TI = KT / 16;           // per thread: TI u columns x 8 stripes
+  constexpr int UW = KT, VW = KT + kWSS;  // staged values per row (VW - 1 used)
   constexpr int ROW = UW + VW;
   extern __shared__ __align__(16) unsigned char wx_smem[];
   Real* stage = reinterpret_cast<Real*>(wx_smem);  // [2][kWSR][ROW]
   Real* lstage = stage + 2 * kWSR * ROW;           // [2][kWSR]
   const int n = a.n;
-  const int k0 = blockIdx.x * kWSK;
+  const int k0 = blockIdx.x * KT;
   const int s0 = a.s_begin + blockIdx.y * kWSS;
   const int tk = threadIdx.x & 15, ts = threadIdx.x >> 4;
   const Real* __restrict__ UH = static_cast<const Real*>(a.UH);
@@ -560,11 +679,15 @@ __global__ void __launch_bounds__(kWSThreads, 1) wx_dense_kernel(const WSDenseAr
     if (threadIdx.x < kWSR) lstage[buf * kWSR + threadIdx.x] = threadIdx.x < rows ? LH[h0 + threadIdx.x] : Real(0);
     asm volatile("cp.async.commit_group;");
   };
-  Real acc[8][8];
+  Real acc[TI][8], acct[GEN ? TI : 1][8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < TI; ++i)
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc[i][j] = Real(0);
+    for (int j = 0; j < 8; ++j) {
+      acc[i][j] = Real(0);
+      if (GEN) acct[i][j] = Real(0);
+    }
+  const Real alpha = static_cast<Real>(a.alpha);
   if (H > 0) load(0, 0);
   int buf = 0;
   for (int64_t h0 = 0; h0 < H; h0 += kWSR) {
@@ -583,14 +706,23 @@ __global__ void __launch_bounds__(kWSThreads, 1) wx_dense_kernel(const WSDenseAr
       const Real* ur = st + rr * ROW + tk;
       const Real* vr = st + rr * ROW + UW + tk + ts;
       const Real L = lstage[buf * kWSR + rr];
-      Real win[16];
+      Real win[TI + 7];
 #pragma unroll
-      for (int q = 0; q < 15; ++q) win[q] = vr[16 * q];
+      for (int q = 0; q < TI + 7; ++q) win[q] = vr[16 * q];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
+      for (int i = 0; i < TI; ++i) {
         const Real u = ur[16 * i];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = fma(fabs(u - win[i + j]), L, acc[i][j]);
+        for (int j = 0; j < 8; ++j) {
+          if constexpr (GEN) {
+            Real ds, ts;
+            wx_gen_terms<Real, SQ>(u, win[i + j], L, alpha, ds, ts);
+            acc[i][j] += ds;
+            acct[i][j] += ts;
+          } else {
+            acc[i][j] = fma(fabs(u - win[i + j]), L, acc[i][j]);
+          }
+        }
       }
     }
     __syncthreads();
@@ -604,13 +736,21 @@ __global__ void __launch_bounds__(kWSThreads, 1) wx_dense_kernel(const WSDenseAr
     const int s = s0 + ts + 16 * j;
     if (s >= a.s_end) break;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < TI; ++i) {
       const int k = k0 + tk + 16 * i;
       if (k >= n) break;
       const int64_t o = static_cast<int64_t>(s - a.out_begin) * n + k;
       const double dv = static_cast<double>(acc[i][j]) + __ldcs(a.lightd + o);  // read once
       if (M == kWU) {
         __stcs(dist + o, static_cast<Real>(dv));
+        continue;
+      }
+      if constexpr (GEN) {
+        const Real tr = static_cast<Real>(static_cast<double>(acct[i][j]) + __ldcs(a.lightt + o));
+        Real dr = static_cast<Real>(dv);
+        if (a.finalize) dr = tr == Real(0) ? Real(0) : dr / tr;
+        __stcs(dist + o, dr);
+        __stcs(tot + o, tr);
         continue;
       }
       const int64_t li = static_cast<int64_t>(k) + s + 1;

@@ -97,12 +97,58 @@ def test_wsplit_wide_lengths(device_ok, monkeypatch):
         _assert_close(3, 8, False, t, wt, N.KERNEL_WSPLIT)
 
 
-def test_wsplit_rejects_generalized_and_unweighted(device_ok):
+def test_wsplit_rejects_unweighted(device_ok):
     inst = sf.random_instance(3, 10, 12, 0.3)
     problem = sf.flatten(inst.tree, inst.table)
     with pytest.raises(N.NativeError):
         _gpu_stripes(problem, 1, 8, 0, 5, N.KERNEL_WSPLIT)
-    ex, _keep = N.make_exec([0], N.KERNEL_WSPLIT, False, 0, 0.5)
-    d = np.zeros((5, 10))
-    t = np.zeros((5, 10))
-    assert N.lib().sf_compute_stripes(problem.ref, 4, 8, 0, 5, N.ptr(d), N.ptr(t), 1, C.byref(ex), None) != 0
+
+
+def _gen13(problem, alpha, prec, start, stop, monkeypatch, frac):
+    if frac is None:
+        monkeypatch.delenv("SF_WHEAVY_FRAC", raising=False)
+    else:
+        monkeypatch.setenv("SF_WHEAVY_FRAC", frac)
+    n = problem.n_samples
+    dt = np.float64 if prec == 8 else np.float32
+    d = np.full((stop - start, n), np.nan, dt)
+    t = np.full((stop - start, n), np.nan, dt)
+    ex, _keep = N.make_exec([0], N.KERNEL_WSPLIT, False, 0, alpha)
+    N.check(N.lib().sf_compute_stripes(problem.ref, N.SF_GENERALIZED, prec, start, stop, N.ptr(d), N.ptr(t), 1,
+                                       C.byref(ex), None))
+    return d, t
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("alpha", [0.0, 0.5, 1.0, 1.7])
+def test_wsplit_generalized_matches_oracle(device_ok, alpha, prec, monkeypatch):
+    """Generalized UniFrac (extension; parity unpinned: the reference has no
+    generalized metric) on the weighted split against the oracle's statement
+    of the published form: fp64 within 1e-12 relative (alpha = 0.5 through
+    rsqrt, other exponents through pow), fp32 within max(1e-5 |x|, 1e-6)."""
+    for seed, n, leaves, dens in [(81, 150, 500, 0.02), (82, 41, 120, 0.1), (83, 200, 900, 0.01)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        for start, stop in [(0, S), (S // 3, S)]:
+            wd, wt = op.compute_stripes_generalized(problem, alpha, prec, start, stop)
+            for frac in SPLITS:
+                d, t = _gen13(problem, alpha, prec, start, stop, monkeypatch, frac)
+                for got, want in ((d, wd), (t, wt)):
+                    if prec == 8:
+                        err = np.abs(got - want)
+                        assert np.all(err <= 1e-12 * np.abs(want)), f"alpha {alpha} frac {frac}: {err.max()}"
+                    else:
+                        w = want.astype(np.float64)
+                        assert np.all(np.abs(got.astype(np.float64) - w) <= np.maximum(1e-5 * np.abs(w), 1e-6))
+
+
+def test_wsplit_generalized_identical_samples_are_exactly_zero(device_ok, monkeypatch):
+    inst = sf.random_instance(65, 120, 400, 0.03)
+    table = _dup_table(inst, {7: 3, 100: 3, 61: 60})
+    problem = sf.flatten(inst.tree, table)
+    for frac in SPLITS:
+        d, _ = _gen13(problem, 0.5, 8, 0, 60, monkeypatch, frac)
+        dm = op.condense(8, 120, d)
+        for a, b in ((3, 7), (3, 100), (7, 100), (60, 61)):
+            assert dm[a, b] == 0.0 and dm[b, a] == 0.0

@@ -22,11 +22,11 @@ import bench  # noqa: E402
 from paper_2005_05826_b200 import _native as N  # noqa: E402
 
 
-def run(problem, metric, prec, kernel, reps, stripes):
+def run(problem, metric, prec, kernel, reps, stripes, alpha=1.0):
     L = N.lib()
     n = problem.n_samples
     S = stripes or n // 2
-    ex, _keep = N.make_exec([0], kernel)
+    ex, _keep = N.make_exec([0], kernel, alpha=alpha)
     plan = C.c_void_p()
     N.check(L.sf_plan_create(problem.ref, metric, prec, 0, S, C.byref(ex), C.byref(plan)))
     st = N.sf_stats()
@@ -61,13 +61,13 @@ def main():
     prec = {"fp64": 8, "fp32": 4}[args.prec or cfg["precision"]]
     base = None
     if not args.no_uwalk:
-        ms, _, st, d12, t12 = run(problem, metric, prec, 12, args.reps, args.stripes)
+        ms, _, st, d12, t12 = run(problem, metric, prec, 12, args.reps, args.stripes, cfg.get("alpha", 1.0))
         base = (d12, t12)
         print(json.dumps({"config": args.config, "kernel": 12, "prec": prec, "device_ms": round(ms, 3),
                           "fp64_ops": st.fp64_ops}), flush=True)
     for f in args.fracs.split(","):
         os.environ["SF_WHEAVY_FRAC"] = f
-        ms, dms, st, d, t = run(problem, metric, prec, 13, args.reps, args.stripes)
+        ms, dms, st, d, t = run(problem, metric, prec, 13, args.reps, args.stripes, cfg.get("alpha", 1.0))
         rec = {"config": args.config, "kernel": 13, "prec": prec, "heavy_frac": float(f), "device_ms": round(ms, 3),
                "dense_ms": round(dms, 3), "pipe_ops": st.fp64_ops, "updates_exec": st.updates_exec}
         if base is not None:
