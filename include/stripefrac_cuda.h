@@ -81,9 +81,9 @@ typedef struct sf_exec {
                                (bitwise: the reference's adds in its order), 10 = split heavy
                                walk + light scatter (exact fixed-point sums, correctly rounded;
                                the default); weighted only: 11 = present-row walk (bitwise in
-                               exact mode), 12 = u-walk (the SF_GENERALIZED default), 13 = weighted
-                               split: dense heavy rows + exact fixed-point light scatter (the
-                               WN / WU default; falls back to 12 without the memory for it) */
+                               exact mode), 12 = u-walk, 13 = weighted split: dense heavy rows +
+                               exact fixed-point light scatter (the default for WN / WU /
+                               SF_GENERALIZED; falls back to 12 without the memory for it) */
   int32_t flags;            /* bit 0: SF_EXEC_EXACT_NO_FMA: bitwise-identical results (weighted:
                                no FMA; unweighted auto: the sparse walk instead of kernel 10) */
   double alpha;             /* SF_GENERALIZED only: the exponent, finite, >= 0 (ABI v3) */

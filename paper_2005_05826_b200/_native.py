@@ -26,8 +26,8 @@ SF_EXEC_EXACT_NO_FMA = 1
 KERNEL_AUTO, KERNEL_DENSE, KERNEL_SPARSE = 0, 1, 2  # auto, dense tiled (every metric), bitwise union walk (UW)
 KERNEL_SPLIT = 10  # unweighted: heavy walk + light scatter, exact fixed-point sums (the default)
 KERNEL_WSPARSE = 11  # weighted metrics: present-row walk (bitwise; the exact-mode default)
-KERNEL_WUWALK = 12  # weighted metrics: warp-uniform u-walk + double-double remainder (generalized default)
-KERNEL_WSPLIT = 13  # WN/WU: dense heavy rows (FP64) + exact fixed-point light scatter (the default)
+KERNEL_WUWALK = 12  # weighted metrics: warp-uniform u-walk + double-double remainder
+KERNEL_WSPLIT = 13  # weighted / generalized: dense heavy rows (FP64) + exact fixed-point light scatter (the default)
 
 
 class sf_problem(C.Structure):

@@ -1493,10 +1493,12 @@ sf_status wuwalk_build(sf_plan* plan, DeviceState& d, int32_t r0, int32_t C, cud
   return SF_OK;
 }
 
-// Heavy threshold of kernel 13 as a fraction of n (SF_WHEAVY_FRAC).
-double ws_heavy_frac() {
+// Heavy threshold of kernel 13 as a fraction of n (SF_WHEAVY_FRAC): a dense
+// generalized term costs ~7x a weighted one (rsqrt or pow), so generalized
+// keeps fewer rows dense.
+double ws_heavy_frac(int metric) {
   const char* e = std::getenv("SF_WHEAVY_FRAC");
-  return e ? std::atof(e) : 0.25;
+  return e ? std::atof(e) : metric == SF_GENERALIZED ? 0.6 : 0.25;
 }
 
 // Kernel 13 (wsplit_kernels.cuh), after kernel 12's build of every chunk and
@@ -1534,7 +1536,7 @@ sf_status wsplit_run(sf_plan* plan, DeviceState& d, int32_t finalize, cudaStream
   const size_t tb = std::max(t1, std::max(t2, t3));
   if (d.ws_tmp.bytes < tb) SF_TRY(d.ws_tmp.alloc(d.dev, tb, "scan scratch"));
   wx_rowcount_kernel<<<std::min(W, 148 * 16), 256, 0, st>>>(nb, n_ext, n, W, E, d.ws_cnt.as<uint32_t>());
-  const uint32_t thr = static_cast<uint32_t>(std::max(1.0, std::ceil(ws_heavy_frac() * n)));
+  const uint32_t thr = static_cast<uint32_t>(std::max(1.0, std::ceil(ws_heavy_frac(plan->metric) * n)));
   wx_classify_kernel<<<grid_for(Wr, 256), 256, 0, st>>>(d.ws_cnt.as<uint32_t>(), d.lens_pad.as<double>(), E, W, thr,
                                                          d.ws_hflag.as<uint32_t>(), d.ws_lcnt.as<unsigned long long>(),
                                                          d.ws_hmask.as<uint32_t>(), d.ws_lmask.as<uint32_t>());
@@ -2479,10 +2481,9 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                       nodepacked_bytes(k, p->n_rows, n) <= static_cast<size_t>(ex->mem_budget_bytes);
     plan->kernel = fits ? k : 1;
   }
-  // auto, weighted: WN / WU the weighted split (kernel 13), generalized the
-  // u-walk (12); in exact mode the bitwise present-row walk (11)
-  if ((!ex || ex->kernel == 0) && metric != SF_UNWEIGHTED)
-    plan->kernel = plan->exact ? 11 : metric == SF_GENERALIZED ? 12 : 13;
+  // auto, weighted and generalized: the weighted split (kernel 13); in exact
+  // mode the bitwise present-row walk (11)
+  if ((!ex || ex->kernel == 0) && metric != SF_UNWEIGHTED) plan->kernel = plan->exact ? 11 : 13;
   if ((plan->kernel == 2 || plan->kernel == 10) && metric != SF_UNWEIGHTED)
     return fail(SF_EINVAL, "the sparse bit kernels implement the unweighted metric only");
   if (plan->kernel >= 11 && metric == SF_UNWEIGHTED)
