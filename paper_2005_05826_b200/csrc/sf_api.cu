@@ -586,7 +586,8 @@ struct DeviceState {
   // kernel 13: row counts / flags / scans, dense heavy rows, light member and
   // column lists, light column sums, the light part of every slot
   DevBuf ws_cnt, ws_hflag, ws_hidx, ws_lcnt, ws_lptr, ws_hmask, ws_lmask, ws_UH, ws_LH, ws_lmid, ws_lval,
-      ws_ccnt, ws_cptr, ws_crow, ws_cval, ws_AL, ws_lightd, ws_tmp, ws_prank, ws_crank, ws_lvala, ws_lightt;
+      ws_ccnt, ws_cptr, ws_crow, ws_cval, ws_AL, ws_lightd, ws_tmp, ws_prank, ws_crank, ws_lvala, ws_lightt,
+      ws_pool64;
   uint64_t host_fp64_ops = 0;  // FP64/FP32-pipe lane-ops counted on the host (kernel 13's dense part)
   DevBuf wnbo;               // kernel 12: combined (offset, presence word) cells
   int32_t light_pass = 0;  // stripes per light-sum pass (memory-bounded)
@@ -619,6 +620,9 @@ struct sf_plan {
   int metric = 0, prec = 0;
   int32_t n = 0, E = 0, start = 0, stop = 0;
   bool bits = false, exact = false;
+  // kernel 13: presence-bit embedding rows + a sparse value build (no dense
+  // value rows); SF_WS_DENSE_EMBED=1 keeps the chunked dense build (A/B)
+  bool wbits = false;
   size_t mem_budget = 0;  // sf_exec.mem_budget_bytes (0: none)
   double alpha = 1.0;  // generalized UniFrac exponent
   int kernel = 1;  // 1 dense, 2 sparse-bit walk, 10 split, 11 weighted present-row walk, 12 u-walk,
@@ -1729,6 +1733,58 @@ uint64_t present_bound(const sf_problem* p) {
 // Layout of one chunk's schedule arrays inside the packed device buffer.
 enum { kLeafRows, kLeafFeat, kIntRows, kCptr, kCodes, kCarrySrc, kCarryDst, kNumArr };
 
+// Kernel 13's sparse value build (wsplit_kernels.cuh): from the chunk's
+// presence bit rows (K1, every row in one chunk) to the presence words, pool
+// offsets and the value pool of the chunked build — without dense value rows.
+template <class Real, class Arr>
+sf_status wx_values_build(sf_plan* plan, DeviceState& d, const Chunk& c, Arr arr, cudaStream_t st) {
+  const int n = plan->n;
+  const int32_t E = plan->E;
+  const int32_t W = (E + 31) / 32;
+  const int64_t n_ext = sparse_n_ext(n);
+  const int64_t RW = plan->row_words;
+  const int64_t cells = static_cast<int64_t>(W) * n_ext;
+  uint32_t* nb = d.wnb.as<uint32_t>();
+  uint32_t* off = d.woff.as<uint32_t>();
+  wx_words_kernel<<<grid_for(cells, 256), 256, 0, st>>>(d.emb.as<uint32_t>(), RW, E, n, W, n_ext, nb,
+                                                         d.wcnt.as<uint32_t>());
+  size_t tmp = d.cub_bytes;
+  SF_CUDA(cub::DeviceScan::ExclusiveSum(d.cubtmp.p, tmp, d.wcnt.as<uint32_t>(), off, static_cast<int>(cells), st));
+  // the pool's size (fp32: the cast below)
+  wu_chunk_total_kernel<<<1, 1, 0, st>>>(off, d.wcnt.as<uint32_t>(), cells - 1, d.wbase.as<unsigned long long>());
+  ws_extend_kernel<<<grid_for(static_cast<int64_t>(W) * (n_ext - n), 256), 256, 0, st>>>(nb, off, n, W, n_ext);
+  double* pool64 = nullptr;
+  if (sizeof(Real) == 8) {
+    pool64 = d.wpool.as<double>();
+  } else {
+    const size_t need = d.wpool.bytes / sizeof(Real) * 8;
+    if (d.ws_pool64.bytes < need) SF_TRY(d.ws_pool64.alloc(d.dev, need, "fp64 value pool"));
+    pool64 = d.ws_pool64.as<double>();
+  }
+  const int nl = static_cast<int>(c.leaf_rows.size());
+  if (nl > 0)
+    wx_leaf_values_kernel<<<grid_for(static_cast<int64_t>(nl) * 32, 256), 256, 0, st>>>(
+        pool64, nb, off, n_ext, arr(kLeafRows), arr(kLeafFeat), nl, d.feat_ptr.as<int64_t>(), d.sidx.as<int32_t>(),
+        d.counts.as<double>(), d.totals.as<double>());
+  for (size_t h = 0; h + 1 < c.lvl_ptr.size(); ++h) {
+    const int lo = c.lvl_ptr[h], hi = c.lvl_ptr[h + 1];
+    if (hi <= lo) continue;
+    wx_level_values_kernel<<<grid_for(static_cast<int64_t>(hi - lo) * RW, 256), 256, 0, st>>>(
+        pool64, d.emb.as<uint32_t>(), RW, nb, off, n_ext, arr(kIntRows) + lo, arr(kCptr) + lo, arr(kCodes), hi - lo);
+    d.launches++;
+  }
+  if (sizeof(Real) == 4)
+    wx_pool_to_float_kernel<<<grid_for(static_cast<int64_t>(d.wpool.bytes / sizeof(Real)), 256), 256, 0, st>>>(
+        pool64, d.wbase.as<unsigned long long>(), d.wpool.as<float>());
+  if (plan->metric == SF_GENERALIZED && d.wpoola.p)  // the u-walk fallback's second pool
+    wx_poola_kernel<Real><<<grid_for(static_cast<int64_t>(W) * n, 256), 256, 0, st>>>(
+        nb, off, n_ext, n, W, d.lens_pad.as<double>(), plan->alpha, d.wpool.as<Real>(), d.wpoola.as<Real>());
+  SF_CUDA(cudaGetLastError());
+  d.launches += 6;
+  return SF_OK;
+}
+
+
 sf_status upload_schedule(DeviceState& d, const Schedule& s) {
   std::vector<int32_t> packed;
   d.sched_off.clear();
@@ -1782,15 +1838,17 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
   SF_CUDA(cudaMemsetAsync(d.exec_ctr.p, 0, 2 * sizeof(unsigned long long), st));
 
   const int64_t stride = plan->row_words;
-  const int ncols = static_cast<int>(plan->bits ? (n + 31) / 32 : n);
+  const int ncols = static_cast<int>((plan->bits || plan->wbits) ? (n + 31) / 32 : n);
   const int32_t* base = d.sched.as<int32_t>();
   for (size_t ci = 0; ci < plan->sched.chunks.size(); ++ci) {
     const Chunk& c = plan->sched.chunks[ci];
     auto arr = [&](int k) { return base + d.sched_off[ci * kNumArr + static_cast<size_t>(k)]; };
     const int C = c.r1 - c.r0;
     SF_CUDA(cudaEventRecord(d.events[1 + 3 * ci], st));
-    // ---- K1: embedding rows of this chunk
-    const size_t row_bytes = static_cast<size_t>(stride) * (plan->bits ? 4 : 8);
+    // ---- K1: embedding rows of this chunk (bit rows: unweighted presence, or
+    // the weighted rows' presence for the sparse value build)
+    const bool bitrows = plan->bits || plan->wbits;
+    const size_t row_bytes = static_cast<size_t>(stride) * (bitrows ? 4 : 8);
     SF_CUDA(cudaMemsetAsync(d.emb.p, 0, row_bytes * static_cast<size_t>(C), st));
     const int nl = static_cast<int>(c.leaf_rows.size());
     if (nl > 0) {
@@ -1799,6 +1857,10 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
         embed_leaf_bits<<<blocks, 256, 0, st>>>(d.emb.as<uint32_t>(), stride, arr(kLeafRows),
                                                 arr(kLeafFeat), nl, d.feat_ptr.as<int64_t>(),
                                                 d.sidx.as<int32_t>(), d.counts.as<double>());
+      else if (plan->wbits)
+        wx_leaf_bits_kernel<<<blocks, 256, 0, st>>>(d.emb.as<uint32_t>(), stride, arr(kLeafRows), arr(kLeafFeat),
+                                                    nl, d.feat_ptr.as<int64_t>(), d.sidx.as<int32_t>(),
+                                                    d.counts.as<double>(), d.totals.as<double>());
       else
         embed_leaf_values<<<blocks, 256, 0, st>>>(d.emb.as<double>(), stride, arr(kLeafRows),
                                                   arr(kLeafFeat), nl, d.feat_ptr.as<int64_t>(),
@@ -1811,7 +1873,7 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       const int lo = c.lvl_ptr[h], hi = c.lvl_ptr[h + 1];
       if (hi <= lo) continue;
       const dim3 grid((ncols + 127) / 128, std::min(hi - lo, 65535));
-      if (plan->bits)
+      if (bitrows)
         embed_level_bits<<<grid, 128, 0, st>>>(d.emb.as<uint32_t>(), stride, d.pend.as<uint32_t>(),
                                                arr(kIntRows) + lo, arr(kCptr) + lo, arr(kCodes),
                                                hi - lo, ncols);
@@ -1822,7 +1884,10 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
       SF_CUDA(cudaGetLastError());
       d.launches++;
     }
-    if (plan->kernel == 12 || plan->kernel == 13) {
+    if (plan->wbits) {
+      SF_TRY(plan->prec == SF_FP64 ? wx_values_build<double>(plan, d, c, arr, st)
+                                   : wx_values_build<float>(plan, d, c, arr, st));
+    } else if (plan->kernel == 12 || plan->kernel == 13) {
       if (ci == 0) SF_CUDA(cudaMemsetAsync(d.wbase.p, 0, 16, st));
       SF_TRY(wuwalk_build(plan, d, c.r0, C, st));
     } else if (plan->kernel == 11) {
@@ -2509,7 +2574,11 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     const int term_bits = (lmax > 0 ? std::ilogb(3.0 * lmax * f) + 2 : 1) + plan->ws_G + 1;
     plan->ws_nd = std::min(8, std::max(4, (term_bits + 15) / 16));
   }
-  plan->row_words = plan->bits ? (n + 31) / 32 : ((n + 1) / 2) * 2;
+  {
+    const char* de = std::getenv("SF_WS_DENSE_EMBED");
+    plan->wbits = plan->kernel == 13 && !(de && std::atoi(de) == 1);
+  }
+  plan->row_words = (plan->bits || plan->wbits) ? (n + 31) / 32 : ((n + 1) / 2) * 2;
   const size_t w = prec == SF_FP64 ? 8 : 4;
   const bool has_t = metric != SF_WEIGHTED_UNNORMALIZED;
 
@@ -2527,7 +2596,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   }
 
   // chunk capacity from the smallest device budget
-  const size_t row_bytes = static_cast<size_t>(plan->row_words) * (plan->bits ? 4 : 8);
+  const size_t row_bytes = static_cast<size_t>(plan->row_words) * ((plan->bits || plan->wbits) ? 4 : 8);
   // kernel 11 holds, per chunk row, the dense row + its share of the value
   // pool (worst case n values) + presence words / counts / offsets
   const size_t wsp_row_bytes =
@@ -2544,7 +2613,7 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   // the resident sparse bit kernels (2-10) take every row in one chunk
   // whatever the budget, so they skip the free-memory query here (it took
   // 28-64 ms on some calls); kernel 10 sizes its light pass at device setup
-  const bool budget_free = plan->kernel >= 2 && !wsp;
+  const bool budget_free = (plan->kernel >= 2 && !wsp) || plan->wbits;
   for (auto& d : plan->devs) {
     if (budget_free) break;
     SF_CUDA(cudaSetDevice(d->dev));
@@ -2623,13 +2692,14 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     if (cmax < plan->E) cmax = cmax / 32 * 32;
     if (cmax < 32) cmax = std::min<int64_t>(32, plan->E);
   }
+  if (plan->wbits) cmax = plan->E;  // bit rows: every row in one chunk
   cmax = std::min<int64_t>(cmax, plan->E);
   if (cmax < 1) return fail(SF_ENOMEM, "not enough device memory for one embedding row");
   for (;;) {
     plan->sched = build_schedule(p, static_cast<int32_t>(cmax));
     const size_t need = (static_cast<size_t>(cmax) + static_cast<size_t>(plan->sched.n_pending)) * row_bytes +
                         static_cast<size_t>(cmax) * wsp_row_bytes;
-    if (need <= budget || cmax == 1 || (plan->kernel >= 2 && !wsp) || (wsp && cmax <= 32)) break;
+    if (need <= budget || cmax == 1 || (plan->kernel >= 2 && !wsp) || (wsp && cmax <= 32) || plan->wbits) break;
     cmax = std::max<int64_t>(1, cmax * 3 / 4);
     if (wsp) cmax = std::max<int64_t>(32, cmax / 32 * 32);
   }
@@ -3000,6 +3070,7 @@ sf_status sf_embed_rows(const sf_problem* p, int32_t weighted, int32_t r0, int32
   sf_plan* raw = nullptr;
   const sf_metric m = weighted ? SF_WEIGHTED_UNNORMALIZED : SF_UNWEIGHTED;
   ex.mem_budget_bytes = 0;
+  ex.kernel = weighted ? 12 : 0;  // dense value rows (kernel 13 keeps presence bits only)
   SF_TRY(sf_plan_create(p, m, SF_FP64, 0, 1, &ex, &raw));
   std::unique_ptr<sf_plan> plan(raw);
   if (plan->sched.chunks.size() != 1)

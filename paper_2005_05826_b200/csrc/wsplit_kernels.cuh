@@ -95,6 +95,144 @@ __device__ __forceinline__ void wx_gen_terms(Real u, Real v, Real L, Real alpha,
 
 // ---- build --------------------------------------------------------------------
 
+// ---- sparse value build (no dense embedding rows) ---------------------------------
+// The weighted rows are built from presence bits and the value pool alone:
+// 1. presence bit rows [E][RW] (leaves: value != 0, internal: OR of the
+//    children — exactly the rows whose dense value is nonzero);
+// 2. presence words nb[w][c] (32 rows) + counts, scanned into pool offsets;
+// 3. leaf values c / total[s] straight into the pool (table.cpp:208-214);
+// 4. internal values, one launch per tree height: 0 + the present children's
+//    values in postorder (a child absent from the column adds +0.0 in the
+//    reference's fold, embed.cpp:71-79, so skipping it changes no bit).
+// The pool, offsets and words are the chunked build's, bit for bit.
+
+// Weighted leaf presence: the value c / total[s] is nonzero.
+__global__ void wx_leaf_bits_kernel(uint32_t* __restrict__ bits, int64_t RW, const int32_t* __restrict__ leaf_rows,
+                                    const int32_t* __restrict__ leaf_feat, int32_t n_leaf,
+                                    const int64_t* __restrict__ feat_ptr, const int32_t* __restrict__ sidx,
+                                    const double* __restrict__ counts, const double* __restrict__ totals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_leaf; i += nwarps) {
+    uint32_t* row = bits + static_cast<int64_t>(leaf_rows[i]) * RW;
+    const int f = leaf_feat[i];
+    for (int64_t e = feat_ptr[f] + lane; e < feat_ptr[f + 1]; e += 32) {
+      const int s = sidx[e];
+      if (counts[e] / totals[s] != 0.0) atomicOr(row + (s >> 5), 1u << (s & 31));
+    }
+  }
+}
+
+// Presence words (row 32w + i at bit 31 - i) and their counts; columns past
+// n count 0 (their words are copied in by ws_extend_kernel after the scan).
+__global__ void wx_words_kernel(const uint32_t* __restrict__ bits, int64_t RW, int32_t E, int32_t n, int32_t W,
+                                int64_t n_ext, uint32_t* __restrict__ nb, uint32_t* __restrict__ cnt) {
+  const int64_t total = static_cast<int64_t>(W) * n_ext;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = i / n_ext;
+    const int64_t c = i - w * n_ext;
+    uint32_t x = 0u;
+    if (c < n) {
+      const int r_end = min(32, E - static_cast<int>(32 * w));
+      const uint32_t* col = bits + 32 * w * RW + (c >> 5);
+      const int b = static_cast<int>(c & 31);
+      for (int r = 0; r < r_end; ++r)
+        if ((__ldg(col + static_cast<int64_t>(r) * RW) >> b) & 1u) x |= 0x80000000u >> r;
+    }
+    nb[i] = x;
+    cnt[i] = static_cast<uint32_t>(__popc(x));
+  }
+}
+
+// Pool index of (row r, column c), r present in c.
+__device__ __forceinline__ uint32_t wx_pos(const uint32_t* __restrict__ nb, const uint32_t* __restrict__ off,
+                                           int64_t n_ext, int32_t r, int32_t c) {
+  const int64_t cell = static_cast<int64_t>(r >> 5) * n_ext + c;
+  const int i = r & 31;
+  return __ldg(off + cell) + static_cast<uint32_t>(__popc(__ldg(nb + cell) & ~(0xffffffffu >> i)));
+}
+
+// Leaf values into the pool: warp per leaf row (embed_leaf_values' formula).
+__global__ void wx_leaf_values_kernel(double* __restrict__ pool, const uint32_t* __restrict__ nb,
+                                      const uint32_t* __restrict__ off, int64_t n_ext,
+                                      const int32_t* __restrict__ leaf_rows, const int32_t* __restrict__ leaf_feat,
+                                      int32_t n_leaf, const int64_t* __restrict__ feat_ptr,
+                                      const int32_t* __restrict__ sidx, const double* __restrict__ counts,
+                                      const double* __restrict__ totals) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_leaf; i += nwarps) {
+    const int32_t r = leaf_rows[i];
+    const int f = leaf_feat[i];
+    for (int64_t e = feat_ptr[f] + lane; e < feat_ptr[f + 1]; e += 32) {
+      const int s = sidx[e];
+      const double v = counts[e] / totals[s];
+      if (v != 0.0) pool[wx_pos(nb, off, n_ext, r, s)] = v;
+    }
+  }
+}
+
+// Internal rows of one height: thread per (row, 32-column word); per present
+// column, 0 + the present children's values in postorder (codes: child rows).
+__global__ void wx_level_values_kernel(double* __restrict__ pool, const uint32_t* __restrict__ bits, int64_t RW,
+                                       const uint32_t* __restrict__ nb, const uint32_t* __restrict__ off,
+                                       int64_t n_ext, const int32_t* __restrict__ rows,
+                                       const int32_t* __restrict__ cptr, const int32_t* __restrict__ codes,
+                                       int32_t n_rows) {
+  const int64_t total = static_cast<int64_t>(n_rows) * RW;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t i = t / RW;
+    const int64_t cw = t - i * RW;
+    const int32_t r = rows[i];
+    uint32_t b = __ldg(bits + static_cast<int64_t>(r) * RW + cw);
+    while (b) {
+      const int j = __ffs(b) - 1;
+      b &= b - 1u;
+      const int32_t c = static_cast<int32_t>(32 * cw + j);
+      double acc = 0.0;  // pending_ starts at zero (embed.cpp:75-76)
+      for (int k = cptr[i]; k < cptr[i + 1]; ++k) {
+        const int32_t ch = codes[k];
+        if ((__ldg(bits + static_cast<int64_t>(ch) * RW + cw) >> j) & 1u) acc += pool[wx_pos(nb, off, n_ext, ch, c)];
+      }
+      pool[wx_pos(nb, off, n_ext, r, c)] = acc;
+    }
+  }
+}
+
+// Generalized: the u-walk's second pool (kernel 12's fallback), a = v^alpha L
+// per present entry in pool order (wu_fill_kernel's formula).
+template <class Real>
+__global__ void wx_poola_kernel(const uint32_t* __restrict__ nb, const uint32_t* __restrict__ off, int64_t n_ext,
+                                int32_t n, int32_t W, const double* __restrict__ lens, double alpha,
+                                const Real* __restrict__ pool, Real* __restrict__ poola) {
+  const int64_t total = static_cast<int64_t>(W) * n;
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t w = t / n;
+    const int64_t c = t - w * n;
+    uint32_t bits = nb[w * n_ext + c];
+    uint32_t q = off[w * n_ext + c];
+    while (bits) {
+      const int r = __clz(bits);
+      bits ^= 0x80000000u >> r;
+      poola[q] = pow_alpha(pool[q], static_cast<Real>(alpha)) * static_cast<Real>(lens[32 * w + r]);
+      ++q;
+    }
+  }
+}
+
+__global__ void wx_pool_to_float_kernel(const double* __restrict__ p64, const unsigned long long* __restrict__ total,
+                                        float* __restrict__ p32) {
+  const unsigned long long m = *total;
+  for (unsigned long long i = static_cast<unsigned long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<unsigned long long>(gridDim.x) * blockDim.x)
+    p32[i] = static_cast<float>(p64[i]);  // cast_batch: the fp64 row rounded once (embed.hpp:71-84)
+}
+
 // m_r: samples with row r present (presence words nb[w][c], row 32w+i at bit 31-i).
 __global__ void wx_rowcount_kernel(const uint32_t* __restrict__ nb, int64_t n_ext, int32_t n, int32_t W,
                                    int32_t E, uint32_t* __restrict__ cnt) {

@@ -152,3 +152,26 @@ def test_wsplit_generalized_identical_samples_are_exactly_zero(device_ok, monkey
         dm = op.condense(8, 120, d)
         for a, b in ((3, 7), (3, 100), (7, 100), (60, 61)):
             assert dm[a, b] == 0.0 and dm[b, a] == 0.0
+
+
+@pytest.mark.parametrize("prec", [8, 4])
+@pytest.mark.parametrize("metric", [2, 3, 4])
+def test_wsplit_sparse_value_build_is_bitwise_the_dense_build(device_ok, metric, prec, monkeypatch):
+    """The sparse value build (presence bit rows + pool values, no dense
+    embedding rows) gives the chunked dense build's pool bit for bit, so the
+    stripes are identical (SF_WS_DENSE_EMBED=1: the dense build)."""
+    for seed, n, leaves, dens in [(91, 200, 700, 0.01), (92, 97, 300, 0.05), (93, 64, 64, 0.3)]:
+        inst = sf.random_instance(seed, n, leaves, dens)
+        problem = sf.flatten(inst.tree, inst.table)
+        S = n // 2
+        out = []
+        for dense in ("0", "1"):
+            monkeypatch.setenv("SF_WS_DENSE_EMBED", dense)
+            if metric == 4:
+                out.append(_gen13(problem, 0.5, prec, 0, S, monkeypatch, None))
+            else:
+                out.append(_run(problem, metric, prec, 0, S, monkeypatch, None)[:2])
+        monkeypatch.delenv("SF_WS_DENSE_EMBED")
+        assert np.array_equal(out[0][0], out[1][0])
+        if out[0][1] is not None:
+            assert np.array_equal(out[0][1], out[1][1])
