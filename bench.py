@@ -442,9 +442,10 @@ def roofline_record(args, cfg, metric, prec, device, world, stop_all, E, n, str_
             "bound": "tensor", "achieved": round(achieved, 1), "peak": round(pk["tops"], 1),
             "unit": "TFLOP/s", "unit_note": "int8 tensor-core ops (MAC = 2), exact integer accumulation",
             "frac": round(achieved / pk["tops"], 4),
-            "traffic": (round(tr["dram_bytes"] / tr["stripes"] * (stop_all / max(world, 1))) if tr else None),
-            "traffic_unit": "DRAM bytes per step (all heavy GEMM launches)",
-            "traffic_source": (f"{tr['source']} ({tr['stripes']} stripes, scaled per stripe)" if tr else None),
+            "traffic": (round(tr["dram_bytes"] / tr["launches"]) if tr else None),
+            "traffic_unit": "DRAM bytes per heavy GEMM launch (dram__bytes_read.sum + dram__bytes_write.sum)",
+            "traffic_source": (f"{tr['source']} ({tr['launches']} launches of the {tr['stripes']}-stripe run)"
+                               if tr else None),
             "kernel": "heavy-row int8 digit-plane GEMMs (cuBLASLt IMMA, tcgen05) of the split path",
             "peak_source": (f"cuBLASLt int8 GEMM {pk['shape']} measured live on this device (best of 5)"
                             + (f"; MEASURED_PEAKS bf16 {bf16} TF/s x2 = {2 * bf16:.0f} for reference" if bf16 else "")),

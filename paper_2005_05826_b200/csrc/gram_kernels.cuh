@@ -127,6 +127,7 @@ struct GramArgs {
   const int32_t* C;                  // [W][M] column-major GEMM output, M = bk * nd
   const int32_t* dj;                 // digit index of each plane, nd entries
   int32_t nd, bk, k0;                // planes, block columns, first column
+  int32_t dj0;                       // first digit when the planes are consecutive, else -1
   int32_t c0, c1;                    // stripes of this launch
   int64_t M;
   int32_t n;
@@ -144,15 +145,21 @@ struct GramArgs {
 
 // Slots (s, k), s in [c0, c1), k in [k0, k0 + bk): G = heavy (tensor) +
 // light, then t = p_k + p_l + C - G and d = x_k + x_l - 2 G in exact
-// integers, rounded once (finalize: d / t, 0/0 -> 0).
-template <class Real>
+// integers, rounded once (finalize: d / t, 0/0 -> 0). LO, VB > 0: the
+// limb split and level width as compile-time constants (lo_bits = 32,
+// vb = 63 whenever E < 2^21): the 128/192-bit shifts by them become moves.
+template <class Real, int LO, int VB>
 __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
+  const int lo_bits = LO > 0 ? LO : a.lo_bits;
+  const int vb = VB > 0 ? VB : a.vb;
   const int n = a.n;
   const int kcount = min(a.bk, n - a.k0);
   const int64_t total = static_cast<int64_t>(a.c1 - a.c0) * kcount;
   const unsigned long long* xs = a.colsum;
-  const __int128 Cd = (static_cast<__int128>(a.cacc[0]) << a.lo_bits) + static_cast<__int128>(a.cacc[1]);
-  const unsigned long long lo_mask = (1ull << a.lo_bits) - 1ull;
+  const __int128 Cd = (static_cast<__int128>(a.cacc[0]) << lo_bits) + static_cast<__int128>(a.cacc[1]);
+  const __int128 C1 = a.levels == 2 ? (static_cast<__int128>(a.dcacc[0]) << lo_bits) + static_cast<__int128>(a.dcacc[1])
+                                    : __int128(0);
+  const unsigned long long lo_mask = (1ull << lo_bits) - 1ull;
   Real* dist = static_cast<Real*>(a.dist);
   Real* tot = static_cast<Real*>(a.tot);
   for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
@@ -165,7 +172,7 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
     if (l >= n) l -= n;
     const int32_t* cp = a.C + static_cast<int64_t>(kk + ds) * a.M + static_cast<int64_t>(kk) * a.nd;
     __int128 G = 0;
-    if (a.nd == 8 && a.dj[0] == 0 && a.dj[7] == 7) {
+    if (a.nd == 8 && a.dj0 == 0) {
       // planes 0..7: the slot's 32 bytes as two 16-byte loads, combined
       // Horner-style from the top digit (no per-plane 128-bit shifts)
       const int4 lo = __ldg(reinterpret_cast<const int4*>(cp));
@@ -173,6 +180,13 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
       const int32_t c8[8] = {lo.x, lo.y, lo.z, lo.w, hi.x, hi.y, hi.z, hi.w};
 #pragma unroll
       for (int jj = 7; jj >= 0; --jj) G = G * 256 + static_cast<__int128>(c8[jj]);
+    } else if (a.dj0 >= 0) {
+      // consecutive planes dj0 .. dj0 + nd - 1 (C3: 1..7): Horner from the
+      // top plane, one 128-bit shift by 8 dj0 at the end
+#pragma unroll
+      for (int jj = kMaxDigits - 1; jj >= 0; --jj)
+        if (jj < a.nd) G = G * 256 + static_cast<__int128>(__ldg(cp + jj));
+      G <<= 8 * a.dj0;
     } else {
       for (int jj = 0; jj < a.nd; ++jj) G += static_cast<__int128>(cp[jj]) * (static_cast<__int128>(1) << (8 * a.dj[jj]));
     }
@@ -184,30 +198,29 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
 #else
     const ulonglong2 light = reinterpret_cast<const ulonglong2*>(a.gl)[cell];
 #endif
-    G += (static_cast<__int128>(light.x) << a.lo_bits) + static_cast<__int128>(light.y);
+    G += (static_cast<__int128>(light.x) << lo_bits) + static_cast<__int128>(light.y);
     if (a.levels > 2) {  // sp_deep_epilogue_kernel finishes the slot from (hi, lo)
       reinterpret_cast<longlong2*>(a.gl)[cell] =
-          make_longlong2(static_cast<long long>(G >> a.lo_bits), static_cast<long long>(G & lo_mask));
+          make_longlong2(static_cast<long long>(G >> lo_bits), static_cast<long long>(G & lo_mask));
       continue;
     }
-    const __int128 P = (static_cast<__int128>(xs[2 * n + k] + xs[2 * n + l]) << a.lo_bits) +
+    const __int128 P = (static_cast<__int128>(xs[2 * n + k] + xs[2 * n + l]) << lo_bits) +
                        static_cast<__int128>(xs[3 * n + k] + xs[3 * n + l]);
-    const __int128 X = (static_cast<__int128>(xs[k] + xs[l]) << a.lo_bits) +
+    const __int128 X = (static_cast<__int128>(xs[k] + xs[l]) << lo_bits) +
                        static_cast<__int128>(xs[n + k] + xs[n + l]);
     Real tv, dv;
     if (a.levels == 2) {  // lengths off the main grid: the second level, exact, fused
       const unsigned long long* ys = a.dcolsum;
       const ulonglong2 G1l = reinterpret_cast<const ulonglong2*>(a.dacc)[cell];
-      const __int128 G1 = (static_cast<__int128>(G1l.x) << a.lo_bits) + static_cast<__int128>(G1l.y);
-      const __int128 P1 = (static_cast<__int128>(ys[2 * n + k] + ys[2 * n + l]) << a.lo_bits) +
+      const __int128 G1 = (static_cast<__int128>(G1l.x) << lo_bits) + static_cast<__int128>(G1l.y);
+      const __int128 P1 = (static_cast<__int128>(ys[2 * n + k] + ys[2 * n + l]) << lo_bits) +
                           static_cast<__int128>(ys[3 * n + k] + ys[3 * n + l]);
-      const __int128 X1 = (static_cast<__int128>(ys[k] + ys[l]) << a.lo_bits) +
+      const __int128 X1 = (static_cast<__int128>(ys[k] + ys[l]) << lo_bits) +
                           static_cast<__int128>(ys[n + k] + ys[n + l]);
-      const __int128 C1 = (static_cast<__int128>(a.dcacc[0]) << a.lo_bits) + static_cast<__int128>(a.dcacc[1]);
       tv = two_levels_to_real<Real>(static_cast<unsigned __int128>(P + Cd - G),
-                                    static_cast<unsigned __int128>(P1 + C1 - G1), a.vb, a.scale);
+                                    static_cast<unsigned __int128>(P1 + C1 - G1), vb, a.scale);
       dv = two_levels_to_real<Real>(static_cast<unsigned __int128>(X - 2 * G),
-                                    static_cast<unsigned __int128>(X1 - 2 * G1), a.vb, a.scale);
+                                    static_cast<unsigned __int128>(X1 - 2 * G1), vb, a.scale);
     } else {
       tv = fixed_to_real<Real>(P + Cd - G, a.scale);
       dv = fixed_to_real<Real>(X - 2 * G, a.scale);

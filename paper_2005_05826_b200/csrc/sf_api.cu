@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <array>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -256,7 +257,13 @@ sf_status usable_devices(const sf_exec* ex, std::vector<int>& out) {
 }
 
 // ------------------------------------------------------------ validation
-sf_status validate_problem(const sf_problem* p) {
+sf_status validate_table(const sf_problem* p);
+
+// The tree part (rows, parents, lengths, leaf features) and the table part
+// (CSR, counts, totals) of the problem; sf_plan_create starts the embedding
+// schedule (which reads only the tree) between the two.
+sf_status validate_problem(const sf_problem* p);
+sf_status validate_tree(const sf_problem* p) {
   if (!p) return fail(SF_EINVAL, "problem is null");
   if (p->n_samples < 2)
     return fail(SF_EINVAL, "need at least 2 samples, got " + std::to_string(p->n_samples));
@@ -285,6 +292,15 @@ sf_status validate_problem(const sf_problem* p) {
       return fail(SF_EINVAL, "row " + std::to_string(r) +
                                  (leaf ? " is a leaf with children" : " is an internal row without children"));
   }
+  return SF_OK;
+}
+
+sf_status validate_problem(const sf_problem* p) {
+  SF_TRY(validate_tree(p));
+  return validate_table(p);
+}
+
+sf_status validate_table(const sf_problem* p) {
   if (p->feat_ptr[0] != 0) return fail(SF_EINVAL, "feat_ptr[0] must be 0");
   for (int f = 0; f < p->n_features; ++f)
     if (p->feat_ptr[f + 1] < p->feat_ptr[f]) return fail(SF_EINVAL, "feat_ptr is not monotone");
@@ -361,10 +377,101 @@ struct Schedule {
   int32_t cmax = 0;
 };
 
+// Single-chunk schedule (every row resident: the split, weighted-split and
+// sparse walk paths): the same arrays as the general loop below, built with
+// branch-free passes (leaf / internal rows interleave unpredictably in
+// postorder), a counting sort by height and a threaded gather of the
+// children codes.
+Schedule build_schedule_single(const sf_problem* p) {
+  const int E = p->n_rows;
+  const int32_t* par = p->parent_row;
+  const int32_t* lf = p->leaf_feature;
+  std::vector<int32_t> height(static_cast<size_t>(E), 0), kptr(static_cast<size_t>(E) + 1, 0);
+  int32_t nleaf = 0, hall = 0;
+  for (int r = 0; r < E; ++r) {
+    const int q = par[r];
+    nleaf += lf[r] >= 0;
+    if (q >= 0) {
+      const int32_t h = height[static_cast<size_t>(r)] + 1;
+      int32_t& hq = height[static_cast<size_t>(q)];
+      hq = hq > h ? hq : h;
+      hall = hall > h ? hall : h;
+      ++kptr[static_cast<size_t>(q) + 1];
+    }
+  }
+  for (int r = 0; r < E; ++r) kptr[static_cast<size_t>(r) + 1] += kptr[static_cast<size_t>(r)];
+  std::vector<int32_t> kids(static_cast<size_t>(kptr[static_cast<size_t>(E)]));
+  {
+    std::vector<int32_t> at(kptr.begin(), kptr.end() - 1);
+    for (int r = 0; r < E; ++r)  // ascending r: children in postorder = fold order
+      if (par[r] >= 0) kids[static_cast<size_t>(at[static_cast<size_t>(par[r])]++)] = r;
+  }
+  Schedule sch;
+  sch.cmax = E;
+  sch.chunks.emplace_back();
+  Chunk& c = sch.chunks.back();
+  c.r0 = 0;
+  c.r1 = E;
+  c.leaf_rows.resize(static_cast<size_t>(nleaf) + 1);
+  c.leaf_feat.resize(static_cast<size_t>(nleaf) + 1);
+  int32_t hmax = 0;
+  std::vector<int32_t> cnt(static_cast<size_t>(hall) + 2, 0);  // internal rows per height
+  {
+    int32_t j = 0;
+    for (int r = 0; r < E; ++r) {  // branch-free compaction of the leaf rows
+      const int32_t f = lf[r];
+      c.leaf_rows[static_cast<size_t>(j)] = r;
+      c.leaf_feat[static_cast<size_t>(j)] = f;
+      j += f >= 0;
+      const int32_t h = f >= 0 ? 0 : height[static_cast<size_t>(r)];
+      hmax = hmax > h ? hmax : h;
+      ++cnt[static_cast<size_t>(h) + 1];
+    }
+    c.leaf_rows.resize(static_cast<size_t>(nleaf));
+    c.leaf_feat.resize(static_cast<size_t>(nleaf));
+  }
+  // internal rows by height, ascending rows within a height (stable)
+  cnt[1] = 0;  // leaves (height 0) are not internal rows
+  c.lvl_ptr.assign(1, 0);
+  for (int h = 1; h <= hmax; ++h) {
+    cnt[static_cast<size_t>(h) + 1] += cnt[static_cast<size_t>(h)];
+    c.lvl_ptr.push_back(cnt[static_cast<size_t>(h) + 1]);
+  }
+  c.int_rows.resize(static_cast<size_t>(c.lvl_ptr.back()));
+  for (int r = 0; r < E; ++r)
+    if (lf[r] < 0) c.int_rows[static_cast<size_t>(cnt[static_cast<size_t>(height[static_cast<size_t>(r)])]++)] = r;
+  // children codes in int_rows order (all chunk-relative: one chunk)
+  const size_t NI = c.int_rows.size();
+  c.cptr.resize(NI + 1);
+  c.cptr[0] = 0;
+  for (size_t i = 0; i < NI; ++i) {
+    const int r = c.int_rows[i];
+    c.cptr[i + 1] = c.cptr[i] + (kptr[static_cast<size_t>(r) + 1] - kptr[static_cast<size_t>(r)]);
+  }
+  c.codes.resize(static_cast<size_t>(c.cptr[NI]));
+  auto gather = [&](size_t i0, size_t i1) {
+    for (size_t i = i0; i < i1; ++i) {
+      const int r = c.int_rows[i];
+      std::copy(kids.begin() + kptr[static_cast<size_t>(r)], kids.begin() + kptr[static_cast<size_t>(r) + 1],
+                c.codes.begin() + c.cptr[i]);
+    }
+  };
+  const unsigned T = NI > (1u << 16) ? std::max(1u, std::min(8u, std::thread::hardware_concurrency())) : 1u;
+  if (T > 1) {
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < T; ++t) pool.emplace_back(gather, NI * t / T, NI * (t + 1) / T);
+    for (auto& th : pool) th.join();
+  } else {
+    gather(0, NI);
+  }
+  return sch;
+}
+
 // Postorder rows in chunks of <= cmax rows. Internal rows are grouped by
 // height (children strictly lower), rows whose parent is in a later chunk
 // are carried to pending slots, slots are recycled once consumed.
 Schedule build_schedule(const sf_problem* p, int32_t cmax) {
+  if (cmax >= p->n_rows) return build_schedule_single(p);
   const int E = p->n_rows;
   std::vector<int32_t> height(static_cast<size_t>(E), 0);
   std::vector<int32_t> kptr(static_cast<size_t>(E) + 1, 0), kids;
@@ -570,7 +677,7 @@ struct DeviceState {
   DevBuf gbits, growdig, gmask, gdj, gA, gC, gws;
   int64_t gram_kp = 0, gram_kpmax = 0;  // heavy rows (padded), digit-plane stride
   int64_t gram_h = 0;                   // heavy rows
-  int32_t gram_nd = 0;
+  int32_t gram_nd = 0, gram_dj0 = 0;
   cublasLtHandle_t lt = nullptr;
   cublasLtMatmulDesc_t lt_op = nullptr;
   cublasLtMatrixLayout_t lt_a = nullptr, lt_b = nullptr, lt_c = nullptr;
@@ -689,7 +796,9 @@ struct SplitCfg {
 // profiles/r02_heavyfrac_c3_col3.jsonl); beyond, the size-aware form of
 // round 1 (light pairs grow as x^2 and spread over more columns).
 int split_heavy_min(int n) {
-  double frac = n > 25000 ? 0.04 * std::pow(25000.0 / n, 0.25) : 0.04;
+  // measured optima: 0.055 at C3 (profiles/r02_heavyfrac_c3_gemm_v4.jsonl,
+  // the tensor-core path), 0.04 (25k/n)^(1/4) at the C5 shard
+  double frac = n > 25000 ? 0.04 * std::pow(25000.0 / n, 0.25) : 0.055;
   if (const char* e = std::getenv("SF_HEAVY_FRAC")) frac = std::atof(e);
   return std::max(2, static_cast<int>(frac * n));
 }
@@ -917,7 +1026,7 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
         d.emb.as<uint32_t>(), plan->row_words, plan->E, n, d.perm.as<int32_t>(),
         d.nheavy.as<unsigned int>(), d.mcount.as<int32_t>(), d.lptr.as<uint32_t>(),
         d.fix.as<unsigned long long>(), plan->lo_bits, d.lmem.as<int32_t>(),
-        d.colsum.as<unsigned long long>());
+        d.colsum.as<unsigned long long>(), d.light_columns ? 2 : INT_MAX);
     SF_CUDA(cudaGetLastError());
     d.launches += 3;
   }
@@ -951,6 +1060,11 @@ sf_status split_scatter_banded(sf_plan* plan, DeviceState& d, cudaStream_t st, i
       sp_col_fill_kernel<<<wblocks, 256, 0, st>>>(d.lmem.as<int32_t>(), d.lptr.as<uint32_t>(), plan->E,
                                                   d.nheavy.as<unsigned int>(), d.ccnt.as<uint32_t>(),
                                                   d.cent.as<uint2>());
+      // the light rows' column sums (rows with >= 2 members) from the entries
+      sp_light_colsum_kernel<<<grid_for(static_cast<int64_t>(n) * 32, 256), 256, 0, st>>>(
+          d.cptr.as<uint32_t>(), d.cent.as<uint2>(), d.perm.as<int32_t>(), d.mcount.as<int32_t>(),
+          d.fix.as<unsigned long long>(), plan->lo_bits, n, d.colsum.as<unsigned long long>());
+      d.launches++;
       if (d.linfo.bytes < static_cast<size_t>(E) * sizeof(LightRowInfo))
         SF_TRY(d.linfo.alloc(d.dev, static_cast<size_t>(E) * sizeof(LightRowInfo), "light row records"));
       sp_light_rowinfo_kernel<<<grid_for(E, 256), 256, 0, st>>>(d.perm.as<int32_t>(), plan->E,
@@ -1023,7 +1137,7 @@ sf_status split_scatter_deep(sf_plan* plan, DeviceState& d, cudaStream_t st, int
     d.launches += 3;
   }
   if (d.deep_entries > 0) {
-    sp_deep_scatter_kernel<<<grid_for(d.deep_entries, 256), 256, 0, st>>>(
+    sp_deep_scatter_kernel<<<grid_for(d.deep_entries * 32, 256), 256, 0, st>>>(
         d.dptr.as<uint32_t>(), d.dmem.as<int32_t>(), d.dent.as<uint32_t>(), d.deep_entries,
         d.dfix.as<unsigned long long>(), J, plan->lo_bits, n, s0, s1, d.deepsum.as<unsigned long long>());
     SF_CUDA(cudaGetLastError());
@@ -1132,7 +1246,7 @@ sf_status split_build(sf_plan* plan, DeviceState& d, cudaStream_t st) {
       d.dmask.as<unsigned long long>(), d.nodebits.as<unsigned long long>(), n_ext);
   sp_extend_kernel<<<grid_for(W * (n_ext - n), 256), 256, 0, st>>>(
       d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>());
-  sp_heavy_colsum_kernel<<<grid_for(n, 128), 128, 0, st>>>(
+  sp_heavy_colsum_kernel<<<grid_for(static_cast<int64_t>(kHeavyColSlices) * n, 256), 256, 0, st>>>(
       d.nodebits.as<unsigned long long>(), n_ext, n, d.nheavy.as<unsigned int>(),
       d.dmask.as<unsigned long long>(), d.fixbit.as<unsigned long long>(), plan->lo_bits,
       d.colsum.as<unsigned long long>());
@@ -1214,6 +1328,9 @@ sf_status gram_prepare(sf_plan* plan, DeviceState& d, cudaStream_t st) {
   d.gram_kp = Kp;
   d.gram_h = H;
   d.gram_nd = static_cast<int32_t>(dj.size());
+  d.gram_dj0 = dj.front();
+  for (size_t j = 1; j < dj.size(); ++j)
+    if (dj[j] != dj[j - 1] + 1) d.gram_dj0 = -1;
   if (d.gdj.bytes < dj.size() * 4) SF_TRY(d.gdj.alloc(d.dev, kMaxDigits * 4, "digit planes"));
   SF_CUDA(cudaMemcpyAsync(d.gdj.p, dj.data(), dj.size() * 4, cudaMemcpyHostToDevice, st));
   const size_t bbytes = static_cast<size_t>(n_ext) * static_cast<size_t>(Kp);
@@ -1302,6 +1419,7 @@ sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, 
   GramArgs g;
   g.C = d.gC.as<int32_t>();
   g.dj = d.gdj.as<int32_t>();
+  g.dj0 = d.gram_dj0;
   g.nd = nd;
   g.bk = bk;
   g.c0 = c0;
@@ -1343,10 +1461,11 @@ sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, 
                        static_cast<uint64_t>(std::min(bk, k_end - k0));
     g.k0 = k0;
     const int64_t slots = static_cast<int64_t>(span) * std::min(bk, n - k0);
+    const bool c32 = plan->lo_bits == 32 && plan->vb == 63;  // the common split: constant shifts
     if (plan->prec == SF_FP64)
-      sp_gram_epilogue_kernel<double><<<grid_for(slots, 256), 256, 0, st>>>(g);
+      (c32 ? sp_gram_epilogue_kernel<double, 32, 63> : sp_gram_epilogue_kernel<double, 0, 0>)<<<grid_for(slots, 256), 256, 0, st>>>(g);
     else
-      sp_gram_epilogue_kernel<float><<<grid_for(slots, 256), 256, 0, st>>>(g);
+      (c32 ? sp_gram_epilogue_kernel<float, 32, 63> : sp_gram_epilogue_kernel<float, 0, 0>)<<<grid_for(slots, 256), 256, 0, st>>>(g);
     SF_CUDA(cudaGetLastError());
     d.launches += 3;
   }
@@ -2150,7 +2269,9 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
           // a host destination, every group of blocks (a column strip of the
           // pass's stripes) is copied while the next group computes
           const int bk = gram_block(span);
-          const int ngrp = host_d ? std::max(1, std::min(8, n / (2 * bk))) : 1;
+          const char* cg = std::getenv("SF_COPY_GROUPS");  // A/B: column strips per pass
+          const int gmax = cg ? std::max(1, std::atoi(cg)) : 12;
+          const int ngrp = host_d ? std::max(1, std::min(gmax, n / (2 * bk))) : 1;
           const int gw = ((n + ngrp - 1) / ngrp + bk - 1) / bk * bk;
           for (int k0 = 0; k0 < n; k0 += gw) {
             const int k1 = std::min(n, k0 + gw);
@@ -2513,9 +2634,21 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
                  std::chrono::duration<double, std::milli>(now - tick).count());
     tick = now;
   };
-  SF_TRY(validate_problem(p));
+  SF_TRY(validate_tree(p));
+  // the single-chunk embedding schedule (every resident path; the chunked
+  // dense paths rebuild it for their chunk size) reads only the tree: it is
+  // built on a host thread while the table is validated, the devices are
+  // set up, the table uploads and the fixed-point levels are formed
+  Schedule sched_all;
+  std::thread sched_thread([&] { sched_all = build_schedule(p, p->n_rows); });
+  struct SchedJoiner {
+    std::thread& t;
+    ~SchedJoiner() {
+      if (t.joinable()) t.join();
+    }
+  } sched_joiner{sched_thread};
   SF_TRY(validate_range(p->n_samples, start, stop));
-  phase("validate");
+  phase("validate tree");
   std::vector<int> devices;
   SF_TRY(usable_devices(ex, devices));
   phase("devices");
@@ -2595,6 +2728,56 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     plan->devs.push_back(std::move(d));
   }
 
+  // the table upload (C3: 192 MB from pageable memory) runs on a host thread
+  // while this one validates the table and sizes the plan (a table that
+  // fails validation is uploaded for nothing: the error is returned after
+  // the join)
+  std::vector<sf_status> up_status(plan->devs.size(), SF_OK);
+  std::vector<std::string> up_error(plan->devs.size());
+  std::thread uploader([&] {
+    for (size_t i = 0; i < plan->devs.size(); ++i) {
+      DeviceState& d = *plan->devs[i];
+      auto run = [&]() -> sf_status {
+        SF_CUDA(cudaSetDevice(d.dev));
+        SF_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+        const int64_t F = p->n_features;
+        const int64_t nnz = p->feat_ptr[F];
+        SF_TRY(upload(d.lens, d.dev, p->lengths, static_cast<size_t>(plan->E), d.stream, "lengths"));
+        SF_TRY(upload(d.feat_ptr, d.dev, p->feat_ptr, static_cast<size_t>(F + 1), d.stream, "feat_ptr"));
+        // the table's big arrays (C3: 180 MB) through the pinned staging buffers
+        SF_TRY(d.sidx.alloc(d.dev, static_cast<size_t>(nnz) * 4, "sample_idx"));
+        SF_TRY(d.counts.alloc(d.dev, static_cast<size_t>(nnz) * 8, "counts"));
+        const unsigned th = copy_threads(plan->devs.size());
+        if (host_pinned(p->sample_idx))
+          SF_CUDA(cudaMemcpyAsync(d.sidx.p, p->sample_idx, static_cast<size_t>(nnz) * 4, cudaMemcpyHostToDevice, d.stream));
+        else
+          SF_TRY(staged_h2d(d.dev, d.stream, reinterpret_cast<const char*>(p->sample_idx), d.sidx.as<char>(),
+                            static_cast<size_t>(nnz) * 4, th));
+        if (host_pinned(p->counts))
+          SF_CUDA(cudaMemcpyAsync(d.counts.p, p->counts, static_cast<size_t>(nnz) * 8, cudaMemcpyHostToDevice, d.stream));
+        else
+          SF_TRY(staged_h2d(d.dev, d.stream, reinterpret_cast<const char*>(p->counts), d.counts.as<char>(),
+                            static_cast<size_t>(nnz) * 8, th));
+        SF_TRY(upload(d.totals, d.dev, p->sample_totals, static_cast<size_t>(n), d.stream, "totals"));
+        return SF_OK;
+      };
+      up_status[i] = run();
+      if (up_status[i] != SF_OK) {
+        up_error[i] = sf::last_error();
+        return;
+      }
+    }
+  });
+  struct Joiner {
+    std::thread& t;
+    ~Joiner() {
+      if (t.joinable()) t.join();
+    }
+  } joiner{uploader};
+  phase("spawn uploader");
+  SF_TRY(validate_table(p));
+  phase("validate table");
+
   // chunk capacity from the smallest device budget
   const size_t row_bytes = static_cast<size_t>(plan->row_words) * ((plan->bits || plan->wbits) ? 4 : 8);
   // kernel 11 holds, per chunk row, the dense row + its share of the value
@@ -2639,51 +2822,6 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   if (ex && ex->mem_budget_bytes > 0) budget = std::min(budget, static_cast<size_t>(ex->mem_budget_bytes));
   phase("budget");
 
-  // the table upload (C3: 192 MB from pageable memory) runs on a host thread
-  // while this one builds the schedule
-  std::vector<sf_status> up_status(plan->devs.size(), SF_OK);
-  std::vector<std::string> up_error(plan->devs.size());
-  std::thread uploader([&] {
-    for (size_t i = 0; i < plan->devs.size(); ++i) {
-      DeviceState& d = *plan->devs[i];
-      auto run = [&]() -> sf_status {
-        SF_CUDA(cudaSetDevice(d.dev));
-        SF_CUDA(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
-        const int64_t F = p->n_features;
-        const int64_t nnz = p->feat_ptr[F];
-        SF_TRY(upload(d.lens, d.dev, p->lengths, static_cast<size_t>(plan->E), d.stream, "lengths"));
-        SF_TRY(upload(d.feat_ptr, d.dev, p->feat_ptr, static_cast<size_t>(F + 1), d.stream, "feat_ptr"));
-        // the table's big arrays (C3: 180 MB) through the pinned staging buffers
-        SF_TRY(d.sidx.alloc(d.dev, static_cast<size_t>(nnz) * 4, "sample_idx"));
-        SF_TRY(d.counts.alloc(d.dev, static_cast<size_t>(nnz) * 8, "counts"));
-        const unsigned th = copy_threads(plan->devs.size());
-        if (host_pinned(p->sample_idx))
-          SF_CUDA(cudaMemcpyAsync(d.sidx.p, p->sample_idx, static_cast<size_t>(nnz) * 4, cudaMemcpyHostToDevice, d.stream));
-        else
-          SF_TRY(staged_h2d(d.dev, d.stream, reinterpret_cast<const char*>(p->sample_idx), d.sidx.as<char>(),
-                            static_cast<size_t>(nnz) * 4, th));
-        if (host_pinned(p->counts))
-          SF_CUDA(cudaMemcpyAsync(d.counts.p, p->counts, static_cast<size_t>(nnz) * 8, cudaMemcpyHostToDevice, d.stream));
-        else
-          SF_TRY(staged_h2d(d.dev, d.stream, reinterpret_cast<const char*>(p->counts), d.counts.as<char>(),
-                            static_cast<size_t>(nnz) * 8, th));
-        SF_TRY(upload(d.totals, d.dev, p->sample_totals, static_cast<size_t>(n), d.stream, "totals"));
-        return SF_OK;
-      };
-      up_status[i] = run();
-      if (up_status[i] != SF_OK) {
-        up_error[i] = sf::last_error();
-        return;
-      }
-    }
-  });
-  struct Joiner {
-    std::thread& t;
-    ~Joiner() {
-      if (t.joinable()) t.join();
-    }
-  } joiner{uploader};
-  phase("spawn uploader");
   int64_t cmax = static_cast<int64_t>(budget / std::max<size_t>(row_bytes + wsp_row_bytes, 1));
   if (plan->kernel >= 2 && !wsp) cmax = plan->E;  // the sparse bit paths keep all rows
   if (wsp) {
@@ -2695,8 +2833,18 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   if (plan->wbits) cmax = plan->E;  // bit rows: every row in one chunk
   cmax = std::min<int64_t>(cmax, plan->E);
   if (cmax < 1) return fail(SF_ENOMEM, "not enough device memory for one embedding row");
+  FixedLevels fl;
+  if (plan->kernel == 10) {
+    SF_TRY(fixed_levels(p->lengths, plan->E, prec == SF_FP32, fl));
+    phase("fixed-point levels");
+  }
+  sched_thread.join();
+  phase("schedule (overlapped)");
   for (;;) {
-    plan->sched = build_schedule(p, static_cast<int32_t>(cmax));
+    if (cmax == plan->E && sched_all.cmax == cmax)
+      plan->sched = std::move(sched_all);
+    else
+      plan->sched = build_schedule(p, static_cast<int32_t>(cmax));
     const size_t need = (static_cast<size_t>(cmax) + static_cast<size_t>(plan->sched.n_pending)) * row_bytes +
                         static_cast<size_t>(cmax) * wsp_row_bytes;
     if (need <= budget || cmax == 1 || (plan->kernel >= 2 && !wsp) || (wsp && cmax <= 32) || plan->wbits) break;
@@ -2705,14 +2853,11 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
   }
   plan->stats.n_chunks = plan->sched.chunks.size();
 
-  phase("schedule");
   uploader.join();
   for (size_t i = 0; i < up_status.size(); ++i)
     if (up_status[i] != SF_OK) return fail(up_status[i], up_error[i]);
   phase("upload table (overlapped)");
   if (plan->kernel == 10) {
-    FixedLevels fl;
-    SF_TRY(fixed_levels(p->lengths, plan->E, prec == SF_FP32, fl));
     plan->scale = fl.scale;
     plan->lo_bits = fl.lo_bits;
     plan->vb = fl.vb;
@@ -2720,7 +2865,6 @@ sf_status sf_plan_create(const sf_problem* p, sf_metric metric, sf_precision pre
     plan->fix = std::move(fl.fix);
     plan->deep_rows = std::move(fl.deep_rows);
     plan->dfix = std::move(fl.dfix);
-    phase("fixed-point levels");
   }
   for (auto& dp : plan->devs) {
     DeviceState& d = *dp;

@@ -178,17 +178,21 @@ __global__ void sp_extend_kernel(unsigned long long* __restrict__ nx, int64_t n_
 
 // Column sums over the heavy words: thread per column (coalesced over c).
 // colsum layout [4][n] = x_hi, x_lo, p_hi, p_lo (p: rows that are not dense).
+constexpr int kHeavyColSlices = 16;
 __global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx, int64_t n_ext,
                                        int32_t n, const unsigned int* __restrict__ n_heavy,
                                        const unsigned long long* __restrict__ dmask64,
                                        const unsigned long long* __restrict__ fixbit, int32_t lo_bits,
                                        unsigned long long* __restrict__ colsum) {
+  // thread per (column, slice of the heavy words): coalesced along the
+  // columns, kHeavyColSlices partial sums per column (exact u64 atomics)
   const int64_t Hw = (static_cast<int64_t>(*n_heavy) + 63) / 64;
   const unsigned long long lo_mask = (1ull << lo_bits) - 1ull;
-  for (int64_t c = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; c < n;
-       c += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < kHeavyColSlices * n;
+       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t z = t / n, c = t - z * n;
     unsigned long long xh = 0, xl = 0, ph = 0, pl = 0;
-    for (int64_t w = 0; w < Hw; ++w) {
+    for (int64_t w = Hw * z / kHeavyColSlices; w < Hw * (z + 1) / kHeavyColSlices; ++w) {
       const unsigned long long x = __ldg(nx + w * n_ext + c);
       if (!x) continue;
       const unsigned long long dm = __ldg(dmask64 + w);
@@ -207,10 +211,14 @@ __global__ void sp_heavy_colsum_kernel(const unsigned long long* __restrict__ nx
         }
       }
     }
-    atomicAdd(colsum + c, xh);
-    atomicAdd(colsum + n + c, xl);
-    atomicAdd(colsum + 2 * static_cast<int64_t>(n) + c, ph);
-    atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, pl);
+    if (xh | xl) {
+      atomicAdd(colsum + c, xh);
+      atomicAdd(colsum + n + c, xl);
+    }
+    if (ph | pl) {
+      atomicAdd(colsum + 2 * static_cast<int64_t>(n) + c, ph);
+      atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, pl);
+    }
   }
 }
 
@@ -397,7 +405,8 @@ __global__ void sp_light_members_kernel(const uint32_t* __restrict__ rows, int64
                                         const int32_t* __restrict__ mcount,
                                         const uint32_t* __restrict__ lptr,
                                         const unsigned long long* __restrict__ fix, int32_t lo_bits,
-                                        int32_t* __restrict__ lmem, unsigned long long* __restrict__ colsum) {
+                                        int32_t* __restrict__ lmem, unsigned long long* __restrict__ colsum,
+                                        int32_t gather_min) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
@@ -409,6 +418,13 @@ __global__ void sp_light_members_kernel(const uint32_t* __restrict__ rows, int64
     const bool dense = 2 * m > n;
     const int x = dense ? n - m : m;
     if (x == 0) continue;
+    // rows with >= gather_min members reach the column sums through the
+    // column entries (sp_light_colsum_kernel): no per-member atomics here
+    if (x >= gather_min) {
+      list_members(rows + static_cast<int64_t>(r) * stride, stride, dense, tail, x, lane, lmem + lptr[idx],
+                   [](int) {});
+      continue;
+    }
     const ulonglong2 L = ilimbs_of(fix[r], lo_bits);
     list_members(rows + static_cast<int64_t>(r) * stride, stride, dense, tail, x, lane, lmem + lptr[idx],
                  [&](int smp) {
@@ -419,6 +435,43 @@ __global__ void sp_light_members_kernel(const uint32_t* __restrict__ rows, int64
                      atomicAdd(colsum + 3 * static_cast<int64_t>(n) + smp, L.y);
                    }
                  });
+  }
+}
+
+// The light rows' column sums from the column entries (rows with >= 2
+// members): warp per column, exact u64 limb sums, four atomics per column
+// (the heavy rows and the single-member rows add theirs elsewhere).
+__global__ void sp_light_colsum_kernel(const uint32_t* __restrict__ cptr, const uint2* __restrict__ cent,
+                                       const int32_t* __restrict__ perm, const int32_t* __restrict__ mcount,
+                                       const unsigned long long* __restrict__ fix, int32_t lo_bits, int32_t n,
+                                       unsigned long long* __restrict__ colsum) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t c = warp; c < n; c += nwarps) {
+    unsigned long long xh = 0, xl = 0, ph = 0, pl = 0;
+    for (uint32_t e = cptr[c] + lane; e < cptr[c + 1]; e += 32) {
+      const int r = perm[cent[e].x];
+      const ulonglong2 L = ilimbs_of(fix[r], lo_bits);
+      xh += L.x;
+      xl += L.y;
+      if (2 * mcount[r] <= n) {
+        ph += L.x;
+        pl += L.y;
+      }
+    }
+    for (int off = 16; off > 0; off >>= 1) {
+      xh += __shfl_down_sync(0xffffffffu, xh, off);
+      xl += __shfl_down_sync(0xffffffffu, xl, off);
+      ph += __shfl_down_sync(0xffffffffu, ph, off);
+      pl += __shfl_down_sync(0xffffffffu, pl, off);
+    }
+    if (lane == 0) {
+      atomicAdd(colsum + c, xh);
+      atomicAdd(colsum + n + c, xl);
+      atomicAdd(colsum + 2 * static_cast<int64_t>(n) + c, ph);
+      atomicAdd(colsum + 3 * static_cast<int64_t>(n) + c, pl);
+    }
   }
 }
 
@@ -826,22 +879,26 @@ __device__ __forceinline__ void deep_add(unsigned long long* __restrict__ dacc, 
   }
 }
 
-// Thread per deep-row member entry: every partner above it, both slots of
-// the pair as in sp_add_pair, the deeper levels' limbs into dacc
-// [(s - s_begin) * n + k][J-1] (hi, lo).
+// Warp per deep-row member entry a, lanes over its partners above (b after
+// a in the row's sorted list): both slots of the pair as in sp_add_pair, the
+// deeper levels' limbs into dacc [(s - s_begin) * n + k][J-1] (hi, lo). (A
+// thread per entry walked up to a whole row alone: rows of thousands of
+// members serialised the kernel.)
 __global__ void sp_deep_scatter_kernel(const uint32_t* __restrict__ dptr, const int32_t* __restrict__ dmem,
                                        const uint32_t* __restrict__ dent, int64_t M,
                                        const unsigned long long* __restrict__ dfix, int32_t J, int32_t lo_bits,
                                        int32_t n, int32_t s_begin, int32_t s_end,
                                        unsigned long long* __restrict__ dacc) {
   const int S = n / 2;
-  for (int64_t g = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; g < M;
-       g += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t g = warp; g < M; g += nwarps) {
     const uint32_t i = dent[g];
     const int64_t end = dptr[i + 1];
     const unsigned long long* v = dfix + static_cast<int64_t>(i) * (J - 1);
     const int a = dmem[g];
-    for (int64_t q = g + 1; q < end; ++q) {
+    for (int64_t q = g + 1 + lane; q < end; q += 32) {
       const int b = __ldg(dmem + q);
       const int d = b - a;
       int s = d - 1;
