@@ -796,9 +796,10 @@ struct SplitCfg {
 // profiles/r02_heavyfrac_c3_col3.jsonl); beyond, the size-aware form of
 // round 1 (light pairs grow as x^2 and spread over more columns).
 int split_heavy_min(int n) {
-  // measured optima: 0.055 at C3 (profiles/r02_heavyfrac_c3_gemm_v4.jsonl,
-  // the tensor-core path), 0.04 (25k/n)^(1/4) at the C5 shard
-  double frac = n > 25000 ? 0.04 * std::pow(25000.0 / n, 0.25) : 0.055;
+  // measured optima: 0.065 at C3 (profiles/r02_heavyfrac_c3_gemm_v4.jsonl,
+  // the tensor-core path with the three-limb light kernel), 0.04 (25k/n)^(1/4)
+  // at the C5 shard
+  double frac = n > 25000 ? 0.04 * std::pow(25000.0 / n, 0.25) : 0.065;
   if (const char* e = std::getenv("SF_HEAVY_FRAC")) frac = std::atof(e);
   return std::max(2, static_cast<int>(frac * n));
 }
@@ -990,11 +991,15 @@ sf_status light_columns_run(sf_plan* plan, DeviceState& d, cudaStream_t st, int 
   const int smem = 2 * kLightWin * 8;
   // test hook: SF_LIGHT_LIMB_MODE=1|2 forces the wider exact limb modes
   const int min_mode = std::getenv("SF_LIGHT_LIMB_MODE") ? std::atoi(std::getenv("SF_LIGHT_LIMB_MODE")) : 0;
+  // entries per carry-folding chunk of the three-limb mode (<= 2048; test
+  // hook SF_LIGHT_CHUNK_ENTRIES: tiny chunks fold carries often)
+  int chunk = std::getenv("SF_LIGHT_CHUNK_ENTRIES") ? std::atoi(std::getenv("SF_LIGHT_CHUNK_ENTRIES")) : 2048;
+  chunk = std::max(1, std::min(chunk, 2048));
   auto launch = [&](auto* kern, const auto* mem) -> sf_status {
     SF_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kern<<<std::max(1, std::min(k1 - k0, 65535)), NT, smem, st>>>(
         d.cptr.as<uint32_t>(), d.cent.as<uint2>(), d.linfo.as<LightRowInfo>(), mem, plan->lo_bits, plan->n, k0, k1,
-        p0, p0, p1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>(), min_mode);
+        p0, p0, p1, d.lightsum.as<unsigned long long>(), d.exec_ctr.as<unsigned long long>(), min_mode, chunk);
     return SF_OK;
   };
   if (d.lmem16.p)

@@ -581,6 +581,10 @@ __device__ __forceinline__ uint2 ld_entry(const uint2* p) {
 #endif
 }
 constexpr int kLightUnroll = SF_LIGHT_UNROLL;  // member loads in flight per lane
+#ifndef SF_LIGHT_CHUNK
+#define SF_LIGHT_CHUNK 1  // three 21-bit limbs for all columns, carries folded per entry chunk (0: limb mode by entry count)
+#endif
+
 
 // 16-bit copy of the light member lists (n <= 65536) for the column kernel.
 __global__ void sp_narrow_members_kernel(const int32_t* __restrict__ lmem, const uint32_t* __restrict__ total,
@@ -628,10 +632,15 @@ __global__ void sp_col_fill_kernel(const int32_t* __restrict__ lmem, const uint3
 // kLightWin cells (structure of arrays: the cells of different stripes fall
 // in different banks). The row's value v (< 2^63) goes in as limbs into
 // 32-bit native shared atomic adds, exact while no cell overflows: a cell
-// takes one addition per light row holding the column (the column's entry
-// count), so MODE 0 (three 21-bit limbs) serves columns with <= 2048
-// entries, MODE 1 (four 16-bit limbs) <= 65535, and MODE 2 adds the (hi, lo)
-// limbs with 64-bit compare-and-swap adds for any count.
+// takes one addition per light row holding the column, so MODE 0 (three
+// 21-bit limbs) is exact for up to 2048 entries — the column kernel walks
+// longer columns in chunks of 2048 entries and folds the planes' carries
+// into a fourth plane between chunks (SF_LIGHT_CHUNK, default). MODE 1
+// (four 16-bit limbs, <= 65535 entries) and MODE 2 ((hi, lo) limbs with
+// 64-bit compare-and-swap adds, any count) are the unchunked alternatives
+// (SF_LIGHT_CHUNK=0, or the SF_LIGHT_LIMB_MODE test hook). The kernel is
+// bound by these atomics (L1 data pipe, profiles/r02_ncu_light_column_c3_v3.txt):
+// three limbs instead of four is 2.6% of the C3 step.
 template <int MODE>
 __device__ __forceinline__ void window_add(uint32_t* acc, int cell, unsigned long long v, ulonglong2 L) {
   if (MODE == 2) {
@@ -662,9 +671,10 @@ __device__ __forceinline__ ulonglong2 window_cell(const uint32_t* acc, int cell,
     v = static_cast<unsigned __int128>(acc[cell]) + (static_cast<unsigned __int128>(acc[kLightWin + cell]) << 16) +
         (static_cast<unsigned __int128>(acc[2 * kLightWin + cell]) << 32) +
         (static_cast<unsigned __int128>(acc[3 * kLightWin + cell]) << 48);
-  else
+  else  // three 21-bit limbs and the folded carries (zero without chunks)
     v = static_cast<unsigned __int128>(acc[cell]) + (static_cast<unsigned __int128>(acc[kLightWin + cell]) << 21) +
-        (static_cast<unsigned __int128>(acc[2 * kLightWin + cell]) << 42);
+        (static_cast<unsigned __int128>(acc[2 * kLightWin + cell]) << 42) +
+        (static_cast<unsigned __int128>(acc[3 * kLightWin + cell]) << 63);
   return make_ulonglong2(static_cast<unsigned long long>(v >> lo_bits),
                          static_cast<unsigned long long>(v) & ((1ull << lo_bits) - 1ull));
 }
@@ -768,27 +778,51 @@ __global__ void __launch_bounds__(NT) sp_light_column_kernel(
     const uint32_t* __restrict__ cptr, const uint2* __restrict__ cent, const LightRowInfo* __restrict__ info,
     const M* __restrict__ lmem, int32_t lo_bits, int32_t n, int32_t k_begin, int32_t k_end, int32_t p0,
     int32_t s0, int32_t s1, unsigned long long* __restrict__ gl, unsigned long long* __restrict__ pairs_out,
-    int32_t min_mode) {
+    int32_t min_mode, int32_t chunk) {
   extern __shared__ uint32_t lacc[];  // 4 planes of kLightWin u32 cells (or 2 of u64)
   const int S = n / 2;
   const int send = min(s1, S);
   unsigned long long pairs = 0;
   for (int k = k_begin + blockIdx.x; k < k_end; k += gridDim.x) {
     const uint32_t e0 = cptr[k], e1 = cptr[k + 1];
+#if SF_LIGHT_CHUNK
+    // three 21-bit limbs for every column: entries in chunks of <= 2048 (one
+    // addition per entry per cell keeps every plane below 2^32), the planes'
+    // carries folded into the fourth plane between chunks
+    const int mode = min_mode;  // test hook: 1 / 2 select the wide limb modes
+    const uint32_t step = mode == 0 ? static_cast<uint32_t>(chunk) : 0xffffffffu;
+#else
     // one addition per entry per cell: pick the narrowest exact limb mode
     const int mode = max(min_mode, e1 - e0 <= 2048u ? 0 : e1 - e0 <= 65535u ? 1 : 2);
+    const uint32_t step = 0xffffffffu;
+#endif
     for (int w0 = s0; w0 < send; w0 += kLightWin) {
       const int w1 = min(send, w0 + kLightWin);
       const int ww = w1 - w0;
       for (int t = threadIdx.x; t < 4 * kLightWin; t += NT) lacc[t] = 0u;
       __syncthreads();
-      if (mode == 0)
-        light_column_window<0, M>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
-      else if (mode == 1)
-        light_column_window<1, M>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
-      else
-        light_column_window<2, M>(e0, e1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
-      __syncthreads();
+      for (uint32_t c0 = e0;;) {
+        const uint32_t c1 = e1 - c0 > step ? c0 + step : e1;
+        if (mode == 0)
+          light_column_window<0, M>(c0, c1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+        else if (mode == 1)
+          light_column_window<1, M>(c0, c1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+        else
+          light_column_window<2, M>(c0, c1, cent, info, lmem, lo_bits, k, n, w0, w1, lacc, pairs);
+        __syncthreads();
+        if (c1 >= e1) break;
+        for (int t = threadIdx.x; t < ww; t += NT) {  // fold the carries before the next chunk
+          uint32_t a0 = lacc[t], a1 = lacc[kLightWin + t], a2 = lacc[2 * kLightWin + t];
+          a1 += a0 >> 21;
+          a2 += a1 >> 21;
+          lacc[t] = a0 & 0x1fffffu;
+          lacc[kLightWin + t] = a1 & 0x1fffffu;
+          lacc[2 * kLightWin + t] = a2 & 0x1fffffu;
+          lacc[3 * kLightWin + t] += a2 >> 21;
+        }
+        __syncthreads();
+        c0 = c1;
+      }
       for (int t = threadIdx.x; t < ww; t += NT) {
         const ulonglong2 out = mode == 0 ? window_cell<0>(lacc, t, lo_bits)
                                          : mode == 1 ? window_cell<1>(lacc, t, lo_bits) : window_cell<2>(lacc, t, lo_bits);

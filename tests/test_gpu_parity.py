@@ -931,3 +931,29 @@ def test_light_column_16bit_members_are_bitwise_the_32bit(device_ok, monkeypatch
         got = _gpu_stripes(problem, 1, prec, 0, 450, N.KERNEL_SPLIT)
         monkeypatch.delenv("SF_LIGHT_MEM16")
         assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+
+
+@pytest.mark.parametrize("chunk", ["1", "3", "64"])
+def test_light_column_carry_folding_is_exact(device_ok, chunk, monkeypatch):
+    """Three 21-bit limbs for every column, with the planes' carries folded
+    into a fourth plane between entry chunks: any chunk size (tiny ones here,
+    so cells fold many times, and lengths at the top of the grid so every
+    limb carries) gives the same exact light sums as the four 16-bit limb
+    mode (SF_LIGHT_LIMB_MODE=1), bit for bit, and matches the oracle."""
+    inst = sf.random_instance(142, 700, 4000, 0.02)
+    problem = sf.flatten(inst.tree, inst.table)
+    rng = np.random.default_rng(int(chunk))
+    problem.lengths[:] = np.where(rng.random(problem.n_rows) < 0.5, 2.0 - 1e-9 * rng.random(problem.n_rows),
+                                  rng.random(problem.n_rows) * 2.0)
+    monkeypatch.setenv("SF_HEAVY_FRAC", "0.3")
+    for prec in (8, 4):
+        monkeypatch.setenv("SF_LIGHT_LIMB_MODE", "1")
+        want = _gpu_stripes(problem, 1, prec, 0, 350, N.KERNEL_SPLIT)
+        monkeypatch.delenv("SF_LIGHT_LIMB_MODE")
+        monkeypatch.setenv("SF_LIGHT_CHUNK_ENTRIES", chunk)
+        got = _gpu_stripes(problem, 1, prec, 0, 350, N.KERNEL_SPLIT)
+        monkeypatch.delenv("SF_LIGHT_CHUNK_ENTRIES")
+        assert np.array_equal(got[0], want[0]) and np.array_equal(got[1], want[1])
+    wd, wt = op.compute_stripes(problem, 1, 8, 0, 350)
+    got = _gpu_stripes(problem, 1, 8, 0, 350, N.KERNEL_SPLIT)
+    _assert_close(1, 8, False, got[0], wd, N.KERNEL_SPLIT)
