@@ -2278,8 +2278,10 @@ sf_status run_device(sf_plan* plan, DeviceState& d, int32_t finalize, void* host
           const int gmax = cg ? std::max(1, std::atoi(cg)) : 12;
           const int ngrp = host_d ? std::max(1, std::min(gmax, n / (2 * bk))) : 1;
           const int gw = ((n + ngrp - 1) / ngrp + bk - 1) / bk * bk;
-          for (int k0 = 0; k0 < n; k0 += gw) {
-            const int k1 = std::min(n, k0 + gw);
+          // the first strip is one GEMM block wide, so its copy starts early
+          // (the D2H of 5 GB at C3 is as long as the compute it overlaps)
+          for (int k0 = 0, k1 = 0; k0 < n; k0 = k1) {
+            k1 = std::min(n, k0 + (k0 == 0 && ngrp > 1 ? bk : gw));
             if (d.defer_light) SF_TRY(light_columns_run(plan, d, st, p0, p1, k0, k1));
             SF_TRY(gram_run(plan, d, p0, p1, p0, finalize, st, k0, k1));
             if (plan->levels > 2) SF_TRY(deep_epilogue(p0, p1, k0, k1));  // two levels: fused in the epilogue
