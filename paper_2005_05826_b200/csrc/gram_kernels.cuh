@@ -154,7 +154,6 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
   const int vb = VB > 0 ? VB : a.vb;
   const int n = a.n;
   const int kcount = min(a.bk, n - a.k0);
-  const int64_t total = static_cast<int64_t>(a.c1 - a.c0) * kcount;
   const unsigned long long* xs = a.colsum;
   const __int128 Cd = (static_cast<__int128>(a.cacc[0]) << lo_bits) + static_cast<__int128>(a.cacc[1]);
   const __int128 C1 = a.levels == 2 ? (static_cast<__int128>(a.dcacc[0]) << lo_bits) + static_cast<__int128>(a.dcacc[1])
@@ -162,10 +161,11 @@ __global__ void sp_gram_epilogue_kernel(const GramArgs a) {
   const unsigned long long lo_mask = (1ull << lo_bits) - 1ull;
   Real* dist = static_cast<Real*>(a.dist);
   Real* tot = static_cast<Real*>(a.tot);
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; t < total;
-       t += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int ds = static_cast<int>(t / kcount);
-    const int kk = static_cast<int>(t - static_cast<int64_t>(ds) * kcount);
+  // 2D grid: x over the block's columns, y strides over the stripes (no
+  // 64-bit division per slot)
+  const int span = a.c1 - a.c0;
+  for (int ds = blockIdx.y; ds < span; ds += gridDim.y)
+  for (int kk = blockIdx.x * blockDim.x + threadIdx.x; kk < kcount; kk += gridDim.x * blockDim.x) {
     const int s = a.c0 + ds;
     const int k = a.k0 + kk;
     int l = k + s + 1;

@@ -1465,12 +1465,13 @@ sf_status gram_run(sf_plan* plan, DeviceState& d, int c0, int c1, int gl_begin, 
     d.heavy_updates += static_cast<uint64_t>(d.gram_h) * static_cast<uint64_t>(span) *
                        static_cast<uint64_t>(std::min(bk, k_end - k0));
     g.k0 = k0;
-    const int64_t slots = static_cast<int64_t>(span) * std::min(bk, n - k0);
     const bool c32 = plan->lo_bits == 32 && plan->vb == 63;  // the common split: constant shifts
+    const int kc = std::min(bk, n - k0);
+    const dim3 egrid((kc + 255) / 256, std::max(1, std::min(span, 148 * 32 / ((kc + 255) / 256))));
     if (plan->prec == SF_FP64)
-      (c32 ? sp_gram_epilogue_kernel<double, 32, 63> : sp_gram_epilogue_kernel<double, 0, 0>)<<<grid_for(slots, 256), 256, 0, st>>>(g);
+      (c32 ? sp_gram_epilogue_kernel<double, 32, 63> : sp_gram_epilogue_kernel<double, 0, 0>)<<<egrid, 256, 0, st>>>(g);
     else
-      (c32 ? sp_gram_epilogue_kernel<float, 32, 63> : sp_gram_epilogue_kernel<float, 0, 0>)<<<grid_for(slots, 256), 256, 0, st>>>(g);
+      (c32 ? sp_gram_epilogue_kernel<float, 32, 63> : sp_gram_epilogue_kernel<float, 0, 0>)<<<egrid, 256, 0, st>>>(g);
     SF_CUDA(cudaGetLastError());
     d.launches += 3;
   }
