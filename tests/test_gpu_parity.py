@@ -957,3 +957,51 @@ def test_light_column_carry_folding_is_exact(device_ok, chunk, monkeypatch):
     wd, wt = op.compute_stripes(problem, 1, 8, 0, 350)
     got = _gpu_stripes(problem, 1, 8, 0, 350, N.KERNEL_SPLIT)
     _assert_close(1, 8, False, got[0], wd, N.KERNEL_SPLIT)
+
+
+@pytest.mark.parametrize("metric", [1, 3])
+def test_plan_create_rejects_invalid_problems(device_ok, metric):
+    """sf_plan_create validates the tree before starting the schedule thread
+    and the table after starting the table upload: every invalid problem is
+    rejected with SF_EINVAL and its message, with no plan and no hang, on the
+    split (unweighted) and weighted-split paths; a valid problem still plans."""
+    inst = sf.random_instance(143, 40, 120, 0.2)
+    base = sf.flatten(inst.tree, inst.table)
+
+    def fresh():
+        return N.Problem(base.parent_row.copy(), base.lengths.copy(), base.leaf_feature.copy(), base.n_samples,
+                         base.feat_ptr.copy(), base.sample_idx.copy(), base.counts.copy(),
+                         base.sample_totals.copy())
+
+    def create(p):
+        ex, _keep = N.make_exec([0], 0)
+        plan = C.c_void_p()
+        rc = N.lib().sf_plan_create(p.ref, metric, 8, 0, p.n_samples // 2, C.byref(ex), C.byref(plan))
+        if plan.value:
+            N.lib().sf_plan_destroy(plan)
+        return rc, N.lib().sf_last_error().decode()
+
+    def bad_length(p):
+        p.lengths[3] = -1.0
+
+    def bad_parent(p):
+        p.parent_row[5] = 2
+
+    def bad_order(p):
+        f = int(np.argmax(np.diff(p.feat_ptr) >= 2))
+        a = int(p.feat_ptr[f])
+        p.sample_idx[a], p.sample_idx[a + 1] = p.sample_idx[a + 1], p.sample_idx[a]
+
+    def bad_count(p):
+        p.counts[7] = -2.0
+
+    def bad_total(p):
+        p.sample_totals[4] = 0.0
+
+    for mutate, msg in ((bad_length, "branch length"), (bad_parent, "parent row"),
+                        (bad_order, "ascending"), (bad_count, "non-negative"), (bad_total, "no counts")):
+        p = fresh()
+        mutate(p)
+        rc, err = create(p)
+        assert rc == N.SF_EINVAL and msg in err, (mutate.__name__, rc, err)
+    assert create(fresh())[0] == 0
