@@ -987,7 +987,7 @@ bool light_banded() {
 #endif
 // Column-owned light scatter of stripes [p0, p1) for columns [k0, k1).
 sf_status light_columns_run(sf_plan* plan, DeviceState& d, cudaStream_t st, int p0, int p1, int k0, int k1) {
-  constexpr int NT = SF_LIGHT_NT;  // the kernel is bound by member-list reads: many warps
+  constexpr int NT = SF_LIGHT_NT;  // many warps: member-list reads and shared atomics in flight
   const int smem = 2 * kLightWin * 8;
   // test hook: SF_LIGHT_LIMB_MODE=1|2 forces the wider exact limb modes
   const int min_mode = std::getenv("SF_LIGHT_LIMB_MODE") ? std::atoi(std::getenv("SF_LIGHT_LIMB_MODE")) : 0;
