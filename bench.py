@@ -447,8 +447,8 @@ def roofline_record(args, cfg, metric, prec, device, world, stop_all, E, n, str_
             "traffic_source": (f"{tr['source']} ({tr['launches']} launches of the {tr['stripes']}-stripe run)"
                                if tr else None),
             "kernel": "heavy-row int8 digit-plane GEMMs (cuBLASLt IMMA, tcgen05) of the split path",
-            "largest_kernel_note": ("at C3 the light column kernel (sp_light_column_kernel, ~45% of the "
-                                    "step in the ncu launch list) takes longer than the GEMMs (~33%); it is "
+            "largest_kernel_note": ("at C3 the light column kernel (sp_light_column_kernel, ~48% of the "
+                                    "step in the ncu launch list) takes longer than the GEMMs (~29%); it is "
                                     "bound by the L1 data pipe (shared-memory atomics: 90% of cycles, "
                                     "profiles/r02_ncu_light_column_c3_v3.txt), which has no HBM or tensor "
                                     "roofline; the frac above is the GEMMs'"),
