@@ -18,6 +18,9 @@ VARIANTS = {
     "lw4224u4n512": dict(SF_LIGHT_WIN=4224, SF_LIGHT_UNROLL=4, SF_LIGHT_NT=512),
     "lnostream": dict(SF_LIGHT_STREAM=0),
     "lnochunk": dict(SF_LIGHT_CHUNK=0),
+    "lu2": dict(SF_LIGHT_UNROLL=2),
+    "lu8": dict(SF_LIGHT_UNROLL=8),
+    "lu6": dict(SF_LIGHT_UNROLL=6),
     # weighted split: dense rows per cp.async stage / light member loads in flight
     "wsr16": dict(SF_WS_R=16),
     "wsu2": dict(SF_WS_UNROLL=2),
